@@ -1,0 +1,205 @@
+/*
+ * chgpu.h — C ABI of libchgpu.so, the B200 (sm_100a) Cascade Hashing matcher.
+ *
+ * This is the drop-in boundary for the reference's matching path.  The reference has no FFI
+ * layer: its boundary is the C++ library API in namespace cashash (static lib `cashash`,
+ * /root/reference/proj/src/CMakeLists.txt:1-13).  Every entry point below names the reference
+ * interface it replaces (paths relative to /root/reference/proj).  The C++ facade that restores
+ * the reference's signatures on top of this ABI is include/cashash_b200/cashash.hpp.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; all pointers are HOST pointers unless stated otherwise;
+ *   - every call returns a chgpu_status; chgpu_last_error(ctx) gives the message;
+ *   - one context per GPU; a context is thread-compatible (serialise calls on one context);
+ *   - there is NO CPU fallback: without a CUDA device chgpu_create fails with CHGPU_ECUDA.
+ *
+ * Supported parameter envelope on the device path (CHGPU_EUNSUPPORTED outside it):
+ *   short_bits m <= 12, table_count L <= 8, long_bits n <= 128, top_k <= 32,
+ *   points per image <= 65,536.
+ */
+#ifndef CHGPU_H
+#define CHGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct chgpu_ctx chgpu_ctx;
+
+typedef enum chgpu_status {
+    CHGPU_OK = 0,
+    CHGPU_EINVAL = 1,       /* reference: std::invalid_argument */
+    CHGPU_ELOGIC = 2,       /* reference: std::logic_error (e.g. centering not set, hashing.cpp:131) */
+    CHGPU_ECUDA = 3,        /* CUDA runtime failure / no device */
+    CHGPU_ENOMEM = 4,
+    CHGPU_EUNSUPPORTED = 5, /* outside the envelope above */
+    CHGPU_EFORMAT = 6,      /* reference: FeatureFileError (feature_io.hpp:61-80) */
+    CHGPU_ENOTFOUND = 7     /* unknown image id */
+} chgpu_status;
+
+/* hashing.hpp:45-52 FamilyParams */
+typedef struct chgpu_family_params {
+    uint32_t short_bits;  /* m, default 8   */
+    uint32_t long_bits;   /* n, default 128 */
+    uint32_t table_count; /* L, default 6   */
+    uint64_t seed;        /* default 1      */
+} chgpu_family_params;
+
+/* matcher.hpp:14-23 MatchConfig */
+typedef struct chgpu_match_cfg {
+    uint32_t top_k;                    /* default 10  */
+    uint32_t hamming_threshold;        /* default 40  */
+    double ratio;                      /* default 0.8 */
+    uint32_t min_candidates_for_ratio; /* default 2   */
+    int32_t reduce_rounds;             /* default 3; validated, exact distances do not depend on it */
+} chgpu_match_cfg;
+
+/* feature_io.hpp:51-57 MatchRecord — identical 16-byte layout. */
+typedef struct chgpu_match_record {
+    uint32_t query_index;
+    uint32_t train_index;
+    double distance_sq;
+} chgpu_match_record;
+
+/* feature_io.hpp:53-59 FeatureFileFault */
+typedef enum chgpu_file_fault {
+    CHGPU_FAULT_NONE = 0,
+    CHGPU_FAULT_MISSING_FILE = 1,
+    CHGPU_FAULT_BAD_MAGIC = 2,
+    CHGPU_FAULT_BAD_VERSION = 3,
+    CHGPU_FAULT_TRUNCATED = 4,
+    CHGPU_FAULT_UNWRITABLE = 5
+} chgpu_file_fault;
+
+/* Counters and timings of one chgpu_match_pairs* call (device-side event timing on the
+ * library's own compute stream). */
+typedef struct chgpu_match_stats {
+    uint64_t pairs;
+    uint64_t matches;           /* Mx */
+    uint64_t raw_candidates;    /* R */
+    uint64_t verified_queries;  /* Vq */
+    uint64_t distances;         /* V  */
+    uint64_t query_points;      /* sum of Nq over pairs */
+    uint64_t train_points;      /* sum of Nt over pairs */
+    uint64_t records_checksum;  /* order-independent FNV-style checksum of all records */
+    uint32_t match_launches;    /* launches of the match kernel */
+    uint32_t total_launches;    /* all kernels launched by the call */
+    float match_kernel_ms;      /* sum of match-kernel durations (CUDA events) */
+    float total_ms;             /* first launch -> last result resident (device) or delivered (host) */
+} chgpu_match_stats;
+
+typedef struct chgpu_device_props {
+    char name[64];
+    int sm_count;
+    int cc_major, cc_minor;
+    size_t total_mem, free_mem;
+    size_t smem_per_block_optin;
+} chgpu_device_props;
+
+/* ---- context --------------------------------------------------------------------------- */
+chgpu_status chgpu_create(int device, chgpu_ctx** out);
+void chgpu_destroy(chgpu_ctx* ctx);
+const char* chgpu_last_error(const chgpu_ctx* ctx);
+const char* chgpu_status_name(chgpu_status s);
+chgpu_status chgpu_get_device_props(chgpu_ctx* ctx, chgpu_device_props* out);
+chgpu_status chgpu_sync(chgpu_ctx* ctx);
+/* Pinned host memory for zero-staging uploads / result sinks. */
+chgpu_status chgpu_host_alloc(chgpu_ctx* ctx, size_t bytes, void** out);
+chgpu_status chgpu_host_free(chgpu_ctx* ctx, void* p);
+
+/* ---- hash family ----------------------------------------------------------------------- */
+/* Replaces build_hash_family (hashing.hpp:74, hashing.cpp:38-50): host-side, deterministic.
+ * short_planes: L*m*128 doubles [table*m+bit][128]; long_planes: n*128 doubles. */
+chgpu_status chgpu_family_generate(const chgpu_family_params* p, double* short_planes, double* long_planes);
+/* Installs a family (planes as produced above, or by the reference) on the device. */
+chgpu_status chgpu_set_family(chgpu_ctx* ctx, const chgpu_family_params* p,
+                              const double* short_planes, const double* long_planes);
+/* Replaces set_centering / CenteringAccumulator (hashing.hpp:78,166-172; hashing.cpp:52-70). */
+chgpu_status chgpu_centering_reset(chgpu_ctx* ctx);
+chgpu_status chgpu_centering_add_image(chgpu_ctx* ctx, uint32_t image_id);
+chgpu_status chgpu_centering_get_sums(chgpu_ctx* ctx, uint64_t* sums128, uint64_t* count);
+chgpu_status chgpu_centering_add_sums(chgpu_ctx* ctx, const uint64_t* sums128, uint64_t count);
+chgpu_status chgpu_centering_apply(chgpu_ctx* ctx, double* centering128_out /* nullable */);
+chgpu_status chgpu_set_centering(chgpu_ctx* ctx, const double* centering128);
+
+/* ---- descriptor load ------------------------------------------------------------------- */
+/* Replaces the arena load of a FeatureSet (engine.cpp:394-412).  desc: n x 128 u8 row-major;
+ * keypoints: n x 4 f32 (x, y, scale, orientation) or NULL.  Re-uploading an id replaces it. */
+chgpu_status chgpu_upload_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n,
+                                const uint8_t* desc, const float* keypoints);
+/* Replaces load_features / parse_features_blob (feature_io.cpp:65-106, engine.cpp:458-488) for a
+ * CHFT blob already in host memory: header checked on the host, the 144-byte AoS records are
+ * split into SoA on the device.  On CHGPU_EFORMAT *fault / *fault_offset carry the reference's
+ * FeatureFileFault class and byte offset. */
+chgpu_status chgpu_upload_chft(chgpu_ctx* ctx, uint32_t image_id, const void* blob, size_t nbytes,
+                               uint32_t* count_out, chgpu_file_fault* fault, uint64_t* fault_offset);
+chgpu_status chgpu_evict_image(chgpu_ctx* ctx, uint32_t image_id);
+chgpu_status chgpu_image_points(chgpu_ctx* ctx, uint32_t image_id, uint32_t* n);
+chgpu_status chgpu_download_descriptors(chgpu_ctx* ctx, uint32_t image_id, uint8_t* desc, float* keypoints);
+
+/* ---- hash build ------------------------------------------------------------------------ */
+/* Replaces compute_codes (hashing.hpp:131, hashing.cpp:130-149) + build_bucket_index
+ * (matcher.hpp:43, matcher.cpp:27-51) for the listed images.  reduce_rounds = N_r in 0..7. */
+chgpu_status chgpu_hash_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32_t count, int reduce_rounds);
+/* shorts: n x L u32 [point*L+table]; longs: n x 2 u64 (ShortCodes / LongCode, hashing.hpp:80-96). */
+chgpu_status chgpu_download_codes(chgpu_ctx* ctx, uint32_t image_id, uint32_t* shorts, uint64_t* longs);
+/* Installs externally computed codes (e.g. a CHCC code cache, hashing.hpp:138-162) and builds buckets. */
+chgpu_status chgpu_upload_codes(chgpu_ctx* ctx, uint32_t image_id, const uint32_t* shorts, const uint64_t* longs);
+/* Dense CSR of the bucket index: offsets L*(2^m+1) u32, points L*n u32 (bucket-major, ascending id). */
+chgpu_status chgpu_download_bucket_index(chgpu_ctx* ctx, uint32_t image_id, uint32_t* offsets, uint32_t* points);
+
+/* ---- match ----------------------------------------------------------------------------- */
+/* Replaces match_pair over a pair list (matcher.hpp:98-100, matcher.cpp:141-203; pair list as in
+ * PlanTask::pairs, scheduler.hpp:36-40).  pairs[2k] is the query image I, pairs[2k+1] the train
+ * image J.  offsets (npairs+1) and records (capacity entries) are filled in pair order; records
+ * of one pair are ascending in query_index, at most one per query.  If capacity is too small the
+ * call returns CHGPU_ENOMEM and *total holds the required number of records. */
+chgpu_status chgpu_match_pairs(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
+                               const chgpu_match_cfg* cfg, uint64_t* offsets,
+                               chgpu_match_record* records, uint64_t capacity, uint64_t* total,
+                               chgpu_match_stats* stats /* nullable */);
+
+/* Streaming form: the asynchronous sink contract of FileMatchSink::accept (engine.cpp:145-160).
+ * The sink is called on the calling thread, in pair order, with pinned host memory that stays
+ * valid until it returns; the next sub-batch is already computing on the device meanwhile.
+ * offsets has npairs_chunk+1 entries relative to records.  A nonzero return aborts the call. */
+typedef int (*chgpu_sink_fn)(void* user, uint32_t first_pair, uint32_t npairs_chunk,
+                             const uint64_t* offsets, const chgpu_match_record* records);
+chgpu_status chgpu_match_pairs_stream(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
+                                      const chgpu_match_cfg* cfg, chgpu_sink_fn sink, void* user,
+                                      chgpu_match_stats* stats /* nullable */);
+
+/* Device-resident form used for kernel-only timing: results are compacted into device memory
+ * and only the counters / checksum in stats come back. */
+chgpu_status chgpu_match_pairs_device(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
+                                      const chgpu_match_cfg* cfg, chgpu_match_stats* stats);
+
+/* Parity hook: the ranked candidate list each query hands to verification (after the re-rank
+ * fallback, matcher.cpp:176-189).  ranked: n_i*top_k u32, ranked_count: n_i u32. */
+chgpu_status chgpu_debug_ranked(chgpu_ctx* ctx, uint32_t image_i, uint32_t image_j,
+                                const chgpu_match_cfg* cfg, uint32_t* ranked, uint32_t* ranked_count);
+
+/* ---- match output ---------------------------------------------------------------------- */
+/* Replaces save_matches (feature_io.hpp:106-107, feature_io.cpp:161-183): byte-identical text. */
+chgpu_status chgpu_save_matches(const char* image_id_i, const char* image_id_j,
+                                const chgpu_match_record* records, uint32_t count, const char* path);
+/* pair_file_name (engine.cpp:724-728): "match_%06u_%06u.txt"; buf must hold 48 bytes. */
+void chgpu_pair_file_name(uint32_t image_i, uint32_t image_j, char* buf);
+
+/* ---- pair lists ------------------------------------------------------------------------ */
+/* Exhaustive pair list in the reference's locality order (plan_exhaustive, scheduler.cpp:99-142)
+ * for image_count images in blocks of block_images, blocks_per_group blocks per group.
+ * pairs_out holds image_count*(image_count-1) u32 (2 per pair). */
+chgpu_status chgpu_plan_exhaustive(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group,
+                                   uint32_t* pairs_out, uint64_t* npairs_out);
+/* Shard [0,npairs) for rank `rank` of `world`: contiguous ranges of the plan, so each GPU keeps
+ * its train images hot (replaces assign_workers, scheduler.cpp:166-173). */
+void chgpu_shard_range(uint64_t npairs, uint32_t rank, uint32_t world, uint64_t* first, uint64_t* last);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

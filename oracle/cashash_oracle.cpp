@@ -1,0 +1,510 @@
+// cashash_oracle.cpp — CPU restatement of the reference Cascade Hashing hot path.
+//
+// TEST INFRASTRUCTURE ONLY (see chor.h).  This file restates, independently and over flat
+// arrays, what /root/reference/proj computes on the path
+//     build_hash_family -> set_centering -> compute_codes -> build_bucket_index -> match_pair
+// Each function cites the reference file:line it follows.  Parity is PINNED: tests/test_oracle.py
+// checks this file against (a) SPEC.md's worked examples, (b) the golden vectors in
+// tests/golden/ produced by the compiled reference (oracle/_ref, see oracle/Makefile and
+// tests/golden/make_golden.py) and (c), when oracle/_ref is present, the compiled reference
+// itself on fresh random inputs.
+//
+// Build: g++ -std=gnu++20 -O3 -ffp-contract=off (no -march: an FMA contraction of the
+// product/add pairs in reduce_dot would change sign bits of near-zero projections).
+
+#include "chor.h"
+
+#include <algorithm>
+#include <bit>
+#include <charconv>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+constexpr int kDim = 128;
+
+// splitmix64 finaliser and the seed-derivation tuples: reference rng.hpp:18-31.
+uint64_t mix1(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+uint64_t mix3(uint64_t seed, uint64_t a, uint64_t b) {
+    return mix1(mix1(seed ^ mix1(a)) ^ mix1(b ^ 0xd6e8feb86659fd93ULL));
+}
+
+// 53-bit uniform and Box-Muller normal, two generator words per variate: rng.hpp:34-54.
+double unit53(std::mt19937_64& g) { return static_cast<double>(g() >> 11) * 0x1.0p-53; }
+double normal_bm(std::mt19937_64& g) {
+    const double u1 = 1.0 - unit53(g);
+    const double u2 = unit53(g);
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586476925286766559 * u2);
+}
+
+// Tree-then-serial inner product: hashing.hpp:24-43.  Products are rounded before any add.
+double tree_dot(const double* a, const double* b, int tail_rounds) {
+    double s[kDim];
+    for (int i = 0; i < kDim; ++i) s[i] = a[i] * b[i];
+    const int tail = 1 << tail_rounds;
+    for (int w = kDim / 2; w >= tail; w /= 2)
+        for (int i = 0; i < w; ++i) s[i] = s[i] + s[i + w];
+    double acc = s[0];
+    for (int i = 1; i < tail; ++i) acc = acc + s[i];
+    return acc;
+}
+
+bool family_ok(const chor_family_params& p) {  // hashing.cpp:30-36
+    if (p.short_bits < 1 || p.short_bits > 32) return false;
+    if (p.long_bits <= p.short_bits || p.long_bits > static_cast<uint32_t>(kDim)) return false;
+    return p.table_count >= 1;
+}
+
+bool cfg_ok(const chor_match_cfg& c, uint32_t long_bits) {  // matcher.cpp:9-17
+    if (c.top_k < 2) return false;
+    if (c.hamming_threshold > long_bits) return false;
+    if (!(c.ratio > 0.0 && c.ratio < 1.0)) return false;
+    return c.reduce_rounds >= 0 && c.reduce_rounds <= 7;
+}
+
+int hamming128(const uint64_t* a, const uint64_t* b) {  // hashing.hpp:98-101
+    return std::popcount(a[0] ^ b[0]) + std::popcount(a[1] ^ b[1]);
+}
+
+// Exact squared distance via the same tree reduction on integer-valued doubles: matcher.cpp:106-113.
+double dist_sq(const uint8_t* a, const uint8_t* b, int rounds) {
+    double diff[kDim];
+    for (int i = 0; i < kDim; ++i) diff[i] = static_cast<double>(a[i]) - static_cast<double>(b[i]);
+    return tree_dot(diff, diff, rounds);
+}
+
+// Sparse bucket index exactly as the reference stores it (sorted unique codes + CSR):
+// matcher.cpp:27-51.  Works for every m <= 32.
+struct SparseTable {
+    std::vector<uint32_t> codes, offsets, points;
+    void lookup(uint32_t code, const uint32_t*& first, const uint32_t*& last) const {  // matcher.cpp:19-25
+        const auto it = std::lower_bound(codes.begin(), codes.end(), code);
+        if (it == codes.end() || *it != code) {
+            first = last = nullptr;
+            return;
+        }
+        const size_t slot = static_cast<size_t>(it - codes.begin());
+        first = points.data() + offsets[slot];
+        last = points.data() + offsets[slot + 1];
+    }
+};
+
+std::vector<SparseTable> build_sparse_index(uint32_t L, const uint32_t* shorts, uint32_t npts) {
+    std::vector<SparseTable> tables(L);
+    std::vector<std::pair<uint32_t, uint32_t>> e(npts);
+    for (uint32_t t = 0; t < L; ++t) {
+        for (uint32_t p = 0; p < npts; ++p) e[p] = {shorts[static_cast<size_t>(p) * L + t], p};
+        std::sort(e.begin(), e.end());
+        SparseTable& tb = tables[t];
+        tb.points.resize(npts);
+        for (uint32_t i = 0; i < npts; ++i) {
+            if (i == 0 || e[i].first != e[i - 1].first) {
+                tb.codes.push_back(e[i].first);
+                tb.offsets.push_back(i);
+            }
+            tb.points[i] = e[i].second;
+        }
+        tb.offsets.push_back(npts);
+    }
+    return tables;
+}
+
+// Two-pass counting sort over distances 0..threshold: matcher.cpp:68-84.
+struct Ranker {
+    std::vector<uint32_t> dists, offsets, items, cursor;
+    void fill(const uint64_t* q, const std::vector<uint32_t>& cands, const uint64_t* train_longs,
+              uint32_t threshold) {
+        dists.resize(cands.size());
+        offsets.assign(threshold + 2, 0);
+        for (size_t i = 0; i < cands.size(); ++i) {
+            const uint32_t d = static_cast<uint32_t>(hamming128(q, train_longs + 2 * static_cast<size_t>(cands[i])));
+            dists[i] = d;
+            if (d <= threshold) ++offsets[d + 1];
+        }
+        for (uint32_t d = 0; d <= threshold; ++d) offsets[d + 1] += offsets[d];
+        items.resize(offsets[threshold + 1]);
+        cursor.assign(offsets.begin(), offsets.end() - 1);
+        for (size_t i = 0; i < cands.size(); ++i)
+            if (dists[i] <= threshold) items[cursor[dists[i]]++] = cands[i];
+    }
+};
+
+int match_pair_impl(const chor_family_params& p, const chor_match_cfg& cfg,
+                    const uint8_t* desc_i, uint32_t n_i, const uint32_t* shorts_i, const uint64_t* longs_i,
+                    const uint8_t* desc_j, uint32_t n_j, const uint32_t* shorts_j, const uint64_t* longs_j,
+                    chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
+                    uint32_t* ranked_out, uint32_t* ranked_count) {
+    // matcher.cpp:141-195.  Family equality / count checks are structural in this flat ABI.
+    if (!family_ok(p) || !cfg_ok(cfg, p.long_bits)) return 1;
+    chor_pair_stats st{};
+    uint32_t nrec = 0;
+    if (ranked_count) std::fill(ranked_count, ranked_count + n_i, 0u);
+    if (n_i != 0 && n_j != 0) {
+        const uint32_t L = p.table_count;
+        const auto index = build_sparse_index(L, shorts_j, n_j);
+        const uint32_t min_ranked = std::max<uint32_t>(2, cfg.min_candidates_for_ratio);
+        std::vector<uint32_t> cands;
+        Ranker rk;
+        for (uint32_t q = 0; q < n_i; ++q) {
+            cands.clear();
+            for (uint32_t t = 0; t < L; ++t) {
+                const uint32_t *f, *l;
+                index[t].lookup(shorts_i[static_cast<size_t>(q) * L + t], f, l);
+                cands.insert(cands.end(), f, l);
+            }
+            st.raw_candidates += cands.size();
+            std::sort(cands.begin(), cands.end());
+            cands.erase(std::unique(cands.begin(), cands.end()), cands.end());
+            st.unique_candidates += cands.size();
+            if (cands.empty()) continue;
+
+            const uint64_t* ql = longs_i + 2 * static_cast<size_t>(q);
+            rk.fill(ql, cands, longs_j, cfg.hamming_threshold);
+            size_t keep = std::min<size_t>(cfg.top_k, rk.items.size());
+            if (keep != 0) ++st.ranked_queries;
+            // Re-rank fallback (matcher.cpp:179-189): non-empty, too small for the ratio test,
+            // and the threshold actually cut something.
+            if (keep != 0 && keep < min_ranked && cands.size() > rk.items.size()) {
+                rk.fill(ql, cands, longs_j, p.long_bits);
+                keep = std::min<size_t>(cfg.top_k, rk.items.size());
+                ++st.fallback_queries;
+            }
+            if (ranked_out) {
+                for (size_t r = 0; r < keep; ++r) ranked_out[static_cast<size_t>(q) * cfg.top_k + r] = rk.items[r];
+                ranked_count[q] = static_cast<uint32_t>(keep);
+            }
+            // euclidean_verify, matcher.cpp:115-137.
+            if (keep < 2) continue;
+            ++st.verified_queries;
+            double best = std::numeric_limits<double>::infinity();
+            double second = std::numeric_limits<double>::infinity();
+            uint32_t best_index = 0;
+            const uint8_t* qd = desc_i + static_cast<size_t>(q) * kDim;
+            for (size_t r = 0; r < keep; ++r) {
+                const uint32_t idx = rk.items[r];
+                const double d = dist_sq(qd, desc_j + static_cast<size_t>(idx) * kDim, cfg.reduce_rounds);
+                ++st.distances;
+                if (d < best) {
+                    second = best;
+                    best = d;
+                    best_index = idx;
+                } else if (d < second) {
+                    second = d;
+                }
+            }
+            if (second == 0.0) continue;
+            if (best < cfg.ratio * cfg.ratio * second) {
+                records[nrec].query_index = q;
+                records[nrec].train_index = best_index;
+                records[nrec].distance_sq = best;
+                ++nrec;
+            }
+        }
+    }
+    st.matches = nrec;
+    *record_count = nrec;
+    if (stats) *stats = st;
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* chor_name(void) { return "restatement"; }
+
+int chor_mix64_3(uint64_t seed, uint64_t a, uint64_t b, uint64_t* out) {
+    *out = mix3(seed, a, b);
+    return 0;
+}
+
+int chor_reduce_dot(const double* a, const double* b, int tail_rounds, double* out) {
+    if (tail_rounds < 0 || tail_rounds > 7) return 1;
+    *out = tree_dot(a, b, tail_rounds);
+    return 0;
+}
+
+int chor_build_family(const chor_family_params* p, double* short_planes, double* long_planes) {
+    // hashing.cpp:19-26 (draw_plane), :38-50 (table-major short planes, sentinel stream for long).
+    if (!family_ok(*p)) return 1;
+    auto draw = [&](uint64_t table, uint64_t bit, double* dst) {
+        std::mt19937_64 g(mix3(p->seed, table, bit));
+        for (int i = 0; i < kDim; ++i) dst[i] = normal_bm(g);
+    };
+    for (uint32_t t = 0; t < p->table_count; ++t)
+        for (uint32_t j = 0; j < p->short_bits; ++j)
+            draw(t, j, short_planes + (static_cast<size_t>(t) * p->short_bits + j) * kDim);
+    for (uint32_t j = 0; j < p->long_bits; ++j) draw(0xffffffffULL, j, long_planes + static_cast<size_t>(j) * kDim);
+    return 0;
+}
+
+int chor_centering_accumulate(const uint8_t* desc, uint64_t npts, uint64_t* sums128, uint64_t* count) {
+    // hashing.cpp:52-57: exact integer column sums.
+    for (uint64_t p = 0; p < npts; ++p)
+        for (int c = 0; c < kDim; ++c) sums128[c] += desc[p * kDim + c];
+    *count += npts;
+    return 0;
+}
+
+int chor_centering_apply(const uint64_t* sums128, uint64_t count, double* centering128) {
+    // hashing.cpp:59-64.
+    if (count == 0) return 1;
+    for (int c = 0; c < kDim; ++c)
+        centering128[c] = static_cast<double>(sums128[c]) / static_cast<double>(count);
+    return 0;
+}
+
+int chor_compute_codes(const chor_family_params* p, const double* short_planes,
+                       const double* long_planes, const double* centering128, int reduce_rounds,
+                       const uint8_t* desc, uint32_t npts, uint32_t* shorts, uint64_t* longs) {
+    // hashing.cpp:72-99 and :130-149.  Bit = (dot > 0.0); ties give 0.
+    if (!family_ok(*p)) return 1;
+    if (reduce_rounds < 0 || reduce_rounds > 7) return 1;
+    if (centering128 == nullptr) return 2;  // "centering has not been set" (hashing.cpp:131-132)
+    double c[kDim];
+    for (uint32_t pt = 0; pt < npts; ++pt) {
+        const uint8_t* d = desc + static_cast<size_t>(pt) * kDim;
+        for (int i = 0; i < kDim; ++i) c[i] = static_cast<double>(d[i]) - centering128[i];
+        for (uint32_t t = 0; t < p->table_count; ++t) {
+            uint32_t code = 0;
+            for (uint32_t j = 0; j < p->short_bits; ++j) {
+                const double* h = short_planes + (static_cast<size_t>(t) * p->short_bits + j) * kDim;
+                if (tree_dot(c, h, reduce_rounds) > 0.0) code |= (1u << j);
+            }
+            shorts[static_cast<size_t>(pt) * p->table_count + t] = code;
+        }
+        uint64_t w[2] = {0, 0};
+        for (uint32_t j = 0; j < p->long_bits; ++j)
+            if (tree_dot(c, long_planes + static_cast<size_t>(j) * kDim, reduce_rounds) > 0.0)
+                w[j / 64] |= (uint64_t{1} << (j % 64));
+        longs[2 * static_cast<size_t>(pt)] = w[0];
+        longs[2 * static_cast<size_t>(pt) + 1] = w[1];
+    }
+    return 0;
+}
+
+int chor_build_bucket_index(uint32_t m, uint32_t L, const uint32_t* shorts, uint32_t npts,
+                            uint32_t* offsets, uint32_t* points) {
+    if (m < 1 || m > 16 || L < 1) return 1;
+    const uint32_t nb = 1u << m;
+    const auto sparse = build_sparse_index(L, shorts, npts);
+    for (uint32_t t = 0; t < L; ++t) {
+        uint32_t* off = offsets + static_cast<size_t>(t) * (nb + 1);
+        std::fill(off, off + nb + 1, 0u);
+        const SparseTable& tb = sparse[t];
+        // Dense view: bucket c = [off[c], off[c+1]); absent codes are empty ranges.
+        size_t slot = 0;
+        for (uint32_t c = 0; c <= nb; ++c) {
+            while (slot < tb.codes.size() && tb.codes[slot] < c) ++slot;
+            off[c] = slot < tb.codes.size() ? tb.offsets[slot] : npts;
+        }
+        std::copy(tb.points.begin(), tb.points.end(), points + static_cast<size_t>(t) * npts);
+    }
+    return 0;
+}
+
+int chor_lookup_candidates(uint32_t m, uint32_t L, const uint32_t* query_codes,
+                           const uint32_t* train_shorts, uint32_t ntrain, uint32_t* out,
+                           uint32_t* out_count) {
+    (void)m;
+    const auto index = build_sparse_index(L, train_shorts, ntrain);
+    std::vector<uint32_t> c;
+    for (uint32_t t = 0; t < L; ++t) {
+        const uint32_t *f, *l;
+        index[t].lookup(query_codes[t], f, l);
+        c.insert(c.end(), f, l);
+    }
+    std::sort(c.begin(), c.end());
+    c.erase(std::unique(c.begin(), c.end()), c.end());
+    std::copy(c.begin(), c.end(), out);
+    *out_count = static_cast<uint32_t>(c.size());
+    return 0;
+}
+
+int chor_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
+                    const uint8_t* desc_i, uint32_t n_i, const uint32_t* shorts_i, const uint64_t* longs_i,
+                    const uint8_t* desc_j, uint32_t n_j, const uint32_t* shorts_j, const uint64_t* longs_j,
+                    chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
+                    uint32_t* ranked, uint32_t* ranked_count) {
+    return match_pair_impl(*p, *cfg, desc_i, n_i, shorts_i, longs_i, desc_j, n_j, shorts_j, longs_j,
+                           records, record_count, stats, ranked, ranked_count);
+}
+
+int chor_brute_force_match(const uint8_t* desc_i, uint32_t n_i, const uint8_t* desc_j, uint32_t n_j,
+                           double ratio, chor_match_record* records, uint32_t* record_count) {
+    // matcher.cpp:212-243: exact integer NN / 2nd-NN, same ratio rule.
+    uint32_t nrec = 0;
+    if (n_j >= 2) {
+        const double r2 = ratio * ratio;
+        for (uint32_t q = 0; q < n_i; ++q) {
+            uint64_t best = std::numeric_limits<uint64_t>::max(), second = best;
+            uint32_t bi = 0;
+            for (uint32_t t = 0; t < n_j; ++t) {
+                uint64_t d = 0;
+                for (int c = 0; c < kDim; ++c) {
+                    const int df = int(desc_i[size_t(q) * kDim + c]) - int(desc_j[size_t(t) * kDim + c]);
+                    d += static_cast<uint64_t>(df * df);
+                }
+                if (d < best) {
+                    second = best;
+                    best = d;
+                    bi = t;
+                } else if (d < second) {
+                    second = d;
+                }
+            }
+            if (second == 0) continue;
+            if (static_cast<double>(best) < r2 * static_cast<double>(second))
+                records[nrec++] = {q, bi, static_cast<double>(best)};
+        }
+    }
+    *record_count = nrec;
+    return 0;
+}
+
+int chor_save_matches(const char* id_i, const char* id_j, const chor_match_record* records,
+                      uint32_t count, const char* path) {
+    // feature_io.cpp:161-183: "# I J count\n" then "q t dist\n", dist = shortest round-trip decimal.
+    std::string out = "# ";
+    out += id_i;
+    out += ' ';
+    out += id_j;
+    out += ' ';
+    out += std::to_string(count);
+    out += '\n';
+    char buf[64];
+    for (uint32_t i = 0; i < count; ++i) {
+        out += std::to_string(records[i].query_index);
+        out += ' ';
+        out += std::to_string(records[i].train_index);
+        out += ' ';
+        const auto r = std::to_chars(buf, buf + sizeof(buf), records[i].distance_sq);
+        out.append(buf, r.ptr);
+        out += '\n';
+    }
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return 3;
+    const size_t w = std::fwrite(out.data(), 1, out.size(), f);
+    std::fclose(f);
+    return w == out.size() ? 0 : 3;
+}
+
+int chor_time_match_pairs(const chor_family_params* p, const chor_match_cfg* cfg,
+                          const uint8_t* const* desc, const uint32_t* counts,
+                          const uint32_t* const* shorts, const uint64_t* const* longs,
+                          const uint32_t* pairs, uint32_t npairs, uint32_t threads,
+                          double* seconds, uint64_t* total_matches) {
+    if (threads == 0) return 1;
+    std::vector<uint64_t> per_thread(threads, 0);
+    std::vector<int> rc(threads, 0);
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (uint32_t w = 0; w < threads; ++w) {
+        pool.emplace_back([&, w] {
+            std::vector<chor_match_record> rec;
+            for (uint32_t k = w; k < npairs; k += threads) {
+                const uint32_t a = pairs[2 * k], b = pairs[2 * k + 1];
+                rec.resize(counts[a]);
+                uint32_t n = 0;
+                const int r = match_pair_impl(*p, *cfg, desc[a], counts[a], shorts[a], longs[a], desc[b],
+                                              counts[b], shorts[b], longs[b], rec.data(), &n, nullptr,
+                                              nullptr, nullptr);
+                if (r != 0) rc[w] = r;
+                per_thread[w] += n;
+            }
+        });
+    }
+    for (auto& t : pool) t.join();
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    uint64_t total = 0;
+    for (uint32_t w = 0; w < threads; ++w) {
+        total += per_thread[w];
+        if (rc[w] != 0) return rc[w];
+    }
+    *total_matches = total;
+    return 0;
+}
+
+int chor_plan_exhaustive(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group,
+                         uint32_t* pairs_out, uint64_t* npairs_out, uint32_t* task_sizes, uint32_t* ntasks_out) {
+    // scheduler.cpp:10-33 (partition), :47-75 (cross / self tasks), :77-95 (chained edges), :99-142 (plan).
+    if (image_count == 0 || block_images == 0 || blocks_per_group == 0) return 1;
+    std::vector<std::pair<uint32_t, uint32_t>> ranges;
+    for (uint32_t f = 0; f < image_count; f += block_images) ranges.emplace_back(f, std::min(f + block_images, image_count));
+    const uint32_t nblocks = static_cast<uint32_t>(ranges.size());
+    std::vector<std::vector<uint32_t>> groups;
+    for (uint32_t b = 0; b < nblocks; b += blocks_per_group) {
+        groups.emplace_back();
+        for (uint32_t i = b; i < std::min(b + blocks_per_group, nblocks); ++i) groups.back().push_back(i);
+    }
+    // first the task list as (block_a, block_b) with a == b for self tasks, then the expansion
+    std::vector<std::pair<uint32_t, uint32_t>> tasks;
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const auto& A = groups[gi];
+        uint32_t j = 0;
+        bool jf = true;
+        for (size_t gk = gi + 1; gk < groups.size(); ++gk) {
+            const auto& B = groups[gk];
+            uint32_t l = 0;
+            bool lf = true;
+            for (size_t js = 0; js < A.size(); ++js) {
+                for (size_t ls = 0; ls < B.size(); ++ls) {
+                    tasks.emplace_back(std::min(A[j], B[l]), std::max(A[j], B[l]));
+                    if (ls + 1 < B.size()) l = lf ? l + 1 : l - 1;
+                }
+                lf = !lf;
+                if (js + 1 < A.size()) j = jf ? j + 1 : j - 1;
+            }
+            jf = !jf;
+        }
+        std::vector<uint32_t> label{j};
+        for (uint32_t v = 0; v < A.size(); ++v)
+            if (v != j) label.push_back(v);
+        const uint32_t cnt = static_cast<uint32_t>(A.size());
+        for (uint32_t a = 0; a + 1 < cnt; ++a) {
+            if (a % 2 == 0) {
+                for (uint32_t b = a + 1; b < cnt; ++b)
+                    tasks.emplace_back(std::min(A[label[a]], A[label[b]]), std::max(A[label[a]], A[label[b]]));
+            } else {
+                for (uint32_t b = cnt; b-- > a + 1;)
+                    tasks.emplace_back(std::min(A[label[a]], A[label[b]]), std::max(A[label[a]], A[label[b]]));
+            }
+        }
+        for (uint32_t blk : A)
+            if (ranges[blk].second - ranges[blk].first >= 2) tasks.emplace_back(blk, blk);
+    }
+    uint64_t np = 0;
+    uint32_t nt = 0;
+    for (const auto& [ba, bb] : tasks) {
+        uint32_t sz = 0;
+        if (ba == bb) {
+            for (uint32_t a = ranges[ba].first; a < ranges[ba].second; ++a)
+                for (uint32_t b = a + 1; b < ranges[ba].second; ++b, ++sz)
+                    if (pairs_out) { pairs_out[2 * np] = a; pairs_out[2 * np + 1] = b; ++np; } else ++np;
+        } else {
+            for (uint32_t a = ranges[ba].first; a < ranges[ba].second; ++a)
+                for (uint32_t b = ranges[bb].first; b < ranges[bb].second; ++b, ++sz)
+                    if (pairs_out) { pairs_out[2 * np] = a; pairs_out[2 * np + 1] = b; ++np; } else ++np;
+        }
+        if (task_sizes) task_sizes[nt] = sz;
+        ++nt;
+    }
+    *npairs_out = np;
+    if (ntasks_out) *ntasks_out = nt;
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+/*
+ * chor.h — C ABI shared by the two CPU checkers of the Cascade Hashing hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Two shared objects export exactly this ABI:
+ *   oracle/libchoracle.so        independent CPU restatement (oracle/cashash_oracle.cpp)
+ *   oracle/_ref/libcashash_ref.so the reference's own translation units, compiled in place
+ *                                 from /root/reference/proj/src, behind oracle/ref_shim.cpp
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+ * legs may load them.  The product (libchgpu.so) never links or calls anything here.
+ *
+ * All arrays are flat, caller-allocated, little-endian host memory.
+ *   descriptors : npts x 128 u8, row-major
+ *   short codes : npts x L u32, [point*L + table]        (reference ShortCodes::values, hashing.hpp:80-89)
+ *   long codes  : npts x 2 u64, bit j in word j/64 bit j%64 (reference LongCode, hashing.hpp:91-96)
+ *   planes      : double[128] per plane; short planes ordered [table*m + bit] (hashing.hpp:62-72)
+ */
+#ifndef CHOR_H
+#define CHOR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct chor_family_params {
+    uint32_t short_bits;  /* m */
+    uint32_t long_bits;   /* n */
+    uint32_t table_count; /* L */
+    uint64_t seed;
+} chor_family_params;
+
+typedef struct chor_match_cfg {
+    uint32_t top_k;
+    uint32_t hamming_threshold;
+    double ratio;
+    uint32_t min_candidates_for_ratio;
+    int32_t reduce_rounds;
+} chor_match_cfg;
+
+/* Layout-identical to the reference MatchRecord (feature_io.hpp:51-57): 16 bytes. */
+typedef struct chor_match_record {
+    uint32_t query_index;
+    uint32_t train_index;
+    double distance_sq;
+} chor_match_record;
+
+/* Per-pair statistics used by bench.py to evaluate SURVEY.md §8(d)'s bytes_pair formula. */
+typedef struct chor_pair_stats {
+    uint64_t raw_candidates;    /* R  : sum over queries and tables of bucket sizes */
+    uint64_t unique_candidates; /* sum over queries of |deduplicated candidate set|  */
+    uint64_t ranked_queries;    /* queries with a non-empty thresholded ranking        */
+    uint64_t fallback_queries;  /* queries re-ranked without the threshold             */
+    uint64_t verified_queries;  /* Vq : queries reaching verification with >=2 ranked  */
+    uint64_t distances;         /* V  : Euclidean distances computed                   */
+    uint64_t matches;           /* Mx */
+} chor_pair_stats;
+
+/* Return codes: 0 ok, 1 invalid argument (std::invalid_argument in the reference),
+ * 2 logic error (std::logic_error), 3 other failure. */
+const char* chor_name(void);
+
+int chor_mix64_3(uint64_t seed, uint64_t a, uint64_t b, uint64_t* out);
+int chor_reduce_dot(const double* a, const double* b, int tail_rounds, double* out);
+
+int chor_build_family(const chor_family_params* p, double* short_planes, double* long_planes);
+
+int chor_centering_accumulate(const uint8_t* desc, uint64_t npts, uint64_t* sums128, uint64_t* count);
+int chor_centering_apply(const uint64_t* sums128, uint64_t count, double* centering128);
+
+int chor_compute_codes(const chor_family_params* p, const double* short_planes,
+                       const double* long_planes, const double* centering128, int reduce_rounds,
+                       const uint8_t* desc, uint32_t npts, uint32_t* shorts, uint64_t* longs);
+
+/* Dense CSR view of the bucket index (requires m <= 16): per table 2^m+1 offsets and npts
+ * point ids, bucket-major, ascending id inside a bucket (matcher.cpp:27-51). */
+int chor_build_bucket_index(uint32_t m, uint32_t L, const uint32_t* shorts, uint32_t npts,
+                            uint32_t* offsets /* L*(2^m+1) */, uint32_t* points /* L*npts */);
+
+/* Deduplicated ascending candidate set of one query (matcher.cpp:53-63). Returns count. */
+int chor_lookup_candidates(uint32_t m, uint32_t L, const uint32_t* query_codes /* L */,
+                           const uint32_t* train_shorts, uint32_t ntrain, uint32_t* out /* ntrain */,
+                           uint32_t* out_count);
+
+/* Full pair pipeline (matcher.cpp:141-203).  records must hold n_i entries.
+ * ranked / ranked_count (optional, may be NULL): the final ranked list per query that
+ * euclidean_verify consumed (after the re-rank fallback), ranked[q*top_k + r]. */
+int chor_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
+                    const uint8_t* desc_i, uint32_t n_i, const uint32_t* shorts_i, const uint64_t* longs_i,
+                    const uint8_t* desc_j, uint32_t n_j, const uint32_t* shorts_j, const uint64_t* longs_j,
+                    chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
+                    uint32_t* ranked, uint32_t* ranked_count);
+
+int chor_brute_force_match(const uint8_t* desc_i, uint32_t n_i, const uint8_t* desc_j, uint32_t n_j,
+                           double ratio, chor_match_record* records, uint32_t* record_count);
+
+/* Text match file exactly as the reference writes it (feature_io.cpp:161-183). */
+int chor_save_matches(const char* id_i, const char* id_j, const chor_match_record* records,
+                      uint32_t count, const char* path);
+
+/* CPU throughput probe for bench.py: runs match_pair over pairs[2*npairs] of a dataset held as
+ * arrays of per-image pointers, on `threads` std::threads each taking a disjoint strided slice
+ * (the reference's worker model, engine.cpp:686).  Returns wall seconds and total matches. */
+int chor_time_match_pairs(const chor_family_params* p, const chor_match_cfg* cfg,
+                          const uint8_t* const* desc, const uint32_t* counts,
+                          const uint32_t* const* shorts, const uint64_t* const* longs,
+                          const uint32_t* pairs, uint32_t npairs, uint32_t threads,
+                          double* seconds, uint64_t* total_matches);
+
+/* Flattened pair list of plan_exhaustive (scheduler.cpp:99-142) in task order; pairs_out holds
+ * image_count*(image_count-1) u32.  task_sizes (optional) receives the pair count of every task,
+ * ntasks_out their number. */
+int chor_plan_exhaustive(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group,
+                         uint32_t* pairs_out, uint64_t* npairs_out, uint32_t* task_sizes, uint32_t* ntasks_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

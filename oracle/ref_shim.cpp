@@ -1,0 +1,339 @@
+// ref_shim.cpp — chor.h ABI implemented by CALLING the reference's own code.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled together with the reference translation units
+// /root/reference/proj/src/{feature_io,hashing,matcher}.cpp where they lie (see oracle/Makefile)
+// into oracle/_ref/libcashash_ref.so.  No reference source is copied into this repository;
+// this file only marshals flat arrays into the reference's value types and back.
+
+#include "chor.h"
+
+#include <chrono>
+#include <cstring>
+#include <stdexcept>
+#include <thread>
+#include <vector>
+
+#include "cashash/feature_io.hpp"
+#include "cashash/hashing.hpp"
+#include "cashash/matcher.hpp"
+#include "cashash/rng.hpp"
+#include "cashash/scheduler.hpp"
+
+namespace {
+
+using namespace cashash;
+
+FamilyParams to_params(const chor_family_params& p) {
+    FamilyParams fp;
+    fp.short_bits = p.short_bits;
+    fp.long_bits = p.long_bits;
+    fp.table_count = p.table_count;
+    fp.seed = p.seed;
+    return fp;
+}
+
+MatchConfig to_cfg(const chor_match_cfg& c) {
+    MatchConfig mc;
+    mc.top_k = c.top_k;
+    mc.hamming_threshold = c.hamming_threshold;
+    mc.ratio = c.ratio;
+    mc.min_candidates_for_ratio = c.min_candidates_for_ratio;
+    mc.reduce_rounds = c.reduce_rounds;
+    return mc;
+}
+
+FeatureSet to_features(const uint8_t* desc, uint32_t n) {
+    FeatureSet fs;
+    fs.keypoints.resize(n);
+    fs.descriptors.resize(n);
+    for (uint32_t i = 0; i < n; ++i) std::memcpy(fs.descriptors[i].data(), desc + size_t(i) * 128, 128);
+    return fs;
+}
+
+ImageCodes to_codes(const FamilyParams& fp, const uint32_t* shorts, const uint64_t* longs, uint32_t n) {
+    ImageCodes c;
+    c.params = fp;
+    c.shorts.short_bits = fp.short_bits;
+    c.shorts.table_count = fp.table_count;
+    c.shorts.point_count = n;
+    c.shorts.values.assign(shorts, shorts + size_t(n) * fp.table_count);
+    c.longs.long_bits = fp.long_bits;
+    c.longs.codes.resize(n);
+    for (uint32_t i = 0; i < n; ++i) {
+        c.longs.codes[i].words = {longs[2 * size_t(i)], longs[2 * size_t(i) + 1]};
+        c.longs.codes[i].bits = static_cast<uint16_t>(fp.long_bits);
+    }
+    return c;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return 1;
+    } catch (const std::logic_error&) {
+        return 2;
+    } catch (...) {
+        return 3;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* chor_name(void) { return "reference"; }
+
+int chor_mix64_3(uint64_t seed, uint64_t a, uint64_t b, uint64_t* out) {
+    *out = mix64(seed, a, b);
+    return 0;
+}
+
+int chor_reduce_dot(const double* a, const double* b, int tail_rounds, double* out) {
+    return guarded([&] {
+        *out = reduce_dot<double>(std::span<const double>(a, 128), std::span<const double>(b, 128), tail_rounds);
+    });
+}
+
+int chor_build_family(const chor_family_params* p, double* short_planes, double* long_planes) {
+    return guarded([&] {
+        const HashFamily fam = build_hash_family(to_params(*p));
+        for (size_t i = 0; i < fam.short_planes.size(); ++i)
+            std::memcpy(short_planes + i * 128, fam.short_planes[i].data(), 128 * sizeof(double));
+        for (size_t i = 0; i < fam.long_planes.size(); ++i)
+            std::memcpy(long_planes + i * 128, fam.long_planes[i].data(), 128 * sizeof(double));
+    });
+}
+
+int chor_centering_accumulate(const uint8_t* desc, uint64_t npts, uint64_t* sums128, uint64_t* count) {
+    return guarded([&] {
+        CenteringAccumulator acc;
+        std::memcpy(acc.sums.data(), sums128, sizeof(acc.sums));
+        acc.count = *count;
+        acc.add(to_features(desc, static_cast<uint32_t>(npts)));
+        std::memcpy(sums128, acc.sums.data(), sizeof(acc.sums));
+        *count = acc.count;
+    });
+}
+
+int chor_centering_apply(const uint64_t* sums128, uint64_t count, double* centering128) {
+    return guarded([&] {
+        CenteringAccumulator acc;
+        std::memcpy(acc.sums.data(), sums128, sizeof(acc.sums));
+        acc.count = count;
+        HashFamily fam;
+        acc.apply(fam);
+        std::memcpy(centering128, fam.centering.data(), sizeof(fam.centering));
+    });
+}
+
+static HashFamily make_family(const chor_family_params& p, const double* sp, const double* lp,
+                              const double* centering) {
+    HashFamily fam;
+    fam.params = to_params(p);
+    fam.short_planes.resize(size_t(p.table_count) * p.short_bits);
+    fam.long_planes.resize(p.long_bits);
+    for (size_t i = 0; i < fam.short_planes.size(); ++i)
+        std::memcpy(fam.short_planes[i].data(), sp + i * 128, 128 * sizeof(double));
+    for (size_t i = 0; i < fam.long_planes.size(); ++i)
+        std::memcpy(fam.long_planes[i].data(), lp + i * 128, 128 * sizeof(double));
+    if (centering) {
+        std::memcpy(fam.centering.data(), centering, sizeof(fam.centering));
+        fam.centering_set = true;
+    }
+    return fam;
+}
+
+int chor_compute_codes(const chor_family_params* p, const double* short_planes,
+                       const double* long_planes, const double* centering128, int reduce_rounds,
+                       const uint8_t* desc, uint32_t npts, uint32_t* shorts, uint64_t* longs) {
+    return guarded([&] {
+        validate(to_params(*p));
+        const HashFamily fam = make_family(*p, short_planes, long_planes, centering128);
+        const ImageCodes codes = compute_codes(fam, to_features(desc, npts), reduce_rounds);
+        std::memcpy(shorts, codes.shorts.values.data(), codes.shorts.values.size() * sizeof(uint32_t));
+        for (uint32_t i = 0; i < npts; ++i) {
+            longs[2 * size_t(i)] = codes.longs.codes[i].words[0];
+            longs[2 * size_t(i) + 1] = codes.longs.codes[i].words[1];
+        }
+    });
+}
+
+int chor_build_bucket_index(uint32_t m, uint32_t L, const uint32_t* shorts, uint32_t npts,
+                            uint32_t* offsets, uint32_t* points) {
+    if (m < 1 || m > 16 || L < 1) return 1;
+    return guarded([&] {
+        ShortCodes sc;
+        sc.short_bits = m;
+        sc.table_count = L;
+        sc.point_count = npts;
+        sc.values.assign(shorts, shorts + size_t(npts) * L);
+        const BucketIndex idx = build_bucket_index(sc);
+        const uint32_t nb = 1u << m;
+        for (uint32_t t = 0; t < L; ++t) {
+            uint32_t* off = offsets + size_t(t) * (nb + 1);
+            uint32_t running = 0;
+            for (uint32_t c = 0; c < nb; ++c) {
+                off[c] = running;
+                running += static_cast<uint32_t>(idx.bucket(t, c).size());
+            }
+            off[nb] = running;
+            std::memcpy(points + size_t(t) * npts, idx.tables[t].points.data(), size_t(npts) * sizeof(uint32_t));
+        }
+    });
+}
+
+int chor_lookup_candidates(uint32_t m, uint32_t L, const uint32_t* query_codes,
+                           const uint32_t* train_shorts, uint32_t ntrain, uint32_t* out,
+                           uint32_t* out_count) {
+    return guarded([&] {
+        ShortCodes sc;
+        sc.short_bits = m;
+        sc.table_count = L;
+        sc.point_count = ntrain;
+        sc.values.assign(train_shorts, train_shorts + size_t(ntrain) * L);
+        const BucketIndex idx = build_bucket_index(sc);
+        const auto c = lookup_candidates(std::span<const uint32_t>(query_codes, L), idx);
+        std::memcpy(out, c.data(), c.size() * sizeof(uint32_t));
+        *out_count = static_cast<uint32_t>(c.size());
+    });
+}
+
+int chor_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
+                    const uint8_t* desc_i, uint32_t n_i, const uint32_t* shorts_i, const uint64_t* longs_i,
+                    const uint8_t* desc_j, uint32_t n_j, const uint32_t* shorts_j, const uint64_t* longs_j,
+                    chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
+                    uint32_t* ranked, uint32_t* ranked_count) {
+    return guarded([&] {
+        const FamilyParams fp = to_params(*p);
+        validate(fp);
+        const MatchConfig mc = to_cfg(*cfg);
+        const FeatureSet fi = to_features(desc_i, n_i), fj = to_features(desc_j, n_j);
+        const ImageCodes ci = to_codes(fp, shorts_i, longs_i, n_i), cj = to_codes(fp, shorts_j, longs_j, n_j);
+        const std::vector<MatchRecord> out = match_pair(fi, fj, ci, cj, mc);
+        static_assert(sizeof(MatchRecord) == sizeof(chor_match_record));
+        std::memcpy(records, out.data(), out.size() * sizeof(MatchRecord));
+        *record_count = static_cast<uint32_t>(out.size());
+
+        if (stats || ranked) {
+            // Intermediate artefacts through the reference's PUBLIC ops only (lookup_candidates,
+            // rank_histogram); the re-rank rule is the one stated at matcher.hpp:18-21.
+            chor_pair_stats st{};
+            if (ranked_count) std::fill(ranked_count, ranked_count + n_i, 0u);
+            if (n_i && n_j) {
+                const BucketIndex idx = build_bucket_index(cj.shorts);
+                const uint32_t min_ranked = std::max<uint32_t>(2, mc.min_candidates_for_ratio);
+                for (uint32_t q = 0; q < n_i; ++q) {
+                    std::span<const uint32_t> qc(ci.shorts.values.data() + size_t(q) * fp.table_count, fp.table_count);
+                    for (uint32_t t = 0; t < fp.table_count; ++t) st.raw_candidates += idx.bucket(t, qc[t]).size();
+                    const auto cands = lookup_candidates(qc, idx);
+                    st.unique_candidates += cands.size();
+                    if (cands.empty()) continue;
+                    RankHistogram h = rank_histogram(ci.longs.codes[q], cands, cj.longs.codes, mc.hamming_threshold);
+                    size_t keep = std::min<size_t>(mc.top_k, h.items.size());
+                    if (keep) ++st.ranked_queries;
+                    if (keep && keep < min_ranked && cands.size() > h.items.size()) {
+                        h = rank_histogram(ci.longs.codes[q], cands, cj.longs.codes, fp.long_bits);
+                        keep = std::min<size_t>(mc.top_k, h.items.size());
+                        ++st.fallback_queries;
+                    }
+                    if (ranked) {
+                        for (size_t r = 0; r < keep; ++r) ranked[size_t(q) * mc.top_k + r] = h.items[r];
+                        ranked_count[q] = static_cast<uint32_t>(keep);
+                    }
+                    if (keep >= 2) {
+                        ++st.verified_queries;
+                        st.distances += keep;
+                    }
+                }
+            }
+            st.matches = out.size();
+            if (stats) *stats = st;
+        }
+    });
+}
+
+int chor_brute_force_match(const uint8_t* desc_i, uint32_t n_i, const uint8_t* desc_j, uint32_t n_j,
+                           double ratio, chor_match_record* records, uint32_t* record_count) {
+    return guarded([&] {
+        const auto out = brute_force_match(to_features(desc_i, n_i), to_features(desc_j, n_j), ratio);
+        std::memcpy(records, out.data(), out.size() * sizeof(MatchRecord));
+        *record_count = static_cast<uint32_t>(out.size());
+    });
+}
+
+int chor_save_matches(const char* id_i, const char* id_j, const chor_match_record* records,
+                      uint32_t count, const char* path) {
+    return guarded([&] {
+        std::vector<MatchRecord> v(count);
+        std::memcpy(static_cast<void*>(v.data()), records, size_t(count) * sizeof(MatchRecord));
+        save_matches(id_i, id_j, v, path);
+    });
+}
+
+int chor_time_match_pairs(const chor_family_params* p, const chor_match_cfg* cfg,
+                          const uint8_t* const* desc, const uint32_t* counts,
+                          const uint32_t* const* shorts, const uint64_t* const* longs,
+                          const uint32_t* pairs, uint32_t npairs, uint32_t threads,
+                          double* seconds, uint64_t* total_matches) {
+    if (threads == 0) return 1;
+    return guarded([&] {
+        const FamilyParams fp = to_params(*p);
+        const MatchConfig mc = to_cfg(*cfg);
+        // Marshal every image touched by the sample once, outside the timed region: the
+        // reference's engine also holds FeatureSet/ImageCodes resident (engine.cpp:394-412).
+        uint32_t max_img = 0;
+        for (uint32_t k = 0; k < 2 * npairs; ++k) max_img = std::max(max_img, pairs[k]);
+        std::vector<FeatureSet> fs(max_img + 1);
+        std::vector<ImageCodes> cs(max_img + 1);
+        std::vector<char> have(max_img + 1, 0);
+        for (uint32_t k = 0; k < 2 * npairs; ++k) {
+            const uint32_t a = pairs[k];
+            if (have[a]) continue;
+            fs[a] = to_features(desc[a], counts[a]);
+            cs[a] = to_codes(fp, shorts[a], longs[a], counts[a]);
+            have[a] = 1;
+        }
+        std::vector<uint64_t> per_thread(threads, 0);
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        for (uint32_t w = 0; w < threads; ++w)
+            pool.emplace_back([&, w] {
+                for (uint32_t k = w; k < npairs; k += threads) {
+                    const uint32_t a = pairs[2 * k], b = pairs[2 * k + 1];
+                    per_thread[w] += match_pair(fs[a], fs[b], cs[a], cs[b], mc).size();
+                }
+            });
+        for (auto& t : pool) t.join();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        uint64_t total = 0;
+        for (uint64_t v : per_thread) total += v;
+        *total_matches = total;
+    });
+}
+
+int chor_plan_exhaustive(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group,
+                         uint32_t* pairs_out, uint64_t* npairs_out, uint32_t* task_sizes, uint32_t* ntasks_out) {
+    return guarded([&] {
+        const PairPlan plan = plan_exhaustive(make_partition(image_count, block_images, blocks_per_group));
+        uint64_t np = 0;
+        uint32_t nt = 0;
+        for (const PlanTask& t : plan.tasks) {
+            for (const auto& [a, b] : t.pairs) {
+                if (pairs_out) {
+                    pairs_out[2 * np] = a;
+                    pairs_out[2 * np + 1] = b;
+                }
+                ++np;
+            }
+            if (task_sizes) task_sizes[nt] = static_cast<uint32_t>(t.pairs.size());
+            ++nt;
+        }
+        *npairs_out = np;
+        if (ntasks_out) *ntasks_out = nt;
+    });
+}
+
+}  // extern "C"

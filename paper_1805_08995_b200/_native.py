@@ -1,0 +1,126 @@
+"""ctypes binding of libchgpu.so (include/chgpu.h).  There is no fallback: a missing library or a
+missing CUDA device raises."""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libchgpu.so"
+SYNTH_PATH = PKG / "libchsynth.so"
+
+u8p = C.POINTER(C.c_uint8)
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+f32p = C.POINTER(C.c_float)
+f64p = C.POINTER(C.c_double)
+
+OK, EINVAL, ELOGIC, ECUDA, ENOMEM, EUNSUPPORTED, EFORMAT, ENOTFOUND = range(8)
+
+
+class FamilyParamsC(C.Structure):
+    _fields_ = [("short_bits", C.c_uint32), ("long_bits", C.c_uint32), ("table_count", C.c_uint32),
+                ("seed", C.c_uint64)]
+
+
+class MatchCfgC(C.Structure):
+    _fields_ = [("top_k", C.c_uint32), ("hamming_threshold", C.c_uint32), ("ratio", C.c_double),
+                ("min_candidates_for_ratio", C.c_uint32), ("reduce_rounds", C.c_int32)]
+
+
+class MatchRecordC(C.Structure):
+    _fields_ = [("query_index", C.c_uint32), ("train_index", C.c_uint32), ("distance_sq", C.c_double)]
+
+
+class MatchStatsC(C.Structure):
+    _fields_ = [("pairs", C.c_uint64), ("matches", C.c_uint64), ("raw_candidates", C.c_uint64),
+                ("verified_queries", C.c_uint64), ("distances", C.c_uint64), ("query_points", C.c_uint64),
+                ("train_points", C.c_uint64), ("records_checksum", C.c_uint64),
+                ("match_launches", C.c_uint32), ("total_launches", C.c_uint32),
+                ("match_kernel_ms", C.c_float), ("total_ms", C.c_float)]
+
+    def as_dict(self) -> dict:
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class DevicePropsC(C.Structure):
+    _fields_ = [("name", C.c_char * 64), ("sm_count", C.c_int), ("cc_major", C.c_int), ("cc_minor", C.c_int),
+                ("total_mem", C.c_size_t), ("free_mem", C.c_size_t), ("smem_per_block_optin", C.c_size_t)]
+
+
+SINK_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, u64p, C.POINTER(MatchRecordC))
+
+# name -> (restype, argtypes); every symbol include/chgpu.h declares
+SIGNATURES = {
+    "chgpu_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "chgpu_destroy": (None, [C.c_void_p]),
+    "chgpu_last_error": (C.c_char_p, [C.c_void_p]),
+    "chgpu_status_name": (C.c_char_p, [C.c_int]),
+    "chgpu_get_device_props": (C.c_int, [C.c_void_p, C.POINTER(DevicePropsC)]),
+    "chgpu_sync": (C.c_int, [C.c_void_p]),
+    "chgpu_host_alloc": (C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "chgpu_host_free": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "chgpu_family_generate": (C.c_int, [C.POINTER(FamilyParamsC), f64p, f64p]),
+    "chgpu_set_family": (C.c_int, [C.c_void_p, C.POINTER(FamilyParamsC), f64p, f64p]),
+    "chgpu_centering_reset": (C.c_int, [C.c_void_p]),
+    "chgpu_centering_add_image": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "chgpu_centering_get_sums": (C.c_int, [C.c_void_p, u64p, u64p]),
+    "chgpu_centering_add_sums": (C.c_int, [C.c_void_p, u64p, C.c_uint64]),
+    "chgpu_centering_apply": (C.c_int, [C.c_void_p, f64p]),
+    "chgpu_set_centering": (C.c_int, [C.c_void_p, f64p]),
+    "chgpu_upload_image": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "chgpu_upload_chft": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_size_t, u32p,
+                                    C.POINTER(C.c_int), u64p]),
+    "chgpu_evict_image": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "chgpu_image_points": (C.c_int, [C.c_void_p, C.c_uint32, u32p]),
+    "chgpu_download_descriptors": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "chgpu_hash_images": (C.c_int, [C.c_void_p, u32p, C.c_uint32, C.c_int]),
+    "chgpu_download_codes": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "chgpu_upload_codes": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "chgpu_download_bucket_index": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "chgpu_match_pairs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(MatchCfgC), C.c_void_p,
+                                    C.c_void_p, C.c_uint64, u64p, C.POINTER(MatchStatsC)]),
+    "chgpu_match_pairs_stream": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(MatchCfgC), SINK_FN,
+                                           C.c_void_p, C.POINTER(MatchStatsC)]),
+    "chgpu_match_pairs_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(MatchCfgC),
+                                           C.POINTER(MatchStatsC)]),
+    "chgpu_debug_ranked": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(MatchCfgC), C.c_void_p,
+                                     C.c_void_p]),
+    "chgpu_save_matches": (C.c_int, [C.c_char_p, C.c_char_p, C.c_void_p, C.c_uint32, C.c_char_p]),
+    "chgpu_pair_file_name": (None, [C.c_uint32, C.c_uint32, C.c_char_p]),
+    "chgpu_plan_exhaustive": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p, u64p]),
+    "chgpu_shard_range": (None, [C.c_uint64, C.c_uint32, C.c_uint32, u64p, u64p]),
+}
+
+_lib = None
+_synth = None
+
+
+def load() -> C.CDLL:
+    """Loads libchgpu.so and binds every exported entry point; raises if it is absent."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_1805_08995_b200.build` "
+                "(the CUDA library is mandatory, there is no CPU fallback)")
+        lib = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)  # AttributeError if the header and the library disagree
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def load_synth() -> C.CDLL:
+    global _synth
+    if _synth is None:
+        if not SYNTH_PATH.exists():
+            raise RuntimeError(f"{SYNTH_PATH} is missing: run `python -m paper_1805_08995_b200.build`")
+        lib = C.CDLL(str(SYNTH_PATH))
+        lib.chsynth_dataset.restype = C.c_int
+        lib.chsynth_dataset.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, C.c_double,
+                                        C.c_int, C.c_uint32, C.c_void_p]
+        _synth = lib
+    return _synth

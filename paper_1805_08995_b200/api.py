@@ -1,0 +1,454 @@
+"""Python harness over the C ABI, shaped like the reference's matcher API.
+
+The product's host side is C++ (include/cashash_b200/cashash.hpp keeps the reference's
+signatures).  This module exists so pytest and bench.py can drive the same C ABI; names follow
+the reference: FamilyParams / MatchConfig / build_hash_family / set_centering / compute_codes /
+build_bucket_index / match_pair / save_matches (hashing.hpp, matcher.hpp, feature_io.hpp).
+Errors map to the reference's exception classes:
+    CHGPU_EINVAL -> ValueError          (std::invalid_argument)
+    CHGPU_ELOGIC -> LogicError          (std::logic_error)
+    CHGPU_EFORMAT -> FeatureFileError   (fault class + byte offset)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+
+RECORD_DTYPE = np.dtype([("query_index", "<u4"), ("train_index", "<u4"), ("distance_sq", "<f8")])
+assert RECORD_DTYPE.itemsize == 16
+
+
+class LogicError(RuntimeError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class UnsupportedError(RuntimeError):
+    pass
+
+
+class FeatureFileError(RuntimeError):
+    FAULTS = {1: "MissingFile", 2: "BadMagic", 3: "BadVersion", 4: "Truncated", 5: "Unwritable"}
+
+    def __init__(self, msg: str, fault: int, byte_offset: int):
+        super().__init__(msg)
+        self.fault = self.FAULTS.get(fault, str(fault))
+        self.byte_offset = byte_offset
+
+
+@dataclass(frozen=True)
+class FamilyParams:  # hashing.hpp:45-52
+    short_bits: int = 8
+    long_bits: int = 128
+    table_count: int = 6
+    seed: int = 1
+
+    def c(self) -> N.FamilyParamsC:
+        return N.FamilyParamsC(self.short_bits, self.long_bits, self.table_count, self.seed)
+
+
+@dataclass(frozen=True)
+class MatchConfig:  # matcher.hpp:14-23
+    top_k: int = 10
+    hamming_threshold: int = 40
+    ratio: float = 0.8
+    min_candidates_for_ratio: int = 2
+    reduce_rounds: int = 3
+
+    def c(self) -> N.MatchCfgC:
+        return N.MatchCfgC(self.top_k, self.hamming_threshold, self.ratio, self.min_candidates_for_ratio,
+                           self.reduce_rounds)
+
+
+@dataclass
+class HashFamily:  # hashing.hpp:62-72
+    params: FamilyParams
+    short_planes: np.ndarray  # (L*m, 128) f64, [table*m + bit]
+    long_planes: np.ndarray   # (n, 128) f64
+    centering: np.ndarray | None = None
+
+
+@dataclass
+class ImageCodes:  # hashing.hpp:110-114
+    params: FamilyParams
+    shorts: np.ndarray  # (n, L) u32
+    longs: np.ndarray   # (n, 2) u64
+
+
+@dataclass
+class BucketIndex:  # dense view of matcher.hpp:30-41
+    short_bits: int
+    point_count: int
+    offsets: np.ndarray  # (L, 2^m + 1) u32
+    points: np.ndarray   # (L, n) u32
+
+    def bucket(self, table: int, code: int) -> np.ndarray:
+        return self.points[table, self.offsets[table, code]:self.offsets[table, code + 1]]
+
+
+def _raise(status: int, msg: str):
+    if status == N.EINVAL:
+        raise ValueError(msg)
+    if status == N.ELOGIC:
+        raise LogicError(msg)
+    if status == N.EUNSUPPORTED:
+        raise UnsupportedError(msg)
+    if status == N.ENOMEM:
+        raise MemoryError(msg)
+    if status == N.ENOTFOUND:
+        raise KeyError(msg)
+    raise CudaError(msg)
+
+
+def build_hash_family(params: FamilyParams = FamilyParams()) -> HashFamily:
+    """build_hash_family (hashing.hpp:74): host-side, bit-identical hyperplanes."""
+    lib = N.load()
+    p = params.c()
+    if not (1 <= params.short_bits <= 32 and params.short_bits < params.long_bits <= 128 and params.table_count >= 1):
+        raise ValueError("family parameters out of range")
+    sp = np.empty((params.table_count * params.short_bits, 128), dtype=np.float64)
+    lp = np.empty((params.long_bits, 128), dtype=np.float64)
+    st = lib.chgpu_family_generate(C.byref(p), sp.ctypes.data_as(N.f64p), lp.ctypes.data_as(N.f64p))
+    if st != N.OK:
+        _raise(st, "chgpu_family_generate failed")
+    return HashFamily(params, sp, lp)
+
+
+def save_matches(image_id_i: str, image_id_j: str, records: np.ndarray, path: str) -> None:
+    """save_matches (feature_io.hpp:106-107)."""
+    lib = N.load()
+    rec = np.ascontiguousarray(records, dtype=RECORD_DTYPE)
+    st = lib.chgpu_save_matches(image_id_i.encode(), image_id_j.encode(), rec.ctypes.data, len(rec), str(path).encode())
+    if st != N.OK:
+        raise FeatureFileError(f"{path}: unwritable path at byte 0", 5, 0)
+
+
+def pair_file_name(i: int, j: int) -> str:
+    buf = C.create_string_buffer(48)
+    N.load().chgpu_pair_file_name(i, j, buf)
+    return buf.value.decode()
+
+
+def plan_exhaustive(image_count: int, block_images: int, blocks_per_group: int) -> np.ndarray:
+    """Pair list of plan_exhaustive (scheduler.hpp:53), flattened in task order: (npairs, 2) u32."""
+    lib = N.load()
+    n = C.c_uint64(0)
+    pairs = np.empty((image_count * (image_count - 1) // 2, 2), dtype=np.uint32)
+    st = lib.chgpu_plan_exhaustive(image_count, block_images, blocks_per_group, pairs.ctypes.data, C.byref(n))
+    if st != N.OK:
+        _raise(st, "partition: image_count, block_images and blocks_per_group must be >= 1")
+    assert n.value == len(pairs)
+    return pairs
+
+
+def shard_range(npairs: int, rank: int, world: int) -> tuple[int, int]:
+    a, b = C.c_uint64(0), C.c_uint64(0)
+    N.load().chgpu_shard_range(npairs, rank, world, C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
+class Matcher:
+    """One device context (one per GPU / per process)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = N.load()
+        h = C.c_void_p()
+        st = self.lib.chgpu_create(device, C.byref(h))
+        if st != N.OK:
+            raise CudaError(f"chgpu_create(device={device}) failed: {self.lib.chgpu_status_name(st).decode()} "
+                            "(a CUDA sm_100 device is required; there is no CPU fallback)")
+        self.h = h
+        self.params: FamilyParams | None = None
+        self._sink_keepalive = None
+
+    # -- plumbing -------------------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.chgpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _ck(self, st: int):
+        if st != N.OK:
+            _raise(st, self.lib.chgpu_last_error(self.h).decode())
+
+    def sync(self):
+        self._ck(self.lib.chgpu_sync(self.h))
+
+    def device_props(self) -> dict:
+        p = N.DevicePropsC()
+        self._ck(self.lib.chgpu_get_device_props(self.h, C.byref(p)))
+        return {"name": p.name.decode(), "sm_count": p.sm_count, "cc": (p.cc_major, p.cc_minor),
+                "total_mem": p.total_mem, "free_mem": p.free_mem, "smem_per_block_optin": p.smem_per_block_optin}
+
+    def pinned_empty(self, shape, dtype) -> np.ndarray:
+        """numpy array over pinned host memory (zero-staging uploads)."""
+        dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dtype.itemsize
+        p = C.c_void_p()
+        self._ck(self.lib.chgpu_host_alloc(self.h, nbytes, C.byref(p)))
+        buf = (C.c_uint8 * max(nbytes, 1)).from_address(p.value)
+        arr = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+        return arr
+
+    # -- family ---------------------------------------------------------------------------------
+    def set_family(self, family: HashFamily):
+        p = family.params.c()
+        sp = np.ascontiguousarray(family.short_planes, dtype=np.float64)
+        lp = np.ascontiguousarray(family.long_planes, dtype=np.float64)
+        self._ck(self.lib.chgpu_set_family(self.h, C.byref(p), sp.ctypes.data_as(N.f64p), lp.ctypes.data_as(N.f64p)))
+        self.params = family.params
+        if family.centering is not None:
+            self.set_centering(family.centering)
+
+    def set_centering(self, centering: np.ndarray):
+        c = np.ascontiguousarray(centering, dtype=np.float64)
+        assert c.shape == (128,)
+        self._ck(self.lib.chgpu_set_centering(self.h, c.ctypes.data_as(N.f64p)))
+
+    def centering_reset(self):
+        self._ck(self.lib.chgpu_centering_reset(self.h))
+
+    def centering_add(self, image_id: int):
+        self._ck(self.lib.chgpu_centering_add_image(self.h, image_id))
+
+    def centering_sums(self) -> tuple[np.ndarray, int]:
+        sums = np.zeros(128, dtype=np.uint64)
+        cnt = C.c_uint64(0)
+        self._ck(self.lib.chgpu_centering_get_sums(self.h, sums.ctypes.data_as(N.u64p), C.byref(cnt)))
+        return sums, cnt.value
+
+    def centering_add_sums(self, sums: np.ndarray, count: int):
+        s = np.ascontiguousarray(sums, dtype=np.uint64)
+        self._ck(self.lib.chgpu_centering_add_sums(self.h, s.ctypes.data_as(N.u64p), count))
+
+    def centering_apply(self) -> np.ndarray:
+        out = np.empty(128, dtype=np.float64)
+        self._ck(self.lib.chgpu_centering_apply(self.h, out.ctypes.data_as(N.f64p)))
+        return out
+
+    # -- descriptor load ------------------------------------------------------------------------
+    def upload(self, image_id: int, desc: np.ndarray, keypoints: np.ndarray | None = None):
+        d = np.ascontiguousarray(desc, dtype=np.uint8)
+        n = 0 if d.size == 0 else d.shape[0]
+        assert d.size == n * 128
+        kp = None
+        if keypoints is not None:
+            kp = np.ascontiguousarray(keypoints, dtype=np.float32)
+            assert kp.size == n * 4
+        self._ck(self.lib.chgpu_upload_image(self.h, image_id, n, d.ctypes.data if n else None,
+                                             kp.ctypes.data if kp is not None and n else None))
+
+    def upload_chft(self, image_id: int, blob: bytes) -> int:
+        cnt = C.c_uint32(0)
+        fault = C.c_int(0)
+        off = C.c_uint64(0)
+        buf = np.frombuffer(blob, dtype=np.uint8)
+        st = self.lib.chgpu_upload_chft(self.h, image_id, buf.ctypes.data if buf.size else C.c_void_p(1), len(blob),
+                                        C.byref(cnt), C.byref(fault), C.byref(off))
+        if st == N.EFORMAT:
+            raise FeatureFileError(self.lib.chgpu_last_error(self.h).decode(), fault.value, off.value)
+        self._ck(st)
+        return cnt.value
+
+    def evict(self, image_id: int):
+        self._ck(self.lib.chgpu_evict_image(self.h, image_id))
+
+    def points(self, image_id: int) -> int:
+        n = C.c_uint32(0)
+        self._ck(self.lib.chgpu_image_points(self.h, image_id, C.byref(n)))
+        return n.value
+
+    def descriptors(self, image_id: int) -> tuple[np.ndarray, np.ndarray]:
+        n = self.points(image_id)
+        d = np.empty((n, 128), dtype=np.uint8)
+        kp = np.empty((n, 4), dtype=np.float32)
+        self._ck(self.lib.chgpu_download_descriptors(self.h, image_id, d.ctypes.data, kp.ctypes.data))
+        return d, kp
+
+    # -- hash build -----------------------------------------------------------------------------
+    def hash(self, image_ids, reduce_rounds: int = 3):
+        ids = np.ascontiguousarray(image_ids, dtype=np.uint32)
+        self._ck(self.lib.chgpu_hash_images(self.h, ids.ctypes.data_as(N.u32p), len(ids), reduce_rounds))
+
+    def codes(self, image_id: int) -> ImageCodes:
+        n = self.points(image_id)
+        shorts = np.empty((n, self.params.table_count), dtype=np.uint32)
+        longs = np.empty((n, 2), dtype=np.uint64)
+        self._ck(self.lib.chgpu_download_codes(self.h, image_id, shorts.ctypes.data, longs.ctypes.data))
+        return ImageCodes(self.params, shorts, longs)
+
+    def upload_codes(self, image_id: int, codes: ImageCodes):
+        s = np.ascontiguousarray(codes.shorts, dtype=np.uint32)
+        l = np.ascontiguousarray(codes.longs, dtype=np.uint64)
+        self._ck(self.lib.chgpu_upload_codes(self.h, image_id, s.ctypes.data, l.ctypes.data))
+
+    def bucket_index(self, image_id: int) -> BucketIndex:
+        n = self.points(image_id)
+        L, m = self.params.table_count, self.params.short_bits
+        offs = np.empty((L, (1 << m) + 1), dtype=np.uint32)
+        pts = np.empty((L, n), dtype=np.uint32)
+        self._ck(self.lib.chgpu_download_bucket_index(self.h, image_id, offs.ctypes.data, pts.ctypes.data))
+        return BucketIndex(m, n, offs, pts)
+
+    # -- match ----------------------------------------------------------------------------------
+    def match_pairs(self, pairs, cfg: MatchConfig = MatchConfig(), capacity: int | None = None):
+        """Returns (offsets (npairs+1) u64, records structured array, stats dict)."""
+        pr = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
+        npairs = len(pr)
+        if capacity is None:
+            capacity = int(sum(self.points(int(a)) for a in pr[:, 0])) if npairs <= 4096 else None
+        c = cfg.c()
+        stats = N.MatchStatsC()
+        offsets = np.zeros(npairs + 1, dtype=np.uint64)
+        total = C.c_uint64(0)
+        if capacity is None:  # size by a first device-only pass
+            self._ck(self.lib.chgpu_match_pairs_device(self.h, pr.ctypes.data, npairs, C.byref(c), C.byref(stats)))
+            capacity = int(stats.matches)
+        records = np.zeros(max(capacity, 1), dtype=RECORD_DTYPE)
+        st = self.lib.chgpu_match_pairs(self.h, pr.ctypes.data, npairs, C.byref(c), offsets.ctypes.data,
+                                        records.ctypes.data, capacity, C.byref(total), C.byref(stats))
+        self._ck(st)
+        return offsets, records[: total.value], stats.as_dict()
+
+    def match_pairs_device(self, pairs, cfg: MatchConfig = MatchConfig()) -> dict:
+        pr = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
+        c = cfg.c()
+        stats = N.MatchStatsC()
+        self._ck(self.lib.chgpu_match_pairs_device(self.h, pr.ctypes.data, len(pr), C.byref(c), C.byref(stats)))
+        return stats.as_dict()
+
+    def match_pairs_stream(self, pairs, cfg: MatchConfig, sink) -> dict:
+        """sink(first_pair, offsets ndarray (k+1), records ndarray) -> None; called in pair order."""
+        pr = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
+        c = cfg.c()
+        stats = N.MatchStatsC()
+        err: list[BaseException] = []
+
+        def _cb(_user, first, count, offs_p, rec_p):
+            try:
+                offs = np.ctypeslib.as_array(offs_p, shape=(count + 1,))
+                total = int(offs[count])
+                if total:
+                    rec = np.frombuffer((N.MatchRecordC * total).from_address(C.addressof(rec_p.contents)),
+                                        dtype=RECORD_DTYPE)
+                else:
+                    rec = np.zeros(0, dtype=RECORD_DTYPE)
+                if sink is not None:
+                    sink(int(first), offs, rec)
+                return 0
+            except BaseException as e:  # noqa: BLE001 - propagate through the C frame
+                err.append(e)
+                return 1
+
+        cb = N.SINK_FN(_cb)
+        st = self.lib.chgpu_match_pairs_stream(self.h, pr.ctypes.data, len(pr), C.byref(c), cb, None, C.byref(stats))
+        if err:
+            raise err[0]
+        self._ck(st)
+        return stats.as_dict()
+
+    def ranked(self, image_i: int, image_j: int, cfg: MatchConfig = MatchConfig()):
+        n = self.points(image_i)
+        ranked = np.zeros((n, cfg.top_k), dtype=np.uint32)
+        count = np.zeros(n, dtype=np.uint32)
+        c = cfg.c()
+        self._ck(self.lib.chgpu_debug_ranked(self.h, image_i, image_j, C.byref(c), ranked.ctypes.data, count.ctypes.data))
+        return ranked, count
+
+
+# ---- reference-shaped free functions over a default context ---------------------------------------
+_default: Matcher | None = None
+
+
+def default_matcher() -> Matcher:
+    global _default
+    if _default is None:
+        _default = Matcher(0)
+    return _default
+
+
+def set_centering(family: HashFamily, feature_sets) -> None:
+    """set_centering (hashing.hpp:78): exact integer column sums on the device, divide on the host."""
+    m = default_matcher()
+    _install(m, family)
+    m.centering_reset()
+    total = 0
+    for k, fs in enumerate(feature_sets):
+        d = np.asarray(fs, dtype=np.uint8).reshape(-1, 128)
+        total += len(d)
+        m.upload(0xC0000000 + k, d)
+        m.centering_add(0xC0000000 + k)
+        m.evict(0xC0000000 + k)
+    if total == 0:
+        raise ValueError("set_centering: no descriptors")
+    family.centering = m.centering_apply()
+
+
+def _install(m: Matcher, family: HashFamily):
+    if m.params != family.params or getattr(m, "_family_obj", None) is not family:
+        for img in list(getattr(m, "_tmp_ids", [])):
+            m.evict(img)
+        m._tmp_ids = []
+        m.set_family(family)
+        m._family_obj = family
+    elif family.centering is not None:
+        m.set_centering(family.centering)
+
+
+def compute_codes(family: HashFamily, desc: np.ndarray, reduce_rounds: int = 3) -> ImageCodes:
+    """compute_codes (hashing.hpp:131)."""
+    if not (0 <= reduce_rounds <= 7):
+        raise ValueError("reduce_dot tail rounds out of range 0..7")
+    if family.centering is None:
+        raise LogicError("compute_codes: centering has not been set")
+    m = default_matcher()
+    _install(m, family)
+    m.upload(0xD0000000, np.asarray(desc, dtype=np.uint8).reshape(-1, 128))
+    try:
+        m.hash([0xD0000000], reduce_rounds)
+        return m.codes(0xD0000000)
+    finally:
+        m.evict(0xD0000000)
+
+
+def match_pair(family: HashFamily, desc_i, desc_j, codes_i: ImageCodes, codes_j: ImageCodes,
+               cfg: MatchConfig = MatchConfig()) -> np.ndarray:
+    """match_pair (matcher.hpp:98-100) with externally supplied codes."""
+    if codes_i.params != codes_j.params:
+        raise ValueError("match_pair: codes come from different hash families")
+    di = np.asarray(desc_i, dtype=np.uint8).reshape(-1, 128)
+    dj = np.asarray(desc_j, dtype=np.uint8).reshape(-1, 128)
+    if len(di) != len(codes_i.shorts) or len(dj) != len(codes_j.shorts):
+        raise ValueError("match_pair: code/point count mismatch")
+    m = default_matcher()
+    _install(m, family)
+    a, b = 0xE0000000, 0xE0000001
+    m.upload(a, di)
+    m.upload(b, dj)
+    try:
+        m.upload_codes(a, codes_i)
+        m.upload_codes(b, codes_j)
+        _, rec, _ = m.match_pairs([(a, b)], cfg)
+        return rec.copy()
+    finally:
+        m.evict(a)
+        m.evict(b)

@@ -1,0 +1,1116 @@
+// chgpu.cu — context, memory management and the C ABI of libchgpu.so (see include/chgpu.h).
+//
+// Data layout in HBM: every resident image owns ONE arena block holding, 256-byte aligned,
+//   desc (n*128 B) | kp (n*16 B) | longs (n*16 B) | shorts (n*L*4 B) | offs (L*(2^m+1)*4 B) | points (L*n*2 B)
+// (1,466,648 B for n = 8192, m = 8, L = 6).  Blocks are bump-allocated from 256 MiB slabs and
+// recycled through an exact-size free list, so streaming a dataset through a bounded working
+// set never calls cudaMalloc in steady state.
+//
+// Streams: `copy` carries H2D uploads (pinned staging ring for pageable sources) and result
+// D2H; `compute` carries every kernel.  Events order the two; nothing here uses the legacy
+// default stream.
+
+#include "../../include/chgpu.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "dev_types.cuh"
+#include "hash_kernels.cuh"
+#include "match_kernels.cuh"
+
+using namespace chgpu;
+
+// host_util.cpp
+extern "C" int chgpu_host_check_family(const chgpu_family_params* p);
+
+namespace {
+
+constexpr size_t kAlign = 256;
+constexpr size_t kSlabBytes = size_t(256) << 20;
+constexpr size_t kStageBytes = size_t(32) << 20;
+constexpr int kStageSlots = 2;
+constexpr uint64_t kSubBatchQueries = uint64_t(16) << 20;  // per sub-batch: sum of Nq (res 128 MiB, records <= 256 MiB)
+
+size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a; }
+
+struct Arena {
+    struct Slab {
+        char* base;
+        size_t size, used;
+    };
+    std::vector<Slab> slabs;
+    std::map<size_t, std::vector<char*>> free_lists;
+    size_t live_bytes = 0;
+
+    cudaError_t alloc(size_t bytes, char** out) {
+        bytes = align_up(bytes);
+        auto it = free_lists.find(bytes);
+        if (it != free_lists.end() && !it->second.empty()) {
+            *out = it->second.back();
+            it->second.pop_back();
+            live_bytes += bytes;
+            return cudaSuccess;
+        }
+        for (Slab& s : slabs)
+            if (s.size - s.used >= bytes) {
+                *out = s.base + s.used;
+                s.used += bytes;
+                live_bytes += bytes;
+                return cudaSuccess;
+            }
+        Slab s{nullptr, std::max(kSlabBytes, bytes), 0};
+        const cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&s.base), s.size);
+        if (e != cudaSuccess) return e;
+        s.used = bytes;
+        *out = s.base;
+        slabs.push_back(s);
+        live_bytes += bytes;
+        return cudaSuccess;
+    }
+    void release(char* p, size_t bytes) {
+        bytes = align_up(bytes);
+        free_lists[bytes].push_back(p);
+        live_bytes -= bytes;
+    }
+    void destroy() {
+        for (Slab& s : slabs) cudaFree(s.base);
+        slabs.clear();
+        free_lists.clear();
+    }
+};
+
+struct ImageRec {
+    DevImage dev{};
+    char* block = nullptr;
+    size_t block_bytes = 0;
+    uint32_t image_id = 0;
+    bool used = false;
+};
+
+struct MatchBuffers {
+    PairDesc* h_pairs = nullptr;  // pinned
+    PairDesc* d_pairs = nullptr;
+    size_t pairs_cap = 0;
+    uint32_t* d_counts = nullptr;
+    unsigned long long* d_offsets = nullptr;
+    unsigned long long* h_offsets = nullptr;  // pinned
+    uint4* d_records = nullptr;
+    size_t records_cap = 0;  // entries
+    chgpu_match_record* h_records = nullptr;  // pinned
+    size_t h_records_cap = 0;
+    cudaEvent_t ev_done = nullptr, ev_k0 = nullptr, ev_k1 = nullptr;
+};
+
+}  // namespace
+
+struct chgpu_ctx {
+    int device = 0;
+    cudaDeviceProp prop{};
+    cudaStream_t compute = nullptr, copy = nullptr;
+    cudaEvent_t ev_upload = nullptr, ev_compute = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+    std::string err;
+
+    Arena arena;
+    std::vector<ImageRec> images;
+    std::vector<uint32_t> free_slots;
+    std::unordered_map<uint32_t, uint32_t> slot_of;
+    DevImage* d_images = nullptr;
+    DevImage* h_images = nullptr;  // pinned mirror
+    size_t images_cap = 0;
+
+    // staging ring for pageable uploads
+    char* stage[kStageSlots] = {nullptr, nullptr};
+    cudaEvent_t stage_ev[kStageSlots] = {nullptr, nullptr};
+    int stage_next = 0;
+
+    // family
+    bool has_family = false, has_centering = false;
+    chgpu_family_params fam{};
+    double* d_planes = nullptr;
+    double* d_centering = nullptr;
+    unsigned long long* d_sums = nullptr;
+    uint64_t sum_count = 0;
+    uint64_t extra_sums[128] = {0};  // sums merged from other ranks
+
+    // match workspace
+    uint2* d_res = nullptr;
+    size_t res_cap = 0;
+    MatchBuffers mb[2];
+    DevStats* d_stats = nullptr;
+    DevStats* h_stats = nullptr;  // pinned
+    unsigned int* d_counter = nullptr;
+    uint32_t* d_slots = nullptr;  // scratch list of slots for hash launches
+    size_t slots_cap = 0;
+    uint32_t* d_dbg = nullptr;
+    size_t dbg_cap = 0;
+};
+
+namespace {
+
+chgpu_status fail(chgpu_ctx* ctx, chgpu_status s, const char* fmt, ...) {
+    if (ctx) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof(buf), fmt, ap);
+        va_end(ap);
+        ctx->err = buf;
+    }
+    return s;
+}
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        const cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? CHGPU_ENOMEM : CHGPU_ECUDA,         \
+                        "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+struct DeviceGuard {
+    explicit DeviceGuard(int dev) { cudaSetDevice(dev); }
+};
+
+size_t image_block_bytes(uint32_t n, uint32_t m, uint32_t L, size_t off[6]) {
+    size_t o = 0;
+    off[0] = o; o += align_up(size_t(n) * kDim);
+    off[1] = o; o += align_up(size_t(n) * 16);
+    off[2] = o; o += align_up(size_t(n) * 16);
+    off[3] = o; o += align_up(size_t(n) * L * 4);
+    off[4] = o; o += align_up(size_t(L) * ((size_t(1) << m) + 1) * 4);
+    off[5] = o; o += align_up(size_t(L) * n * 2);
+    return std::max(o, kAlign);
+}
+
+chgpu_status ensure_images_cap(chgpu_ctx* ctx, size_t need) {
+    if (need <= ctx->images_cap) return CHGPU_OK;
+    size_t cap = std::max<size_t>(ctx->images_cap * 2, 1 << 16);
+    while (cap < need) cap *= 2;
+    CK(cudaStreamSynchronize(ctx->copy));
+    CK(cudaStreamSynchronize(ctx->compute));
+    DevImage *nd = nullptr, *nh = nullptr;
+    CK(cudaMalloc(&nd, cap * sizeof(DevImage)));
+    CK(cudaMallocHost(&nh, cap * sizeof(DevImage)));
+    memset(nh, 0, cap * sizeof(DevImage));
+    if (ctx->images_cap) {
+        memcpy(nh, ctx->h_images, ctx->images_cap * sizeof(DevImage));
+        CK(cudaMemcpy(nd, ctx->d_images, ctx->images_cap * sizeof(DevImage), cudaMemcpyDeviceToDevice));
+        cudaFree(ctx->d_images);
+        cudaFreeHost(ctx->h_images);
+    }
+    ctx->d_images = nd;
+    ctx->h_images = nh;
+    ctx->images_cap = cap;
+    return CHGPU_OK;
+}
+
+// Pushes images[slot].dev to the device table through the pinned mirror (copy stream).
+chgpu_status publish_slot(chgpu_ctx* ctx, uint32_t slot) {
+    ctx->h_images[slot] = ctx->images[slot].dev;
+    CK(cudaMemcpyAsync(ctx->d_images + slot, ctx->h_images + slot, sizeof(DevImage), cudaMemcpyHostToDevice,
+                       ctx->copy));
+    return CHGPU_OK;
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// H2D on the copy stream.  Pageable sources go through the pinned staging ring so the copy
+// engine overlaps the host memcpy of the next chunk; pinned sources are copied in place and
+// the stream is drained before returning (the caller may reuse the buffer immediately).
+chgpu_status h2d(chgpu_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return CHGPU_OK;
+    if (is_pinned(src)) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->copy));
+        CK(cudaStreamSynchronize(ctx->copy));
+        return CHGPU_OK;
+    }
+    size_t done = 0;
+    while (done < bytes) {
+        const size_t chunk = std::min(kStageBytes, bytes - done);
+        const int s = ctx->stage_next;
+        ctx->stage_next = (s + 1) % kStageSlots;
+        CK(cudaEventSynchronize(ctx->stage_ev[s]));
+        memcpy(ctx->stage[s], static_cast<const char*>(src) + done, chunk);
+        CK(cudaMemcpyAsync(static_cast<char*>(dst) + done, ctx->stage[s], chunk, cudaMemcpyHostToDevice, ctx->copy));
+        CK(cudaEventRecord(ctx->stage_ev[s], ctx->copy));
+        done += chunk;
+    }
+    return CHGPU_OK;
+}
+
+chgpu_status find_slot(chgpu_ctx* ctx, uint32_t image_id, uint32_t* slot) {
+    const auto it = ctx->slot_of.find(image_id);
+    if (it == ctx->slot_of.end()) return fail(ctx, CHGPU_ENOTFOUND, "image %u is not resident", image_id);
+    *slot = it->second;
+    return CHGPU_OK;
+}
+
+// copy stream waits for compute (WAR on recycled blocks), compute waits for uploads (RAW).
+chgpu_status order_copy_after_compute(chgpu_ctx* ctx) {
+    CK(cudaEventRecord(ctx->ev_compute, ctx->compute));
+    CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_compute, 0));
+    return CHGPU_OK;
+}
+chgpu_status order_compute_after_copy(chgpu_ctx* ctx) {
+    CK(cudaEventRecord(ctx->ev_upload, ctx->copy));
+    CK(cudaStreamWaitEvent(ctx->compute, ctx->ev_upload, 0));
+    return CHGPU_OK;
+}
+
+chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t* slot_out) {
+    if (!ctx->has_family)
+        return fail(ctx, CHGPU_ELOGIC, "chgpu_set_family must precede image uploads (block layout depends on m, L)");
+    if (n > kMaxPoints) return fail(ctx, CHGPU_EUNSUPPORTED, "image %u has %u points; device path holds <= %u", image_id, n, kMaxPoints);
+    const auto it = ctx->slot_of.find(image_id);
+    if (it != ctx->slot_of.end()) {
+        // replacing: drain both streams so no kernel or copy still reads the old block
+        CK(cudaStreamSynchronize(ctx->copy));
+        CK(cudaStreamSynchronize(ctx->compute));
+        ImageRec& old = ctx->images[it->second];
+        ctx->arena.release(old.block, old.block_bytes);
+        old.used = false;
+        ctx->free_slots.push_back(it->second);
+        ctx->slot_of.erase(it);
+    }
+    uint32_t slot;
+    if (!ctx->free_slots.empty()) {
+        slot = ctx->free_slots.back();
+        ctx->free_slots.pop_back();
+    } else {
+        slot = static_cast<uint32_t>(ctx->images.size());
+        ctx->images.emplace_back();
+    }
+    if (const chgpu_status s = ensure_images_cap(ctx, size_t(slot) + 1)) return s;
+    size_t off[6];
+    const size_t bytes = image_block_bytes(n, ctx->fam.short_bits, ctx->fam.table_count, off);
+    char* block = nullptr;
+    const cudaError_t e = ctx->arena.alloc(bytes, &block);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        ctx->free_slots.push_back(slot);
+        return fail(ctx, CHGPU_ENOMEM, "arena allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+    }
+    ImageRec& r = ctx->images[slot];
+    r.block = block;
+    r.block_bytes = bytes;
+    r.image_id = image_id;
+    r.used = true;
+    r.dev.desc = reinterpret_cast<const uint8_t*>(block + off[0]);
+    r.dev.kp = reinterpret_cast<const float4*>(block + off[1]);
+    r.dev.longs = reinterpret_cast<uint4*>(block + off[2]);
+    r.dev.shorts = reinterpret_cast<uint32_t*>(block + off[3]);
+    r.dev.offs = reinterpret_cast<uint32_t*>(block + off[4]);
+    r.dev.points = reinterpret_cast<uint16_t*>(block + off[5]);
+    r.dev.n = n;
+    r.dev.flags = 0;
+    ctx->slot_of[image_id] = slot;
+    *slot_out = slot;
+    return CHGPU_OK;
+}
+
+chgpu_status ensure_slots_scratch(chgpu_ctx* ctx, size_t count) {
+    if (count <= ctx->slots_cap) return CHGPU_OK;
+    CK(cudaStreamSynchronize(ctx->compute));
+    CK(cudaStreamSynchronize(ctx->copy));
+    if (ctx->d_slots) cudaFree(ctx->d_slots);
+    ctx->slots_cap = std::max<size_t>(count, 4096);
+    CK(cudaMalloc(&ctx->d_slots, ctx->slots_cap * sizeof(uint32_t)));
+    return CHGPU_OK;
+}
+
+chgpu_status launch_bucket_build(chgpu_ctx* ctx, uint32_t count) {
+    const uint32_t m = ctx->fam.short_bits, L = ctx->fam.table_count;
+    const size_t smem = size_t(L) << m << 2;
+    CK(cudaFuncSetAttribute(bucket_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    bucket_build_kernel<<<count, L * 32, smem, ctx->compute>>>(ctx->d_images, ctx->d_slots, m, L);
+    CK(cudaGetLastError());
+    return CHGPU_OK;
+}
+
+template <int RR>
+cudaError_t launch_hash_rr(chgpu_ctx* ctx, dim3 grid) {
+    const size_t smem = hash_smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(hash_codes_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    hash_codes_kernel<RR><<<grid, kHashThreads, smem, ctx->compute>>>(
+        ctx->d_images, ctx->d_slots, ctx->d_planes, ctx->d_centering, ctx->fam.short_bits, ctx->fam.table_count,
+        ctx->fam.long_bits);
+    return cudaGetLastError();
+}
+
+bool cfg_valid(const chgpu_match_cfg& c, uint32_t long_bits, const char** why) {
+    // validate(MatchConfig), matcher.cpp:9-17
+    if (c.top_k < 2) { *why = "top_k must be >= 2 for the ratio test"; return false; }
+    if (c.hamming_threshold > long_bits) { *why = "hamming_threshold exceeds long code length"; return false; }
+    if (!(c.ratio > 0.0 && c.ratio < 1.0)) { *why = "ratio must be in (0, 1)"; return false; }
+    if (c.reduce_rounds < 0 || c.reduce_rounds > 7) { *why = "reduce_rounds out of range 0..7"; return false; }
+    return true;
+}
+
+template <bool SMEM, int LT>
+cudaError_t launch_match_variant(chgpu_ctx* ctx, const MatchParams& P, size_t smem, uint32_t* grid_out) {
+    auto kfn = match_kernel<SMEM, LT>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kMatchThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+    const uint32_t grid = std::min<uint32_t>(P.nunits, uint32_t(per_sm) * ctx->prop.multiProcessorCount);
+    *grid_out = grid;
+    kfn<<<grid, kMatchThreads, smem, ctx->compute>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_match(chgpu_ctx* ctx, const MatchParams& P, bool smem_train, uint32_t max_nt, uint32_t* grid) {
+    const size_t smem = smem_train ? std::max<size_t>(size_t(max_nt) * 16, 16) : 16;
+    const uint32_t L = P.L;
+    if (smem_train) {
+        if (L <= 4) return launch_match_variant<true, 4>(ctx, P, smem, grid);
+        if (L <= 6) return launch_match_variant<true, 6>(ctx, P, smem, grid);
+        return launch_match_variant<true, 8>(ctx, P, smem, grid);
+    }
+    if (L <= 4) return launch_match_variant<false, 4>(ctx, P, smem, grid);
+    if (L <= 6) return launch_match_variant<false, 6>(ctx, P, smem, grid);
+    return launch_match_variant<false, 8>(ctx, P, smem, grid);
+}
+
+size_t smem_train_capacity(const chgpu_ctx* ctx) {
+    // dynamic smem available to a 1-CTA/SM launch, minus the kernel's static 16 B and 1 KiB reserve
+    return (ctx->prop.sharedMemPerBlockOptin - 1024 - 64) / 16;
+}
+
+enum class SinkMode { Host, Stream, Device };
+
+struct SubBatch {
+    uint32_t first, count;
+    uint64_t queries;
+    uint32_t max_nt, max_nq;
+};
+
+chgpu_status ensure_match_buffers(chgpu_ctx* ctx, MatchBuffers& b, const SubBatch& sb, bool host_side) {
+    if (b.pairs_cap < sb.count) {
+        CK(cudaStreamSynchronize(ctx->compute));
+        CK(cudaStreamSynchronize(ctx->copy));
+        if (b.d_pairs) { cudaFree(b.d_pairs); cudaFreeHost(b.h_pairs); cudaFree(b.d_counts); cudaFree(b.d_offsets); cudaFreeHost(b.h_offsets); }
+        const size_t cap = std::max<size_t>(sb.count, 4096);
+        CK(cudaMalloc(&b.d_pairs, cap * sizeof(PairDesc)));
+        CK(cudaMallocHost(&b.h_pairs, cap * sizeof(PairDesc)));
+        CK(cudaMalloc(&b.d_counts, cap * sizeof(uint32_t)));
+        CK(cudaMalloc(&b.d_offsets, (cap + 1) * sizeof(unsigned long long)));
+        CK(cudaMallocHost(&b.h_offsets, (cap + 1) * sizeof(unsigned long long)));
+        b.pairs_cap = cap;
+    }
+    if (b.records_cap < sb.queries) {
+        CK(cudaStreamSynchronize(ctx->compute));
+        CK(cudaStreamSynchronize(ctx->copy));
+        if (b.d_records) cudaFree(b.d_records);
+        const size_t cap = std::max<size_t>(sb.queries, 1 << 20);
+        CK(cudaMalloc(&b.d_records, cap * sizeof(uint4)));
+        b.records_cap = cap;
+    }
+    if (!b.ev_done) {
+        CK(cudaEventCreateWithFlags(&b.ev_done, cudaEventDisableTiming));
+        CK(cudaEventCreate(&b.ev_k0));
+        CK(cudaEventCreate(&b.ev_k1));
+    }
+    (void)host_side;
+    return CHGPU_OK;
+}
+
+chgpu_status ensure_host_records(chgpu_ctx* ctx, MatchBuffers& b, size_t need) {
+    if (need <= b.h_records_cap) return CHGPU_OK;
+    if (b.h_records) cudaFreeHost(b.h_records);
+    size_t cap = std::max<size_t>(b.h_records_cap * 2, size_t(4) << 20);
+    while (cap < need) cap *= 2;
+    b.h_records = nullptr;
+    b.h_records_cap = 0;
+    CK(cudaMallocHost(&b.h_records, cap * sizeof(chgpu_match_record)));
+    b.h_records_cap = cap;
+    return CHGPU_OK;
+}
+
+struct MatchRun {
+    const uint32_t* pairs;
+    uint32_t npairs;
+    chgpu_match_cfg cfg;
+    SinkMode mode;
+    // Host mode
+    uint64_t* offsets = nullptr;
+    chgpu_match_record* records = nullptr;
+    uint64_t capacity = 0;
+    uint64_t total = 0;
+    bool overflow = false;
+    // Stream mode
+    chgpu_sink_fn sink = nullptr;
+    void* user = nullptr;
+    // debug
+    uint32_t* dbg_ranked = nullptr;
+    uint32_t* dbg_count = nullptr;
+};
+
+chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_out) {
+    DeviceGuard guard(ctx->device);
+    if (!ctx->has_family) return fail(ctx, CHGPU_ELOGIC, "no hash family installed");
+    const char* why = nullptr;
+    if (!cfg_valid(run.cfg, ctx->fam.long_bits, &why)) return fail(ctx, CHGPU_EINVAL, "%s", why);
+    if (run.cfg.top_k > uint32_t(kMaxTopK))
+        return fail(ctx, CHGPU_EUNSUPPORTED, "top_k %u > %d is outside the device envelope", run.cfg.top_k, kMaxTopK);
+    const uint32_t npairs = run.npairs;
+    chgpu_match_stats st{};
+    st.pairs = npairs;
+    if (run.mode == SinkMode::Host && run.offsets) run.offsets[0] = 0;
+    if (npairs == 0) {
+        if (stats_out) *stats_out = st;
+        return CHGPU_OK;
+    }
+
+    // ---- resolve pairs, cut sub-batches ---------------------------------------------------
+    std::vector<PairDesc> descs(npairs);
+    std::vector<SubBatch> subs;
+    {
+        SubBatch cur{0, 0, 0, 0, 0};
+        for (uint32_t k = 0; k < npairs; ++k) {
+            uint32_t si, sj;
+            if (const chgpu_status s = find_slot(ctx, run.pairs[2 * k], &si)) return s;
+            if (const chgpu_status s = find_slot(ctx, run.pairs[2 * k + 1], &sj)) return s;
+            const DevImage& I = ctx->images[si].dev;
+            const DevImage& J = ctx->images[sj].dev;
+            if (!(I.flags & 1u) || !(J.flags & 1u))
+                return fail(ctx, CHGPU_ELOGIC, "pair (%u,%u): codes not computed (call chgpu_hash_images first)",
+                            run.pairs[2 * k], run.pairs[2 * k + 1]);
+            if (cur.count && (cur.queries + I.n > kSubBatchQueries || cur.count >= (1u << 20))) {
+                subs.push_back(cur);
+                cur = SubBatch{k, 0, 0, 0, 0};
+            }
+            descs[k] = PairDesc{si, sj, cur.queries};
+            cur.count += 1;
+            cur.queries += I.n;
+            cur.max_nt = std::max(cur.max_nt, J.n);
+            cur.max_nq = std::max(cur.max_nq, I.n);
+            st.query_points += I.n;
+            st.train_points += J.n;
+        }
+        subs.push_back(cur);
+    }
+    uint64_t max_queries = 0;
+    for (const SubBatch& sb : subs) max_queries = std::max(max_queries, sb.queries);
+    if (ctx->res_cap < max_queries) {
+        CK(cudaStreamSynchronize(ctx->compute));
+        if (ctx->d_res) cudaFree(ctx->d_res);
+        ctx->res_cap = std::max<size_t>(max_queries, 1 << 20);
+        CK(cudaMalloc(&ctx->d_res, ctx->res_cap * sizeof(uint2)));
+    }
+    if (run.dbg_ranked) {
+        const size_t need = size_t(subs[0].max_nq) * (run.cfg.top_k + 1);
+        if (ctx->dbg_cap < need) {
+            if (ctx->d_dbg) cudaFree(ctx->d_dbg);
+            CK(cudaMalloc(&ctx->d_dbg, need * sizeof(uint32_t)));
+            ctx->dbg_cap = need;
+        }
+        CK(cudaMemsetAsync(ctx->d_dbg, 0, need * sizeof(uint32_t), ctx->compute));
+    }
+
+    if (const chgpu_status s = order_compute_after_copy(ctx)) return s;
+    CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(DevStats), ctx->compute));
+    CK(cudaEventRecord(ctx->ev_t0, ctx->compute));
+
+    const size_t cap_nt = smem_train_capacity(ctx);
+    const bool host_side = run.mode != SinkMode::Device;
+    float match_ms = 0.f;
+    uint64_t delivered_records = 0;
+
+    // finishes sub-batch s (already launched into mb[s & 1]): D2H + delivery
+    auto finish = [&](size_t s) -> chgpu_status {
+        MatchBuffers& b = ctx->mb[s & 1];
+        const SubBatch& sb = subs[s];
+        CK(cudaEventSynchronize(b.ev_done));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, b.ev_k0, b.ev_k1));
+        match_ms += ms;
+        if (!host_side) return CHGPU_OK;
+        CK(cudaMemcpyAsync(b.h_offsets, b.d_offsets, (size_t(sb.count) + 1) * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, ctx->copy));
+        CK(cudaStreamSynchronize(ctx->copy));
+        const uint64_t total = b.h_offsets[sb.count];
+        if (run.mode == SinkMode::Host) {
+            for (uint32_t k = 0; k < sb.count; ++k) run.offsets[sb.first + k + 1] = delivered_records + b.h_offsets[k + 1];
+            if (delivered_records + total > run.capacity) {
+                run.overflow = true;
+            } else if (total) {
+                CK(cudaMemcpyAsync(run.records + delivered_records, b.d_records, total * sizeof(uint4),
+                                   cudaMemcpyDeviceToHost, ctx->copy));
+                CK(cudaStreamSynchronize(ctx->copy));
+            }
+        } else {
+            if (const chgpu_status e = ensure_host_records(ctx, b, std::max<uint64_t>(total, 1))) return e;
+            if (total) {
+                CK(cudaMemcpyAsync(b.h_records, b.d_records, total * sizeof(uint4), cudaMemcpyDeviceToHost, ctx->copy));
+                CK(cudaStreamSynchronize(ctx->copy));
+            }
+            if (run.sink) {
+                static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "offset width");
+                if (run.sink(run.user, sb.first, sb.count, reinterpret_cast<const uint64_t*>(b.h_offsets), b.h_records) != 0)
+                    return fail(ctx, CHGPU_EINVAL, "sink aborted at pair %u", sb.first);
+            }
+        }
+        delivered_records += total;
+        return CHGPU_OK;
+    };
+
+    for (size_t s = 0; s < subs.size(); ++s) {
+        const SubBatch& sb = subs[s];
+        MatchBuffers& b = ctx->mb[s & 1];
+        if (const chgpu_status e = ensure_match_buffers(ctx, b, sb, host_side)) return e;
+        memcpy(b.h_pairs, descs.data() + sb.first, size_t(sb.count) * sizeof(PairDesc));
+        CK(cudaMemcpyAsync(b.d_pairs, b.h_pairs, size_t(sb.count) * sizeof(PairDesc), cudaMemcpyHostToDevice, ctx->compute));
+        CK(cudaMemsetAsync(b.d_counts, 0, size_t(sb.count) * sizeof(uint32_t), ctx->compute));
+        CK(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), ctx->compute));
+
+        const bool smem_train = sb.max_nt <= cap_nt;
+        // enough units to balance the persistent grid: >= 4 per CTA, chunks of >= 256 queries
+        const uint32_t ctas = uint32_t(ctx->prop.multiProcessorCount) * (smem_train && sb.max_nt * 16u > 100000u ? 1u : 2u);
+        uint32_t chunks = 1;
+        if (sb.count < 4 * ctas) chunks = std::min<uint32_t>((4 * ctas + sb.count - 1) / sb.count, std::max<uint32_t>(1, sb.max_nq / 256));
+
+        MatchParams P{};
+        P.images = ctx->d_images;
+        P.pairs = b.d_pairs;
+        P.res = ctx->d_res;
+        P.pair_counts = b.d_counts;
+        P.stats = ctx->d_stats;
+        P.unit_counter = ctx->d_counter;
+        P.nunits = sb.count * chunks;
+        P.chunks_per_pair = chunks;
+        P.m = ctx->fam.short_bits;
+        P.L = ctx->fam.table_count;
+        P.top_k = run.cfg.top_k;
+        P.tau = run.cfg.hamming_threshold;
+        P.min_ranked = std::max<uint32_t>(2, run.cfg.min_candidates_for_ratio);
+        P.long_bits = ctx->fam.long_bits;
+        P.ratio_sq = run.cfg.ratio * run.cfg.ratio;
+        if (run.dbg_ranked) {
+            P.dbg_ranked = ctx->d_dbg;
+            P.dbg_count = ctx->d_dbg + size_t(sb.max_nq) * run.cfg.top_k;
+        }
+        CK(cudaEventRecord(b.ev_k0, ctx->compute));
+        uint32_t grid = 0;
+        CK(launch_match(ctx, P, smem_train, sb.max_nt, &grid));
+        CK(cudaEventRecord(b.ev_k1, ctx->compute));
+        scan_counts_kernel<<<1, 1024, 0, ctx->compute>>>(b.d_counts, sb.count, b.d_offsets, ctx->d_stats);
+        CK(cudaGetLastError());
+        compact_kernel<<<sb.count, 256, 0, ctx->compute>>>(b.d_pairs, ctx->d_images, ctx->d_res, b.d_offsets,
+                                                            b.d_records, sb.first, ctx->d_stats);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(b.ev_done, ctx->compute));
+        st.match_launches += 1;
+        st.total_launches += 3;
+        // the result scratch d_res is shared: the next match kernel must not start before this
+        // sub-batch's compaction, which stream order on `compute` already guarantees.
+        if (s >= 1)
+            if (const chgpu_status e = finish(s - 1)) return e;
+    }
+    if (const chgpu_status e = finish(subs.size() - 1)) return e;
+
+    CK(cudaEventRecord(ctx->ev_t1, ctx->compute));
+    CK(cudaMemcpyAsync(ctx->h_stats, ctx->d_stats, sizeof(DevStats), cudaMemcpyDeviceToHost, ctx->compute));
+    if (run.dbg_ranked) {
+        const uint32_t nq = subs[0].max_nq;
+        CK(cudaMemcpyAsync(run.dbg_ranked, ctx->d_dbg, size_t(nq) * run.cfg.top_k * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->compute));
+        CK(cudaMemcpyAsync(run.dbg_count, ctx->d_dbg + size_t(nq) * run.cfg.top_k, size_t(nq) * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->compute));
+    }
+    CK(cudaStreamSynchronize(ctx->compute));
+    float total_ms = 0.f;
+    CK(cudaEventElapsedTime(&total_ms, ctx->ev_t0, ctx->ev_t1));
+    st.matches = ctx->h_stats->matches;
+    st.raw_candidates = ctx->h_stats->raw_candidates;
+    st.verified_queries = ctx->h_stats->verified_queries;
+    st.distances = ctx->h_stats->distances;
+    st.records_checksum = ctx->h_stats->checksum;
+    st.match_kernel_ms = match_ms;
+    st.total_ms = total_ms;
+    run.total = host_side ? delivered_records : st.matches;
+    if (stats_out) *stats_out = st;
+    return CHGPU_OK;
+}
+
+}  // namespace
+
+// =================================================================================================
+extern "C" {
+
+const char* chgpu_status_name(chgpu_status s) {
+    switch (s) {
+        case CHGPU_OK: return "ok";
+        case CHGPU_EINVAL: return "invalid argument";
+        case CHGPU_ELOGIC: return "logic error";
+        case CHGPU_ECUDA: return "cuda error";
+        case CHGPU_ENOMEM: return "out of memory";
+        case CHGPU_EUNSUPPORTED: return "unsupported";
+        case CHGPU_EFORMAT: return "format error";
+        case CHGPU_ENOTFOUND: return "not found";
+    }
+    return "?";
+}
+
+chgpu_status chgpu_create(int device, chgpu_ctx** out) {
+    if (!out) return CHGPU_EINVAL;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0 || device < 0 || device >= count) {
+        cudaGetLastError();
+        return CHGPU_ECUDA;  // no CPU fallback by design
+    }
+    chgpu_ctx* ctx = new chgpu_ctx();
+    ctx->device = device;
+    auto bail = [&](chgpu_status s) {
+        chgpu_destroy(ctx);
+        return s;
+    };
+    if (cudaSetDevice(device) != cudaSuccess) return bail(CHGPU_ECUDA);
+    if (cudaGetDeviceProperties(&ctx->prop, device) != cudaSuccess) return bail(CHGPU_ECUDA);
+    if (ctx->prop.major < 10) {
+        fprintf(stderr, "chgpu: device %d is sm_%d%d; this library is built for sm_100a only\n", device,
+                ctx->prop.major, ctx->prop.minor);
+        return bail(CHGPU_EUNSUPPORTED);
+    }
+    bool ok = true;
+    ok &= cudaStreamCreateWithFlags(&ctx->compute, cudaStreamNonBlocking) == cudaSuccess;
+    ok &= cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) == cudaSuccess;
+    ok &= cudaEventCreateWithFlags(&ctx->ev_upload, cudaEventDisableTiming) == cudaSuccess;
+    ok &= cudaEventCreateWithFlags(&ctx->ev_compute, cudaEventDisableTiming) == cudaSuccess;
+    ok &= cudaEventCreate(&ctx->ev_t0) == cudaSuccess;
+    ok &= cudaEventCreate(&ctx->ev_t1) == cudaSuccess;
+    for (int s = 0; s < kStageSlots && ok; ++s) {
+        ok &= cudaMallocHost(reinterpret_cast<void**>(&ctx->stage[s]), kStageBytes) == cudaSuccess;
+        ok &= cudaEventCreateWithFlags(&ctx->stage_ev[s], cudaEventDisableTiming) == cudaSuccess;
+    }
+    ok &= cudaMalloc(&ctx->d_centering, 128 * sizeof(double)) == cudaSuccess;
+    ok &= cudaMalloc(&ctx->d_sums, 128 * sizeof(unsigned long long)) == cudaSuccess;
+    ok &= cudaMemset(ctx->d_sums, 0, 128 * sizeof(unsigned long long)) == cudaSuccess;
+    ok &= cudaMalloc(&ctx->d_stats, sizeof(DevStats)) == cudaSuccess;
+    ok &= cudaMallocHost(reinterpret_cast<void**>(&ctx->h_stats), sizeof(DevStats)) == cudaSuccess;
+    ok &= cudaMalloc(&ctx->d_counter, sizeof(unsigned int)) == cudaSuccess;
+    if (!ok) return bail(CHGPU_ECUDA);
+    *out = ctx;
+    return CHGPU_OK;
+}
+
+void chgpu_destroy(chgpu_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    ctx->arena.destroy();
+    for (MatchBuffers& b : ctx->mb) {
+        cudaFree(b.d_pairs); cudaFreeHost(b.h_pairs); cudaFree(b.d_counts); cudaFree(b.d_offsets);
+        cudaFreeHost(b.h_offsets); cudaFree(b.d_records); cudaFreeHost(b.h_records);
+        if (b.ev_done) cudaEventDestroy(b.ev_done);
+        if (b.ev_k0) cudaEventDestroy(b.ev_k0);
+        if (b.ev_k1) cudaEventDestroy(b.ev_k1);
+    }
+    cudaFree(ctx->d_images); cudaFreeHost(ctx->h_images);
+    for (int s = 0; s < kStageSlots; ++s) {
+        cudaFreeHost(ctx->stage[s]);
+        if (ctx->stage_ev[s]) cudaEventDestroy(ctx->stage_ev[s]);
+    }
+    cudaFree(ctx->d_planes); cudaFree(ctx->d_centering); cudaFree(ctx->d_sums); cudaFree(ctx->d_res);
+    cudaFree(ctx->d_stats); cudaFreeHost(ctx->h_stats); cudaFree(ctx->d_counter); cudaFree(ctx->d_slots);
+    cudaFree(ctx->d_dbg);
+    if (ctx->ev_upload) cudaEventDestroy(ctx->ev_upload);
+    if (ctx->ev_compute) cudaEventDestroy(ctx->ev_compute);
+    if (ctx->ev_t0) cudaEventDestroy(ctx->ev_t0);
+    if (ctx->ev_t1) cudaEventDestroy(ctx->ev_t1);
+    if (ctx->compute) cudaStreamDestroy(ctx->compute);
+    if (ctx->copy) cudaStreamDestroy(ctx->copy);
+    cudaGetLastError();
+    delete ctx;
+}
+
+const char* chgpu_last_error(const chgpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+chgpu_status chgpu_get_device_props(chgpu_ctx* ctx, chgpu_device_props* out) {
+    if (!ctx || !out) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    memset(out, 0, sizeof(*out));
+    snprintf(out->name, sizeof(out->name), "%s", ctx->prop.name);
+    out->sm_count = ctx->prop.multiProcessorCount;
+    out->cc_major = ctx->prop.major;
+    out->cc_minor = ctx->prop.minor;
+    out->smem_per_block_optin = ctx->prop.sharedMemPerBlockOptin;
+    CK(cudaMemGetInfo(&out->free_mem, &out->total_mem));
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_sync(chgpu_ctx* ctx) {
+    if (!ctx) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    CK(cudaStreamSynchronize(ctx->copy));
+    CK(cudaStreamSynchronize(ctx->compute));
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_host_alloc(chgpu_ctx* ctx, size_t bytes, void** out) {
+    if (!ctx || !out) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    CK(cudaMallocHost(out, std::max<size_t>(bytes, 1)));
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_host_free(chgpu_ctx* ctx, void* p) {
+    if (!ctx) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    CK(cudaFreeHost(p));
+    return CHGPU_OK;
+}
+
+// ---- family -------------------------------------------------------------------------------------
+chgpu_status chgpu_set_family(chgpu_ctx* ctx, const chgpu_family_params* p, const double* short_planes,
+                              const double* long_planes) {
+    if (!ctx || !p || !short_planes || !long_planes) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    if (chgpu_host_check_family(p) != 0)
+        return fail(ctx, CHGPU_EINVAL, "family parameters violate 1<=m<=32, m<n<=128, L>=1 (hashing.cpp:30-36)");
+    if (p->short_bits > uint32_t(kMaxShortBits) || p->table_count > uint32_t(kMaxTables))
+        return fail(ctx, CHGPU_EUNSUPPORTED, "device envelope is m <= %d, L <= %d (got m=%u, L=%u)", kMaxShortBits,
+                    kMaxTables, p->short_bits, p->table_count);
+    if (!ctx->slot_of.empty())
+        return fail(ctx, CHGPU_ELOGIC, "evict all images before installing a different family");
+    CK(cudaStreamSynchronize(ctx->compute));
+    const size_t ns = size_t(p->table_count) * p->short_bits, nl = p->long_bits;
+    if (ctx->d_planes) cudaFree(ctx->d_planes);
+    ctx->d_planes = nullptr;
+    CK(cudaMalloc(&ctx->d_planes, (ns + nl) * kDim * sizeof(double)));
+    CK(cudaMemcpy(ctx->d_planes, short_planes, ns * kDim * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_planes + ns * kDim, long_planes, nl * kDim * sizeof(double), cudaMemcpyHostToDevice));
+    ctx->fam = *p;
+    ctx->has_family = true;
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_centering_reset(chgpu_ctx* ctx) {
+    if (!ctx) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    CK(cudaMemsetAsync(ctx->d_sums, 0, 128 * sizeof(unsigned long long), ctx->compute));
+    ctx->sum_count = 0;
+    memset(ctx->extra_sums, 0, sizeof(ctx->extra_sums));
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_centering_add_image(chgpu_ctx* ctx, uint32_t image_id) {
+    if (!ctx) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    uint32_t slot;
+    if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
+    const DevImage& d = ctx->images[slot].dev;
+    if (d.n == 0) return CHGPU_OK;
+    if (const chgpu_status s = order_compute_after_copy(ctx)) return s;
+    const uint32_t blocks = std::max(1u, std::min((d.n + 255u) / 256u, 4u * uint32_t(ctx->prop.multiProcessorCount)));
+    centering_sums_kernel<<<blocks, 256, 0, ctx->compute>>>(d.desc, d.n, ctx->d_sums);
+    CK(cudaGetLastError());
+    ctx->sum_count += d.n;
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_centering_get_sums(chgpu_ctx* ctx, uint64_t* sums128, uint64_t* count) {
+    if (!ctx || !sums128 || !count) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    unsigned long long tmp[128];
+    CK(cudaMemcpyAsync(tmp, ctx->d_sums, sizeof(tmp), cudaMemcpyDeviceToHost, ctx->compute));
+    CK(cudaStreamSynchronize(ctx->compute));
+    for (int i = 0; i < 128; ++i) sums128[i] = tmp[i] + ctx->extra_sums[i];
+    *count = ctx->sum_count;
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_centering_add_sums(chgpu_ctx* ctx, const uint64_t* sums128, uint64_t count) {
+    if (!ctx || !sums128) return CHGPU_EINVAL;
+    for (int i = 0; i < 128; ++i) ctx->extra_sums[i] += sums128[i];
+    ctx->sum_count += count;
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_set_centering(chgpu_ctx* ctx, const double* centering128) {
+    if (!ctx || !centering128) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    CK(cudaStreamSynchronize(ctx->compute));
+    CK(cudaMemcpy(ctx->d_centering, centering128, 128 * sizeof(double), cudaMemcpyHostToDevice));
+    ctx->has_centering = true;
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_centering_apply(chgpu_ctx* ctx, double* centering128_out) {
+    if (!ctx) return CHGPU_EINVAL;
+    uint64_t sums[128], count = 0;
+    if (const chgpu_status s = chgpu_centering_get_sums(ctx, sums, &count)) return s;
+    if (count == 0) return fail(ctx, CHGPU_EINVAL, "set_centering: no descriptors");  // hashing.cpp:60
+    double c[128];
+    for (int i = 0; i < 128; ++i) c[i] = static_cast<double>(sums[i]) / static_cast<double>(count);  // hashing.cpp:61-62
+    if (centering128_out) memcpy(centering128_out, c, sizeof(c));
+    return chgpu_set_centering(ctx, c);
+}
+
+// ---- descriptor load ----------------------------------------------------------------------------
+chgpu_status chgpu_upload_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, const uint8_t* desc,
+                                const float* keypoints) {
+    if (!ctx || (n && !desc)) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    uint32_t slot;
+    if (const chgpu_status s = alloc_image(ctx, image_id, n, &slot)) return s;
+    if (const chgpu_status s = order_copy_after_compute(ctx)) return s;
+    ImageRec& r = ctx->images[slot];
+    if (const chgpu_status s = h2d(ctx, const_cast<uint8_t*>(r.dev.desc), desc, size_t(n) * kDim)) return s;
+    if (keypoints) {
+        if (const chgpu_status s = h2d(ctx, const_cast<float4*>(r.dev.kp), keypoints, size_t(n) * 16)) return s;
+    } else if (n) {
+        CK(cudaMemsetAsync(const_cast<float4*>(r.dev.kp), 0, size_t(n) * 16, ctx->copy));
+    }
+    return publish_slot(ctx, slot);
+}
+
+chgpu_status chgpu_upload_chft(chgpu_ctx* ctx, uint32_t image_id, const void* blob, size_t nbytes,
+                               uint32_t* count_out, chgpu_file_fault* fault, uint64_t* fault_offset) {
+    if (!ctx || !blob) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    auto bad = [&](chgpu_file_fault f, uint64_t off, const char* what) {
+        if (fault) *fault = f;
+        if (fault_offset) *fault_offset = off;
+        return fail(ctx, CHGPU_EFORMAT, "image %u: %s at byte %llu", image_id, what, (unsigned long long)off);
+    };
+    if (fault) *fault = CHGPU_FAULT_NONE;
+    // header checks in the order of parse_features_blob (engine.cpp:458-472)
+    const unsigned char* b = static_cast<const unsigned char*>(blob);
+    if (nbytes < 16) return bad(CHGPU_FAULT_TRUNCATED, nbytes, "truncated payload (header)");
+    if (memcmp(b, "CHFT", 4) != 0) return bad(CHGPU_FAULT_BAD_MAGIC, 0, "bad magic");
+    uint32_t version, count;
+    memcpy(&version, b + 4, 4);
+    memcpy(&count, b + 8, 4);
+    if (version != 1) return bad(CHGPU_FAULT_BAD_VERSION, 4, "unsupported version");
+    const size_t expected = 16 + size_t(count) * 144;
+    if (nbytes < expected) return bad(CHGPU_FAULT_TRUNCATED, nbytes, "truncated payload");
+    if (count_out) *count_out = count;
+
+    uint32_t slot;
+    if (const chgpu_status s = alloc_image(ctx, image_id, count, &slot)) return s;
+    ImageRec& r = ctx->images[slot];
+    if (count) {
+        // raw AoS records travel once over PCIe into a scratch block, the device splits them
+        char* raw = nullptr;
+        const size_t raw_bytes = size_t(count) * 144;
+        if (ctx->arena.alloc(raw_bytes, &raw) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, CHGPU_ENOMEM, "staging block of %zu bytes", raw_bytes);
+        }
+        if (const chgpu_status s = order_copy_after_compute(ctx)) return s;
+        if (const chgpu_status s = h2d(ctx, raw, b + 16, raw_bytes)) return s;
+        if (const chgpu_status s = order_compute_after_copy(ctx)) return s;
+        const uint32_t blocks = std::min<uint64_t>((uint64_t(count) * 9 + 255) / 256, 8u * ctx->prop.multiProcessorCount);
+        chft_split_kernel<<<blocks, 256, 0, ctx->compute>>>(reinterpret_cast<const uint4*>(raw), count,
+                                                           reinterpret_cast<uint4*>(const_cast<uint8_t*>(r.dev.desc)),
+                                                           reinterpret_cast<uint4*>(const_cast<float4*>(r.dev.kp)));
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(ctx->compute));
+        ctx->arena.release(raw, raw_bytes);
+    }
+    return publish_slot(ctx, slot);
+}
+
+chgpu_status chgpu_evict_image(chgpu_ctx* ctx, uint32_t image_id) {
+    if (!ctx) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    uint32_t slot;
+    if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
+    CK(cudaStreamSynchronize(ctx->copy));
+    CK(cudaStreamSynchronize(ctx->compute));
+    ImageRec& r = ctx->images[slot];
+    ctx->arena.release(r.block, r.block_bytes);
+    r = ImageRec{};
+    ctx->free_slots.push_back(slot);
+    ctx->slot_of.erase(image_id);
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_image_points(chgpu_ctx* ctx, uint32_t image_id, uint32_t* n) {
+    if (!ctx || !n) return CHGPU_EINVAL;
+    uint32_t slot;
+    if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
+    *n = ctx->images[slot].dev.n;
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_download_descriptors(chgpu_ctx* ctx, uint32_t image_id, uint8_t* desc, float* keypoints) {
+    if (!ctx) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    uint32_t slot;
+    if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
+    if (const chgpu_status s = chgpu_sync(ctx)) return s;
+    const DevImage& d = ctx->images[slot].dev;
+    if (desc && d.n) CK(cudaMemcpy(desc, d.desc, size_t(d.n) * kDim, cudaMemcpyDeviceToHost));
+    if (keypoints && d.n) CK(cudaMemcpy(keypoints, d.kp, size_t(d.n) * 16, cudaMemcpyDeviceToHost));
+    return CHGPU_OK;
+}
+
+// ---- hash build ---------------------------------------------------------------------------------
+chgpu_status chgpu_hash_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32_t count, int reduce_rounds) {
+    if (!ctx || (count && !image_ids)) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    if (reduce_rounds < 0 || reduce_rounds > 7)
+        return fail(ctx, CHGPU_EINVAL, "reduce_dot tail rounds out of range 0..7");  // hashing.hpp:28-29
+    if (!ctx->has_family) return fail(ctx, CHGPU_ELOGIC, "no hash family installed");
+    if (!ctx->has_centering) return fail(ctx, CHGPU_ELOGIC, "compute_codes: centering has not been set");  // hashing.cpp:131-132
+    if (count == 0) return CHGPU_OK;
+    std::vector<uint32_t> slots(count);
+    uint32_t max_n = 0;
+    for (uint32_t i = 0; i < count; ++i) {
+        if (const chgpu_status s = find_slot(ctx, image_ids[i], &slots[i])) return s;
+        max_n = std::max(max_n, ctx->images[slots[i]].dev.n);
+    }
+    if (const chgpu_status s = ensure_slots_scratch(ctx, count)) return s;
+    if (const chgpu_status s = order_compute_after_copy(ctx)) return s;
+    // d_slots is reused by successive calls; the pageable source is consumed synchronously
+    CK(cudaStreamSynchronize(ctx->compute));
+    CK(cudaMemcpyAsync(ctx->d_slots, slots.data(), count * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->compute));
+    if (max_n) {
+        const dim3 grid((max_n + kHashTilePoints - 1) / kHashTilePoints, count);
+        cudaError_t e = cudaSuccess;
+        switch (reduce_rounds) {
+            case 0: e = launch_hash_rr<0>(ctx, grid); break;
+            case 1: e = launch_hash_rr<1>(ctx, grid); break;
+            case 2: e = launch_hash_rr<2>(ctx, grid); break;
+            case 3: e = launch_hash_rr<3>(ctx, grid); break;
+            case 4: e = launch_hash_rr<4>(ctx, grid); break;
+            case 5: e = launch_hash_rr<5>(ctx, grid); break;
+            case 6: e = launch_hash_rr<6>(ctx, grid); break;
+            default: e = launch_hash_rr<7>(ctx, grid); break;
+        }
+        CK(e);
+    }
+    if (const chgpu_status s = launch_bucket_build(ctx, count)) return s;
+    for (uint32_t i = 0; i < count; ++i) {
+        ImageRec& r = ctx->images[slots[i]];
+        r.dev.flags |= 1u;
+        ctx->h_images[slots[i]] = r.dev;
+    }
+    // flags live only on the host mirror and in the device table; kernels never read them, so
+    // the table entries pushed at upload time stay valid.
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_download_codes(chgpu_ctx* ctx, uint32_t image_id, uint32_t* shorts, uint64_t* longs) {
+    if (!ctx) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    uint32_t slot;
+    if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
+    const DevImage& d = ctx->images[slot].dev;
+    if (!(d.flags & 1u)) return fail(ctx, CHGPU_ELOGIC, "image %u: codes not computed", image_id);
+    if (const chgpu_status s = chgpu_sync(ctx)) return s;
+    if (shorts && d.n) CK(cudaMemcpy(shorts, d.shorts, size_t(d.n) * ctx->fam.table_count * 4, cudaMemcpyDeviceToHost));
+    // uint4 words (x,y,z,w) = bits 0..127 little-endian = LongCode::words[0], words[1]
+    if (longs && d.n) CK(cudaMemcpy(longs, d.longs, size_t(d.n) * 16, cudaMemcpyDeviceToHost));
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_upload_codes(chgpu_ctx* ctx, uint32_t image_id, const uint32_t* shorts, const uint64_t* longs) {
+    if (!ctx || !shorts || !longs) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    uint32_t slot;
+    if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
+    ImageRec& r = ctx->images[slot];
+    const uint32_t n = r.dev.n, L = ctx->fam.table_count, m = ctx->fam.short_bits;
+    for (size_t i = 0; i < size_t(n) * L; ++i)
+        if (m < 32 && (shorts[i] >> m) != 0) return fail(ctx, CHGPU_EINVAL, "short code %u exceeds %u bits", shorts[i], m);
+    if (const chgpu_status s = order_copy_after_compute(ctx)) return s;
+    if (const chgpu_status s = h2d(ctx, r.dev.shorts, shorts, size_t(n) * L * 4)) return s;
+    if (const chgpu_status s = h2d(ctx, r.dev.longs, longs, size_t(n) * 16)) return s;
+    if (const chgpu_status s = ensure_slots_scratch(ctx, 1)) return s;
+    if (const chgpu_status s = order_compute_after_copy(ctx)) return s;
+    CK(cudaStreamSynchronize(ctx->compute));
+    CK(cudaMemcpyAsync(ctx->d_slots, &slot, sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->compute));
+    if (const chgpu_status s = launch_bucket_build(ctx, 1)) return s;
+    CK(cudaStreamSynchronize(ctx->compute));
+    r.dev.flags |= 1u;
+    ctx->h_images[slot] = r.dev;
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_download_bucket_index(chgpu_ctx* ctx, uint32_t image_id, uint32_t* offsets, uint32_t* points) {
+    if (!ctx) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    uint32_t slot;
+    if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
+    const DevImage& d = ctx->images[slot].dev;
+    if (!(d.flags & 1u)) return fail(ctx, CHGPU_ELOGIC, "image %u: codes not computed", image_id);
+    if (const chgpu_status s = chgpu_sync(ctx)) return s;
+    const uint32_t L = ctx->fam.table_count;
+    const size_t noff = size_t(L) * ((size_t(1) << ctx->fam.short_bits) + 1);
+    if (offsets) CK(cudaMemcpy(offsets, d.offs, noff * 4, cudaMemcpyDeviceToHost));
+    if (points && d.n) {
+        std::vector<uint16_t> tmp(size_t(L) * d.n);
+        CK(cudaMemcpy(tmp.data(), d.points, tmp.size() * 2, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < tmp.size(); ++i) points[i] = tmp[i];
+    }
+    return CHGPU_OK;
+}
+
+// ---- match --------------------------------------------------------------------------------------
+chgpu_status chgpu_match_pairs(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs, const chgpu_match_cfg* cfg,
+                               uint64_t* offsets, chgpu_match_record* records, uint64_t capacity, uint64_t* total,
+                               chgpu_match_stats* stats) {
+    if (!ctx || !cfg || !offsets || (npairs && !pairs) || (capacity && !records)) return CHGPU_EINVAL;
+    MatchRun run{pairs, npairs, *cfg, SinkMode::Host};
+    run.offsets = offsets;
+    run.records = records;
+    run.capacity = capacity;
+    const chgpu_status s = run_match(ctx, run, stats);
+    if (total) *total = run.total;
+    if (s != CHGPU_OK) return s;
+    if (run.overflow)
+        return fail(ctx, CHGPU_ENOMEM, "record capacity %llu < %llu required", (unsigned long long)capacity,
+                    (unsigned long long)run.total);
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_match_pairs_stream(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
+                                      const chgpu_match_cfg* cfg, chgpu_sink_fn sink, void* user,
+                                      chgpu_match_stats* stats) {
+    if (!ctx || !cfg || (npairs && !pairs)) return CHGPU_EINVAL;
+    MatchRun run{pairs, npairs, *cfg, SinkMode::Stream};
+    run.sink = sink;
+    run.user = user;
+    return run_match(ctx, run, stats);
+}
+
+chgpu_status chgpu_match_pairs_device(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
+                                      const chgpu_match_cfg* cfg, chgpu_match_stats* stats) {
+    if (!ctx || !cfg || (npairs && !pairs)) return CHGPU_EINVAL;
+    MatchRun run{pairs, npairs, *cfg, SinkMode::Device};
+    return run_match(ctx, run, stats);
+}
+
+chgpu_status chgpu_debug_ranked(chgpu_ctx* ctx, uint32_t image_i, uint32_t image_j, const chgpu_match_cfg* cfg,
+                                uint32_t* ranked, uint32_t* ranked_count) {
+    if (!ctx || !cfg || !ranked || !ranked_count) return CHGPU_EINVAL;
+    const uint32_t pr[2] = {image_i, image_j};
+    MatchRun run{pr, 1, *cfg, SinkMode::Device};
+    run.dbg_ranked = ranked;
+    run.dbg_count = ranked_count;
+    return run_match(ctx, run, nullptr);
+}
+
+}  // extern "C"

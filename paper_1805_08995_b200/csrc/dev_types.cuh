@@ -1,0 +1,48 @@
+// dev_types.cuh — device-side records shared by the hash-build and match kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace chgpu {
+
+constexpr int kDim = 128;            // descriptor dimension (feature_io.hpp:14 kDescriptorDim)
+constexpr int kMaxTables = 8;        // L envelope of the device path
+constexpr int kMaxShortBits = 12;    // m envelope (dense 2^m+1 CSR per table)
+constexpr int kMaxTopK = 32;         // ranked list lives one entry per lane
+constexpr uint32_t kMaxPoints = 65536;  // bucket point ids are u16
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+// One resident image.  All arrays live in one arena block (see Arena in chgpu.cu):
+//   desc   n x 128 u8          SoA descriptors (reference Descriptor, feature_io.hpp:27)
+//   kp     n x float4          keypoints (x, y, scale, orientation)
+//   longs  n x uint4           128-bit ranking code, word w = bits 32w..32w+31 (LongCode, hashing.hpp:91)
+//   shorts n x L u32           bucket ids [point*L + table] (ShortCodes::values, hashing.hpp:80)
+//   offs   L x (2^m + 1) u32   dense CSR offsets per table (BucketIndex, matcher.hpp:30-41)
+//   points L x n u16           point ids bucket-major, ascending id inside a bucket
+struct DevImage {
+    const uint8_t* desc;
+    const float4* kp;
+    uint4* longs;
+    uint32_t* shorts;
+    uint32_t* offs;
+    uint16_t* points;
+    uint32_t n;
+    uint32_t flags;  // bit0: codes + buckets valid
+};
+
+struct PairDesc {
+    uint32_t slot_i;   // query image
+    uint32_t slot_j;   // train image
+    uint64_t res_off;  // first entry of this pair in the per-query result scratch
+};
+
+struct DevStats {
+    unsigned long long raw_candidates;
+    unsigned long long verified_queries;
+    unsigned long long distances;
+    unsigned long long matches;
+    unsigned long long checksum;
+};
+
+}  // namespace chgpu

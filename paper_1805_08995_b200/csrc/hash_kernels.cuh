@@ -1,0 +1,254 @@
+// hash_kernels.cuh — descriptor staging, centering sums, hash codes (K1) and bucket build (K2).
+//
+// All arithmetic that decides a hash bit is fp64 in the reference's exact operation order
+// (reduce_dot, hashing.hpp:24-43): products rounded individually (__dmul_rn, never FMA), the
+// first 7-N_r halving rounds as a pairwise tree, the last 2^N_r partial sums serially.
+#pragma once
+
+#include "dev_types.cuh"
+
+namespace chgpu {
+
+// ---------------------------------------------------------------------------------------------
+// K0: split the 144-byte AoS records of a CHFT blob (feature_io.hpp:82-89) into SoA.
+// One 16-byte chunk per thread: chunk 0 of a record is the keypoint, chunks 1..8 the descriptor.
+__global__ void chft_split_kernel(const uint4* __restrict__ records, uint32_t n,
+                                  uint4* __restrict__ desc, uint4* __restrict__ kp) {
+    const uint64_t total = uint64_t(n) * 9;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t p = uint32_t(i / 9), c = uint32_t(i % 9);
+        const uint4 v = __ldg(records + i);
+        if (c == 0) kp[p] = v;
+        else desc[uint64_t(p) * 8 + (c - 1)] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Centering pass: exact integer column sums (CenteringAccumulator::add, hashing.cpp:52-57).
+// Each lane owns 4 adjacent byte columns of the 128-byte row; a warp reads whole rows.
+__global__ void centering_sums_kernel(const uint8_t* __restrict__ desc, uint32_t n,
+                                      unsigned long long* __restrict__ sums /*128*/) {
+    __shared__ unsigned int s_acc[kDim];
+    if (threadIdx.x < kDim) s_acc[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    // 255 * rows_per_block must stay below 2^32: rows_per_block <= 2^20 is enforced by the launcher.
+    unsigned int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    const uint32_t rows_per_block = (n + gridDim.x - 1) / gridDim.x;
+    const uint32_t r0 = blockIdx.x * rows_per_block;
+    const uint32_t r1 = min(n, r0 + rows_per_block);
+    for (uint32_t r = r0 + warp; r < r1; r += nwarps) {
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(desc + uint64_t(r) * kDim) + lane);
+        a0 += w & 0xff;
+        a1 += (w >> 8) & 0xff;
+        a2 += (w >> 16) & 0xff;
+        a3 += w >> 24;
+    }
+    atomicAdd(&s_acc[lane * 4 + 0], a0);
+    atomicAdd(&s_acc[lane * 4 + 1], a1);
+    atomicAdd(&s_acc[lane * 4 + 2], a2);
+    atomicAdd(&s_acc[lane * 4 + 3], a3);
+    __syncthreads();
+    if (threadIdx.x < kDim) atomicAdd(&sums[threadIdx.x], (unsigned long long)s_acc[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------------------------------------
+// K1: hash codes.  One CTA = 64 points x all planes; 8 warps, each lane owns 2 points
+// (lane, lane+32) and each warp 2 planes of the current 16-plane chunk, so one pass of the
+// reduction DAG evaluates 4 dots with 2+2 shared-memory operands per product group.
+//
+// Shared memory: cT[128][64] centered descriptors (fp64, component-major => conflict-free),
+// hs[16][128] plane chunk (broadcast reads), pbits[64][kPlaneWords] result bits.
+constexpr int kHashTilePoints = 64;
+constexpr int kHashChunkPlanes = 16;
+constexpr int kHashThreads = 256;
+constexpr int kPlaneWords = (kMaxTables * 32 + 128 + 31) / 32;  // 12 words cover L*m + n <= 384 planes
+
+constexpr size_t hash_smem_bytes() {
+    return sizeof(double) * (kDim * kHashTilePoints + kHashChunkPlanes * kDim) +
+           sizeof(uint32_t) * kHashTilePoints * kPlaneWords;
+}
+
+// Node of the reduction DAG.  value(W, X) = sums[X] after the halving round of width W:
+//   value(128, X) = c[X] * h[X]                       (rounded product)
+//   value(W, X)   = value(2W, X) + value(2W, X + W)    (sums[i] += sums[i + width])
+template <int W, int X>
+__device__ __forceinline__ void dag_node(const double* __restrict__ c, const double* __restrict__ h,
+                                         double (&o)[4]) {
+    if constexpr (W == kDim) {
+        const double c0 = c[X * kHashTilePoints], c1 = c[X * kHashTilePoints + 32];
+        const double h0 = h[X], h1 = h[kDim + X];
+        o[0] = __dmul_rn(c0, h0);
+        o[1] = __dmul_rn(c0, h1);
+        o[2] = __dmul_rn(c1, h0);
+        o[3] = __dmul_rn(c1, h1);
+    } else {
+        double a[4], b[4];
+        dag_node<W * 2, X>(c, h, a);
+        dag_node<W * 2, X + W>(c, h, b);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] = __dadd_rn(a[i], b[i]);
+    }
+}
+
+// Serial tail: acc = sums[0]; acc += sums[1..T-1]  with T = 2^N_r.
+template <int T, int J>
+__device__ __forceinline__ void dag_tail(const double* __restrict__ c, const double* __restrict__ h,
+                                         double (&acc)[4]) {
+    if constexpr (J < T) {
+        double v[4];
+        dag_node<T, J>(c, h, v);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] = (J == 0) ? v[i] : __dadd_rn(acc[i], v[i]);
+        dag_tail<T, J + 1>(c, h, acc);
+    }
+}
+
+__device__ __forceinline__ uint32_t take_bits(const uint32_t* w, uint32_t start, uint32_t len) {
+    const uint32_t idx = start >> 5, sh = start & 31;
+    uint64_t v = w[idx];
+    if (sh + len > 32) v |= uint64_t(w[idx + 1]) << 32;
+    v >>= sh;
+    return len >= 32 ? uint32_t(v) : uint32_t(v) & ((1u << len) - 1u);
+}
+
+template <int RR>
+__global__ void __launch_bounds__(kHashThreads)
+hash_codes_kernel(const DevImage* __restrict__ images, const uint32_t* __restrict__ slots,
+                  const double* __restrict__ planes /* (L*m + n) x 128: short planes then long */,
+                  const double* __restrict__ centering /* 128 */, uint32_t m, uint32_t L, uint32_t nlong) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* cT = reinterpret_cast<double*>(smem_raw);
+    double* hs = cT + kDim * kHashTilePoints;
+    uint32_t* pbits = reinterpret_cast<uint32_t*>(hs + kHashChunkPlanes * kDim);
+
+    const DevImage img = images[slots[blockIdx.y]];
+    const uint32_t p0 = blockIdx.x * kHashTilePoints;
+    if (p0 >= img.n) return;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t nplanes = L * m + nlong;
+
+    // Stage: c[x][p] = double(desc[p][x]) - centering[x]   (center_descriptor, hashing.cpp:72-78)
+    for (uint32_t i = tid; i < kHashTilePoints * (kDim / 4); i += kHashThreads) {
+        const uint32_t p = i >> 5, x4 = i & 31;  // 32 words per descriptor row
+        uint32_t w = 0;
+        if (p0 + p < img.n) w = __ldg(reinterpret_cast<const uint32_t*>(img.desc + uint64_t(p0 + p) * kDim) + x4);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const uint32_t x = x4 * 4 + b;
+            cT[x * kHashTilePoints + p] = __dsub_rn(double((w >> (8 * b)) & 0xff), __ldg(centering + x));
+        }
+    }
+    for (uint32_t i = tid; i < kHashTilePoints * kPlaneWords; i += kHashThreads) pbits[i] = 0;
+
+    const double* c = cT + lane;
+    const double* h = hs + (2 * warp) * kDim;
+    for (uint32_t g0 = 0; g0 < nplanes; g0 += kHashChunkPlanes) {
+        __syncthreads();  // previous chunk consumed (and, first time, cT / pbits staged)
+        for (uint32_t i = tid; i < kHashChunkPlanes * kDim; i += kHashThreads) {
+            const uint32_t g = g0 + i / kDim;
+            hs[i] = g < nplanes ? __ldg(planes + uint64_t(g) * kDim + (i % kDim)) : 0.0;
+        }
+        __syncthreads();
+        double acc[4];
+        dag_tail<(1 << RR), 0>(c, h, acc);
+        // Bit = (dot > 0.0), ties give 0 (hashing.cpp:80-99).
+        const uint32_t ga = g0 + 2 * warp, gb = ga + 1;
+        if (ga < nplanes) {
+            if (acc[0] > 0.0) atomicOr(&pbits[lane * kPlaneWords + (ga >> 5)], 1u << (ga & 31));
+            if (acc[2] > 0.0) atomicOr(&pbits[(lane + 32) * kPlaneWords + (ga >> 5)], 1u << (ga & 31));
+        }
+        if (gb < nplanes) {
+            if (acc[1] > 0.0) atomicOr(&pbits[lane * kPlaneWords + (gb >> 5)], 1u << (gb & 31));
+            if (acc[3] > 0.0) atomicOr(&pbits[(lane + 32) * kPlaneWords + (gb >> 5)], 1u << (gb & 31));
+        }
+    }
+    __syncthreads();
+
+    // Pack: short code t = planes [t*m, t*m+m), bit j at 1u<<j (hashing.cpp:80-88);
+    // long code bit j = plane L*m + j, word j/32 of the uint4 (hashing.cpp:90-99).
+    if (tid < kHashTilePoints && p0 + tid < img.n) {
+        const uint32_t p = p0 + tid;
+        uint32_t w[kPlaneWords + 1];
+#pragma unroll
+        for (int i = 0; i < kPlaneWords; ++i) w[i] = pbits[tid * kPlaneWords + i];
+        w[kPlaneWords] = 0;
+        for (uint32_t t = 0; t < L; ++t) img.shorts[uint64_t(p) * L + t] = take_bits(w, t * m, m);
+        uint32_t lw[4];
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) {
+            const uint32_t first = k * 32;
+            lw[k] = first < nlong ? take_bits(w, L * m + first, min(32u, nlong - first)) : 0u;
+        }
+        img.longs[p] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K2: bucket build.  One CTA per image, one warp per table: a stable counting sort of the
+// image's points by m-bit code (build_bucket_index, matcher.cpp:27-51).  Points are consumed
+// in ascending id order 32 at a time; __match_any_sync ranks equal codes inside the step, a
+// shared-memory cursor per bucket carries the running position, so ids inside a bucket come
+// out ascending exactly as the reference's sort of (code, point) pairs leaves them.
+__global__ void bucket_build_kernel(const DevImage* __restrict__ images, const uint32_t* __restrict__ slots,
+                                    uint32_t m, uint32_t L) {
+    extern __shared__ uint32_t s_cursor[];  // L x 2^m
+    const DevImage img = images[slots[blockIdx.x]];
+    const uint32_t lane = threadIdx.x & 31, t = threadIdx.x >> 5;
+    if (t >= L) return;
+    const uint32_t nb = 1u << m, n = img.n;
+    uint32_t* cur = s_cursor + t * nb;
+    for (uint32_t b = lane; b < nb; b += 32) cur[b] = 0;
+    __syncwarp();
+
+    // Pass 1: histogram.
+    for (uint32_t base = 0; base < n; base += 32) {
+        const uint32_t p = base + lane;
+        const bool valid = p < n;
+        const uint32_t code = valid ? __ldg(img.shorts + uint64_t(p) * L + t) : kNone;
+        const uint32_t peers = __match_any_sync(0xffffffffu, code);
+        if (valid && (__ffs(peers) - 1) == int(lane)) cur[code] += __popc(peers);
+        __syncwarp();
+    }
+    // Exclusive scan of the histogram -> CSR offsets; cursors restart at the bucket starts.
+    uint32_t* offs = img.offs + uint64_t(t) * (nb + 1);
+    uint32_t carry = 0;
+    for (uint32_t b0 = 0; b0 < nb; b0 += 32) {
+        const uint32_t b = b0 + lane;
+        const uint32_t v = b < nb ? cur[b] : 0;
+        uint32_t incl = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, d);
+            if (int(lane) >= d) incl += u;
+        }
+        if (b < nb) {
+            offs[b] = carry + incl - v;
+            cur[b] = carry + incl - v;
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) offs[nb] = n;
+    __syncwarp();
+
+    // Pass 2: stable placement.
+    uint16_t* pts = img.points + uint64_t(t) * n;
+    for (uint32_t base = 0; base < n; base += 32) {
+        const uint32_t p = base + lane;
+        const bool valid = p < n;
+        const uint32_t code = valid ? __ldg(img.shorts + uint64_t(p) * L + t) : kNone;
+        const uint32_t peers = __match_any_sync(0xffffffffu, code);
+        const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+        uint32_t start = 0;
+        if (valid) start = cur[code];
+        __syncwarp();
+        if (valid) {
+            pts[start + rank] = uint16_t(p);
+            if (rank == 0) cur[code] = start + __popc(peers);
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace chgpu
