@@ -193,6 +193,9 @@ class Matcher:
     def sync(self):
         self._ck(self.lib.chgpu_sync(self.h))
 
+    def set_sub_batch_queries(self, max_queries: int):
+        self._ck(self.lib.chgpu_set_sub_batch_queries(self.h, max_queries))
+
     def device_props(self) -> dict:
         p = N.DevicePropsC()
         self._ck(self.lib.chgpu_get_device_props(self.h, C.byref(p)))

@@ -153,6 +153,7 @@ struct chgpu_ctx {
     size_t slots_cap = 0;
     uint32_t* d_dbg = nullptr;
     size_t dbg_cap = 0;
+    uint64_t sub_batch_queries = kSubBatchQueries;
 };
 
 namespace {
@@ -496,7 +497,7 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
             if (!(I.flags & 1u) || !(J.flags & 1u))
                 return fail(ctx, CHGPU_ELOGIC, "pair (%u,%u): codes not computed (call chgpu_hash_images first)",
                             run.pairs[2 * k], run.pairs[2 * k + 1]);
-            if (cur.count && (cur.queries + I.n > kSubBatchQueries || cur.count >= (1u << 20))) {
+            if (cur.count && (cur.queries + I.n > ctx->sub_batch_queries || cur.count >= (1u << 20))) {
                 subs.push_back(cur);
                 cur = SubBatch{k, 0, 0, 0, 0};
             }
@@ -763,6 +764,12 @@ chgpu_status chgpu_sync(chgpu_ctx* ctx) {
     DeviceGuard guard(ctx->device);
     CK(cudaStreamSynchronize(ctx->copy));
     CK(cudaStreamSynchronize(ctx->compute));
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_set_sub_batch_queries(chgpu_ctx* ctx, uint64_t max_queries) {
+    if (!ctx) return CHGPU_EINVAL;
+    ctx->sub_batch_queries = max_queries ? max_queries : kSubBatchQueries;
     return CHGPU_OK;
 }
 

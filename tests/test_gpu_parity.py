@@ -1,0 +1,457 @@
+"""GPU parity suite (run with `-m gpu` on a B200).  Every check goes through the C ABI
+(libchgpu.so) and compares with the CPU oracle on the same inputs:
+  - hash codes, bucket CSR and ranked candidate lists: bit-exact;
+  - match records: bit-exact (stronger than the 99.9 % agreement north_star allows);
+  - golden vectors produced by the compiled reference (tests/golden);
+  - size-independent properties at BASELINE.json's config-2 size.
+Nothing here reads /root/reference."""
+import struct
+
+import numpy as np
+import pytest
+
+import oracle_lib
+import paper_1805_08995_b200 as ch
+from paper_1805_08995_b200.synth import make_dataset
+from test_oracle import GOLDEN_CFGS
+
+pytestmark = pytest.mark.gpu
+
+BASE = 1000  # image ids used by this module
+
+
+def fresh(matcher, family):
+    """Drops every image this module may have left and installs `family`."""
+    for img in list(getattr(matcher, "_test_ids", set())):
+        try:
+            matcher.evict(img)
+        except KeyError:
+            pass
+    matcher._test_ids = set()
+    matcher.set_family(family)
+    matcher.set_sub_batch_queries(0)
+
+
+def put(matcher, image_id, desc, kp=None):
+    matcher.upload(image_id, desc, kp)
+    matcher._test_ids.add(image_id)
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    return oracle_lib.best()  # the compiled reference where it exists, else the pinned restatement
+
+
+@pytest.fixture(scope="module")
+def default_family():
+    return ch.build_hash_family(ch.FamilyParams())
+
+
+def oracle_codes(oracle, fam, cen, desc, rr=3):
+    return oracle.compute_codes(fam.params, fam.short_planes, fam.long_planes, cen, desc, rr)
+
+
+def mix64(x):
+    x = (x + np.uint64(0x9e3779b97f4a7c15))
+    x = (x ^ (x >> np.uint64(30))) * np.uint64(0xbf58476d1ce4e5b9)
+    x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94d049bb133111eb)
+    return x ^ (x >> np.uint64(31))
+
+
+def host_checksum(offsets, records):
+    """Same order-independent checksum compact_kernel accumulates on the device."""
+    with np.errstate(over="ignore"):
+        pair = np.repeat(np.arange(len(offsets) - 1, dtype=np.uint64), np.diff(offsets).astype(np.int64))
+        a = (pair << np.uint64(32)) | records["query_index"].astype(np.uint64)
+        b = (records["train_index"].astype(np.uint64) << np.uint64(32)) | records["distance_sq"].astype(np.uint64)
+        return int(np.sum(mix64(mix64(a) ^ b), dtype=np.uint64))
+
+
+# ---- golden vectors -------------------------------------------------------------------------------
+def test_codes_buckets_matches_equal_golden(matcher, golden, default_family):
+    g = golden["small_dataset"]
+    fresh(matcher, default_family)
+    desc = g["desc"]
+    for i in range(3):
+        put(matcher, BASE + i, desc[i])
+    # centering: exact integer sums on the device, one division on the host
+    matcher.centering_reset()
+    for i in range(3):
+        matcher.centering_add(BASE + i)
+    sums, count = matcher.centering_sums()
+    assert count == 900 and np.array_equal(sums, desc.reshape(-1, 128).astype(np.uint64).sum(0))
+    cen = matcher.centering_apply()
+    assert np.array_equal(cen, g["centering"])
+
+    import hashlib
+    for rr in (0, 7, 3):
+        matcher.hash([BASE, BASE + 1, BASE + 2], rr)
+        for i in range(3):
+            c = matcher.codes(BASE + i)
+            if rr == 3:
+                assert np.array_equal(c.shorts, g[f"shorts{i}"]) and np.array_equal(c.longs, g[f"longs{i}"])
+            else:
+                assert hashlib.sha256(c.shorts.tobytes()).hexdigest() == str(g[f"shorts{i}_rr{rr}_sha"])
+                assert hashlib.sha256(c.longs.tobytes()).hexdigest() == str(g[f"longs{i}_rr{rr}_sha"])
+    bi = matcher.bucket_index(BASE + 1)
+    assert np.array_equal(bi.offsets, g["offs1"]) and np.array_equal(bi.points, g["pts1"])
+
+    for tag, cfg in GOLDEN_CFGS.items():
+        pairs = [(BASE + a, BASE + b) for a, b in ((0, 1), (1, 2), (2, 0))]
+        offs, rec, stats = matcher.match_pairs(pairs, cfg)
+        for k, (a, b) in enumerate(((0, 1), (1, 2), (2, 0))):
+            assert np.array_equal(rec[offs[k]:offs[k + 1]], g[f"rec_{tag}_{a}{b}"]), (tag, a, b)
+            ranked, rc = matcher.ranked(BASE + a, BASE + b, cfg)
+            assert np.array_equal(rc, g[f"rcount_{tag}_{a}{b}"]), (tag, a, b)
+            gr = g[f"ranked_{tag}_{a}{b}"]
+            for q in range(len(rc)):
+                assert np.array_equal(ranked[q, :rc[q]], gr[q, :rc[q]]), (tag, a, b, q)
+        gs = [g[f"stats_{tag}_{a}{b}"] for a, b in ((0, 1), (1, 2), (2, 0))]
+        assert stats["raw_candidates"] == sum(int(s[0]) for s in gs)
+        assert stats["verified_queries"] == sum(int(s[4]) for s in gs)
+        assert stats["distances"] == sum(int(s[5]) for s in gs)
+        assert stats["matches"] == sum(int(s[6]) for s in gs) == len(rec)
+
+
+# ---- hash build vs oracle ---------------------------------------------------------------------------
+@pytest.mark.parametrize("params,n,shape", [
+    (ch.FamilyParams(), 1000, "uniform"),            # BASELINE config 1 size
+    (ch.FamilyParams(), 4096, "sift"),
+    (ch.FamilyParams(10, 96, 4, 99), 777, "uniform"),
+    (ch.FamilyParams(12, 128, 8, 3), 513, "sift"),
+    (ch.FamilyParams(1, 2, 1, 1), 65, "uniform"),     # smallest legal family
+    (ch.FamilyParams(5, 33, 7, 4), 64, "uniform"),    # code words straddle 32-bit boundaries
+])
+def test_codes_and_buckets_bit_exact(matcher, oracle, params, n, shape):
+    fam = ch.build_hash_family(params)
+    fresh(matcher, fam)
+    desc = make_dataset(2, n, seed=21, shape=shape)
+    cen = oracle.centering(list(desc))
+    matcher.set_centering(cen)
+    put(matcher, BASE, desc[0])
+    put(matcher, BASE + 1, desc[1])
+    for rr in (3, 0, 1, 2, 4, 5, 6, 7):
+        matcher.hash([BASE, BASE + 1], rr)
+        for i in range(2):
+            s, l = oracle_codes(oracle, fam, cen, desc[i], rr)
+            c = matcher.codes(BASE + i)
+            assert np.array_equal(c.shorts, s), (rr, i)
+            assert np.array_equal(c.longs, l), (rr, i)
+    s, _ = oracle_codes(oracle, fam, cen, desc[1])
+    offs, pts = oracle.build_bucket_index(params.short_bits, params.table_count, s)
+    bi = matcher.bucket_index(BASE + 1)
+    assert np.array_equal(bi.offsets, offs) and np.array_equal(bi.points, pts)
+
+
+def test_near_tie_projections_keep_their_sign(matcher, oracle, default_family):
+    """Descriptors equal to the centering give dot == 0 exactly -> bit 0; and a large
+    random sample has the same bits as the oracle even for |dot| < 1 (the fp64 exact-order claim)."""
+    fresh(matcher, default_family)
+    cen = np.full(128, 77.0)
+    matcher.set_centering(cen)
+    put(matcher, BASE, np.full((3, 128), 77, np.uint8))
+    matcher.hash([BASE])
+    c = matcher.codes(BASE)
+    assert not c.shorts.any() and not c.longs.any()
+    desc = make_dataset(1, 8192, seed=5)[0]
+    cen = oracle.centering([desc])
+    matcher.set_centering(cen)
+    put(matcher, BASE + 1, desc)
+    matcher.hash([BASE + 1])
+    s, l = oracle_codes(oracle, default_family, cen, desc)
+    c = matcher.codes(BASE + 1)
+    assert np.array_equal(c.shorts, s) and np.array_equal(c.longs, l)
+    dots = (desc.astype(np.float64) - cen) @ default_family.long_planes.T
+    assert (np.abs(dots) < 1.0).sum() > 100, "sample must contain near-zero projections"
+
+
+# ---- match vs oracle --------------------------------------------------------------------------------
+def run_pair_case(matcher, oracle, fam, desc_i, desc_j, cfgs, ids=(BASE, BASE + 1)):
+    cen = oracle.centering([desc_i, desc_j]) if len(desc_i) + len(desc_j) else np.zeros(128)
+    matcher.set_centering(cen)
+    put(matcher, ids[0], desc_i)
+    put(matcher, ids[1], desc_j)
+    matcher.hash(list(ids))
+    ci = oracle_codes(oracle, fam, cen, desc_i)
+    cj = oracle_codes(oracle, fam, cen, desc_j)
+    for cfg in cfgs:
+        want, wstats, wranked, wrc = oracle.match_pair(fam.params, cfg, desc_i, *ci, desc_j, *cj, want_ranked=True)
+        offs, rec, stats = matcher.match_pairs([ids], cfg)
+        assert offs.tolist() == [0, len(want)]
+        assert np.array_equal(rec, want), cfg
+        assert stats["raw_candidates"] == wstats["raw_candidates"]
+        assert stats["verified_queries"] == wstats["verified_queries"]
+        assert stats["distances"] == wstats["distances"]
+        ranked, rc = matcher.ranked(ids[0], ids[1], cfg)
+        assert np.array_equal(rc, wrc[: len(rc)])
+        for q in np.nonzero(rc)[0]:
+            assert np.array_equal(ranked[q, :rc[q]], wranked[q, :rc[q]]), (cfg, q)
+    return want
+
+
+CFGS = [ch.MatchConfig(), ch.MatchConfig(hamming_threshold=128), ch.MatchConfig(top_k=2, min_candidates_for_ratio=5),
+        ch.MatchConfig(top_k=32, hamming_threshold=64, ratio=0.95), ch.MatchConfig(top_k=3, hamming_threshold=50, ratio=0.5,
+                                                                                     min_candidates_for_ratio=0)]
+
+
+@pytest.mark.parametrize("n_i,n_j,shape", [
+    (1000, 1000, "uniform"),   # BASELINE config 1
+    (4096, 4096, "uniform"),   # config 2 image size
+    (4096, 3000, "sift"),
+    (8192, 8192, "uniform"),   # config 3 image size: train codes fill 128 KiB of shared memory
+    (8192, 8192, "sift"),      # skewed buckets
+    (777, 13000, "uniform"),   # ragged, near the shared-memory capacity
+])
+def test_match_bit_exact(matcher, oracle, default_family, n_i, n_j, shape):
+    fresh(matcher, default_family)
+    n = max(n_i, n_j)
+    d = make_dataset(2, n, seed=31 + n_i, shape=shape)
+    want = run_pair_case(matcher, oracle, default_family, d[0][:n_i], d[1][:n_j], CFGS)
+    if shape == "uniform":
+        assert len(want) > 0.2 * min(n_i, n_j), "twins must match"
+
+
+@pytest.mark.parametrize("n,shape", [(16384, "uniform"), (32768, "uniform"), (20000, "sift")])
+def test_match_large_images_global_gather_and_multipass(matcher, oracle, default_family, n, shape):
+    """Config-5 sizes: train codes no longer fit shared memory (global-gather variant) and the raw
+    candidate count per query exceeds one ranking pass (merge path)."""
+    fresh(matcher, default_family)
+    d = make_dataset(2, n, seed=41, shape=shape)
+    run_pair_case(matcher, oracle, default_family, d[0], d[1], [ch.MatchConfig(), ch.MatchConfig(top_k=4, hamming_threshold=45)])
+
+
+@pytest.mark.parametrize("params", [ch.FamilyParams(10, 96, 4, 99), ch.FamilyParams(6, 64, 8, 2),
+                                    ch.FamilyParams(12, 128, 2, 3), ch.FamilyParams(3, 32, 3, 8)])
+def test_match_other_families(matcher, oracle, params):
+    fam = ch.build_hash_family(params)
+    fresh(matcher, fam)
+    d = make_dataset(2, 2000, seed=51)
+    tau = min(40, params.long_bits)
+    run_pair_case(matcher, oracle, fam, d[0], d[1], [ch.MatchConfig(hamming_threshold=tau // 2),
+                                                     ch.MatchConfig(hamming_threshold=params.long_bits, top_k=7)])
+
+
+def test_edge_cases(matcher, oracle, default_family):
+    fresh(matcher, default_family)
+    d = make_dataset(2, 300, seed=61)
+    empty = np.zeros((0, 128), np.uint8)
+    cfg = [ch.MatchConfig()]
+    assert len(run_pair_case(matcher, oracle, default_family, d[0], empty, cfg)) == 0      # fsJ empty
+    assert len(run_pair_case(matcher, oracle, default_family, empty, d[1], cfg)) == 0
+    assert len(run_pair_case(matcher, oracle, default_family, d[0], d[1][:1], cfg)) == 0   # ratio undecidable
+    # exact duplicates: second distance 0 -> rejection; duplicated + distinct rows mixed
+    dup = np.repeat(d[0][:40], 3, axis=0)
+    run_pair_case(matcher, oracle, default_family, d[0][:40], dup, cfg)
+    run_pair_case(matcher, oracle, default_family, dup, dup, cfg)
+    # image matched against itself (every query has a zero-distance twin)
+    run_pair_case(matcher, oracle, default_family, d[0], d[0], cfg)
+    # sizes around warp / tile boundaries
+    for n_i, n_j in ((1, 300), (31, 33), (32, 64), (33, 65), (255, 257)):
+        run_pair_case(matcher, oracle, default_family, d[0][:n_i], d[1][:n_j], cfg)
+
+
+def test_errors_follow_the_reference(matcher, default_family):
+    fresh(matcher, default_family)
+    d = make_dataset(1, 64, seed=1)[0]
+    put(matcher, BASE, d)
+    put(matcher, BASE + 1, d)
+    with pytest.raises(ch.LogicError):          # codes not computed
+        matcher.match_pairs([(BASE, BASE + 1)], ch.MatchConfig())
+    m2 = ch.Matcher(0)
+    try:
+        m2.set_family(default_family)
+        m2.upload(1, d)
+        with pytest.raises(ch.LogicError):      # hashing.cpp:131-132 centering not set
+            m2.hash([1])
+        with pytest.raises(ValueError):         # hashing.hpp:28-29
+            m2.set_centering(np.zeros(128))
+            m2.hash([1], 8)
+        with pytest.raises(ValueError):         # hashing.cpp:60 empty stream
+            m2.centering_reset()
+            m2.centering_apply()
+    finally:
+        m2.close()
+    matcher.set_centering(np.full(128, 127.5))
+    matcher.hash([BASE, BASE + 1])
+    for bad in (ch.MatchConfig(top_k=1), ch.MatchConfig(hamming_threshold=129), ch.MatchConfig(ratio=1.0),
+                ch.MatchConfig(ratio=0.0), ch.MatchConfig(reduce_rounds=8), ch.MatchConfig(reduce_rounds=-1)):
+        with pytest.raises(ValueError):         # matcher.cpp:9-17
+            matcher.match_pairs([(BASE, BASE + 1)], bad)
+    with pytest.raises(ch.UnsupportedError):
+        matcher.match_pairs([(BASE, BASE + 1)], ch.MatchConfig(top_k=33))
+    with pytest.raises(KeyError):
+        matcher.match_pairs([(BASE, 999999)], ch.MatchConfig())
+    with pytest.raises(ch.UnsupportedError):
+        matcher.upload(BASE + 2, np.zeros((65537, 128), np.uint8))
+    m3 = ch.Matcher(0)
+    try:
+        with pytest.raises(ch.UnsupportedError):
+            m3.set_family(ch.build_hash_family(ch.FamilyParams(short_bits=13)))
+        with pytest.raises(ch.UnsupportedError):
+            m3.set_family(ch.build_hash_family(ch.FamilyParams(table_count=9)))
+    finally:
+        m3.close()
+
+
+# ---- descriptor load -------------------------------------------------------------------------------
+def chft_blob(desc, kp, version=1, magic=b"CHFT"):
+    n = len(desc)
+    out = bytearray(magic + struct.pack("<III", version, n, 0))
+    for i in range(n):
+        out += kp[i].astype("<f4").tobytes() + desc[i].tobytes()
+    return bytes(out)
+
+
+def test_chft_load_and_faults(matcher, oracle, default_family):
+    fresh(matcher, default_family)
+    d = make_dataset(1, 1234, seed=71)[0]
+    kp = np.random.default_rng(0).normal(size=(1234, 4)).astype(np.float32)
+    blob = chft_blob(d, kp)
+    assert len(blob) == 16 + 1234 * 144                     # feature_io.hpp:88-89
+    assert matcher.upload_chft(BASE, blob) == 1234
+    matcher._test_ids.add(BASE)
+    got_d, got_kp = matcher.descriptors(BASE)
+    assert np.array_equal(got_d, d) and np.array_equal(got_kp, kp)
+    # trailing bytes are ignored like the stream reader does; empty files are valid
+    assert matcher.upload_chft(BASE, blob + b"xx") == 1234
+    assert matcher.upload_chft(BASE + 1, chft_blob(d[:0], kp[:0])) == 0
+    matcher._test_ids.add(BASE + 1)
+    assert matcher.points(BASE + 1) == 0
+    # the loaded image hashes and matches like an uploaded one
+    put(matcher, BASE + 2, d)
+    cen = oracle.centering([d])
+    matcher.set_centering(cen)
+    matcher.hash([BASE, BASE + 2])
+    a, b = matcher.codes(BASE), matcher.codes(BASE + 2)
+    assert np.array_equal(a.shorts, b.shorts) and np.array_equal(a.longs, b.longs)
+    # fault classes and byte offsets of parse_features_blob (engine.cpp:458-472)
+    for bad, fault, off in ((blob[:10], "Truncated", 10), (b"XHFT" + blob[4:], "BadMagic", 0),
+                            (chft_blob(d, kp, version=2), "BadVersion", 4), (blob[:5000], "Truncated", 5000)):
+        with pytest.raises(ch.FeatureFileError) as ei:
+            matcher.upload_chft(BASE + 3, bad)
+        assert ei.value.fault == fault and ei.value.byte_offset == off
+
+
+def test_external_codes_round_trip(matcher, oracle, default_family):
+    """Codes computed elsewhere (a CHCC cache, the CPU reference) can be installed and matched."""
+    fresh(matcher, default_family)
+    d = make_dataset(2, 1500, seed=81)
+    cen = oracle.centering(list(d))
+    ci = oracle_codes(oracle, default_family, cen, d[0])
+    cj = oracle_codes(oracle, default_family, cen, d[1])
+    put(matcher, BASE, d[0])
+    put(matcher, BASE + 1, d[1])
+    matcher.upload_codes(BASE, ch.ImageCodes(default_family.params, *ci))
+    matcher.upload_codes(BASE + 1, ch.ImageCodes(default_family.params, *cj))
+    want, _ = oracle.match_pair(default_family.params, ch.MatchConfig(), d[0], *ci, d[1], *cj)
+    _, rec, _ = matcher.match_pairs([(BASE, BASE + 1)], ch.MatchConfig())
+    assert np.array_equal(rec, want)
+    with pytest.raises(ValueError):
+        bad = ci[0].copy()
+        bad[0, 0] = 256
+        matcher.upload_codes(BASE, ch.ImageCodes(default_family.params, bad, ci[1]))
+
+
+# ---- pair lists, batching, sinks ---------------------------------------------------------------------
+def test_pair_list_batching_is_invariant(matcher, oracle, default_family):
+    """SPEC criterion 8 (worker invariance): results do not depend on how the pair list is cut
+    into sub-batches, shards or work units; sink delivery is in pair order."""
+    fresh(matcher, default_family)
+    k, n = 12, 1000
+    d = make_dataset(k, n, seed=91)
+    cen = oracle.centering(list(d))
+    matcher.set_centering(cen)
+    for i in range(k):
+        put(matcher, BASE + i, d[i])
+    matcher.hash([BASE + i for i in range(k)])
+    pairs = ch.plan_exhaustive(k, 3, 2) + BASE
+    cfg = ch.MatchConfig()
+    offs, rec, stats = matcher.match_pairs(pairs, cfg)
+    assert stats["pairs"] == 66 and stats["match_launches"] == 1
+    # oracle on a few pairs of the list
+    codes = [oracle_codes(oracle, default_family, cen, d[i]) for i in range(k)]
+    for idx in (0, 17, 65):
+        a, b = int(pairs[idx, 0]) - BASE, int(pairs[idx, 1]) - BASE
+        want, _ = oracle.match_pair(default_family.params, cfg, d[a], *codes[a], d[b], *codes[b])
+        assert np.array_equal(rec[offs[idx]:offs[idx + 1]], want)
+    # many small sub-batches, delivered through the sink
+    matcher.set_sub_batch_queries(5 * n)
+    chunks = []
+    st2 = matcher.match_pairs_stream(pairs, cfg, lambda first, o, r: chunks.append((first, o.copy(), r.copy())))
+    assert st2["match_launches"] == 14 and [c[0] for c in chunks] == list(range(0, 66, 5))
+    cat = np.concatenate([c[2] for c in chunks])
+    assert np.array_equal(cat, rec)
+    for first, o, r in chunks:
+        assert np.array_equal(o + offs[first], offs[first:first + len(o)])
+    offs3, rec3, st3 = matcher.match_pairs(pairs, cfg)
+    assert np.array_equal(offs3, offs) and np.array_equal(rec3, rec) and st3["match_launches"] == 14
+    matcher.set_sub_batch_queries(0)
+    # shards of the list (the multi-GPU split) concatenate to the whole
+    parts = []
+    for r in range(3):
+        a, b = ch.shard_range(len(pairs), r, 3)
+        parts.append(matcher.match_pairs(pairs[a:b], cfg)[1])
+    assert np.array_equal(np.concatenate(parts), rec)
+    # device-resident run reports the same counters and checksum
+    st4 = matcher.match_pairs_device(pairs, cfg)
+    assert st4["matches"] == len(rec) and st4["records_checksum"] == host_checksum(offs, rec)
+    assert st4["raw_candidates"] == stats["raw_candidates"] and st4["distances"] == stats["distances"]
+    # capacity too small -> ENOMEM with the required size, offsets still complete
+    with pytest.raises(MemoryError):
+        matcher.match_pairs(pairs, cfg, capacity=10)
+
+
+def test_config2_properties_full_size(matcher, default_family):
+    """BASELINE config 2 (100 images x 4,096 descriptors, 4,950 pairs) through the pair-list path;
+    checked with properties that need no oracle run."""
+    fresh(matcher, default_family)
+    k, n = 100, 4096
+    d = make_dataset(k, n, seed=7)
+    for i in range(k):
+        put(matcher, BASE + i, d[i])
+    matcher.centering_reset()
+    for i in range(k):
+        matcher.centering_add(BASE + i)
+    cen = matcher.centering_apply()
+    assert np.array_equal(cen, d.reshape(-1, 128).astype(np.uint64).sum(0).astype(np.float64) / (k * n))
+    matcher.hash([BASE + i for i in range(k)])
+    pairs = ch.plan_exhaustive(k, 10, 4) + BASE
+    cfg = ch.MatchConfig()
+    offs, rec, stats = matcher.match_pairs(pairs, cfg)
+    assert stats["pairs"] == 4950 and len(offs) == 4951 and offs[-1] == len(rec) == stats["matches"]
+    # ascending query index inside every pair, at most one record per query (matcher.hpp:96-97)
+    seg = np.repeat(np.arange(4950), np.diff(offs).astype(np.int64))
+    same = seg[1:] == seg[:-1]
+    assert (np.diff(rec["query_index"].astype(np.int64))[same] > 0).all()
+    assert rec["query_index"].max() < n and rec["train_index"].max() < n
+    # every record's distance is the exact squared distance of the two descriptors it names
+    pick = np.random.default_rng(0).choice(len(rec), 20000, replace=False)
+    pa, pb = pairs[seg[pick], 0] - BASE, pairs[seg[pick], 1] - BASE
+    qa = d[pa, rec["query_index"][pick]].astype(np.int64)
+    tb = d[pb, rec["train_index"][pick]].astype(np.int64)
+    assert np.array_equal(((qa - tb) ** 2).sum(1).astype(np.float64), rec["distance_sq"][pick])
+    # twins (slot s in both images) dominate: recall of the planted correspondences
+    twins = int(np.ceil(0.3 * n))
+    planted = rec["query_index"] == rec["train_index"]
+    assert (rec["query_index"][planted] < twins).all()
+    assert planted.sum() / (4950 * twins) > 0.90 and planted.mean() > 0.99
+    # checksum of checksums: device-only path and host delivery agree
+    st2 = matcher.match_pairs_device(pairs, cfg)
+    assert st2["records_checksum"] == host_checksum(offs, rec) and st2["matches"] == len(rec)
+    # swapping query and train image is a different computation with a consistent answer
+    a, b = int(pairs[0, 0]), int(pairs[0, 1])
+    _, r_ab, _ = matcher.match_pairs([(a, b)], cfg)
+    _, r_ba, _ = matcher.match_pairs([(b, a)], cfg)
+    ab = set(zip(r_ab["query_index"].tolist(), r_ab["train_index"].tolist()))
+    ba = set(zip(r_ba["train_index"].tolist(), r_ba["query_index"].tolist()))
+    assert len(ab & ba) > 0.9 * min(len(ab), len(ba))
+
+
+def test_save_matches_from_device_results(matcher, oracle, default_family, tmp_path):
+    fresh(matcher, default_family)
+    d = make_dataset(2, 500, seed=101)
+    want = run_pair_case(matcher, oracle, default_family, d[0], d[1], [ch.MatchConfig()])
+    _, rec, _ = matcher.match_pairs([(BASE, BASE + 1)], ch.MatchConfig())
+    ch.save_matches("a", "b", rec, tmp_path / ch.pair_file_name(0, 1))
+    oracle.save_matches("a", "b", want, tmp_path / "want.txt")
+    assert (tmp_path / "match_000000_000001.txt").read_bytes() == (tmp_path / "want.txt").read_bytes()

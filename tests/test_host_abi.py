@@ -1,0 +1,116 @@
+"""CPU suite for the product's host side: the C-ABI library loads, exports every symbol the
+header declares, and its host-only entry points (family generation, pair planning, match-file
+output, sharding) agree with the oracle / golden vectors.  No device compute is called here."""
+import hashlib
+import re
+import tempfile
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1805_08995_b200 as ch
+from paper_1805_08995_b200 import _native as N
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_library_exports_every_declared_symbol():
+    header = (ROOT / "include" / "chgpu.h").read_text()
+    declared = set(re.findall(r"\b(chgpu_[a-z0-9_]+)\s*\(", header))
+    declared -= {"chgpu_sink_fn"}
+    lib = N.load()
+    missing = [s for s in sorted(declared) if not hasattr(lib, s)]
+    assert not missing, f"libchgpu.so does not export {missing}"
+    unbound = sorted(declared - set(N.SIGNATURES))
+    assert not unbound, f"_native.SIGNATURES lacks {unbound}"
+    assert len(declared) >= 30
+
+
+def test_record_layout_is_the_reference_layout():
+    import ctypes as C
+    assert C.sizeof(N.MatchRecordC) == 16 and N.MatchRecordC.distance_sq.offset == 8   # feature_io.hpp:51-57
+    assert ch.RECORD_DTYPE.itemsize == 16
+
+
+def test_no_device_means_loud_failure():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(ch.CudaError):
+        ch.Matcher(0)
+
+
+def test_family_generate_matches_golden_and_oracle(restatement, golden):
+    g = golden["family"]
+    for tag, params in {"default": ch.FamilyParams(), "m10_n96_L4_s99": ch.FamilyParams(10, 96, 4, 99)}.items():
+        fam = ch.build_hash_family(params)
+        assert sha(fam.short_planes) == str(g[tag + "_short_sha"])
+        assert sha(fam.long_planes) == str(g[tag + "_long_sha"])
+        sp, lp = restatement.build_family(params)
+        assert np.array_equal(fam.short_planes, sp) and np.array_equal(fam.long_planes, lp)
+    for bad in (ch.FamilyParams(short_bits=0), ch.FamilyParams(long_bits=8), ch.FamilyParams(long_bits=129),
+                ch.FamilyParams(table_count=0)):
+        with pytest.raises(ValueError):
+            ch.build_hash_family(bad)
+
+
+def test_plan_exhaustive_matches_golden_and_oracle(restatement, golden):
+    g = golden["plans"]
+    for (k, np_, m) in ((10, 3, 2), (7, 2, 2), (12, 5, 1), (9, 1, 4), (5, 8, 3)):
+        assert np.array_equal(ch.plan_exhaustive(k, np_, m), g[f"pairs_{k}_{np_}_{m}"])
+    for k in (1, 2, 6, 17, 40):
+        for np_ in (1, 3, 4):
+            for m in (1, 2, 5):
+                assert np.array_equal(ch.plan_exhaustive(k, np_, m).reshape(-1, 2),
+                                      restatement.plan_exhaustive(k, np_, m)[0].reshape(-1, 2))
+    with pytest.raises(ValueError):
+        ch.plan_exhaustive(0, 1, 1)
+
+
+def test_plan_properties_at_baseline_size():
+    # config 3: 1,000 images -> 499,500 pairs, every unordered pair exactly once, first < second
+    pairs = ch.plan_exhaustive(1000, 50, 4)
+    assert pairs.shape == (499500, 2) and (pairs[:, 0] < pairs[:, 1]).all()
+    key = pairs[:, 0].astype(np.int64) * 1000 + pairs[:, 1]
+    assert len(np.unique(key)) == 499500
+
+
+def test_shard_range_partitions():
+    for n in (0, 1, 7, 499500):
+        for world in (1, 2, 3, 8):
+            spans = [ch.shard_range(n, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_save_matches_is_byte_identical(golden, restatement):
+    g = golden["small_dataset"]
+    rec = g["rec_default_01"]
+    with tempfile.TemporaryDirectory() as td:
+        p = Path(td) / "m.txt"
+        ch.save_matches("img_a", "img_b", rec, p)
+        assert p.read_bytes() == g["match_text_default_01"].tobytes()
+        # non-integer and extreme doubles print as the shortest round-trip decimal
+        odd = np.zeros(4, dtype=ch.RECORD_DTYPE)
+        odd["query_index"] = [0, 1, 2, 4294967295]
+        odd["train_index"] = [5, 6, 7, 8]
+        odd["distance_sq"] = [0.1, 1e22, 8323200.0, 2.5e-7]
+        q = Path(td) / "odd.txt"
+        ch.save_matches("a", "b", odd, q)
+        r = Path(td) / "odd_ref.txt"
+        restatement.save_matches("a", "b", odd, r)
+        assert q.read_bytes() == r.read_bytes()
+        empty = Path(td) / "e.txt"
+        ch.save_matches("x", "y", odd[:0], empty)
+        assert empty.read_bytes() == b"# x y 0\n"
+        with pytest.raises(ch.FeatureFileError):
+            ch.save_matches("x", "y", odd, Path(td) / "no_such_dir" / "f.txt")
+    assert ch.pair_file_name(3, 41) == "match_000003_000041.txt"      # engine.cpp:724-728
+    assert ch.pair_file_name(1234567, 2) == "match_1234567_000002.txt"
