@@ -22,8 +22,11 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-O3", "-std=c++17",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
-    "-shared",
 ]
+
+# translation units of libchgpu.so; the match kernel's variants are split so they compile in parallel
+CHGPU_UNITS = ["chgpu.cu", "match_smem.cu", "match_global.cu", "host_util.cpp"]
+CHGPU_HEADERS = ["dev_types.cuh", "hash_kernels.cuh", "match_kernels.cuh", "match_launch.cuh", "compact_kernels.cuh"]
 
 
 def _nvcc() -> str:
@@ -41,15 +44,29 @@ def _stale(target: Path, sources: list[Path]) -> bool:
 
 
 def build_chgpu(force: bool = False, verbose: bool = False) -> Path:
+    from concurrent.futures import ThreadPoolExecutor
+
     target = PKG / "libchgpu.so"
-    sources = [CSRC / "chgpu.cu", CSRC / "host_util.cpp"]
-    deps = sources + [CSRC / "dev_types.cuh", CSRC / "hash_kernels.cuh", CSRC / "match_kernels.cuh",
-                      ROOT / "include" / "chgpu.h"]
-    if force or _stale(target, deps):
-        cmd = [_nvcc(), *NVCC_FLAGS, "-o", str(target), *map(str, sources)]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-        subprocess.run(cmd, check=True, cwd=str(CSRC))
+    headers = [CSRC / h for h in CHGPU_HEADERS] + [ROOT / "include" / "chgpu.h"]
+    objdir = CSRC / "_obj"
+    objdir.mkdir(exist_ok=True)
+    nvcc = _nvcc()
+
+    def compile_unit(name: str) -> Path:
+        src = CSRC / name
+        obj = objdir / (src.stem + ".o")
+        if force or _stale(obj, [src, *headers]):
+            cmd = [nvcc, *NVCC_FLAGS, *os.environ.get("CHGPU_NVCC_EXTRA", "").split(), "-c", "-o", str(obj), str(src)]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            subprocess.run(cmd, check=True, cwd=str(CSRC))
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(CHGPU_UNITS)) as ex:
+        objs = list(ex.map(compile_unit, CHGPU_UNITS))
+    if force or _stale(target, objs):
+        subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(target),
+                        *map(str, objs)], check=True, cwd=str(CSRC))
     return target
 
 

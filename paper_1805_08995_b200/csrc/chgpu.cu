@@ -26,7 +26,8 @@
 
 #include "dev_types.cuh"
 #include "hash_kernels.cuh"
-#include "match_kernels.cuh"
+#include "compact_kernels.cuh"
+#include "match_launch.cuh"
 
 using namespace chgpu;
 
@@ -190,6 +191,7 @@ size_t image_block_bytes(uint32_t n, uint32_t m, uint32_t L, size_t off[6]) {
     off[3] = o; o += align_up(size_t(n) * L * 4);
     off[4] = o; o += align_up(size_t(L) * ((size_t(1) << m) + 1) * 4);
     off[5] = o; o += align_up(size_t(L) * n * 2);
+    o += kAlign;  // slack: the match kernel may read one id past an empty last bucket
     return std::max(o, kAlign);
 }
 
@@ -365,37 +367,27 @@ bool cfg_valid(const chgpu_match_cfg& c, uint32_t long_bits, const char** why) {
     return true;
 }
 
-template <bool SMEM, int LT>
-cudaError_t launch_match_variant(chgpu_ctx* ctx, const MatchParams& P, size_t smem, uint32_t* grid_out) {
-    auto kfn = match_kernel<SMEM, LT>;
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kMatchThreads, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorLaunchOutOfResources;
-    const uint32_t grid = std::min<uint32_t>(P.nunits, uint32_t(per_sm) * ctx->prop.multiProcessorCount);
-    *grid_out = grid;
-    kfn<<<grid, kMatchThreads, smem, ctx->compute>>>(P);
-    return cudaGetLastError();
+size_t offs_smem_bytes(const chgpu_ctx* ctx) {
+    // dense bucket offsets of one image, rounded up to the 16-byte granule of cp.async.bulk
+    return (size_t(ctx->fam.table_count) * ((size_t(1) << ctx->fam.short_bits) + 1) * 4 + 15) & ~size_t(15);
 }
 
-cudaError_t launch_match(chgpu_ctx* ctx, const MatchParams& P, bool smem_train, uint32_t max_nt, uint32_t* grid) {
-    const size_t smem = smem_train ? std::max<size_t>(size_t(max_nt) * 16, 16) : 16;
-    const uint32_t L = P.L;
+cudaError_t launch_match(chgpu_ctx* ctx, MatchParams& P, bool smem_train, uint32_t max_nt, uint32_t* grid) {
+    const int sms = ctx->prop.multiProcessorCount;
     if (smem_train) {
-        if (L <= 4) return launch_match_variant<true, 4>(ctx, P, smem, grid);
-        if (L <= 6) return launch_match_variant<true, 6>(ctx, P, smem, grid);
-        return launch_match_variant<true, 8>(ctx, P, smem, grid);
+        P.smem_long_bytes = std::max<uint32_t>(max_nt * 16u, 16u);
+        return launch_match_smem(P, size_t(P.smem_long_bytes) + offs_smem_bytes(ctx), sms, ctx->compute, grid);
     }
-    if (L <= 4) return launch_match_variant<false, 4>(ctx, P, smem, grid);
-    if (L <= 6) return launch_match_variant<false, 6>(ctx, P, smem, grid);
-    return launch_match_variant<false, 8>(ctx, P, smem, grid);
+    P.smem_long_bytes = 0;
+    return launch_match_global(P, 16, sms, ctx->compute, grid);
 }
 
 size_t smem_train_capacity(const chgpu_ctx* ctx) {
-    // dynamic smem available to a 1-CTA/SM launch, minus the kernel's static 16 B and 1 KiB reserve
-    return (ctx->prop.sharedMemPerBlockOptin - 1024 - 64) / 16;
+    // points whose codes fit next to the bucket offsets in the dynamic smem of a 1-CTA/SM launch
+    // (minus the kernel's static 16 B and the 1 KiB the driver reserves per block)
+    const size_t avail = ctx->prop.sharedMemPerBlockOptin - 1024 - 64;
+    const size_t offs = offs_smem_bytes(ctx);
+    return avail > offs ? (avail - offs) / 16 : 0;
 }
 
 enum class SinkMode { Host, Stream, Device };

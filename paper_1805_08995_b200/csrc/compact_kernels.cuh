@@ -1,0 +1,102 @@
+// compact_kernels.cuh — per-pair record offsets and the ordered compaction of the match
+// kernel's per-query scratch into the reference's MatchRecord stream.
+#pragma once
+
+#include "dev_types.cuh"
+
+namespace chgpu {
+
+// Exclusive scan of per-pair match counts -> record offsets (one CTA; npairs is a sub-batch).
+__global__ void scan_counts_kernel(const uint32_t* __restrict__ counts, uint32_t npairs,
+                                   unsigned long long* __restrict__ offsets /* npairs + 1 */,
+                                   DevStats* stats) {
+    __shared__ unsigned long long s_warp[32];
+    __shared__ unsigned long long s_carry;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < npairs; base += blockDim.x) {
+        const uint32_t i = base + tid;
+        const unsigned long long v = i < npairs ? counts[i] : 0;
+        unsigned long long incl = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, d);
+            if (int(lane) >= d) incl += u;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned long long w = lane < (blockDim.x >> 5) ? s_warp[lane] : 0;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned long long u = __shfl_up_sync(0xffffffffu, w, d);
+                if (int(lane) >= d) w += u;
+            }
+            s_warp[lane] = w;  // inclusive over warps
+        }
+        __syncthreads();
+        const unsigned long long before = s_carry + (warp ? s_warp[warp - 1] : 0);
+        if (i < npairs) offsets[i] = before + incl - v;
+        __syncthreads();
+        if (tid == blockDim.x - 1) s_carry = before + incl;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        offsets[npairs] = s_carry;
+        atomicAdd(&stats->matches, s_carry);
+    }
+}
+
+__device__ __forceinline__ unsigned long long mix64_dev(unsigned long long x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+// One CTA per pair: ordered compaction of the per-query scratch into MatchRecord{u32 q, u32 t, f64 d^2}
+// (feature_io.hpp:51-57), ascending q, at most one per query (matcher.cpp:191-192).
+__global__ void compact_kernel(const PairDesc* __restrict__ pairs, const DevImage* __restrict__ images,
+                               const uint2* __restrict__ res, const unsigned long long* __restrict__ offsets,
+                               uint4* __restrict__ records, uint32_t first_pair_global, DevStats* stats) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_base;
+    const uint32_t pair = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const PairDesc pd = pairs[pair];
+    const uint32_t nq = images[pd.slot_i].n;
+    if (tid == 0) s_base = 0;
+    __syncthreads();
+    uint4* out = records + offsets[pair];
+    unsigned long long csum = 0;
+    for (uint32_t q0 = 0; q0 < nq; q0 += blockDim.x) {
+        const uint32_t q = q0 + tid;
+        uint2 r = make_uint2(kNone, 0);
+        if (q < nq) r = res[pd.res_off + q];
+        const bool hit = r.x != kNone;
+        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+        if (lane == 0) s_warp[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t before = s_base;
+        for (uint32_t w = 0; w < warp; ++w) before += s_warp[w];
+        if (hit) {
+            const uint32_t pos = before + __popc(bal & ((1u << lane) - 1u));
+            const unsigned long long db = (unsigned long long)__double_as_longlong(double(r.y));
+            out[pos] = make_uint4(q, r.x, uint32_t(db), uint32_t(db >> 32));
+            csum += mix64_dev(mix64_dev((unsigned long long)(first_pair_global + pair) << 32 | q) ^
+                              ((unsigned long long)r.x << 32 | r.y));
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t tot = 0;
+            for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) tot += s_warp[w];
+            s_base += tot;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, d);
+    if (lane == 0 && csum) atomicAdd(&stats->checksum, csum);
+}
+
+}  // namespace chgpu

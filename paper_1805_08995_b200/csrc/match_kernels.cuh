@@ -1,23 +1,31 @@
 // match_kernels.cuh — K3 (pair matching) and the ordered compaction of its results.
 //
 // K3 is a persistent kernel: one CTA per SM pulls work units (pair, query range) from a global
-// counter.  For each unit the train image's 128-bit codes are brought into shared memory with
-// one bulk async copy (cp.async.bulk + mbarrier, the sm_90+/sm_100 TMA path), then every warp
-// owns one query point at a time:
+// counter.  For each unit the train image's 128-bit codes and its dense bucket offsets are
+// brought into shared memory with bulk async copies (cp.async.bulk + mbarrier, the sm_90+/sm_100
+// TMA path), then every warp owns one query point at a time:
 //
-//   1. bucket lookup   : lanes t < L read the query's table-t code and the two CSR offsets of
-//                        that bucket in the train image; a warp scan flattens the L buckets
-//                        into one index space [0, R)                     (matcher.cpp:164-169)
-//   2. Hamming scan    : lane l evaluates raw candidates l, l+32, ...; key = distance<<24 | id
-//                        (train code gathered from shared memory, 4x LOP3 + 4x POPC)
-//                                                                         (matcher.cpp:68-84)
+//   1. bucket lookup   : the query's L table codes are warp-uniform; each selects one CSR range
+//                        [lo, lo+len) of the train image's bucket index      (matcher.cpp:164-169)
+//   2. Hamming scan    : 32 candidates per step, one per lane: id = points[...], train code
+//                        gathered from shared memory, 4x LOP3 + 4x POPC,
+//                        key = distance<<24 | id                              (matcher.cpp:68-84)
+//                        Step t covers the first 32 entries of table t's bucket (no index
+//                        arithmetic beyond one add); the entries past 32 of all buckets are
+//                        flattened into kOverSlots further steps.  All steps are
+//                        straight-line code, so their loads overlap.  Queries whose buckets
+//                        overflow that (large images) take rounds of 32 entries per table: a
+//                        first pass keeps only the smallest key, and only queries with a
+//                        candidate within tau pay for a second, merging pass.
 //   3. ranking         : the ranked list is the first n keys in ascending (distance, id) order
 //                        with EQUAL KEYS COLLAPSED — the same point reached through several
 //                        tables has the same key, so the reference's sort+unique
-//                        (matcher.cpp:170-171) is implicit.  Keys are pulled one at a time with
-//                        a warp-wide REDUX.MIN over "keys greater than the previous one"; the
-//                        threshold tau and the re-rank fallback (matcher.cpp:176-189) only
-//                        decide where the pulling stops, so no histogram has to be stored.
+//                        (matcher.cpp:170-171) is implicit.  Keys are pulled one at a time:
+//                        every lane folds its slots with min(acc, key - (prev+1)) (one
+//                        VIADDMNMX per slot; keys <= prev wrap to the top of the u32 range) and
+//                        a warp-wide REDUX.MIN picks the winner.  The threshold tau and the
+//                        re-rank fallback (matcher.cpp:176-189) only decide where the pulling
+//                        stops, so no histogram has to be stored.
 //   4. verification    : 8 lanes per candidate row, __vabsdiffu4 + __dp4a (exact u32 squared
 //                        distance), best / second with rank-order tie-break, Lowe ratio in
 //                        fp64 exactly as matcher.cpp:115-137.
@@ -31,7 +39,7 @@
 namespace chgpu {
 
 constexpr int kMatchThreads = 1024;
-constexpr int kKeySlots = 10;  // 320 raw candidates per pass (max observed 309 at N=8192, L=6, m=8)
+constexpr int kOverSlots = 2;  // register slots for bucket entries past the first 32 of every table
 
 struct MatchParams {
     const DevImage* images;
@@ -44,6 +52,7 @@ struct MatchParams {
     uint32_t chunks_per_pair;
     uint32_t m, L;
     uint32_t top_k, tau, min_ranked, long_bits;
+    uint32_t smem_long_bytes;   // SMEM_TRAIN: bytes reserved for the train codes (offsets follow)
     double ratio_sq;            // cfg.ratio * cfg.ratio, formed on the host in fp64
     uint32_t* dbg_ranked;       // optional: n_i x top_k
     uint32_t* dbg_count;        // optional: n_i
@@ -80,9 +89,40 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_addr(bar))
                  : "memory");
 }
+// Shared-memory loads by 32-bit shared-window address (keeps the address arithmetic to one LEA).
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint2 lds64x(uint32_t addr) {  // two adjacent u32 (need not be 8-byte aligned)
+    uint2 v;
+    asm volatile("ld.shared.u32 %0, [%2];\n\tld.shared.u32 %1, [%2+4];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+
+// Read-once global loads that must not displace the train image's bucket lists from L1.
+__device__ __forceinline__ uint4 ldg_stream128(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldg_stream32(const void* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
 
 __device__ __forceinline__ uint32_t hamming128(const uint4& a, const uint4& b) {
+#ifdef CHGPU_CSA_POPC
+    // carry-save adder over three of the four xor words: 3 POPC + 2 LOP3 instead of 4 POPC
+    const uint32_t x = a.x ^ b.x, y = a.y ^ b.y, z = a.z ^ b.z, w = a.w ^ b.w;
+    const uint32_t s = x ^ y ^ z, c = (x & y) | (z & (x ^ y));
+    return __popc(s) + __popc(w) + 2u * __popc(c);
+#else
     return __popc(a.x ^ b.x) + __popc(a.y ^ b.y) + __popc(a.z ^ b.z) + __popc(a.w ^ b.w);
+#endif
 }
 
 // Sum over 4 byte lanes of (a_i - b_i)^2, exact in u32.
@@ -91,30 +131,61 @@ __device__ __forceinline__ uint32_t sqdiff4(uint32_t a, uint32_t b) {
     return __dp4a(ad, ad, 0u);
 }
 
-// Smallest key strictly greater than `prev` over the warp's key slots (+ one extra slot).
+// Warp-wide smallest key over all slots (+ one extra value).
 template <int SLOTS>
-__device__ __forceinline__ uint32_t next_key(const uint32_t (&key)[SLOTS], uint32_t extra, uint32_t prev,
-                                             bool first) {
-    uint32_t lmin = kNone;
+__device__ __forceinline__ uint32_t first_key(const uint32_t (&key)[SLOTS], uint32_t extra) {
+    uint32_t lmin = extra;
 #pragma unroll
-    for (int i = 0; i < SLOTS; ++i) {
-        const uint32_t k = key[i];
-        if (first || k > prev) lmin = min(lmin, k);
-    }
-    if (first || extra > prev) lmin = min(lmin, extra);
+    for (int i = 0; i < SLOTS; ++i) lmin = min(lmin, key[i]);
     return __reduce_min_sync(0xffffffffu, lmin);
 }
 
-template <bool SMEM_TRAIN, int LT>
+// Warp-wide smallest key strictly greater than `prev`, or kNone when there is none.
+// key - (prev + 1) in u32 arithmetic: keys <= prev (and empty kNone slots) wrap to values
+// >= kNone - prev - 1, which no key > prev can reach (valid keys are < 2^31 + 2^24).
+template <int SLOTS>
+__device__ __forceinline__ uint32_t next_key(const uint32_t (&key)[SLOTS], uint32_t extra, uint32_t prev) {
+    const uint32_t nb = ~prev;  // -(prev + 1)
+    uint32_t acc = extra + nb;
+#pragma unroll
+    for (int i = 0; i < SLOTS; ++i) acc = min(acc, key[i] + nb);
+    const uint32_t g = __reduce_min_sync(0xffffffffu, acc);
+    return g >= nb - 1u ? kNone : g - nb;
+}
+
+// One step of the Hamming scan: candidate `first + lane` of the bucket-major id list, clamped
+// to `last` (lanes past the end re-evaluate the last candidate: equal keys collapse).
+template <bool SMEM_TRAIN>
+__device__ __forceinline__ uint32_t scan_step(const uint16_t* __restrict__ pts, uint32_t first, uint32_t last,
+                                              uint32_t lane, const uint4& ql, uint32_t s_long,
+                                              const uint4* __restrict__ g_long) {
+    const uint32_t p = min(first + lane, last);
+    const uint32_t id = __ldg(pts + p);
+    uint4 c;
+    if (SMEM_TRAIN) c = lds128(s_long + id * 16u);
+    else c = __ldg(g_long + id);
+    return (hamming128(c, ql) << 24) | id;
+}
+
+// LT = number of table slots unrolled in registers (>= L); EXACT: L == LT, no per-table guards.
+template <bool SMEM_TRAIN, int LT, bool EXACT>
 __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchParams P) {
-    extern __shared__ __align__(16) uint4 s_long[];
+    extern __shared__ __align__(16) unsigned char s_raw[];  // [train codes | bucket offsets]
     __shared__ unsigned int s_unit;
     __shared__ __align__(8) uint64_t s_bar;
 
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int KS = LT + kOverSlots;
     constexpr uint32_t kWarps = kMatchThreads / 32;
     constexpr uint32_t FULL = 0xffffffffu;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t nb1 = (1u << P.m) + 1;
+    const uint32_t L = EXACT ? uint32_t(LT) : P.L;
+    // shared-window addresses, pinned in registers (the compiler would otherwise re-derive
+    // them from SR_CgaCtaId in front of every gather)
+    uint32_t s_long = smem_addr(s_raw);
+    asm volatile("" : "+r"(s_long));
+    uint32_t s_offs = s_long + P.smem_long_bytes;
+    asm volatile("" : "+r"(s_offs));
 
     if (SMEM_TRAIN && tid == 0) {
         mbar_init(&s_bar, 1);
@@ -123,7 +194,6 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
     uint32_t bar_parity = 0;
     uint32_t resident = kNone;
 
-    // per-warp statistics, flushed once per unit
     for (;;) {
         if (tid == 0) s_unit = atomicAdd(P.unit_counter, 1u);
         __syncthreads();
@@ -140,10 +210,14 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                 // order them before the async-proxy writes.
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 const uint32_t bytes = J.n * 16u;
-                mbar_expect_tx(&s_bar, bytes);
+                const uint32_t obytes = (L * nb1 * 4u + 15u) & ~15u;  // the arena pads every array to 256 B
+                mbar_expect_tx(&s_bar, bytes + obytes);
                 for (uint32_t off = 0; off < bytes; off += 65536u)
-                    bulk_g2s(reinterpret_cast<unsigned char*>(s_long) + off,
-                             reinterpret_cast<const unsigned char*>(J.longs) + off, min(65536u, bytes - off), &s_bar);
+                    bulk_g2s(s_raw + off, reinterpret_cast<const unsigned char*>(J.longs) + off,
+                             min(65536u, bytes - off), &s_bar);
+                for (uint32_t off = 0; off < obytes; off += 65536u)
+                    bulk_g2s(s_raw + P.smem_long_bytes + off, reinterpret_cast<const unsigned char*>(J.offs) + off,
+                             min(65536u, obytes - off), &s_bar);
             }
             mbar_wait(&s_bar, bar_parity);
             bar_parity ^= 1;
@@ -159,146 +233,177 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
         for (uint32_t q = q0 + warp; q < q1; q += kWarps) {
             uint32_t out_t = kNone, out_d = 0;
             if (J.n != 0) {
-                // ---- 1. bucket lookup ------------------------------------------------------
-                uint32_t lo = 0, len = 0;
-                if (lane < P.L) {
-                    const uint32_t code = __ldg(I.shorts + uint64_t(q) * P.L + lane);
-                    const uint32_t* o = J.offs + lane * nb1 + code;
-                    lo = __ldg(o);
-                    len = __ldg(o + 1) - lo;
-                }
-                uint32_t incl = len;
-#pragma unroll
-                for (int d = 1; d < LT; d <<= 1) {
-                    const uint32_t u = __shfl_up_sync(FULL, incl, d);
-                    if (int(lane) >= d) incl += u;
-                }
-                const uint32_t R = __shfl_sync(FULL, incl, LT - 1);
-                const uint32_t excl = incl - len;
-                const uint32_t bias = lane * J.n + lo - excl;  // flat index r -> points[r + bias]
-                uint32_t pre[LT], bs[LT];
+                // ---- 1. bucket lookup (warp-uniform) -------------------------------------------
+                const uint32_t* __restrict__ qcodes = I.shorts + uint64_t(q) * L;
+                uint32_t lo[LT], len[LT];  // lo: index of the bucket's first entry in J.points
+                uint32_t total = 0, tover = 0;
 #pragma unroll
                 for (int t = 0; t < LT; ++t) {
-                    pre[t] = __shfl_sync(FULL, excl, t);
-                    bs[t] = __shfl_sync(FULL, bias, t);
+                    lo[t] = 0;
+                    len[t] = 0;
+                    if (EXACT || t < int(L)) {
+                        const uint32_t code = ldg_stream32(qcodes + t);
+                        uint32_t a, b;
+                        if (SMEM_TRAIN) {
+                            const uint2 o = lds64x(s_offs + (t * nb1 + code) * 4u);
+                            a = o.x;
+                            b = o.y;
+                        } else {
+                            const uint32_t* o = J.offs + t * nb1 + code;
+                            a = __ldg(o);
+                            b = __ldg(o + 1);
+                        }
+                        lo[t] = t * J.n + a;
+                        len[t] = b - a;
+                    }
+                    total += len[t];
+                    tover += max(len[t], 32u) - 32u;
                 }
-                st_raw += R;
+                st_raw += total;
 
-                if (R != 0) {
-                    const uint4 ql = __ldg(I.longs + q);
-                    uint32_t mykey = kNone;  // lane r holds the r-th ranked key
-                    uint32_t n = 0;          // ranked count
-                    uint32_t wmax = 0;       // multi-pass only: largest key seen
-                    const bool single = R <= 32u * kKeySlots;
+                const uint4 ql = ldg_stream128(I.longs + q);
+                uint32_t mykey = kNone;  // lane r holds the r-th ranked key
+                uint32_t n = 0;          // ranked count
 
-                    for (uint32_t base = 0; base < R; base += 32u * kKeySlots) {
-                        // ---- 2. Hamming scan ------------------------------------------------
-                        uint32_t key[kKeySlots];
+                if (tover <= 32u * kOverSlots) {
+                    // ---- 2. Hamming scan: the first 32 entries of every bucket, one table per slot,
+                    //         then the entries past 32 of all buckets flattened into the last slots
+                    uint32_t key[KS];
 #pragma unroll
-                        for (int it = 0; it < kKeySlots; ++it) {
-                            key[it] = kNone;
-                            const uint32_t rb = base + it * 32u;
-                            if (rb < R) {  // warp-uniform
-                                // lanes past the end re-evaluate the last candidate: equal keys collapse
-                                const uint32_t r = min(rb + lane, R - 1);
-                                uint32_t b = bs[0];
+                    for (int t = 0; t < LT; ++t) {
+                        const uint32_t k = scan_step<SMEM_TRAIN>(J.points, lo[t], lo[t] + max(len[t], 1u) - 1u, lane, ql,
+                                                                 s_long, J.longs);
+                        key[t] = len[t] != 0 ? k : kNone;  // (an empty bucket re-reads a neighbour: discarded)
+                    }
+#pragma unroll
+                    for (int s = 0; s < kOverSlots; ++s) key[LT + s] = kNone;
+                    if (tover != 0) {
+                        uint32_t pre = 0;
+                        uint32_t bias[LT], start[LT];
+#pragma unroll
+                        for (int t = 0; t < LT; ++t) {
+                            start[t] = pre;
+                            bias[t] = lo[t] + 32u - pre;  // flat overflow index r -> J.points[r + bias]
+                            pre += max(len[t], 32u) - 32u;
+                        }
+#pragma unroll
+                        for (int s = 0; s < kOverSlots; ++s) {
+                            if (uint32_t(s) * 32u < tover) {
+                                const uint32_t r = min(uint32_t(s) * 32u + lane, tover - 1u);
+                                uint32_t b = bias[0];
 #pragma unroll
                                 for (int t = 1; t < LT; ++t)
-                                    if (r >= pre[t]) b = bs[t];
-                                const uint32_t id = __ldg(J.points + (r + b));
-                                uint4 c;
-                                if (SMEM_TRAIN) c = s_long[id];
-                                else c = __ldg(J.longs + id);
-                                key[it] = (hamming128(c, ql) << 24) | id;
+                                    if (r >= start[t]) b = bias[t];
+                                key[LT + s] = scan_step<SMEM_TRAIN>(J.points, r + b, r + b, 0u, ql, s_long, J.longs);
                             }
                         }
-                        // ---- 3. ranking -----------------------------------------------------
-                        if (single) {
-                            uint32_t k0 = next_key(key, kNone, 0u, true);
-                            if ((k0 >> 24) <= P.tau) {
-                                if (lane == 0) mykey = k0;
-                                n = 1;
-                                bool fallback = false;
-                                uint32_t prev = k0;
-                                while (n < P.top_k) {
-                                    const uint32_t nk = next_key(key, kNone, prev, false);
-                                    if (nk == kNone) break;
-                                    if (!fallback && (nk >> 24) > P.tau) {
-                                        if (n >= P.min_ranked) break;
-                                        fallback = true;  // threshold cut something and the ranking is too small
-                                    }
-                                    if (lane == n) mykey = nk;
-                                    ++n;
-                                    prev = nk;
-                                }
+                    }
+                    // ---- 3. ranking: pull straight out of the slots -------------------------------
+                    const uint32_t k0 = first_key(key, kNone);
+                    if ((k0 >> 24) <= P.tau) {
+                        if (lane == 0) mykey = k0;
+                        n = 1;
+                        bool fallback = false;
+                        uint32_t prev = k0;
+                        while (n < P.top_k) {
+                            const uint32_t nk = next_key(key, kNone, prev);
+                            if (nk == kNone) break;
+                            if (!fallback && (nk >> 24) > P.tau) {
+                                if (n >= P.min_ranked) break;
+                                fallback = true;  // threshold cut something and the ranking is too small
                             }
-                        } else {
-                            // merge this pass into the running top-k (ascending, unique)
-                            uint32_t lmax = 0;
+                            if (lane == n) mykey = nk;
+                            ++n;
+                            prev = nk;
+                        }
+                    }
+                } else {
+                    // ---- long buckets: rounds of 32 entries per table ----------------------------
+                    uint32_t maxlen = 0;
 #pragma unroll
-                            for (int it = 0; it < kKeySlots; ++it)
-                                if (key[it] != kNone) lmax = max(lmax, key[it]);
-                            wmax = max(wmax, __reduce_max_sync(FULL, lmax));
+                    for (int t = 0; t < LT; ++t) maxlen = max(maxlen, len[t]);
+                    // pass 1: smallest and largest key only — most queries have nothing within tau
+                    uint32_t lmin = kNone, lmax = 0;
+                    for (uint32_t off = 0; off < maxlen; off += 32u) {
+#pragma unroll
+                        for (int t = 0; t < LT; ++t)
+                            if (off < len[t]) {
+                                const uint32_t k = scan_step<SMEM_TRAIN>(J.points, lo[t] + off, lo[t] + len[t] - 1u,
+                                                                         lane, ql, s_long, J.longs);
+                                lmin = min(lmin, k);
+                                lmax = max(lmax, k);
+                            }
+                    }
+                    const uint32_t gmin = __reduce_min_sync(FULL, lmin);
+                    if ((gmin >> 24) <= P.tau) {
+                        // pass 2: merge every round into the running top-k (ascending, unique)
+                        const bool anycut = (__reduce_max_sync(FULL, lmax) >> 24) > P.tau;
+                        for (uint32_t off = 0; off < maxlen; off += 32u) {
+                            uint32_t key[LT];
+#pragma unroll
+                            for (int t = 0; t < LT; ++t) {
+                                key[t] = kNone;
+                                if (off < len[t])
+                                    key[t] = scan_step<SMEM_TRAIN>(J.points, lo[t] + off, lo[t] + len[t] - 1u, lane, ql,
+                                                                   s_long, J.longs);
+                            }
+                            // a round whose smallest key is beyond a full list's last entry changes nothing
+                            const uint32_t kth = __shfl_sync(FULL, mykey, P.top_k - 1);
+                            uint32_t prev = first_key(key, kNone);
+                            if (prev > kth) continue;
                             const uint32_t old = mykey;
-                            uint32_t prev = 0;
+                            prev = min(prev, __shfl_sync(FULL, old, 0));
                             mykey = kNone;
-                            for (uint32_t r = 0; r < P.top_k; ++r) {
-                                const uint32_t nk = next_key(key, old, prev, r == 0);
-                                if (nk == kNone) break;
-                                if (lane == r) mykey = nk;
-                                prev = nk;
+                            for (uint32_t r = 0; r < P.top_k && prev != kNone; ++r) {
+                                if (lane == r) mykey = prev;
+                                prev = next_key(key, old, prev);
                             }
                         }
-                    }
-                    if (!single) {
-                        // thresholded size s, unique total (<= k); fallback rule as in the single-pass path
-                        const uint32_t total = __popc(__ballot_sync(FULL, mykey != kNone));
+                        // thresholded size s, unique total (<= k); fallback rule as in the single-round path
+                        const uint32_t tot = __popc(__ballot_sync(FULL, mykey != kNone));
                         const uint32_t s = __popc(__ballot_sync(FULL, mykey != kNone && (mykey >> 24) <= P.tau));
-                        const bool anycut = (wmax >> 24) > P.tau;
-                        if (s == 0) n = 0;
-                        else if (s >= P.min_ranked || !anycut) n = s;
-                        else n = total;
+                        n = (s >= P.min_ranked || !anycut) ? s : tot;
                     }
+                }
 
-                    if (P.dbg_ranked != nullptr) {
-                        if (lane < n) P.dbg_ranked[uint64_t(q) * P.top_k + lane] = mykey & 0xffffffu;
-                        if (lane == 0) P.dbg_count[q] = n;
+                if (P.dbg_ranked != nullptr) {
+                    if (lane < n) P.dbg_ranked[uint64_t(q) * P.top_k + lane] = mykey & 0xffffffu;
+                    if (lane == 0) P.dbg_count[q] = n;
+                }
+
+                // ---- 4. verification (euclidean_verify, matcher.cpp:115-137) ------------------
+                if (n >= 2) {
+                    st_vq += 1;
+                    st_dist += n;
+                    const uint32_t sub = lane & 7, grp = lane >> 3;
+                    const uint4 qa = ldg_stream128(reinterpret_cast<const uint4*>(I.desc + uint64_t(q) * kDim) + sub);
+                    uint32_t mydist = kNone;
+                    for (uint32_t j0 = 0; j0 < n; j0 += 4) {
+                        const uint32_t j = min(j0 + grp, n - 1);
+                        const uint32_t id = __shfl_sync(FULL, mykey, j) & 0xffffffu;
+                        const uint4 ta = ldg_stream128(reinterpret_cast<const uint4*>(J.desc + uint64_t(id) * kDim) + sub);
+                        uint32_t s = sqdiff4(qa.x, ta.x) + sqdiff4(qa.y, ta.y) + sqdiff4(qa.z, ta.z) +
+                                     sqdiff4(qa.w, ta.w);
+                        s += __shfl_xor_sync(FULL, s, 1);
+                        s += __shfl_xor_sync(FULL, s, 2);
+                        s += __shfl_xor_sync(FULL, s, 4);
+                        const uint32_t v = __shfl_sync(FULL, s, ((lane - j0) & 3u) * 8u);
+                        if (lane >= j0 && lane < j0 + 4 && lane < n) mydist = v;
                     }
-
-                    // ---- 4. verification (euclidean_verify, matcher.cpp:115-137) ----------
-                    if (n >= 2) {
-                        st_vq += 1;
-                        st_dist += n;
-                        const uint32_t sub = lane & 7, grp = lane >> 3;
-                        const uint4 qa = __ldg(reinterpret_cast<const uint4*>(I.desc + uint64_t(q) * kDim) + sub);
-                        uint32_t mydist = kNone;
-                        for (uint32_t j0 = 0; j0 < n; j0 += 4) {
-                            const uint32_t j = min(j0 + grp, n - 1);
-                            const uint32_t id = __shfl_sync(FULL, mykey, j) & 0xffffffu;
-                            const uint4 ta = __ldg(reinterpret_cast<const uint4*>(J.desc + uint64_t(id) * kDim) + sub);
-                            uint32_t s = sqdiff4(qa.x, ta.x) + sqdiff4(qa.y, ta.y) + sqdiff4(qa.z, ta.z) +
-                                         sqdiff4(qa.w, ta.w);
-                            s += __shfl_xor_sync(FULL, s, 1);
-                            s += __shfl_xor_sync(FULL, s, 2);
-                            s += __shfl_xor_sync(FULL, s, 4);
-                            const uint32_t v = __shfl_sync(FULL, s, ((lane - j0) & 3u) * 8u);
-                            if (lane >= j0 && lane < j0 + 4 && lane < n) mydist = v;
-                        }
-                        // best = smallest d^2, ties to the earlier rank (strict '<' in the reference loop)
-                        const uint32_t packed = lane < n ? ((mydist << 8) | lane) : kNone;
-                        const uint32_t bestp = __reduce_min_sync(FULL, packed);
-                        const uint32_t bl = bestp & 0xffu, best = bestp >> 8;
-                        const uint32_t second = __reduce_min_sync(FULL, (lane < n && lane != bl) ? mydist : kNone);
-                        const uint32_t bid = __shfl_sync(FULL, mykey, bl) & 0xffffffu;
-                        if (second != 0u && double(best) < __dmul_rn(P.ratio_sq, double(second))) {
-                            out_t = bid;
-                            out_d = best;
-                            st_match += 1;
-                        }
+                    // best = smallest d^2, ties to the earlier rank (strict '<' in the reference loop)
+                    const uint32_t packed = lane < n ? ((mydist << 8) | lane) : kNone;
+                    const uint32_t bestp = __reduce_min_sync(FULL, packed);
+                    const uint32_t bl = bestp & 0xffu, best = bestp >> 8;
+                    const uint32_t second = __reduce_min_sync(FULL, (lane < n && lane != bl) ? mydist : kNone);
+                    const uint32_t bid = __shfl_sync(FULL, mykey, bl) & 0xffffffu;
+                    if (second != 0u && double(best) < __dmul_rn(P.ratio_sq, double(second))) {
+                        out_t = bid;
+                        out_d = best;
+                        st_match += 1;
                     }
                 }
             }
-            if (lane == 0) P.res[pd.res_off + q] = make_uint2(out_t, out_d);
+            if (lane == 0) __stcs(P.res + pd.res_off + q, make_uint2(out_t, out_d));
         }
 
         if (lane == 0) {
@@ -307,101 +412,8 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
             if (st_dist) atomicAdd(&P.stats->distances, (unsigned long long)st_dist);
             if (st_match) atomicAdd(&P.pair_counts[pair], st_match);
         }
-        __syncthreads();  // all warps done with s_long / s_unit before the next unit
+        __syncthreads();  // all warps done with the train tile / s_unit before the next unit
     }
-}
-
-// Exclusive scan of per-pair match counts -> record offsets (one CTA; npairs is a sub-batch).
-__global__ void scan_counts_kernel(const uint32_t* __restrict__ counts, uint32_t npairs,
-                                   unsigned long long* __restrict__ offsets /* npairs + 1 */,
-                                   DevStats* stats) {
-    __shared__ unsigned long long s_warp[32];
-    __shared__ unsigned long long s_carry;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_carry = 0;
-    __syncthreads();
-    for (uint32_t base = 0; base < npairs; base += blockDim.x) {
-        const uint32_t i = base + tid;
-        const unsigned long long v = i < npairs ? counts[i] : 0;
-        unsigned long long incl = v;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, d);
-            if (int(lane) >= d) incl += u;
-        }
-        if (lane == 31) s_warp[warp] = incl;
-        __syncthreads();
-        if (warp == 0) {
-            unsigned long long w = lane < (blockDim.x >> 5) ? s_warp[lane] : 0;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const unsigned long long u = __shfl_up_sync(0xffffffffu, w, d);
-                if (int(lane) >= d) w += u;
-            }
-            s_warp[lane] = w;  // inclusive over warps
-        }
-        __syncthreads();
-        const unsigned long long before = s_carry + (warp ? s_warp[warp - 1] : 0);
-        if (i < npairs) offsets[i] = before + incl - v;
-        __syncthreads();
-        if (tid == blockDim.x - 1) s_carry = before + incl;
-        __syncthreads();
-    }
-    if (tid == 0) {
-        offsets[npairs] = s_carry;
-        atomicAdd(&stats->matches, s_carry);
-    }
-}
-
-__device__ __forceinline__ unsigned long long mix64_dev(unsigned long long x) {
-    x += 0x9e3779b97f4a7c15ULL;
-    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
-    return x ^ (x >> 31);
-}
-
-// One CTA per pair: ordered compaction of the per-query scratch into MatchRecord{u32 q, u32 t, f64 d^2}
-// (feature_io.hpp:51-57), ascending q, at most one per query (matcher.cpp:191-192).
-__global__ void compact_kernel(const PairDesc* __restrict__ pairs, const DevImage* __restrict__ images,
-                               const uint2* __restrict__ res, const unsigned long long* __restrict__ offsets,
-                               uint4* __restrict__ records, uint32_t first_pair_global, DevStats* stats) {
-    __shared__ uint32_t s_warp[32];
-    __shared__ uint32_t s_base;
-    const uint32_t pair = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const PairDesc pd = pairs[pair];
-    const uint32_t nq = images[pd.slot_i].n;
-    if (tid == 0) s_base = 0;
-    __syncthreads();
-    uint4* out = records + offsets[pair];
-    unsigned long long csum = 0;
-    for (uint32_t q0 = 0; q0 < nq; q0 += blockDim.x) {
-        const uint32_t q = q0 + tid;
-        uint2 r = make_uint2(kNone, 0);
-        if (q < nq) r = res[pd.res_off + q];
-        const bool hit = r.x != kNone;
-        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-        if (lane == 0) s_warp[warp] = __popc(bal);
-        __syncthreads();
-        uint32_t before = s_base;
-        for (uint32_t w = 0; w < warp; ++w) before += s_warp[w];
-        if (hit) {
-            const uint32_t pos = before + __popc(bal & ((1u << lane) - 1u));
-            const unsigned long long db = (unsigned long long)__double_as_longlong(double(r.y));
-            out[pos] = make_uint4(q, r.x, uint32_t(db), uint32_t(db >> 32));
-            csum += mix64_dev(mix64_dev((unsigned long long)(first_pair_global + pair) << 32 | q) ^
-                              ((unsigned long long)r.x << 32 | r.y));
-        }
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t tot = 0;
-            for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) tot += s_warp[w];
-            s_base += tot;
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, d);
-    if (lane == 0 && csum) atomicAdd(&stats->checksum, csum);
 }
 
 }  // namespace chgpu

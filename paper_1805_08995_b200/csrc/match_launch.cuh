@@ -1,0 +1,44 @@
+// match_launch.cuh — launchers of the match kernel's instantiations.  The shared-memory and the
+// global-gather variants live in separate translation units (match_smem.cu, match_global.cu)
+// so that nvcc compiles them in parallel.
+#pragma once
+
+#include "match_kernels.cuh"
+
+namespace chgpu {
+
+// Launches match_kernel<SMEM_TRAIN, LT, EXACT> for P.L tables on `stream` as a persistent grid
+// (one CTA per SM at most, never more CTAs than units).  smem = dynamic shared memory bytes.
+cudaError_t launch_match_smem(const MatchParams& P, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid);
+cudaError_t launch_match_global(const MatchParams& P, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid);
+
+template <bool SMEM, int LT, bool EXACT>
+cudaError_t launch_match_variant(const MatchParams& P, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid_out) {
+    auto kfn = match_kernel<SMEM, LT, EXACT>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kMatchThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+    const uint32_t cap = uint32_t(per_sm) * uint32_t(sm_count);
+    const uint32_t grid = P.nunits < cap ? P.nunits : cap;
+    *grid_out = grid;
+    kfn<<<grid, kMatchThreads, smem, stream>>>(P);
+    return cudaGetLastError();
+}
+
+template <bool SMEM>
+cudaError_t launch_match_any(const MatchParams& P, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid) {
+    switch (P.L) {
+        case 4: return launch_match_variant<SMEM, 4, true>(P, smem, sm_count, stream, grid);
+        case 6: return launch_match_variant<SMEM, 6, true>(P, smem, sm_count, stream, grid);
+        case 8: return launch_match_variant<SMEM, 8, true>(P, smem, sm_count, stream, grid);
+        default: break;
+    }
+    if (P.L < 4) return launch_match_variant<SMEM, 4, false>(P, smem, sm_count, stream, grid);
+    if (P.L < 6) return launch_match_variant<SMEM, 6, false>(P, smem, sm_count, stream, grid);
+    return launch_match_variant<SMEM, 8, false>(P, smem, sm_count, stream, grid);
+}
+
+}  // namespace chgpu
