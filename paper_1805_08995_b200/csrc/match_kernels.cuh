@@ -38,8 +38,14 @@
 
 namespace chgpu {
 
-constexpr int kMatchThreads = 1024;
-constexpr int kOverSlots = 2;  // register slots for bucket entries past the first 32 of every table
+#ifndef CHGPU_MATCH_THREADS
+#define CHGPU_MATCH_THREADS 1024
+#endif
+#ifndef CHGPU_OVER_SLOTS
+#define CHGPU_OVER_SLOTS 3
+#endif
+constexpr int kMatchThreads = CHGPU_MATCH_THREADS;
+constexpr int kOverSlots = CHGPU_OVER_SLOTS;  // register slots for bucket entries past the first 32 of every table
 
 struct MatchParams {
     const DevImage* images;
@@ -236,7 +242,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                 // ---- 1. bucket lookup (warp-uniform) -------------------------------------------
                 const uint32_t* __restrict__ qcodes = I.shorts + uint64_t(q) * L;
                 uint32_t lo[LT], len[LT];  // lo: index of the bucket's first entry in J.points
-                uint32_t total = 0, tover = 0;
+                uint32_t total = 0, tover = 0, minlen = kNone;
 #pragma unroll
                 for (int t = 0; t < LT; ++t) {
                     lo[t] = 0;
@@ -257,6 +263,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                         len[t] = b - a;
                     }
                     total += len[t];
+                    minlen = min(minlen, len[t]);
                     tover += max(len[t], 32u) - 32u;
                 }
                 st_raw += total;
@@ -270,10 +277,13 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     //         then the entries past 32 of all buckets flattened into the last slots
                     uint32_t key[KS];
 #pragma unroll
-                    for (int t = 0; t < LT; ++t) {
-                        const uint32_t k = scan_step<SMEM_TRAIN>(J.points, lo[t], lo[t] + max(len[t], 1u) - 1u, lane, ql,
-                                                                 s_long, J.longs);
-                        key[t] = len[t] != 0 ? k : kNone;  // (an empty bucket re-reads a neighbour: discarded)
+                    for (int t = 0; t < LT; ++t)  // (an empty bucket re-reads a neighbour's entry: discarded below)
+                        key[t] = scan_step<SMEM_TRAIN>(J.points, lo[t], lo[t] + max(len[t], 1u) - 1u, lane, ql, s_long,
+                                                       J.longs);
+                    if (minlen == 0) {
+#pragma unroll
+                        for (int t = 0; t < LT; ++t)
+                            if (len[t] == 0) key[t] = kNone;
                     }
 #pragma unroll
                     for (int s = 0; s < kOverSlots; ++s) key[LT + s] = kNone;
@@ -303,18 +313,23 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     if ((k0 >> 24) <= P.tau) {
                         if (lane == 0) mykey = k0;
                         n = 1;
-                        bool fallback = false;
-                        uint32_t prev = k0;
+                        uint32_t prev = k0, nk = kNone;
+                        // keys within tau, in order (usually this loop ends at its first pull)
                         while (n < P.top_k) {
-                            const uint32_t nk = next_key(key, kNone, prev);
-                            if (nk == kNone) break;
-                            if (!fallback && (nk >> 24) > P.tau) {
-                                if (n >= P.min_ranked) break;
-                                fallback = true;  // threshold cut something and the ranking is too small
-                            }
+                            nk = next_key(key, kNone, prev);
+                            if ((nk >> 24) > P.tau) break;  // beyond the threshold, or kNone: no key left
                             if (lane == n) mykey = nk;
                             ++n;
                             prev = nk;
+                        }
+                        // the threshold cut something and the ranking is too small: re-rank without it
+                        if (n < P.top_k && nk != kNone && n < P.min_ranked) {
+                            do {
+                                if (lane == n) mykey = nk;
+                                ++n;
+                                if (n == P.top_k) break;
+                                nk = next_key(key, kNone, nk);
+                            } while (nk != kNone);
                         }
                     }
                 } else {
@@ -375,20 +390,23 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                 if (n >= 2) {
                     st_vq += 1;
                     st_dist += n;
-                    const uint32_t sub = lane & 7, grp = lane >> 3;
-                    const uint4 qa = ldg_stream128(reinterpret_cast<const uint4*>(I.desc + uint64_t(q) * kDim) + sub);
+                    // two lanes per candidate row (64 bytes each), 16 candidates per round
+                    const uint32_t half = lane & 1u, cand = lane >> 1;
+                    const uint4* __restrict__ qrow = reinterpret_cast<const uint4*>(I.desc + uint64_t(q) * kDim) + half * 4u;
                     uint32_t mydist = kNone;
-                    for (uint32_t j0 = 0; j0 < n; j0 += 4) {
-                        const uint32_t j = min(j0 + grp, n - 1);
+                    for (uint32_t j0 = 0; j0 < n; j0 += 16) {
+                        const uint32_t j = min(j0 + cand, n - 1);
                         const uint32_t id = __shfl_sync(FULL, mykey, j) & 0xffffffu;
-                        const uint4 ta = ldg_stream128(reinterpret_cast<const uint4*>(J.desc + uint64_t(id) * kDim) + sub);
-                        uint32_t s = sqdiff4(qa.x, ta.x) + sqdiff4(qa.y, ta.y) + sqdiff4(qa.z, ta.z) +
-                                     sqdiff4(qa.w, ta.w);
+                        const uint4* __restrict__ trow = reinterpret_cast<const uint4*>(J.desc + uint64_t(id) * kDim) + half * 4u;
+                        uint32_t s = 0;
+#pragma unroll 2
+                        for (int w = 0; w < 4; ++w) {
+                            const uint4 qa = __ldg(qrow + w), ta = __ldg(trow + w);
+                            s += sqdiff4(qa.x, ta.x) + sqdiff4(qa.y, ta.y) + sqdiff4(qa.z, ta.z) + sqdiff4(qa.w, ta.w);
+                        }
                         s += __shfl_xor_sync(FULL, s, 1);
-                        s += __shfl_xor_sync(FULL, s, 2);
-                        s += __shfl_xor_sync(FULL, s, 4);
-                        const uint32_t v = __shfl_sync(FULL, s, ((lane - j0) & 3u) * 8u);
-                        if (lane >= j0 && lane < j0 + 4 && lane < n) mydist = v;
+                        const uint32_t v = __shfl_sync(FULL, s, ((lane - j0) & 15u) * 2u);
+                        if (lane >= j0 && lane < j0 + 16 && lane < n) mydist = v;
                     }
                     // best = smallest d^2, ties to the earlier rank (strict '<' in the reference loop)
                     const uint32_t packed = lane < n ? ((mydist << 8) | lane) : kNone;
