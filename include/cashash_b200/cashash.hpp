@@ -1,0 +1,673 @@
+// cashash.hpp — C++ host side of the B200 Cascade Hashing matcher.
+//
+// Header-only facade over the C ABI of libchgpu.so (include/chgpu.h) that keeps the reference's
+// C++ matcher API for the matching path: same type names, member names, argument meaning and
+// exception behaviour as namespace `cashash` of the reference (paths below are relative to
+// /root/reference/proj):
+//
+//     descriptor load   load_features / save_features          include/cashash/feature_io.hpp:85-86
+//     hash family       build_hash_family / set_centering      include/cashash/hashing.hpp:74-78
+//                       CenteringAccumulator                    include/cashash/hashing.hpp:166-172
+//     hash build        compute_codes                           include/cashash/hashing.hpp:131
+//     bucket index      build_bucket_index                      include/cashash/matcher.hpp:43
+//     match             match_pair                              include/cashash/matcher.hpp:98-100
+//     match output      save_matches / pair_file_name           include/cashash/feature_io.hpp:106,
+//                                                               include/cashash/engine.hpp:79
+//     pair list         plan_exhaustive (flattened)             include/cashash/scheduler.hpp:53
+//
+// A caller of the reference switches by including this header and `namespace cashash =
+// cashash_b200;`.  The free functions run on a process-wide default
+// context for device 0 and serialise on it; they exist for drop-in use and for parity tests.
+// Throughput comes from the batch interface, `Matcher`: upload every image once, hash them in
+// one launch, match a whole pair list per call.
+//
+// There is no CPU fallback: every function that computes goes through libchgpu.so and throws
+// std::runtime_error when no sm_100 device is present.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../chgpu.h"
+
+namespace cashash_b200 {
+
+inline constexpr std::size_t kDescriptorDim = 128;
+inline constexpr int kMaxReduceRounds = 7;
+inline constexpr int kDefaultReduceRounds = 3;
+inline constexpr std::size_t kFeatureFileHeaderBytes = 16;
+inline constexpr std::size_t kFeatureRecordBytes = 16 + kDescriptorDim;
+
+// ---- feature_io.hpp types ---------------------------------------------------------------------
+struct Keypoint {  // feature_io.hpp:16-23
+    float x = 0.0f;
+    float y = 0.0f;
+    float scale = 0.0f;
+    float orientation = 0.0f;
+    friend bool operator==(const Keypoint&, const Keypoint&) = default;
+};
+static_assert(sizeof(Keypoint) == 16, "keypoints travel to the device as float4");
+
+using Descriptor = std::array<std::uint8_t, kDescriptorDim>;  // feature_io.hpp:27
+
+struct FeatureSet {  // feature_io.hpp:29-36
+    std::string image_id;
+    std::vector<Keypoint> keypoints;
+    std::vector<Descriptor> descriptors;
+    std::size_t size() const { return keypoints.size(); }
+    bool empty() const { return keypoints.empty(); }
+};
+
+struct MatchRecord {  // feature_io.hpp:51-57
+    std::uint32_t query_index = 0;
+    std::uint32_t train_index = 0;
+    double distance_sq = 0.0;
+    friend bool operator==(const MatchRecord&, const MatchRecord&) = default;
+};
+static_assert(sizeof(MatchRecord) == sizeof(chgpu_match_record) && sizeof(MatchRecord) == 16,
+              "MatchRecord is copied from the device byte for byte");
+
+enum class FeatureFileFault { MissingFile, BadMagic, BadVersion, Truncated, Unwritable };  // feature_io.hpp:61-67
+
+class FeatureFileError : public std::runtime_error {  // feature_io.hpp:69-80
+public:
+    FeatureFileError(FeatureFileFault fault, const std::filesystem::path& path, std::uint64_t byte_offset,
+                     const std::string& detail)
+        : std::runtime_error(message(fault, path, byte_offset, detail)), fault_(fault), byte_offset_(byte_offset) {}
+    FeatureFileFault fault() const { return fault_; }
+    std::uint64_t byte_offset() const { return byte_offset_; }
+
+private:
+    static std::string message(FeatureFileFault fault, const std::filesystem::path& path, std::uint64_t offset,
+                               const std::string& detail) {
+        static const char* const names[] = {"missing file", "bad magic", "unsupported version", "truncated payload",
+                                            "unwritable path"};
+        std::string s = path.string() + ": " + names[static_cast<int>(fault)] + " at byte " + std::to_string(offset);
+        if (!detail.empty()) s += " (" + detail + ")";
+        return s;
+    }
+    FeatureFileFault fault_;
+    std::uint64_t byte_offset_;
+};
+
+// ---- hashing.hpp types ------------------------------------------------------------------------
+struct FamilyParams {  // hashing.hpp:45-52
+    std::uint32_t short_bits = 8;
+    std::uint32_t long_bits = 128;
+    std::uint32_t table_count = 6;
+    std::uint64_t seed = 1;
+    friend bool operator==(const FamilyParams&, const FamilyParams&) = default;
+};
+
+using Hyperplane = std::array<double, kDescriptorDim>;
+
+struct HashFamily {  // hashing.hpp:62-72
+    FamilyParams params;
+    std::vector<Hyperplane> short_planes;  // [table * short_bits + bit]
+    std::vector<Hyperplane> long_planes;   // [bit]
+    std::array<double, kDescriptorDim> centering{};
+    bool centering_set = false;
+    const Hyperplane& short_plane(std::uint32_t table, std::uint32_t bit) const {
+        return short_planes[table * params.short_bits + bit];
+    }
+};
+
+struct ShortCodes {  // hashing.hpp:80-89
+    std::uint32_t short_bits = 0;
+    std::uint32_t table_count = 0;
+    std::uint32_t point_count = 0;
+    std::vector<std::uint32_t> values;  // [point * table_count + table]
+    std::uint32_t at(std::uint32_t point, std::uint32_t table) const {
+        return values[static_cast<std::size_t>(point) * table_count + table];
+    }
+};
+
+struct LongCode {  // hashing.hpp:91-96
+    std::array<std::uint64_t, 2> words{};
+    std::uint16_t bits = 0;
+    friend bool operator==(const LongCode&, const LongCode&) = default;
+};
+
+struct LongCodeSet {
+    std::uint32_t long_bits = 0;
+    std::vector<LongCode> codes;
+};
+
+struct ImageCodes {  // hashing.hpp:110-114
+    FamilyParams params;
+    ShortCodes shorts;
+    LongCodeSet longs;
+};
+
+// ---- matcher.hpp types ------------------------------------------------------------------------
+struct MatchConfig {  // matcher.hpp:14-23
+    std::uint32_t top_k = 10;
+    std::uint32_t hamming_threshold = 40;
+    double ratio = 0.8;
+    std::uint32_t min_candidates_for_ratio = 2;
+    int reduce_rounds = kDefaultReduceRounds;
+};
+
+struct BucketIndex {  // matcher.hpp:30-41
+    struct Table {
+        std::vector<std::uint32_t> codes;    // sorted unique bucket codes
+        std::vector<std::uint32_t> offsets;  // codes.size() + 1
+        std::vector<std::uint32_t> points;   // point ids, bucket-major
+    };
+    std::uint32_t short_bits = 0;
+    std::uint32_t point_count = 0;
+    std::vector<Table> tables;
+
+    std::span<const std::uint32_t> bucket(std::uint32_t table, std::uint32_t code) const {
+        const Table& t = tables.at(table);
+        std::size_t lo = 0, hi = t.codes.size();  // lower_bound over the unique codes (matcher.cpp:19-25)
+        while (lo < hi) {
+            const std::size_t mid = (lo + hi) / 2;
+            if (t.codes[mid] < code) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo == t.codes.size() || t.codes[lo] != code) return {};
+        return {t.points.data() + t.offsets[lo], t.points.data() + t.offsets[lo + 1]};
+    }
+};
+
+// ---- error mapping ----------------------------------------------------------------------------
+namespace detail {
+
+inline chgpu_family_params to_c(const FamilyParams& p) {
+    chgpu_family_params c{};
+    c.short_bits = p.short_bits;
+    c.long_bits = p.long_bits;
+    c.table_count = p.table_count;
+    c.seed = p.seed;
+    return c;
+}
+inline chgpu_match_cfg to_c(const MatchConfig& m) {
+    chgpu_match_cfg c{};
+    c.top_k = m.top_k;
+    c.hamming_threshold = m.hamming_threshold;
+    c.ratio = m.ratio;
+    c.min_candidates_for_ratio = m.min_candidates_for_ratio;
+    c.reduce_rounds = m.reduce_rounds;
+    return c;
+}
+
+// chgpu_status -> the exception class the reference throws for the same condition.
+[[noreturn]] inline void raise(chgpu_status st, const std::string& msg) {
+    switch (st) {
+        case CHGPU_EINVAL: throw std::invalid_argument(msg);
+        case CHGPU_ELOGIC: throw std::logic_error(msg);
+        case CHGPU_ENOMEM: throw std::bad_alloc();
+        case CHGPU_ENOTFOUND: throw std::out_of_range(msg);
+        default: throw std::runtime_error(msg + " [" + chgpu_status_name(st) + "]");
+    }
+}
+
+}  // namespace detail
+
+// ---- host-only operations (no device needed) ----------------------------------------------------
+inline void validate(const FamilyParams& p) {  // hashing.cpp:30-36
+    if (p.short_bits < 1 || p.short_bits > 32) throw std::invalid_argument("short_bits must be in 1..32");
+    if (p.long_bits <= p.short_bits || p.long_bits > 128) throw std::invalid_argument("long_bits must satisfy m < n <= 128");
+    if (p.table_count < 1) throw std::invalid_argument("table_count must be >= 1");
+}
+
+// build_hash_family (hashing.hpp:74): bit-identical hyperplanes, generated on the host.
+inline HashFamily build_hash_family(const FamilyParams& params) {
+    validate(params);
+    HashFamily f;
+    f.params = params;
+    f.short_planes.resize(static_cast<std::size_t>(params.table_count) * params.short_bits);
+    f.long_planes.resize(params.long_bits);
+    const chgpu_family_params c = detail::to_c(params);
+    const chgpu_status st = chgpu_family_generate(&c, f.short_planes.front().data(), f.long_planes.front().data());
+    if (st != CHGPU_OK) detail::raise(st, "build_hash_family");
+    return f;
+}
+
+// load_features (feature_io.hpp:85): CHFT file -> FeatureSet, the reference's fault classes and offsets.
+inline FeatureSet load_features(const std::filesystem::path& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw FeatureFileError(FeatureFileFault::MissingFile, path, 0, "");
+    unsigned char header[kFeatureFileHeaderBytes];
+    in.read(reinterpret_cast<char*>(header), sizeof(header));
+    if (in.gcount() != static_cast<std::streamsize>(sizeof(header)))
+        throw FeatureFileError(FeatureFileFault::Truncated, path, static_cast<std::uint64_t>(in.gcount()), "header");
+    if (std::memcmp(header, "CHFT", 4) != 0) throw FeatureFileError(FeatureFileFault::BadMagic, path, 0, "");
+    std::uint32_t version = 0, count = 0;
+    std::memcpy(&version, header + 4, 4);
+    std::memcpy(&count, header + 8, 4);
+    if (version != 1)
+        throw FeatureFileError(FeatureFileFault::BadVersion, path, 4, "version " + std::to_string(version));
+    // one bulk read, then de-interleave; a short file is reported at the byte where it ends
+    std::vector<unsigned char> body(static_cast<std::size_t>(count) * kFeatureRecordBytes);
+    in.read(reinterpret_cast<char*>(body.data()), static_cast<std::streamsize>(body.size()));
+    const std::uint64_t got = static_cast<std::uint64_t>(in.gcount());
+    if (got != body.size()) {
+        const std::uint64_t rec = got / kFeatureRecordBytes;
+        throw FeatureFileError(FeatureFileFault::Truncated, path, kFeatureFileHeaderBytes + got,
+                               "record " + std::to_string(rec) + " of " + std::to_string(count));
+    }
+    FeatureSet fs;
+    fs.keypoints.resize(count);
+    fs.descriptors.resize(count);
+    for (std::uint32_t i = 0; i < count; ++i) {
+        const unsigned char* r = body.data() + static_cast<std::size_t>(i) * kFeatureRecordBytes;
+        std::memcpy(&fs.keypoints[i], r, 16);
+        std::memcpy(fs.descriptors[i].data(), r + 16, kDescriptorDim);
+    }
+    return fs;
+}
+
+inline void save_features(const FeatureSet& fs, const std::filesystem::path& path) {  // feature_io.hpp:86
+    if (fs.keypoints.size() != fs.descriptors.size())
+        throw std::invalid_argument("feature set keypoint/descriptor length mismatch");
+    std::vector<unsigned char> out(kFeatureFileHeaderBytes + fs.size() * kFeatureRecordBytes, 0);
+    std::memcpy(out.data(), "CHFT", 4);
+    const std::uint32_t version = 1, count = static_cast<std::uint32_t>(fs.size());
+    std::memcpy(out.data() + 4, &version, 4);
+    std::memcpy(out.data() + 8, &count, 4);
+    for (std::size_t i = 0; i < fs.size(); ++i) {
+        unsigned char* r = out.data() + kFeatureFileHeaderBytes + i * kFeatureRecordBytes;
+        std::memcpy(r, &fs.keypoints[i], 16);
+        std::memcpy(r + 16, fs.descriptors[i].data(), kDescriptorDim);
+    }
+    std::ofstream os(path, std::ios::binary | std::ios::trunc);
+    if (!os) throw FeatureFileError(FeatureFileFault::Unwritable, path, 0, "");
+    os.write(reinterpret_cast<const char*>(out.data()), static_cast<std::streamsize>(out.size()));
+    if (!os) throw FeatureFileError(FeatureFileFault::Unwritable, path, 0, "short write");
+}
+
+// save_matches (feature_io.hpp:106-107): byte-identical text.
+inline void save_matches(const std::string& image_id_i, const std::string& image_id_j,
+                         const std::vector<MatchRecord>& matches, const std::filesystem::path& path) {
+    const chgpu_status st =
+        chgpu_save_matches(image_id_i.c_str(), image_id_j.c_str(), reinterpret_cast<const chgpu_match_record*>(matches.data()),
+                           static_cast<std::uint32_t>(matches.size()), path.string().c_str());
+    if (st != CHGPU_OK) throw FeatureFileError(FeatureFileFault::Unwritable, path, 0, "");
+}
+
+inline std::string pair_file_name(std::uint32_t i, std::uint32_t j) {  // engine.hpp:79
+    char buf[48];
+    chgpu_pair_file_name(i, j, buf);
+    return buf;
+}
+
+// plan_exhaustive (scheduler.hpp:53), flattened in task order: pairs (a < b), a is the query image.
+inline std::vector<std::pair<std::uint32_t, std::uint32_t>> plan_exhaustive(std::uint32_t image_count,
+                                                                            std::uint32_t block_images,
+                                                                            std::uint32_t blocks_per_group) {
+    if (image_count == 0 || block_images == 0 || blocks_per_group == 0)
+        throw std::invalid_argument("partition: image_count, block_images and blocks_per_group must be >= 1");
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> pairs(static_cast<std::size_t>(image_count) * (image_count - 1) / 2);
+    static_assert(sizeof(std::pair<std::uint32_t, std::uint32_t>) == 8, "pair list is passed as flat u32");
+    std::uint64_t n = 0;
+    const chgpu_status st = chgpu_plan_exhaustive(image_count, block_images, blocks_per_group,
+                                                  reinterpret_cast<std::uint32_t*>(pairs.data()), &n);
+    if (st != CHGPU_OK) detail::raise(st, "plan_exhaustive");
+    pairs.resize(n);
+    return pairs;
+}
+
+// ---- batch interface: one device context ----------------------------------------------------------
+struct MatchStats : chgpu_match_stats {};
+
+struct PairMatches {  // what the reference's sink receives (engine.cpp:145-160), one per pair
+    std::uint32_t image_i = 0, image_j = 0;
+    std::vector<MatchRecord> matches;
+};
+
+class Matcher {
+public:
+    explicit Matcher(int device = 0) {
+        const chgpu_status st = chgpu_create(device, &ctx_);
+        if (st != CHGPU_OK)
+            throw std::runtime_error(std::string("chgpu_create failed: ") + chgpu_status_name(st) +
+                                     " (an sm_100 CUDA device is required; there is no CPU fallback)");
+    }
+    ~Matcher() { chgpu_destroy(ctx_); }
+    Matcher(const Matcher&) = delete;
+    Matcher& operator=(const Matcher&) = delete;
+
+    chgpu_ctx* handle() const { return ctx_; }
+
+    void set_family(const HashFamily& family) {
+        const chgpu_family_params c = detail::to_c(family.params);
+        ck(chgpu_set_family(ctx_, &c, family.short_planes.front().data(), family.long_planes.front().data()));
+        params_ = family.params;
+        if (family.centering_set) ck(chgpu_set_centering(ctx_, family.centering.data()));
+    }
+    const FamilyParams& params() const { return params_; }
+
+    // descriptor load: FeatureSet -> resident image (engine.cpp:394-412)
+    void upload(std::uint32_t image_id, const FeatureSet& fs) {
+        if (fs.keypoints.size() != fs.descriptors.size())
+            throw std::invalid_argument("feature set keypoint/descriptor length mismatch");
+        ck(chgpu_upload_image(ctx_, image_id, static_cast<std::uint32_t>(fs.size()),
+                              fs.empty() ? nullptr : fs.descriptors.front().data(),
+                              fs.empty() ? nullptr : &fs.keypoints.front().x));
+    }
+    // descriptor load straight from CHFT bytes (parse_features_blob, engine.cpp:458-488)
+    std::uint32_t upload_chft(std::uint32_t image_id, const void* blob, std::size_t nbytes,
+                              const std::filesystem::path& origin = "<memory>") {
+        std::uint32_t count = 0;
+        chgpu_file_fault fault = CHGPU_FAULT_NONE;
+        std::uint64_t off = 0;
+        const chgpu_status st = chgpu_upload_chft(ctx_, image_id, blob, nbytes, &count, &fault, &off);
+        if (st == CHGPU_EFORMAT) throw FeatureFileError(static_cast<FeatureFileFault>(int(fault) - 1), origin, off, "");
+        ck(st);
+        return count;
+    }
+    void evict(std::uint32_t image_id) { ck(chgpu_evict_image(ctx_, image_id)); }
+
+    // centering pass (hashing.cpp:52-70): exact integer sums on the device, one division on the host
+    void centering_reset() { ck(chgpu_centering_reset(ctx_)); }
+    void centering_add(std::uint32_t image_id) { ck(chgpu_centering_add_image(ctx_, image_id)); }
+    std::array<double, kDescriptorDim> centering_apply() {
+        std::array<double, kDescriptorDim> c{};
+        ck(chgpu_centering_apply(ctx_, c.data()));
+        return c;
+    }
+
+    // hash build + bucket index for resident images (compute_codes + build_bucket_index)
+    void hash(std::span<const std::uint32_t> image_ids, int reduce_rounds = kDefaultReduceRounds) {
+        ck(chgpu_hash_images(ctx_, image_ids.data(), static_cast<std::uint32_t>(image_ids.size()), reduce_rounds));
+    }
+    ImageCodes codes(std::uint32_t image_id) {
+        std::uint32_t n = 0;
+        ck(chgpu_image_points(ctx_, image_id, &n));
+        ImageCodes out;
+        out.params = params_;
+        out.shorts.short_bits = params_.short_bits;
+        out.shorts.table_count = params_.table_count;
+        out.shorts.point_count = n;
+        out.shorts.values.resize(static_cast<std::size_t>(n) * params_.table_count);
+        std::vector<std::uint64_t> words(static_cast<std::size_t>(n) * 2);
+        ck(chgpu_download_codes(ctx_, image_id, out.shorts.values.data(), words.data()));
+        out.longs.long_bits = params_.long_bits;
+        out.longs.codes.resize(n);
+        for (std::uint32_t p = 0; p < n; ++p) {
+            out.longs.codes[p].words = {words[2 * p], words[2 * p + 1]};
+            out.longs.codes[p].bits = static_cast<std::uint16_t>(params_.long_bits);
+        }
+        return out;
+    }
+    void upload_codes(std::uint32_t image_id, const ImageCodes& codes) {
+        std::vector<std::uint64_t> words(codes.longs.codes.size() * 2);
+        for (std::size_t p = 0; p < codes.longs.codes.size(); ++p) {
+            words[2 * p] = codes.longs.codes[p].words[0];
+            words[2 * p + 1] = codes.longs.codes[p].words[1];
+        }
+        static const std::uint32_t none32 = 0;
+        static const std::uint64_t none64 = 0;
+        ck(chgpu_upload_codes(ctx_, image_id, codes.shorts.values.empty() ? &none32 : codes.shorts.values.data(),
+                              words.empty() ? &none64 : words.data()));
+    }
+    BucketIndex bucket_index(std::uint32_t image_id) {
+        std::uint32_t n = 0;
+        ck(chgpu_image_points(ctx_, image_id, &n));
+        const std::uint32_t L = params_.table_count, nb = 1u << params_.short_bits;
+        std::vector<std::uint32_t> offs(static_cast<std::size_t>(L) * (nb + 1)), pts(static_cast<std::size_t>(L) * n);
+        ck(chgpu_download_bucket_index(ctx_, image_id, offs.data(), pts.data()));
+        BucketIndex idx;
+        idx.short_bits = params_.short_bits;
+        idx.point_count = n;
+        idx.tables.resize(L);
+        for (std::uint32_t t = 0; t < L; ++t) {  // dense CSR -> CSR over the non-empty codes (matcher.cpp:27-51)
+            BucketIndex::Table& tb = idx.tables[t];
+            const std::uint32_t* o = offs.data() + static_cast<std::size_t>(t) * (nb + 1);
+            for (std::uint32_t c = 0; c < nb; ++c)
+                if (o[c + 1] != o[c]) {
+                    tb.codes.push_back(c);
+                    tb.offsets.push_back(o[c]);
+                }
+            tb.offsets.push_back(n);
+            tb.points.assign(pts.begin() + static_cast<std::size_t>(t) * n, pts.begin() + static_cast<std::size_t>(t + 1) * n);
+        }
+        return idx;
+    }
+
+    // match a pair list; results in pair order, records of a pair ascending in query index
+    std::vector<PairMatches> match_pairs(std::span<const std::pair<std::uint32_t, std::uint32_t>> pairs,
+                                         const MatchConfig& cfg, MatchStats* stats = nullptr) {
+        std::vector<PairMatches> out(pairs.size());
+        for (std::size_t k = 0; k < pairs.size(); ++k) {
+            out[k].image_i = pairs[k].first;
+            out[k].image_j = pairs[k].second;
+        }
+        match_pairs_stream(pairs, cfg,
+                           [&](std::uint32_t first, std::span<const std::uint64_t> offs, std::span<const MatchRecord> rec) {
+                               for (std::size_t k = 0; k + 1 < offs.size(); ++k)
+                                   out[first + k].matches.assign(rec.begin() + offs[k], rec.begin() + offs[k + 1]);
+                           },
+                           stats);
+        return out;
+    }
+
+    // streaming form: sink(first_pair, offsets (k+1), records) per sub-batch, in pair order, while
+    // the next sub-batch is already computing (FileMatchSink::accept, engine.cpp:154-160)
+    using Sink = std::function<void(std::uint32_t, std::span<const std::uint64_t>, std::span<const MatchRecord>)>;
+    void match_pairs_stream(std::span<const std::pair<std::uint32_t, std::uint32_t>> pairs, const MatchConfig& cfg,
+                            const Sink& sink, MatchStats* stats = nullptr) {
+        const chgpu_match_cfg c = detail::to_c(cfg);
+        struct Thunk {
+            const Sink* sink;
+            std::exception_ptr error;
+        } thunk{&sink, nullptr};
+        auto trampoline = [](void* user, std::uint32_t first, std::uint32_t count, const std::uint64_t* offs,
+                             const chgpu_match_record* rec) -> int {
+            Thunk* t = static_cast<Thunk*>(user);
+            try {
+                (*t->sink)(first, {offs, static_cast<std::size_t>(count) + 1},
+                           {reinterpret_cast<const MatchRecord*>(rec), static_cast<std::size_t>(offs[count])});
+                return 0;
+            } catch (...) {
+                t->error = std::current_exception();
+                return 1;
+            }
+        };
+        const chgpu_status st =
+            chgpu_match_pairs_stream(ctx_, reinterpret_cast<const std::uint32_t*>(pairs.data()),
+                                     static_cast<std::uint32_t>(pairs.size()), &c, trampoline, &thunk, stats);
+        if (thunk.error) std::rethrow_exception(thunk.error);
+        ck(st);
+    }
+
+    void sync() { ck(chgpu_sync(ctx_)); }
+
+private:
+    void ck(chgpu_status st) const {
+        if (st != CHGPU_OK) detail::raise(st, chgpu_last_error(ctx_));
+    }
+    chgpu_ctx* ctx_ = nullptr;
+    FamilyParams params_{};
+};
+
+// ---- reference-shaped free functions over a default context ---------------------------------------
+namespace detail {
+
+struct DefaultContext {
+    std::mutex mu;
+    std::unique_ptr<Matcher> matcher;
+    const HashFamily* installed = nullptr;
+    FamilyParams installed_params{};
+    bool has_family = false;
+
+    // Installs `family` (planes + centering) unless it is the one already resident.
+    Matcher& with(const HashFamily& family) {
+        if (!matcher) matcher = std::make_unique<Matcher>(0);
+        if (!has_family || installed != &family || !(installed_params == family.params)) {
+            matcher->set_family(family);
+            installed = &family;
+            installed_params = family.params;
+            has_family = true;
+        } else if (family.centering_set) {
+            // same object, possibly re-centered since the last call
+            if (chgpu_set_centering(matcher->handle(), family.centering.data()) != CHGPU_OK)
+                throw std::runtime_error(chgpu_last_error(matcher->handle()));
+        }
+        return *matcher;
+    }
+};
+
+inline DefaultContext& default_context() {
+    static DefaultContext ctx;
+    return ctx;
+}
+
+inline constexpr std::uint32_t kScratchA = 0xE0000000u, kScratchB = 0xE0000001u;
+
+struct ScopedImage {  // evicts a scratch image on every exit path
+    Matcher& m;
+    std::uint32_t id;
+    ~ScopedImage() {
+        try {
+            m.evict(id);
+        } catch (...) {
+        }
+    }
+};
+
+}  // namespace detail
+
+// Streaming accumulator behind set_centering (hashing.hpp:166-172).  add() sums on the device.
+struct CenteringAccumulator {
+    std::array<std::uint64_t, kDescriptorDim> sums{};
+    std::uint64_t count = 0;
+
+    void add(const FeatureSet& fs) {
+        if (fs.empty()) return;
+        detail::DefaultContext& dc = detail::default_context();
+        std::lock_guard<std::mutex> lock(dc.mu);
+        if (!dc.matcher) dc.matcher = std::make_unique<Matcher>(0);
+        Matcher& m = *dc.matcher;
+        if (!dc.has_family) {  // image blocks are laid out per family; any valid one will do for a sum
+            static const HashFamily scratch = build_hash_family(FamilyParams{});
+            m.set_family(scratch);
+            dc.installed = &scratch;
+            dc.installed_params = scratch.params;
+            dc.has_family = true;
+        }
+        m.upload(detail::kScratchA, fs);
+        detail::ScopedImage guard{m, detail::kScratchA};
+        m.centering_reset();
+        m.centering_add(detail::kScratchA);
+        std::array<std::uint64_t, kDescriptorDim> part{};
+        std::uint64_t n = 0;
+        if (chgpu_centering_get_sums(m.handle(), part.data(), &n) != CHGPU_OK)
+            throw std::runtime_error(chgpu_last_error(m.handle()));
+        for (std::size_t c = 0; c < kDescriptorDim; ++c) sums[c] += part[c];
+        count += n;
+    }
+    void apply(HashFamily& family) const {  // hashing.cpp:59-64
+        if (count == 0) throw std::invalid_argument("set_centering: no descriptors");
+        for (std::size_t c = 0; c < kDescriptorDim; ++c)
+            family.centering[c] = static_cast<double>(sums[c]) / static_cast<double>(count);
+        family.centering_set = true;
+    }
+};
+
+inline void set_centering(HashFamily& family, std::span<const FeatureSet> sets) {  // hashing.hpp:78
+    CenteringAccumulator acc;
+    for (const FeatureSet& fs : sets) acc.add(fs);
+    acc.apply(family);
+}
+
+// compute_codes (hashing.hpp:131): fp64 sign tests in the reference's summation order, on the device.
+inline ImageCodes compute_codes(const HashFamily& family, const FeatureSet& fs, int reduce_rounds = kDefaultReduceRounds) {
+    if (!family.centering_set) throw std::logic_error("compute_codes: centering has not been set");
+    if (reduce_rounds < 0 || reduce_rounds > kMaxReduceRounds)
+        throw std::invalid_argument("reduce_dot tail rounds out of range 0..7");
+    detail::DefaultContext& dc = detail::default_context();
+    std::lock_guard<std::mutex> lock(dc.mu);
+    Matcher& m = dc.with(family);
+    m.upload(detail::kScratchA, fs);
+    detail::ScopedImage guard{m, detail::kScratchA};
+    const std::uint32_t id = detail::kScratchA;
+    m.hash({&id, 1}, reduce_rounds);
+    return m.codes(id);
+}
+
+// build_bucket_index (matcher.hpp:43): counting sort on the device, returned in the reference's CSR form.
+inline BucketIndex build_bucket_index(const ShortCodes& train_codes) {
+    FamilyParams p;
+    p.short_bits = train_codes.short_bits;
+    p.table_count = train_codes.table_count;
+    p.long_bits = std::max<std::uint32_t>(p.short_bits + 1, 128);
+    static std::mutex fam_mu;
+    static std::vector<std::unique_ptr<HashFamily>> families;  // one resident family object per (m, L)
+    const HashFamily* fam = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(fam_mu);
+        for (const auto& f : families)
+            if (f->params == p) fam = f.get();
+        if (!fam) {
+            families.push_back(std::make_unique<HashFamily>(build_hash_family(p)));
+            fam = families.back().get();
+        }
+    }
+    detail::DefaultContext& dc = detail::default_context();
+    std::lock_guard<std::mutex> lock(dc.mu);
+    Matcher& m = dc.with(*fam);
+    FeatureSet blank;
+    blank.keypoints.resize(train_codes.point_count);
+    blank.descriptors.resize(train_codes.point_count);
+    m.upload(detail::kScratchA, blank);
+    detail::ScopedImage guard{m, detail::kScratchA};
+    ImageCodes codes;
+    codes.params = p;
+    codes.shorts = train_codes;
+    codes.longs.long_bits = p.long_bits;
+    codes.longs.codes.resize(train_codes.point_count);
+    m.upload_codes(detail::kScratchA, codes);
+    return m.bucket_index(detail::kScratchA);
+}
+
+// match_pair (matcher.hpp:98-100) with externally supplied codes: one pair through the batch path.
+// The hash family is only needed for its parameters here (codes are given), so any HashFamily with
+// codes_i.params is installed.
+inline std::vector<MatchRecord> match_pair(const FeatureSet& fs_i, const FeatureSet& fs_j, const ImageCodes& codes_i,
+                                           const ImageCodes& codes_j, const MatchConfig& cfg) {
+    if (!(codes_i.params == codes_j.params))
+        throw std::invalid_argument("match_pair: codes come from different hash families");  // matcher.cpp:144
+    if (codes_i.shorts.point_count != fs_i.size() || codes_j.shorts.point_count != fs_j.size())
+        throw std::invalid_argument("match_pair: code/point count mismatch");  // matcher.cpp:146-148
+    static std::mutex fam_mu;
+    static std::vector<std::unique_ptr<HashFamily>> families;
+    const HashFamily* fam = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(fam_mu);
+        for (const auto& f : families)
+            if (f->params == codes_i.params) fam = f.get();
+        if (!fam) {
+            families.push_back(std::make_unique<HashFamily>(build_hash_family(codes_i.params)));
+            fam = families.back().get();
+        }
+    }
+    detail::DefaultContext& dc = detail::default_context();
+    std::lock_guard<std::mutex> lock(dc.mu);
+    Matcher& m = dc.with(*fam);
+    m.upload(detail::kScratchA, fs_i);
+    detail::ScopedImage ga{m, detail::kScratchA};
+    m.upload(detail::kScratchB, fs_j);
+    detail::ScopedImage gb{m, detail::kScratchB};
+    m.upload_codes(detail::kScratchA, codes_i);
+    m.upload_codes(detail::kScratchB, codes_j);
+    const std::pair<std::uint32_t, std::uint32_t> pr{detail::kScratchA, detail::kScratchB};
+    std::vector<PairMatches> out = m.match_pairs({&pr, 1}, cfg);
+    return std::move(out.front().matches);
+}
+
+}  // namespace cashash_b200

@@ -1,0 +1,331 @@
+// facade_test.cpp — exercises include/cashash_b200/cashash.hpp (the reference-shaped C++ host API
+// over libchgpu.so) against the CPU oracle's C ABI (oracle/chor.h).  Reads like a test of the
+// reference's own library: build_hash_family -> set_centering -> compute_codes -> match_pair ->
+// save_matches.  `--host` runs only the checks that need no GPU.
+//
+// Built and run by tests/test_cpp_facade.py:
+//   g++ -std=c++20 -I include -I oracle tests/cpp/facade_test.cpp -L... -lchgpu -lchoracle
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <iostream>
+#include <random>
+#include <sstream>
+
+#include "cashash_b200/cashash.hpp"
+#include "chor.h"
+
+namespace ch = cashash_b200;
+
+static int g_checks = 0;
+#define CHECK(cond)                                                                     \
+    do {                                                                                \
+        ++g_checks;                                                                     \
+        if (!(cond)) {                                                                  \
+            std::fprintf(stderr, "FAILED %s:%d: %s\n", __FILE__, __LINE__, #cond);      \
+            std::exit(1);                                                               \
+        }                                                                               \
+    } while (0)
+
+template <class E, class F>
+static bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+// uniform u8 descriptors; the first `twins` points are sigma=8 noisy copies of a shared pool
+static ch::FeatureSet make_image(std::uint64_t seed, std::uint32_t n, std::uint32_t twins, const std::string& id) {
+    std::mt19937_64 pool_rng(12345), rng(seed);
+    std::normal_distribution<double> noise(0.0, 8.0);
+    ch::FeatureSet fs;
+    fs.image_id = id;
+    fs.keypoints.resize(n);
+    fs.descriptors.resize(n);
+    for (std::uint32_t p = 0; p < n; ++p) {
+        fs.keypoints[p] = {float(p % 1000), float(p / 1000), 2.0f, 0.0f};
+        for (std::size_t c = 0; c < ch::kDescriptorDim; ++c) {
+            if (p < twins) {
+                const double base = double(pool_rng() & 0xff);
+                const double v = std::min(255.0, std::max(0.0, base + noise(rng)));
+                fs.descriptors[p][c] = std::uint8_t(v);
+            } else {
+                fs.descriptors[p][c] = std::uint8_t(rng() & 0xff);
+            }
+        }
+    }
+    return fs;
+}
+
+static std::string slurp(const std::filesystem::path& p) {
+    std::ifstream in(p, std::ios::binary);
+    std::ostringstream os;
+    os << in.rdbuf();
+    return os.str();
+}
+
+static chor_family_params to_chor(const ch::FamilyParams& p) { return {p.short_bits, p.long_bits, p.table_count, p.seed}; }
+static chor_match_cfg to_chor(const ch::MatchConfig& c) {
+    return {c.top_k, c.hamming_threshold, c.ratio, c.min_candidates_for_ratio, c.reduce_rounds};
+}
+
+struct OracleCodes {
+    std::vector<std::uint32_t> shorts;
+    std::vector<std::uint64_t> longs;
+};
+
+static OracleCodes oracle_codes(const ch::HashFamily& fam, const ch::FeatureSet& fs, int rr = 3) {
+    OracleCodes oc;
+    oc.shorts.resize(fs.size() * fam.params.table_count);
+    oc.longs.resize(fs.size() * 2);
+    const chor_family_params p = to_chor(fam.params);
+    const int rc = chor_compute_codes(&p, fam.short_planes.front().data(), fam.long_planes.front().data(),
+                                      fam.centering.data(), rr, fs.descriptors.empty() ? nullptr : fs.descriptors.front().data(),
+                                      std::uint32_t(fs.size()), oc.shorts.data(), oc.longs.data());
+    CHECK(rc == 0);
+    return oc;
+}
+
+static std::vector<ch::MatchRecord> oracle_match(const ch::HashFamily& fam, const ch::MatchConfig& cfg, const ch::FeatureSet& a,
+                                                 const OracleCodes& ca, const ch::FeatureSet& b, const OracleCodes& cb) {
+    std::vector<ch::MatchRecord> rec(a.size() + 1);
+    std::uint32_t count = 0;
+    const chor_family_params p = to_chor(fam.params);
+    const chor_match_cfg c = to_chor(cfg);
+    const int rc = chor_match_pair(&p, &c, a.descriptors.front().data(), std::uint32_t(a.size()), ca.shorts.data(), ca.longs.data(),
+                                   b.descriptors.front().data(), std::uint32_t(b.size()), cb.shorts.data(), cb.longs.data(),
+                                   reinterpret_cast<chor_match_record*>(rec.data()), &count, nullptr, nullptr, nullptr);
+    CHECK(rc == 0);
+    rec.resize(count);
+    return rec;
+}
+
+static void host_checks(const std::filesystem::path& tmp) {
+    // build_hash_family: bit-identical to the oracle's planes; bad parameters throw invalid_argument
+    for (const ch::FamilyParams& p : {ch::FamilyParams{}, ch::FamilyParams{10, 96, 4, 99}}) {
+        const ch::HashFamily fam = ch::build_hash_family(p);
+        std::vector<double> sp(fam.short_planes.size() * 128), lp(fam.long_planes.size() * 128);
+        const chor_family_params cp = to_chor(p);
+        CHECK(chor_build_family(&cp, sp.data(), lp.data()) == 0);
+        CHECK(std::memcmp(sp.data(), fam.short_planes.front().data(), sp.size() * 8) == 0);
+        CHECK(std::memcmp(lp.data(), fam.long_planes.front().data(), lp.size() * 8) == 0);
+        CHECK(!fam.centering_set);
+    }
+    CHECK(throws<std::invalid_argument>([] { ch::build_hash_family({0, 128, 6, 1}); }));
+    CHECK(throws<std::invalid_argument>([] { ch::build_hash_family({8, 8, 6, 1}); }));
+    CHECK(throws<std::invalid_argument>([] { ch::build_hash_family({8, 129, 6, 1}); }));
+    CHECK(throws<std::invalid_argument>([] { ch::build_hash_family({8, 128, 0, 1}); }));
+
+    // CHFT round trip and the reference's fault classes / byte offsets (feature_io.cpp:65-106)
+    const ch::FeatureSet fs = make_image(3, 37, 5, "img");
+    const auto f = tmp / "a.chft";
+    ch::save_features(fs, f);
+    CHECK(std::filesystem::file_size(f) == 16 + 37 * 144);
+    const ch::FeatureSet back = ch::load_features(f);
+    CHECK(back.keypoints == fs.keypoints && back.descriptors == fs.descriptors);
+    auto fault_of = [&](const std::filesystem::path& p, ch::FeatureFileFault want, std::uint64_t off) {
+        try {
+            ch::load_features(p);
+        } catch (const ch::FeatureFileError& e) {
+            return e.fault() == want && e.byte_offset() == off;
+        }
+        return false;
+    };
+    CHECK(fault_of(tmp / "nope.chft", ch::FeatureFileFault::MissingFile, 0));
+    std::string blob = slurp(f);
+    auto write = [&](const std::string& name, const std::string& bytes) {
+        std::ofstream(tmp / name, std::ios::binary).write(bytes.data(), std::streamsize(bytes.size()));
+        return tmp / name;
+    };
+    CHECK(fault_of(write("short_header", blob.substr(0, 9)), ch::FeatureFileFault::Truncated, 9));
+    std::string bad = blob;
+    bad[0] = 'X';
+    CHECK(fault_of(write("bad_magic", bad), ch::FeatureFileFault::BadMagic, 0));
+    bad = blob;
+    bad[4] = 2;
+    CHECK(fault_of(write("bad_version", bad), ch::FeatureFileFault::BadVersion, 4));
+    CHECK(fault_of(write("cut", blob.substr(0, 16 + 144 * 10 + 77)), ch::FeatureFileFault::Truncated, 16 + 144 * 10 + 77));
+    CHECK(throws<ch::FeatureFileError>([&] { ch::save_features(fs, tmp / "no_such_dir" / "x.chft"); }));
+
+    // save_matches: byte-identical to the oracle's writer; integers print without a decimal point
+    std::vector<ch::MatchRecord> rec = {{0, 5, 1250.0}, {3, 1, 0.5}, {9, 2, 8323200.0}, {11, 7, 1e-3}};
+    ch::save_matches("imgA", "imgB", rec, tmp / "m_ours.txt");
+    CHECK(chor_save_matches("imgA", "imgB", reinterpret_cast<const chor_match_record*>(rec.data()), 4,
+                            (tmp / "m_ref.txt").string().c_str()) == 0);
+    CHECK(slurp(tmp / "m_ours.txt") == slurp(tmp / "m_ref.txt"));
+    CHECK(slurp(tmp / "m_ours.txt").rfind("# imgA imgB 4\n0 5 1250\n", 0) == 0);
+    CHECK(ch::pair_file_name(3, 41) == "match_000003_000041.txt");
+    CHECK(throws<ch::FeatureFileError>([&] { ch::save_matches("a", "b", rec, tmp / "no_such_dir" / "m.txt"); }));
+
+    // plan_exhaustive: every unordered pair exactly once, a < b
+    const auto pairs = ch::plan_exhaustive(23, 4, 3);
+    CHECK(pairs.size() == 23 * 22 / 2);
+    std::vector<char> seen(23 * 23, 0);
+    for (const auto& [a, b] : pairs) {
+        CHECK(a < b && b < 23 && !seen[a * 23 + b]);
+        seen[a * 23 + b] = 1;
+    }
+    CHECK(throws<std::invalid_argument>([] { ch::plan_exhaustive(0, 1, 1); }));
+}
+
+static void device_checks(const std::filesystem::path& tmp) {
+    ch::HashFamily fam = ch::build_hash_family(ch::FamilyParams{});
+    std::vector<ch::FeatureSet> sets;
+    for (int i = 0; i < 4; ++i) sets.push_back(make_image(100 + i, i == 3 ? 700 : 1000, 300, "img" + std::to_string(i)));
+
+    // compute_codes before set_centering is a logic error (hashing.cpp:131-132)
+    CHECK(throws<std::logic_error>([&] { ch::compute_codes(fam, sets[0]); }));
+    CHECK(throws<std::invalid_argument>([&] {
+        ch::HashFamily f2 = fam;
+        ch::set_centering(f2, std::span<const ch::FeatureSet>{});
+    }));
+
+    // set_centering: exact integer sums / count
+    ch::set_centering(fam, sets);
+    std::uint64_t sums[128] = {0}, count = 0;
+    for (const auto& fs : sets) CHECK(chor_centering_accumulate(fs.descriptors.front().data(), fs.size(), sums, &count) == 0);
+    double want[128];
+    CHECK(chor_centering_apply(sums, count, want) == 0);
+    CHECK(fam.centering_set && std::memcmp(want, fam.centering.data(), sizeof(want)) == 0);
+    CHECK(throws<std::invalid_argument>([&] { ch::compute_codes(fam, sets[0], 8); }));
+
+    // compute_codes: bit-exact short and long codes, for the default and the extreme reduction orders
+    std::vector<ch::ImageCodes> codes;
+    std::vector<OracleCodes> ocodes;
+    for (const auto& fs : sets) {
+        codes.push_back(ch::compute_codes(fam, fs));
+        ocodes.push_back(oracle_codes(fam, fs));
+        const ch::ImageCodes& c = codes.back();
+        CHECK(c.params == fam.params && c.shorts.point_count == fs.size() && c.longs.long_bits == 128);
+        CHECK(c.shorts.values == ocodes.back().shorts);
+        for (std::size_t p = 0; p < fs.size(); ++p)
+            CHECK(c.longs.codes[p].words[0] == ocodes.back().longs[2 * p] && c.longs.codes[p].words[1] == ocodes.back().longs[2 * p + 1] &&
+                  c.longs.codes[p].bits == 128);
+    }
+    for (int rr : {0, 7}) CHECK(ch::compute_codes(fam, sets[1], rr).shorts.values == oracle_codes(fam, sets[1], rr).shorts);
+
+    // build_bucket_index: the reference's CSR over the non-empty codes, ascending ids inside a bucket
+    {
+        const ch::BucketIndex idx = ch::build_bucket_index(codes[1].shorts);
+        const std::uint32_t n = std::uint32_t(sets[1].size());
+        std::vector<std::uint32_t> offs(6 * 257), pts(6 * n);
+        CHECK(chor_build_bucket_index(8, 6, ocodes[1].shorts.data(), n, offs.data(), pts.data()) == 0);
+        CHECK(idx.tables.size() == 6 && idx.point_count == n && idx.short_bits == 8);
+        for (std::uint32_t t = 0; t < 6; ++t)
+            for (std::uint32_t c = 0; c < 256; ++c) {
+                const auto b = idx.bucket(t, c);
+                const std::uint32_t lo = offs[t * 257 + c], hi = offs[t * 257 + c + 1];
+                CHECK(b.size() == hi - lo);
+                for (std::uint32_t k = 0; k < b.size(); ++k) CHECK(b[k] == pts[t * n + lo + k]);
+            }
+    }
+
+    // match_pair: identical MatchRecords, several configurations incl. the re-rank fallback being off
+    ch::MatchConfig strict;
+    strict.hamming_threshold = 128;
+    ch::MatchConfig loose;
+    loose.top_k = 4;
+    loose.ratio = 0.9;
+    loose.min_candidates_for_ratio = 3;
+    for (const ch::MatchConfig& cfg : {ch::MatchConfig{}, strict, loose}) {
+        const auto got = ch::match_pair(sets[0], sets[1], codes[0], codes[1], cfg);
+        const auto want_rec = oracle_match(fam, cfg, sets[0], ocodes[0], sets[1], ocodes[1]);
+        CHECK(!want_rec.empty() && got == want_rec);
+    }
+    // ragged pair (1000 x 700) both ways, and empty inputs (matcher.cpp:151)
+    CHECK(ch::match_pair(sets[2], sets[3], codes[2], codes[3], {}) == oracle_match(fam, {}, sets[2], ocodes[2], sets[3], ocodes[3]));
+    CHECK(ch::match_pair(sets[3], sets[2], codes[3], codes[2], {}) == oracle_match(fam, {}, sets[3], ocodes[3], sets[2], ocodes[2]));
+    {
+        ch::FeatureSet none;
+        ch::ImageCodes cnone;
+        cnone.params = fam.params;
+        cnone.shorts.short_bits = 8;
+        cnone.shorts.table_count = 6;
+        cnone.longs.long_bits = 128;
+        CHECK(ch::match_pair(none, sets[1], cnone, codes[1], {}).empty());
+        CHECK(ch::match_pair(sets[1], none, codes[1], cnone, {}).empty());
+    }
+    // argument errors (matcher.cpp:144-148, :9-17)
+    {
+        ch::ImageCodes other = codes[1];
+        other.params.seed = 2;
+        CHECK(throws<std::invalid_argument>([&] { ch::match_pair(sets[0], sets[1], codes[0], other, {}); }));
+        CHECK(throws<std::invalid_argument>([&] { ch::match_pair(sets[0], sets[3], codes[0], codes[1], {}); }));
+        ch::MatchConfig bad;
+        bad.top_k = 1;
+        CHECK(throws<std::invalid_argument>([&] { ch::match_pair(sets[0], sets[1], codes[0], codes[1], bad); }));
+        bad = {};
+        bad.ratio = 1.0;
+        CHECK(throws<std::invalid_argument>([&] { ch::match_pair(sets[0], sets[1], codes[0], codes[1], bad); }));
+        bad = {};
+        bad.hamming_threshold = 129;
+        CHECK(throws<std::invalid_argument>([&] { ch::match_pair(sets[0], sets[1], codes[0], codes[1], bad); }));
+    }
+
+    // batch interface: upload once, centering + hash on the device, whole pair list in one call,
+    // files written with the reference's names and bytes
+    {
+        ch::Matcher m(0);
+        ch::HashFamily fam2 = ch::build_hash_family(ch::FamilyParams{});
+        m.set_family(fam2);
+        std::vector<std::uint32_t> ids;
+        for (std::uint32_t i = 0; i < sets.size(); ++i) {
+            if (i % 2 == 0) {
+                m.upload(i, sets[i]);
+            } else {  // the CHFT path: raw file bytes, split on the device
+                ch::save_features(sets[i], tmp / "img.chft");
+                const std::string blob = slurp(tmp / "img.chft");
+                CHECK(m.upload_chft(i, blob.data(), blob.size()) == sets[i].size());
+            }
+            ids.push_back(i);
+        }
+        m.centering_reset();
+        for (std::uint32_t i : ids) m.centering_add(i);
+        CHECK(m.centering_apply() == fam.centering);
+        m.hash(ids);
+        const auto pairs = ch::plan_exhaustive(4, 2, 2);
+        ch::MatchStats st{};
+        const auto res = m.match_pairs(pairs, {}, &st);
+        CHECK(res.size() == 6 && st.pairs == 6);
+        std::uint64_t total = 0;
+        for (std::size_t k = 0; k < pairs.size(); ++k) {
+            const auto [a, b] = pairs[k];
+            CHECK(res[k].image_i == a && res[k].image_j == b);
+            CHECK(res[k].matches == oracle_match(fam, {}, sets[a], ocodes[a], sets[b], ocodes[b]));
+            total += res[k].matches.size();
+            const auto f = tmp / ch::pair_file_name(a, b);
+            ch::save_matches(sets[a].image_id, sets[b].image_id, res[k].matches, f);
+            CHECK(chor_save_matches(sets[a].image_id.c_str(), sets[b].image_id.c_str(),
+                                    reinterpret_cast<const chor_match_record*>(res[k].matches.data()),
+                                    std::uint32_t(res[k].matches.size()), (tmp / "ref.txt").string().c_str()) == 0);
+            CHECK(slurp(f) == slurp(tmp / "ref.txt"));
+        }
+        CHECK(st.matches == total);
+        // a truncated CHFT blob is refused with the reference's fault class and offset
+        ch::save_features(sets[0], tmp / "img.chft");
+        const std::string blob = slurp(tmp / "img.chft");
+        try {
+            m.upload_chft(99, blob.data(), blob.size() - 5);
+            CHECK(false);
+        } catch (const ch::FeatureFileError& e) {
+            CHECK(e.fault() == ch::FeatureFileFault::Truncated && e.byte_offset() == blob.size() - 5);
+        }
+        CHECK(throws<std::out_of_range>([&] { m.codes(12345); }));
+    }
+}
+
+int main(int argc, char** argv) {
+    const bool host_only = argc > 1 && std::string(argv[1]) == "--host";
+    const std::filesystem::path tmp = std::filesystem::temp_directory_path() / ("chfacade_" + std::to_string(::getpid()));
+    std::filesystem::create_directories(tmp);
+    host_checks(tmp);
+    if (!host_only) device_checks(tmp);
+    std::filesystem::remove_all(tmp);
+    std::printf("facade_test ok: %d checks (%s), oracle = %s\n", g_checks, host_only ? "host only" : "host + device", chor_name());
+    return 0;
+}

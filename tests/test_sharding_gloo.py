@@ -1,0 +1,64 @@
+"""Multi-GPU host logic under gloo on CPU (world sizes 2 and 3): sharding, the 1 KB centering
+exchange and the host-side gather, with worker invariance (SPEC.md:497 / acceptance criterion 8:
+the gathered output does not depend on the number of workers)."""
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle_lib
+import paper_1805_08995_b200 as ch
+
+ROOT = Path(__file__).resolve().parent.parent
+IMAGES, POINTS = 7, 300
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.fixture(scope="module")
+def single_process_truth():
+    orc = oracle_lib.restatement()
+    fam = ch.build_hash_family(ch.FamilyParams())
+    data = ch.make_dataset(IMAGES, POINTS, seed=11)
+    cen = orc.centering([data[i] for i in range(IMAGES)])
+    codes = [orc.compute_codes(fam.params, fam.short_planes, fam.long_planes, cen, data[i]) for i in range(IMAGES)]
+    pairs = ch.plan_exhaustive(IMAGES, 2, 2)
+    recs = [orc.match_pair(fam.params, ch.MatchConfig(), data[a], *codes[a], data[b], *codes[b])[0] for a, b in pairs]
+    return cen, pairs, recs
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_job_is_worker_invariant(tmp_path, single_process_truth, world):
+    cen, pairs, recs = single_process_truth
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           str(ROOT / "tests" / "dist_worker.py"), str(tmp_path), str(IMAGES), str(POINTS)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+
+    g = np.load(tmp_path / "gathered.npz")
+    assert np.array_equal(g["pairs"], pairs)
+    offsets, records = g["offsets"], g["records"]
+    assert len(offsets) == len(pairs) + 1 and offsets[-1] == len(records)
+    for k in range(len(pairs)):  # plan order restored, records identical to the single-process run
+        assert np.array_equal(records[offsets[k]:offsets[k + 1]], recs[k]), k
+
+    spans = []
+    for rank in range(world):
+        z = np.load(tmp_path / f"rank{rank}.npz")
+        assert np.array_equal(z["centering"], cen)  # every rank divides the same exact integer sums
+        spans.append((int(z["first"]), int(z["last"])))
+        mine = pairs[spans[-1][0]:spans[-1][1]]
+        assert set(z["resident"].tolist()) == set(np.unique(mine).tolist())  # only what the shard touches stays
+        assert int(z["uploads"]) <= IMAGES + len(range(rank, IMAGES, world))
+    assert spans[0][0] == 0 and spans[-1][1] == len(pairs)
+    assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+    sizes = [b - a for a, b in spans]
+    assert max(sizes) - min(sizes) <= 1
