@@ -37,7 +37,8 @@ typedef enum chgpu_status {
     CHGPU_ENOMEM = 4,
     CHGPU_EUNSUPPORTED = 5, /* outside the envelope above */
     CHGPU_EFORMAT = 6,      /* reference: FeatureFileError (feature_io.hpp:61-80) */
-    CHGPU_ENOTFOUND = 7     /* unknown image id */
+    CHGPU_ENOTFOUND = 7,    /* unknown image id / no such cache file */
+    CHGPU_EMISMATCH = 8     /* reference: std::runtime_error "code cache parameters mismatch active config" */
 } chgpu_status;
 
 /* hashing.hpp:45-52 FamilyParams */
@@ -153,6 +154,34 @@ chgpu_status chgpu_download_codes(chgpu_ctx* ctx, uint32_t image_id, uint32_t* s
 chgpu_status chgpu_upload_codes(chgpu_ctx* ctx, uint32_t image_id, const uint32_t* shorts, const uint64_t* longs);
 /* Dense CSR of the bucket index: offsets L*(2^m+1) u32, points L*n u32 (bucket-major, ascending id). */
 chgpu_status chgpu_download_bucket_index(chgpu_ctx* ctx, uint32_t image_id, uint32_t* offsets, uint32_t* points);
+
+/* ---- code cache / centering files (interop with the CPU reference, resume) -------------- */
+/* centering_fingerprint (hashing.cpp:151-162): FNV-1a over the 128 doubles' bytes. */
+uint64_t chgpu_centering_fingerprint(const double* centering128);
+/* save_code_cache (hashing.hpp:138-146, hashing.cpp:184-206): "CHCC", u32 version=1, m, n, L, u64 seed,
+ * u64 centering fingerprint, u32 count, u32 reserved; count*L u32 short codes; count*2 u64 long words. */
+chgpu_status chgpu_save_code_cache(const char* path, const chgpu_family_params* p, uint64_t centering_fp,
+                                   uint32_t count, const uint32_t* shorts, const uint64_t* longs);
+/* read_code_cache_header (hashing.cpp:208-226): CHGPU_ENOTFOUND for a missing file, foreign magic,
+ * other version or short header (the reference returns false for all of these). */
+chgpu_status chgpu_read_code_cache_header(const char* path, chgpu_family_params* p, uint64_t* centering_fp,
+                                          uint32_t* count);
+/* load_code_cache / parse_code_cache (hashing.cpp:228-272).  CHGPU_EFORMAT with *fault / *fault_offset as the
+ * reference reports them (a payload cut short is reported at offset UINT64_MAX: the reference casts a failed
+ * tellg()), CHGPU_EMISMATCH when the echoed parameters or fingerprint differ, CHGPU_ENOMEM (with *count set)
+ * when capacity < count.  shorts: count*L u32, longs: count*2 u64. */
+chgpu_status chgpu_load_code_cache(const char* path, const chgpu_family_params* expected, uint64_t expected_fp,
+                                   uint32_t capacity, uint32_t* count, uint32_t* shorts, uint64_t* longs,
+                                   chgpu_file_fault* fault, uint64_t* fault_offset);
+/* Centering file "CHCV" (engine.cpp:522-541): magic, u32 version=1, m, n, L, u64 seed, 128 f64. */
+chgpu_status chgpu_save_centering_file(const char* path, const chgpu_family_params* p, const double* centering128);
+chgpu_status chgpu_load_centering_file(const char* path, chgpu_family_params* p, double* centering128);
+/* Device conveniences: write the codes of a resident image as a CHCC cache (fingerprint of the context's
+ * centering), or install a cache as the image's codes + bucket index (hash build skipped: the reference's
+ * cache_is_current resume path, engine.cpp:575-582).  The image must be resident with the cache's count. */
+chgpu_status chgpu_image_save_code_cache(chgpu_ctx* ctx, uint32_t image_id, const char* path);
+chgpu_status chgpu_image_load_code_cache(chgpu_ctx* ctx, uint32_t image_id, const char* path,
+                                         chgpu_file_fault* fault, uint64_t* fault_offset);
 
 /* ---- match ----------------------------------------------------------------------------- */
 /* Replaces match_pair over a pair list (matcher.hpp:98-100, matcher.cpp:141-203; pair list as in

@@ -402,6 +402,78 @@ int chor_save_matches(const char* id_i, const char* id_j, const chor_match_recor
     return w == out.size() ? 0 : 3;
 }
 
+// centering_fingerprint: FNV-1a over the bytes of the 128 doubles, low byte first (hashing.cpp:151-162).
+int chor_centering_fingerprint(const double* centering128, uint64_t* out) {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (int i = 0; i < kDim; ++i) {
+        unsigned char b[8];
+        std::memcpy(b, centering128 + i, 8);
+        for (int k = 0; k < 8; ++k) h = (h ^ b[k]) * 0x100000001b3ULL;
+    }
+    *out = h;
+    return 0;
+}
+
+// save_code_cache (hashing.cpp:184-206): 44-byte header, then point-major short codes, then long words.
+int chor_save_code_cache(const chor_family_params* p, uint64_t centering_fp, const uint32_t* shorts,
+                         const uint64_t* longs, uint32_t npts, const char* path) {
+    std::string out("CHCC");
+    auto put = [&out](const void* v, size_t n) { out.append(static_cast<const char*>(v), n); };
+    const uint32_t version = 1, reserved = 0;
+    put(&version, 4);
+    put(&p->short_bits, 4);
+    put(&p->long_bits, 4);
+    put(&p->table_count, 4);
+    put(&p->seed, 8);
+    put(&centering_fp, 8);
+    put(&npts, 4);
+    put(&reserved, 4);
+    put(shorts, size_t(npts) * p->table_count * 4);
+    put(longs, size_t(npts) * 16);
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return 3;
+    const bool ok = std::fwrite(out.data(), 1, out.size(), f) == out.size();
+    return (std::fclose(f) == 0 && ok) ? 0 : 3;
+}
+
+// load_code_cache / parse_code_cache (hashing.cpp:228-272).  Fault codes as documented in chor.h.
+int chor_load_code_cache(const char* path, const chor_family_params* expected, uint64_t expected_fp,
+                         uint32_t capacity, uint32_t* shorts, uint64_t* longs, uint32_t* count, int* fault,
+                         uint64_t* fault_offset) {
+    *fault = 0;
+    *fault_offset = 0;
+    *count = 0;
+    FILE* f = std::fopen(path, "rb");
+    if (!f) { *fault = 1; return 0; }  // MissingFile at 0
+    std::vector<unsigned char> b;
+    unsigned char buf[65536];
+    size_t got;
+    while ((got = std::fread(buf, 1, sizeof(buf), f)) > 0) b.insert(b.end(), buf, buf + got);
+    std::fclose(f);
+    if (b.size() < 4 || std::memcmp(b.data(), "CHCC", 4) != 0) { *fault = 2; return 0; }       // BadMagic at 0
+    if (b.size() < 44) { *fault = 4; *fault_offset = 4; return 0; }                              // Truncated "cache header" at 4
+    uint32_t version, m, n, L, cnt;
+    uint64_t seed, fp;
+    std::memcpy(&version, &b[4], 4);
+    std::memcpy(&m, &b[8], 4);
+    std::memcpy(&n, &b[12], 4);
+    std::memcpy(&L, &b[16], 4);
+    std::memcpy(&seed, &b[20], 8);
+    std::memcpy(&fp, &b[28], 8);
+    std::memcpy(&cnt, &b[36], 4);
+    if (version != 1) { *fault = 3; *fault_offset = 4; return 0; }                               // BadVersion at 4
+    if (m != expected->short_bits || n != expected->long_bits || L != expected->table_count || seed != expected->seed ||
+        fp != expected_fp) { *fault = 6; return 0; }
+    *count = cnt;
+    const size_t sb = size_t(cnt) * L * 4, lb = size_t(cnt) * 16;
+    // a short payload surfaces as static_cast<uint64_t>(in.tellg()) on a failed stream, i.e. 2^64 - 1
+    if (b.size() < 44 + sb + lb) { *fault = 4; *fault_offset = std::numeric_limits<uint64_t>::max(); return 0; }
+    if (cnt > capacity) return 3;
+    std::memcpy(shorts, &b[44], sb);
+    std::memcpy(longs, b.data() + 44 + sb, lb);
+    return 0;
+}
+
 int chor_time_match_pairs(const chor_family_params* p, const chor_match_cfg* cfg,
                           const uint8_t* const* desc, const uint32_t* counts,
                           const uint32_t* const* shorts, const uint64_t* const* longs,

@@ -94,6 +94,16 @@ int chor_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
 int chor_brute_force_match(const uint8_t* desc_i, uint32_t n_i, const uint8_t* desc_j, uint32_t n_j,
                            double ratio, chor_match_record* records, uint32_t* record_count);
 
+/* Code cache (hashing.cpp:151-272).  chor_load_code_cache: *fault = 0 ok, 1..5 = FeatureFileFault + 1
+ * (MissingFile..Unwritable), 6 = parameter/fingerprint mismatch (std::runtime_error); returns 0 unless the
+ * arguments are invalid.  shorts/longs must hold `capacity` points. */
+int chor_centering_fingerprint(const double* centering128, uint64_t* out);
+int chor_save_code_cache(const chor_family_params* p, uint64_t centering_fp, const uint32_t* shorts,
+                         const uint64_t* longs, uint32_t npts, const char* path);
+int chor_load_code_cache(const char* path, const chor_family_params* expected, uint64_t expected_fp,
+                         uint32_t capacity, uint32_t* shorts, uint64_t* longs, uint32_t* count, int* fault,
+                         uint64_t* fault_offset);
+
 /* Text match file exactly as the reference writes it (feature_io.cpp:161-183). */
 int chor_save_matches(const char* id_i, const char* id_j, const chor_match_record* records,
                       uint32_t count, const char* path);

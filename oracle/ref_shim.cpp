@@ -273,6 +273,43 @@ int chor_save_matches(const char* id_i, const char* id_j, const chor_match_recor
     });
 }
 
+int chor_centering_fingerprint(const double* centering128, uint64_t* out) {
+    return guarded([&] {
+        HashFamily fam;
+        std::memcpy(fam.centering.data(), centering128, sizeof(fam.centering));
+        *out = centering_fingerprint(fam);
+    });
+}
+
+int chor_save_code_cache(const chor_family_params* p, uint64_t centering_fp, const uint32_t* shorts,
+                         const uint64_t* longs, uint32_t npts, const char* path) {
+    return guarded([&] { save_code_cache(to_codes(to_params(*p), shorts, longs, npts), centering_fp, path); });
+}
+
+int chor_load_code_cache(const char* path, const chor_family_params* expected, uint64_t expected_fp,
+                         uint32_t capacity, uint32_t* shorts, uint64_t* longs, uint32_t* count, int* fault,
+                         uint64_t* fault_offset) {
+    *fault = 0;
+    *fault_offset = 0;
+    *count = 0;
+    try {
+        const ImageCodes c = load_code_cache(path, to_params(*expected), expected_fp);
+        *count = c.shorts.point_count;
+        if (c.shorts.point_count > capacity) return 3;
+        std::memcpy(shorts, c.shorts.values.data(), c.shorts.values.size() * 4);
+        for (uint32_t i = 0; i < c.shorts.point_count; ++i) {
+            longs[2 * size_t(i)] = c.longs.codes[i].words[0];
+            longs[2 * size_t(i) + 1] = c.longs.codes[i].words[1];
+        }
+    } catch (const FeatureFileError& e) {
+        *fault = static_cast<int>(e.fault()) + 1;
+        *fault_offset = e.byte_offset();
+    } catch (const std::runtime_error&) {
+        *fault = 6;
+    }
+    return 0;
+}
+
 int chor_time_match_pairs(const chor_family_params* p, const chor_match_cfg* cfg,
                           const uint8_t* const* desc, const uint32_t* counts,
                           const uint32_t* const* shorts, const uint64_t* const* longs,

@@ -15,7 +15,7 @@ u64p = C.POINTER(C.c_uint64)
 f32p = C.POINTER(C.c_float)
 f64p = C.POINTER(C.c_double)
 
-OK, EINVAL, ELOGIC, ECUDA, ENOMEM, EUNSUPPORTED, EFORMAT, ENOTFOUND = range(8)
+OK, EINVAL, ELOGIC, ECUDA, ENOMEM, EUNSUPPORTED, EFORMAT, ENOTFOUND, EMISMATCH = range(9)
 
 
 class FamilyParamsC(C.Structure):
@@ -79,6 +79,15 @@ SIGNATURES = {
     "chgpu_download_codes": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
     "chgpu_upload_codes": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
     "chgpu_download_bucket_index": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "chgpu_centering_fingerprint": (C.c_uint64, [f64p]),
+    "chgpu_save_code_cache": (C.c_int, [C.c_char_p, C.POINTER(FamilyParamsC), C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "chgpu_read_code_cache_header": (C.c_int, [C.c_char_p, C.POINTER(FamilyParamsC), u64p, u32p]),
+    "chgpu_load_code_cache": (C.c_int, [C.c_char_p, C.POINTER(FamilyParamsC), C.c_uint64, C.c_uint32, u32p, C.c_void_p,
+                                        C.c_void_p, C.POINTER(C.c_int), u64p]),
+    "chgpu_save_centering_file": (C.c_int, [C.c_char_p, C.POINTER(FamilyParamsC), f64p]),
+    "chgpu_load_centering_file": (C.c_int, [C.c_char_p, C.POINTER(FamilyParamsC), f64p]),
+    "chgpu_image_save_code_cache": (C.c_int, [C.c_void_p, C.c_uint32, C.c_char_p]),
+    "chgpu_image_load_code_cache": (C.c_int, [C.c_void_p, C.c_uint32, C.c_char_p, C.POINTER(C.c_int), u64p]),
     "chgpu_match_pairs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(MatchCfgC), C.c_void_p,
                                     C.c_void_p, C.c_uint64, u64p, C.POINTER(MatchStatsC)]),
     "chgpu_match_pairs_stream": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(MatchCfgC), SINK_FN,

@@ -130,6 +130,71 @@ def save_matches(image_id_i: str, image_id_j: str, records: np.ndarray, path: st
         raise FeatureFileError(f"{path}: unwritable path at byte 0", 5, 0)
 
 
+# ---- code cache (CHCC) / centering (CHCV) files: hashing.hpp:138-162, engine.cpp:522-541 ----------------
+class CacheMismatchError(RuntimeError):
+    """std::runtime_error "code cache parameters mismatch active config" (hashing.cpp:244-245)."""
+
+
+def centering_fingerprint(centering: np.ndarray) -> int:
+    c = np.ascontiguousarray(centering, dtype=np.float64)
+    assert c.shape == (128,)
+    return int(N.load().chgpu_centering_fingerprint(c.ctypes.data_as(N.f64p)))
+
+
+def save_code_cache(codes: "ImageCodes", centering_fp: int, path) -> None:
+    p = codes.params.c()
+    s = np.ascontiguousarray(codes.shorts, dtype=np.uint32)
+    l = np.ascontiguousarray(codes.longs, dtype=np.uint64)
+    st = N.load().chgpu_save_code_cache(str(path).encode(), C.byref(p), centering_fp, len(l), s.ctypes.data, l.ctypes.data)
+    if st != N.OK:
+        raise FeatureFileError(f"{path}: unwritable path at byte 0", 5, 0)
+
+
+def read_code_cache_header(path):
+    """(FamilyParams, centering_fp, count) or None (missing file / foreign magic: the reference returns false)."""
+    p = N.FamilyParamsC()
+    fp, cnt = C.c_uint64(0), C.c_uint32(0)
+    st = N.load().chgpu_read_code_cache_header(str(path).encode(), C.byref(p), C.byref(fp), C.byref(cnt))
+    if st != N.OK:
+        return None
+    return FamilyParams(p.short_bits, p.long_bits, p.table_count, p.seed), fp.value, cnt.value
+
+
+def load_code_cache(path, expected: "FamilyParams", expected_centering_fp: int) -> "ImageCodes":
+    lib = N.load()
+    p = expected.c()
+    cnt, fault, off = C.c_uint32(0), C.c_int(0), C.c_uint64(0)
+    hdr = read_code_cache_header(path)
+    cap = hdr[2] if hdr else 0
+    shorts = np.zeros((cap, expected.table_count), dtype=np.uint32)
+    longs = np.zeros((cap, 2), dtype=np.uint64)
+    st = lib.chgpu_load_code_cache(str(path).encode(), C.byref(p), expected_centering_fp, cap, C.byref(cnt),
+                                   shorts.ctypes.data, longs.ctypes.data, C.byref(fault), C.byref(off))
+    if st == N.EFORMAT:
+        raise FeatureFileError(f"{path}: code cache fault {fault.value} at byte {off.value}", fault.value, off.value)
+    if st == N.EMISMATCH:
+        raise CacheMismatchError(f"{path}: code cache parameters mismatch active config")
+    if st != N.OK:
+        _raise(st, f"{path}: load_code_cache failed")
+    return ImageCodes(expected, shorts[: cnt.value], longs[: cnt.value])
+
+
+def save_centering_file(path, params: "FamilyParams", centering: np.ndarray) -> None:
+    p = params.c()
+    c = np.ascontiguousarray(centering, dtype=np.float64)
+    if N.load().chgpu_save_centering_file(str(path).encode(), C.byref(p), c.ctypes.data_as(N.f64p)) != N.OK:
+        raise FeatureFileError(f"{path}: unwritable path at byte 0", 5, 0)
+
+
+def load_centering_file(path):
+    p = N.FamilyParamsC()
+    c = np.zeros(128, dtype=np.float64)
+    st = N.load().chgpu_load_centering_file(str(path).encode(), C.byref(p), c.ctypes.data_as(N.f64p))
+    if st != N.OK:
+        raise FeatureFileError(f"{path}: not a centering file", 1 if st == N.ENOTFOUND else 2, 0)
+    return FamilyParams(p.short_bits, p.long_bits, p.table_count, p.seed), c
+
+
 def pair_file_name(i: int, j: int) -> str:
     buf = C.create_string_buffer(48)
     N.load().chgpu_pair_file_name(i, j, buf)
@@ -303,6 +368,19 @@ class Matcher:
         s = np.ascontiguousarray(codes.shorts, dtype=np.uint32)
         l = np.ascontiguousarray(codes.longs, dtype=np.uint64)
         self._ck(self.lib.chgpu_upload_codes(self.h, image_id, s.ctypes.data, l.ctypes.data))
+
+    def save_code_cache(self, image_id: int, path):
+        self._ck(self.lib.chgpu_image_save_code_cache(self.h, image_id, str(path).encode()))
+
+    def load_code_cache(self, image_id: int, path):
+        """Installs a CHCC cache as the image's codes (hash build skipped); raises like the reference."""
+        fault, off = C.c_int(0), C.c_uint64(0)
+        st = self.lib.chgpu_image_load_code_cache(self.h, image_id, str(path).encode(), C.byref(fault), C.byref(off))
+        if st == N.EFORMAT:
+            raise FeatureFileError(self.lib.chgpu_last_error(self.h).decode(), fault.value, off.value)
+        if st == N.EMISMATCH:
+            raise CacheMismatchError(self.lib.chgpu_last_error(self.h).decode())
+        self._ck(st)
 
     def bucket_index(self, image_id: int) -> BucketIndex:
         n = self.points(image_id)

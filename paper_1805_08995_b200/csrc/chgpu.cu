@@ -139,6 +139,7 @@ struct chgpu_ctx {
     chgpu_family_params fam{};
     double* d_planes = nullptr;
     double* d_centering = nullptr;
+    double h_centering[128] = {0};  // host copy (code-cache fingerprints)
     unsigned long long* d_sums = nullptr;
     uint64_t sum_count = 0;
     uint64_t extra_sums[128] = {0};  // sums merged from other ranks
@@ -659,6 +660,7 @@ const char* chgpu_status_name(chgpu_status s) {
         case CHGPU_EUNSUPPORTED: return "unsupported";
         case CHGPU_EFORMAT: return "format error";
         case CHGPU_ENOTFOUND: return "not found";
+        case CHGPU_EMISMATCH: return "parameter mismatch";
     }
     return "?";
 }
@@ -850,6 +852,7 @@ chgpu_status chgpu_set_centering(chgpu_ctx* ctx, const double* centering128) {
     DeviceGuard guard(ctx->device);
     CK(cudaStreamSynchronize(ctx->compute));
     CK(cudaMemcpy(ctx->d_centering, centering128, 128 * sizeof(double), cudaMemcpyHostToDevice));
+    memcpy(ctx->h_centering, centering128, sizeof(ctx->h_centering));
     ctx->has_centering = true;
     return CHGPU_OK;
 }
@@ -1065,6 +1068,41 @@ chgpu_status chgpu_download_bucket_index(chgpu_ctx* ctx, uint32_t image_id, uint
         for (size_t i = 0; i < tmp.size(); ++i) points[i] = tmp[i];
     }
     return CHGPU_OK;
+}
+
+// ---- code caches ----------------------------------------------------------------------------------
+chgpu_status chgpu_image_save_code_cache(chgpu_ctx* ctx, uint32_t image_id, const char* path) {
+    if (!ctx || !path) return CHGPU_EINVAL;
+    if (!ctx->has_centering) return fail(ctx, CHGPU_ELOGIC, "code cache: centering has not been set");
+    uint32_t slot;
+    if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
+    const uint32_t n = ctx->images[slot].dev.n;
+    std::vector<uint32_t> shorts(size_t(n) * ctx->fam.table_count);
+    std::vector<uint64_t> longs(size_t(n) * 2);
+    if (const chgpu_status s = chgpu_download_codes(ctx, image_id, shorts.data(), longs.data())) return s;
+    const chgpu_status s = chgpu_save_code_cache(path, &ctx->fam, chgpu_centering_fingerprint(ctx->h_centering), n,
+                                                 shorts.data(), longs.data());
+    if (s != CHGPU_OK) return fail(ctx, s, "%s: unwritable path at byte 0", path);
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_image_load_code_cache(chgpu_ctx* ctx, uint32_t image_id, const char* path, chgpu_file_fault* fault,
+                                         uint64_t* fault_offset) {
+    if (!ctx || !path) return CHGPU_EINVAL;
+    if (!ctx->has_centering) return fail(ctx, CHGPU_ELOGIC, "code cache: centering has not been set");
+    uint32_t slot;
+    if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
+    const uint32_t n = ctx->images[slot].dev.n;
+    std::vector<uint32_t> shorts(std::max<size_t>(1, size_t(n) * ctx->fam.table_count));
+    std::vector<uint64_t> longs(std::max<size_t>(1, size_t(n) * 2));
+    uint32_t count = 0;
+    const chgpu_status s = chgpu_load_code_cache(path, &ctx->fam, chgpu_centering_fingerprint(ctx->h_centering), n, &count,
+                                                 shorts.data(), longs.data(), fault, fault_offset);
+    if (s == CHGPU_EMISMATCH) return fail(ctx, s, "%s: code cache parameters mismatch active config", path);
+    if (s == CHGPU_ENOMEM || (s == CHGPU_OK && count != n))  // cache_is_current also compares the point count (engine.cpp:581)
+        return fail(ctx, CHGPU_EMISMATCH, "%s: code cache holds %u points, image %u has %u", path, count, image_id, n);
+    if (s != CHGPU_OK) return fail(ctx, s, "%s: unreadable code cache", path);
+    return chgpu_upload_codes(ctx, image_id, shorts.data(), longs.data());
 }
 
 // ---- match --------------------------------------------------------------------------------------

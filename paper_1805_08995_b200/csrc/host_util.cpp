@@ -159,6 +159,169 @@ chgpu_status chgpu_plan_exhaustive(uint32_t image_count, uint32_t block_images, 
     return CHGPU_OK;
 }
 
+// ---- code cache (CHCC) and centering (CHCV) files ------------------------------------------------
+uint64_t chgpu_centering_fingerprint(const double* centering128) {
+    // FNV-1a, byte by byte from the least significant byte of each double (hashing.cpp:151-162)
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (int i = 0; i < 128; ++i) {
+        uint64_t bits;
+        std::memcpy(&bits, centering128 + i, 8);
+        for (int b = 0; b < 8; ++b) {
+            h ^= (bits >> (8 * b)) & 0xff;
+            h *= 0x100000001b3ULL;
+        }
+    }
+    return h;
+}
+
+namespace {
+struct CacheHeader {  // 44 bytes on disk, little-endian, no padding between fields
+    char magic[4];
+    uint32_t version, short_bits, long_bits, table_count;
+    uint64_t seed, centering_fp;
+    uint32_t count, reserved;
+};
+constexpr size_t kCacheHeaderBytes = 44;
+
+void pack_header(const CacheHeader& h, unsigned char* out) {
+    std::memcpy(out, h.magic, 4);
+    std::memcpy(out + 4, &h.version, 4);
+    std::memcpy(out + 8, &h.short_bits, 4);
+    std::memcpy(out + 12, &h.long_bits, 4);
+    std::memcpy(out + 16, &h.table_count, 4);
+    std::memcpy(out + 20, &h.seed, 8);
+    std::memcpy(out + 28, &h.centering_fp, 8);
+    std::memcpy(out + 36, &h.count, 4);
+    std::memcpy(out + 40, &h.reserved, 4);
+}
+}  // namespace
+
+chgpu_status chgpu_save_code_cache(const char* path, const chgpu_family_params* p, uint64_t centering_fp,
+                                   uint32_t count, const uint32_t* shorts, const uint64_t* longs) {
+    if (!path || !p || (count && (!shorts || !longs))) return CHGPU_EINVAL;
+    std::vector<unsigned char> out(kCacheHeaderBytes + size_t(count) * p->table_count * 4 + size_t(count) * 16);
+    CacheHeader h{{'C', 'H', 'C', 'C'}, 1, p->short_bits, p->long_bits, p->table_count, p->seed, centering_fp, count, 0};
+    unsigned char head[kCacheHeaderBytes];
+    pack_header(h, head);
+    std::memcpy(out.data(), head, 44);
+    if (count) {
+        std::memcpy(out.data() + 44, shorts, size_t(count) * p->table_count * 4);
+        std::memcpy(out.data() + 44 + size_t(count) * p->table_count * 4, longs, size_t(count) * 16);
+    }
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return CHGPU_EFORMAT;  // FeatureFileFault::Unwritable
+    const size_t w = std::fwrite(out.data(), 1, out.size(), f);
+    const int c = std::fclose(f);
+    return (w == out.size() && c == 0) ? CHGPU_OK : CHGPU_EFORMAT;
+}
+
+namespace {
+// Parses the 44-byte header; returns 0 ok, 1 bad magic, 2 truncated header.
+int parse_header(const unsigned char* b, size_t n, CacheHeader& h) {
+    if (n < 4 || std::memcmp(b, "CHCC", 4) != 0) return 1;
+    if (n < 44) return 2;
+    std::memcpy(&h.version, b + 4, 4);
+    std::memcpy(&h.short_bits, b + 8, 4);
+    std::memcpy(&h.long_bits, b + 12, 4);
+    std::memcpy(&h.table_count, b + 16, 4);
+    std::memcpy(&h.seed, b + 20, 8);
+    std::memcpy(&h.centering_fp, b + 28, 8);
+    std::memcpy(&h.count, b + 36, 4);
+    std::memcpy(&h.reserved, b + 40, 4);
+    return 0;
+}
+
+bool read_file(const char* path, std::vector<unsigned char>& out, size_t limit = ~size_t(0)) {
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return false;
+    unsigned char buf[1 << 16];
+    size_t got;
+    while (out.size() < limit && (got = std::fread(buf, 1, sizeof(buf), f)) > 0) out.insert(out.end(), buf, buf + got);
+    std::fclose(f);
+    return true;
+}
+}  // namespace
+
+chgpu_status chgpu_read_code_cache_header(const char* path, chgpu_family_params* p, uint64_t* centering_fp,
+                                          uint32_t* count) {
+    if (!path || !p || !centering_fp || !count) return CHGPU_EINVAL;
+    std::vector<unsigned char> bytes;
+    if (!read_file(path, bytes, 44)) return CHGPU_ENOTFOUND;
+    CacheHeader h{};
+    if (parse_header(bytes.data(), bytes.size(), h) != 0 || h.version != 1) return CHGPU_ENOTFOUND;
+    *p = chgpu_family_params{h.short_bits, h.long_bits, h.table_count, h.seed};
+    *centering_fp = h.centering_fp;
+    *count = h.count;
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_load_code_cache(const char* path, const chgpu_family_params* expected, uint64_t expected_fp,
+                                   uint32_t capacity, uint32_t* count, uint32_t* shorts, uint64_t* longs,
+                                   chgpu_file_fault* fault, uint64_t* fault_offset) {
+    if (!path || !expected || !count) return CHGPU_EINVAL;
+    auto bad = [&](chgpu_file_fault f, uint64_t off) {
+        if (fault) *fault = f;
+        if (fault_offset) *fault_offset = off;
+        return CHGPU_EFORMAT;
+    };
+    if (fault) *fault = CHGPU_FAULT_NONE;
+    std::vector<unsigned char> bytes;
+    if (!read_file(path, bytes)) return bad(CHGPU_FAULT_MISSING_FILE, 0);
+    CacheHeader h{};
+    const int hr = parse_header(bytes.data(), bytes.size(), h);
+    if (hr == 1) return bad(CHGPU_FAULT_BAD_MAGIC, 0);
+    if (hr == 2) return bad(CHGPU_FAULT_TRUNCATED, 4);  // "cache header"
+    if (h.version != 1) return bad(CHGPU_FAULT_BAD_VERSION, 4);
+    if (h.short_bits != expected->short_bits || h.long_bits != expected->long_bits ||
+        h.table_count != expected->table_count || h.seed != expected->seed || h.centering_fp != expected_fp)
+        return CHGPU_EMISMATCH;
+    *count = h.count;
+    const size_t sbytes = size_t(h.count) * h.table_count * 4, lbytes = size_t(h.count) * 16;
+    // the reference reads value by value and reports a short payload through a failed tellg(): offset -1
+    if (bytes.size() < 44 + sbytes + lbytes) return bad(CHGPU_FAULT_TRUNCATED, ~uint64_t(0));
+    if (h.count > capacity) return CHGPU_ENOMEM;
+    if (h.count) {
+        if (!shorts || !longs) return CHGPU_EINVAL;
+        std::memcpy(shorts, bytes.data() + 44, sbytes);
+        std::memcpy(longs, bytes.data() + 44 + sbytes, lbytes);
+    }
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_save_centering_file(const char* path, const chgpu_family_params* p, const double* centering128) {
+    if (!path || !p || !centering128) return CHGPU_EINVAL;
+    unsigned char out[4 + 4 + 12 + 8 + 1024];
+    std::memcpy(out, "CHCV", 4);
+    const uint32_t version = 1;
+    std::memcpy(out + 4, &version, 4);
+    std::memcpy(out + 8, &p->short_bits, 4);
+    std::memcpy(out + 12, &p->long_bits, 4);
+    std::memcpy(out + 16, &p->table_count, 4);
+    std::memcpy(out + 20, &p->seed, 8);
+    std::memcpy(out + 28, centering128, 1024);
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return CHGPU_EFORMAT;
+    const size_t w = std::fwrite(out, 1, sizeof(out), f);
+    const int c = std::fclose(f);
+    return (w == sizeof(out) && c == 0) ? CHGPU_OK : CHGPU_EFORMAT;
+}
+
+chgpu_status chgpu_load_centering_file(const char* path, chgpu_family_params* p, double* centering128) {
+    if (!path || !p || !centering128) return CHGPU_EINVAL;
+    std::vector<unsigned char> b;
+    if (!read_file(path, b)) return CHGPU_ENOTFOUND;
+    uint32_t version = 0;
+    if (b.size() != 28 + 1024 || std::memcmp(b.data(), "CHCV", 4) != 0) return CHGPU_EFORMAT;
+    std::memcpy(&version, b.data() + 4, 4);
+    if (version != 1) return CHGPU_EFORMAT;
+    std::memcpy(&p->short_bits, b.data() + 8, 4);
+    std::memcpy(&p->long_bits, b.data() + 12, 4);
+    std::memcpy(&p->table_count, b.data() + 16, 4);
+    std::memcpy(&p->seed, b.data() + 20, 8);
+    std::memcpy(centering128, b.data() + 28, 1024);
+    return CHGPU_OK;
+}
+
 void chgpu_shard_range(uint64_t npairs, uint32_t rank, uint32_t world, uint64_t* first, uint64_t* last) {
     if (world == 0) world = 1;
     const uint64_t base = npairs / world, rem = npairs % world;

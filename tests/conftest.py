@@ -45,7 +45,7 @@ def reference():
 def golden():
     import numpy as np
     g = ROOT / "tests" / "golden"
-    return {name: np.load(g / f"{name}.npz") for name in ("family", "small_dataset", "plans")}
+    return {name: np.load(g / f"{name}.npz") for name in ("family", "small_dataset", "plans", "cache")}
 
 
 @pytest.fixture(scope="session")

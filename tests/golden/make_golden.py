@@ -94,6 +94,13 @@ def main() -> None:
         plans[f"pairs_{k}_{np_}_{m}"] = pairs
         plans[f"sizes_{k}_{np_}_{m}"] = sizes
     np.savez_compressed(OUT / "plans.npz", **plans)
+    # ---- code cache written by the reference (hashing.cpp:184-206) for image 0 of the small dataset --
+    cache = {"centering_fp": np.uint64(ref.centering_fingerprint(centering))}
+    with tempfile.TemporaryDirectory() as td:
+        p = Path(td) / "c.chcc"
+        ref.save_code_cache(params, int(cache["centering_fp"]), codes[0][0], codes[0][1], p)
+        cache["chcc_image0"] = np.frombuffer(p.read_bytes(), dtype=np.uint8)
+    np.savez_compressed(OUT / "cache.npz", **cache)
     print("wrote", [p.name for p in OUT.glob("*.npz")])
 
 

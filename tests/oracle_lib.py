@@ -64,6 +64,9 @@ class Oracle:
             "chor_save_matches": [C.c_char_p, C.c_char_p, P, U32, C.c_char_p],
             "chor_time_match_pairs": [P, P, P, P, P, P, P, U32, U32, P, P],
             "chor_plan_exhaustive": [U32, U32, U32, P, P, P, P],
+            "chor_centering_fingerprint": [P, P],
+            "chor_save_code_cache": [P, U64, P, P, U32, C.c_char_p],
+            "chor_load_code_cache": [C.c_char_p, P, U64, U32, P, P, P, P, P],
         }
         for name, args in sigs.items():
             fn = getattr(self.lib, name)
@@ -191,6 +194,32 @@ class Oracle:
         rec = np.ascontiguousarray(records, dtype=RECORD_DTYPE)
         self._check(self.lib.chor_save_matches(id_i.encode(), id_j.encode(), rec.ctypes.data, len(rec),
                                                str(path).encode()), "save_matches")
+
+    def centering_fingerprint(self, centering) -> int:
+        c = np.ascontiguousarray(centering, dtype=np.float64)
+        out = C.c_uint64(0)
+        self._check(self.lib.chor_centering_fingerprint(c.ctypes.data, C.byref(out)), "centering_fingerprint")
+        return out.value
+
+    def save_code_cache(self, params, centering_fp: int, shorts, longs, path):
+        p = self._fp(params)
+        s = np.ascontiguousarray(shorts, dtype=np.uint32)
+        l = np.ascontiguousarray(longs, dtype=np.uint64)
+        self._check(self.lib.chor_save_code_cache(C.byref(p), C.c_uint64(centering_fp), s.ctypes.data, l.ctypes.data,
+                                                  len(l.reshape(-1, 2)), str(path).encode()), "save_code_cache")
+
+    def load_code_cache(self, path, expected, expected_fp: int, capacity: int):
+        """Returns (shorts, longs, fault, fault_offset); fault 0 = ok, 1..5 FeatureFileFault+1, 6 mismatch."""
+        p = self._fp(expected)
+        shorts = np.zeros((max(capacity, 1), expected.table_count), dtype=np.uint32)
+        longs = np.zeros((max(capacity, 1), 2), dtype=np.uint64)
+        cnt, fault, off = C.c_uint32(0), C.c_int(0), C.c_uint64(0)
+        rc = self.lib.chor_load_code_cache(str(path).encode(), C.byref(p), C.c_uint64(expected_fp), capacity,
+                                           shorts.ctypes.data, longs.ctypes.data, C.byref(cnt), C.byref(fault),
+                                           C.byref(off))
+        if rc == 3 and fault.value == 0:
+            raise MemoryError("capacity")
+        return shorts[: cnt.value], longs[: cnt.value], fault.value, off.value
 
     def plan_exhaustive(self, image_count: int, block_images: int, blocks_per_group: int):
         pairs = np.zeros((max(image_count * (image_count - 1) // 2, 1), 2), dtype=np.uint32)

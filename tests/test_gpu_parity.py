@@ -455,3 +455,27 @@ def test_save_matches_from_device_results(matcher, oracle, default_family, tmp_p
     ch.save_matches("a", "b", rec, tmp_path / ch.pair_file_name(0, 1))
     oracle.save_matches("a", "b", want, tmp_path / "want.txt")
     assert (tmp_path / "match_000000_000001.txt").read_bytes() == (tmp_path / "want.txt").read_bytes()
+
+
+# ---- multi-GPU host logic on the real engine (world 1; worlds 2 and 3 run under gloo on CPU) -----------
+def test_sharded_job_on_device(matcher, oracle, default_family):
+    from paper_1805_08995_b200.sharding import CollectingSink, Comm, ShardedJob
+
+    fresh(matcher, default_family)
+    images, points = 6, 1000
+    data = make_dataset(images, points, seed=21)
+    job = ShardedJob(matcher, Comm(0, 1))
+    cen = job.set_centering(lambda i: data[i], images)
+    matcher._test_ids |= set(range(images))
+    assert np.array_equal(cen, oracle.centering([data[i] for i in range(images)]))
+    pairs = ch.plan_exhaustive(images, 2, 2)
+    sink = CollectingSink()
+    stats = job.match(lambda i: data[i], pairs, ch.MatchConfig(), sink)
+    assert (stats["first_pair"], stats["last_pair"]) == (0, len(pairs))
+    counts, records = sink.result()
+    offsets, recs = job.gather_results(counts, records)
+    assert stats["matches"] == len(recs) == offsets[-1]
+    codes = [oracle_codes(oracle, default_family, cen, data[i]) for i in range(images)]
+    for k, (a, b) in enumerate(pairs):
+        want, _ = oracle.match_pair(default_family.params, ch.MatchConfig(), data[a], *codes[a], data[b], *codes[b])
+        assert np.array_equal(recs[offsets[k]:offsets[k + 1]], want), (k, a, b)
