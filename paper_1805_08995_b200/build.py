@@ -75,7 +75,8 @@ def build_chsynth(force: bool = False) -> Path:
     src = CSRC / "synth.cpp"
     if force or _stale(target, [src]):
         cxx = os.environ.get("CXX") or shutil.which("g++") or "g++"
-        subprocess.run([cxx, "-std=gnu++17", "-O2", "-fPIC", "-shared", "-pthread", "-o", str(target), str(src)],
+        subprocess.run([cxx, "-std=gnu++17", "-O2", "-fPIC", "-shared", "-pthread", "-Wl,-Bsymbolic", "-Wl,--exclude-libs,ALL",
+                        "-o", str(target), str(src)],
                        check=True)
     return target
 
