@@ -2,7 +2,8 @@
 //
 // Data layout in HBM: every resident image owns ONE arena block holding, 256-byte aligned,
 //   desc (n*128 B) | kp (n*16 B) | longs (n*16 B) | shorts (n*L*4 B) | offs (L*(2^m+1)*4 B) | points (L*n*2 B)
-// (1,466,648 B for n = 8192, m = 8, L = 6).  Blocks are bump-allocated from 256 MiB slabs and
+//   | scan (L*n*2 B)
+// (1,565,208 B for n = 8192, m = 8, L = 6).  Blocks are bump-allocated from 256 MiB slabs and
 // recycled through an exact-size free list, so streaming a dataset through a bounded working
 // set never calls cudaMalloc in steady state.
 //
@@ -184,7 +185,7 @@ struct DeviceGuard {
     explicit DeviceGuard(int dev) { cudaSetDevice(dev); }
 };
 
-size_t image_block_bytes(uint32_t n, uint32_t m, uint32_t L, size_t off[6]) {
+size_t image_block_bytes(uint32_t n, uint32_t m, uint32_t L, size_t off[7]) {
     size_t o = 0;
     off[0] = o; o += align_up(size_t(n) * kDim);
     off[1] = o; o += align_up(size_t(n) * 16);
@@ -192,6 +193,7 @@ size_t image_block_bytes(uint32_t n, uint32_t m, uint32_t L, size_t off[6]) {
     off[3] = o; o += align_up(size_t(n) * L * 4);
     off[4] = o; o += align_up(size_t(L) * ((size_t(1) << m) + 1) * 4);
     off[5] = o; o += align_up(size_t(L) * n * 2);
+    off[6] = o; o += align_up(size_t(L) * n * 2);
     o += kAlign;  // slack: the match kernel may read one id past an empty last bucket
     return std::max(o, kAlign);
 }
@@ -302,7 +304,7 @@ chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t
         ctx->images.emplace_back();
     }
     if (const chgpu_status s = ensure_images_cap(ctx, size_t(slot) + 1)) return s;
-    size_t off[6];
+    size_t off[7];
     const size_t bytes = image_block_bytes(n, ctx->fam.short_bits, ctx->fam.table_count, off);
     char* block = nullptr;
     const cudaError_t e = ctx->arena.alloc(bytes, &block);
@@ -322,6 +324,7 @@ chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t
     r.dev.shorts = reinterpret_cast<uint32_t*>(block + off[3]);
     r.dev.offs = reinterpret_cast<uint32_t*>(block + off[4]);
     r.dev.points = reinterpret_cast<uint16_t*>(block + off[5]);
+    r.dev.scan = reinterpret_cast<uint16_t*>(block + off[6]);
     r.dev.n = n;
     r.dev.flags = 0;
     ctx->slot_of[image_id] = slot;

@@ -20,6 +20,9 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 //   shorts n x L u32           bucket ids [point*L + table] (ShortCodes::values, hashing.hpp:80)
 //   offs   L x (2^m + 1) u32   dense CSR offsets per table (BucketIndex, matcher.hpp:30-41)
 //   points L x n u16           point ids bucket-major, ascending id inside a bucket
+//   scan   L x n u16           the same buckets in the order the match kernel walks them: ids dealt
+//                              round-robin over (id mod 8), so that 8 consecutive entries gather their
+//                              16-byte codes from 8 different shared-memory bank groups
 struct DevImage {
     const uint8_t* desc;
     const float4* kp;
@@ -27,6 +30,7 @@ struct DevImage {
     uint32_t* shorts;
     uint32_t* offs;
     uint16_t* points;
+    uint16_t* scan;
     uint32_t n;
     uint32_t flags;  // bit0: codes + buckets valid
 };

@@ -249,6 +249,33 @@ __global__ void bucket_build_kernel(const DevImage* __restrict__ images, const u
         }
         __syncwarp();
     }
+
+    // Pass 3: scan order.  The match kernel gathers the 16-byte codes of 8 consecutive bucket entries
+    // with one quarter-warp LDS.128; the gather is conflict-free iff their ids differ mod 8.  Entries are
+    // re-dealt by (rank inside the residue class, residue): the first min-count rounds hold all 8
+    // residues.  Only the order inside a bucket changes, which no result depends on.  One bucket per lane.
+    uint16_t* scan = img.scan + uint64_t(t) * n;
+    for (uint32_t b = lane; b < nb; b += 32) {
+        const uint32_t lo = offs[b], hi = offs[b + 1], s = hi - lo;
+        if (s <= 8 || s >= 256) {  // one octet, or counts that do not fit the packed bytes: keep the order
+            for (uint32_t e = lo; e < hi; ++e) scan[e] = pts[e];
+            continue;
+        }
+        unsigned long long cnt = 0, seen = 0;  // 8 x 8-bit counters, one per residue
+        for (uint32_t e = lo; e < hi; ++e) cnt += 1ull << (8u * (pts[e] & 7u));
+        for (uint32_t e = lo; e < hi; ++e) {
+            const uint32_t id = pts[e], r = id & 7u;
+            const uint32_t k = uint32_t(seen >> (8u * r)) & 0xffu;
+            uint32_t pos = 0;
+#pragma unroll
+            for (uint32_t r2 = 0; r2 < 8; ++r2) {
+                const uint32_t c = uint32_t(cnt >> (8u * r2)) & 0xffu;
+                pos += min(c, k) + ((r2 < r && c > k) ? 1u : 0u);
+            }
+            scan[lo + pos] = uint16_t(id);
+            seen += 1ull << (8u * r);
+        }
+    }
 }
 
 }  // namespace chgpu

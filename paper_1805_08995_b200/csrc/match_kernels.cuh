@@ -45,6 +45,12 @@ namespace chgpu {
 #define CHGPU_OVER_SLOTS 3
 #endif
 constexpr int kMatchThreads = CHGPU_MATCH_THREADS;
+// bucket lists in the bank-friendly scan order (default) or, for A/B measurements, the canonical one
+#ifdef CHGPU_SCAN_CANONICAL
+#define CH_IDS(img) (img).points
+#else
+#define CH_IDS(img) (img).scan
+#endif
 constexpr int kOverSlots = CHGPU_OVER_SLOTS;  // register slots for bucket entries past the first 32 of every table
 
 struct MatchParams {
@@ -241,7 +247,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
             if (J.n != 0) {
                 // ---- 1. bucket lookup (warp-uniform) -------------------------------------------
                 const uint32_t* __restrict__ qcodes = I.shorts + uint64_t(q) * L;
-                uint32_t lo[LT], len[LT];  // lo: index of the bucket's first entry in J.points
+                uint32_t lo[LT], len[LT];  // lo: index of the bucket's first entry in J.scan
                 uint32_t total = 0, tover = 0, minlen = kNone;
 #pragma unroll
                 for (int t = 0; t < LT; ++t) {
@@ -278,7 +284,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     uint32_t key[KS];
 #pragma unroll
                     for (int t = 0; t < LT; ++t)  // (an empty bucket re-reads a neighbour's entry: discarded below)
-                        key[t] = scan_step<SMEM_TRAIN>(J.points, lo[t], lo[t] + max(len[t], 1u) - 1u, lane, ql, s_long,
+                        key[t] = scan_step<SMEM_TRAIN>(CH_IDS(J), lo[t], lo[t] + max(len[t], 1u) - 1u, lane, ql, s_long,
                                                        J.longs);
                     if (minlen == 0) {
 #pragma unroll
@@ -293,7 +299,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 #pragma unroll
                         for (int t = 0; t < LT; ++t) {
                             start[t] = pre;
-                            bias[t] = lo[t] + 32u - pre;  // flat overflow index r -> J.points[r + bias]
+                            bias[t] = lo[t] + 32u - pre;  // flat overflow index r -> J.scan[r + bias]
                             pre += max(len[t], 32u) - 32u;
                         }
 #pragma unroll
@@ -304,7 +310,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 #pragma unroll
                                 for (int t = 1; t < LT; ++t)
                                     if (r >= start[t]) b = bias[t];
-                                key[LT + s] = scan_step<SMEM_TRAIN>(J.points, r + b, r + b, 0u, ql, s_long, J.longs);
+                                key[LT + s] = scan_step<SMEM_TRAIN>(CH_IDS(J), r + b, r + b, 0u, ql, s_long, J.longs);
                             }
                         }
                     }
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 #pragma unroll
                         for (int t = 0; t < LT; ++t)
                             if (off < len[t]) {
-                                const uint32_t k = scan_step<SMEM_TRAIN>(J.points, lo[t] + off, lo[t] + len[t] - 1u,
+                                const uint32_t k = scan_step<SMEM_TRAIN>(CH_IDS(J), lo[t] + off, lo[t] + len[t] - 1u,
                                                                          lane, ql, s_long, J.longs);
                                 lmin = min(lmin, k);
                                 lmax = max(lmax, k);
@@ -359,7 +365,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                             for (int t = 0; t < LT; ++t) {
                                 key[t] = kNone;
                                 if (off < len[t])
-                                    key[t] = scan_step<SMEM_TRAIN>(J.points, lo[t] + off, lo[t] + len[t] - 1u, lane, ql,
+                                    key[t] = scan_step<SMEM_TRAIN>(CH_IDS(J), lo[t] + off, lo[t] + len[t] - 1u, lane, ql,
                                                                    s_long, J.longs);
                             }
                             // a round whose smallest key is beyond a full list's last entry changes nothing
