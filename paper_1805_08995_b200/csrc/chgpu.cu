@@ -376,21 +376,29 @@ size_t offs_smem_bytes(const chgpu_ctx* ctx) {
     return (size_t(ctx->fam.table_count) * ((size_t(1) << ctx->fam.short_bits) + 1) * 4 + 15) & ~size_t(15);
 }
 
+size_t stage_smem_bytes(const chgpu_ctx* ctx) {
+    // per-warp lookup staging of the match kernel; LT is the table count rounded up to 4, 6 or 8
+    const uint32_t L = ctx->fam.table_count;
+    const int LT = L <= 4 ? 4 : (L <= 6 ? 6 : 8);
+    return size_t(kMatchThreads / 32) * stage_bytes_per_warp(LT);
+}
+
 cudaError_t launch_match(chgpu_ctx* ctx, MatchParams& P, bool smem_train, uint32_t max_nt, uint32_t* grid) {
     const int sms = ctx->prop.multiProcessorCount;
     if (smem_train) {
         P.smem_long_bytes = std::max<uint32_t>(max_nt * 16u, 16u);
-        return launch_match_smem(P, size_t(P.smem_long_bytes) + offs_smem_bytes(ctx), sms, ctx->compute, grid);
+        return launch_match_smem(P, size_t(P.smem_long_bytes) + offs_smem_bytes(ctx) + stage_smem_bytes(ctx), sms,
+                                 ctx->compute, grid);
     }
     P.smem_long_bytes = 0;
-    return launch_match_global(P, 16, sms, ctx->compute, grid);
+    return launch_match_global(P, stage_smem_bytes(ctx), sms, ctx->compute, grid);
 }
 
 size_t smem_train_capacity(const chgpu_ctx* ctx) {
     // points whose codes fit next to the bucket offsets in the dynamic smem of a 1-CTA/SM launch
     // (minus the kernel's static 16 B and the 1 KiB the driver reserves per block)
     const size_t avail = ctx->prop.sharedMemPerBlockOptin - 1024 - 64;
-    const size_t offs = offs_smem_bytes(ctx);
+    const size_t offs = offs_smem_bytes(ctx) + stage_smem_bytes(ctx);
     return avail > offs ? (avail - offs) / 16 : 0;
 }
 

@@ -34,9 +34,21 @@
 // reference's MatchRecord stream, ascending query index inside every pair.
 #pragma once
 
+#include <utility>
+
 #include "dev_types.cuh"
 
 namespace chgpu {
+
+// Compile-time loop: f(std::integral_constant<int, 0>{}), ..., f(std::integral_constant<int, N-1>{}).
+template <class F, int... Is>
+__device__ __forceinline__ void static_for_impl(F& f, std::integer_sequence<int, Is...>) {
+    (f(std::integral_constant<int, Is>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
 
 #ifndef CHGPU_MATCH_THREADS
 #define CHGPU_MATCH_THREADS 1024
@@ -107,6 +119,32 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+template <uint32_t OFF>
+__device__ __forceinline__ uint2 lds64_at(uint32_t base) {  // [base + OFF], 8-byte aligned
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2+%3];" : "=r"(v.x), "=r"(v.y) : "r"(base), "n"(OFF));
+    return v;
+}
+template <uint32_t OFF>
+__device__ __forceinline__ uint4 lds128_at(uint32_t base) {  // [base + OFF], 16-byte aligned
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+%5];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(base), "n"(OFF));
+    return v;
+}
+__device__ __forceinline__ void sts64(uint32_t addr, uint32_t a, uint32_t b) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t addr, const uint4& v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
 __device__ __forceinline__ uint2 lds64x(uint32_t addr) {  // two adjacent u32 (need not be 8-byte aligned)
     uint2 v;
     asm volatile("ld.shared.u32 %0, [%2];\n\tld.shared.u32 %1, [%2+4];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
@@ -165,24 +203,37 @@ __device__ __forceinline__ uint32_t next_key(const uint32_t (&key)[SLOTS], uint3
     return g >= nb - 1u ? kNone : g - nb;
 }
 
-// One step of the Hamming scan: candidate `first + lane` of the bucket-major id list, clamped
-// to `last` (lanes past the end re-evaluate the last candidate: equal keys collapse).
+// Hamming key of one candidate id: distance<<24 | id.
 template <bool SMEM_TRAIN>
-__device__ __forceinline__ uint32_t scan_step(const uint16_t* __restrict__ pts, uint32_t first, uint32_t last,
-                                              uint32_t lane, const uint4& ql, uint32_t s_long,
-                                              const uint4* __restrict__ g_long) {
-    const uint32_t p = min(first + lane, last);
-    const uint32_t id = __ldg(pts + p);
+__device__ __forceinline__ uint32_t key_of(uint32_t id, const uint4& ql, uint32_t s_long, const uint4* __restrict__ g_long) {
     uint4 c;
     if (SMEM_TRAIN) c = lds128(s_long + id * 16u);
     else c = __ldg(g_long + id);
     return (hamming128(c, ql) << 24) | id;
 }
 
+// One step of the Hamming scan: candidate `first + lane` of the bucket-major id list, clamped
+// to `last` (lanes past the end re-evaluate the last candidate: equal keys collapse).
+template <bool SMEM_TRAIN>
+__device__ __forceinline__ uint32_t scan_step(const uint16_t* __restrict__ pts, uint32_t first, uint32_t last,
+                                              uint32_t lane, const uint4& ql, uint32_t s_long,
+                                              const uint4* __restrict__ g_long) {
+    const uint32_t id = __ldg(pts + min(first + lane, last));
+    return key_of<SMEM_TRAIN>(id, ql, s_long, g_long);
+}
+
+// Per-warp staging of the bucket lookups of kBatch consecutive queries of the warp (shared memory),
+// one record per query:
+//   ql uint4 | {total, tover, empty-table mask, longest bucket} | LT x {first, last} entry of the bucket
+// `last` is clamped to `first` for an empty bucket (its lanes read a neighbour's entry, discarded later).
+constexpr uint32_t kBatch = 16;
+__host__ __device__ constexpr uint32_t stage_record_bytes(int LT) { return 32u + uint32_t(LT) * 8u; }
+__host__ __device__ constexpr uint32_t stage_bytes_per_warp(int LT) { return kBatch * stage_record_bytes(LT); }
+
 // LT = number of table slots unrolled in registers (>= L); EXACT: L == LT, no per-table guards.
 template <bool SMEM_TRAIN, int LT, bool EXACT>
 __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchParams P) {
-    extern __shared__ __align__(16) unsigned char s_raw[];  // [train codes | bucket offsets]
+    extern __shared__ __align__(16) unsigned char s_raw[];  // [train codes | bucket offsets | lookup staging]
     __shared__ unsigned int s_unit;
     __shared__ __align__(8) uint64_t s_bar;
 
@@ -192,12 +243,16 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t nb1 = (1u << P.m) + 1;
     const uint32_t L = EXACT ? uint32_t(LT) : P.L;
+    const uint32_t obytes = SMEM_TRAIN ? ((L * nb1 * 4u + 15u) & ~15u) : 0u;  // the arena pads every array to 256 B
     // shared-window addresses, pinned in registers (the compiler would otherwise re-derive
     // them from SR_CgaCtaId in front of every gather)
     uint32_t s_long = smem_addr(s_raw);
     asm volatile("" : "+r"(s_long));
     uint32_t s_offs = s_long + P.smem_long_bytes;
     asm volatile("" : "+r"(s_offs));
+    uint32_t s_stage = s_offs + obytes + warp * stage_bytes_per_warp(LT);
+    asm volatile("" : "+r"(s_stage));
+    constexpr uint32_t kRec = stage_record_bytes(LT);
 
     if (SMEM_TRAIN && tid == 0) {
         mbar_init(&s_bar, 1);
@@ -222,7 +277,6 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                 // order them before the async-proxy writes.
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 const uint32_t bytes = J.n * 16u;
-                const uint32_t obytes = (L * nb1 * 4u + 15u) & ~15u;  // the arena pads every array to 256 B
                 mbar_expect_tx(&s_bar, bytes + obytes);
                 for (uint32_t off = 0; off < bytes; off += 65536u)
                     bulk_g2s(s_raw + off, reinterpret_cast<const unsigned char*>(J.longs) + off,
@@ -239,42 +293,80 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
         // query range of this unit: chunks are multiples of 32 queries
         const uint32_t qc = (((I.n + P.chunks_per_pair - 1) / P.chunks_per_pair) + 31u) & ~31u;
         const uint32_t q0 = min(I.n, chunk * qc), q1 = min(I.n, q0 + qc);
+        const uint16_t* __restrict__ ids = CH_IDS(J);
 
         uint32_t st_raw = 0, st_vq = 0, st_dist = 0, st_match = 0;
 
-        for (uint32_t q = q0 + warp; q < q1; q += kWarps) {
-            uint32_t out_t = kNone, out_d = 0;
-            if (J.n != 0) {
-                // ---- 1. bucket lookup (warp-uniform) -------------------------------------------
-                const uint32_t* __restrict__ qcodes = I.shorts + uint64_t(q) * L;
-                uint32_t lo[LT], len[LT];  // lo: index of the bucket's first entry in J.scan
-                uint32_t total = 0, tover = 0, minlen = kNone;
+        if (J.n == 0) {
+            for (uint32_t q = q0 + tid; q < q1; q += kMatchThreads) __stcs(P.res + pd.res_off + q, make_uint2(kNone, 0u));
+        } else {
+            // ---- 1. bucket lookup, kBatch queries at a time, one query per lane -------------------
+            // (matcher.cpp:164-169).  Lane i resolves the L table ranges of the warp's (base+i)-th query
+            // and parks them, with the query's long code, in the warp's staging area: the global-memory
+            // round trip for the query-side data is paid once per batch, not once per query.
+            auto lookup_batch = [&](uint32_t qb) {
+                const uint32_t q = qb + lane * kWarps;
+                if (lane < kBatch && q < q1) {
+                    const uint32_t* __restrict__ qcodes = I.shorts + uint64_t(q) * L;
+                    const uint32_t rec = s_stage + lane * kRec;
+                    sts128(rec, __ldg(I.longs + q));
+                    uint32_t total = 0, tover = 0, empty = 0, maxlen = 0;
 #pragma unroll
-                for (int t = 0; t < LT; ++t) {
-                    lo[t] = 0;
-                    len[t] = 0;
-                    if (EXACT || t < int(L)) {
-                        const uint32_t code = ldg_stream32(qcodes + t);
-                        uint32_t a, b;
-                        if (SMEM_TRAIN) {
-                            const uint2 o = lds64x(s_offs + (t * nb1 + code) * 4u);
-                            a = o.x;
-                            b = o.y;
-                        } else {
-                            const uint32_t* o = J.offs + t * nb1 + code;
-                            a = __ldg(o);
-                            b = __ldg(o + 1);
+                    for (int t = 0; t < LT; ++t) {
+                        uint32_t a = 0, b = 0;
+                        if (EXACT || t < int(L)) {
+                            const uint32_t code = __ldg(qcodes + t);
+                            if (SMEM_TRAIN) {
+                                const uint2 o = lds64x(s_offs + (t * nb1 + code) * 4u);
+                                a = o.x;
+                                b = o.y;
+                            } else {
+                                const uint32_t* o = J.offs + t * nb1 + code;
+                                a = __ldg(o);
+                                b = __ldg(o + 1);
+                            }
                         }
-                        lo[t] = t * J.n + a;
-                        len[t] = b - a;
+                        const uint32_t len = b - a, first = t * J.n + a;
+                        total += len;
+                        tover += max(len, 32u) - 32u;
+                        maxlen = max(maxlen, len);
+                        if (len == 0) empty |= 1u << t;
+                        sts64(rec + 32u + t * 8u, first, first + max(len, 1u) - 1u);
                     }
-                    total += len[t];
-                    minlen = min(minlen, len[t]);
-                    tover += max(len[t], 32u) - 32u;
+                    sts128(rec + 16u, make_uint4(total, tover, empty, maxlen));
                 }
-                st_raw += total;
+                __syncwarp();
+            };
+            // ids of the first 32 entries of each of a query's buckets, one per lane (lanes past the end
+            // re-read the last entry: equal keys collapse)
+            auto load_ids = [&](uint32_t rec, uint32_t (&out)[LT]) {
+                static_for<LT>([&](auto T) {
+                    constexpr int t = decltype(T)::value;
+                    const uint2 fl = lds64_at<32u + t * 8u>(rec);
+                    out[t] = __ldg(ids + min(fl.x + lane, fl.y));
+                });
+            };
 
-                const uint4 ql = ldg_stream128(I.longs + q);
+            uint32_t idn[LT];  // prefetched ids of the NEXT query
+            uint32_t q = q0 + warp;
+            if (q < q1) {
+                lookup_batch(q);
+                load_ids(s_stage, idn);
+            }
+            for (uint32_t j = 0; q < q1; ++j, q += kWarps) {
+                const uint32_t slot = j & (kBatch - 1);
+                const uint32_t rec = s_stage + slot * kRec;
+                uint32_t out_t = kNone, out_d = 0;
+                const uint4 ql = lds128_at<0>(rec);
+                const uint4 hdr = lds128_at<16>(rec);  // total, tover, empty mask, longest bucket
+                const uint32_t tover = hdr.y;
+                st_raw += hdr.x;
+                uint32_t id[LT];
+#pragma unroll
+                for (int t = 0; t < LT; ++t) id[t] = idn[t];
+                // the next query's ids travel while this one is scanned, ranked and verified
+                if (slot != kBatch - 1 && q + kWarps < q1) load_ids(rec + kRec, idn);
+
                 uint32_t mykey = kNone;  // lane r holds the r-th ranked key
                 uint32_t n = 0;          // ranked count
 
@@ -283,25 +375,17 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     //         then the entries past 32 of all buckets flattened into the last slots
                     uint32_t key[KS];
 #pragma unroll
-                    for (int t = 0; t < LT; ++t)  // (an empty bucket re-reads a neighbour's entry: discarded below)
-                        key[t] = scan_step<SMEM_TRAIN>(CH_IDS(J), lo[t], lo[t] + max(len[t], 1u) - 1u, lane, ql, s_long,
-                                                       J.longs);
-                    if (minlen == 0) {
-#pragma unroll
-                        for (int t = 0; t < LT; ++t)
-                            if (len[t] == 0) key[t] = kNone;
-                    }
-#pragma unroll
                     for (int s = 0; s < kOverSlots; ++s) key[LT + s] = kNone;
                     if (tover != 0) {
                         uint32_t pre = 0;
                         uint32_t bias[LT], start[LT];
-#pragma unroll
-                        for (int t = 0; t < LT; ++t) {
+                        static_for<LT>([&](auto T) {
+                            constexpr int t = decltype(T)::value;
+                            const uint2 fl = lds64_at<32u + t * 8u>(rec);
                             start[t] = pre;
-                            bias[t] = lo[t] + 32u - pre;  // flat overflow index r -> J.scan[r + bias]
-                            pre += max(len[t], 32u) - 32u;
-                        }
+                            bias[t] = fl.x + 32u - pre;  // flat overflow index r -> ids[r + bias]
+                            pre += max(fl.y - fl.x, 31u) - 31u;  // max(len, 32) - 32 with len = last - first + 1
+                        });
 #pragma unroll
                         for (int s = 0; s < kOverSlots; ++s) {
                             if (uint32_t(s) * 32u < tover) {
@@ -310,10 +394,20 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 #pragma unroll
                                 for (int t = 1; t < LT; ++t)
                                     if (r >= start[t]) b = bias[t];
-                                key[LT + s] = scan_step<SMEM_TRAIN>(CH_IDS(J), r + b, r + b, 0u, ql, s_long, J.longs);
+                                key[LT + s] = __ldg(ids + r + b);  // id for now; its key after the first steps
                             }
                         }
                     }
+#pragma unroll
+                    for (int t = 0; t < LT; ++t) key[t] = key_of<SMEM_TRAIN>(id[t], ql, s_long, J.longs);
+                    if (hdr.z != 0) {  // empty buckets (rare)
+#pragma unroll
+                        for (int t = 0; t < LT; ++t)
+                            if (hdr.z & (1u << t)) key[t] = kNone;
+                    }
+#pragma unroll
+                    for (int s = 0; s < kOverSlots; ++s)
+                        if (uint32_t(s) * 32u < tover) key[LT + s] = key_of<SMEM_TRAIN>(key[LT + s], ql, s_long, J.longs);
                     // ---- 3. ranking: pull straight out of the slots -------------------------------
                     const uint32_t k0 = first_key(key, kNone);
                     if ((k0 >> 24) <= P.tau) {
@@ -340,17 +434,22 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     }
                 } else {
                     // ---- long buckets: rounds of 32 entries per table ----------------------------
-                    uint32_t maxlen = 0;
-#pragma unroll
-                    for (int t = 0; t < LT; ++t) maxlen = max(maxlen, len[t]);
+                    const uint32_t maxlen = hdr.w;
+                    uint32_t lo[LT], len[LT];
+                    static_for<LT>([&](auto T) {
+                        constexpr int t = decltype(T)::value;
+                        const uint2 fl = lds64_at<32u + t * 8u>(rec);
+                        lo[t] = fl.x;
+                        len[t] = (hdr.z & (1u << t)) ? 0u : fl.y - fl.x + 1u;
+                    });
                     // pass 1: smallest and largest key only — most queries have nothing within tau
                     uint32_t lmin = kNone, lmax = 0;
                     for (uint32_t off = 0; off < maxlen; off += 32u) {
 #pragma unroll
                         for (int t = 0; t < LT; ++t)
                             if (off < len[t]) {
-                                const uint32_t k = scan_step<SMEM_TRAIN>(CH_IDS(J), lo[t] + off, lo[t] + len[t] - 1u,
-                                                                         lane, ql, s_long, J.longs);
+                                const uint32_t k = scan_step<SMEM_TRAIN>(ids, lo[t] + off, lo[t] + len[t] - 1u, lane, ql,
+                                                                         s_long, J.longs);
                                 lmin = min(lmin, k);
                                 lmax = max(lmax, k);
                             }
@@ -365,8 +464,8 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                             for (int t = 0; t < LT; ++t) {
                                 key[t] = kNone;
                                 if (off < len[t])
-                                    key[t] = scan_step<SMEM_TRAIN>(CH_IDS(J), lo[t] + off, lo[t] + len[t] - 1u, lane, ql,
-                                                                   s_long, J.longs);
+                                    key[t] = scan_step<SMEM_TRAIN>(ids, lo[t] + off, lo[t] + len[t] - 1u, lane, ql, s_long,
+                                                                   J.longs);
                             }
                             // a round whose smallest key is beyond a full list's last entry changes nothing
                             const uint32_t kth = __shfl_sync(FULL, mykey, P.top_k - 1);
@@ -401,9 +500,9 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     const uint4* __restrict__ qrow = reinterpret_cast<const uint4*>(I.desc + uint64_t(q) * kDim) + half * 4u;
                     uint32_t mydist = kNone;
                     for (uint32_t j0 = 0; j0 < n; j0 += 16) {
-                        const uint32_t j = min(j0 + cand, n - 1);
-                        const uint32_t id = __shfl_sync(FULL, mykey, j) & 0xffffffu;
-                        const uint4* __restrict__ trow = reinterpret_cast<const uint4*>(J.desc + uint64_t(id) * kDim) + half * 4u;
+                        const uint32_t jj = min(j0 + cand, n - 1);
+                        const uint32_t cid = __shfl_sync(FULL, mykey, jj) & 0xffffffu;
+                        const uint4* __restrict__ trow = reinterpret_cast<const uint4*>(J.desc + uint64_t(cid) * kDim) + half * 4u;
                         uint32_t s = 0;
 #pragma unroll 2
                         for (int w = 0; w < 4; ++w) {
@@ -426,8 +525,15 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                         st_match += 1;
                     }
                 }
+                if (lane == 0) __stcs(P.res + pd.res_off + q, make_uint2(out_t, out_d));
+
+                // batch boundary: resolve the next kBatch queries (this one's ranges are in registers)
+                if (slot == kBatch - 1 && q + kWarps < q1) {
+                    __syncwarp();
+                    lookup_batch(q + kWarps);
+                    load_ids(s_stage, idn);
+                }
             }
-            if (lane == 0) __stcs(P.res + pd.res_off + q, make_uint2(out_t, out_d));
         }
 
         if (lane == 0) {

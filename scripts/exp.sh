@@ -1,6 +1,6 @@
 run() { python bench.py --steps 2 --warmup 2 --no-e2e --no-cpu --pairs 40960 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', d['value'], d['roofline']['avg_launch_ms'])"; }
 b() { CHGPU_NVCC_EXTRA="$1" python -m paper_1805_08995_b200.build --force > /dev/null 2>&1; }
-b "-DCHGPU_SCAN_CANONICAL"; run canonical
-b ""; run scan_order
+run v3b
 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-ncu --set full --clock-control none --import-source on -k regex:match_kernel -s 2 -c 1 -f -o gpurun_out/prof_match_r01d python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --pairs 8192 > gpurun_out/prof_r01d.log 2>&1
+b "-DCHGPU_MATCH_THREADS=896"; run v3b_t896
+ncu --set full --clock-control none --import-source on -k regex:match_kernel -s 2 -c 1 -f -o gpurun_out/prof_match_r01f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --pairs 8192 > gpurun_out/prof_r01f.log 2>&1
