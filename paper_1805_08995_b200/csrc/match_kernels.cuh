@@ -51,7 +51,7 @@ __device__ __forceinline__ void static_for(F&& f) {
 }
 
 #ifndef CHGPU_MATCH_THREADS
-#define CHGPU_MATCH_THREADS 1024
+#define CHGPU_MATCH_THREADS 896
 #endif
 #ifndef CHGPU_OVER_SLOTS
 #define CHGPU_OVER_SLOTS 3
@@ -64,6 +64,7 @@ constexpr int kMatchThreads = CHGPU_MATCH_THREADS;
 #define CH_IDS(img) (img).scan
 #endif
 constexpr int kOverSlots = CHGPU_OVER_SLOTS;  // register slots for bucket entries past the first 32 of every table
+static_assert(kOverSlots >= 1 && kOverSlots <= 3, "the staging record carries three overflow segment masks");
 
 struct MatchParams {
     const DevImage* images;
@@ -224,10 +225,16 @@ __device__ __forceinline__ uint32_t scan_step(const uint16_t* __restrict__ pts, 
 
 // Per-warp staging of the bucket lookups of kBatch consecutive queries of the warp (shared memory),
 // one record per query:
-//   ql uint4 | {total, tover, empty-table mask, longest bucket} | LT x {first, last} entry of the bucket
-// `last` is clamped to `first` for an empty bucket (its lanes read a neighbour's entry, discarded later).
+//   +0   ql uint4
+//   +16  hdr = tover (capped at 255) | empty-table mask << 8 | base1 << 16 | base2 << 24
+//   +20  M0, M1, M2: for overflow step s, bit l set iff flat overflow index 32 s + l starts a table's segment
+//   +32  LT x {first, last} entry of the query's bucket in table t (`last` clamped to `first` when empty:
+//        such lanes read a neighbour's entry, discarded later)
+//   +32+8LT  adj[k], k-th table WITH overflow: flat overflow index r of that segment -> ids[r + adj]
+// tover = entries past the first 32 of every bucket, summed over the tables; base_s = segments that start
+// before step s.  Lane l of step s belongs to segment base_s + popc(M_s & lanes<=l) - 1.
 constexpr uint32_t kBatch = 16;
-__host__ __device__ constexpr uint32_t stage_record_bytes(int LT) { return 32u + uint32_t(LT) * 8u; }
+__host__ __device__ constexpr uint32_t stage_record_bytes(int LT) { return (32u + uint32_t(LT) * 12u + 15u) & ~15u; }
 __host__ __device__ constexpr uint32_t stage_bytes_per_warp(int LT) { return kBatch * stage_record_bytes(LT); }
 
 // LT = number of table slots unrolled in registers (>= L); EXACT: L == LT, no per-table guards.
@@ -252,7 +259,8 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
     asm volatile("" : "+r"(s_offs));
     uint32_t s_stage = s_offs + obytes + warp * stage_bytes_per_warp(LT);
     asm volatile("" : "+r"(s_stage));
-    constexpr uint32_t kRec = stage_record_bytes(LT);
+    constexpr uint32_t kRec = stage_record_bytes(LT), kAdj = 32u + uint32_t(LT) * 8u;
+    const uint32_t le_mask = (2u << lane) - 1u;  // lanes <= this one
 
     if (SMEM_TRAIN && tid == 0) {
         mbar_init(&s_bar, 1);
@@ -310,7 +318,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     const uint32_t* __restrict__ qcodes = I.shorts + uint64_t(q) * L;
                     const uint32_t rec = s_stage + lane * kRec;
                     sts128(rec, __ldg(I.longs + q));
-                    uint32_t total = 0, tover = 0, empty = 0, maxlen = 0;
+                    uint32_t total = 0, pre = 0, empty = 0, nseg = 0, m0 = 0, m1 = 0, m2 = 0;
 #pragma unroll
                     for (int t = 0; t < LT; ++t) {
                         uint32_t a = 0, b = 0;
@@ -328,12 +336,21 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                         }
                         const uint32_t len = b - a, first = t * J.n + a;
                         total += len;
-                        tover += max(len, 32u) - 32u;
-                        maxlen = max(maxlen, len);
                         if (len == 0) empty |= 1u << t;
                         sts64(rec + 32u + t * 8u, first, first + max(len, 1u) - 1u);
+                        if (len > 32u) {
+                            sts32(rec + kAdj + nseg * 4u, first + 32u - pre);
+                            ++nseg;
+                            const uint32_t bit = 1u << (pre & 31u);
+                            if (pre < 32u) m0 |= bit;
+                            else if (pre < 64u) m1 |= bit;
+                            else if (pre < 96u) m2 |= bit;
+                            pre += len - 32u;
+                        }
                     }
-                    sts128(rec + 16u, make_uint4(total, tover, empty, maxlen));
+                    const uint32_t base1 = __popc(m0), base2 = base1 + __popc(m1);
+                    sts128(rec + 16u, make_uint4(min(pre, 255u) | (empty << 8) | (base1 << 16) | (base2 << 24), m0, m1, m2));
+                    st_raw += total;  // per lane; reduced over the warp when the unit ends
                 }
                 __syncwarp();
             };
@@ -358,9 +375,8 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                 const uint32_t rec = s_stage + slot * kRec;
                 uint32_t out_t = kNone, out_d = 0;
                 const uint4 ql = lds128_at<0>(rec);
-                const uint4 hdr = lds128_at<16>(rec);  // total, tover, empty mask, longest bucket
-                const uint32_t tover = hdr.y;
-                st_raw += hdr.x;
+                const uint4 hdr = lds128_at<16>(rec);  // tover | empty << 8 | base1 << 16 | base2 << 24, M0, M1, M2
+                const uint32_t tover = hdr.x & 0xffu;
                 uint32_t id[LT];
 #pragma unroll
                 for (int t = 0; t < LT; ++t) id[t] = idn[t];
@@ -377,33 +393,23 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 #pragma unroll
                     for (int s = 0; s < kOverSlots; ++s) key[LT + s] = kNone;
                     if (tover != 0) {
-                        uint32_t pre = 0;
-                        uint32_t bias[LT], start[LT];
-                        static_for<LT>([&](auto T) {
-                            constexpr int t = decltype(T)::value;
-                            const uint2 fl = lds64_at<32u + t * 8u>(rec);
-                            start[t] = pre;
-                            bias[t] = fl.x + 32u - pre;  // flat overflow index r -> ids[r + bias]
-                            pre += max(fl.y - fl.x, 31u) - 31u;  // max(len, 32) - 32 with len = last - first + 1
-                        });
+                        const uint32_t seg_mask[3] = {hdr.y, hdr.z, hdr.w};
 #pragma unroll
                         for (int s = 0; s < kOverSlots; ++s) {
                             if (uint32_t(s) * 32u < tover) {
+                                const uint32_t base = s == 0 ? 0u : (hdr.x >> (8 + 8 * s)) & 0xffu;
+                                const uint32_t seg = base + __popc(seg_mask[s] & le_mask) - 1u;
                                 const uint32_t r = min(uint32_t(s) * 32u + lane, tover - 1u);
-                                uint32_t b = bias[0];
-#pragma unroll
-                                for (int t = 1; t < LT; ++t)
-                                    if (r >= start[t]) b = bias[t];
-                                key[LT + s] = __ldg(ids + r + b);  // id for now; its key after the first steps
+                                key[LT + s] = __ldg(ids + r + lds32(rec + kAdj + seg * 4u));  // id for now; its key below
                             }
                         }
                     }
 #pragma unroll
                     for (int t = 0; t < LT; ++t) key[t] = key_of<SMEM_TRAIN>(id[t], ql, s_long, J.longs);
-                    if (hdr.z != 0) {  // empty buckets (rare)
+                    if ((hdr.x & 0xff00u) != 0) {  // empty buckets (rare)
 #pragma unroll
                         for (int t = 0; t < LT; ++t)
-                            if (hdr.z & (1u << t)) key[t] = kNone;
+                            if (hdr.x & (0x100u << t)) key[t] = kNone;
                     }
 #pragma unroll
                     for (int s = 0; s < kOverSlots; ++s)
@@ -434,13 +440,14 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     }
                 } else {
                     // ---- long buckets: rounds of 32 entries per table ----------------------------
-                    const uint32_t maxlen = hdr.w;
+                    uint32_t maxlen = 0;
                     uint32_t lo[LT], len[LT];
                     static_for<LT>([&](auto T) {
                         constexpr int t = decltype(T)::value;
                         const uint2 fl = lds64_at<32u + t * 8u>(rec);
                         lo[t] = fl.x;
-                        len[t] = (hdr.z & (1u << t)) ? 0u : fl.y - fl.x + 1u;
+                        len[t] = (hdr.x & (0x100u << t)) ? 0u : fl.y - fl.x + 1u;
+                        maxlen = max(maxlen, len[t]);
                     });
                     // pass 1: smallest and largest key only — most queries have nothing within tau
                     uint32_t lmin = kNone, lmax = 0;
@@ -536,6 +543,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
             }
         }
 
+        st_raw = __reduce_add_sync(FULL, st_raw);
         if (lane == 0) {
             if (st_raw) atomicAdd(&P.stats->raw_candidates, (unsigned long long)st_raw);
             if (st_vq) atomicAdd(&P.stats->verified_queries, (unsigned long long)st_vq);
