@@ -1,22 +1,29 @@
-// match_kernels.cuh — K3 (pair matching) and the ordered compaction of its results.
+// match_kernels.cuh — K3, the pair-matching kernel.
 //
 // K3 is a persistent kernel: one CTA per SM pulls work units (pair, query range) from a global
 // counter.  For each unit the train image's 128-bit codes and its dense bucket offsets are
 // brought into shared memory with bulk async copies (cp.async.bulk + mbarrier, the sm_90+/sm_100
 // TMA path), then every warp owns one query point at a time:
 //
-//   1. bucket lookup   : the query's L table codes are warp-uniform; each selects one CSR range
-//                        [lo, lo+len) of the train image's bucket index      (matcher.cpp:164-169)
-//   2. Hamming scan    : 32 candidates per step, one per lane: id = points[...], train code
-//                        gathered from shared memory, 4x LOP3 + 4x POPC,
+//   1. bucket lookup   : kBatch queries at a time, ONE QUERY PER LANE: the lane reads its query's L
+//                        table codes and long code from global memory, resolves the L CSR ranges
+//                        [first, last] in the train image's bucket index (shared memory) and parks
+//                        everything the warp-wide steps below need in a per-warp staging record
+//                        (matcher.cpp:164-169).  The query-side global round trip is paid once per
+//                        batch; the per-query code reads the record with uniform shared loads.
+//   2. Hamming scan    : 32 candidates per step, one per lane: id = ids[...], train code gathered
+//                        from shared memory (LDS.128), 4x LOP3 + 4x POPC,
 //                        key = distance<<24 | id                              (matcher.cpp:68-84)
-//                        Step t covers the first 32 entries of table t's bucket (no index
-//                        arithmetic beyond one add); the entries past 32 of all buckets are
-//                        flattened into kOverSlots further steps.  All steps are
-//                        straight-line code, so their loads overlap.  Queries whose buckets
-//                        overflow that (large images) take rounds of 32 entries per table: a
-//                        first pass keeps only the smallest key, and only queries with a
-//                        candidate within tau pay for a second, merging pass.
+//                        Step t covers the first 32 entries of table t's bucket; its ids were
+//                        PREFETCHED while the previous query was ranked and verified.  The entries
+//                        past 32 of all buckets form one flat index space walked by up to
+//                        kOverSlots further steps; the table a flat index falls in comes from a
+//                        staged lane mask (segment = popc(mask & lanes<=l)), not a compare chain.
+//                        The bucket lists are stored in a bank-friendly order (see DevImage::scan),
+//                        so 8 consecutive entries gather from 8 different bank groups.
+//                        Queries whose buckets overflow that (large images) take rounds of 32
+//                        entries per table: a first pass keeps only the smallest key, and only
+//                        queries with a candidate within tau pay for a second, merging pass.
 //   3. ranking         : the ranked list is the first n keys in ascending (distance, id) order
 //                        with EQUAL KEYS COLLAPSED — the same point reached through several
 //                        tables has the same key, so the reference's sort+unique
@@ -26,12 +33,12 @@
 //                        a warp-wide REDUX.MIN picks the winner.  The threshold tau and the
 //                        re-rank fallback (matcher.cpp:176-189) only decide where the pulling
 //                        stops, so no histogram has to be stored.
-//   4. verification    : 8 lanes per candidate row, __vabsdiffu4 + __dp4a (exact u32 squared
+//   4. verification    : 2 lanes per candidate row, __vabsdiffu4 + __dp4a (exact u32 squared
 //                        distance), best / second with rank-order tie-break, Lowe ratio in
 //                        fp64 exactly as matcher.cpp:115-137.
 //
-// Results go to a per-query scratch (train id, d^2); compact_kernel turns them into the
-// reference's MatchRecord stream, ascending query index inside every pair.
+// Results go to a per-query scratch (train id, d^2); compact_kernel (compact_kernels.cuh) turns
+// them into the reference's MatchRecord stream, ascending query index inside every pair.
 #pragma once
 
 #include <utility>
