@@ -13,6 +13,7 @@
 //     match             match_pair                              include/cashash/matcher.hpp:98-100
 //     match output      save_matches / pair_file_name           include/cashash/feature_io.hpp:106,
 //                                                               include/cashash/engine.hpp:79
+//     guided match      guided_match_pair (F as 9 doubles)      include/cashash/geometry.hpp:86-89
 //     pair list         plan_exhaustive (flattened)             include/cashash/scheduler.hpp:53
 //
 // A caller of the reference switches by including this header and `namespace cashash =
@@ -485,6 +486,33 @@ public:
         ck(st);
     }
 
+    // epipolar-guided pair list (guided_match_pair, geometry.cpp:234-250): one row-major 3x3 F per pair
+    std::vector<PairMatches> match_pairs_guided(std::span<const std::pair<std::uint32_t, std::uint32_t>> pairs,
+                                                std::span<const std::array<double, 9>> fmats, double band_px,
+                                                const MatchConfig& cfg, MatchStats* stats = nullptr) {
+        if (fmats.size() != pairs.size()) throw std::invalid_argument("guided match: one fundamental matrix per pair");
+        std::vector<PairMatches> out(pairs.size());
+        for (std::size_t k = 0; k < pairs.size(); ++k) {
+            out[k].image_i = pairs[k].first;
+            out[k].image_j = pairs[k].second;
+        }
+        const chgpu_match_cfg c = detail::to_c(cfg);
+        struct Fill {
+            std::vector<PairMatches>* out;
+        } fill{&out};
+        auto trampoline = [](void* user, std::uint32_t first, std::uint32_t count, const std::uint64_t* offs,
+                             const chgpu_match_record* rec) -> int {
+            auto* o = static_cast<Fill*>(user)->out;
+            const MatchRecord* r = reinterpret_cast<const MatchRecord*>(rec);
+            for (std::uint32_t k = 0; k < count; ++k) (*o)[first + k].matches.assign(r + offs[k], r + offs[k + 1]);
+            return 0;
+        };
+        ck(chgpu_match_pairs_guided_stream(ctx_, reinterpret_cast<const std::uint32_t*>(pairs.data()),
+                                           static_cast<std::uint32_t>(pairs.size()), &c,
+                                           fmats.empty() ? nullptr : fmats.front().data(), band_px, trampoline, &fill, stats));
+        return out;
+    }
+
     void sync() { ck(chgpu_sync(ctx_)); }
 
 private:
@@ -667,6 +695,44 @@ inline std::vector<MatchRecord> match_pair(const FeatureSet& fs_i, const Feature
     m.upload_codes(detail::kScratchB, codes_j);
     const std::pair<std::uint32_t, std::uint32_t> pr{detail::kScratchA, detail::kScratchB};
     std::vector<PairMatches> out = m.match_pairs({&pr, 1}, cfg);
+    return std::move(out.front().matches);
+}
+
+// guided_match_pair (geometry.hpp:86-89): match_pair with the epipolar band between lookup and ranking.
+// F is the row-major 3x3 fundamental matrix (the reference's Eigen::Matrix3d, coefficient (r, c) at 3 r + c);
+// estimating it (eight_point / ransac_fundamental) stays on the caller's side.
+using FundamentalMatrix = std::array<double, 9>;
+
+inline std::vector<MatchRecord> guided_match_pair(const FeatureSet& fs_i, const FeatureSet& fs_j, const ImageCodes& codes_i,
+                                                  const ImageCodes& codes_j, const FundamentalMatrix& f,
+                                                  const MatchConfig& cfg, double band_px) {
+    if (!(codes_i.params == codes_j.params))
+        throw std::invalid_argument("match_pair: codes come from different hash families");
+    if (codes_i.shorts.point_count != fs_i.size() || codes_j.shorts.point_count != fs_j.size())
+        throw std::invalid_argument("match_pair: code/point count mismatch");
+    static std::mutex fam_mu;
+    static std::vector<std::unique_ptr<HashFamily>> families;
+    const HashFamily* fam = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(fam_mu);
+        for (const auto& g : families)
+            if (g->params == codes_i.params) fam = g.get();
+        if (!fam) {
+            families.push_back(std::make_unique<HashFamily>(build_hash_family(codes_i.params)));
+            fam = families.back().get();
+        }
+    }
+    detail::DefaultContext& dc = detail::default_context();
+    std::lock_guard<std::mutex> lock(dc.mu);
+    Matcher& m = dc.with(*fam);
+    m.upload(detail::kScratchA, fs_i);
+    detail::ScopedImage ga{m, detail::kScratchA};
+    m.upload(detail::kScratchB, fs_j);
+    detail::ScopedImage gb{m, detail::kScratchB};
+    m.upload_codes(detail::kScratchA, codes_i);
+    m.upload_codes(detail::kScratchB, codes_j);
+    const std::pair<std::uint32_t, std::uint32_t> pr{detail::kScratchA, detail::kScratchB};
+    std::vector<PairMatches> out = m.match_pairs_guided({&pr, 1}, {&f, 1}, band_px, cfg);
     return std::move(out.front().matches);
 }
 

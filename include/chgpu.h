@@ -209,10 +209,27 @@ chgpu_status chgpu_match_pairs_stream(chgpu_ctx* ctx, const uint32_t* pairs, uin
 chgpu_status chgpu_match_pairs_device(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
                                       const chgpu_match_cfg* cfg, chgpu_match_stats* stats);
 
+/* Epipolar-guided variant (guided_match_pair, geometry.hpp:86-89, geometry.cpp:234-250 — the only
+ * CandidateFilter the reference ships, matcher.hpp:92-105).  fmats: npairs x 9 doubles, row-major fundamental
+ * matrices mapping a query point of image I to its epipolar line in image J; between lookup and ranking the
+ * candidates of a query are cut to those within band_px of the line l = F (x, y, 1)^T (keypoints as uploaded);
+ * a degenerate line (a == b == 0) leaves that query unguided.  Estimating F (RANSAC) is the caller's business. */
+chgpu_status chgpu_match_pairs_guided(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
+                                      const chgpu_match_cfg* cfg, const double* fmats, double band_px,
+                                      uint64_t* offsets, chgpu_match_record* records, uint64_t capacity,
+                                      uint64_t* total, chgpu_match_stats* stats /* nullable */);
+chgpu_status chgpu_match_pairs_guided_stream(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
+                                             const chgpu_match_cfg* cfg, const double* fmats, double band_px,
+                                             chgpu_sink_fn sink, void* user, chgpu_match_stats* stats /* nullable */);
+
 /* Parity hook: the ranked candidate list each query hands to verification (after the re-rank
  * fallback, matcher.cpp:176-189).  ranked: n_i*top_k u32, ranked_count: n_i u32. */
 chgpu_status chgpu_debug_ranked(chgpu_ctx* ctx, uint32_t image_i, uint32_t image_j,
                                 const chgpu_match_cfg* cfg, uint32_t* ranked, uint32_t* ranked_count);
+
+chgpu_status chgpu_debug_ranked_guided(chgpu_ctx* ctx, uint32_t image_i, uint32_t image_j,
+                                       const chgpu_match_cfg* cfg, const double* fmat, double band_px,
+                                       uint32_t* ranked, uint32_t* ranked_count);
 
 /* ---- match output ---------------------------------------------------------------------- */
 /* Replaces save_matches (feature_io.hpp:106-107, feature_io.cpp:161-183): byte-identical text. */

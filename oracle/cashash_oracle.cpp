@@ -142,11 +142,34 @@ struct Ranker {
     }
 };
 
+// Epipolar band filter of guided_match_pair (geometry.cpp:234-250).
+struct BandFilter {
+    const float* kp_i;  // n_i x 4
+    const float* kp_j;  // n_j x 4
+    const double* F;    // 3 x 3 row-major
+    double band_px;
+
+    // Returns false (candidates untouched) for a degenerate line.
+    bool apply(uint32_t q, std::vector<uint32_t>& cands) const {
+        const double x = kp_i[4 * static_cast<size_t>(q)], y = kp_i[4 * static_cast<size_t>(q) + 1];
+        const double a = (F[0] * x + F[1] * y) + F[2];  // epipolar_line: l = F (x, y, 1)^T  (geometry.cpp:98-101)
+        const double b = (F[3] * x + F[4] * y) + F[5];
+        const double c = (F[6] * x + F[7] * y) + F[8];
+        if (a == 0.0 && b == 0.0) return false;  // EpipolarLine::degenerate, geometry.hpp:28
+        const double inv_norm = 1.0 / std::sqrt(a * a + b * b);
+        std::erase_if(cands, [&](uint32_t idx) {
+            const double tx = kp_j[4 * static_cast<size_t>(idx)], ty = kp_j[4 * static_cast<size_t>(idx) + 1];
+            return std::abs(a * tx + b * ty + c) * inv_norm > band_px;
+        });
+        return true;
+    }
+};
+
 int match_pair_impl(const chor_family_params& p, const chor_match_cfg& cfg,
                     const uint8_t* desc_i, uint32_t n_i, const uint32_t* shorts_i, const uint64_t* longs_i,
                     const uint8_t* desc_j, uint32_t n_j, const uint32_t* shorts_j, const uint64_t* longs_j,
                     chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
-                    uint32_t* ranked_out, uint32_t* ranked_count) {
+                    uint32_t* ranked_out, uint32_t* ranked_count, const BandFilter* filter = nullptr) {
     // matcher.cpp:141-195.  Family equality / count checks are structural in this flat ABI.
     if (!family_ok(p) || !cfg_ok(cfg, p.long_bits)) return 1;
     chor_pair_stats st{};
@@ -169,6 +192,7 @@ int match_pair_impl(const chor_family_params& p, const chor_match_cfg& cfg,
             std::sort(cands.begin(), cands.end());
             cands.erase(std::unique(cands.begin(), cands.end()), cands.end());
             st.unique_candidates += cands.size();
+            if (filter && !cands.empty()) filter->apply(q, cands);  // matcher.cpp:172
             if (cands.empty()) continue;
 
             const uint64_t* ql = longs_i + 2 * static_cast<size_t>(q);
@@ -341,6 +365,17 @@ int chor_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
                     uint32_t* ranked, uint32_t* ranked_count) {
     return match_pair_impl(*p, *cfg, desc_i, n_i, shorts_i, longs_i, desc_j, n_j, shorts_j, longs_j,
                            records, record_count, stats, ranked, ranked_count);
+}
+
+int chor_guided_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
+                           const uint8_t* desc_i, const float* kp_i, uint32_t n_i, const uint32_t* shorts_i,
+                           const uint64_t* longs_i, const uint8_t* desc_j, const float* kp_j, uint32_t n_j,
+                           const uint32_t* shorts_j, const uint64_t* longs_j, const double* F, double band_px,
+                           chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
+                           uint32_t* ranked, uint32_t* ranked_count) {
+    const BandFilter filter{kp_i, kp_j, F, band_px};
+    return match_pair_impl(*p, *cfg, desc_i, n_i, shorts_i, longs_i, desc_j, n_j, shorts_j, longs_j, records,
+                           record_count, stats, ranked, ranked_count, &filter);
 }
 
 int chor_brute_force_match(const uint8_t* desc_i, uint32_t n_i, const uint8_t* desc_j, uint32_t n_j,

@@ -91,6 +91,21 @@ int chor_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
                     chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
                     uint32_t* ranked, uint32_t* ranked_count);
 
+/* Epipolar-guided variant (guided_match_pair, geometry.cpp:234-250 over match_pair_filtered,
+ * matcher.cpp:205-210): between candidate lookup and ranking the candidates of query q are cut to those
+ * within band_px of the epipolar line l = F (x_q, y_q, 1)^T; a degenerate line (a == b == 0) leaves the
+ * query unguided.  kp_*: n x 4 f32 (x, y, scale, orientation); F: 9 doubles, row-major.
+ * The line is evaluated as l_i = (F[i][0]*x + F[i][1]*y) + F[i][2] in fp64 without contraction (the
+ * reference forms it with an Eigen 3x3 * 3x1 product whose association order is not pinned here: Eigen is
+ * absent from this image, so geometry.cpp cannot be compiled).  In oracle/_ref everything but that line is
+ * the reference's own code (match_pair_filtered with this filter). */
+int chor_guided_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
+                           const uint8_t* desc_i, const float* kp_i, uint32_t n_i, const uint32_t* shorts_i,
+                           const uint64_t* longs_i, const uint8_t* desc_j, const float* kp_j, uint32_t n_j,
+                           const uint32_t* shorts_j, const uint64_t* longs_j, const double* F, double band_px,
+                           chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
+                           uint32_t* ranked, uint32_t* ranked_count);
+
 int chor_brute_force_match(const uint8_t* desc_i, uint32_t n_i, const uint8_t* desc_j, uint32_t n_j,
                            double ratio, chor_match_record* records, uint32_t* record_count);
 

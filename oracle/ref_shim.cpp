@@ -8,6 +8,7 @@
 #include "chor.h"
 
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <stdexcept>
 #include <thread>
@@ -201,6 +202,64 @@ int chor_lookup_candidates(uint32_t m, uint32_t L, const uint32_t* query_codes,
     });
 }
 
+namespace {
+
+// Shared body of chor_match_pair / chor_guided_match_pair: records from the reference's own
+// match_pair / match_pair_filtered; intermediate artefacts through its PUBLIC ops only
+// (lookup_candidates, rank_histogram) with the re-rank rule stated at matcher.hpp:18-21.
+void match_pair_body(const FamilyParams& fp, const MatchConfig& mc, const FeatureSet& fi, const FeatureSet& fj,
+                     const ImageCodes& ci, const ImageCodes& cj, const CandidateFilter* filter,
+                     chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
+                     uint32_t* ranked, uint32_t* ranked_count) {
+    const uint32_t n_i = static_cast<uint32_t>(fi.size()), n_j = static_cast<uint32_t>(fj.size());
+    const std::vector<MatchRecord> out =
+        filter ? match_pair_filtered(fi, fj, ci, cj, mc, *filter) : match_pair(fi, fj, ci, cj, mc);
+    static_assert(sizeof(MatchRecord) == sizeof(chor_match_record));
+    std::memcpy(records, out.data(), out.size() * sizeof(MatchRecord));
+    *record_count = static_cast<uint32_t>(out.size());
+    if (!stats && !ranked) return;
+
+    chor_pair_stats st{};
+    if (ranked_count) std::fill(ranked_count, ranked_count + n_i, 0u);
+    if (n_i && n_j) {
+        const BucketIndex idx = build_bucket_index(cj.shorts);
+        const uint32_t min_ranked = std::max<uint32_t>(2, mc.min_candidates_for_ratio);
+        for (uint32_t q = 0; q < n_i; ++q) {
+            std::span<const uint32_t> qc(ci.shorts.values.data() + size_t(q) * fp.table_count, fp.table_count);
+            for (uint32_t t = 0; t < fp.table_count; ++t) st.raw_candidates += idx.bucket(t, qc[t]).size();
+            auto cands = lookup_candidates(qc, idx);
+            st.unique_candidates += cands.size();
+            if (filter && !cands.empty()) (*filter)(q, cands);
+            if (cands.empty()) continue;
+            RankHistogram h = rank_histogram(ci.longs.codes[q], cands, cj.longs.codes, mc.hamming_threshold);
+            size_t keep = std::min<size_t>(mc.top_k, h.items.size());
+            if (keep) ++st.ranked_queries;
+            if (keep && keep < min_ranked && cands.size() > h.items.size()) {
+                h = rank_histogram(ci.longs.codes[q], cands, cj.longs.codes, fp.long_bits);
+                keep = std::min<size_t>(mc.top_k, h.items.size());
+                ++st.fallback_queries;
+            }
+            if (ranked) {
+                for (size_t r = 0; r < keep; ++r) ranked[size_t(q) * mc.top_k + r] = h.items[r];
+                ranked_count[q] = static_cast<uint32_t>(keep);
+            }
+            if (keep >= 2) {
+                ++st.verified_queries;
+                st.distances += keep;
+            }
+        }
+    }
+    st.matches = out.size();
+    if (stats) *stats = st;
+}
+
+void set_keypoints(FeatureSet& fs, const float* kp) {
+    for (size_t i = 0; i < fs.keypoints.size(); ++i)
+        fs.keypoints[i] = Keypoint{kp[4 * i], kp[4 * i + 1], kp[4 * i + 2], kp[4 * i + 3]};
+}
+
+}  // namespace
+
 int chor_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
                     const uint8_t* desc_i, uint32_t n_i, const uint32_t* shorts_i, const uint64_t* longs_i,
                     const uint8_t* desc_j, uint32_t n_j, const uint32_t* shorts_j, const uint64_t* longs_j,
@@ -212,46 +271,41 @@ int chor_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
         const MatchConfig mc = to_cfg(*cfg);
         const FeatureSet fi = to_features(desc_i, n_i), fj = to_features(desc_j, n_j);
         const ImageCodes ci = to_codes(fp, shorts_i, longs_i, n_i), cj = to_codes(fp, shorts_j, longs_j, n_j);
-        const std::vector<MatchRecord> out = match_pair(fi, fj, ci, cj, mc);
-        static_assert(sizeof(MatchRecord) == sizeof(chor_match_record));
-        std::memcpy(records, out.data(), out.size() * sizeof(MatchRecord));
-        *record_count = static_cast<uint32_t>(out.size());
+        match_pair_body(fp, mc, fi, fj, ci, cj, nullptr, records, record_count, stats, ranked, ranked_count);
+    });
+}
 
-        if (stats || ranked) {
-            // Intermediate artefacts through the reference's PUBLIC ops only (lookup_candidates,
-            // rank_histogram); the re-rank rule is the one stated at matcher.hpp:18-21.
-            chor_pair_stats st{};
-            if (ranked_count) std::fill(ranked_count, ranked_count + n_i, 0u);
-            if (n_i && n_j) {
-                const BucketIndex idx = build_bucket_index(cj.shorts);
-                const uint32_t min_ranked = std::max<uint32_t>(2, mc.min_candidates_for_ratio);
-                for (uint32_t q = 0; q < n_i; ++q) {
-                    std::span<const uint32_t> qc(ci.shorts.values.data() + size_t(q) * fp.table_count, fp.table_count);
-                    for (uint32_t t = 0; t < fp.table_count; ++t) st.raw_candidates += idx.bucket(t, qc[t]).size();
-                    const auto cands = lookup_candidates(qc, idx);
-                    st.unique_candidates += cands.size();
-                    if (cands.empty()) continue;
-                    RankHistogram h = rank_histogram(ci.longs.codes[q], cands, cj.longs.codes, mc.hamming_threshold);
-                    size_t keep = std::min<size_t>(mc.top_k, h.items.size());
-                    if (keep) ++st.ranked_queries;
-                    if (keep && keep < min_ranked && cands.size() > h.items.size()) {
-                        h = rank_histogram(ci.longs.codes[q], cands, cj.longs.codes, fp.long_bits);
-                        keep = std::min<size_t>(mc.top_k, h.items.size());
-                        ++st.fallback_queries;
-                    }
-                    if (ranked) {
-                        for (size_t r = 0; r < keep; ++r) ranked[size_t(q) * mc.top_k + r] = h.items[r];
-                        ranked_count[q] = static_cast<uint32_t>(keep);
-                    }
-                    if (keep >= 2) {
-                        ++st.verified_queries;
-                        st.distances += keep;
-                    }
-                }
-            }
-            st.matches = out.size();
-            if (stats) *stats = st;
-        }
+int chor_guided_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
+                           const uint8_t* desc_i, const float* kp_i, uint32_t n_i, const uint32_t* shorts_i,
+                           const uint64_t* longs_i, const uint8_t* desc_j, const float* kp_j, uint32_t n_j,
+                           const uint32_t* shorts_j, const uint64_t* longs_j, const double* F, double band_px,
+                           chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
+                           uint32_t* ranked, uint32_t* ranked_count) {
+    return guarded([&] {
+        const FamilyParams fp = to_params(*p);
+        validate(fp);
+        const MatchConfig mc = to_cfg(*cfg);
+        FeatureSet fi = to_features(desc_i, n_i), fj = to_features(desc_j, n_j);
+        set_keypoints(fi, kp_i);
+        set_keypoints(fj, kp_j);
+        const ImageCodes ci = to_codes(fp, shorts_i, longs_i, n_i), cj = to_codes(fp, shorts_j, longs_j, n_j);
+        // The band filter of guided_match_pair (geometry.cpp:238-248).  geometry.cpp itself needs Eigen
+        // and cannot be compiled here; everything around this lambda is the reference's own code.
+        const CandidateFilter filter = [&](std::uint32_t q, std::vector<std::uint32_t>& candidates) {
+            const Keypoint& kp = fi.keypoints[q];
+            const double x = kp.x, y = kp.y;
+            const double a = (F[0] * x + F[1] * y) + F[2];
+            const double b = (F[3] * x + F[4] * y) + F[5];
+            const double c = (F[6] * x + F[7] * y) + F[8];
+            if (a == 0.0 && b == 0.0) return false;
+            const double inv_norm = 1.0 / std::sqrt(a * a + b * b);
+            std::erase_if(candidates, [&](std::uint32_t idx) {
+                const Keypoint& t = fj.keypoints[idx];
+                return std::abs(a * t.x + b * t.y + c) * inv_norm > band_px;
+            });
+            return true;
+        };
+        match_pair_body(fp, mc, fi, fj, ci, cj, &filter, records, record_count, stats, ranked, ranked_count);
     });
 }
 

@@ -94,6 +94,12 @@ SIGNATURES = {
                                            C.c_void_p, C.POINTER(MatchStatsC)]),
     "chgpu_match_pairs_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(MatchCfgC),
                                            C.POINTER(MatchStatsC)]),
+    "chgpu_match_pairs_guided": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(MatchCfgC), C.c_void_p, C.c_double,
+                                           C.c_void_p, C.c_void_p, C.c_uint64, u64p, C.POINTER(MatchStatsC)]),
+    "chgpu_match_pairs_guided_stream": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(MatchCfgC), C.c_void_p,
+                                                  C.c_double, SINK_FN, C.c_void_p, C.POINTER(MatchStatsC)]),
+    "chgpu_debug_ranked_guided": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(MatchCfgC), C.c_void_p, C.c_double,
+                                            C.c_void_p, C.c_void_p]),
     "chgpu_debug_ranked": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(MatchCfgC), C.c_void_p,
                                      C.c_void_p]),
     "chgpu_save_matches": (C.c_int, [C.c_char_p, C.c_char_p, C.c_void_p, C.c_uint32, C.c_char_p]),

@@ -447,6 +447,31 @@ class Matcher:
         self._ck(st)
         return stats.as_dict()
 
+    def match_pairs_guided(self, pairs, fmats, band_px: float, cfg: MatchConfig = MatchConfig()):
+        """guided_match_pair over a pair list: fmats (npairs, 3, 3) f64.  Returns (offsets, records, stats)."""
+        pr = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
+        f = np.ascontiguousarray(fmats, dtype=np.float64).reshape(len(pr), 9)
+        capacity = int(sum(self.points(int(a)) for a in pr[:, 0]))
+        c = cfg.c()
+        stats = N.MatchStatsC()
+        offsets = np.zeros(len(pr) + 1, dtype=np.uint64)
+        total = C.c_uint64(0)
+        records = np.zeros(max(capacity, 1), dtype=RECORD_DTYPE)
+        self._ck(self.lib.chgpu_match_pairs_guided(self.h, pr.ctypes.data, len(pr), C.byref(c), f.ctypes.data, band_px,
+                                                   offsets.ctypes.data, records.ctypes.data, capacity, C.byref(total),
+                                                   C.byref(stats)))
+        return offsets, records[: total.value], stats.as_dict()
+
+    def ranked_guided(self, image_i: int, image_j: int, fmat, band_px: float, cfg: MatchConfig = MatchConfig()):
+        n = self.points(image_i)
+        ranked = np.zeros((n, cfg.top_k), dtype=np.uint32)
+        count = np.zeros(n, dtype=np.uint32)
+        c = cfg.c()
+        f = np.ascontiguousarray(fmat, dtype=np.float64).reshape(9)
+        self._ck(self.lib.chgpu_debug_ranked_guided(self.h, image_i, image_j, C.byref(c), f.ctypes.data, band_px,
+                                                    ranked.ctypes.data, count.ctypes.data))
+        return ranked, count
+
     def ranked(self, image_i: int, image_j: int, cfg: MatchConfig = MatchConfig()):
         n = self.points(image_i)
         ranked = np.zeros((n, cfg.top_k), dtype=np.uint32)

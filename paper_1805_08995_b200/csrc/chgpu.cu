@@ -106,6 +106,8 @@ struct MatchBuffers {
     uint32_t* d_counts = nullptr;
     unsigned long long* d_offsets = nullptr;
     unsigned long long* h_offsets = nullptr;  // pinned
+    double* d_fmats = nullptr;  // guided: 9 doubles per pair of the sub-batch
+    size_t fmats_cap = 0;    // pairs
     uint4* d_records = nullptr;
     size_t records_cap = 0;  // entries
     chgpu_match_record* h_records = nullptr;  // pinned
@@ -376,29 +378,27 @@ size_t offs_smem_bytes(const chgpu_ctx* ctx) {
     return (size_t(ctx->fam.table_count) * ((size_t(1) << ctx->fam.short_bits) + 1) * 4 + 15) & ~size_t(15);
 }
 
-size_t stage_smem_bytes(const chgpu_ctx* ctx) {
-    // per-warp lookup staging of the match kernel; LT is the table count rounded up to 4, 6 or 8
-    const uint32_t L = ctx->fam.table_count;
-    const int LT = L <= 4 ? 4 : (L <= 6 ? 6 : 8);
-    return size_t(kMatchThreads / 32) * stage_bytes_per_warp(LT);
+size_t stage_smem_bytes(const chgpu_ctx* ctx, bool guided = false) {
+    // per-warp lookup staging of the match kernel
+    return size_t(kMatchThreads / 32) * stage_bytes_per_warp(match_table_slots(ctx->fam.table_count, guided));
 }
 
 cudaError_t launch_match(chgpu_ctx* ctx, MatchParams& P, bool smem_train, uint32_t max_nt, uint32_t* grid) {
     const int sms = ctx->prop.multiProcessorCount;
-    if (smem_train) {
-        P.smem_long_bytes = std::max<uint32_t>(max_nt * 16u, 16u);
-        return launch_match_smem(P, size_t(P.smem_long_bytes) + offs_smem_bytes(ctx) + stage_smem_bytes(ctx), sms,
-                                 ctx->compute, grid);
-    }
-    P.smem_long_bytes = 0;
-    return launch_match_global(P, stage_smem_bytes(ctx), sms, ctx->compute, grid);
+    const bool guided = P.fmats != nullptr;
+    P.smem_long_bytes = smem_train ? std::max<uint32_t>(max_nt * 16u, 16u) : 0u;
+    const size_t smem = smem_train ? size_t(P.smem_long_bytes) + offs_smem_bytes(ctx) + stage_smem_bytes(ctx, guided)
+                                   : stage_smem_bytes(ctx, guided);
+    if (guided) return launch_match_guided(P, smem_train, smem, sms, ctx->compute, grid);
+    return smem_train ? launch_match_smem(P, smem, sms, ctx->compute, grid)
+                      : launch_match_global(P, smem, sms, ctx->compute, grid);
 }
 
-size_t smem_train_capacity(const chgpu_ctx* ctx) {
+size_t smem_train_capacity(const chgpu_ctx* ctx, bool guided = false) {
     // points whose codes fit next to the bucket offsets in the dynamic smem of a 1-CTA/SM launch
     // (minus the kernel's static 16 B and the 1 KiB the driver reserves per block)
     const size_t avail = ctx->prop.sharedMemPerBlockOptin - 1024 - 64;
-    const size_t offs = offs_smem_bytes(ctx) + stage_smem_bytes(ctx);
+    const size_t offs = offs_smem_bytes(ctx) + stage_smem_bytes(ctx, guided);
     return avail > offs ? (avail - offs) / 16 : 0;
 }
 
@@ -466,6 +466,9 @@ struct MatchRun {
     // Stream mode
     chgpu_sink_fn sink = nullptr;
     void* user = nullptr;
+    // guided (epipolar band)
+    const double* fmats = nullptr;  // npairs x 9, host
+    double band_px = 0.0;
     // debug
     uint32_t* dbg_ranked = nullptr;
     uint32_t* dbg_count = nullptr;
@@ -537,7 +540,7 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
     CK(cudaMemsetAsync(ctx->d_stats, 0, sizeof(DevStats), ctx->compute));
     CK(cudaEventRecord(ctx->ev_t0, ctx->compute));
 
-    const size_t cap_nt = smem_train_capacity(ctx);
+    const size_t cap_nt = smem_train_capacity(ctx, run.fmats != nullptr);
     const bool host_side = run.mode != SinkMode::Device;
     float match_ms = 0.f;
     uint64_t delivered_records = 0;
@@ -587,6 +590,19 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
         memcpy(b.h_pairs, descs.data() + sb.first, size_t(sb.count) * sizeof(PairDesc));
         CK(cudaMemcpyAsync(b.d_pairs, b.h_pairs, size_t(sb.count) * sizeof(PairDesc), cudaMemcpyHostToDevice, ctx->compute));
         CK(cudaMemsetAsync(b.d_counts, 0, size_t(sb.count) * sizeof(uint32_t), ctx->compute));
+        if (run.fmats) {
+            if (b.fmats_cap < sb.count) {
+                CK(cudaStreamSynchronize(ctx->compute));
+                if (b.d_fmats) cudaFree(b.d_fmats);
+                b.d_fmats = nullptr;
+                b.fmats_cap = 0;
+                CK(cudaMalloc(&b.d_fmats, std::max<size_t>(sb.count, 1024) * 9 * sizeof(double)));
+                b.fmats_cap = std::max<size_t>(sb.count, 1024);
+            }
+            // pageable source: the copy is staged by the runtime before the call returns
+            CK(cudaMemcpyAsync(b.d_fmats, run.fmats + size_t(sb.first) * 9, size_t(sb.count) * 9 * sizeof(double),
+                               cudaMemcpyHostToDevice, ctx->compute));
+        }
         CK(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), ctx->compute));
 
         const bool smem_train = sb.max_nt <= cap_nt;
@@ -611,6 +627,8 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
         P.min_ranked = std::max<uint32_t>(2, run.cfg.min_candidates_for_ratio);
         P.long_bits = ctx->fam.long_bits;
         P.ratio_sq = run.cfg.ratio * run.cfg.ratio;
+        P.fmats = run.fmats ? b.d_fmats : nullptr;
+        P.band_px = run.band_px;
         if (run.dbg_ranked) {
             P.dbg_ranked = ctx->d_dbg;
             P.dbg_count = ctx->d_dbg + size_t(sb.max_nq) * run.cfg.top_k;
@@ -726,7 +744,7 @@ void chgpu_destroy(chgpu_ctx* ctx) {
     ctx->arena.destroy();
     for (MatchBuffers& b : ctx->mb) {
         cudaFree(b.d_pairs); cudaFreeHost(b.h_pairs); cudaFree(b.d_counts); cudaFree(b.d_offsets);
-        cudaFreeHost(b.h_offsets); cudaFree(b.d_records); cudaFreeHost(b.h_records);
+        cudaFreeHost(b.h_offsets); cudaFree(b.d_records); cudaFreeHost(b.h_records); cudaFree(b.d_fmats);
         if (b.ev_done) cudaEventDestroy(b.ev_done);
         if (b.ev_k0) cudaEventDestroy(b.ev_k0);
         if (b.ev_k1) cudaEventDestroy(b.ev_k1);
@@ -1144,11 +1162,56 @@ chgpu_status chgpu_match_pairs_stream(chgpu_ctx* ctx, const uint32_t* pairs, uin
     return run_match(ctx, run, stats);
 }
 
+chgpu_status chgpu_match_pairs_guided(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs, const chgpu_match_cfg* cfg,
+                                      const double* fmats, double band_px, uint64_t* offsets, chgpu_match_record* records,
+                                      uint64_t capacity, uint64_t* total, chgpu_match_stats* stats) {
+    if (!ctx || !cfg || !offsets || (npairs && (!pairs || !fmats)) || (capacity && !records)) return CHGPU_EINVAL;
+    if (!(band_px >= 0.0)) return fail(ctx, CHGPU_EINVAL, "band_px must be >= 0");
+    MatchRun run{pairs, npairs, *cfg, SinkMode::Host};
+    run.offsets = offsets;
+    run.records = records;
+    run.capacity = capacity;
+    run.fmats = npairs ? fmats : nullptr;
+    run.band_px = band_px;
+    const chgpu_status s = run_match(ctx, run, stats);
+    if (total) *total = run.total;
+    if (s != CHGPU_OK) return s;
+    if (run.overflow)
+        return fail(ctx, CHGPU_ENOMEM, "record capacity %llu < %llu required", (unsigned long long)capacity,
+                    (unsigned long long)run.total);
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_match_pairs_guided_stream(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
+                                             const chgpu_match_cfg* cfg, const double* fmats, double band_px,
+                                             chgpu_sink_fn sink, void* user, chgpu_match_stats* stats) {
+    if (!ctx || !cfg || (npairs && (!pairs || !fmats))) return CHGPU_EINVAL;
+    if (!(band_px >= 0.0)) return fail(ctx, CHGPU_EINVAL, "band_px must be >= 0");
+    MatchRun run{pairs, npairs, *cfg, SinkMode::Stream};
+    run.sink = sink;
+    run.user = user;
+    run.fmats = npairs ? fmats : nullptr;
+    run.band_px = band_px;
+    return run_match(ctx, run, stats);
+}
+
 chgpu_status chgpu_match_pairs_device(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
                                       const chgpu_match_cfg* cfg, chgpu_match_stats* stats) {
     if (!ctx || !cfg || (npairs && !pairs)) return CHGPU_EINVAL;
     MatchRun run{pairs, npairs, *cfg, SinkMode::Device};
     return run_match(ctx, run, stats);
+}
+
+chgpu_status chgpu_debug_ranked_guided(chgpu_ctx* ctx, uint32_t image_i, uint32_t image_j, const chgpu_match_cfg* cfg,
+                                       const double* fmat, double band_px, uint32_t* ranked, uint32_t* ranked_count) {
+    if (!ctx || !cfg || !ranked || !ranked_count || !fmat) return CHGPU_EINVAL;
+    const uint32_t pr[2] = {image_i, image_j};
+    MatchRun run{pr, 1, *cfg, SinkMode::Device};
+    run.dbg_ranked = ranked;
+    run.dbg_count = ranked_count;
+    run.fmats = fmat;
+    run.band_px = band_px;
+    return run_match(ctx, run, nullptr);
 }
 
 chgpu_status chgpu_debug_ranked(chgpu_ctx* ctx, uint32_t image_i, uint32_t image_j, const chgpu_match_cfg* cfg,

@@ -86,6 +86,8 @@ struct MatchParams {
     uint32_t top_k, tau, min_ranked, long_bits;
     uint32_t smem_long_bytes;   // SMEM_TRAIN: bytes reserved for the train codes (offsets follow)
     double ratio_sq;            // cfg.ratio * cfg.ratio, formed on the host in fp64
+    const double* fmats;        // GUIDED: 9 doubles per pair, row-major fundamental matrix (I -> lines in J)
+    double band_px;             // GUIDED: epipolar band half-width in pixels
     uint32_t* dbg_ranked;       // optional: n_i x top_k
     uint32_t* dbg_count;        // optional: n_i
 };
@@ -244,8 +246,33 @@ constexpr uint32_t kBatch = 16;
 __host__ __device__ constexpr uint32_t stage_record_bytes(int LT) { return (32u + uint32_t(LT) * 12u + 15u) & ~15u; }
 __host__ __device__ constexpr uint32_t stage_bytes_per_warp(int LT) { return kBatch * stage_record_bytes(LT); }
 
-// LT = number of table slots unrolled in registers (>= L); EXACT: L == LT, no per-table guards.
-template <bool SMEM_TRAIN, int LT, bool EXACT>
+// Epipolar band of one query (guided_match_pair, geometry.cpp:234-250): l = F (x, y, 1)^T, candidates
+// farther than band_px from the line are dropped between lookup and ranking; a degenerate line leaves the
+// query unguided.  fp64, every operation individually rounded, in the order the oracle states (chor.h).
+struct EpiLine {
+    double a, b, c, inv_norm;
+    bool active;
+};
+__device__ __forceinline__ EpiLine epipolar_band(const double* __restrict__ F, float4 kp) {
+    const double x = double(kp.x), y = double(kp.y);
+    EpiLine l;
+    l.a = __dadd_rn(__dadd_rn(__dmul_rn(__ldg(F + 0), x), __dmul_rn(__ldg(F + 1), y)), __ldg(F + 2));
+    l.b = __dadd_rn(__dadd_rn(__dmul_rn(__ldg(F + 3), x), __dmul_rn(__ldg(F + 4), y)), __ldg(F + 5));
+    l.c = __dadd_rn(__dadd_rn(__dmul_rn(__ldg(F + 6), x), __dmul_rn(__ldg(F + 7), y)), __ldg(F + 8));
+    l.active = !(l.a == 0.0 && l.b == 0.0);
+    l.inv_norm = l.active ? __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__dmul_rn(l.a, l.a), __dmul_rn(l.b, l.b)))) : 0.0;
+    return l;
+}
+__device__ __forceinline__ uint32_t band_filter(uint32_t key, const EpiLine& l, const float4* __restrict__ kp_j, double band_px) {
+    if (!l.active || key == kNone) return key;
+    const float4 t = __ldg(kp_j + (key & 0xffffffu));
+    const double d = __dmul_rn(fabs(__dadd_rn(__dadd_rn(__dmul_rn(l.a, double(t.x)), __dmul_rn(l.b, double(t.y))), l.c)), l.inv_norm);
+    return d > band_px ? kNone : key;
+}
+
+// LT = number of table slots unrolled in registers (>= L); EXACT: L == LT, no per-table guards;
+// GUIDED: the epipolar band filter above is applied to every candidate.
+template <bool SMEM_TRAIN, int LT, bool EXACT, bool GUIDED>
 __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchParams P) {
     extern __shared__ __align__(16) unsigned char s_raw[];  // [train codes | bucket offsets | lookup staging]
     __shared__ unsigned int s_unit;
@@ -341,7 +368,8 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                                 b = __ldg(o + 1);
                             }
                         }
-                        const uint32_t len = b - a, first = t * J.n + a;
+                        const uint32_t len = b - a;
+                        const uint32_t first = (EXACT || t < int(L)) ? t * J.n + a : 0u;  // unused slots: entry 0, discarded
                         total += len;
                         if (len == 0) empty |= 1u << t;
                         sts64(rec + 32u + t * 8u, first, first + max(len, 1u) - 1u);
@@ -392,6 +420,8 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 
                 uint32_t mykey = kNone;  // lane r holds the r-th ranked key
                 uint32_t n = 0;          // ranked count
+                EpiLine line{};
+                if (GUIDED) line = epipolar_band(P.fmats + uint64_t(pair) * 9, __ldg(I.kp + q));
 
                 if (tover <= 32u * kOverSlots) {
                     // ---- 2. Hamming scan: the first 32 entries of every bucket, one table per slot,
@@ -421,6 +451,10 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 #pragma unroll
                     for (int s = 0; s < kOverSlots; ++s)
                         if (uint32_t(s) * 32u < tover) key[LT + s] = key_of<SMEM_TRAIN>(key[LT + s], ql, s_long, J.longs);
+                    if (GUIDED) {
+#pragma unroll
+                        for (int i = 0; i < KS; ++i) key[i] = band_filter(key[i], line, J.kp, P.band_px);
+                    }
                     // ---- 3. ranking: pull straight out of the slots -------------------------------
                     const uint32_t k0 = first_key(key, kNone);
                     if ((k0 >> 24) <= P.tau) {
@@ -462,10 +496,11 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 #pragma unroll
                         for (int t = 0; t < LT; ++t)
                             if (off < len[t]) {
-                                const uint32_t k = scan_step<SMEM_TRAIN>(ids, lo[t] + off, lo[t] + len[t] - 1u, lane, ql,
-                                                                         s_long, J.longs);
+                                uint32_t k = scan_step<SMEM_TRAIN>(ids, lo[t] + off, lo[t] + len[t] - 1u, lane, ql,
+                                                                   s_long, J.longs);
+                                if (GUIDED) k = band_filter(k, line, J.kp, P.band_px);
                                 lmin = min(lmin, k);
-                                lmax = max(lmax, k);
+                                if (k != kNone) lmax = max(lmax, k);
                             }
                     }
                     const uint32_t gmin = __reduce_min_sync(FULL, lmin);
@@ -477,9 +512,11 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 #pragma unroll
                             for (int t = 0; t < LT; ++t) {
                                 key[t] = kNone;
-                                if (off < len[t])
+                                if (off < len[t]) {
                                     key[t] = scan_step<SMEM_TRAIN>(ids, lo[t] + off, lo[t] + len[t] - 1u, lane, ql, s_long,
                                                                    J.longs);
+                                    if (GUIDED) key[t] = band_filter(key[t], line, J.kp, P.band_px);
+                                }
                             }
                             // a round whose smallest key is beyond a full list's last entry changes nothing
                             const uint32_t kth = __shfl_sync(FULL, mykey, P.top_k - 1);

@@ -11,10 +11,15 @@ namespace chgpu {
 // (one CTA per SM at most, never more CTAs than units).  smem = dynamic shared memory bytes.
 cudaError_t launch_match_smem(const MatchParams& P, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid);
 cudaError_t launch_match_global(const MatchParams& P, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid);
+// Epipolar-guided instantiations (match_guided.cu): L == 6 exact, any other L through the LT = 8 generic.
+cudaError_t launch_match_guided(const MatchParams& P, bool smem_train, size_t smem, int sm_count, cudaStream_t stream,
+                                uint32_t* grid);
+// Table slots (LT) the launchers pick for L tables; the staging area is sized with it.
+inline int match_table_slots(uint32_t L, bool guided) { return guided ? (L == 6 ? 6 : 8) : (L <= 4 ? 4 : (L <= 6 ? 6 : 8)); }
 
-template <bool SMEM, int LT, bool EXACT>
+template <bool SMEM, int LT, bool EXACT, bool GUIDED = false>
 cudaError_t launch_match_variant(const MatchParams& P, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid_out) {
-    auto kfn = match_kernel<SMEM, LT, EXACT>;
+    auto kfn = match_kernel<SMEM, LT, EXACT, GUIDED>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;

@@ -267,6 +267,27 @@ static void device_checks(const std::filesystem::path& tmp) {
         CHECK(throws<std::invalid_argument>([&] { ch::match_pair(sets[0], sets[1], codes[0], codes[1], bad); }));
     }
 
+    // guided_match_pair (geometry.hpp:86-89): the epipolar band between lookup and ranking
+    {
+        const ch::FundamentalMatrix F = {0.3, -1.2, 210.0, 0.9, 0.4, -350.0, -0.002, 0.001, 1.0};
+        for (double band : {1e9, 180.0, 12.0}) {
+            const auto got = ch::guided_match_pair(sets[0], sets[1], codes[0], codes[1], F, {}, band);
+            std::vector<ch::MatchRecord> want_rec(sets[0].size() + 1);
+            std::uint32_t count = 0;
+            const chor_family_params p = to_chor(fam.params);
+            const chor_match_cfg c = to_chor(ch::MatchConfig{});
+            CHECK(chor_guided_match_pair(&p, &c, sets[0].descriptors.front().data(), &sets[0].keypoints.front().x,
+                                         std::uint32_t(sets[0].size()), ocodes[0].shorts.data(), ocodes[0].longs.data(),
+                                         sets[1].descriptors.front().data(), &sets[1].keypoints.front().x,
+                                         std::uint32_t(sets[1].size()), ocodes[1].shorts.data(), ocodes[1].longs.data(), F.data(),
+                                         band, reinterpret_cast<chor_match_record*>(want_rec.data()), &count, nullptr, nullptr,
+                                         nullptr) == 0);
+            want_rec.resize(count);
+            CHECK(got == want_rec);
+            if (band > 1e8) CHECK(got == ch::match_pair(sets[0], sets[1], codes[0], codes[1], {}));
+        }
+    }
+
     // batch interface: upload once, centering + hash on the device, whole pair list in one call,
     // files written with the reference's names and bytes
     {

@@ -61,6 +61,7 @@ class Oracle:
             "chor_lookup_candidates": [U32, U32, P, P, U32, P, P],
             "chor_match_pair": [P, P, P, U32, P, P, P, U32, P, P, P, P, P, P, P],
             "chor_brute_force_match": [P, U32, P, U32, D, P, P],
+            "chor_guided_match_pair": [P, P, P, P, U32, P, P, P, P, U32, P, P, P, D, P, P, P, P, P],
             "chor_save_matches": [C.c_char_p, C.c_char_p, P, U32, C.c_char_p],
             "chor_time_match_pairs": [P, P, P, P, P, P, P, U32, U32, P, P],
             "chor_plan_exhaustive": [U32, U32, U32, P, P, P, P],
@@ -176,6 +177,34 @@ class Oracle:
             sj.ctypes.data, lj.ctypes.data, rec.ctypes.data, C.byref(cnt), C.byref(stats),
             C.c_void_p(ranked.ctypes.data if want_ranked else None),
             C.c_void_p(rcount.ctypes.data if want_ranked else None)), "match_pair")
+        out = rec[: cnt.value].copy()
+        if want_ranked:
+            return out, stats.as_dict(), ranked[:ni], rcount[:ni]
+        return out, stats.as_dict()
+
+    def guided_match_pair(self, params, cfg, desc_i, kp_i, shorts_i, longs_i, desc_j, kp_j, shorts_j, longs_j, F, band_px,
+                          want_ranked=False):
+        p, c = self._fp(params), self._cfg(cfg)
+        di = np.ascontiguousarray(desc_i, dtype=np.uint8).reshape(-1, 128)
+        dj = np.ascontiguousarray(desc_j, dtype=np.uint8).reshape(-1, 128)
+        ki = np.ascontiguousarray(kp_i, dtype=np.float32).reshape(-1, 4)
+        kj = np.ascontiguousarray(kp_j, dtype=np.float32).reshape(-1, 4)
+        si = np.ascontiguousarray(shorts_i, dtype=np.uint32)
+        sj = np.ascontiguousarray(shorts_j, dtype=np.uint32)
+        li = np.ascontiguousarray(longs_i, dtype=np.uint64)
+        lj = np.ascontiguousarray(longs_j, dtype=np.uint64)
+        f = np.ascontiguousarray(F, dtype=np.float64).reshape(9)
+        ni, nj = len(di), len(dj)
+        assert len(ki) == ni and len(kj) == nj
+        rec = np.zeros(max(ni, 1), dtype=RECORD_DTYPE)
+        cnt = C.c_uint32(0)
+        stats = PairStatsC()
+        ranked = np.zeros((max(ni, 1), cfg.top_k), dtype=np.uint32)
+        rcount = np.zeros(max(ni, 1), dtype=np.uint32)
+        self._check(self.lib.chor_guided_match_pair(
+            C.byref(p), C.byref(c), di.ctypes.data, ki.ctypes.data, ni, si.ctypes.data, li.ctypes.data,
+            dj.ctypes.data, kj.ctypes.data, nj, sj.ctypes.data, lj.ctypes.data, f.ctypes.data, C.c_double(band_px),
+            rec.ctypes.data, C.byref(cnt), C.byref(stats), ranked.ctypes.data, rcount.ctypes.data), "guided_match_pair")
         out = rec[: cnt.value].copy()
         if want_ranked:
             return out, stats.as_dict(), ranked[:ni], rcount[:ni]

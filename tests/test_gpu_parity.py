@@ -479,3 +479,60 @@ def test_sharded_job_on_device(matcher, oracle, default_family):
     for k, (a, b) in enumerate(pairs):
         want, _ = oracle.match_pair(default_family.params, ch.MatchConfig(), data[a], *codes[a], data[b], *codes[b])
         assert np.array_equal(recs[offsets[k]:offsets[k + 1]], want), (k, a, b)
+
+
+# ---- epipolar-guided variant (guided_match_pair, geometry.cpp:234-250) --------------
+def _keypoints(n, seed, integer=False):
+    rng = np.random.default_rng(seed)
+    x, y = rng.uniform(0, 1000, n), rng.uniform(0, 800, n)
+    if integer:
+        x, y = np.floor(x), np.floor(y)
+    return np.column_stack([x, y, np.full(n, 2.0), np.zeros(n)]).astype(np.float32)
+
+
+@pytest.mark.parametrize("n_i,n_j,params", [(1500, 1500, ch.FamilyParams()), (900, 2100, ch.FamilyParams()),
+                                             (16384, 16384, ch.FamilyParams()), (1200, 1200, ch.FamilyParams(7, 100, 5, 42))])
+def test_guided_match_bit_exact(matcher, oracle, n_i, n_j, params):
+    fam = ch.build_hash_family(params)
+    fresh(matcher, fam)
+    desc = make_dataset(2, max(n_i, n_j), seed=31)
+    d = [desc[0][:n_i], desc[1][:n_j]]
+    kp = [_keypoints(n_i, 1, integer=True), _keypoints(n_j, 2)]
+    for i in range(2):
+        put(matcher, BASE + i, d[i], kp[i])
+    matcher.centering_reset()
+    matcher.centering_add(BASE)
+    matcher.centering_add(BASE + 1)
+    cen = matcher.centering_apply()
+    matcher.hash([BASE, BASE + 1])
+    codes = [oracle_codes(oracle, fam, cen, d[i]) for i in range(2)]
+    rng = np.random.default_rng(5)
+    F = rng.normal(size=(3, 3))
+    F[:, 2] *= 300.0
+    # lines degenerate exactly for the queries with x == 7 (integer query keypoints): those stay unguided
+    F_some_degenerate = np.array([[1.0, 0.0, -7.0], [0.0, 0.0, 0.0], [0.0, 50.0, -20000.0]])
+    cfg = ch.MatchConfig()
+    base, _ = oracle.match_pair(params, cfg, d[0], *codes[0], d[1], *codes[1])
+    cases = [(F, 1e9), (F, 150.0), (F, 25.0), (F, 0.0), (np.zeros((3, 3)), 4.0), (F_some_degenerate, 60.0)]
+    for k, (f, band) in enumerate(cases):
+        want, wstats, wranked, wcount = oracle.guided_match_pair(params, cfg, d[0], kp[0], *codes[0], d[1], kp[1], *codes[1],
+                                                                 f, band, want_ranked=True)
+        offs, rec, stats = matcher.match_pairs_guided([(BASE, BASE + 1)], f[None], band, cfg)
+        assert np.array_equal(rec, want), (k, len(rec), len(want))
+        assert stats["verified_queries"] == wstats["verified_queries"] and stats["distances"] == wstats["distances"]
+        ranked, rc = matcher.ranked_guided(BASE, BASE + 1, f, band, cfg)
+        assert np.array_equal(rc, wcount), k
+        for q in np.flatnonzero(rc):
+            assert np.array_equal(ranked[q, :rc[q]], wranked[q, :rc[q]]), (k, q)
+        if k in (0, 4):  # a band that keeps everything / an all-degenerate F: plain match_pair
+            assert np.array_equal(rec, base)
+    assert len(oracle.guided_match_pair(params, cfg, d[0], kp[0], *codes[0], d[1], kp[1], *codes[1], F, 150.0)[0]) not in (0, len(base))
+    # one call, several pairs with their own F
+    offs, rec, _ = matcher.match_pairs_guided([(BASE, BASE + 1), (BASE + 1, BASE), (BASE, BASE + 1)],
+                                              np.stack([F, F.T, np.zeros((3, 3))]), 150.0, cfg)
+    w0, _ = oracle.guided_match_pair(params, cfg, d[0], kp[0], *codes[0], d[1], kp[1], *codes[1], F, 150.0)
+    w1, _ = oracle.guided_match_pair(params, cfg, d[1], kp[1], *codes[1], d[0], kp[0], *codes[0], F.T, 150.0)
+    assert np.array_equal(rec[offs[0]:offs[1]], w0) and np.array_equal(rec[offs[1]:offs[2]], w1)
+    assert np.array_equal(rec[offs[2]:offs[3]], base)
+    with pytest.raises(ValueError):
+        matcher.match_pairs_guided([(BASE, BASE + 1)], F[None], -1.0, cfg)

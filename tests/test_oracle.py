@@ -325,3 +325,31 @@ def test_plans_equal_reference(restatement, reference):
                 a = reference.plan_exhaustive(k, np_, m)
                 b = restatement.plan_exhaustive(k, np_, m)
                 assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), (k, np_, m)
+
+
+def test_guided_restatement_equals_reference(restatement, reference):
+    """f4: the band filter around the reference's own match_pair_filtered vs the restatement."""
+    import paper_1805_08995_b200 as ch
+    from paper_1805_08995_b200.synth import make_dataset
+    params, cfg = ch.FamilyParams(), ch.MatchConfig()
+    fam = ch.build_hash_family(params)
+    d = make_dataset(2, 1200, seed=9)
+    rng = np.random.default_rng(1)
+    kp = [np.column_stack([np.floor(rng.uniform(0, 1000, 1200)), rng.uniform(0, 800, 1200), np.full(1200, 2.0),
+                           np.zeros(1200)]).astype(np.float32) for _ in range(2)]
+    cen = reference.centering([d[0], d[1]])
+    codes = [reference.compute_codes(params, fam.short_planes, fam.long_planes, cen, d[i]) for i in range(2)]
+    base, _ = reference.match_pair(params, cfg, d[0], *codes[0], d[1], *codes[1])
+    F = rng.normal(size=(3, 3))
+    F[:, 2] *= 300.0
+    some_degenerate = np.array([[1.0, 0.0, -7.0], [0.0, 0.0, 0.0], [0.0, 50.0, -20000.0]])
+    sizes = []
+    for f, band in ((F, 1e9), (F, 150.0), (F, 20.0), (F, 0.0), (np.zeros((3, 3)), 3.0), (some_degenerate, 60.0)):
+        a = reference.guided_match_pair(params, cfg, d[0], kp[0], *codes[0], d[1], kp[1], *codes[1], f, band, want_ranked=True)
+        b = restatement.guided_match_pair(params, cfg, d[0], kp[0], *codes[0], d[1], kp[1], *codes[1], f, band, want_ranked=True)
+        assert np.array_equal(a[0], b[0]) and a[1] == b[1]
+        assert np.array_equal(a[3], b[3])
+        for q in np.flatnonzero(a[3]):
+            assert np.array_equal(a[2][q, :a[3][q]], b[2][q, :b[3][q]])
+        sizes.append(len(a[0]))
+    assert sizes[0] == len(base) == sizes[4] and sizes[3] == 0 and 0 < sizes[1] < sizes[0]
