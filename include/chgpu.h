@@ -140,6 +140,29 @@ chgpu_status chgpu_upload_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n,
  * FeatureFileFault class and byte offset. */
 chgpu_status chgpu_upload_chft(chgpu_ctx* ctx, uint32_t image_id, const void* blob, size_t nbytes,
                                uint32_t* count_out, chgpu_file_fault* fault, uint64_t* fault_offset);
+/* Disk -> pinned host -> HBM streaming loader: the paper's Disk-Memory-GPU exchange and the
+ * reference's loader thread (ResidencyDriver::load_group / load_block, engine.cpp:328-412), rebuilt as
+ * `io_threads` reader threads filling a ring of pinned staging slots while the calling thread validates each
+ * header, issues cudaMemcpyAsync on the copy stream and the AoS->SoA split kernel on the compute stream; reads,
+ * H2D copies and kernels of different files overlap.  Files are consumed in list order.  A file that cannot be
+ * read or parsed is reported in results[i] (reference fault class + byte offset) and skipped, the rest of the
+ * batch proceeds (engine.cpp:315-318).  accumulate_centering != 0 adds every loaded image to the running
+ * centering sums (centering_pass, engine.cpp:545-559) on the fly. */
+typedef struct chgpu_file_result {
+    int32_t status;        /* chgpu_status of this file */
+    int32_t fault;         /* chgpu_file_fault when status == CHGPU_EFORMAT */
+    uint64_t fault_offset;
+    uint32_t count;        /* points loaded */
+    uint32_t reserved;
+} chgpu_file_result;
+typedef struct chgpu_load_stats {
+    uint64_t files_ok, files_failed, bytes_read, points;
+    double read_seconds;   /* summed over the reader threads */
+    double wall_seconds;   /* first read issued -> last split kernel complete */
+} chgpu_load_stats;
+chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, const uint32_t* image_ids, uint32_t count,
+                                   uint32_t io_threads, int accumulate_centering, chgpu_file_result* results,
+                                   chgpu_load_stats* stats /* nullable */);
 chgpu_status chgpu_evict_image(chgpu_ctx* ctx, uint32_t image_id);
 chgpu_status chgpu_image_points(chgpu_ctx* ctx, uint32_t image_id, uint32_t* n);
 chgpu_status chgpu_download_descriptors(chgpu_ctx* ctx, uint32_t image_id, uint8_t* desc, float* keypoints);

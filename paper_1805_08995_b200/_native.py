@@ -43,6 +43,19 @@ class MatchStatsC(C.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+class FileResultC(C.Structure):
+    _fields_ = [("status", C.c_int32), ("fault", C.c_int32), ("fault_offset", C.c_uint64), ("count", C.c_uint32),
+                ("reserved", C.c_uint32)]
+
+
+class LoadStatsC(C.Structure):
+    _fields_ = [("files_ok", C.c_uint64), ("files_failed", C.c_uint64), ("bytes_read", C.c_uint64), ("points", C.c_uint64),
+                ("read_seconds", C.c_double), ("wall_seconds", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
 class DevicePropsC(C.Structure):
     _fields_ = [("name", C.c_char * 64), ("sm_count", C.c_int), ("cc_major", C.c_int), ("cc_minor", C.c_int),
                 ("total_mem", C.c_size_t), ("free_mem", C.c_size_t), ("smem_per_block_optin", C.c_size_t)]
@@ -72,6 +85,8 @@ SIGNATURES = {
     "chgpu_upload_image": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
     "chgpu_upload_chft": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_size_t, u32p,
                                     C.POINTER(C.c_int), u64p]),
+    "chgpu_load_chft_files": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), u32p, C.c_uint32, C.c_uint32, C.c_int,
+                                        C.POINTER(FileResultC), C.POINTER(LoadStatsC)]),
     "chgpu_evict_image": (C.c_int, [C.c_void_p, C.c_uint32]),
     "chgpu_image_points": (C.c_int, [C.c_void_p, C.c_uint32, u32p]),
     "chgpu_download_descriptors": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),

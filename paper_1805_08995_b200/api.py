@@ -337,6 +337,28 @@ class Matcher:
         self._ck(st)
         return cnt.value
 
+    def load_chft_files(self, paths, image_ids, io_threads: int = 8, accumulate_centering: bool = False):
+        """Disk -> pinned ring -> HBM streaming load (chgpu_load_chft_files).  Returns (results, stats): results[i] is
+        the point count of file i, or a FeatureFileError / exception INSTANCE for a file that was skipped."""
+        n = len(paths)
+        arr = (C.c_char_p * max(n, 1))(*[str(p).encode() for p in paths])
+        ids = np.ascontiguousarray(image_ids, dtype=np.uint32)
+        assert len(ids) == n
+        res = (N.FileResultC * max(n, 1))()
+        st = N.LoadStatsC()
+        self._ck(self.lib.chgpu_load_chft_files(self.h, arr, ids.ctypes.data_as(N.u32p), n, io_threads,
+                                                1 if accumulate_centering else 0, res, C.byref(st)))
+        out = []
+        for i in range(n):
+            r = res[i]
+            if r.status == N.OK:
+                out.append(int(r.count))
+            elif r.status == N.EFORMAT:
+                out.append(FeatureFileError(f"{paths[i]}: fault {r.fault} at byte {r.fault_offset}", r.fault, r.fault_offset))
+            else:
+                out.append(RuntimeError(f"{paths[i]}: status {r.status}"))
+        return out, st.as_dict()
+
     def evict(self, image_id: int):
         self._ck(self.lib.chgpu_evict_image(self.h, image_id))
 

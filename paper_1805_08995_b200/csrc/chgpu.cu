@@ -16,12 +16,16 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -960,6 +964,253 @@ chgpu_status chgpu_upload_chft(chgpu_ctx* ctx, uint32_t image_id, const void* bl
         ctx->arena.release(raw, raw_bytes);
     }
     return publish_slot(ctx, slot);
+}
+
+// ---- streaming loader: disk -> pinned ring -> HBM ---------------------------------------------------
+namespace {
+
+struct LoadSlot {
+    enum State { Free, Filling, Ready } state = Free;
+    char* buf = nullptr;   // pinned
+    size_t cap = 0;
+    size_t bytes = 0;      // bytes read
+    bool missing = false;  // fopen failed
+    uint32_t file = 0;     // index of the file it holds (valid in Ready)
+    uint32_t turn = 0;     // index of the file allowed to fill it next
+    cudaEvent_t copied = nullptr;  // H2D of this slot's contents complete
+    bool in_flight = false;        // `copied` recorded, not yet observed
+};
+
+struct LoadRing {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<LoadSlot> slots;
+    std::atomic<uint32_t> next{0};
+    std::atomic<bool> abort{false};
+    double read_seconds = 0.0;
+    uint64_t bytes_read = 0;
+};
+
+// Reader thread: claims file indices in order; file i travels through slot i % S once the slot's previous
+// tenant (file i - S) has been copied to the device.
+void loader_thread(LoadRing* ring, const char* const* paths, uint32_t count) {
+    const size_t S = ring->slots.size();
+    double seconds = 0.0;
+    uint64_t bytes = 0;
+    for (;;) {
+        const uint32_t i = ring->next.fetch_add(1);
+        if (i >= count || ring->abort.load()) break;
+        LoadSlot& s = ring->slots[i % S];
+        {
+            std::unique_lock<std::mutex> lock(ring->mu);
+            // slots are handed out in file order: wait until it is free AND it is this file's turn
+            ring->cv.wait(lock, [&] { return ring->abort.load() || (s.state == LoadSlot::Free && s.turn == i); });
+            if (ring->abort.load()) break;
+            s.state = LoadSlot::Filling;
+        }
+        const auto t0 = std::chrono::steady_clock::now();
+        s.bytes = 0;
+        s.missing = false;
+        FILE* f = std::fopen(paths[i], "rb");
+        if (!f) {
+            s.missing = true;
+        } else {
+            std::fseek(f, 0, SEEK_END);
+            const long sz = std::ftell(f);
+            std::fseek(f, 0, SEEK_SET);
+            const size_t need = sz > 0 ? size_t(sz) : 0;
+            if (need > s.cap) {  // grow this slot's pinned buffer (rare: sized by the largest file seen)
+                if (s.buf) cudaFreeHost(s.buf);
+                s.buf = nullptr;
+                s.cap = 0;
+                const size_t cap = std::max<size_t>(need + need / 8, size_t(2) << 20);
+                if (cudaMallocHost(reinterpret_cast<void**>(&s.buf), cap) == cudaSuccess) s.cap = cap;
+                else cudaGetLastError();
+            }
+            if (need <= s.cap && need) s.bytes = std::fread(s.buf, 1, need, f);
+            std::fclose(f);
+        }
+        seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        bytes += s.bytes;
+        {
+            std::lock_guard<std::mutex> lock(ring->mu);
+            s.file = i;
+            s.state = LoadSlot::Ready;
+        }
+        ring->cv.notify_all();
+    }
+    std::lock_guard<std::mutex> lock(ring->mu);
+    ring->read_seconds += seconds;
+    ring->bytes_read += bytes;
+}
+
+}  // namespace
+
+chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, const uint32_t* image_ids, uint32_t count,
+                                   uint32_t io_threads, int accumulate_centering, chgpu_file_result* results,
+                                   chgpu_load_stats* stats) {
+    if (!ctx || (count && (!paths || !image_ids || !results))) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    if (!ctx->has_family)
+        return fail(ctx, CHGPU_ELOGIC, "chgpu_set_family must precede image uploads (block layout depends on m, L)");
+    chgpu_load_stats st{};
+    if (count == 0) {
+        if (stats) *stats = st;
+        return CHGPU_OK;
+    }
+    io_threads = std::max<uint32_t>(1, std::min<uint32_t>(io_threads ? io_threads : 4, 64));
+    const size_t S = std::max<size_t>(4, 2 * size_t(io_threads));
+    LoadRing ring;
+    ring.slots.resize(S);
+    for (size_t k = 0; k < S; ++k) {
+        ring.slots[k].turn = uint32_t(k);  // slot k serves files k, k + S, k + 2 S, ...
+        if (cudaEventCreateWithFlags(&ring.slots[k].copied, cudaEventDisableTiming) != cudaSuccess)
+            return fail(ctx, CHGPU_ECUDA, "loader: event creation failed");
+    }
+    // device-side raw (AoS) scratch, double buffered; grown to the largest file
+    struct Scratch {
+        char* ptr = nullptr;
+        size_t cap = 0;
+        cudaEvent_t split_done = nullptr;
+        bool used = false;
+    } scratch[2];
+    for (Scratch& sc : scratch) cudaEventCreateWithFlags(&sc.split_done, cudaEventDisableTiming);
+
+    const auto wall0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> readers;
+    for (uint32_t t = 0; t < io_threads; ++t) readers.emplace_back(loader_thread, &ring, paths, count);
+
+    chgpu_status rc = CHGPU_OK;
+    auto poll_copies = [&]() {  // slots whose H2D completed go back to the readers
+        bool freed = false;
+        std::lock_guard<std::mutex> lock(ring.mu);
+        for (LoadSlot& s : ring.slots)
+            if (s.in_flight && cudaEventQuery(s.copied) == cudaSuccess) {
+                s.in_flight = false;
+                s.state = LoadSlot::Free;
+                s.turn = s.file + uint32_t(S);
+                freed = true;
+            }
+        if (freed) ring.cv.notify_all();
+    };
+    for (uint32_t i = 0; i < count && rc == CHGPU_OK; ++i) {
+        LoadSlot& s = ring.slots[i % S];
+        {
+            std::unique_lock<std::mutex> lock(ring.mu);
+            while (!(s.state == LoadSlot::Ready && s.file == i)) {
+                lock.unlock();
+                poll_copies();
+                lock.lock();
+                if (s.state == LoadSlot::Ready && s.file == i) break;
+                ring.cv.wait_for(lock, std::chrono::microseconds(200));
+            }
+        }
+        chgpu_file_result& r = results[i];
+        r = chgpu_file_result{};
+        auto release_slot = [&]() {
+            std::lock_guard<std::mutex> lock(ring.mu);
+            s.state = LoadSlot::Free;
+            s.turn = i + uint32_t(S);
+            ring.cv.notify_all();
+        };
+        auto bad = [&](chgpu_file_fault f, uint64_t off) {
+            r.status = CHGPU_EFORMAT;
+            r.fault = f;
+            r.fault_offset = off;
+            ++st.files_failed;
+            release_slot();
+        };
+        // header checks in the order of load_features (feature_io.cpp:65-85)
+        const unsigned char* b = reinterpret_cast<const unsigned char*>(s.buf);
+        if (s.missing) { bad(CHGPU_FAULT_MISSING_FILE, 0); continue; }
+        if (s.bytes < 16) { bad(CHGPU_FAULT_TRUNCATED, s.bytes); continue; }
+        if (memcmp(b, "CHFT", 4) != 0) { bad(CHGPU_FAULT_BAD_MAGIC, 0); continue; }
+        uint32_t version, n;
+        memcpy(&version, b + 4, 4);
+        memcpy(&n, b + 8, 4);
+        if (version != 1) { bad(CHGPU_FAULT_BAD_VERSION, 4); continue; }
+        const size_t raw_bytes = size_t(n) * 144;
+        if (s.bytes < 16 + raw_bytes) { bad(CHGPU_FAULT_TRUNCATED, s.bytes); continue; }
+
+        uint32_t slot_img;
+        if (const chgpu_status e = alloc_image(ctx, image_ids[i], n, &slot_img)) {
+            r.status = e;
+            ++st.files_failed;
+            release_slot();
+            if (e == CHGPU_ENOMEM || e == CHGPU_ECUDA) rc = e;  // device trouble ends the batch; bad input does not
+            continue;
+        }
+        ImageRec& img = ctx->images[slot_img];
+        if (n) {
+            Scratch& sc = scratch[i & 1];
+            if (sc.used) cudaEventSynchronize(sc.split_done);  // its previous split kernel has consumed it
+            if (sc.cap < raw_bytes) {
+                if (sc.ptr) cudaFree(sc.ptr);
+                sc.ptr = nullptr;
+                sc.cap = 0;
+                const size_t cap = std::max<size_t>(raw_bytes + raw_bytes / 8, size_t(2) << 20);
+                if (cudaMalloc(reinterpret_cast<void**>(&sc.ptr), cap) != cudaSuccess) {
+                    cudaGetLastError();
+                    rc = fail(ctx, CHGPU_ENOMEM, "loader: device staging of %zu bytes", cap);
+                    release_slot();
+                    break;
+                }
+                sc.cap = cap;
+            }
+            cudaMemcpyAsync(sc.ptr, s.buf + 16, raw_bytes, cudaMemcpyHostToDevice, ctx->copy);
+            cudaEventRecord(s.copied, ctx->copy);
+            {
+                std::lock_guard<std::mutex> lock(ring.mu);
+                s.in_flight = true;
+            }
+            cudaStreamWaitEvent(ctx->compute, s.copied, 0);
+            const uint32_t blocks = uint32_t(std::min<uint64_t>((uint64_t(n) * 9 + 255) / 256, 8u * ctx->prop.multiProcessorCount));
+            chft_split_kernel<<<blocks, 256, 0, ctx->compute>>>(reinterpret_cast<const uint4*>(sc.ptr), n,
+                                                               reinterpret_cast<uint4*>(const_cast<uint8_t*>(img.dev.desc)),
+                                                               reinterpret_cast<uint4*>(const_cast<float4*>(img.dev.kp)));
+            cudaEventRecord(sc.split_done, ctx->compute);
+            sc.used = true;
+            if (accumulate_centering) {
+                const uint32_t cb = std::max(1u, std::min((n + 255u) / 256u, 4u * uint32_t(ctx->prop.multiProcessorCount)));
+                centering_sums_kernel<<<cb, 256, 0, ctx->compute>>>(img.dev.desc, n, ctx->d_sums);
+                ctx->sum_count += n;
+            }
+        } else {
+            release_slot();
+        }
+        if (const chgpu_status e = publish_slot(ctx, slot_img)) rc = e;
+        r.status = CHGPU_OK;
+        r.count = n;
+        ++st.files_ok;
+        st.points += n;
+        poll_copies();
+    }
+    // drain
+    if (rc != CHGPU_OK) ring.abort.store(true);
+    cudaStreamSynchronize(ctx->copy);
+    cudaStreamSynchronize(ctx->compute);
+    poll_copies();
+    {
+        std::lock_guard<std::mutex> lock(ring.mu);
+        ring.abort.store(true);
+    }
+    ring.cv.notify_all();
+    for (std::thread& t : readers) t.join();
+    const cudaError_t last = cudaGetLastError();
+    for (LoadSlot& s : ring.slots) {
+        if (s.buf) cudaFreeHost(s.buf);
+        cudaEventDestroy(s.copied);
+    }
+    for (Scratch& sc : scratch) {
+        if (sc.ptr) cudaFree(sc.ptr);
+        cudaEventDestroy(sc.split_done);
+    }
+    st.bytes_read = ring.bytes_read;
+    st.read_seconds = ring.read_seconds;
+    st.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    if (stats) *stats = st;
+    if (rc == CHGPU_OK && last != cudaSuccess) return fail(ctx, CHGPU_ECUDA, "loader: %s", cudaGetErrorString(last));
+    return rc;
 }
 
 chgpu_status chgpu_evict_image(chgpu_ctx* ctx, uint32_t image_id) {
