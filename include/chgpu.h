@@ -261,6 +261,29 @@ chgpu_status chgpu_save_matches(const char* image_id_i, const char* image_id_j,
 /* pair_file_name (engine.cpp:724-728): "match_%06u_%06u.txt"; buf must hold 48 bytes. */
 void chgpu_pair_file_name(uint32_t image_i, uint32_t image_j, char* buf);
 
+/* Asynchronous batched match-file writer: the reference's FileMatchSink (engine.cpp:145-211: one writer thread,
+ * one text file per pair) with `threads` writers and whole sub-batches as queue items.  Every pair (i, j) becomes
+ * <dir>/match_%06u_%06u.txt with exactly the bytes save_matches writes (feature_io.cpp:161-183); the header line
+ * carries image_names[i] / image_names[j] (NULL: the decimal image index).  accept() copies its arguments and
+ * returns at once (it blocks only while max_queued_batches items are waiting); per-file failures are counted,
+ * never fatal (engine.cpp:188-199).  close() drains the queue, joins the writers and frees the sink. */
+typedef struct chgpu_sink chgpu_sink;
+typedef struct chgpu_sink_stats {
+    uint64_t files_written, files_failed, records, bytes;
+    double busy_seconds;  /* summed over the writer threads */
+    double wall_seconds;  /* open -> close */
+} chgpu_sink_stats;
+chgpu_status chgpu_sink_open(const char* dir, const char* const* image_names, uint32_t image_count, uint32_t threads,
+                             uint32_t max_queued_batches, chgpu_sink** out);
+chgpu_status chgpu_sink_accept(chgpu_sink* sink, const uint32_t* pairs /* 2 per pair */, uint32_t npairs,
+                               const uint64_t* offsets /* npairs + 1, relative to records */,
+                               const chgpu_match_record* records);
+chgpu_status chgpu_sink_close(chgpu_sink* sink, chgpu_sink_stats* stats /* nullable */);
+/* chgpu_match_pairs_stream with the writer above as its sink: match results go straight from the pinned result
+ * buffers into the writer queue while the next sub-batch computes. */
+chgpu_status chgpu_match_pairs_to_files(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs, const chgpu_match_cfg* cfg,
+                                        chgpu_sink* sink, chgpu_match_stats* stats /* nullable */);
+
 /* ---- pair lists ------------------------------------------------------------------------ */
 /* Exhaustive pair list in the reference's locality order (plan_exhaustive, scheduler.cpp:99-142)
  * for image_count images in blocks of block_images, blocks_per_group blocks per group.

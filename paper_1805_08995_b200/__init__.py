@@ -9,6 +9,6 @@ from .api import (  # noqa: F401
     Matcher, RECORD_DTYPE, UnsupportedError, build_hash_family, compute_codes, match_pair, pair_file_name,
     plan_exhaustive, save_matches, set_centering, shard_range,
     CacheMismatchError, centering_fingerprint, load_centering_file, load_code_cache, read_code_cache_header,
-    save_centering_file, save_code_cache,
+    save_centering_file, save_code_cache, MatchFileSink,
 )
 from .synth import make_dataset  # noqa: F401

@@ -56,6 +56,14 @@ class LoadStatsC(C.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+class SinkStatsC(C.Structure):
+    _fields_ = [("files_written", C.c_uint64), ("files_failed", C.c_uint64), ("records", C.c_uint64), ("bytes", C.c_uint64),
+                ("busy_seconds", C.c_double), ("wall_seconds", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
 class DevicePropsC(C.Structure):
     _fields_ = [("name", C.c_char * 64), ("sm_count", C.c_int), ("cc_major", C.c_int), ("cc_minor", C.c_int),
                 ("total_mem", C.c_size_t), ("free_mem", C.c_size_t), ("smem_per_block_optin", C.c_size_t)]
@@ -118,6 +126,11 @@ SIGNATURES = {
     "chgpu_debug_ranked": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(MatchCfgC), C.c_void_p,
                                      C.c_void_p]),
     "chgpu_save_matches": (C.c_int, [C.c_char_p, C.c_char_p, C.c_void_p, C.c_uint32, C.c_char_p]),
+    "chgpu_sink_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_char_p), C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "chgpu_sink_accept": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "chgpu_sink_close": (C.c_int, [C.c_void_p, C.POINTER(SinkStatsC)]),
+    "chgpu_match_pairs_to_files": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(MatchCfgC), C.c_void_p,
+                                             C.POINTER(MatchStatsC)]),
     "chgpu_pair_file_name": (None, [C.c_uint32, C.c_uint32, C.c_char_p]),
     "chgpu_plan_exhaustive": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p, u64p]),
     "chgpu_shard_range": (None, [C.c_uint64, C.c_uint32, C.c_uint32, u64p, u64p]),

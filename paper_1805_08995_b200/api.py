@@ -201,6 +201,39 @@ def pair_file_name(i: int, j: int) -> str:
     return buf.value.decode()
 
 
+class MatchFileSink:
+    """Asynchronous batched writer of match files (chgpu_sink_*): FileMatchSink, engine.cpp:145-211."""
+
+    def __init__(self, directory, image_names=None, threads: int = 4, max_queued_batches: int = 8):
+        self.lib = N.load()
+        names = None
+        n = 0
+        if image_names is not None:
+            n = len(image_names)
+            names = (C.c_char_p * max(n, 1))(*[str(s).encode() for s in image_names])
+        h = C.c_void_p()
+        st = self.lib.chgpu_sink_open(str(directory).encode(), names, n, threads, max_queued_batches, C.byref(h))
+        if st != N.OK:
+            _raise(st, "chgpu_sink_open failed")
+        self.h = h
+
+    def accept(self, pairs, offsets, records):
+        pr = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
+        offs = np.ascontiguousarray(offsets, dtype=np.uint64)
+        rec = np.ascontiguousarray(records, dtype=RECORD_DTYPE)
+        assert len(offs) == len(pr) + 1
+        st = self.lib.chgpu_sink_accept(self.h, pr.ctypes.data, len(pr), offs.ctypes.data, rec.ctypes.data if len(rec) else None)
+        if st != N.OK:
+            _raise(st, "chgpu_sink_accept failed")
+
+    def close(self) -> dict:
+        stats = N.SinkStatsC()
+        h, self.h = self.h, None
+        if h is not None:
+            self.lib.chgpu_sink_close(h, C.byref(stats))
+        return stats.as_dict()
+
+
 def plan_exhaustive(image_count: int, block_images: int, blocks_per_group: int) -> np.ndarray:
     """Pair list of plan_exhaustive (scheduler.hpp:53), flattened in task order: (npairs, 2) u32."""
     lib = N.load()
@@ -483,6 +516,13 @@ class Matcher:
                                                    offsets.ctypes.data, records.ctypes.data, capacity, C.byref(total),
                                                    C.byref(stats)))
         return offsets, records[: total.value], stats.as_dict()
+
+    def match_pairs_to_files(self, pairs, sink: "MatchFileSink", cfg: MatchConfig = MatchConfig()) -> dict:
+        pr = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
+        c = cfg.c()
+        stats = N.MatchStatsC()
+        self._ck(self.lib.chgpu_match_pairs_to_files(self.h, pr.ctypes.data, len(pr), C.byref(c), sink.h, C.byref(stats)))
+        return stats.as_dict()
 
     def ranked_guided(self, image_i: int, image_j: int, fmat, band_px: float, cfg: MatchConfig = MatchConfig()):
         n = self.points(image_i)

@@ -1446,6 +1446,23 @@ chgpu_status chgpu_match_pairs_guided_stream(chgpu_ctx* ctx, const uint32_t* pai
     return run_match(ctx, run, stats);
 }
 
+chgpu_status chgpu_match_pairs_to_files(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs, const chgpu_match_cfg* cfg,
+                                        chgpu_sink* sink, chgpu_match_stats* stats) {
+    if (!ctx || !cfg || !sink || (npairs && !pairs)) return CHGPU_EINVAL;
+    struct Feed {
+        chgpu_sink* sink;
+        const uint32_t* pairs;
+    } feed{sink, pairs};
+    auto to_writer = [](void* user, uint32_t first, uint32_t count, const uint64_t* offs, const chgpu_match_record* rec) -> int {
+        Feed* f = static_cast<Feed*>(user);
+        return chgpu_sink_accept(f->sink, f->pairs + 2 * size_t(first), count, offs, rec) == CHGPU_OK ? 0 : 1;
+    };
+    MatchRun run{pairs, npairs, *cfg, SinkMode::Stream};
+    run.sink = to_writer;
+    run.user = &feed;
+    return run_match(ctx, run, stats);
+}
+
 chgpu_status chgpu_match_pairs_device(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
                                       const chgpu_match_cfg* cfg, chgpu_match_stats* stats) {
     if (!ctx || !cfg || (npairs && !pairs)) return CHGPU_EINVAL;

@@ -5,7 +5,14 @@
 #include "../../include/chgpu.h"
 
 #include <algorithm>
+#include <atomic>
 #include <charconv>
+#include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -39,9 +46,162 @@ void fill_plane(uint64_t seed, uint64_t stream, uint64_t index, double* dst) {
     }
 }
 
+// Text of one match file (save_matches, feature_io.cpp:161-183): "# idI idJ count" then "q t dist" lines,
+// dist as the shortest decimal that round-trips (std::to_chars; integers print without a point).
+void format_matches(const char* id_i, const char* id_j, const chgpu_match_record* records, uint32_t count, std::string& out) {
+    out.clear();
+    out.reserve(64 + size_t(count) * 24);
+    out.append("# ").append(id_i).append(" ").append(id_j).append(" ");
+    char buf[64];
+    auto put_u = [&](unsigned long long v) {
+        const auto r = std::to_chars(buf, buf + sizeof(buf), v);
+        out.append(buf, r.ptr);
+    };
+    put_u(count);
+    out.push_back('\n');
+    for (uint32_t i = 0; i < count; ++i) {
+        put_u(records[i].query_index);
+        out.push_back(' ');
+        put_u(records[i].train_index);
+        out.push_back(' ');
+        const auto r = std::to_chars(buf, buf + sizeof(buf), records[i].distance_sq);
+        out.append(buf, r.ptr);
+        out.push_back('\n');
+    }
+}
+
+bool write_whole_file(const char* path, const std::string& bytes) {
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return false;
+    const size_t w = std::fwrite(bytes.data(), 1, bytes.size(), f);
+    const int c = std::fclose(f);
+    return w == bytes.size() && c == 0;
+}
+
 }  // namespace
 
+// ---- asynchronous match-file writer ---------------------------------------------------------------
+struct chgpu_sink {
+    struct Batch {
+        std::vector<uint32_t> pairs;
+        std::vector<uint64_t> offsets;
+        std::vector<chgpu_match_record> records;
+    };
+    std::string dir;
+    std::vector<std::string> names;
+    std::mutex mu;
+    std::condition_variable cv_work, cv_room;
+    std::deque<std::unique_ptr<Batch>> queue;
+    size_t max_queued = 8;
+    bool closing = false;
+    std::vector<std::thread> workers;
+    uint64_t files_written = 0, files_failed = 0, records = 0, bytes = 0;
+    double busy_seconds = 0.0;
+    std::chrono::steady_clock::time_point opened;
+
+    void run() {
+        std::string text, path, a, b;
+        uint64_t ok = 0, failed = 0, nrec = 0, nbytes = 0;
+        double busy = 0.0;
+        for (;;) {
+            std::unique_ptr<Batch> item;
+            {
+                std::unique_lock<std::mutex> lock(mu);
+                cv_work.wait(lock, [&] { return closing || !queue.empty(); });
+                if (queue.empty()) break;
+                item = std::move(queue.front());
+                queue.pop_front();
+            }
+            cv_room.notify_one();
+            const auto t0 = std::chrono::steady_clock::now();
+            const uint32_t n = uint32_t(item->pairs.size() / 2);
+            for (uint32_t k = 0; k < n; ++k) {
+                const uint32_t i = item->pairs[2 * k], j = item->pairs[2 * k + 1];
+                const char* id_i = i < names.size() ? names[i].c_str() : (a = std::to_string(i)).c_str();
+                const char* id_j = j < names.size() ? names[j].c_str() : (b = std::to_string(j)).c_str();
+                const uint32_t count = uint32_t(item->offsets[k + 1] - item->offsets[k]);
+                format_matches(id_i, id_j, item->records.data() + item->offsets[k], count, text);
+                char name[48];
+                chgpu_pair_file_name(i, j, name);
+                path.assign(dir).append("/").append(name);
+                if (write_whole_file(path.c_str(), text)) {
+                    ++ok;
+                    nrec += count;
+                    nbytes += text.size();
+                } else {
+                    ++failed;
+                }
+            }
+            busy += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+        std::lock_guard<std::mutex> lock(mu);
+        files_written += ok;
+        files_failed += failed;
+        records += nrec;
+        bytes += nbytes;
+        busy_seconds += busy;
+    }
+};
+
 extern "C" {
+
+chgpu_status chgpu_sink_open(const char* dir, const char* const* image_names, uint32_t image_count, uint32_t threads,
+                             uint32_t max_queued_batches, chgpu_sink** out) {
+    if (!dir || !out) return CHGPU_EINVAL;
+    *out = nullptr;
+    auto sink = std::make_unique<chgpu_sink>();
+    sink->dir = dir;
+    if (image_names)
+        for (uint32_t i = 0; i < image_count; ++i) sink->names.emplace_back(image_names[i] ? image_names[i] : "");
+    sink->max_queued = std::max<uint32_t>(1, max_queued_batches ? max_queued_batches : 8);
+    sink->opened = std::chrono::steady_clock::now();
+    threads = std::max<uint32_t>(1, std::min<uint32_t>(threads ? threads : 4, 256));
+    chgpu_sink* raw = sink.release();
+    for (uint32_t t = 0; t < threads; ++t) raw->workers.emplace_back([raw] { raw->run(); });
+    *out = raw;
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_sink_accept(chgpu_sink* sink, const uint32_t* pairs, uint32_t npairs, const uint64_t* offsets,
+                               const chgpu_match_record* records) {
+    if (!sink || (npairs && (!pairs || !offsets))) return CHGPU_EINVAL;
+    if (npairs == 0) return CHGPU_OK;
+    auto item = std::make_unique<chgpu_sink::Batch>();
+    item->pairs.assign(pairs, pairs + 2 * size_t(npairs));
+    item->offsets.resize(size_t(npairs) + 1);
+    for (uint32_t k = 0; k <= npairs; ++k) item->offsets[k] = offsets[k] - offsets[0];
+    const uint64_t total = offsets[npairs] - offsets[0];
+    if (total && !records) return CHGPU_EINVAL;
+    item->records.assign(records + offsets[0], records + offsets[0] + total);
+    {
+        std::unique_lock<std::mutex> lock(sink->mu);
+        if (sink->closing) return CHGPU_ELOGIC;
+        sink->cv_room.wait(lock, [&] { return sink->queue.size() < sink->max_queued; });
+        sink->queue.push_back(std::move(item));
+    }
+    sink->cv_work.notify_one();
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_sink_close(chgpu_sink* sink, chgpu_sink_stats* stats) {
+    if (!sink) return CHGPU_EINVAL;
+    {
+        std::lock_guard<std::mutex> lock(sink->mu);
+        sink->closing = true;
+    }
+    sink->cv_work.notify_all();
+    for (std::thread& t : sink->workers) t.join();
+    if (stats) {
+        stats->files_written = sink->files_written;
+        stats->files_failed = sink->files_failed;
+        stats->records = sink->records;
+        stats->bytes = sink->bytes;
+        stats->busy_seconds = sink->busy_seconds;
+        stats->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - sink->opened).count();
+    }
+    delete sink;
+    return CHGPU_OK;
+}
 
 int chgpu_host_check_family(const chgpu_family_params* p) {
     // validate(FamilyParams), hashing.cpp:30-36
@@ -66,30 +226,8 @@ chgpu_status chgpu_save_matches(const char* image_id_i, const char* image_id_j,
                                 const chgpu_match_record* records, uint32_t count, const char* path) {
     if (!image_id_i || !image_id_j || !path || (count && !records)) return CHGPU_EINVAL;
     std::string out;
-    out.reserve(64 + size_t(count) * 24);
-    out.append("# ").append(image_id_i).append(" ").append(image_id_j).append(" ");
-    char buf[64];
-    auto put_u = [&](unsigned long long v) {
-        const auto r = std::to_chars(buf, buf + sizeof(buf), v);
-        out.append(buf, r.ptr);
-    };
-    put_u(count);
-    out.push_back('\n');
-    for (uint32_t i = 0; i < count; ++i) {
-        put_u(records[i].query_index);
-        out.push_back(' ');
-        put_u(records[i].train_index);
-        out.push_back(' ');
-        // shortest decimal that round-trips (feature_io.cpp:48-52); integers print without a point
-        const auto r = std::to_chars(buf, buf + sizeof(buf), records[i].distance_sq);
-        out.append(buf, r.ptr);
-        out.push_back('\n');
-    }
-    FILE* f = std::fopen(path, "wb");
-    if (!f) return CHGPU_EFORMAT;  // FeatureFileFault::Unwritable
-    const size_t w = std::fwrite(out.data(), 1, out.size(), f);
-    const int c = std::fclose(f);
-    return (w == out.size() && c == 0) ? CHGPU_OK : CHGPU_EFORMAT;
+    format_matches(image_id_i, image_id_j, records, count, out);
+    return write_whole_file(path, out) ? CHGPU_OK : CHGPU_EFORMAT;  // FeatureFileFault::Unwritable
 }
 
 void chgpu_pair_file_name(uint32_t image_i, uint32_t image_j, char* buf) {
