@@ -363,6 +363,17 @@ def run_ours(args):
                 "so frac may exceed 1; see DESIGN.md for the on-chip (POPC / LDS) bounds",
     }
 
+    # on-chip bound of the same kernel: POPC is the one quarter-rate instruction the scan cannot avoid
+    # (4 per raw candidate, 16 lanes/clk/SM on the XU pipe); DESIGN.md section 4
+    props = m.device_props()
+    sm_mhz = clocks.get("sm_mhz") or 1965.0
+    popc_peak = props["sm_count"] * 16 * sm_mhz * 1e6
+    popc_rate = 4.0 * last["raw_candidates"] / (kern_ms_per_step * 1e-3)
+    roofline["on_chip"] = {"bound": "xu_popc", "achieved_gpopc_s": popc_rate / 1e9, "peak_gpopc_s": popc_peak / 1e9,
+                           "frac": popc_rate / popc_peak,
+                           "note": "lower bound on POPC work (padding lanes not counted); ncu pipe utilisations of the "
+                                   "committed capture: profiles/r01h_match_kernel_ncu_full.json"}
+
     # ---- e2e: host buffers in, host records out, every step ------------------------------------------
     e2e = None
     if not args.no_e2e:
