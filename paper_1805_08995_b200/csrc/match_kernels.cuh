@@ -63,7 +63,12 @@ __device__ __forceinline__ void static_for(F&& f) {
 #ifndef CHGPU_OVER_SLOTS
 #define CHGPU_OVER_SLOTS 3
 #endif
+#ifndef CHGPU_VERIFY_LANES
+#define CHGPU_VERIFY_LANES 4
+#endif
 constexpr int kMatchThreads = CHGPU_MATCH_THREADS;
+constexpr uint32_t kVerifyLanes = CHGPU_VERIFY_LANES;  // lanes per descriptor row in the verification (2, 4 or 8)
+static_assert(kVerifyLanes == 2 || kVerifyLanes == 4 || kVerifyLanes == 8, "lanes per row");
 // bucket lists in the bank-friendly scan order (default) or, for A/B measurements, the canonical one
 #ifdef CHGPU_SCAN_CANONICAL
 #define CH_IDS(img) (img).points
@@ -546,23 +551,28 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                 if (n >= 2) {
                     st_vq += 1;
                     st_dist += n;
-                    // two lanes per candidate row (64 bytes each), 16 candidates per round
-                    const uint32_t half = lane & 1u, cand = lane >> 1;
-                    const uint4* __restrict__ qrow = reinterpret_cast<const uint4*>(I.desc + uint64_t(q) * kDim) + half * 4u;
+                    // kVerifyLanes lanes per candidate row (128 / kVerifyLanes bytes each), 32 / kVerifyLanes rows per round
+                    constexpr uint32_t VL = kVerifyLanes, ROWS = 32u / VL, PIECES = 8u / VL;
+                    const uint32_t part = lane % VL, cand = lane / VL;
+                    const uint4* __restrict__ qrow = reinterpret_cast<const uint4*>(I.desc + uint64_t(q) * kDim) + part * PIECES;
+                    uint4 qa[PIECES];
+#pragma unroll
+                    for (uint32_t w = 0; w < PIECES; ++w) qa[w] = __ldg(qrow + w);
                     uint32_t mydist = kNone;
-                    for (uint32_t j0 = 0; j0 < n; j0 += 16) {
+                    for (uint32_t j0 = 0; j0 < n; j0 += ROWS) {
                         const uint32_t jj = min(j0 + cand, n - 1);
                         const uint32_t cid = __shfl_sync(FULL, mykey, jj) & 0xffffffu;
-                        const uint4* __restrict__ trow = reinterpret_cast<const uint4*>(J.desc + uint64_t(cid) * kDim) + half * 4u;
+                        const uint4* __restrict__ trow = reinterpret_cast<const uint4*>(J.desc + uint64_t(cid) * kDim) + part * PIECES;
                         uint32_t s = 0;
-#pragma unroll 2
-                        for (int w = 0; w < 4; ++w) {
-                            const uint4 qa = __ldg(qrow + w), ta = __ldg(trow + w);
-                            s += sqdiff4(qa.x, ta.x) + sqdiff4(qa.y, ta.y) + sqdiff4(qa.z, ta.z) + sqdiff4(qa.w, ta.w);
+#pragma unroll
+                        for (uint32_t w = 0; w < PIECES; ++w) {
+                            const uint4 ta = __ldg(trow + w);
+                            s += sqdiff4(qa[w].x, ta.x) + sqdiff4(qa[w].y, ta.y) + sqdiff4(qa[w].z, ta.z) + sqdiff4(qa[w].w, ta.w);
                         }
-                        s += __shfl_xor_sync(FULL, s, 1);
-                        const uint32_t v = __shfl_sync(FULL, s, ((lane - j0) & 15u) * 2u);
-                        if (lane >= j0 && lane < j0 + 16 && lane < n) mydist = v;
+#pragma unroll
+                        for (uint32_t d = 1; d < VL; d <<= 1) s += __shfl_xor_sync(FULL, s, d);
+                        const uint32_t v = __shfl_sync(FULL, s, ((lane - j0) % ROWS) * VL);
+                        if (lane >= j0 && lane < j0 + ROWS && lane < n) mydist = v;
                     }
                     // best = smallest d^2, ties to the earlier rank (strict '<' in the reference loop)
                     const uint32_t packed = lane < n ? ((mydist << 8) | lane) : kNone;
