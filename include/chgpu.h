@@ -171,6 +171,24 @@ chgpu_status chgpu_download_descriptors(chgpu_ctx* ctx, uint32_t image_id, uint8
 /* Replaces compute_codes (hashing.hpp:131, hashing.cpp:130-149) + build_bucket_index
  * (matcher.hpp:43, matcher.cpp:27-51) for the listed images.  reduce_rounds = N_r in 0..7. */
 chgpu_status chgpu_hash_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32_t count, int reduce_rounds);
+/* How chgpu_hash_images evaluates the L*m + n hyperplane signs of a descriptor.  Both modes give the reference's
+ * bits exactly (compute_codes, hashing.cpp:130-149).
+ *   FILTERED (default): an fp32 contraction with an a-priori error bound decides every sign it can prove; the dots
+ *                       it cannot (|value| below the bound, ~1e-4 of them, ties included) are re-evaluated in the
+ *                       reference's fp64 operation order (reduce_dot, hashing.hpp:24-43).  Falls back to EXACT by
+ *                       itself for planes / centerings outside the bound's premises (non-finite or huge values).
+ *   EXACT:              every dot in the reference's fp64 operation order.
+ * The environment variable CHGPU_HASH_EXACT=1 selects EXACT for new contexts. */
+typedef enum chgpu_hash_mode { CHGPU_HASH_FILTERED = 0, CHGPU_HASH_EXACT = 1 } chgpu_hash_mode;
+typedef struct chgpu_hash_stats {
+    uint64_t undecided_dots;      /* dots the filter handed to the exact path (cumulative per context) */
+    uint64_t flipped_bits;        /* of those, bits whose fp32 sign differed from the reference's */
+    uint64_t overflowed_batches;  /* launches whose undecided queue overflowed and were recomputed in EXACT mode */
+    int32_t filter_active;        /* 1 if the next chgpu_hash_images call will use the filter */
+    int32_t reserved;
+} chgpu_hash_stats;
+chgpu_status chgpu_set_hash_mode(chgpu_ctx* ctx, chgpu_hash_mode mode);
+chgpu_status chgpu_get_hash_stats(chgpu_ctx* ctx, chgpu_hash_stats* out);
 /* shorts: n x L u32 [point*L+table]; longs: n x 2 u64 (ShortCodes / LongCode, hashing.hpp:80-96). */
 chgpu_status chgpu_download_codes(chgpu_ctx* ctx, uint32_t image_id, uint32_t* shorts, uint64_t* longs);
 /* Installs externally computed codes (e.g. a CHCC code cache, hashing.hpp:138-162) and builds buckets. */

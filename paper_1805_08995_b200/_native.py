@@ -64,6 +64,14 @@ class SinkStatsC(C.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+class HashStatsC(C.Structure):
+    _fields_ = [("undecided_dots", C.c_uint64), ("flipped_bits", C.c_uint64), ("overflowed_batches", C.c_uint64),
+                ("filter_active", C.c_int32), ("reserved", C.c_int32)]
+
+    def as_dict(self) -> dict:
+        return {n: getattr(self, n) for n, _ in self._fields_ if n != "reserved"}
+
+
 class DevicePropsC(C.Structure):
     _fields_ = [("name", C.c_char * 64), ("sm_count", C.c_int), ("cc_major", C.c_int), ("cc_minor", C.c_int),
                 ("total_mem", C.c_size_t), ("free_mem", C.c_size_t), ("smem_per_block_optin", C.c_size_t)]
@@ -98,6 +106,8 @@ SIGNATURES = {
     "chgpu_evict_image": (C.c_int, [C.c_void_p, C.c_uint32]),
     "chgpu_image_points": (C.c_int, [C.c_void_p, C.c_uint32, u32p]),
     "chgpu_download_descriptors": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "chgpu_set_hash_mode": (C.c_int, [C.c_void_p, C.c_int]),
+    "chgpu_get_hash_stats": (C.c_int, [C.c_void_p, C.POINTER(HashStatsC)]),
     "chgpu_hash_images": (C.c_int, [C.c_void_p, u32p, C.c_uint32, C.c_int]),
     "chgpu_download_codes": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
     "chgpu_upload_codes": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),

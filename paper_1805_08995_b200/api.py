@@ -412,6 +412,15 @@ class Matcher:
         ids = np.ascontiguousarray(image_ids, dtype=np.uint32)
         self._ck(self.lib.chgpu_hash_images(self.h, ids.ctypes.data_as(N.u32p), len(ids), reduce_rounds))
 
+    def set_hash_mode(self, exact: bool):
+        """False: fp32 filter + exact fp64 fixup (default); True: every dot in the reference's fp64 order."""
+        self._ck(self.lib.chgpu_set_hash_mode(self.h, 1 if exact else 0))
+
+    def hash_stats(self) -> dict:
+        st = N.HashStatsC()
+        self._ck(self.lib.chgpu_get_hash_stats(self.h, C.byref(st)))
+        return st.as_dict()
+
     def codes(self, image_id: int) -> ImageCodes:
         n = self.points(image_id)
         shorts = np.empty((n, self.params.table_count), dtype=np.uint32)

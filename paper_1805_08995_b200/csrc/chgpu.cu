@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
@@ -45,6 +46,8 @@ constexpr size_t kAlign = 256;
 constexpr size_t kSlabBytes = size_t(256) << 20;
 constexpr size_t kStageBytes = size_t(32) << 20;
 constexpr int kStageSlots = 2;
+constexpr uint32_t kHashQueueCap = 1u << 21;    // undecided dots per hash launch (16 MiB); ~110 per 8K-point image are expected
+constexpr uint32_t kHashBatchImages = 2048;     // images per hash launch
 constexpr uint64_t kSubBatchQueries = uint64_t(16) << 20;  // per sub-batch: sum of Nq (res 128 MiB, records <= 256 MiB)
 
 size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a; }
@@ -147,6 +150,18 @@ struct chgpu_ctx {
     double* d_planes = nullptr;
     double* d_centering = nullptr;
     double h_centering[128] = {0};  // host copy (code-cache fingerprints)
+    // fp32-filtered hash path (K1f, hash_kernels.cuh): constants derived from planes + centering
+    std::vector<double> h_planes;   // host copy of the installed planes, (L*m + n) x 128
+    float* d_planes_t = nullptr;    // [128][gpad] fp32-rounded, component-major
+    double* d_bias = nullptr;       // [gpad]
+    double* d_hnorm = nullptr;      // [gpad]
+    uint32_t gpad = 0;
+    double filt_a_rel = 0.0, filt_a_abs = 0.0;
+    bool filter_ready = false;      // constants valid for the current planes + centering
+    int hash_mode = 0;              // chgpu_hash_mode
+    uint2* d_hq = nullptr;          // queue of undecided dots
+    unsigned int* d_hq_count = nullptr;
+    HashFilterStats* d_hstats = nullptr;
     unsigned long long* d_sums = nullptr;
     uint64_t sum_count = 0;
     uint64_t extra_sums[128] = {0};  // sums merged from other ranks
@@ -358,14 +373,106 @@ chgpu_status launch_bucket_build(chgpu_ctx* ctx, uint32_t count) {
 }
 
 template <int RR>
-cudaError_t launch_hash_rr(chgpu_ctx* ctx, dim3 grid) {
+cudaError_t launch_hash_rr(chgpu_ctx* ctx, dim3 grid, const uint32_t* slots, bool guarded) {
     const size_t smem = hash_smem_bytes();
     cudaError_t e = cudaFuncSetAttribute(hash_codes_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     hash_codes_kernel<RR><<<grid, kHashThreads, smem, ctx->compute>>>(
-        ctx->d_images, ctx->d_slots, ctx->d_planes, ctx->d_centering, ctx->fam.short_bits, ctx->fam.table_count,
-        ctx->fam.long_bits);
+        ctx->d_images, slots, ctx->d_planes, ctx->d_centering, ctx->fam.short_bits, ctx->fam.table_count,
+        ctx->fam.long_bits, guarded ? ctx->d_hq_count : nullptr, kHashQueueCap);
     return cudaGetLastError();
+}
+
+cudaError_t launch_hash_exact(chgpu_ctx* ctx, dim3 grid, const uint32_t* slots, int reduce_rounds, bool guarded) {
+    switch (reduce_rounds) {
+        case 0: return launch_hash_rr<0>(ctx, grid, slots, guarded);
+        case 1: return launch_hash_rr<1>(ctx, grid, slots, guarded);
+        case 2: return launch_hash_rr<2>(ctx, grid, slots, guarded);
+        case 3: return launch_hash_rr<3>(ctx, grid, slots, guarded);
+        case 4: return launch_hash_rr<4>(ctx, grid, slots, guarded);
+        case 5: return launch_hash_rr<5>(ctx, grid, slots, guarded);
+        case 6: return launch_hash_rr<6>(ctx, grid, slots, guarded);
+        default: return launch_hash_rr<7>(ctx, grid, slots, guarded);
+    }
+}
+
+// K1f + fixup + guarded exact kernel for `count` images whose slots start at `slots` (device).
+cudaError_t launch_hash_filtered(chgpu_ctx* ctx, const uint32_t* slots, uint32_t count, uint32_t max_n, int reduce_rounds) {
+    cudaError_t e = cudaMemsetAsync(ctx->d_hq_count, 0, sizeof(unsigned int), ctx->compute);
+    if (e != cudaSuccess) return e;
+    HashFilterParams P{};
+    P.images = ctx->d_images;
+    P.slots = slots;
+    P.planes_t = ctx->d_planes_t;
+    P.bias = ctx->d_bias;
+    P.hnorm = ctx->d_hnorm;
+    P.a_rel = ctx->filt_a_rel;
+    P.a_abs = ctx->filt_a_abs;
+    P.gpad = ctx->gpad;
+    P.m = ctx->fam.short_bits;
+    P.L = ctx->fam.table_count;
+    P.nlong = ctx->fam.long_bits;
+    P.queue = ctx->d_hq;
+    P.queue_cap = kHashQueueCap;
+    P.queue_count = ctx->d_hq_count;
+    const size_t smem = hash_filter_smem_bytes();
+    e = cudaFuncSetAttribute(hash_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    const dim3 grid((max_n + kFiltPoints - 1) / kFiltPoints, count);
+    hash_filter_kernel<<<grid, kFiltThreads, smem, ctx->compute>>>(P);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    hash_fixup_kernel<<<ctx->prop.multiProcessorCount * 4, 128, 0, ctx->compute>>>(
+        ctx->d_images, ctx->d_planes, ctx->d_centering, ctx->d_hq, kHashQueueCap, ctx->d_hq_count, P.m, P.L,
+        reduce_rounds, ctx->d_hstats);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // overflow path: returns at once unless the queue was too small for this batch
+    return launch_hash_exact(ctx, dim3((max_n + kHashTilePoints - 1) / kHashTilePoints, count), slots, reduce_rounds, true);
+}
+
+// Derives the filter constants of K1f from the installed planes and centering (both must be known).
+chgpu_status refresh_hash_filter(chgpu_ctx* ctx) {
+    ctx->filter_ready = false;
+    if (!ctx->has_family || !ctx->has_centering) return CHGPU_OK;
+    const uint32_t G = ctx->fam.table_count * ctx->fam.short_bits + ctx->fam.long_bits;
+    const uint32_t gpad = (G + kFiltPlanes - 1) / kFiltPlanes * kFiltPlanes;
+    double mean_sq = 0.0;
+    for (int x = 0; x < kDim; ++x) {
+        const double c = ctx->h_centering[x];
+        if (!std::isfinite(c) || std::fabs(c) > 1e6) return CHGPU_OK;  // outside the bound's premises: exact kernel only
+        mean_sq += c * c;
+    }
+    std::vector<float> pt(size_t(kDim) * gpad, 0.0f);
+    std::vector<double> bias(gpad, 0.0), hnorm(gpad, 0.0);
+    for (uint32_t g = 0; g < G; ++g) {
+        const double* h = ctx->h_planes.data() + size_t(g) * kDim;
+        long double b = 0.0L, sq = 0.0L;
+        for (int x = 0; x < kDim; ++x) {
+            if (!std::isfinite(h[x]) || std::fabs(h[x]) > 1e30) return CHGPU_OK;
+            pt[size_t(x) * gpad + g] = static_cast<float>(h[x]);
+            b += static_cast<long double>(ctx->h_centering[x]) * h[x];
+            sq += static_cast<long double>(h[x]) * h[x];
+        }
+        bias[g] = static_cast<double>(b);
+        hnorm[g] = std::sqrt(static_cast<double>(sq)) * (1.0 + 1e-12);
+    }
+    if (gpad != ctx->gpad || !ctx->d_planes_t) {
+        CK(cudaStreamSynchronize(ctx->compute));
+        cudaFree(ctx->d_planes_t); cudaFree(ctx->d_bias); cudaFree(ctx->d_hnorm);
+        ctx->d_planes_t = nullptr; ctx->d_bias = nullptr; ctx->d_hnorm = nullptr;
+        CK(cudaMalloc(&ctx->d_planes_t, pt.size() * sizeof(float)));
+        CK(cudaMalloc(&ctx->d_bias, gpad * sizeof(double)));
+        CK(cudaMalloc(&ctx->d_hnorm, gpad * sizeof(double)));
+        ctx->gpad = gpad;
+    }
+    CK(cudaStreamSynchronize(ctx->compute));
+    CK(cudaMemcpy(ctx->d_planes_t, pt.data(), pt.size() * sizeof(float), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_bias, bias.data(), gpad * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_hnorm, hnorm.data(), gpad * sizeof(double), cudaMemcpyHostToDevice));
+    // A_p = a_rel ||d_p|| + a_abs  (see K1f): 136 u32 + 2^-44 relative, 2^-44 ||centering|| absolute
+    ctx->filt_a_rel = 136.0 * std::ldexp(1.0, -24) + std::ldexp(1.0, -44);
+    ctx->filt_a_abs = std::ldexp(1.0, -44) * std::sqrt(mean_sq) * (1.0 + 1e-12);
+    ctx->filter_ready = true;
+    return CHGPU_OK;
 }
 
 bool cfg_valid(const chgpu_match_cfg& c, uint32_t long_bits, const char** why) {
@@ -736,6 +843,11 @@ chgpu_status chgpu_create(int device, chgpu_ctx** out) {
     ok &= cudaMalloc(&ctx->d_stats, sizeof(DevStats)) == cudaSuccess;
     ok &= cudaMallocHost(reinterpret_cast<void**>(&ctx->h_stats), sizeof(DevStats)) == cudaSuccess;
     ok &= cudaMalloc(&ctx->d_counter, sizeof(unsigned int)) == cudaSuccess;
+    ok &= cudaMalloc(&ctx->d_hq, size_t(kHashQueueCap) * sizeof(uint2)) == cudaSuccess;
+    ok &= cudaMalloc(&ctx->d_hq_count, sizeof(unsigned int)) == cudaSuccess;
+    ok &= cudaMalloc(&ctx->d_hstats, sizeof(HashFilterStats)) == cudaSuccess;
+    ok &= cudaMemset(ctx->d_hstats, 0, sizeof(HashFilterStats)) == cudaSuccess;
+    if (const char* e = getenv("CHGPU_HASH_EXACT")) ctx->hash_mode = (e[0] == '1') ? CHGPU_HASH_EXACT : CHGPU_HASH_FILTERED;
     if (!ok) return bail(CHGPU_ECUDA);
     *out = ctx;
     return CHGPU_OK;
@@ -761,6 +873,8 @@ void chgpu_destroy(chgpu_ctx* ctx) {
     cudaFree(ctx->d_planes); cudaFree(ctx->d_centering); cudaFree(ctx->d_sums); cudaFree(ctx->d_res);
     cudaFree(ctx->d_stats); cudaFreeHost(ctx->h_stats); cudaFree(ctx->d_counter); cudaFree(ctx->d_slots);
     cudaFree(ctx->d_dbg);
+    cudaFree(ctx->d_planes_t); cudaFree(ctx->d_bias); cudaFree(ctx->d_hnorm); cudaFree(ctx->d_hq);
+    cudaFree(ctx->d_hq_count); cudaFree(ctx->d_hstats);
     if (ctx->ev_upload) cudaEventDestroy(ctx->ev_upload);
     if (ctx->ev_compute) cudaEventDestroy(ctx->ev_compute);
     if (ctx->ev_t0) cudaEventDestroy(ctx->ev_t0);
@@ -835,6 +949,27 @@ chgpu_status chgpu_set_family(chgpu_ctx* ctx, const chgpu_family_params* p, cons
     CK(cudaMemcpy(ctx->d_planes + ns * kDim, long_planes, nl * kDim * sizeof(double), cudaMemcpyHostToDevice));
     ctx->fam = *p;
     ctx->has_family = true;
+    ctx->h_planes.assign(short_planes, short_planes + ns * kDim);
+    ctx->h_planes.insert(ctx->h_planes.end(), long_planes, long_planes + nl * kDim);
+    return refresh_hash_filter(ctx);
+}
+
+chgpu_status chgpu_set_hash_mode(chgpu_ctx* ctx, chgpu_hash_mode mode) {
+    if (!ctx || (mode != CHGPU_HASH_FILTERED && mode != CHGPU_HASH_EXACT)) return CHGPU_EINVAL;
+    ctx->hash_mode = mode;
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_get_hash_stats(chgpu_ctx* ctx, chgpu_hash_stats* out) {
+    if (!ctx || !out) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    HashFilterStats hs;
+    CK(cudaMemcpyAsync(&hs, ctx->d_hstats, sizeof(hs), cudaMemcpyDeviceToHost, ctx->compute));
+    CK(cudaStreamSynchronize(ctx->compute));
+    out->undecided_dots = hs.undecided;
+    out->flipped_bits = hs.flipped;
+    out->overflowed_batches = hs.overflows;
+    out->filter_active = (ctx->hash_mode == CHGPU_HASH_FILTERED && ctx->filter_ready) ? 1 : 0;
     return CHGPU_OK;
 }
 
@@ -887,7 +1022,7 @@ chgpu_status chgpu_set_centering(chgpu_ctx* ctx, const double* centering128) {
     CK(cudaMemcpy(ctx->d_centering, centering128, 128 * sizeof(double), cudaMemcpyHostToDevice));
     memcpy(ctx->h_centering, centering128, sizeof(ctx->h_centering));
     ctx->has_centering = true;
-    return CHGPU_OK;
+    return refresh_hash_filter(ctx);
 }
 
 chgpu_status chgpu_centering_apply(chgpu_ctx* ctx, double* centering128_out) {
@@ -1269,19 +1404,18 @@ chgpu_status chgpu_hash_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32
     CK(cudaStreamSynchronize(ctx->compute));
     CK(cudaMemcpyAsync(ctx->d_slots, slots.data(), count * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->compute));
     if (max_n) {
-        const dim3 grid((max_n + kHashTilePoints - 1) / kHashTilePoints, count);
-        cudaError_t e = cudaSuccess;
-        switch (reduce_rounds) {
-            case 0: e = launch_hash_rr<0>(ctx, grid); break;
-            case 1: e = launch_hash_rr<1>(ctx, grid); break;
-            case 2: e = launch_hash_rr<2>(ctx, grid); break;
-            case 3: e = launch_hash_rr<3>(ctx, grid); break;
-            case 4: e = launch_hash_rr<4>(ctx, grid); break;
-            case 5: e = launch_hash_rr<5>(ctx, grid); break;
-            case 6: e = launch_hash_rr<6>(ctx, grid); break;
-            default: e = launch_hash_rr<7>(ctx, grid); break;
+        if (ctx->hash_mode == CHGPU_HASH_FILTERED && ctx->filter_ready) {
+            // fp32 filter + exact fixup, in launches of <= kHashBatchImages images (one queue per launch)
+            for (uint32_t first = 0; first < count; first += kHashBatchImages) {
+                const uint32_t cnt = std::min(kHashBatchImages, count - first);
+                uint32_t mx = 0;
+                for (uint32_t i = 0; i < cnt; ++i) mx = std::max(mx, ctx->images[slots[first + i]].dev.n);
+                if (mx) CK(launch_hash_filtered(ctx, ctx->d_slots + first, cnt, mx, reduce_rounds));
+            }
+        } else {
+            CK(launch_hash_exact(ctx, dim3((max_n + kHashTilePoints - 1) / kHashTilePoints, count), ctx->d_slots,
+                                 reduce_rounds, false));
         }
-        CK(e);
     }
     if (const chgpu_status s = launch_bucket_build(ctx, count)) return s;
     for (uint32_t i = 0; i < count; ++i) {

@@ -117,8 +117,12 @@ template <int RR>
 __global__ void __launch_bounds__(kHashThreads)
 hash_codes_kernel(const DevImage* __restrict__ images, const uint32_t* __restrict__ slots,
                   const double* __restrict__ planes /* (L*m + n) x 128: short planes then long */,
-                  const double* __restrict__ centering /* 128 */, uint32_t m, uint32_t L, uint32_t nlong) {
+                  const double* __restrict__ centering /* 128 */, uint32_t m, uint32_t L, uint32_t nlong,
+                  const unsigned int* __restrict__ guard_count /* nullable */, uint32_t guard_cap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    // Launched behind the filtered kernel (K1f below) as its overflow path: it only runs when the
+    // queue of undecided dots did not hold them all.
+    if (guard_count != nullptr && *guard_count <= guard_cap) return;
     double* cT = reinterpret_cast<double*>(smem_raw);
     double* hs = cT + kDim * kHashTilePoints;
     uint32_t* pbits = reinterpret_cast<uint32_t*>(hs + kHashChunkPlanes * kDim);
@@ -182,6 +186,209 @@ hash_codes_kernel(const DevImage* __restrict__ images, const uint32_t* __restric
             lw[k] = first < nlong ? take_bits(w, L * m + first, min(32u, nlong - first)) : 0u;
         }
         img.longs[p] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K1f: hash codes through an fp32 filter with an a-priori error bound; the default hash path.
+//
+// A hash bit is the sign of the reference's fp64 value r = reduce_dot(c, h) (hashing.hpp:24-43), and
+// it has to be reproduced exactly.  Almost every |r| is ~10^3 while its sign only needs ~10^-1 of
+// accuracy, so the bulk of the work runs as an fp32 SIMT contraction and only the dots the bound
+// cannot decide are re-evaluated by hash_fixup_kernel in the exact fp64 operation DAG.
+//
+//   acc  = fl32( sum_x d_x * fl32(h_x) )        d_x = descriptor byte, exact in fp32; 128 FFMA
+//   v    = double(acc) - bias_g                 bias_g = sum_x centering_x h_x (host, fp64)
+//   E    = A_p * ||h_g||_2 + 1e-30              A_p = (136 * 2^-24 + 2^-44) ||d_p||_2 + 2^-44 ||centering||_2
+//
+// With x the exact real value of sum_x (d_x - centering_x) h_x:  |v - x| <= 132 u32 ||d|| ||h|| + 131 u64
+// ||centering|| ||h|| + u64 |v|  (gamma_128 of the FFMA chain plus one rounding of every h_x, Cauchy-Schwarz
+// on sum |d_x h_x|; the host's bias sum; the final subtraction) and |r - x| <= 131 u64 (||d|| + ||centering||)
+// ||h||  (one rounding of c_x = d_x - centering_x, the rounded products and at most 127 additions on any
+// path of the DAG, for every N_r).  E exceeds their sum, hence |v| > E implies r != 0 and sign(r) = sign(v).
+// Everything else — ties included — goes to the queue.  The host refuses the filter (exact kernel only)
+// for planes or centerings that are not finite or exceed 1e30 / 1e6 in magnitude.
+//
+// One CTA = 128 points x all planes in chunks of 64; thread tile 8 points x 4 planes (32 accumulators),
+// operands from shared memory: dT[128][128] fp32 descriptors component-major, hT[128][64] plane chunk.
+constexpr int kFiltPoints = 128;
+constexpr int kFiltPlanes = 64;
+constexpr int kFiltThreads = 256;
+
+struct HashFilterParams {
+    const DevImage* images;
+    const uint32_t* slots;
+    const float* planes_t;      // [128][gpad] fp32-rounded planes, component-major, zero padded
+    const double* bias;         // [gpad]
+    const double* hnorm;        // [gpad] ||h_g||_2, rounded up
+    double a_rel, a_abs;        // A_p = a_rel * ||d_p|| + a_abs
+    uint32_t gpad, m, L, nlong;
+    uint2* queue;               // undecided dots: (slot, point << 16 | plane)
+    uint32_t queue_cap;
+    unsigned int* queue_count;  // entries wanted (may exceed queue_cap: overflow)
+};
+
+constexpr size_t hash_filter_smem_bytes() {
+    return sizeof(float) * kDim * (kFiltPoints + kFiltPlanes) + sizeof(double) * kFiltPoints +
+           sizeof(uint32_t) * kFiltPoints * (kPlaneWords + 1);
+}
+
+__global__ void __launch_bounds__(kFiltThreads, 2) hash_filter_kernel(const HashFilterParams P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* dT = reinterpret_cast<float*>(smem_raw);
+    float* hT = dT + kDim * kFiltPoints;
+    double* Ap = reinterpret_cast<double*>(hT + kDim * kFiltPlanes);
+    uint32_t* pbits = reinterpret_cast<uint32_t*>(Ap + kFiltPoints);
+    uint32_t* dn2 = pbits + kFiltPoints * kPlaneWords;
+
+    const uint32_t slot = P.slots[blockIdx.y];
+    const DevImage img = P.images[slot];
+    const uint32_t p0 = blockIdx.x * kFiltPoints;
+    if (p0 >= img.n) return;
+    const uint32_t tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const uint32_t nplanes = P.L * P.m + P.nlong;
+
+    for (uint32_t i = tid; i < kFiltPoints * (kPlaneWords + 1); i += kFiltThreads) pbits[i] = 0;  // pbits and dn2
+    __syncthreads();
+    {   // stage: lane <-> point, so the component-major stores are conflict-free; two threads share a row
+        const uint32_t p = tid & (kFiltPoints - 1), half = tid >> 7;
+        const bool live = p0 + p < img.n;
+        const uint4* row = reinterpret_cast<const uint4*>(img.desc + uint64_t(live ? p0 + p : 0) * kDim) + half * 4;
+        uint32_t ss = 0;
+#pragma unroll
+        for (uint32_t w = 0; w < 4; ++w) {
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (live) v = __ldg(row + w);
+            const uint32_t words[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (uint32_t b = 0; b < 16; ++b) {
+                const uint32_t byte = (words[b >> 2] >> (8 * (b & 3))) & 0xffu;
+                dT[(half * 64 + w * 16 + b) * kFiltPoints + p] = float(byte);
+                ss += byte * byte;
+            }
+        }
+        atomicAdd(&dn2[p], ss);
+    }
+    __syncthreads();
+    if (tid < kFiltPoints) Ap[tid] = __dadd_ru(__dmul_ru(P.a_rel, __dsqrt_ru(double(dn2[tid]))), P.a_abs);
+
+    for (uint32_t g0 = 0; g0 < nplanes; g0 += kFiltPlanes) {
+        __syncthreads();  // previous chunk consumed (first time: Ap written)
+        for (uint32_t i = tid; i < kDim * (kFiltPlanes / 4); i += kFiltThreads) {
+            const uint32_t k = i / (kFiltPlanes / 4), c4 = i % (kFiltPlanes / 4);
+            reinterpret_cast<float4*>(hT)[i] = __ldg(reinterpret_cast<const float4*>(P.planes_t + uint64_t(k) * P.gpad + g0) + c4);
+        }
+        __syncthreads();
+        float acc[8][4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+        const float* dcol = dT + ty * 8;
+        const float* hcol = hT + tx * 4;
+#pragma unroll 8
+        for (int k = 0; k < kDim; ++k) {
+            const float4 a0 = *reinterpret_cast<const float4*>(dcol + k * kFiltPoints);
+            const float4 a1 = *reinterpret_cast<const float4*>(dcol + k * kFiltPoints + 4);
+            const float4 b = *reinterpret_cast<const float4*>(hcol + k * kFiltPlanes);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
+        }
+        // decide: sign certain iff |v| > E
+        const uint32_t g = g0 + tx * 4;
+        double bj[4], hj[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            bj[j] = __ldg(P.bias + g + j);
+            hj[j] = __ldg(P.hnorm + g + j);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t p = ty * 8 + i;
+            const double A = Ap[p];
+            uint32_t nib = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const double v = __dsub_rn(double(acc[i][j]), bj[j]);
+                const double E = __dadd_ru(__dmul_ru(A, hj[j]), 1e-30);
+                if (v > 0.0) nib |= 1u << j;
+                if (!(fabs(v) > E) && g + j < nplanes && p0 + p < img.n) {
+                    const unsigned int at = atomicAdd(P.queue_count, 1u);
+                    if (at < P.queue_cap) P.queue[at] = make_uint2(slot, ((p0 + p) << 16) | (g + j));
+                }
+            }
+            if (nib) atomicOr(&pbits[p * kPlaneWords + (g >> 5)], nib << (g & 31));
+        }
+    }
+    __syncthreads();
+
+    // pack exactly as hash_codes_kernel does
+    if (tid < kFiltPoints && p0 + tid < img.n) {
+        const uint32_t p = p0 + tid;
+        uint32_t w[kPlaneWords + 1];
+#pragma unroll
+        for (int i = 0; i < kPlaneWords; ++i) w[i] = pbits[tid * kPlaneWords + i];
+        w[kPlaneWords] = 0;
+        for (uint32_t t = 0; t < P.L; ++t) img.shorts[uint64_t(p) * P.L + t] = take_bits(w, t * P.m, P.m);
+        uint32_t lw[4];
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) {
+            const uint32_t first = k * 32;
+            lw[k] = first < P.nlong ? take_bits(w, P.L * P.m + first, min(32u, P.nlong - first)) : 0u;
+        }
+        img.longs[p] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+}
+
+struct HashFilterStats {
+    unsigned long long undecided;  // dots sent to the exact path
+    unsigned long long flipped;    // of those, bits the fp32 sign had wrong
+    unsigned long long overflows;  // batches whose queue overflowed (recomputed by hash_codes_kernel)
+};
+
+// Exact re-evaluation of the undecided dots: one thread per queue entry walks the reference DAG
+// (center_descriptor hashing.cpp:72-78, reduce_dot hashing.hpp:24-43) and corrects the stored bit.
+__global__ void hash_fixup_kernel(const DevImage* __restrict__ images, const double* __restrict__ planes,
+                                  const double* __restrict__ centering, const uint2* __restrict__ queue,
+                                  uint32_t queue_cap, const unsigned int* __restrict__ queue_count, uint32_t m,
+                                  uint32_t L, int reduce_rounds, HashFilterStats* __restrict__ stats) {
+    const uint32_t want = *queue_count, n = min(want, queue_cap);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        atomicAdd(&stats->undecided, (unsigned long long)want);
+        if (want > queue_cap) atomicAdd(&stats->overflows, 1ull);
+    }
+    const uint32_t tail = 1u << reduce_rounds;
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        const uint2 q = queue[e];
+        const DevImage img = images[q.x];
+        const uint32_t p = q.y >> 16, g = q.y & 0xffffu;
+        const uint8_t* d = img.desc + uint64_t(p) * kDim;
+        const double* h = planes + uint64_t(g) * kDim;
+        double s[kDim];
+        for (int x = 0; x < kDim; ++x) s[x] = __dmul_rn(__dsub_rn(double(d[x]), centering[x]), h[x]);
+        for (uint32_t width = kDim / 2; width >= tail; width >>= 1)
+            for (uint32_t i = 0; i < width; ++i) s[i] = __dadd_rn(s[i], s[i + width]);
+        double acc = s[0];
+        for (uint32_t j = 1; j < tail; ++j) acc = __dadd_rn(acc, s[j]);
+        const uint32_t bit = acc > 0.0 ? 1u : 0u;
+        uint32_t* word;
+        uint32_t pos;
+        if (g < L * m) {
+            word = img.shorts + uint64_t(p) * L + g / m;
+            pos = g % m;
+        } else {
+            const uint32_t j = g - L * m;
+            word = reinterpret_cast<uint32_t*>(img.longs + p) + (j >> 5);
+            pos = j & 31;
+        }
+        if (((*word >> pos) & 1u) != bit) {
+            atomicXor(word, 1u << pos);
+            atomicAdd(&stats->flipped, 1ull);
+        }
     }
 }
 
