@@ -224,7 +224,14 @@ __device__ __forceinline__ uint32_t key_of(uint32_t id, const uint4& ql, uint32_
     uint4 c;
     if (SMEM_TRAIN) c = lds128(s_long + id * 16u);
     else c = __ldg(g_long + id);
+#ifdef CHGPU_CSA_POPC
     return (hamming128(c, ql) << 24) | id;
+#else
+    // distance << 24 | id with the shift folded into two multiply-adds (id < 2^24: '+' carries nothing)
+    const uint32_t t = __popc(c.x ^ ql.x) + __popc(c.y ^ ql.y) + __popc(c.z ^ ql.z);
+    const uint32_t k = __popc(c.w ^ ql.w) * 0x1000000u + id;
+    return t * 0x1000000u + k;
+#endif
 }
 
 // One step of the Hamming scan: candidate `first + lane` of the bucket-major id list, clamped
@@ -435,14 +442,22 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 #pragma unroll
                     for (int s = 0; s < kOverSlots; ++s) key[LT + s] = kNone;
                     if (tover != 0) {
+                        // id for now; its key below.  r + adj is a u32 sum (adj never wraps: pre < first + 32)
                         const uint32_t seg_mask[3] = {hdr.y, hdr.z, hdr.w};
+                        {
+                            const uint32_t seg = __popc(seg_mask[0] & le_mask) - 1u;
+                            const uint32_t r = min(lane, tover - 1u);
+                            key[LT] = __ldg(ids + uint32_t(r + lds32(rec + kAdj + seg * 4u)));
+                        }
+                        if (tover > 32u) {  // a second / third overflow step is rare: keep it out of line
 #pragma unroll
-                        for (int s = 0; s < kOverSlots; ++s) {
-                            if (uint32_t(s) * 32u < tover) {
-                                const uint32_t base = s == 0 ? 0u : (hdr.x >> (8 + 8 * s)) & 0xffu;
-                                const uint32_t seg = base + __popc(seg_mask[s] & le_mask) - 1u;
-                                const uint32_t r = min(uint32_t(s) * 32u + lane, tover - 1u);
-                                key[LT + s] = __ldg(ids + r + lds32(rec + kAdj + seg * 4u));  // id for now; its key below
+                            for (int s = 1; s < kOverSlots; ++s) {
+                                if (uint32_t(s) * 32u < tover) {
+                                    const uint32_t base = (hdr.x >> (8 + 8 * s)) & 0xffu;
+                                    const uint32_t seg = base + __popc(seg_mask[s] & le_mask) - 1u;
+                                    const uint32_t r = min(uint32_t(s) * 32u + lane, tover - 1u);
+                                    key[LT + s] = __ldg(ids + uint32_t(r + lds32(rec + kAdj + seg * 4u)));
+                                }
                             }
                         }
                     }
