@@ -104,12 +104,18 @@ struct ImageRec {
     size_t block_bytes = 0;
     uint32_t image_id = 0;
     bool used = false;
+    // id-range tiles of an image too large for the match kernel's shared-memory tile: hidden slots of the
+    // image table whose DevImages are slices of this block with their own bucket index (local point ids)
+    std::vector<uint32_t> tile_slots;
 };
 
 struct MatchBuffers {
     PairDesc* h_pairs = nullptr;  // pinned
     PairDesc* d_pairs = nullptr;
     size_t pairs_cap = 0;
+    PairDesc* h_tpairs = nullptr;  // pinned: (query image, tile) pairs of a tiled sub-batch
+    PairDesc* d_tpairs = nullptr;
+    size_t tpairs_cap = 0;
     uint32_t* d_counts = nullptr;
     unsigned long long* d_offsets = nullptr;
     unsigned long long* h_offsets = nullptr;  // pinned
@@ -169,6 +175,10 @@ struct chgpu_ctx {
     // match workspace
     uint2* d_res = nullptr;
     size_t res_cap = 0;
+    uint32_t* d_gmin = nullptr;   // tiled train images: per-query minimum key over the tiles
+    size_t gmin_cap = 0;
+    uint32_t* d_lists = nullptr;  // tiled train images: per-query, per-tile top-k keys
+    size_t lists_cap = 0;
     MatchBuffers mb[2];
     DevStats* d_stats = nullptr;
     DevStats* h_stats = nullptr;  // pinned
@@ -205,6 +215,36 @@ chgpu_status fail(chgpu_ctx* ctx, chgpu_status s, const char* fmt, ...) {
 struct DeviceGuard {
     explicit DeviceGuard(int dev) { cudaSetDevice(dev); }
 };
+
+size_t smem_train_capacity(const chgpu_ctx* ctx, bool guided = false);
+
+// Point ids per tile of a large train image: what fits the kernel's shared memory, at most ~32 entries per
+// bucket (the occupancy the scan is laid out for), a multiple of 1024.
+uint32_t tile_points_of(const chgpu_ctx* ctx) {
+    const size_t cap = smem_train_capacity(ctx) & ~size_t(1023);
+    const size_t want = std::max<size_t>(1024, size_t(32) << ctx->fam.short_bits);
+    return uint32_t(std::max<size_t>(1024, std::min(cap, want)));
+}
+uint32_t tile_count_of(const chgpu_ctx* ctx, uint32_t n) {
+    if (n <= smem_train_capacity(ctx)) return 0;
+    const uint32_t tp = tile_points_of(ctx);
+    return (n + tp - 1) / tp;
+}
+
+// Layout of the tiles' bucket arrays behind the image's own: per tile offs | points | scan.
+size_t tile_block_bytes(uint32_t n, uint32_t m, uint32_t L, uint32_t ntiles, uint32_t tp, std::vector<size_t>* off) {
+    size_t o = 0;
+    for (uint32_t k = 0; k < ntiles; ++k) {
+        const uint32_t nk = std::min(tp, n - k * tp);
+        if (off) off->push_back(o);
+        o += align_up(size_t(L) * ((size_t(1) << m) + 1) * 4);
+        if (off) off->push_back(o);
+        o += align_up(size_t(L) * nk * 2);
+        if (off) off->push_back(o);
+        o += align_up(size_t(L) * nk * 2) + kAlign;
+    }
+    return o;
+}
 
 size_t image_block_bytes(uint32_t n, uint32_t m, uint32_t L, size_t off[7]) {
     size_t o = 0;
@@ -301,6 +341,28 @@ chgpu_status order_compute_after_copy(chgpu_ctx* ctx) {
     return CHGPU_OK;
 }
 
+// Returns the slot (and the hidden tile slots behind it) to the free list and its block to the arena.
+void release_slot(chgpu_ctx* ctx, uint32_t slot) {
+    ImageRec& r = ctx->images[slot];
+    for (const uint32_t ts : r.tile_slots) {
+        ctx->images[ts] = ImageRec{};
+        ctx->free_slots.push_back(ts);
+    }
+    ctx->arena.release(r.block, r.block_bytes);
+    r = ImageRec{};
+    ctx->free_slots.push_back(slot);
+}
+
+uint32_t take_slot(chgpu_ctx* ctx) {
+    if (!ctx->free_slots.empty()) {
+        const uint32_t slot = ctx->free_slots.back();
+        ctx->free_slots.pop_back();
+        return slot;
+    }
+    ctx->images.emplace_back();
+    return static_cast<uint32_t>(ctx->images.size() - 1);
+}
+
 chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t* slot_out) {
     if (!ctx->has_family)
         return fail(ctx, CHGPU_ELOGIC, "chgpu_set_family must precede image uploads (block layout depends on m, L)");
@@ -310,28 +372,33 @@ chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t
         // replacing: drain both streams so no kernel or copy still reads the old block
         CK(cudaStreamSynchronize(ctx->copy));
         CK(cudaStreamSynchronize(ctx->compute));
-        ImageRec& old = ctx->images[it->second];
-        ctx->arena.release(old.block, old.block_bytes);
-        old.used = false;
-        ctx->free_slots.push_back(it->second);
+        release_slot(ctx, it->second);
         ctx->slot_of.erase(it);
     }
-    uint32_t slot;
-    if (!ctx->free_slots.empty()) {
-        slot = ctx->free_slots.back();
-        ctx->free_slots.pop_back();
-    } else {
-        slot = static_cast<uint32_t>(ctx->images.size());
-        ctx->images.emplace_back();
+    const uint32_t m = ctx->fam.short_bits, L = ctx->fam.table_count;
+    const uint32_t ntiles = tile_count_of(ctx, n), tp = tile_points_of(ctx);
+    const uint32_t slot = take_slot(ctx);
+    std::vector<uint32_t> tile_slots(ntiles);
+    for (uint32_t& ts : tile_slots) ts = take_slot(ctx);
+    auto give_back = [&] {
+        for (const uint32_t ts : tile_slots) ctx->free_slots.push_back(ts);
+        ctx->free_slots.push_back(slot);
+    };
+    uint32_t top = slot;
+    for (const uint32_t ts : tile_slots) top = std::max(top, ts);
+    if (const chgpu_status s = ensure_images_cap(ctx, size_t(top) + 1)) {
+        give_back();
+        return s;
     }
-    if (const chgpu_status s = ensure_images_cap(ctx, size_t(slot) + 1)) return s;
     size_t off[7];
-    const size_t bytes = image_block_bytes(n, ctx->fam.short_bits, ctx->fam.table_count, off);
+    std::vector<size_t> toff;
+    const size_t own = image_block_bytes(n, m, L, off);
+    const size_t bytes = own + tile_block_bytes(n, m, L, ntiles, tp, &toff);
     char* block = nullptr;
     const cudaError_t e = ctx->arena.alloc(bytes, &block);
     if (e != cudaSuccess) {
         cudaGetLastError();
-        ctx->free_slots.push_back(slot);
+        give_back();
         return fail(ctx, CHGPU_ENOMEM, "arena allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
     }
     ImageRec& r = ctx->images[slot];
@@ -348,9 +415,35 @@ chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t
     r.dev.scan = reinterpret_cast<uint16_t*>(block + off[6]);
     r.dev.n = n;
     r.dev.flags = 0;
+    r.tile_slots = tile_slots;
+    for (uint32_t k = 0; k < ntiles; ++k) {
+        ImageRec& t = ctx->images[tile_slots[k]];
+        t = ImageRec{};
+        t.image_id = image_id;
+        t.used = true;
+        const size_t base = size_t(k) * tp;
+        t.dev.desc = r.dev.desc + base * kDim;
+        t.dev.kp = r.dev.kp + base;
+        t.dev.longs = r.dev.longs + base;
+        t.dev.shorts = r.dev.shorts + base * L;
+        t.dev.offs = reinterpret_cast<uint32_t*>(block + own + toff[3 * k]);
+        t.dev.points = reinterpret_cast<uint16_t*>(block + own + toff[3 * k + 1]);
+        t.dev.scan = reinterpret_cast<uint16_t*>(block + own + toff[3 * k + 2]);
+        t.dev.n = std::min(tp, n - k * tp);
+        t.dev.flags = 0;
+        if (const chgpu_status s = publish_slot(ctx, tile_slots[k])) return s;
+    }
     ctx->slot_of[image_id] = slot;
     *slot_out = slot;
     return CHGPU_OK;
+}
+
+// Slots whose bucket index has to be (re)built with the codes of `slots`: the images and their tiles.
+std::vector<uint32_t> with_tile_slots(const chgpu_ctx* ctx, const std::vector<uint32_t>& slots) {
+    std::vector<uint32_t> all(slots);
+    for (const uint32_t s : slots)
+        all.insert(all.end(), ctx->images[s].tile_slots.begin(), ctx->images[s].tile_slots.end());
+    return all;
 }
 
 chgpu_status ensure_slots_scratch(chgpu_ctx* ctx, size_t count) {
@@ -505,7 +598,7 @@ cudaError_t launch_match(chgpu_ctx* ctx, MatchParams& P, bool smem_train, uint32
                       : launch_match_global(P, smem, sms, ctx->compute, grid);
 }
 
-size_t smem_train_capacity(const chgpu_ctx* ctx, bool guided = false) {
+size_t smem_train_capacity(const chgpu_ctx* ctx, bool guided) {
     // points whose codes fit next to the bucket offsets in the dynamic smem of a 1-CTA/SM launch
     // (minus the kernel's static 16 B and the 1 KiB the driver reserves per block)
     const size_t avail = ctx->prop.sharedMemPerBlockOptin - 1024 - 64;
@@ -519,7 +612,11 @@ struct SubBatch {
     uint32_t first, count;
     uint64_t queries;
     uint32_t max_nt, max_nq;
+    // train images larger than the shared-memory tile: matched tile by tile (match_kernels.cuh MODE 1 / 2 + merge)
+    bool tiled;
+    uint32_t max_tiles, tile_pairs;
 };
+constexpr uint64_t kTileListBytes = uint64_t(1) << 30;  // cap of the per-query list scratch of a tiled sub-batch
 
 chgpu_status ensure_match_buffers(chgpu_ctx* ctx, MatchBuffers& b, const SubBatch& sb, bool host_side) {
     if (b.pairs_cap < sb.count) {
@@ -605,7 +702,7 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
     std::vector<PairDesc> descs(npairs);
     std::vector<SubBatch> subs;
     {
-        SubBatch cur{0, 0, 0, 0, 0};
+        SubBatch cur{0, 0, 0, 0, 0, false, 0, 0};
         for (uint32_t k = 0; k < npairs; ++k) {
             uint32_t si, sj;
             if (const chgpu_status s = find_slot(ctx, run.pairs[2 * k], &si)) return s;
@@ -615,11 +712,17 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
             if (!(I.flags & 1u) || !(J.flags & 1u))
                 return fail(ctx, CHGPU_ELOGIC, "pair (%u,%u): codes not computed (call chgpu_hash_images first)",
                             run.pairs[2 * k], run.pairs[2 * k + 1]);
-            if (cur.count && (cur.queries + I.n > ctx->sub_batch_queries || cur.count >= (1u << 20))) {
+            const uint32_t tiles = run.fmats ? 0u : uint32_t(ctx->images[sj].tile_slots.size());
+            const bool tiled = tiles != 0;
+            if (cur.count && (cur.queries + I.n > ctx->sub_batch_queries || cur.count >= (1u << 20) || tiled != cur.tiled ||
+                              (tiled && (cur.queries + I.n) * std::max(cur.max_tiles, tiles) * run.cfg.top_k * 4 > kTileListBytes))) {
                 subs.push_back(cur);
-                cur = SubBatch{k, 0, 0, 0, 0};
+                cur = SubBatch{k, 0, 0, 0, 0, false, 0, 0};
             }
-            descs[k] = PairDesc{si, sj, cur.queries};
+            descs[k] = PairDesc{si, sj, cur.queries, 0u, 0u};
+            cur.tiled = tiled;
+            cur.max_tiles = std::max(cur.max_tiles, tiles);
+            cur.tile_pairs += tiles;
             cur.count += 1;
             cur.queries += I.n;
             cur.max_nt = std::max(cur.max_nt, J.n);
@@ -719,8 +822,9 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
         const bool smem_train = sb.max_nt <= cap_nt;
         // enough units to balance the persistent grid: >= 4 per CTA, chunks of >= 256 queries
         const uint32_t ctas = uint32_t(ctx->prop.multiProcessorCount) * (smem_train && sb.max_nt * 16u > 100000u ? 1u : 2u);
+        const uint32_t unit_pairs = sb.tiled ? sb.tile_pairs : sb.count;
         uint32_t chunks = 1;
-        if (sb.count < 4 * ctas) chunks = std::min<uint32_t>((4 * ctas + sb.count - 1) / sb.count, std::max<uint32_t>(1, sb.max_nq / 256));
+        if (unit_pairs < 4 * ctas) chunks = std::min<uint32_t>((4 * ctas + unit_pairs - 1) / unit_pairs, std::max<uint32_t>(1, sb.max_nq / 256));
 
         MatchParams P{};
         P.images = ctx->d_images;
@@ -744,10 +848,69 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
             P.dbg_ranked = ctx->d_dbg;
             P.dbg_count = ctx->d_dbg + size_t(sb.max_nq) * run.cfg.top_k;
         }
-        CK(cudaEventRecord(b.ev_k0, ctx->compute));
         uint32_t grid = 0;
-        CK(launch_match(ctx, P, smem_train, sb.max_nt, &grid));
-        CK(cudaEventRecord(b.ev_k1, ctx->compute));
+        if (sb.tiled) {
+            // (query image, tile) pairs: min pass, top-k pass for the queries with a candidate within tau, merge
+            const uint32_t tp = tile_points_of(ctx);
+            if (b.tpairs_cap < sb.tile_pairs) {
+                CK(cudaStreamSynchronize(ctx->compute));
+                cudaFree(b.d_tpairs);
+                cudaFreeHost(b.h_tpairs);
+                b.d_tpairs = b.h_tpairs = nullptr;
+                b.tpairs_cap = 0;
+                const size_t cap = std::max<size_t>(sb.tile_pairs, 4096);
+                CK(cudaMalloc(&b.d_tpairs, cap * sizeof(PairDesc)));
+                CK(cudaMallocHost(&b.h_tpairs, cap * sizeof(PairDesc)));
+                b.tpairs_cap = cap;
+            }
+            const size_t stride = size_t(sb.max_tiles) * run.cfg.top_k;
+            if (ctx->gmin_cap < sb.queries || ctx->lists_cap < sb.queries * stride) {
+                CK(cudaStreamSynchronize(ctx->compute));
+                if (ctx->gmin_cap < sb.queries) {
+                    cudaFree(ctx->d_gmin);
+                    ctx->d_gmin = nullptr;
+                    ctx->gmin_cap = 0;
+                    CK(cudaMalloc(&ctx->d_gmin, sb.queries * sizeof(uint32_t)));
+                    ctx->gmin_cap = sb.queries;
+                }
+                if (ctx->lists_cap < sb.queries * stride) {
+                    cudaFree(ctx->d_lists);
+                    ctx->d_lists = nullptr;
+                    ctx->lists_cap = 0;
+                    CK(cudaMalloc(&ctx->d_lists, sb.queries * stride * sizeof(uint32_t)));
+                    ctx->lists_cap = sb.queries * stride;
+                }
+            }
+            uint32_t ntp = 0;
+            for (uint32_t k = 0; k < sb.count; ++k) {
+                const PairDesc& pd = descs[sb.first + k];
+                const std::vector<uint32_t>& ts = ctx->images[pd.slot_j].tile_slots;
+                for (uint32_t t = 0; t < ts.size(); ++t) b.h_tpairs[ntp++] = PairDesc{pd.slot_i, ts[t], pd.res_off, t * tp, t};
+            }
+            CK(cudaMemcpyAsync(b.d_tpairs, b.h_tpairs, size_t(ntp) * sizeof(PairDesc), cudaMemcpyHostToDevice, ctx->compute));
+            CK(cudaMemsetAsync(ctx->d_gmin, 0xff, sb.queries * sizeof(uint32_t), ctx->compute));
+            P.gmin = ctx->d_gmin;
+            P.lists = ctx->d_lists;
+            P.list_stride = uint32_t(stride);
+            P.tile_points = tp;
+            P.smem_long_bytes = std::min(tp, sb.max_nt) * 16u;
+            const size_t smem = size_t(P.smem_long_bytes) + offs_smem_bytes(ctx) + stage_smem_bytes(ctx);
+            CK(cudaEventRecord(b.ev_k0, ctx->compute));
+            P.pairs = b.d_tpairs;
+            P.nunits = ntp * chunks;
+            CK(launch_match_tiled(P, kModeTileMin, smem, ctx->prop.multiProcessorCount, ctx->compute, &grid));
+            CK(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), ctx->compute));
+            CK(launch_match_tiled(P, kModeTileTopK, smem, ctx->prop.multiProcessorCount, ctx->compute, &grid));
+            P.pairs = b.d_pairs;
+            CK(launch_tile_merge(P, sb.count, sb.max_nq, ctx->compute));
+            CK(cudaEventRecord(b.ev_k1, ctx->compute));
+            st.match_launches += 2;
+            st.total_launches += 2;
+        } else {
+            CK(cudaEventRecord(b.ev_k0, ctx->compute));
+            CK(launch_match(ctx, P, smem_train, sb.max_nt, &grid));
+            CK(cudaEventRecord(b.ev_k1, ctx->compute));
+        }
         scan_counts_kernel<<<1, 1024, 0, ctx->compute>>>(b.d_counts, sb.count, b.d_offsets, ctx->d_stats);
         CK(cudaGetLastError());
         compact_kernel<<<sb.count, 256, 0, ctx->compute>>>(b.d_pairs, ctx->d_images, ctx->d_res, b.d_offsets,
@@ -861,6 +1024,7 @@ void chgpu_destroy(chgpu_ctx* ctx) {
     for (MatchBuffers& b : ctx->mb) {
         cudaFree(b.d_pairs); cudaFreeHost(b.h_pairs); cudaFree(b.d_counts); cudaFree(b.d_offsets);
         cudaFreeHost(b.h_offsets); cudaFree(b.d_records); cudaFreeHost(b.h_records); cudaFree(b.d_fmats);
+        cudaFree(b.d_tpairs); cudaFreeHost(b.h_tpairs);
         if (b.ev_done) cudaEventDestroy(b.ev_done);
         if (b.ev_k0) cudaEventDestroy(b.ev_k0);
         if (b.ev_k1) cudaEventDestroy(b.ev_k1);
@@ -872,7 +1036,7 @@ void chgpu_destroy(chgpu_ctx* ctx) {
     }
     cudaFree(ctx->d_planes); cudaFree(ctx->d_centering); cudaFree(ctx->d_sums); cudaFree(ctx->d_res);
     cudaFree(ctx->d_stats); cudaFreeHost(ctx->h_stats); cudaFree(ctx->d_counter); cudaFree(ctx->d_slots);
-    cudaFree(ctx->d_dbg);
+    cudaFree(ctx->d_dbg); cudaFree(ctx->d_gmin); cudaFree(ctx->d_lists);
     cudaFree(ctx->d_planes_t); cudaFree(ctx->d_bias); cudaFree(ctx->d_hnorm); cudaFree(ctx->d_hq);
     cudaFree(ctx->d_hq_count); cudaFree(ctx->d_hstats);
     if (ctx->ev_upload) cudaEventDestroy(ctx->ev_upload);
@@ -1355,10 +1519,7 @@ chgpu_status chgpu_evict_image(chgpu_ctx* ctx, uint32_t image_id) {
     if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
     CK(cudaStreamSynchronize(ctx->copy));
     CK(cudaStreamSynchronize(ctx->compute));
-    ImageRec& r = ctx->images[slot];
-    ctx->arena.release(r.block, r.block_bytes);
-    r = ImageRec{};
-    ctx->free_slots.push_back(slot);
+    release_slot(ctx, slot);
     ctx->slot_of.erase(image_id);
     return CHGPU_OK;
 }
@@ -1398,11 +1559,13 @@ chgpu_status chgpu_hash_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32
         if (const chgpu_status s = find_slot(ctx, image_ids[i], &slots[i])) return s;
         max_n = std::max(max_n, ctx->images[slots[i]].dev.n);
     }
-    if (const chgpu_status s = ensure_slots_scratch(ctx, count)) return s;
+    // the images first (hash kernels), their tiles behind them (bucket build covers both)
+    const std::vector<uint32_t> all = with_tile_slots(ctx, slots);
+    if (const chgpu_status s = ensure_slots_scratch(ctx, all.size())) return s;
     if (const chgpu_status s = order_compute_after_copy(ctx)) return s;
     // d_slots is reused by successive calls; the pageable source is consumed synchronously
     CK(cudaStreamSynchronize(ctx->compute));
-    CK(cudaMemcpyAsync(ctx->d_slots, slots.data(), count * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->compute));
+    CK(cudaMemcpyAsync(ctx->d_slots, all.data(), all.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->compute));
     if (max_n) {
         if (ctx->hash_mode == CHGPU_HASH_FILTERED && ctx->filter_ready) {
             // fp32 filter + exact fixup, in launches of <= kHashBatchImages images (one queue per launch)
@@ -1417,11 +1580,11 @@ chgpu_status chgpu_hash_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32
                                  reduce_rounds, false));
         }
     }
-    if (const chgpu_status s = launch_bucket_build(ctx, count)) return s;
-    for (uint32_t i = 0; i < count; ++i) {
-        ImageRec& r = ctx->images[slots[i]];
+    if (const chgpu_status s = launch_bucket_build(ctx, uint32_t(all.size()))) return s;
+    for (const uint32_t sl : all) {
+        ImageRec& r = ctx->images[sl];
         r.dev.flags |= 1u;
-        ctx->h_images[slots[i]] = r.dev;
+        ctx->h_images[sl] = r.dev;
     }
     // flags live only on the host mirror and in the device table; kernels never read them, so
     // the table entries pushed at upload time stay valid.
@@ -1454,14 +1617,17 @@ chgpu_status chgpu_upload_codes(chgpu_ctx* ctx, uint32_t image_id, const uint32_
     if (const chgpu_status s = order_copy_after_compute(ctx)) return s;
     if (const chgpu_status s = h2d(ctx, r.dev.shorts, shorts, size_t(n) * L * 4)) return s;
     if (const chgpu_status s = h2d(ctx, r.dev.longs, longs, size_t(n) * 16)) return s;
-    if (const chgpu_status s = ensure_slots_scratch(ctx, 1)) return s;
+    const std::vector<uint32_t> all = with_tile_slots(ctx, std::vector<uint32_t>{slot});
+    if (const chgpu_status s = ensure_slots_scratch(ctx, all.size())) return s;
     if (const chgpu_status s = order_compute_after_copy(ctx)) return s;
     CK(cudaStreamSynchronize(ctx->compute));
-    CK(cudaMemcpyAsync(ctx->d_slots, &slot, sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->compute));
-    if (const chgpu_status s = launch_bucket_build(ctx, 1)) return s;
+    CK(cudaMemcpyAsync(ctx->d_slots, all.data(), all.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->compute));
+    if (const chgpu_status s = launch_bucket_build(ctx, uint32_t(all.size()))) return s;
     CK(cudaStreamSynchronize(ctx->compute));
-    r.dev.flags |= 1u;
-    ctx->h_images[slot] = r.dev;
+    for (const uint32_t sl : all) {
+        ctx->images[sl].dev.flags |= 1u;
+        ctx->h_images[sl] = ctx->images[sl].dev;
+    }
     return CHGPU_OK;
 }
 

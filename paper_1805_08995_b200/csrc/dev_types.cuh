@@ -36,9 +36,11 @@ struct DevImage {
 };
 
 struct PairDesc {
-    uint32_t slot_i;   // query image
-    uint32_t slot_j;   // train image
-    uint64_t res_off;  // first entry of this pair in the per-query result scratch
+    uint32_t slot_i;     // query image
+    uint32_t slot_j;     // train image, or one id-range tile of a large train image (see match_kernels.cuh)
+    uint64_t res_off;    // first entry of this pair in the per-query result scratch
+    uint32_t tile_base;  // tiles: first point id of the tile inside its image
+    uint32_t tile_idx;   // tiles: position of the tile's list in the per-query list scratch
 };
 
 struct DevStats {

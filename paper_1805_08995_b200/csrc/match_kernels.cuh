@@ -95,7 +95,24 @@ struct MatchParams {
     double band_px;             // GUIDED: epipolar band half-width in pixels
     uint32_t* dbg_ranked;       // optional: n_i x top_k
     uint32_t* dbg_count;        // optional: n_i
+    // tiled train images (MODE 1 / 2 and tile_merge_kernel)
+    uint32_t* gmin;             // per query (res indexing): smallest key over all tiles
+    uint32_t* lists;            // per query: list_stride keys, tile t's top_k keys at [t * top_k, (t + 1) * top_k)
+    uint32_t list_stride;
+    uint32_t tile_points;       // point ids per tile
 };
+
+// Train images too large for the shared-memory tile are matched tile by tile: every id range of
+// tile_points points is a small train image of its own (own bucket index over local ids, built by the
+// same bucket_build_kernel on a slice of the codes), so the kernel below runs unchanged on (query image,
+// tile) pairs and only its output differs:
+//   MODE 1 (kTileMin)   scan only: the smallest key of the tile joins gmin[query] (atomicMin).  Most queries
+//                       have no candidate within tau in any tile and are finished after this pass.
+//   MODE 2 (kTileTopK)  queries with gmin within tau: the tile's top_k smallest distinct keys, no threshold,
+//                       global point ids, go to lists[query][tile].
+// tile_merge_kernel then merges the lists of a query, applies the threshold / re-rank rule of
+// matcher.cpp:176-189 to the merged ranking and verifies it exactly like MODE 0 does.
+constexpr int kModeMatch = 0, kModeTileMin = 1, kModeTileTopK = 2;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -282,9 +299,52 @@ __device__ __forceinline__ uint32_t band_filter(uint32_t key, const EpiLine& l, 
     return d > band_px ? kNone : key;
 }
 
+// Verification of a ranked list (euclidean_verify, matcher.cpp:115-137): lane r holds the r-th ranked key
+// (id in the low 24 bits), n >= 2 entries.  kVerifyLanes lanes per candidate row (128 / kVerifyLanes bytes
+// each), 32 / kVerifyLanes rows per round; exact u32 squared distances; best = smallest d^2 with ties to the
+// earlier rank (strict '<' in the reference loop); Lowe ratio in fp64 with the reference's operand order.
+__device__ __forceinline__ bool verify_ranked(const uint8_t* __restrict__ desc_i, const uint8_t* __restrict__ desc_j,
+                                              uint32_t q, uint32_t n, uint32_t mykey, uint32_t lane, double ratio_sq,
+                                              uint32_t& out_t, uint32_t& out_d) {
+    constexpr uint32_t FULL = 0xffffffffu;
+    constexpr uint32_t VL = kVerifyLanes, ROWS = 32u / VL, PIECES = 8u / VL;
+    const uint32_t part = lane % VL, cand = lane / VL;
+    const uint4* __restrict__ qrow = reinterpret_cast<const uint4*>(desc_i + uint64_t(q) * kDim) + part * PIECES;
+    uint4 qa[PIECES];
+#pragma unroll
+    for (uint32_t w = 0; w < PIECES; ++w) qa[w] = __ldg(qrow + w);
+    uint32_t mydist = kNone;
+    for (uint32_t j0 = 0; j0 < n; j0 += ROWS) {
+        const uint32_t jj = min(j0 + cand, n - 1);
+        const uint32_t cid = __shfl_sync(FULL, mykey, jj) & 0xffffffu;
+        const uint4* __restrict__ trow = reinterpret_cast<const uint4*>(desc_j + uint64_t(cid) * kDim) + part * PIECES;
+        uint32_t s = 0;
+#pragma unroll
+        for (uint32_t w = 0; w < PIECES; ++w) {
+            const uint4 ta = __ldg(trow + w);
+            s += sqdiff4(qa[w].x, ta.x) + sqdiff4(qa[w].y, ta.y) + sqdiff4(qa[w].z, ta.z) + sqdiff4(qa[w].w, ta.w);
+        }
+#pragma unroll
+        for (uint32_t d = 1; d < VL; d <<= 1) s += __shfl_xor_sync(FULL, s, d);
+        const uint32_t v = __shfl_sync(FULL, s, ((lane - j0) % ROWS) * VL);
+        if (lane >= j0 && lane < j0 + ROWS && lane < n) mydist = v;
+    }
+    const uint32_t packed = lane < n ? ((mydist << 8) | lane) : kNone;
+    const uint32_t bestp = __reduce_min_sync(FULL, packed);
+    const uint32_t bl = bestp & 0xffu, best = bestp >> 8;
+    const uint32_t second = __reduce_min_sync(FULL, (lane < n && lane != bl) ? mydist : kNone);
+    const uint32_t bid = __shfl_sync(FULL, mykey, bl) & 0xffffffu;
+    if (second != 0u && double(best) < __dmul_rn(ratio_sq, double(second))) {
+        out_t = bid;
+        out_d = best;
+        return true;
+    }
+    return false;
+}
+
 // LT = number of table slots unrolled in registers (>= L); EXACT: L == LT, no per-table guards;
 // GUIDED: the epipolar band filter above is applied to every candidate.
-template <bool SMEM_TRAIN, int LT, bool EXACT, bool GUIDED>
+template <bool SMEM_TRAIN, int LT, bool EXACT, bool GUIDED, int MODE = kModeMatch>
 __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchParams P) {
     extern __shared__ __align__(16) unsigned char s_raw[];  // [train codes | bucket offsets | lookup staging]
     __shared__ unsigned int s_unit;
@@ -352,7 +412,8 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
         uint32_t st_raw = 0, st_vq = 0, st_dist = 0, st_match = 0;
 
         if (J.n == 0) {
-            for (uint32_t q = q0 + tid; q < q1; q += kMatchThreads) __stcs(P.res + pd.res_off + q, make_uint2(kNone, 0u));
+            if (MODE == kModeMatch)
+                for (uint32_t q = q0 + tid; q < q1; q += kMatchThreads) __stcs(P.res + pd.res_off + q, make_uint2(kNone, 0u));
         } else {
             // ---- 1. bucket lookup, kBatch queries at a time, one query per lane -------------------
             // (matcher.cpp:164-169).  Lane i resolves the L table ranges of the warp's (base+i)-th query
@@ -360,7 +421,16 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
             // round trip for the query-side data is paid once per batch, not once per query.
             auto lookup_batch = [&](uint32_t qb) {
                 const uint32_t q = qb + lane * kWarps;
-                if (lane < kBatch && q < q1) {
+                bool live = lane < kBatch && q < q1;
+                if (MODE == kModeTileTopK && live && (__ldg(P.gmin + pd.res_off + q) >> 24) > P.tau) {
+                    // nothing within tau in any tile: the query is skipped (sentinel header, harmless ranges)
+                    const uint32_t rec = s_stage + lane * kRec;
+                    sts128(rec + 16u, make_uint4(kNone, 0u, 0u, 0u));
+#pragma unroll
+                    for (int t = 0; t < LT; ++t) sts64(rec + 32u + t * 8u, 0u, 0u);
+                    live = false;
+                }
+                if (live) {
                     const uint32_t* __restrict__ qcodes = I.shorts + uint64_t(q) * L;
                     const uint32_t rec = s_stage + lane * kRec;
                     sts128(rec, __ldg(I.longs + q));
@@ -397,7 +467,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     }
                     const uint32_t base1 = __popc(m0), base2 = base1 + __popc(m1);
                     sts128(rec + 16u, make_uint4(min(pre, 255u) | (empty << 8) | (base1 << 16) | (base2 << 24), m0, m1, m2));
-                    st_raw += total;  // per lane; reduced over the warp when the unit ends
+                    if (MODE != kModeTileTopK) st_raw += total;  // per lane; reduced over the warp when the unit ends
                 }
                 __syncwarp();
             };
@@ -435,7 +505,9 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                 EpiLine line{};
                 if (GUIDED) line = epipolar_band(P.fmats + uint64_t(pair) * 9, __ldg(I.kp + q));
 
-                if (tover <= 32u * kOverSlots) {
+                const bool skip = MODE == kModeTileTopK && hdr.x == kNone;  // nothing within tau in any tile
+                if (skip) {
+                } else if (tover <= 32u * kOverSlots) {
                     // ---- 2. Hamming scan: the first 32 entries of every bucket, one table per slot,
                     //         then the entries past 32 of all buckets flattened into the last slots
                     uint32_t key[KS];
@@ -477,7 +549,17 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     }
                     // ---- 3. ranking: pull straight out of the slots -------------------------------
                     const uint32_t k0 = first_key(key, kNone);
-                    if ((k0 >> 24) <= P.tau) {
+                    if (MODE == kModeTileMin) {
+                        if (lane == 0 && k0 != kNone) atomicMin(P.gmin + pd.res_off + q, k0);
+                    } else if (MODE == kModeTileTopK) {
+                        // the tile's top_k smallest distinct keys, whatever their distance
+                        uint32_t prev = k0;
+                        while (prev != kNone) {
+                            if (lane == n) mykey = prev;
+                            if (++n == P.top_k) break;
+                            prev = next_key(key, kNone, prev);
+                        }
+                    } else if ((k0 >> 24) <= P.tau) {
                         if (lane == 0) mykey = k0;
                         n = 1;
                         uint32_t prev = k0, nk = kNone;
@@ -512,7 +594,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     });
                     // pass 1: smallest and largest key only — most queries have nothing within tau
                     uint32_t lmin = kNone, lmax = 0;
-                    for (uint32_t off = 0; off < maxlen; off += 32u) {
+                    for (uint32_t off = 0; MODE != kModeTileTopK && off < maxlen; off += 32u) {
 #pragma unroll
                         for (int t = 0; t < LT; ++t)
                             if (off < len[t]) {
@@ -524,7 +606,9 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                             }
                     }
                     const uint32_t gmin = __reduce_min_sync(FULL, lmin);
-                    if ((gmin >> 24) <= P.tau) {
+                    if (MODE == kModeTileMin) {
+                        if (lane == 0 && gmin != kNone) atomicMin(P.gmin + pd.res_off + q, gmin);
+                    } else if (MODE == kModeTileTopK || (gmin >> 24) <= P.tau) {
                         // pass 2: merge every round into the running top-k (ascending, unique)
                         const bool anycut = (__reduce_max_sync(FULL, lmax) >> 24) > P.tau;
                         for (uint32_t off = 0; off < maxlen; off += 32u) {
@@ -553,55 +637,25 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                         // thresholded size s, unique total (<= k); fallback rule as in the single-round path
                         const uint32_t tot = __popc(__ballot_sync(FULL, mykey != kNone));
                         const uint32_t s = __popc(__ballot_sync(FULL, mykey != kNone && (mykey >> 24) <= P.tau));
-                        n = (s >= P.min_ranked || !anycut) ? s : tot;
+                        n = (MODE != kModeTileTopK && (s >= P.min_ranked || !anycut)) ? s : tot;
                     }
                 }
 
-                if (P.dbg_ranked != nullptr) {
+                if (MODE == kModeTileTopK && !skip && lane < P.top_k)
+                    P.lists[(pd.res_off + q) * P.list_stride + pd.tile_idx * P.top_k + lane] = lane < n ? mykey + pd.tile_base : kNone;
+
+                if (MODE == kModeMatch && P.dbg_ranked != nullptr) {
                     if (lane < n) P.dbg_ranked[uint64_t(q) * P.top_k + lane] = mykey & 0xffffffu;
                     if (lane == 0) P.dbg_count[q] = n;
                 }
 
                 // ---- 4. verification (euclidean_verify, matcher.cpp:115-137) ------------------
-                if (n >= 2) {
+                if (MODE == kModeMatch && n >= 2) {
                     st_vq += 1;
                     st_dist += n;
-                    // kVerifyLanes lanes per candidate row (128 / kVerifyLanes bytes each), 32 / kVerifyLanes rows per round
-                    constexpr uint32_t VL = kVerifyLanes, ROWS = 32u / VL, PIECES = 8u / VL;
-                    const uint32_t part = lane % VL, cand = lane / VL;
-                    const uint4* __restrict__ qrow = reinterpret_cast<const uint4*>(I.desc + uint64_t(q) * kDim) + part * PIECES;
-                    uint4 qa[PIECES];
-#pragma unroll
-                    for (uint32_t w = 0; w < PIECES; ++w) qa[w] = __ldg(qrow + w);
-                    uint32_t mydist = kNone;
-                    for (uint32_t j0 = 0; j0 < n; j0 += ROWS) {
-                        const uint32_t jj = min(j0 + cand, n - 1);
-                        const uint32_t cid = __shfl_sync(FULL, mykey, jj) & 0xffffffu;
-                        const uint4* __restrict__ trow = reinterpret_cast<const uint4*>(J.desc + uint64_t(cid) * kDim) + part * PIECES;
-                        uint32_t s = 0;
-#pragma unroll
-                        for (uint32_t w = 0; w < PIECES; ++w) {
-                            const uint4 ta = __ldg(trow + w);
-                            s += sqdiff4(qa[w].x, ta.x) + sqdiff4(qa[w].y, ta.y) + sqdiff4(qa[w].z, ta.z) + sqdiff4(qa[w].w, ta.w);
-                        }
-#pragma unroll
-                        for (uint32_t d = 1; d < VL; d <<= 1) s += __shfl_xor_sync(FULL, s, d);
-                        const uint32_t v = __shfl_sync(FULL, s, ((lane - j0) % ROWS) * VL);
-                        if (lane >= j0 && lane < j0 + ROWS && lane < n) mydist = v;
-                    }
-                    // best = smallest d^2, ties to the earlier rank (strict '<' in the reference loop)
-                    const uint32_t packed = lane < n ? ((mydist << 8) | lane) : kNone;
-                    const uint32_t bestp = __reduce_min_sync(FULL, packed);
-                    const uint32_t bl = bestp & 0xffu, best = bestp >> 8;
-                    const uint32_t second = __reduce_min_sync(FULL, (lane < n && lane != bl) ? mydist : kNone);
-                    const uint32_t bid = __shfl_sync(FULL, mykey, bl) & 0xffffffu;
-                    if (second != 0u && double(best) < __dmul_rn(P.ratio_sq, double(second))) {
-                        out_t = bid;
-                        out_d = best;
-                        st_match += 1;
-                    }
+                    if (verify_ranked(I.desc, J.desc, q, n, mykey, lane, P.ratio_sq, out_t, out_d)) st_match += 1;
                 }
-                if (lane == 0) __stcs(P.res + pd.res_off + q, make_uint2(out_t, out_d));
+                if (MODE == kModeMatch && lane == 0) __stcs(P.res + pd.res_off + q, make_uint2(out_t, out_d));
 
                 // batch boundary: resolve the next kBatch queries (this one's ranges are in registers)
                 if (slot == kBatch - 1 && q + kWarps < q1) {
@@ -620,6 +674,67 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
             if (st_match) atomicAdd(&P.pair_counts[pair], st_match);
         }
         __syncthreads();  // all warps done with the train tile / s_unit before the next unit
+    }
+}
+
+// Merge + verification for tiled train images: one warp per query of the pair.  The query's T lists
+// (T = tiles of the train image, top_k keys each, global ids, kNone padded) are merged 32 entries at a time
+// into the ascending, duplicate-free top_k — the ranked list the reference builds over the whole image —
+// then cut by the threshold / re-rank rule (matcher.cpp:176-189) and verified (matcher.cpp:106-137).
+// Whether the threshold cut anything can be read off the lists: a tile with a candidate beyond tau that is
+// not in its list has a full list within tau, and then the merged ranking is full as well.
+constexpr int kMergeThreads = 256;
+constexpr uint32_t kMergeChunk = 1024;  // queries per CTA
+template <int kInstance>
+__global__ void __launch_bounds__(kMergeThreads) tile_merge_kernel(const MatchParams P) {
+    constexpr uint32_t FULL = 0xffffffffu;
+    const uint32_t pair = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const PairDesc pd = P.pairs[pair];
+    const DevImage I = P.images[pd.slot_i];
+    const DevImage J = P.images[pd.slot_j];
+    const uint32_t q0 = blockIdx.y * kMergeChunk, q1 = min(I.n, q0 + kMergeChunk);
+    const uint32_t entries = ((J.n + P.tile_points - 1) / P.tile_points) * P.top_k;
+    uint32_t st_vq = 0, st_dist = 0, st_match = 0;
+    for (uint32_t q = q0 + warp; q < q1; q += kMergeThreads / 32) {
+        uint32_t out_t = kNone, out_d = 0, n = 0, mykey = kNone;
+        if ((__ldg(P.gmin + pd.res_off + q) >> 24) <= P.tau) {
+            const uint32_t* __restrict__ list = P.lists + (pd.res_off + q) * P.list_stride;
+            bool cut = false;
+            for (uint32_t e0 = 0; e0 < entries; e0 += 32) {
+                uint32_t key[1];
+                key[0] = e0 + lane < entries ? __ldg(list + e0 + lane) : kNone;
+                cut |= key[0] != kNone && (key[0] >> 24) > P.tau;
+                const uint32_t kth = __shfl_sync(FULL, mykey, P.top_k - 1);
+                uint32_t prev = __reduce_min_sync(FULL, key[0]);
+                if (prev > kth) continue;
+                const uint32_t old = mykey;
+                prev = min(prev, __shfl_sync(FULL, old, 0));
+                mykey = kNone;
+                for (uint32_t r = 0; r < P.top_k && prev != kNone; ++r) {
+                    if (lane == r) mykey = prev;
+                    prev = next_key(key, old, prev);
+                }
+            }
+            const bool anycut = __any_sync(FULL, cut);
+            const uint32_t tot = __popc(__ballot_sync(FULL, mykey != kNone));
+            const uint32_t s = __popc(__ballot_sync(FULL, mykey != kNone && (mykey >> 24) <= P.tau));
+            n = (s >= P.min_ranked || !anycut) ? s : tot;
+        }
+        if (P.dbg_ranked != nullptr) {
+            if (lane < n) P.dbg_ranked[uint64_t(q) * P.top_k + lane] = mykey & 0xffffffu;
+            if (lane == 0) P.dbg_count[q] = n;
+        }
+        if (n >= 2) {
+            st_vq += 1;
+            st_dist += n;
+            if (verify_ranked(I.desc, J.desc, q, n, mykey, lane, P.ratio_sq, out_t, out_d)) st_match += 1;
+        }
+        if (lane == 0) __stcs(P.res + pd.res_off + q, make_uint2(out_t, out_d));
+    }
+    if (lane == 0) {
+        if (st_vq) atomicAdd(&P.stats->verified_queries, (unsigned long long)st_vq);
+        if (st_dist) atomicAdd(&P.stats->distances, (unsigned long long)st_dist);
+        if (st_match) atomicAdd(&P.pair_counts[pair], st_match);
     }
 }
 

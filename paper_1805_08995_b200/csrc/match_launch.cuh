@@ -14,12 +14,16 @@ cudaError_t launch_match_global(const MatchParams& P, size_t smem, int sm_count,
 // Epipolar-guided instantiations (match_guided.cu): L == 6 exact, any other L through the LT = 8 generic.
 cudaError_t launch_match_guided(const MatchParams& P, bool smem_train, size_t smem, int sm_count, cudaStream_t stream,
                                 uint32_t* grid);
+// Tiled train images (match_tiled.cu): mode = kModeTileMin / kModeTileTopK over (query image, tile) pairs with the
+// tile's codes in shared memory, then the per-query merge + verification over the original pairs.
+cudaError_t launch_match_tiled(const MatchParams& P, int mode, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid);
+cudaError_t launch_tile_merge(const MatchParams& P, uint32_t npairs, uint32_t max_nq, cudaStream_t stream);
 // Table slots (LT) the launchers pick for L tables; the staging area is sized with it.
 inline int match_table_slots(uint32_t L, bool guided) { return guided ? (L == 6 ? 6 : 8) : (L <= 4 ? 4 : (L <= 6 ? 6 : 8)); }
 
-template <bool SMEM, int LT, bool EXACT, bool GUIDED = false>
+template <bool SMEM, int LT, bool EXACT, bool GUIDED = false, int MODE = kModeMatch>
 cudaError_t launch_match_variant(const MatchParams& P, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid_out) {
-    auto kfn = match_kernel<SMEM, LT, EXACT, GUIDED>;
+    auto kfn = match_kernel<SMEM, LT, EXACT, GUIDED, MODE>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;

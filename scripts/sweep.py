@@ -50,11 +50,19 @@ def run(m, n, shape, images=64, guided=False, reps=2):
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--points", type=int, nargs="*", default=[1024, 2048, 4096, 8192, 12288, 16384, 32768])
+    ap.add_argument("--shapes", nargs="*", default=["uniform", "sift"])
+    ap.add_argument("--images", type=int, default=64)
+    ap.add_argument("--no-guided", action="store_true")
+    args = ap.parse_args()
     with ch.Matcher(0) as m:
-        for shape in ("uniform", "sift"):
-            for n in (1024, 2048, 4096, 8192, 12288, 16384, 32768):
-                print(json.dumps(run(m, n, shape)), flush=True)
-        print(json.dumps(run(m, 8192, "uniform", guided=True)), flush=True)
+        for shape in args.shapes:
+            for n in args.points:
+                print(json.dumps(run(m, n, shape, images=args.images)), flush=True)
+        if not args.no_guided:
+            print(json.dumps(run(m, 8192, "uniform", guided=True)), flush=True)
 
 
 if __name__ == "__main__":
