@@ -308,8 +308,7 @@ def run_ours(args):
         for i in range(args.images):
             m.upload(i, desc[i])
         m.centering_reset()
-        for i in range(args.images):
-            m.centering_add(i)
+        m.centering_add_many(ids)
         m.centering_apply()
         m.hash(ids)
 
@@ -372,7 +371,7 @@ def run_ours(args):
     roofline["on_chip"] = {"bound": "xu_popc", "achieved_gpopc_s": popc_rate / 1e9, "peak_gpopc_s": popc_peak / 1e9,
                            "frac": popc_rate / popc_peak,
                            "note": "lower bound on POPC work (padding lanes not counted); ncu pipe utilisations of the "
-                                   "committed capture: profiles/r01h_match_kernel_ncu_full.json"}
+                                   "committed capture: profiles/r01k_match_kernel_ncu_full.json"}
 
     # ---- e2e: host buffers in, host records out, every step ------------------------------------------
     e2e = None

@@ -124,6 +124,8 @@ chgpu_status chgpu_set_family(chgpu_ctx* ctx, const chgpu_family_params* p,
 /* Replaces set_centering / CenteringAccumulator (hashing.hpp:78,166-172; hashing.cpp:52-70). */
 chgpu_status chgpu_centering_reset(chgpu_ctx* ctx);
 chgpu_status chgpu_centering_add_image(chgpu_ctx* ctx, uint32_t image_id);
+/* Batch form of chgpu_centering_add_image: one launch over the listed resident images. */
+chgpu_status chgpu_centering_add_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32_t count);
 chgpu_status chgpu_centering_get_sums(chgpu_ctx* ctx, uint64_t* sums128, uint64_t* count);
 chgpu_status chgpu_centering_add_sums(chgpu_ctx* ctx, const uint64_t* sums128, uint64_t count);
 chgpu_status chgpu_centering_apply(chgpu_ctx* ctx, double* centering128_out /* nullable */);

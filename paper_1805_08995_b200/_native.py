@@ -94,6 +94,7 @@ SIGNATURES = {
     "chgpu_set_family": (C.c_int, [C.c_void_p, C.POINTER(FamilyParamsC), f64p, f64p]),
     "chgpu_centering_reset": (C.c_int, [C.c_void_p]),
     "chgpu_centering_add_image": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "chgpu_centering_add_images": (C.c_int, [C.c_void_p, u32p, C.c_uint32]),
     "chgpu_centering_get_sums": (C.c_int, [C.c_void_p, u64p, u64p]),
     "chgpu_centering_add_sums": (C.c_int, [C.c_void_p, u64p, C.c_uint64]),
     "chgpu_centering_apply": (C.c_int, [C.c_void_p, f64p]),

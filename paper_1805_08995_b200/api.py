@@ -331,6 +331,10 @@ class Matcher:
     def centering_add(self, image_id: int):
         self._ck(self.lib.chgpu_centering_add_image(self.h, image_id))
 
+    def centering_add_many(self, image_ids):
+        ids = np.ascontiguousarray(image_ids, dtype=np.uint32)
+        self._ck(self.lib.chgpu_centering_add_images(self.h, ids.ctypes.data_as(N.u32p), len(ids)))
+
     def centering_sums(self) -> tuple[np.ndarray, int]:
         sums = np.zeros(128, dtype=np.uint64)
         cnt = C.c_uint64(0)

@@ -1161,6 +1161,33 @@ chgpu_status chgpu_centering_add_image(chgpu_ctx* ctx, uint32_t image_id) {
     return CHGPU_OK;
 }
 
+chgpu_status chgpu_centering_add_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32_t count) {
+    if (!ctx || (count && !image_ids)) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    if (count == 0) return CHGPU_OK;
+    std::vector<uint32_t> slots(count);
+    uint64_t points = 0;
+    uint32_t max_n = 0;
+    for (uint32_t i = 0; i < count; ++i) {
+        if (const chgpu_status s = find_slot(ctx, image_ids[i], &slots[i])) return s;
+        points += ctx->images[slots[i]].dev.n;
+        max_n = std::max(max_n, ctx->images[slots[i]].dev.n);
+    }
+    if (max_n == 0) return CHGPU_OK;
+    if (const chgpu_status s = ensure_slots_scratch(ctx, count)) return s;
+    if (const chgpu_status s = order_compute_after_copy(ctx)) return s;
+    CK(cudaStreamSynchronize(ctx->compute));  // d_slots is reused by successive calls
+    CK(cudaMemcpyAsync(ctx->d_slots, slots.data(), count * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->compute));
+    for (uint32_t first = 0; first < count; first += 65535u) {
+        const uint32_t cnt = std::min(65535u, count - first);
+        const dim3 grid(std::max(1u, std::min((max_n + 1023u) / 1024u, 16u)), cnt);
+        centering_sums_batch_kernel<<<grid, 256, 0, ctx->compute>>>(ctx->d_images, ctx->d_slots + first, ctx->d_sums);
+        CK(cudaGetLastError());
+    }
+    ctx->sum_count += points;
+    return CHGPU_OK;
+}
+
 chgpu_status chgpu_centering_get_sums(chgpu_ctx* ctx, uint64_t* sums128, uint64_t* count) {
     if (!ctx || !sums128 || !count) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);

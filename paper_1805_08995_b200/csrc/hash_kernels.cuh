@@ -53,6 +53,35 @@ __global__ void centering_sums_kernel(const uint8_t* __restrict__ desc, uint32_t
     if (threadIdx.x < kDim) atomicAdd(&sums[threadIdx.x], (unsigned long long)s_acc[threadIdx.x]);
 }
 
+// The same sums over a list of resident images in one launch: blockIdx.y = image, blockIdx.x = row slice.
+__global__ void centering_sums_batch_kernel(const DevImage* __restrict__ images, const uint32_t* __restrict__ slots,
+                                            unsigned long long* __restrict__ sums /*128*/) {
+    __shared__ unsigned int s_acc[kDim];
+    const DevImage img = images[slots[blockIdx.y]];
+    const uint32_t n = img.n;
+    const uint32_t rows_per_block = (n + gridDim.x - 1) / gridDim.x;   // <= 65536 rows: 255 * rows < 2^32
+    const uint32_t r0 = blockIdx.x * rows_per_block;
+    const uint32_t r1 = min(n, r0 + rows_per_block);
+    if (r0 >= r1) return;
+    if (threadIdx.x < kDim) s_acc[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    unsigned int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    for (uint32_t r = r0 + warp; r < r1; r += nwarps) {
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(img.desc + uint64_t(r) * kDim) + lane);
+        a0 += w & 0xff;
+        a1 += (w >> 8) & 0xff;
+        a2 += (w >> 16) & 0xff;
+        a3 += w >> 24;
+    }
+    atomicAdd(&s_acc[lane * 4 + 0], a0);
+    atomicAdd(&s_acc[lane * 4 + 1], a1);
+    atomicAdd(&s_acc[lane * 4 + 2], a2);
+    atomicAdd(&s_acc[lane * 4 + 3], a3);
+    __syncthreads();
+    if (threadIdx.x < kDim) atomicAdd(&sums[threadIdx.x], (unsigned long long)s_acc[threadIdx.x]);
+}
+
 // ---------------------------------------------------------------------------------------------
 // K1: hash codes.  One CTA = 64 points x all planes; 8 warps, each lane owns 2 points
 // (lane, lane+32) and each warp 2 planes of the current 16-plane chunk, so one pass of the

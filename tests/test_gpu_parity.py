@@ -165,6 +165,25 @@ def test_near_tie_projections_keep_their_sign(matcher, oracle, default_family):
     assert (np.abs(dots) < 1.0).sum() > 100, "sample must contain near-zero projections"
 
 
+def test_batched_centering_sums_equal_the_per_image_sums(matcher, oracle, default_family):
+    fresh(matcher, default_family)
+    sizes = [0, 1, 31, 1000, 4097, 20000]
+    d = [make_dataset(1, max(n, 1), seed=200 + n)[0][:n] for n in sizes]
+    for i, x in enumerate(d):
+        put(matcher, BASE + i, x)
+    ids = [BASE + i for i in range(len(d))]
+    matcher.centering_reset()
+    for i in ids:
+        matcher.centering_add(i)
+    one, cnt1 = matcher.centering_sums()
+    matcher.centering_reset()
+    matcher.centering_add_many(ids)
+    many, cnt2 = matcher.centering_sums()
+    assert cnt1 == cnt2 == sum(sizes) and np.array_equal(one, many)
+    assert np.array_equal(one, np.concatenate(d).astype(np.uint64).sum(axis=0))
+    assert np.array_equal(matcher.centering_apply(), oracle.centering([x for x in d if len(x)]))
+
+
 # ---- match vs oracle --------------------------------------------------------------------------------
 def run_pair_case(matcher, oracle, fam, desc_i, desc_j, cfgs, ids=(BASE, BASE + 1)):
     cen = oracle.centering([desc_i, desc_j]) if len(desc_i) + len(desc_j) else np.zeros(128)
