@@ -23,7 +23,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -77,8 +79,17 @@ struct Arena {
                 live_bytes += bytes;
                 return cudaSuccess;
             }
-        Slab s{nullptr, std::max(kSlabBytes, bytes), 0};
-        const cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&s.base), s.size);
+        // cudaMalloc drains the device before it returns, so a stream of uploads should meet it rarely: slabs
+        // double in size (256 MiB ... 8 GiB); a slab the device cannot give is retried at the minimum size.
+        size_t want = kSlabBytes;
+        if (!slabs.empty()) want = std::min(slabs.back().size * 2, size_t(8) << 30);
+        Slab s{nullptr, std::max(want, bytes), 0};
+        cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&s.base), s.size);
+        if (e != cudaSuccess && s.size > std::max(kSlabBytes, bytes)) {
+            cudaGetLastError();
+            s.size = std::max(kSlabBytes, bytes);
+            e = cudaMalloc(reinterpret_cast<void**>(&s.base), s.size);
+        }
         if (e != cudaSuccess) return e;
         s.used = bytes;
         *out = s.base;
@@ -187,6 +198,10 @@ struct chgpu_ctx {
     size_t slots_cap = 0;
     uint32_t* d_dbg = nullptr;
     size_t dbg_cap = 0;
+    // streaming loader: pinned ring buffers and device staging, kept between calls
+    char* load_pinned = nullptr;       // one region cut into load_pinned_slots slots of load_pinned_slot bytes
+    size_t load_pinned_slot = 0, load_pinned_slots = 0;
+    std::vector<std::pair<char*, size_t>> load_scratch;
     uint64_t sub_batch_queries = kSubBatchQueries;
 };
 
@@ -1037,6 +1052,8 @@ void chgpu_destroy(chgpu_ctx* ctx) {
     cudaFree(ctx->d_planes); cudaFree(ctx->d_centering); cudaFree(ctx->d_sums); cudaFree(ctx->d_res);
     cudaFree(ctx->d_stats); cudaFreeHost(ctx->h_stats); cudaFree(ctx->d_counter); cudaFree(ctx->d_slots);
     cudaFree(ctx->d_dbg); cudaFree(ctx->d_gmin); cudaFree(ctx->d_lists);
+    cudaFreeHost(ctx->load_pinned);
+    for (auto& b : ctx->load_scratch) cudaFree(b.first);
     cudaFree(ctx->d_planes_t); cudaFree(ctx->d_bias); cudaFree(ctx->d_hnorm); cudaFree(ctx->d_hq);
     cudaFree(ctx->d_hq_count); cudaFree(ctx->d_hstats);
     if (ctx->ev_upload) cudaEventDestroy(ctx->ev_upload);
@@ -1295,10 +1312,17 @@ chgpu_status chgpu_upload_chft(chgpu_ctx* ctx, uint32_t image_id, const void* bl
 // ---- streaming loader: disk -> pinned ring -> HBM ---------------------------------------------------
 namespace {
 
+// Every slot has its own lock and condition variables: the issue thread wakes exactly the reader that waits for
+// the slot it frees, and a reader wakes only the issue thread (one shared condition variable made every hand-off
+// wake all readers, which capped the loader far below the copy engine's rate).
 struct LoadSlot {
+    std::mutex mu;
+    std::condition_variable cv_free;   // a reader waits here for its turn
+    std::condition_variable cv_ready;  // the issue thread waits here for the file
     enum State { Free, Filling, Ready } state = Free;
-    char* buf = nullptr;   // pinned
+    char* buf = nullptr;   // pinned: a share of the context's region, or its own buffer (own) after outgrowing it
     size_t cap = 0;
+    bool own = false;
     size_t bytes = 0;      // bytes read
     bool missing = false;  // fopen failed
     uint32_t file = 0;     // index of the file it holds (valid in Ready)
@@ -1308,9 +1332,9 @@ struct LoadSlot {
 };
 
 struct LoadRing {
-    std::mutex mu;
-    std::condition_variable cv;
-    std::vector<LoadSlot> slots;
+    std::mutex mu;  // statistics only
+    std::unique_ptr<LoadSlot[]> slots;
+    size_t nslots = 0;
     std::atomic<uint32_t> next{0};
     std::atomic<bool> abort{false};
     double read_seconds = 0.0;
@@ -1320,7 +1344,7 @@ struct LoadRing {
 // Reader thread: claims file indices in order; file i travels through slot i % S once the slot's previous
 // tenant (file i - S) has been copied to the device.
 void loader_thread(LoadRing* ring, const char* const* paths, uint32_t count) {
-    const size_t S = ring->slots.size();
+    const size_t S = ring->nslots;
     double seconds = 0.0;
     uint64_t bytes = 0;
     for (;;) {
@@ -1328,9 +1352,9 @@ void loader_thread(LoadRing* ring, const char* const* paths, uint32_t count) {
         if (i >= count || ring->abort.load()) break;
         LoadSlot& s = ring->slots[i % S];
         {
-            std::unique_lock<std::mutex> lock(ring->mu);
+            std::unique_lock<std::mutex> lock(s.mu);
             // slots are handed out in file order: wait until it is free AND it is this file's turn
-            ring->cv.wait(lock, [&] { return ring->abort.load() || (s.state == LoadSlot::Free && s.turn == i); });
+            s.cv_free.wait(lock, [&] { return ring->abort.load() || (s.state == LoadSlot::Free && s.turn == i); });
             if (ring->abort.load()) break;
             s.state = LoadSlot::Filling;
         }
@@ -1345,13 +1369,18 @@ void loader_thread(LoadRing* ring, const char* const* paths, uint32_t count) {
             const long sz = std::ftell(f);
             std::fseek(f, 0, SEEK_SET);
             const size_t need = sz > 0 ? size_t(sz) : 0;
-            if (need > s.cap) {  // grow this slot's pinned buffer (rare: sized by the largest file seen)
-                if (s.buf) cudaFreeHost(s.buf);
+            if (need > s.cap) {  // a file larger than the slots were sized for: private pinned buffer for this slot
+                if (s.own) cudaFreeHost(s.buf);
                 s.buf = nullptr;
                 s.cap = 0;
+                s.own = false;
                 const size_t cap = std::max<size_t>(need + need / 8, size_t(2) << 20);
-                if (cudaMallocHost(reinterpret_cast<void**>(&s.buf), cap) == cudaSuccess) s.cap = cap;
-                else cudaGetLastError();
+                if (cudaMallocHost(reinterpret_cast<void**>(&s.buf), cap) == cudaSuccess) {
+                    s.cap = cap;
+                    s.own = true;
+                } else {
+                    cudaGetLastError();
+                }
             }
             if (need <= s.cap && need) s.bytes = std::fread(s.buf, 1, need, f);
             std::fclose(f);
@@ -1359,11 +1388,11 @@ void loader_thread(LoadRing* ring, const char* const* paths, uint32_t count) {
         seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         bytes += s.bytes;
         {
-            std::lock_guard<std::mutex> lock(ring->mu);
+            std::lock_guard<std::mutex> lock(s.mu);
             s.file = i;
             s.state = LoadSlot::Ready;
         }
-        ring->cv.notify_all();
+        s.cv_ready.notify_one();
     }
     std::lock_guard<std::mutex> lock(ring->mu);
     ring->read_seconds += seconds;
@@ -1385,59 +1414,106 @@ chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, con
         return CHGPU_OK;
     }
     io_threads = std::max<uint32_t>(1, std::min<uint32_t>(io_threads ? io_threads : 4, 64));
-    const size_t S = std::max<size_t>(4, 2 * size_t(io_threads));
+    const size_t S = std::max<size_t>(8, 2 * size_t(io_threads));
+    // Pinned ring buffers and device staging live in the context: cudaMallocHost / cudaMalloc cost milliseconds
+    // and take the driver lock, so they are sized up front (first file + 12 %) on this thread and only a later,
+    // larger file makes a reader grow its slot.
+    size_t guess = size_t(2) << 20;
+    if (FILE* f0 = std::fopen(paths[0], "rb")) {
+        std::fseek(f0, 0, SEEK_END);
+        const long sz = std::ftell(f0);
+        std::fclose(f0);
+        if (sz > 0) guess = std::max(guess, size_t(sz) + size_t(sz) / 8);
+    }
+    guess = align_up(guess, 4096);
+    if (ctx->load_pinned_slots < S || ctx->load_pinned_slot < guess) {
+        cudaFreeHost(ctx->load_pinned);
+        ctx->load_pinned = nullptr;
+        ctx->load_pinned_slots = ctx->load_pinned_slot = 0;
+        if (cudaMallocHost(reinterpret_cast<void**>(&ctx->load_pinned), S * guess) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, CHGPU_ENOMEM, "loader: %zu bytes of pinned staging", S * guess);
+        }
+        ctx->load_pinned_slots = S;
+        ctx->load_pinned_slot = guess;
+    }
     LoadRing ring;
-    ring.slots.resize(S);
+    ring.slots.reset(new LoadSlot[S]);
+    ring.nslots = S;
     for (size_t k = 0; k < S; ++k) {
+        ring.slots[k].buf = ctx->load_pinned + k * ctx->load_pinned_slot;
+        ring.slots[k].cap = ctx->load_pinned_slot;
         ring.slots[k].turn = uint32_t(k);  // slot k serves files k, k + S, k + 2 S, ...
         if (cudaEventCreateWithFlags(&ring.slots[k].copied, cudaEventDisableTiming) != cudaSuccess)
             return fail(ctx, CHGPU_ECUDA, "loader: event creation failed");
     }
-    // device-side raw (AoS) scratch, double buffered; grown to the largest file
+    // device-side raw (AoS) scratch ring: deep enough that waiting for a split kernel never stalls the issue loop
+    constexpr size_t kScratch = 8;
     struct Scratch {
         char* ptr = nullptr;
         size_t cap = 0;
         cudaEvent_t split_done = nullptr;
         bool used = false;
-    } scratch[2];
-    for (Scratch& sc : scratch) cudaEventCreateWithFlags(&sc.split_done, cudaEventDisableTiming);
+    } scratch[kScratch];
+    if (ctx->load_scratch.size() < kScratch) ctx->load_scratch.resize(kScratch, {nullptr, 0});
+    for (size_t k = 0; k < kScratch; ++k) {
+        scratch[k].ptr = ctx->load_scratch[k].first;
+        scratch[k].cap = ctx->load_scratch[k].second;
+        cudaEventCreateWithFlags(&scratch[k].split_done, cudaEventDisableTiming);
+    }
+    uint32_t pub_lo = UINT32_MAX, pub_hi = 0;  // image-table range to publish when the batch is in
 
     const auto wall0 = std::chrono::steady_clock::now();
     std::vector<std::thread> readers;
     for (uint32_t t = 0; t < io_threads; ++t) readers.emplace_back(loader_thread, &ring, paths, count);
 
     chgpu_status rc = CHGPU_OK;
-    auto poll_copies = [&]() {  // slots whose H2D completed go back to the readers
-        bool freed = false;
-        std::lock_guard<std::mutex> lock(ring.mu);
-        for (LoadSlot& s : ring.slots)
-            if (s.in_flight && cudaEventQuery(s.copied) == cudaSuccess) {
+    std::deque<uint32_t> in_flight;  // files whose H2D was issued, oldest first (copies complete in this order)
+    auto poll_copies = [&]() {       // slots whose H2D completed go back to the readers
+        size_t done = 0;
+        while (done < in_flight.size() && cudaEventQuery(ring.slots[in_flight[done] % S].copied) == cudaSuccess) ++done;
+        for (size_t k = 0; k < done; ++k) {
+            LoadSlot& s = ring.slots[in_flight[k] % S];
+            {
+                std::lock_guard<std::mutex> lock(s.mu);
                 s.in_flight = false;
                 s.state = LoadSlot::Free;
                 s.turn = s.file + uint32_t(S);
-                freed = true;
             }
-        if (freed) ring.cv.notify_all();
+            s.cv_free.notify_one();
+        }
+        in_flight.erase(in_flight.begin(), in_flight.begin() + done);
+    };
+    const bool trace = getenv("CHGPU_LOADER_TRACE") != nullptr;
+    double t_wait = 0, t_alloc = 0, t_issue = 0;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto secs = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+        return std::chrono::duration<double>(b - a).count();
     };
     for (uint32_t i = 0; i < count && rc == CHGPU_OK; ++i) {
         LoadSlot& s = ring.slots[i % S];
+        const auto tw0 = now();
         {
-            std::unique_lock<std::mutex> lock(ring.mu);
+            std::unique_lock<std::mutex> lock(s.mu);
             while (!(s.state == LoadSlot::Ready && s.file == i)) {
                 lock.unlock();
                 poll_copies();
                 lock.lock();
                 if (s.state == LoadSlot::Ready && s.file == i) break;
-                ring.cv.wait_for(lock, std::chrono::microseconds(200));
+                s.cv_ready.wait_for(lock, std::chrono::microseconds(50));
             }
         }
+        const auto tw1 = now();
+        t_wait += secs(tw0, tw1);
         chgpu_file_result& r = results[i];
         r = chgpu_file_result{};
         auto release_slot = [&]() {
-            std::lock_guard<std::mutex> lock(ring.mu);
-            s.state = LoadSlot::Free;
-            s.turn = i + uint32_t(S);
-            ring.cv.notify_all();
+            {
+                std::lock_guard<std::mutex> lock(s.mu);
+                s.state = LoadSlot::Free;
+                s.turn = i + uint32_t(S);
+            }
+            s.cv_free.notify_one();
         };
         auto bad = [&](chgpu_file_fault f, uint64_t off) {
             r.status = CHGPU_EFORMAT;
@@ -1467,8 +1543,10 @@ chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, con
             continue;
         }
         ImageRec& img = ctx->images[slot_img];
+        const auto tw2 = now();
+        t_alloc += secs(tw1, tw2);
         if (n) {
-            Scratch& sc = scratch[i & 1];
+            Scratch& sc = scratch[i % kScratch];
             if (sc.used) cudaEventSynchronize(sc.split_done);  // its previous split kernel has consumed it
             if (sc.cap < raw_bytes) {
                 if (sc.ptr) cudaFree(sc.ptr);
@@ -1485,51 +1563,62 @@ chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, con
             }
             cudaMemcpyAsync(sc.ptr, s.buf + 16, raw_bytes, cudaMemcpyHostToDevice, ctx->copy);
             cudaEventRecord(s.copied, ctx->copy);
-            {
-                std::lock_guard<std::mutex> lock(ring.mu);
-                s.in_flight = true;
-            }
+            s.in_flight = true;
+            in_flight.push_back(i);
             cudaStreamWaitEvent(ctx->compute, s.copied, 0);
-            const uint32_t blocks = uint32_t(std::min<uint64_t>((uint64_t(n) * 9 + 255) / 256, 8u * ctx->prop.multiProcessorCount));
-            chft_split_kernel<<<blocks, 256, 0, ctx->compute>>>(reinterpret_cast<const uint4*>(sc.ptr), n,
-                                                               reinterpret_cast<uint4*>(const_cast<uint8_t*>(img.dev.desc)),
-                                                               reinterpret_cast<uint4*>(const_cast<float4*>(img.dev.kp)));
+            if (accumulate_centering) {  // one launch: AoS -> SoA split with the column sums folded in
+                const uint32_t blocks = std::max(1u, std::min((n + 127u) / 128u, 2u * uint32_t(ctx->prop.multiProcessorCount)));
+                chft_split_sums_kernel<<<blocks, kSplitSumThreads, 0, ctx->compute>>>(
+                    reinterpret_cast<const uint4*>(sc.ptr), n, reinterpret_cast<uint4*>(const_cast<uint8_t*>(img.dev.desc)),
+                    reinterpret_cast<uint4*>(const_cast<float4*>(img.dev.kp)), ctx->d_sums);
+                ctx->sum_count += n;
+            } else {
+                const uint32_t blocks = uint32_t(std::min<uint64_t>((uint64_t(n) * 9 + 255) / 256, 8u * ctx->prop.multiProcessorCount));
+                chft_split_kernel<<<blocks, 256, 0, ctx->compute>>>(reinterpret_cast<const uint4*>(sc.ptr), n,
+                                                                   reinterpret_cast<uint4*>(const_cast<uint8_t*>(img.dev.desc)),
+                                                                   reinterpret_cast<uint4*>(const_cast<float4*>(img.dev.kp)));
+            }
             cudaEventRecord(sc.split_done, ctx->compute);
             sc.used = true;
-            if (accumulate_centering) {
-                const uint32_t cb = std::max(1u, std::min((n + 255u) / 256u, 4u * uint32_t(ctx->prop.multiProcessorCount)));
-                centering_sums_kernel<<<cb, 256, 0, ctx->compute>>>(img.dev.desc, n, ctx->d_sums);
-                ctx->sum_count += n;
-            }
         } else {
             release_slot();
         }
-        if (const chgpu_status e = publish_slot(ctx, slot_img)) rc = e;
+        // the kernels above take pointers, not table entries: the table is published once, behind the loop
+        ctx->h_images[slot_img] = ctx->images[slot_img].dev;
+        pub_lo = std::min(pub_lo, slot_img);
+        pub_hi = std::max(pub_hi, slot_img);
         r.status = CHGPU_OK;
         r.count = n;
         ++st.files_ok;
         st.points += n;
         poll_copies();
+        t_issue += secs(tw2, now());
     }
+    if (trace)
+        fprintf(stderr, "chgpu loader: %u files, issue thread waited %.3f s for readers, %.3f s in alloc_image, %.3f s issuing\n",
+                count, t_wait, t_alloc, t_issue);
     // drain
     if (rc != CHGPU_OK) ring.abort.store(true);
+    if (pub_lo <= pub_hi)
+        cudaMemcpyAsync(ctx->d_images + pub_lo, ctx->h_images + pub_lo, size_t(pub_hi - pub_lo + 1) * sizeof(DevImage),
+                        cudaMemcpyHostToDevice, ctx->copy);
     cudaStreamSynchronize(ctx->copy);
     cudaStreamSynchronize(ctx->compute);
     poll_copies();
-    {
-        std::lock_guard<std::mutex> lock(ring.mu);
-        ring.abort.store(true);
+    ring.abort.store(true);
+    for (size_t k = 0; k < S; ++k) {
+        { std::lock_guard<std::mutex> lock(ring.slots[k].mu); }
+        ring.slots[k].cv_free.notify_all();
     }
-    ring.cv.notify_all();
     for (std::thread& t : readers) t.join();
     const cudaError_t last = cudaGetLastError();
-    for (LoadSlot& s : ring.slots) {
-        if (s.buf) cudaFreeHost(s.buf);
-        cudaEventDestroy(s.copied);
+    for (size_t k = 0; k < S; ++k) {
+        if (ring.slots[k].own) cudaFreeHost(ring.slots[k].buf);  // a reader outgrew its share of the region
+        cudaEventDestroy(ring.slots[k].copied);
     }
-    for (Scratch& sc : scratch) {
-        if (sc.ptr) cudaFree(sc.ptr);
-        cudaEventDestroy(sc.split_done);
+    for (size_t k = 0; k < kScratch; ++k) {
+        ctx->load_scratch[k] = {scratch[k].ptr, scratch[k].cap};
+        cudaEventDestroy(scratch[k].split_done);
     }
     st.bytes_read = ring.bytes_read;
     st.read_seconds = ring.read_seconds;

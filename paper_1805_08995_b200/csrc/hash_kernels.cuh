@@ -24,6 +24,39 @@ __global__ void chft_split_kernel(const uint4* __restrict__ records, uint32_t n,
     }
 }
 
+// K0 fused with the centering sums (the streaming loader's per-file kernel): blocks of 288 threads = 32 records
+// x 9 chunks, so a thread keeps its chunk position while it strides over the records and can hold the 16 column
+// sums of its descriptor chunk in registers; one shared-memory and one global (u64) atomic pass per block.
+constexpr int kSplitSumThreads = 288;
+__global__ void __launch_bounds__(kSplitSumThreads)
+chft_split_sums_kernel(const uint4* __restrict__ records, uint32_t n, uint4* __restrict__ desc, uint4* __restrict__ kp,
+                       unsigned long long* __restrict__ sums /*128*/) {
+    __shared__ unsigned int s_acc[kDim];
+    if (threadIdx.x < kDim) s_acc[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t c = threadIdx.x % 9, r_in = threadIdx.x / 9;
+    uint32_t acc[16];
+#pragma unroll
+    for (int b = 0; b < 16; ++b) acc[b] = 0;
+    for (uint32_t p = blockIdx.x * 32 + r_in; p < n; p += gridDim.x * 32) {  // <= 65536 records: 255 * rows < 2^32
+        const uint4 v = __ldg(records + uint64_t(p) * 9 + c);
+        if (c == 0) {
+            kp[p] = v;
+        } else {
+            desc[uint64_t(p) * 8 + (c - 1)] = v;
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int b = 0; b < 16; ++b) acc[b] += (w[b >> 2] >> (8 * (b & 3))) & 0xffu;
+        }
+    }
+    if (c != 0) {
+#pragma unroll
+        for (int b = 0; b < 16; ++b) atomicAdd(&s_acc[(c - 1) * 16 + b], acc[b]);
+    }
+    __syncthreads();
+    if (threadIdx.x < kDim && s_acc[threadIdx.x]) atomicAdd(&sums[threadIdx.x], (unsigned long long)s_acc[threadIdx.x]);
+}
+
 // ---------------------------------------------------------------------------------------------
 // Centering pass: exact integer column sums (CenteringAccumulator::add, hashing.cpp:52-57).
 // Each lane owns 4 adjacent byte columns of the 128-byte row; a warp reads whole rows.
