@@ -502,8 +502,9 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 
                 uint32_t mykey = kNone;  // lane r holds the r-th ranked key
                 uint32_t n = 0;          // ranked count
+                // GUIDED: the band can only remove candidates, so a query whose UNFILTERED smallest key is beyond tau
+                // ranks nothing either way; the line and the filter are evaluated only for the others.
                 EpiLine line{};
-                if (GUIDED) line = epipolar_band(P.fmats + uint64_t(pair) * 9, __ldg(I.kp + q));
 
                 const bool skip = MODE == kModeTileTopK && hdr.x == kNone;  // nothing within tau in any tile
                 if (skip) {
@@ -543,12 +544,14 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 #pragma unroll
                     for (int s = 0; s < kOverSlots; ++s)
                         if (uint32_t(s) * 32u < tover) key[LT + s] = key_of<SMEM_TRAIN>(key[LT + s], ql, s_long, J.longs);
-                    if (GUIDED) {
+                    // ---- 3. ranking: pull straight out of the slots -------------------------------
+                    uint32_t k0 = first_key(key, kNone);
+                    if (GUIDED && (k0 >> 24) <= P.tau) {
+                        line = epipolar_band(P.fmats + uint64_t(pair) * 9, __ldg(I.kp + q));
 #pragma unroll
                         for (int i = 0; i < KS; ++i) key[i] = band_filter(key[i], line, J.kp, P.band_px);
+                        k0 = first_key(key, kNone);
                     }
-                    // ---- 3. ranking: pull straight out of the slots -------------------------------
-                    const uint32_t k0 = first_key(key, kNone);
                     if (MODE == kModeTileMin) {
                         if (lane == 0 && k0 != kNone) atomicMin(P.gmin + pd.res_off + q, k0);
                     } else if (MODE == kModeTileTopK) {
@@ -598,10 +601,9 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 #pragma unroll
                         for (int t = 0; t < LT; ++t)
                             if (off < len[t]) {
-                                uint32_t k = scan_step<SMEM_TRAIN>(ids, lo[t] + off, lo[t] + len[t] - 1u, lane, ql,
-                                                                   s_long, J.longs);
-                                if (GUIDED) k = band_filter(k, line, J.kp, P.band_px);
-                                lmin = min(lmin, k);
+                                const uint32_t k = scan_step<SMEM_TRAIN>(ids, lo[t] + off, lo[t] + len[t] - 1u, lane, ql,
+                                                                         s_long, J.longs);
+                                lmin = min(lmin, k);  // GUIDED: unfiltered (lmax is then taken in pass 2)
                                 if (k != kNone) lmax = max(lmax, k);
                             }
                     }
@@ -610,7 +612,10 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                         if (lane == 0 && gmin != kNone) atomicMin(P.gmin + pd.res_off + q, gmin);
                     } else if (MODE == kModeTileTopK || (gmin >> 24) <= P.tau) {
                         // pass 2: merge every round into the running top-k (ascending, unique)
-                        const bool anycut = (__reduce_max_sync(FULL, lmax) >> 24) > P.tau;
+                        if (GUIDED) {
+                            line = epipolar_band(P.fmats + uint64_t(pair) * 9, __ldg(I.kp + q));
+                            lmax = 0;
+                        }
                         for (uint32_t off = 0; off < maxlen; off += 32u) {
                             uint32_t key[LT];
 #pragma unroll
@@ -619,7 +624,10 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                                 if (off < len[t]) {
                                     key[t] = scan_step<SMEM_TRAIN>(ids, lo[t] + off, lo[t] + len[t] - 1u, lane, ql, s_long,
                                                                    J.longs);
-                                    if (GUIDED) key[t] = band_filter(key[t], line, J.kp, P.band_px);
+                                    if (GUIDED) {
+                                        key[t] = band_filter(key[t], line, J.kp, P.band_px);
+                                        if (key[t] != kNone) lmax = max(lmax, key[t]);
+                                    }
                                 }
                             }
                             // a round whose smallest key is beyond a full list's last entry changes nothing
@@ -635,9 +643,11 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                             }
                         }
                         // thresholded size s, unique total (<= k); fallback rule as in the single-round path
+                        const bool anycut = (__reduce_max_sync(FULL, lmax) >> 24) > P.tau;
                         const uint32_t tot = __popc(__ballot_sync(FULL, mykey != kNone));
                         const uint32_t s = __popc(__ballot_sync(FULL, mykey != kNone && (mykey >> 24) <= P.tau));
                         n = (MODE != kModeTileTopK && (s >= P.min_ranked || !anycut)) ? s : tot;
+                        if (GUIDED && s == 0) n = 0;  // the band removed everything within tau: no ranking, no fallback
                     }
                 }
 
