@@ -376,6 +376,9 @@ public:
     // centering pass (hashing.cpp:52-70): exact integer sums on the device, one division on the host
     void centering_reset() { ck(chgpu_centering_reset(ctx_)); }
     void centering_add(std::uint32_t image_id) { ck(chgpu_centering_add_image(ctx_, image_id)); }
+    void centering_add(std::span<const std::uint32_t> image_ids) {  // one launch over all listed images
+        ck(chgpu_centering_add_images(ctx_, image_ids.data(), static_cast<std::uint32_t>(image_ids.size())));
+    }
     std::array<double, kDescriptorDim> centering_apply() {
         std::array<double, kDescriptorDim> c{};
         ck(chgpu_centering_apply(ctx_, c.data()));
@@ -385,6 +388,14 @@ public:
     // hash build + bucket index for resident images (compute_codes + build_bucket_index)
     void hash(std::span<const std::uint32_t> image_ids, int reduce_rounds = kDefaultReduceRounds) {
         ck(chgpu_hash_images(ctx_, image_ids.data(), static_cast<std::uint32_t>(image_ids.size()), reduce_rounds));
+    }
+    // How the hyperplane signs are evaluated (both exact): fp32 filter with an error bound + fp64 re-evaluation
+    // of the undecided dots (default), or every dot in reduce_dot's fp64 order (hashing.hpp:24-43).
+    void set_exact_hashing(bool exact) { ck(chgpu_set_hash_mode(ctx_, exact ? CHGPU_HASH_EXACT : CHGPU_HASH_FILTERED)); }
+    chgpu_hash_stats hash_stats() {
+        chgpu_hash_stats st{};
+        ck(chgpu_get_hash_stats(ctx_, &st));
+        return st;
     }
     ImageCodes codes(std::uint32_t image_id) {
         std::uint32_t n = 0;

@@ -308,6 +308,24 @@ static void device_checks(const std::filesystem::path& tmp) {
         m.centering_reset();
         for (std::uint32_t i : ids) m.centering_add(i);
         CHECK(m.centering_apply() == fam.centering);
+        m.centering_reset();
+        m.centering_add(ids);  // the batched form: one launch, the same sums
+        CHECK(m.centering_apply() == fam.centering);
+        // hash build: fp32 filter + exact fixup (default) and the all-fp64 kernel give the reference's codes
+        m.hash(ids);
+        CHECK(m.hash_stats().filter_active == 1 && m.hash_stats().overflowed_batches == 0);
+        std::vector<ch::ImageCodes> filtered;
+        for (std::uint32_t i : ids) filtered.push_back(m.codes(i));
+        m.set_exact_hashing(true);
+        m.hash(ids);
+        for (std::uint32_t i : ids) {
+            const ch::ImageCodes c = m.codes(i);
+            CHECK(c.shorts.values == filtered[i].shorts.values && c.shorts.values == ocodes[i].shorts);
+            for (std::size_t p = 0; p < c.longs.codes.size(); ++p)
+                CHECK(c.longs.codes[p].words == filtered[i].longs.codes[p].words &&
+                      c.longs.codes[p].words[0] == ocodes[i].longs[2 * p] && c.longs.codes[p].words[1] == ocodes[i].longs[2 * p + 1]);
+        }
+        m.set_exact_hashing(false);
         m.hash(ids);
         const auto pairs = ch::plan_exhaustive(4, 2, 2);
         ch::MatchStats st{};
