@@ -305,8 +305,7 @@ def run_ours(args):
     ids = np.arange(args.images, dtype=np.uint32)
 
     def load_and_hash():
-        for i in range(args.images):
-            m.upload(i, desc[i])
+        m.upload_many(ids, desc)
         m.centering_reset()
         m.centering_add_many(ids)
         m.centering_apply()

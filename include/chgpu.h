@@ -136,6 +136,10 @@ chgpu_status chgpu_set_centering(chgpu_ctx* ctx, const double* centering128);
  * keypoints: n x 4 f32 (x, y, scale, orientation) or NULL.  Re-uploading an id replaces it. */
 chgpu_status chgpu_upload_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n,
                                 const uint8_t* desc, const float* keypoints);
+/* Batch form for `count` images of n points each, stored back to back (desc: count x n x 128 u8, keypoints:
+ * count x n x 4 f32 or NULL): from pinned memory the copies are issued back to back and drained once. */
+chgpu_status chgpu_upload_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32_t count, uint32_t n,
+                                 const uint8_t* desc, const float* keypoints);
 /* Replaces load_features / parse_features_blob (feature_io.cpp:65-106, engine.cpp:458-488) for a
  * CHFT blob already in host memory: header checked on the host, the 144-byte AoS records are
  * split into SoA on the device.  On CHGPU_EFORMAT *fault / *fault_offset carry the reference's

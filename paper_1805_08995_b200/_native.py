@@ -100,6 +100,7 @@ SIGNATURES = {
     "chgpu_centering_apply": (C.c_int, [C.c_void_p, f64p]),
     "chgpu_set_centering": (C.c_int, [C.c_void_p, f64p]),
     "chgpu_upload_image": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "chgpu_upload_images": (C.c_int, [C.c_void_p, u32p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]),
     "chgpu_upload_chft": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_size_t, u32p,
                                     C.POINTER(C.c_int), u64p]),
     "chgpu_load_chft_files": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), u32p, C.c_uint32, C.c_uint32, C.c_int,

@@ -362,6 +362,21 @@ class Matcher:
         self._ck(self.lib.chgpu_upload_image(self.h, image_id, n, d.ctypes.data if n else None,
                                              kp.ctypes.data if kp is not None and n else None))
 
+    def upload_many(self, image_ids, desc: np.ndarray, keypoints: np.ndarray | None = None):
+        """Images of equal size stored back to back: desc (count, n, 128) u8, keypoints (count, n, 4) f32 or None.
+        From pinned memory (Matcher.pinned_empty) the copies are issued back to back and drained once."""
+        ids = np.ascontiguousarray(image_ids, dtype=np.uint32)
+        assert desc.dtype == np.uint8 and desc.flags.c_contiguous and desc.ndim == 3 and desc.shape[2] == 128
+        assert desc.shape[0] == len(ids)
+        n = desc.shape[1]
+        kp = None
+        if keypoints is not None:
+            kp = keypoints
+            assert kp.dtype == np.float32 and kp.flags.c_contiguous and kp.shape == (len(ids), n, 4)
+        self._ck(self.lib.chgpu_upload_images(self.h, ids.ctypes.data_as(N.u32p), len(ids), n,
+                                              desc.ctypes.data if desc.size else None,
+                                              kp.ctypes.data if kp is not None and kp.size else None))
+
     def upload_chft(self, image_id: int, blob: bytes) -> int:
         cnt = C.c_uint32(0)
         fault = C.c_int(0)

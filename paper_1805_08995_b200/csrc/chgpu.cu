@@ -1262,6 +1262,41 @@ chgpu_status chgpu_upload_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, c
     return publish_slot(ctx, slot);
 }
 
+chgpu_status chgpu_upload_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32_t count, uint32_t n,
+                                 const uint8_t* desc, const float* keypoints) {
+    if (!ctx || (count && !image_ids) || (count && n && !desc)) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    if (count == 0) return CHGPU_OK;
+    if (const chgpu_status s = order_copy_after_compute(ctx)) return s;
+    // pinned sources: back-to-back async copies, one drain at the end; pageable ones go through the staging ring
+    const bool pinned = n == 0 || (is_pinned(desc) && (!keypoints || is_pinned(keypoints)));
+    uint32_t lo = UINT32_MAX, hi = 0;
+    for (uint32_t i = 0; i < count; ++i) {
+        uint32_t slot;
+        if (const chgpu_status s = alloc_image(ctx, image_ids[i], n, &slot)) return s;
+        ImageRec& r = ctx->images[slot];
+        const uint8_t* d = desc + size_t(i) * n * kDim;
+        const float* k = keypoints ? keypoints + size_t(i) * n * 4 : nullptr;
+        if (n) {
+            if (pinned) {
+                CK(cudaMemcpyAsync(const_cast<uint8_t*>(r.dev.desc), d, size_t(n) * kDim, cudaMemcpyHostToDevice, ctx->copy));
+                if (k) CK(cudaMemcpyAsync(const_cast<float4*>(r.dev.kp), k, size_t(n) * 16, cudaMemcpyHostToDevice, ctx->copy));
+            } else {
+                if (const chgpu_status s = h2d(ctx, const_cast<uint8_t*>(r.dev.desc), d, size_t(n) * kDim)) return s;
+                if (k) if (const chgpu_status s = h2d(ctx, const_cast<float4*>(r.dev.kp), k, size_t(n) * 16)) return s;
+            }
+            if (!k) CK(cudaMemsetAsync(const_cast<float4*>(r.dev.kp), 0, size_t(n) * 16, ctx->copy));
+        }
+        ctx->h_images[slot] = r.dev;
+        lo = std::min(lo, slot);
+        hi = std::max(hi, slot);
+    }
+    CK(cudaMemcpyAsync(ctx->d_images + lo, ctx->h_images + lo, size_t(hi - lo + 1) * sizeof(DevImage), cudaMemcpyHostToDevice,
+                       ctx->copy));
+    CK(cudaStreamSynchronize(ctx->copy));  // the caller may reuse its buffers
+    return CHGPU_OK;
+}
+
 chgpu_status chgpu_upload_chft(chgpu_ctx* ctx, uint32_t image_id, const void* blob, size_t nbytes,
                                uint32_t* count_out, chgpu_file_fault* fault, uint64_t* fault_offset) {
     if (!ctx || !blob) return CHGPU_EINVAL;

@@ -165,6 +165,23 @@ def test_near_tie_projections_keep_their_sign(matcher, oracle, default_family):
     assert (np.abs(dots) < 1.0).sum() > 100, "sample must contain near-zero projections"
 
 
+def test_batch_upload_equals_single_uploads(matcher, default_family):
+    fresh(matcher, default_family)
+    d = make_dataset(5, 700, seed=77)
+    kp = np.random.default_rng(1).uniform(0, 100, (5, 700, 4)).astype(np.float32)
+    ids = [BASE + i for i in range(5)]
+    pinned = matcher.pinned_empty(d.shape, np.uint8)
+    pinned[:] = d
+    for src, k in ((pinned, None), (np.ascontiguousarray(d), kp)):   # pinned / pageable source
+        matcher.upload_many(ids, src, k)
+        matcher._test_ids.update(ids)
+        for i in range(5):
+            got_d, got_k = matcher.descriptors(ids[i])
+            assert np.array_equal(got_d, d[i])
+            assert np.array_equal(got_k, kp[i] if k is not None else np.zeros((700, 4), np.float32))
+    matcher.upload_many([], np.zeros((0, 700, 128), np.uint8))
+
+
 def test_batched_centering_sums_equal_the_per_image_sums(matcher, oracle, default_family):
     fresh(matcher, default_family)
     sizes = [0, 1, 31, 1000, 4097, 20000]
