@@ -71,6 +71,15 @@ def measured_peak_hbm() -> tuple[float, str]:
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def recorded_instructions_per_query():
+    """Warp instructions per query point of the match kernel, from the committed ncu --set full summary."""
+    p = ROOT / "profiles" / "r01k_match_kernel_ncu_full.json"
+    try:
+        return float(json.loads(p.read_text())["kernels"][0]["warp_instructions_per_query"])
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def recorded_traffic():
     """dram bytes per match-kernel launch from the committed ncu --set full capture, if any."""
     p = ROOT / "profiles" / "traffic.json"
@@ -371,6 +380,18 @@ def run_ours(args):
                            "frac": popc_rate / popc_peak,
                            "note": "lower bound on POPC work (padding lanes not counted); ncu pipe utilisations of the "
                                    "committed capture: profiles/r01k_match_kernel_ncu_full.json"}
+
+    # the limit the kernel actually runs into: warp-instruction issue slots (4 per clock per SM).  Instructions
+    # per query come from the committed ncu capture of this kernel; the rate is this run's.
+    ipq = recorded_instructions_per_query()
+    if ipq:
+        issue_peak = props["sm_count"] * 4 * sm_mhz * 1e6
+        issue_rate = ipq * last["query_points"] / (kern_ms_per_step * 1e-3)
+        roofline["on_chip"]["issue"] = {
+            "bound": "issue_slots", "warp_instructions_per_query": ipq, "achieved_ginst_s": issue_rate / 1e9,
+            "peak_ginst_s": issue_peak / 1e9, "frac": issue_rate / issue_peak,
+            "note": "ncu of the same kernel: issue active 70 %, LSU data pipe 75 %, ALU 61 %, XU 50 % "
+                    "(profiles/r01k_match_kernel_ncu_full.json)"}
 
     # ---- e2e: host buffers in, host records out, every step ------------------------------------------
     e2e = None

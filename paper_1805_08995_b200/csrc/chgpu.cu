@@ -187,6 +187,7 @@ struct chgpu_ctx {
     uint2* d_res = nullptr;
     size_t res_cap = 0;
     uint32_t* d_gmin = nullptr;   // tiled train images: per-query minimum key over the tiles
+    unsigned long long* d_gdone = nullptr;  // ... and the tiles whose list the min pass already wrote
     size_t gmin_cap = 0;
     uint32_t* d_lists = nullptr;  // tiled train images: per-query, per-tile top-k keys
     size_t lists_cap = 0;
@@ -883,9 +884,12 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
                 CK(cudaStreamSynchronize(ctx->compute));
                 if (ctx->gmin_cap < sb.queries) {
                     cudaFree(ctx->d_gmin);
+                    cudaFree(ctx->d_gdone);
                     ctx->d_gmin = nullptr;
+                    ctx->d_gdone = nullptr;
                     ctx->gmin_cap = 0;
                     CK(cudaMalloc(&ctx->d_gmin, sb.queries * sizeof(uint32_t)));
+                    CK(cudaMalloc(&ctx->d_gdone, sb.queries * sizeof(unsigned long long)));
                     ctx->gmin_cap = sb.queries;
                 }
                 if (ctx->lists_cap < sb.queries * stride) {
@@ -904,7 +908,9 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
             }
             CK(cudaMemcpyAsync(b.d_tpairs, b.h_tpairs, size_t(ntp) * sizeof(PairDesc), cudaMemcpyHostToDevice, ctx->compute));
             CK(cudaMemsetAsync(ctx->d_gmin, 0xff, sb.queries * sizeof(uint32_t), ctx->compute));
+            CK(cudaMemsetAsync(ctx->d_gdone, 0, sb.queries * sizeof(unsigned long long), ctx->compute));
             P.gmin = ctx->d_gmin;
+            P.gdone = ctx->d_gdone;
             P.lists = ctx->d_lists;
             P.list_stride = uint32_t(stride);
             P.tile_points = tp;
@@ -1051,7 +1057,7 @@ void chgpu_destroy(chgpu_ctx* ctx) {
     }
     cudaFree(ctx->d_planes); cudaFree(ctx->d_centering); cudaFree(ctx->d_sums); cudaFree(ctx->d_res);
     cudaFree(ctx->d_stats); cudaFreeHost(ctx->h_stats); cudaFree(ctx->d_counter); cudaFree(ctx->d_slots);
-    cudaFree(ctx->d_dbg); cudaFree(ctx->d_gmin); cudaFree(ctx->d_lists);
+    cudaFree(ctx->d_dbg); cudaFree(ctx->d_gmin); cudaFree(ctx->d_gdone); cudaFree(ctx->d_lists);
     cudaFreeHost(ctx->load_pinned);
     for (auto& b : ctx->load_scratch) cudaFree(b.first);
     cudaFree(ctx->d_planes_t); cudaFree(ctx->d_bias); cudaFree(ctx->d_hnorm); cudaFree(ctx->d_hq);

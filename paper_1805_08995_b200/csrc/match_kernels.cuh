@@ -97,6 +97,7 @@ struct MatchParams {
     uint32_t* dbg_count;        // optional: n_i
     // tiled train images (MODE 1 / 2 and tile_merge_kernel)
     uint32_t* gmin;             // per query (res indexing): smallest key over all tiles
+    unsigned long long* gdone;  // per query: bit t set once tile t's list is written
     uint32_t* lists;            // per query: list_stride keys, tile t's top_k keys at [t * top_k, (t + 1) * top_k)
     uint32_t list_stride;
     uint32_t tile_points;       // point ids per tile
@@ -106,10 +107,11 @@ struct MatchParams {
 // tile_points points is a small train image of its own (own bucket index over local ids, built by the
 // same bucket_build_kernel on a slice of the codes), so the kernel below runs unchanged on (query image,
 // tile) pairs and only its output differs:
-//   MODE 1 (kTileMin)   scan only: the smallest key of the tile joins gmin[query] (atomicMin).  Most queries
-//                       have no candidate within tau in any tile and are finished after this pass.
-//   MODE 2 (kTileTopK)  queries with gmin within tau: the tile's top_k smallest distinct keys, no threshold,
-//                       global point ids, go to lists[query][tile].
+//   MODE 1 (kTileMin)   scan: the smallest key of the tile joins gmin[query] (atomicMin).  Most queries have no
+//                       candidate within tau in any tile and are finished after this pass.  A tile that itself
+//                       has one writes its list (below) right away and marks it in gdone[query].
+//   MODE 2 (kTileTopK)  queries with gmin within tau, tiles not yet marked: the tile's top_k smallest distinct
+//                       keys, no threshold, global point ids, go to lists[query][tile].
 // tile_merge_kernel then merges the lists of a query, applies the threshold / re-rank rule of
 // matcher.cpp:176-189 to the merged ranking and verifies it exactly like MODE 0 does.
 constexpr int kModeMatch = 0, kModeTileMin = 1, kModeTileTopK = 2;
@@ -422,8 +424,10 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
             auto lookup_batch = [&](uint32_t qb) {
                 const uint32_t q = qb + lane * kWarps;
                 bool live = lane < kBatch && q < q1;
-                if (MODE == kModeTileTopK && live && (__ldg(P.gmin + pd.res_off + q) >> 24) > P.tau) {
-                    // nothing within tau in any tile: the query is skipped (sentinel header, harmless ranges)
+                if (MODE == kModeTileTopK && live &&
+                    ((__ldg(P.gmin + pd.res_off + q) >> 24) > P.tau || ((__ldg(P.gdone + pd.res_off + q) >> pd.tile_idx) & 1ull))) {
+                    // nothing within tau in any tile, or this tile's list was written by the min pass: the query is
+                    // skipped (sentinel header, harmless ranges)
                     const uint32_t rec = s_stage + lane * kRec;
                     sts128(rec + 16u, make_uint4(kNone, 0u, 0u, 0u));
 #pragma unroll
@@ -506,7 +510,8 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                 // ranks nothing either way; the line and the filter are evaluated only for the others.
                 EpiLine line{};
 
-                const bool skip = MODE == kModeTileTopK && hdr.x == kNone;  // nothing within tau in any tile
+                const bool skip = MODE == kModeTileTopK && hdr.x == kNone;  // see lookup_batch
+                bool emit = MODE == kModeTileTopK && !skip;                 // this (query, tile) writes its list
                 if (skip) {
                 } else if (tover <= 32u * kOverSlots) {
                     // ---- 2. Hamming scan: the first 32 entries of every bucket, one table per slot,
@@ -554,7 +559,10 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     }
                     if (MODE == kModeTileMin) {
                         if (lane == 0 && k0 != kNone) atomicMin(P.gmin + pd.res_off + q, k0);
-                    } else if (MODE == kModeTileTopK) {
+                        emit = (k0 >> 24) <= P.tau;  // the tile itself has a candidate within tau
+                    }
+                    if (MODE == kModeTileMin && !emit) {
+                    } else if (MODE != kModeMatch) {
                         // the tile's top_k smallest distinct keys, whatever their distance
                         uint32_t prev = k0;
                         while (prev != kNone) {
@@ -610,7 +618,10 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     const uint32_t gmin = __reduce_min_sync(FULL, lmin);
                     if (MODE == kModeTileMin) {
                         if (lane == 0 && gmin != kNone) atomicMin(P.gmin + pd.res_off + q, gmin);
-                    } else if (MODE == kModeTileTopK || (gmin >> 24) <= P.tau) {
+                        emit = (gmin >> 24) <= P.tau;
+                    }
+                    if (MODE == kModeTileMin && !emit) {
+                    } else if (MODE != kModeMatch || (gmin >> 24) <= P.tau) {
                         // pass 2: merge every round into the running top-k (ascending, unique)
                         if (GUIDED) {
                             line = epipolar_band(P.fmats + uint64_t(pair) * 9, __ldg(I.kp + q));
@@ -646,13 +657,16 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                         const bool anycut = (__reduce_max_sync(FULL, lmax) >> 24) > P.tau;
                         const uint32_t tot = __popc(__ballot_sync(FULL, mykey != kNone));
                         const uint32_t s = __popc(__ballot_sync(FULL, mykey != kNone && (mykey >> 24) <= P.tau));
-                        n = (MODE != kModeTileTopK && (s >= P.min_ranked || !anycut)) ? s : tot;
+                        n = (MODE == kModeMatch && (s >= P.min_ranked || !anycut)) ? s : tot;
                         if (GUIDED && s == 0) n = 0;  // the band removed everything within tau: no ranking, no fallback
                     }
                 }
 
-                if (MODE == kModeTileTopK && !skip && lane < P.top_k)
-                    P.lists[(pd.res_off + q) * P.list_stride + pd.tile_idx * P.top_k + lane] = lane < n ? mykey + pd.tile_base : kNone;
+                if (MODE != kModeMatch && emit) {
+                    if (lane < P.top_k)
+                        P.lists[(pd.res_off + q) * P.list_stride + pd.tile_idx * P.top_k + lane] = lane < n ? mykey + pd.tile_base : kNone;
+                    if (MODE == kModeTileMin && lane == 0) atomicOr(P.gdone + pd.res_off + q, 1ull << pd.tile_idx);
+                }
 
                 if (MODE == kModeMatch && P.dbg_ranked != nullptr) {
                     if (lane < n) P.dbg_ranked[uint64_t(q) * P.top_k + lane] = mykey & 0xffffffu;
