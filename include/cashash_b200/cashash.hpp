@@ -14,7 +14,7 @@
 //     match output      save_matches / pair_file_name           include/cashash/feature_io.hpp:106,
 //                                                               include/cashash/engine.hpp:79
 //     guided match      guided_match_pair (F as 9 doubles)      include/cashash/geometry.hpp:86-89
-//     pair list         plan_exhaustive (flattened)             include/cashash/scheduler.hpp:53
+//     pair list         plan_exhaustive, plan_guided (flattened) include/cashash/scheduler.hpp:53-58
 //
 // A caller of the reference switches by including this header and `namespace cashash =
 // cashash_b200;`.  The free functions run on a process-wide default
@@ -318,6 +318,23 @@ inline std::vector<std::pair<std::uint32_t, std::uint32_t>> plan_exhaustive(std:
     const chgpu_status st = chgpu_plan_exhaustive(image_count, block_images, blocks_per_group,
                                                   reinterpret_cast<std::uint32_t*>(pairs.data()), &n);
     if (st != CHGPU_OK) detail::raise(st, "plan_exhaustive");
+    pairs.resize(n);
+    return pairs;
+}
+
+// plan_guided (scheduler.hpp:57-58), flattened: the exhaustive traversal restricted to the accepted pairs.
+inline std::vector<std::pair<std::uint32_t, std::uint32_t>> plan_guided(
+    std::uint32_t image_count, std::uint32_t block_images, std::uint32_t blocks_per_group,
+    const std::vector<std::pair<std::uint32_t, std::uint32_t>>& accepted_pairs) {
+    if (image_count == 0 || block_images == 0 || blocks_per_group == 0)
+        throw std::invalid_argument("partition: image_count, block_images and blocks_per_group must be >= 1");
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> pairs(accepted_pairs.size());
+    std::uint64_t n = 0;
+    const chgpu_status st = chgpu_plan_guided(image_count, block_images, blocks_per_group,
+                                              reinterpret_cast<const std::uint32_t*>(accepted_pairs.data()), accepted_pairs.size(),
+                                              reinterpret_cast<std::uint32_t*>(pairs.data()), &n);
+    if (st == CHGPU_EINVAL) throw std::invalid_argument("plan_guided: self pair or unknown image index");
+    if (st != CHGPU_OK) detail::raise(st, "plan_guided");
     pairs.resize(n);
     return pairs;
 }

@@ -314,6 +314,12 @@ chgpu_status chgpu_match_pairs_to_files(chgpu_ctx* ctx, const uint32_t* pairs, u
  * pairs_out holds image_count*(image_count-1) u32 (2 per pair). */
 chgpu_status chgpu_plan_exhaustive(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group,
                                    uint32_t* pairs_out, uint64_t* npairs_out);
+/* The same traversal restricted to the accepted pairs (plan_guided, scheduler.hpp:57-58, scheduler.cpp:144-164):
+ * either order, duplicates collapse; a self pair or an index >= image_count is CHGPU_EINVAL (the reference throws
+ * std::invalid_argument).  pairs_out holds 2 * accepted_count u32.  This is the pair-order scheduling for
+ * arbitrary pair lists (e.g. a k-neighbour list): consecutive pairs share their images. */
+chgpu_status chgpu_plan_guided(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group,
+                               const uint32_t* accepted, uint64_t accepted_count, uint32_t* pairs_out, uint64_t* npairs_out);
 /* Shard [0,npairs) for rank `rank` of `world`: contiguous ranges of the plan, so each GPU keeps
  * its train images hot (replaces assign_workers, scheduler.cpp:166-173). */
 void chgpu_shard_range(uint64_t npairs, uint32_t rank, uint32_t world, uint64_t* first, uint64_t* last);

@@ -25,6 +25,7 @@
 #include <random>
 #include <string>
 #include <thread>
+#include <set>
 #include <vector>
 
 namespace {
@@ -608,6 +609,50 @@ int chor_plan_exhaustive(uint32_t image_count, uint32_t block_images, uint32_t b
         }
         if (task_sizes) task_sizes[nt] = sz;
         ++nt;
+    }
+    *npairs_out = np;
+    if (ntasks_out) *ntasks_out = nt;
+    return 0;
+}
+
+int chor_plan_guided(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group,
+                     const uint32_t* accepted, uint64_t accepted_count, uint32_t* pairs_out, uint64_t* npairs_out,
+                     uint32_t* task_sizes, uint32_t* ntasks_out) {
+    // scheduler.cpp:144-164: accepted pairs as a set of normalised (a < b) keys; every task of the exhaustive plan
+    // keeps the pairs in the set; empty tasks disappear.
+    if (image_count == 0 || block_images == 0 || blocks_per_group == 0) return 1;
+    std::set<uint64_t> keys;
+    for (uint64_t i = 0; i < accepted_count; ++i) {
+        uint32_t a = accepted[2 * i], b = accepted[2 * i + 1];
+        if (a == b) return 1;
+        if (a > b) std::swap(a, b);
+        if (b >= image_count) return 1;
+        keys.insert(static_cast<uint64_t>(a) * image_count + b);
+    }
+    const uint64_t all = static_cast<uint64_t>(image_count) * (image_count - 1) / 2;
+    std::vector<uint32_t> full(std::max<uint64_t>(all, 1) * 2), sizes(static_cast<size_t>(image_count) * image_count + 4);
+    uint64_t nfull = 0;
+    uint32_t nt_full = 0;
+    if (const int rc = chor_plan_exhaustive(image_count, block_images, blocks_per_group, full.data(), &nfull, sizes.data(), &nt_full))
+        return rc;
+    uint64_t np = 0, at = 0;
+    uint32_t nt = 0;
+    for (uint32_t t = 0; t < nt_full; ++t) {
+        uint32_t kept = 0;
+        for (uint32_t k = 0; k < sizes[t]; ++k, ++at) {
+            const uint32_t a = full[2 * at], b = full[2 * at + 1];
+            if (!keys.count(static_cast<uint64_t>(a) * image_count + b)) continue;
+            if (pairs_out) {
+                pairs_out[2 * np] = a;
+                pairs_out[2 * np + 1] = b;
+            }
+            ++np;
+            ++kept;
+        }
+        if (kept) {
+            if (task_sizes) task_sizes[nt] = kept;
+            ++nt;
+        }
     }
     *npairs_out = np;
     if (ntasks_out) *ntasks_out = nt;

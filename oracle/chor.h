@@ -138,6 +138,13 @@ int chor_time_match_pairs(const chor_family_params* p, const chor_match_cfg* cfg
 int chor_plan_exhaustive(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group,
                          uint32_t* pairs_out, uint64_t* npairs_out, uint32_t* task_sizes, uint32_t* ntasks_out);
 
+/* plan_guided (scheduler.cpp:144-164): the exhaustive traversal restricted to the accepted pairs (either order,
+ * duplicates collapse), tasks that end up empty dropped.  Returns 1 (std::invalid_argument) for a self pair or an
+ * unknown image index.  pairs_out holds accepted_count pairs; task_sizes / ntasks_out as above. */
+int chor_plan_guided(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group,
+                     const uint32_t* accepted, uint64_t accepted_count, uint32_t* pairs_out, uint64_t* npairs_out,
+                     uint32_t* task_sizes, uint32_t* ntasks_out);
+
 #ifdef __cplusplus
 }
 #endif

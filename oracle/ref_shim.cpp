@@ -427,4 +427,29 @@ int chor_plan_exhaustive(uint32_t image_count, uint32_t block_images, uint32_t b
     });
 }
 
+int chor_plan_guided(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group,
+                     const uint32_t* accepted, uint64_t accepted_count, uint32_t* pairs_out, uint64_t* npairs_out,
+                     uint32_t* task_sizes, uint32_t* ntasks_out) {
+    return guarded([&] {
+        std::vector<std::pair<std::uint32_t, std::uint32_t>> acc(accepted_count);
+        for (uint64_t i = 0; i < accepted_count; ++i) acc[i] = {accepted[2 * i], accepted[2 * i + 1]};
+        const PairPlan plan = plan_guided(make_partition(image_count, block_images, blocks_per_group), acc);
+        uint64_t np = 0;
+        uint32_t nt = 0;
+        for (const PlanTask& t : plan.tasks) {
+            for (const auto& [a, b] : t.pairs) {
+                if (pairs_out) {
+                    pairs_out[2 * np] = a;
+                    pairs_out[2 * np + 1] = b;
+                }
+                ++np;
+            }
+            if (task_sizes) task_sizes[nt] = static_cast<uint32_t>(t.pairs.size());
+            ++nt;
+        }
+        *npairs_out = np;
+        if (ntasks_out) *ntasks_out = nt;
+    });
+}
+
 }  // extern "C"

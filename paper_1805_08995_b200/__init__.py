@@ -7,7 +7,7 @@ the same C ABI.  Importing this package never falls back to a CPU path.
 from .api import (  # noqa: F401
     BucketIndex, CudaError, FamilyParams, FeatureFileError, HashFamily, ImageCodes, LogicError, MatchConfig,
     Matcher, RECORD_DTYPE, UnsupportedError, build_hash_family, compute_codes, match_pair, pair_file_name,
-    plan_exhaustive, save_matches, set_centering, shard_range,
+    plan_exhaustive, plan_guided, save_matches, set_centering, shard_range,
     CacheMismatchError, centering_fingerprint, load_centering_file, load_code_cache, read_code_cache_header,
     save_centering_file, save_code_cache, MatchFileSink,
 )

@@ -145,6 +145,7 @@ SIGNATURES = {
                                              C.POINTER(MatchStatsC)]),
     "chgpu_pair_file_name": (None, [C.c_uint32, C.c_uint32, C.c_char_p]),
     "chgpu_plan_exhaustive": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p, u64p]),
+    "chgpu_plan_guided": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, u32p, C.c_uint64, u32p, u64p]),
     "chgpu_shard_range": (None, [C.c_uint64, C.c_uint32, C.c_uint32, u64p, u64p]),
 }
 

@@ -246,6 +246,18 @@ def plan_exhaustive(image_count: int, block_images: int, blocks_per_group: int) 
     return pairs
 
 
+def plan_guided(image_count: int, block_images: int, blocks_per_group: int, accepted_pairs) -> np.ndarray:
+    """scheduler.hpp:57 plan_guided, flattened: the exhaustive traversal restricted to `accepted_pairs`."""
+    acc = np.ascontiguousarray(accepted_pairs, dtype=np.uint32).reshape(-1, 2)
+    out = np.empty((max(len(acc), 1), 2), dtype=np.uint32)
+    n = C.c_uint64(0)
+    st = N.load().chgpu_plan_guided(image_count, block_images, blocks_per_group, acc.ctypes.data_as(N.u32p), len(acc),
+                                    out.ctypes.data_as(N.u32p), C.byref(n))
+    if st != N.OK:
+        _raise(st, "plan_guided: self pair or unknown image index")
+    return out[: n.value].copy()
+
+
 def shard_range(npairs: int, rank: int, world: int) -> tuple[int, int]:
     a, b = C.c_uint64(0), C.c_uint64(0)
     N.load().chgpu_shard_range(npairs, rank, world, C.byref(a), C.byref(b))

@@ -54,6 +54,7 @@ def main():
             paths.append(p)
     write_s = time.perf_counter() - t0
     pairs = np.array([(i, i + dd) for i in range(K) for dd in range(1, args.neighbors + 1) if i + dd < K], dtype=np.uint32)
+    pairs = ch.plan_guided(K, 50, 4, pairs)  # the reference's traversal order restricted to this list (scheduler.cpp:144-164)
 
     with ch.Matcher(0) as m:
         m.set_family(ch.build_hash_family(ch.FamilyParams()))

@@ -45,7 +45,7 @@ def reference():
 def golden():
     import numpy as np
     g = ROOT / "tests" / "golden"
-    return {name: np.load(g / f"{name}.npz") for name in ("family", "small_dataset", "plans", "cache")}
+    return {name: np.load(g / f"{name}.npz") for name in ("family", "small_dataset", "plans", "plans_guided", "cache")}
 
 
 @pytest.fixture(scope="session")

@@ -171,6 +171,23 @@ static void host_checks(const std::filesystem::path& tmp) {
         seen[a * 23 + b] = 1;
     }
     CHECK(throws<std::invalid_argument>([] { ch::plan_exhaustive(0, 1, 1); }));
+
+    // plan_guided: the accepted pairs (either order, duplicates collapse) in the exhaustive plan's order == the oracle's
+    {
+        std::vector<std::pair<std::uint32_t, std::uint32_t>> acc;
+        for (std::uint32_t i = 0; i < 23; ++i)
+            for (std::uint32_t d = 1; d <= 3 && i + d < 23; ++d) acc.emplace_back(i % 2 ? i + d : i, i % 2 ? i : i + d);
+        acc.push_back(acc[5]);
+        const auto guided = ch::plan_guided(23, 4, 3, acc);
+        std::vector<std::uint32_t> want(acc.size() * 2);
+        std::uint64_t n = 0;
+        CHECK(chor_plan_guided(23, 4, 3, reinterpret_cast<const std::uint32_t*>(acc.data()), acc.size(), want.data(), &n, nullptr,
+                               nullptr) == 0);
+        CHECK(guided.size() == n && n == acc.size() - 1);
+        for (std::size_t k = 0; k < guided.size(); ++k) CHECK(guided[k].first == want[2 * k] && guided[k].second == want[2 * k + 1]);
+        CHECK(throws<std::invalid_argument>([] { ch::plan_guided(23, 4, 3, {{4, 4}}); }));
+        CHECK(throws<std::invalid_argument>([] { ch::plan_guided(23, 4, 3, {{4, 23}}); }));
+    }
 }
 
 static void device_checks(const std::filesystem::path& tmp) {

@@ -94,6 +94,18 @@ def main() -> None:
         plans[f"pairs_{k}_{np_}_{m}"] = pairs
         plans[f"sizes_{k}_{np_}_{m}"] = sizes
     np.savez_compressed(OUT / "plans.npz", **plans)
+    # plan_guided (scheduler.cpp:144-164) on seeded accepted lists: swapped pairs and duplicates included
+    guided = {}
+    rng = np.random.default_rng(17)
+    for (k, np_, m, cnt) in ((10, 3, 2, 12), (23, 4, 2, 60), (40, 5, 3, 200), (9, 1, 4, 36)):
+        acc = rng.integers(0, k, (cnt, 2)).astype(np.uint32)
+        acc = acc[acc[:, 0] != acc[:, 1]]
+        acc = np.concatenate([acc, acc[:3, ::-1], acc[:2]])
+        pairs, sizes = ref.plan_guided(k, np_, m, acc)
+        guided[f"accepted_{k}_{np_}_{m}"] = acc
+        guided[f"pairs_{k}_{np_}_{m}"] = pairs
+        guided[f"sizes_{k}_{np_}_{m}"] = sizes
+    np.savez_compressed(OUT / "plans_guided.npz", **guided)
     # ---- code cache written by the reference (hashing.cpp:184-206) for image 0 of the small dataset --
     cache = {"centering_fp": np.uint64(ref.centering_fingerprint(centering))}
     with tempfile.TemporaryDirectory() as td:

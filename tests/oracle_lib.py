@@ -65,6 +65,7 @@ class Oracle:
             "chor_save_matches": [C.c_char_p, C.c_char_p, P, U32, C.c_char_p],
             "chor_time_match_pairs": [P, P, P, P, P, P, P, U32, U32, P, P],
             "chor_plan_exhaustive": [U32, U32, U32, P, P, P, P],
+            "chor_plan_guided": [U32, U32, U32, P, C.c_uint64, P, P, P, P],
             "chor_centering_fingerprint": [P, P],
             "chor_save_code_cache": [P, U64, P, P, U32, C.c_char_p],
             "chor_load_code_cache": [C.c_char_p, P, U64, U32, P, P, P, P, P],
@@ -256,6 +257,15 @@ class Oracle:
         n, nt = C.c_uint64(0), C.c_uint32(0)
         self._check(self.lib.chor_plan_exhaustive(image_count, block_images, blocks_per_group, pairs.ctypes.data,
                                                   C.byref(n), sizes.ctypes.data, C.byref(nt)), "plan_exhaustive")
+        return pairs[: n.value].copy(), sizes[: nt.value].copy()
+
+    def plan_guided(self, image_count: int, block_images: int, blocks_per_group: int, accepted):
+        acc = np.ascontiguousarray(accepted, dtype=np.uint32).reshape(-1, 2)
+        pairs = np.zeros((max(len(acc), 1), 2), dtype=np.uint32)
+        sizes = np.zeros(max(len(acc), 4), dtype=np.uint32)
+        n, nt = C.c_uint64(0), C.c_uint32(0)
+        self._check(self.lib.chor_plan_guided(image_count, block_images, blocks_per_group, acc.ctypes.data, C.c_uint64(len(acc)),
+                                              pairs.ctypes.data, C.byref(n), sizes.ctypes.data, C.byref(nt)), "plan_guided")
         return pairs[: n.value].copy(), sizes[: nt.value].copy()
 
     def time_match_pairs(self, params, cfg, descs, shorts, longs, pairs, threads: int):

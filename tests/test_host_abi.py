@@ -80,6 +80,39 @@ def test_plan_properties_at_baseline_size():
     assert len(np.unique(key)) == 499500
 
 
+def test_plan_guided_matches_golden_and_oracle(restatement, golden):
+    g = golden["plans_guided"]
+    for key in [k for k in g.files if k.startswith("accepted_")]:
+        k, np_, m = (int(x) for x in key.split("_")[1:])
+        assert np.array_equal(ch.plan_guided(k, np_, m, g[key]), g[f"pairs_{k}_{np_}_{m}"])
+    rng = np.random.default_rng(8)
+    for (k, np_, m) in ((6, 1, 1), (17, 3, 2), (40, 4, 5), (64, 64, 1)):
+        acc = rng.integers(0, k, (4 * k, 2)).astype(np.uint32)
+        acc = acc[acc[:, 0] != acc[:, 1]]
+        assert np.array_equal(ch.plan_guided(k, np_, m, acc), restatement.plan_guided(k, np_, m, acc)[0])
+        # all pairs accepted: the exhaustive plan itself
+        every = ch.plan_exhaustive(k, np_, m)
+        assert np.array_equal(ch.plan_guided(k, np_, m, every[rng.permutation(len(every))]), every)
+    assert len(ch.plan_guided(9, 2, 2, np.zeros((0, 2), np.uint32))) == 0
+    for bad in ([(3, 3)], [(0, 9)], [(12, 1)]):
+        with pytest.raises(ValueError):
+            ch.plan_guided(9, 2, 2, bad)
+
+
+def test_plan_guided_at_config4_size_keeps_neighbours_together():
+    """BASELINE config 4: 16,384 images, pairs (i, i+d), d <= 30 — planned without enumerating 134 M pairs; the plan is
+    a permutation of the list in which consecutive pairs share blocks (what keeps a train image hot in shared memory)."""
+    k = 16384
+    acc = np.array([(i, i + d) for i in range(k) for d in range(1, 31) if i + d < k], dtype=np.uint32)
+    plan = ch.plan_guided(k, 50, 4, acc)
+    assert plan.shape == acc.shape == (491055, 2)
+    key = lambda p: np.sort(p[:, 0].astype(np.int64) * k + p[:, 1])  # noqa: E731
+    assert np.array_equal(key(plan), key(acc))
+    blocks = plan // 50
+    same_task = (blocks[1:] == blocks[:-1]).all(axis=1)
+    assert same_task.mean() > 0.99
+
+
 def test_shard_range_partitions():
     for n in (0, 1, 7, 499500):
         for world in (1, 2, 3, 8):

@@ -318,6 +318,29 @@ def test_restatement_equals_reference_random(restatement, reference, params, n, 
         assert np.array_equal(oa[0], ob[0]) and np.array_equal(oa[1], ob[1])
 
 
+def test_restatement_matches_golden_guided_plans(restatement, golden):
+    g = golden["plans_guided"]
+    for key in [k for k in g.files if k.startswith("accepted_")]:
+        k, np_, m = (int(x) for x in key.split("_")[1:])
+        pairs, sizes = restatement.plan_guided(k, np_, m, g[key])
+        assert np.array_equal(pairs, g[f"pairs_{k}_{np_}_{m}"]) and np.array_equal(sizes, g[f"sizes_{k}_{np_}_{m}"])
+    with pytest.raises(ValueError):
+        restatement.plan_guided(10, 3, 2, [(1, 1)])      # self pair
+    with pytest.raises(ValueError):
+        restatement.plan_guided(10, 3, 2, [(1, 10)])     # unknown image index
+
+
+def test_guided_plans_equal_reference(restatement, reference):
+    rng = np.random.default_rng(4)
+    for (k, np_, m) in ((31, 4, 3), (17, 17, 1), (50, 1, 5)):
+        acc = rng.integers(0, k, (300, 2)).astype(np.uint32)
+        acc = acc[acc[:, 0] != acc[:, 1]]
+        a = reference.plan_guided(k, np_, m, acc)
+        b = restatement.plan_guided(k, np_, m, acc)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert len(reference.plan_guided(9, 2, 2, np.zeros((0, 2), np.uint32))[0]) == 0
+
+
 def test_plans_equal_reference(restatement, reference):
     for k in (1, 2, 3, 5, 8, 13, 20, 33):
         for np_ in (1, 2, 3, 5):
