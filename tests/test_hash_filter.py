@@ -130,3 +130,21 @@ def test_centering_outside_the_bound_premises_uses_the_exact_kernel(matcher, ora
     check(matcher, oracle, fam, cen, [d])
     matcher.set_centering(oracle.centering([d]))
     assert matcher.hash_stats()["filter_active"] == 1
+
+
+def test_more_images_than_one_hash_launch_holds(matcher, oracle):
+    """The filtered path hashes in launches of <= 2,048 images (one undecided-dot queue per launch)."""
+    fam = ch.build_hash_family(ch.FamilyParams())
+    install(matcher, fam)
+    k = 2300
+    d = make_dataset(k, 24, seed=77)
+    cen = oracle.centering(list(d))
+    matcher.set_centering(cen)
+    ids = [BASE + i for i in range(k)]
+    matcher.upload_many(ids, np.ascontiguousarray(d))
+    matcher._test_ids.update(ids)
+    matcher.hash(ids)
+    for i in (0, 1, 2047, 2048, 2049, k - 1):
+        s, l = oracle.compute_codes(fam.params, fam.short_planes, fam.long_planes, cen, d[i])
+        c = matcher.codes(ids[i])
+        assert np.array_equal(c.shorts, s) and np.array_equal(c.longs, l), i

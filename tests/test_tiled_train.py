@@ -122,3 +122,35 @@ def test_external_codes_build_the_tiles(matcher, oracle, default_family):
     want, _ = oracle.match_pair(default_family.params, cfg, d[0], *codes[0], d[1], *codes[1])
     _, got, _ = matcher.match_pairs([(BASE, BASE + 1)], cfg)
     assert np.array_equal(got, want)
+
+
+def test_slot_churn_with_tiles(matcher, oracle, default_family):
+    """Uploads, replacements and evictions of small and large images in random order: image slots, hidden tile
+    slots and arena blocks are recycled; what is resident at the end still matches like the reference."""
+    fresh(matcher, default_family)
+    rng = np.random.default_rng(12)
+    pool = {n: make_dataset(1, n, seed=300 + n)[0] for n in (500, 3000, 11500, 13000, 17000)}
+    cen = oracle.centering(list(pool.values()))
+    matcher.set_centering(cen)
+    resident = {}
+    for step in range(60):
+        slot = BASE + int(rng.integers(0, 6))
+        if slot in resident and rng.random() < 0.3:
+            matcher.evict(slot)
+            matcher._test_ids.discard(slot)
+            del resident[slot]
+        else:
+            n = int(rng.choice(list(pool)))
+            put(matcher, slot, pool[n])
+            resident[slot] = n
+    ids = sorted(resident)
+    assert len(ids) >= 2
+    matcher.hash(ids)
+    cfg = ch.MatchConfig()
+    codes = {n: oracle_codes(oracle, default_family, cen, pool[n]) for n in set(resident.values())}
+    pairs = [(a, b) for a in ids for b in ids if a != b][:8]
+    offs, rec, _ = matcher.match_pairs(pairs, cfg)
+    for k, (a, b) in enumerate(pairs):
+        na, nb = resident[a], resident[b]
+        want, _ = oracle.match_pair(default_family.params, cfg, pool[na], *codes[na], pool[nb], *codes[nb])
+        assert np.array_equal(rec[offs[k]:offs[k + 1]], want), (na, nb)
