@@ -191,6 +191,9 @@ struct chgpu_ctx {
     size_t gmin_cap = 0;
     uint32_t* d_lists = nullptr;  // tiled train images: per-query, per-tile top-k keys
     size_t lists_cap = 0;
+    uint16_t* d_act = nullptr;    // tiled train images: active queries per (query image, tile) pair
+    uint32_t* d_nact = nullptr;
+    size_t act_cap = 0, nact_cap = 0;
     MatchBuffers mb[2];
     DevStats* d_stats = nullptr;
     DevStats* h_stats = nullptr;  // pinned
@@ -900,6 +903,19 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
                     ctx->lists_cap = sb.queries * stride;
                 }
             }
+            const size_t act_stride = (size_t(sb.max_nq) + 7) & ~size_t(7);
+            if (ctx->act_cap < size_t(sb.tile_pairs) * act_stride || ctx->nact_cap < sb.tile_pairs) {
+                CK(cudaStreamSynchronize(ctx->compute));
+                cudaFree(ctx->d_act);
+                cudaFree(ctx->d_nact);
+                ctx->d_act = nullptr;
+                ctx->d_nact = nullptr;
+                ctx->act_cap = ctx->nact_cap = 0;
+                CK(cudaMalloc(&ctx->d_act, size_t(sb.tile_pairs) * act_stride * sizeof(uint16_t)));
+                CK(cudaMalloc(&ctx->d_nact, size_t(sb.tile_pairs) * sizeof(uint32_t)));
+                ctx->act_cap = size_t(sb.tile_pairs) * act_stride;
+                ctx->nact_cap = sb.tile_pairs;
+            }
             uint32_t ntp = 0;
             for (uint32_t k = 0; k < sb.count; ++k) {
                 const PairDesc& pd = descs[sb.first + k];
@@ -919,14 +935,18 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
             CK(cudaEventRecord(b.ev_k0, ctx->compute));
             P.pairs = b.d_tpairs;
             P.nunits = ntp * chunks;
+            P.act = ctx->d_act;
+            P.nact = ctx->d_nact;
+            P.act_stride = uint32_t(act_stride);
             CK(launch_match_tiled(P, kModeTileMin, smem, ctx->prop.multiProcessorCount, ctx->compute, &grid));
+            CK(launch_tile_compact(P, ntp, ctx->compute));
             CK(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), ctx->compute));
             CK(launch_match_tiled(P, kModeTileTopK, smem, ctx->prop.multiProcessorCount, ctx->compute, &grid));
             P.pairs = b.d_pairs;
             CK(launch_tile_merge(P, sb.count, sb.max_nq, ctx->compute));
             CK(cudaEventRecord(b.ev_k1, ctx->compute));
             st.match_launches += 2;
-            st.total_launches += 2;
+            st.total_launches += 3;
         } else {
             CK(cudaEventRecord(b.ev_k0, ctx->compute));
             CK(launch_match(ctx, P, smem_train, sb.max_nt, &grid));
@@ -1057,7 +1077,7 @@ void chgpu_destroy(chgpu_ctx* ctx) {
     }
     cudaFree(ctx->d_planes); cudaFree(ctx->d_centering); cudaFree(ctx->d_sums); cudaFree(ctx->d_res);
     cudaFree(ctx->d_stats); cudaFreeHost(ctx->h_stats); cudaFree(ctx->d_counter); cudaFree(ctx->d_slots);
-    cudaFree(ctx->d_dbg); cudaFree(ctx->d_gmin); cudaFree(ctx->d_gdone); cudaFree(ctx->d_lists);
+    cudaFree(ctx->d_dbg); cudaFree(ctx->d_gmin); cudaFree(ctx->d_gdone); cudaFree(ctx->d_lists); cudaFree(ctx->d_act); cudaFree(ctx->d_nact);
     cudaFreeHost(ctx->load_pinned);
     for (auto& b : ctx->load_scratch) cudaFree(b.first);
     cudaFree(ctx->d_planes_t); cudaFree(ctx->d_bias); cudaFree(ctx->d_hnorm); cudaFree(ctx->d_hq);

@@ -101,6 +101,9 @@ struct MatchParams {
     uint32_t* lists;            // per query: list_stride keys, tile t's top_k keys at [t * top_k, (t + 1) * top_k)
     uint32_t list_stride;
     uint32_t tile_points;       // point ids per tile
+    uint16_t* act;              // per (query image, tile) pair: the queries the top-k pass has to visit ...
+    uint32_t* nact;             // ... and how many (tile_compact_kernel)
+    uint32_t act_stride;
 };
 
 // Train images too large for the shared-memory tile are matched tile by tile: every id range of
@@ -110,8 +113,9 @@ struct MatchParams {
 //   MODE 1 (kTileMin)   scan: the smallest key of the tile joins gmin[query] (atomicMin).  Most queries have no
 //                       candidate within tau in any tile and are finished after this pass.  A tile that itself
 //                       has one writes its list (below) right away and marks it in gdone[query].
-//   MODE 2 (kTileTopK)  queries with gmin within tau, tiles not yet marked: the tile's top_k smallest distinct
-//                       keys, no threshold, global point ids, go to lists[query][tile].
+//   MODE 2 (kTileTopK)  queries with gmin within tau, tiles not yet marked (tile_compact_kernel lists them per
+//                       (query image, tile) pair, so the pass walks a dense list): the tile's top_k smallest
+//                       distinct keys, no threshold, global point ids, go to lists[query][tile].
 // tile_merge_kernel then merges the lists of a query, applies the threshold / re-rank rule of
 // matcher.cpp:176-189 to the merged ranking and verifies it exactly like MODE 0 does.
 constexpr int kModeMatch = 0, kModeTileMin = 1, kModeTileTopK = 2;
@@ -407,8 +411,12 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
         }
 
         // query range of this unit: chunks are multiples of 32 queries
-        const uint32_t qc = (((I.n + P.chunks_per_pair - 1) / P.chunks_per_pair) + 31u) & ~31u;
-        const uint32_t q0 = min(I.n, chunk * qc), q1 = min(I.n, q0 + qc);
+        // (MODE 2 walks positions of the pair's active-query list instead of query indices)
+        const uint32_t nq_unit = MODE == kModeTileTopK ? __ldg(P.nact + pair) : I.n;
+        const uint32_t qc = (((nq_unit + P.chunks_per_pair - 1) / P.chunks_per_pair) + 31u) & ~31u;
+        const uint32_t q0 = min(nq_unit, chunk * qc), q1 = min(nq_unit, q0 + qc);
+        const uint16_t* __restrict__ act = MODE == kModeTileTopK ? P.act + uint64_t(pair) * P.act_stride : nullptr;
+        uint32_t qa_lane = 0;  // MODE 2: the query index behind batch position `lane`
         const uint16_t* __restrict__ ids = CH_IDS(J);
 
         uint32_t st_raw = 0, st_vq = 0, st_dist = 0, st_match = 0;
@@ -422,17 +430,12 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
             // and parks them, with the query's long code, in the warp's staging area: the global-memory
             // round trip for the query-side data is paid once per batch, not once per query.
             auto lookup_batch = [&](uint32_t qb) {
-                const uint32_t q = qb + lane * kWarps;
-                bool live = lane < kBatch && q < q1;
-                if (MODE == kModeTileTopK && live &&
-                    ((__ldg(P.gmin + pd.res_off + q) >> 24) > P.tau || ((__ldg(P.gdone + pd.res_off + q) >> pd.tile_idx) & 1ull))) {
-                    // nothing within tau in any tile, or this tile's list was written by the min pass: the query is
-                    // skipped (sentinel header, harmless ranges)
-                    const uint32_t rec = s_stage + lane * kRec;
-                    sts128(rec + 16u, make_uint4(kNone, 0u, 0u, 0u));
-#pragma unroll
-                    for (int t = 0; t < LT; ++t) sts64(rec + 32u + t * 8u, 0u, 0u);
-                    live = false;
+                const uint32_t qpos = qb + lane * kWarps;
+                const bool live = lane < kBatch && qpos < q1;
+                uint32_t q = qpos;
+                if (MODE == kModeTileTopK) {
+                    q = live ? uint32_t(__ldg(act + qpos)) : 0u;
+                    qa_lane = q;
                 }
                 if (live) {
                     const uint32_t* __restrict__ qcodes = I.shorts + uint64_t(q) * L;
@@ -510,8 +513,9 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                 // ranks nothing either way; the line and the filter are evaluated only for the others.
                 EpiLine line{};
 
-                const bool skip = MODE == kModeTileTopK && hdr.x == kNone;  // see lookup_batch
-                bool emit = MODE == kModeTileTopK && !skip;                 // this (query, tile) writes its list
+                constexpr bool skip = false;
+                bool emit = MODE == kModeTileTopK;  // this (query, tile) writes its list
+                const uint32_t qa = MODE == kModeTileTopK ? __shfl_sync(FULL, qa_lane, slot) : q;  // the query's index
                 if (skip) {
                 } else if (tover <= 32u * kOverSlots) {
                     // ---- 2. Hamming scan: the first 32 entries of every bucket, one table per slot,
@@ -664,7 +668,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 
                 if (MODE != kModeMatch && emit) {
                     if (lane < P.top_k)
-                        P.lists[(pd.res_off + q) * P.list_stride + pd.tile_idx * P.top_k + lane] = lane < n ? mykey + pd.tile_base : kNone;
+                        P.lists[(pd.res_off + qa) * P.list_stride + pd.tile_idx * P.top_k + lane] = lane < n ? mykey + pd.tile_base : kNone;
                     if (MODE == kModeTileMin && lane == 0) atomicOr(P.gdone + pd.res_off + q, 1ull << pd.tile_idx);
                 }
 
@@ -707,6 +711,28 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 // then cut by the threshold / re-rank rule (matcher.cpp:176-189) and verified (matcher.cpp:106-137).
 // Whether the threshold cut anything can be read off the lists: a tile with a candidate beyond tau that is
 // not in its list has a full list within tau, and then the merged ranking is full as well.
+// The queries the top-k pass visits for every (query image, tile) pair: gmin within tau and the tile's list not
+// yet written by the min pass.  One warp per pair, ballot compaction in query order.
+template <int kInstance>
+__global__ void tile_compact_kernel(const MatchParams P, uint32_t ntile_pairs) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t tp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (tp >= ntile_pairs) return;
+    const PairDesc pd = P.pairs[tp];
+    const uint32_t nq = P.images[pd.slot_i].n;
+    uint16_t* __restrict__ out = P.act + uint64_t(tp) * P.act_stride;
+    uint32_t count = 0;
+    for (uint32_t q0 = 0; q0 < nq; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        const bool f = q < nq && (__ldg(P.gmin + pd.res_off + q) >> 24) <= P.tau &&
+                       !((__ldg(P.gdone + pd.res_off + q) >> pd.tile_idx) & 1ull);
+        const uint32_t bal = __ballot_sync(0xffffffffu, f);
+        if (f) out[count + __popc(bal & ((1u << lane) - 1u))] = uint16_t(q);
+        count += __popc(bal);
+    }
+    if (lane == 0) P.nact[tp] = count;
+}
+
 constexpr int kMergeThreads = 256;
 constexpr uint32_t kMergeChunk = 1024;  // queries per CTA
 template <int kInstance>

@@ -17,6 +17,7 @@ cudaError_t launch_match_guided(const MatchParams& P, bool smem_train, size_t sm
 // Tiled train images (match_tiled.cu): mode = kModeTileMin / kModeTileTopK over (query image, tile) pairs with the
 // tile's codes in shared memory, then the per-query merge + verification over the original pairs.
 cudaError_t launch_match_tiled(const MatchParams& P, int mode, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid);
+cudaError_t launch_tile_compact(const MatchParams& P, uint32_t ntile_pairs, cudaStream_t stream);  // P.pairs = tile pairs
 cudaError_t launch_tile_merge(const MatchParams& P, uint32_t npairs, uint32_t max_nq, cudaStream_t stream);
 // Table slots (LT) the launchers pick for L tables; the staging area is sized with it.
 inline int match_table_slots(uint32_t L, bool guided) { return guided ? (L == 6 ? 6 : 8) : (L <= 4 ? 4 : (L <= 6 ? 6 : 8)); }

@@ -22,6 +22,12 @@ cudaError_t launch_match_tiled(const MatchParams& P, int mode, size_t smem, int 
                                 : launch_tiled_mode<kModeTileTopK>(P, smem, sm_count, stream, grid);
 }
 
+cudaError_t launch_tile_compact(const MatchParams& P, uint32_t ntile_pairs, cudaStream_t stream) {
+    if (ntile_pairs == 0) return cudaSuccess;
+    tile_compact_kernel<0><<<(ntile_pairs + 7) / 8, 256, 0, stream>>>(P, ntile_pairs);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_tile_merge(const MatchParams& P, uint32_t npairs, uint32_t max_nq, cudaStream_t stream) {
     if (npairs == 0 || max_nq == 0) return cudaSuccess;
     const dim3 grid(npairs, (max_nq + kMergeChunk - 1) / kMergeChunk);
