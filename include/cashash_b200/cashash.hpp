@@ -26,6 +26,7 @@
 // std::runtime_error when no sm_100 device is present.
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <cstdio>
@@ -39,6 +40,8 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <exception>
+#include <thread>
 #include <vector>
 
 #include "../chgpu.h"
@@ -763,5 +766,110 @@ inline std::vector<MatchRecord> guided_match_pair(const FeatureSet& fs_i, const 
     std::vector<PairMatches> out = m.match_pairs_guided({&pr, 1}, {&f, 1}, band_px, cfg);
     return std::move(out.front().matches);
 }
+
+// Several GPUs of one box from one process: one Matcher (context) and one host thread per lane, the working set
+// replicated on every lane, the pair list cut into contiguous shards of the plan (chgpu_shard_range), results
+// gathered in pair order on the host.  No device-to-device traffic: pairs are independent.  The
+// reference's counterpart is its W worker threads over one in-memory arena (execute_plan, engine.cpp:667-702);
+// paper_1805_08995_b200/sharding.py is the same protocol with one process per GPU.
+class MultiGpuMatcher {
+public:
+    // devices: CUDA device ordinals, one lane each (an ordinal may repeat: lanes then share that GPU)
+    explicit MultiGpuMatcher(std::span<const int> devices) {
+        if (devices.empty()) throw std::invalid_argument("MultiGpuMatcher: no devices");
+        for (const int d : devices) lanes_.push_back(std::make_unique<Matcher>(d));
+    }
+    std::size_t lane_count() const { return lanes_.size(); }
+    Matcher& lane(std::size_t k) { return *lanes_[k]; }
+
+    void set_family(const HashFamily& family) {
+        for (auto& m : lanes_) m->set_family(family);
+    }
+    void upload(std::uint32_t image_id, const FeatureSet& fs) {
+        for (auto& m : lanes_) m->upload(image_id, fs);
+    }
+    // Dataset centering from the resident images: lane k sums images k, k + G, ... ; the partial sums are
+    // exchanged on the host (128 u64 + a count) and every lane installs the same vector (hashing.cpp:52-64).
+    std::array<double, kDescriptorDim> set_centering(std::span<const std::uint32_t> image_ids) {
+        const std::size_t G = lanes_.size();
+        std::array<std::uint64_t, kDescriptorDim> total{};
+        std::uint64_t count = 0;
+        std::vector<std::array<std::uint64_t, kDescriptorDim>> part(G);
+        std::vector<std::uint64_t> cnt(G, 0);
+        each_lane([&](std::size_t k) {
+            std::vector<std::uint32_t> mine;
+            for (std::size_t i = k; i < image_ids.size(); i += G) mine.push_back(image_ids[i]);
+            lanes_[k]->centering_reset();
+            lanes_[k]->centering_add(mine);
+            ck_lane(k, chgpu_centering_get_sums(lanes_[k]->handle(), part[k].data(), &cnt[k]));
+        });
+        for (std::size_t k = 0; k < G; ++k) {
+            for (int x = 0; x < kDescriptorDim; ++x) total[x] += part[k][x];
+            count += cnt[k];
+        }
+        if (count == 0) throw std::invalid_argument("set_centering: no descriptors");
+        std::array<double, kDescriptorDim> c{};
+        for (int x = 0; x < kDescriptorDim; ++x) c[x] = static_cast<double>(total[x]) / static_cast<double>(count);
+        for (std::size_t k = 0; k < G; ++k) ck_lane(k, chgpu_set_centering(lanes_[k]->handle(), c.data()));
+        return c;
+    }
+    void hash(std::span<const std::uint32_t> image_ids, int reduce_rounds = kDefaultReduceRounds) {
+        each_lane([&](std::size_t k) { lanes_[k]->hash(image_ids, reduce_rounds); });
+    }
+    // The pair list in contiguous shards, one per lane, matched concurrently; results in pair order.
+    std::vector<PairMatches> match_pairs(std::span<const std::pair<std::uint32_t, std::uint32_t>> pairs,
+                                         const MatchConfig& cfg, MatchStats* stats = nullptr) {
+        const std::size_t G = lanes_.size();
+        std::vector<std::vector<PairMatches>> part(G);
+        std::vector<MatchStats> st(G);
+        each_lane([&](std::size_t k) {
+            std::uint64_t first = 0, last = 0;
+            chgpu_shard_range(pairs.size(), static_cast<std::uint32_t>(k), static_cast<std::uint32_t>(G), &first, &last);
+            part[k] = lanes_[k]->match_pairs(pairs.subspan(first, last - first), cfg, &st[k]);
+        });
+        std::vector<PairMatches> out;
+        out.reserve(pairs.size());
+        MatchStats sum{};
+        for (std::size_t k = 0; k < G; ++k) {
+            for (PairMatches& pm : part[k]) out.push_back(std::move(pm));
+            sum.pairs += st[k].pairs;
+            sum.matches += st[k].matches;
+            sum.raw_candidates += st[k].raw_candidates;
+            sum.verified_queries += st[k].verified_queries;
+            sum.distances += st[k].distances;
+            sum.query_points += st[k].query_points;
+            sum.train_points += st[k].train_points;
+            sum.match_launches += st[k].match_launches;
+            sum.total_launches += st[k].total_launches;
+            sum.match_kernel_ms = std::max(sum.match_kernel_ms, st[k].match_kernel_ms);  // lanes run side by side
+            sum.total_ms = std::max(sum.total_ms, st[k].total_ms);
+        }
+        sum.records_checksum = 0;  // keyed by the pair's position in the list each lane saw: not additive over shards
+        if (stats) *stats = sum;
+        return out;
+    }
+
+private:
+    template <class F>
+    void each_lane(F&& f) {  // one host thread per lane; the first exception is rethrown on the caller's thread
+        std::vector<std::thread> threads;
+        std::vector<std::exception_ptr> errors(lanes_.size());
+        for (std::size_t k = 0; k < lanes_.size(); ++k)
+            threads.emplace_back([&, k] {
+                try {
+                    f(k);
+                } catch (...) {
+                    errors[k] = std::current_exception();
+                }
+            });
+        for (std::thread& t : threads) t.join();
+        for (const std::exception_ptr& e : errors)
+            if (e) std::rethrow_exception(e);
+    }
+    void ck_lane(std::size_t k, chgpu_status st) {
+        if (st != CHGPU_OK) detail::raise(st, chgpu_last_error(lanes_[k]->handle()));
+    }
+    std::vector<std::unique_ptr<Matcher>> lanes_;
+};
 
 }  // namespace cashash_b200

@@ -372,6 +372,23 @@ static void device_checks(const std::filesystem::path& tmp) {
             CHECK(e.fault() == ch::FeatureFileFault::Truncated && e.byte_offset() == blob.size() - 5);
         }
         CHECK(throws<std::out_of_range>([&] { m.codes(12345); }));
+
+        // several lanes (here: three contexts on the one GPU): replicated working set, sharded pair list,
+        // partial centering sums exchanged on the host — the same records in the same order
+        const int devs[3] = {0, 0, 0};
+        ch::MultiGpuMatcher mg(devs);
+        CHECK(mg.lane_count() == 3);
+        mg.set_family(fam2);
+        for (std::uint32_t i = 0; i < sets.size(); ++i) mg.upload(i, sets[i]);
+        CHECK(mg.set_centering(ids) == fam.centering);
+        mg.hash(ids);
+        ch::MatchStats mst{};
+        const auto mres = mg.match_pairs(pairs, {}, &mst);
+        CHECK(mres.size() == res.size() && mst.pairs == st.pairs && mst.matches == st.matches &&
+              mst.raw_candidates == st.raw_candidates && mst.distances == st.distances);
+        for (std::size_t k = 0; k < res.size(); ++k)
+            CHECK(mres[k].image_i == res[k].image_i && mres[k].image_j == res[k].image_j && mres[k].matches == res[k].matches);
+        CHECK(throws<std::out_of_range>([&] { mg.hash(std::vector<std::uint32_t>{777}); }));  // a lane's error surfaces
     }
 }
 
