@@ -448,7 +448,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
-            "dtype": "u8/u32 popcount + exact integer distances (fp64 ratio test, fp64 exact-order hashing)",
+            "dtype": "u8/u32 popcount + exact integer distances (fp64 ratio test; hashing: fp32 filter + exact fp64 re-evaluation)",
             "data": "synthetic", "config": workload_config(args, npairs), "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "wall_ms_per_step": 1e3 * wall_s / args.steps, "setup_s": setup_s,

@@ -240,7 +240,8 @@ size_t smem_train_capacity(const chgpu_ctx* ctx, bool guided = false);
 // Point ids per tile of a large train image: what fits the kernel's shared memory, at most ~32 entries per
 // bucket (the occupancy the scan is laid out for), a multiple of 1024.
 uint32_t tile_points_of(const chgpu_ctx* ctx) {
-    const size_t cap = smem_train_capacity(ctx) & ~size_t(1023);
+    // (the guided top-k pass stages more per warp than the unguided kernels: its capacity is the binding one)
+    const size_t cap = std::min(smem_train_capacity(ctx, false), smem_train_capacity(ctx, true)) & ~size_t(1023);
     const size_t want = std::max<size_t>(1024, size_t(32) << ctx->fam.short_bits);
     return uint32_t(std::max<size_t>(1024, std::min(cap, want)));
 }
@@ -731,14 +732,14 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
             if (!(I.flags & 1u) || !(J.flags & 1u))
                 return fail(ctx, CHGPU_ELOGIC, "pair (%u,%u): codes not computed (call chgpu_hash_images first)",
                             run.pairs[2 * k], run.pairs[2 * k + 1]);
-            const uint32_t tiles = run.fmats ? 0u : uint32_t(ctx->images[sj].tile_slots.size());
+            const uint32_t tiles = uint32_t(ctx->images[sj].tile_slots.size());
             const bool tiled = tiles != 0;
             if (cur.count && (cur.queries + I.n > ctx->sub_batch_queries || cur.count >= (1u << 20) || tiled != cur.tiled ||
                               (tiled && (cur.queries + I.n) * std::max(cur.max_tiles, tiles) * run.cfg.top_k * 4 > kTileListBytes))) {
                 subs.push_back(cur);
                 cur = SubBatch{k, 0, 0, 0, 0, false, 0, 0};
             }
-            descs[k] = PairDesc{si, sj, cur.queries, 0u, 0u};
+            descs[k] = PairDesc{si, sj, cur.queries, 0u, 0u, cur.count, 0u};
             cur.tiled = tiled;
             cur.max_tiles = std::max(cur.max_tiles, tiles);
             cur.tile_pairs += tiles;
@@ -920,7 +921,7 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
             for (uint32_t k = 0; k < sb.count; ++k) {
                 const PairDesc& pd = descs[sb.first + k];
                 const std::vector<uint32_t>& ts = ctx->images[pd.slot_j].tile_slots;
-                for (uint32_t t = 0; t < ts.size(); ++t) b.h_tpairs[ntp++] = PairDesc{pd.slot_i, ts[t], pd.res_off, t * tp, t};
+                for (uint32_t t = 0; t < ts.size(); ++t) b.h_tpairs[ntp++] = PairDesc{pd.slot_i, ts[t], pd.res_off, t * tp, t, k, 0u};
             }
             CK(cudaMemcpyAsync(b.d_tpairs, b.h_tpairs, size_t(ntp) * sizeof(PairDesc), cudaMemcpyHostToDevice, ctx->compute));
             CK(cudaMemsetAsync(ctx->d_gmin, 0xff, sb.queries * sizeof(uint32_t), ctx->compute));
@@ -932,6 +933,7 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
             P.tile_points = tp;
             P.smem_long_bytes = std::min(tp, sb.max_nt) * 16u;
             const size_t smem = size_t(P.smem_long_bytes) + offs_smem_bytes(ctx) + stage_smem_bytes(ctx);
+            const size_t smem_topk = size_t(P.smem_long_bytes) + offs_smem_bytes(ctx) + stage_smem_bytes(ctx, run.fmats != nullptr);
             CK(cudaEventRecord(b.ev_k0, ctx->compute));
             P.pairs = b.d_tpairs;
             P.nunits = ntp * chunks;
@@ -941,7 +943,7 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
             CK(launch_match_tiled(P, kModeTileMin, smem, ctx->prop.multiProcessorCount, ctx->compute, &grid));
             CK(launch_tile_compact(P, ntp, ctx->compute));
             CK(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), ctx->compute));
-            CK(launch_match_tiled(P, kModeTileTopK, smem, ctx->prop.multiProcessorCount, ctx->compute, &grid));
+            CK(launch_match_tiled(P, kModeTileTopK, smem_topk, ctx->prop.multiProcessorCount, ctx->compute, &grid));
             P.pairs = b.d_pairs;
             CK(launch_tile_merge(P, sb.count, sb.max_nq, ctx->compute));
             CK(cudaEventRecord(b.ev_k1, ctx->compute));

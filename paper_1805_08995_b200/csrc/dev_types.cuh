@@ -41,6 +41,8 @@ struct PairDesc {
     uint64_t res_off;    // first entry of this pair in the per-query result scratch
     uint32_t tile_base;  // tiles: first point id of the tile inside its image
     uint32_t tile_idx;   // tiles: position of the tile's list in the per-query list scratch
+    uint32_t pair_idx;   // position of the (whole-image) pair in its sub-batch: per-pair inputs such as fmats
+    uint32_t reserved;
 };
 
 struct DevStats {

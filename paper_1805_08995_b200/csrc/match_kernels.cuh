@@ -555,15 +555,16 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                         if (uint32_t(s) * 32u < tover) key[LT + s] = key_of<SMEM_TRAIN>(key[LT + s], ql, s_long, J.longs);
                     // ---- 3. ranking: pull straight out of the slots -------------------------------
                     uint32_t k0 = first_key(key, kNone);
-                    if (GUIDED && (k0 >> 24) <= P.tau) {
-                        line = epipolar_band(P.fmats + uint64_t(pair) * 9, __ldg(I.kp + q));
+                    if (GUIDED && (MODE == kModeTileTopK || (k0 >> 24) <= P.tau)) {
+                        line = epipolar_band(P.fmats + uint64_t(pd.pair_idx) * 9, __ldg(I.kp + qa));
 #pragma unroll
                         for (int i = 0; i < KS; ++i) key[i] = band_filter(key[i], line, J.kp, P.band_px);
                         k0 = first_key(key, kNone);
                     }
                     if (MODE == kModeTileMin) {
                         if (lane == 0 && k0 != kNone) atomicMin(P.gmin + pd.res_off + q, k0);
-                        emit = (k0 >> 24) <= P.tau;  // the tile itself has a candidate within tau
+                        // the tile itself has a candidate within tau (guided runs filter first: top-k pass only)
+                        emit = (k0 >> 24) <= P.tau && P.fmats == nullptr;
                     }
                     if (MODE == kModeTileMin && !emit) {
                     } else if (MODE != kModeMatch) {
@@ -622,13 +623,13 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     const uint32_t gmin = __reduce_min_sync(FULL, lmin);
                     if (MODE == kModeTileMin) {
                         if (lane == 0 && gmin != kNone) atomicMin(P.gmin + pd.res_off + q, gmin);
-                        emit = (gmin >> 24) <= P.tau;
+                        emit = (gmin >> 24) <= P.tau && P.fmats == nullptr;
                     }
                     if (MODE == kModeTileMin && !emit) {
                     } else if (MODE != kModeMatch || (gmin >> 24) <= P.tau) {
                         // pass 2: merge every round into the running top-k (ascending, unique)
                         if (GUIDED) {
-                            line = epipolar_band(P.fmats + uint64_t(pair) * 9, __ldg(I.kp + q));
+                            line = epipolar_band(P.fmats + uint64_t(pd.pair_idx) * 9, __ldg(I.kp + qa));
                             lmax = 0;
                         }
                         for (uint32_t off = 0; off < maxlen; off += 32u) {
@@ -662,7 +663,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                         const uint32_t tot = __popc(__ballot_sync(FULL, mykey != kNone));
                         const uint32_t s = __popc(__ballot_sync(FULL, mykey != kNone && (mykey >> 24) <= P.tau));
                         n = (MODE == kModeMatch && (s >= P.min_ranked || !anycut)) ? s : tot;
-                        if (GUIDED && s == 0) n = 0;  // the band removed everything within tau: no ranking, no fallback
+                        if (GUIDED && MODE == kModeMatch && s == 0) n = 0;  // the band removed everything within tau: no ranking, no fallback
                     }
                 }
 
@@ -769,6 +770,7 @@ __global__ void __launch_bounds__(kMergeThreads) tile_merge_kernel(const MatchPa
             const uint32_t tot = __popc(__ballot_sync(FULL, mykey != kNone));
             const uint32_t s = __popc(__ballot_sync(FULL, mykey != kNone && (mykey >> 24) <= P.tau));
             n = (s >= P.min_ranked || !anycut) ? s : tot;
+            if (s == 0) n = 0;  // guided runs: the band removed everything within tau (no ranking, no fallback)
         }
         if (P.dbg_ranked != nullptr) {
             if (lane < n) P.dbg_ranked[uint64_t(q) * P.top_k + lane] = mykey & 0xffffffu;

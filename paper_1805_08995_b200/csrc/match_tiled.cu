@@ -18,8 +18,11 @@ static cudaError_t launch_tiled_mode(const MatchParams& P, size_t smem, int sm_c
 }
 
 cudaError_t launch_match_tiled(const MatchParams& P, int mode, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid) {
-    return mode == kModeTileMin ? launch_tiled_mode<kModeTileMin>(P, smem, sm_count, stream, grid)
-                                : launch_tiled_mode<kModeTileTopK>(P, smem, sm_count, stream, grid);
+    if (mode == kModeTileMin) return launch_tiled_mode<kModeTileMin>(P, smem, sm_count, stream, grid);  // never filtered
+    if (P.fmats != nullptr)  // epipolar-guided top-k pass: the table slots of match_guided.cu
+        return P.L == 6 ? launch_match_variant<true, 6, true, true, kModeTileTopK>(P, smem, sm_count, stream, grid)
+                        : launch_match_variant<true, 8, false, true, kModeTileTopK>(P, smem, sm_count, stream, grid);
+    return launch_tiled_mode<kModeTileTopK>(P, smem, sm_count, stream, grid);
 }
 
 cudaError_t launch_tile_compact(const MatchParams& P, uint32_t ntile_pairs, cudaStream_t stream) {

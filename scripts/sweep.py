@@ -56,13 +56,15 @@ def main():
     ap.add_argument("--shapes", nargs="*", default=["uniform", "sift"])
     ap.add_argument("--images", type=int, default=64)
     ap.add_argument("--no-guided", action="store_true")
+    ap.add_argument("--guided-points", type=int, nargs="*", default=[8192])
     args = ap.parse_args()
     with ch.Matcher(0) as m:
         for shape in args.shapes:
             for n in args.points:
                 print(json.dumps(run(m, n, shape, images=args.images)), flush=True)
         if not args.no_guided:
-            print(json.dumps(run(m, 8192, "uniform", guided=True)), flush=True)
+            for n in args.guided_points:
+                print(json.dumps(run(m, n, "uniform", images=args.images, guided=True)), flush=True)
 
 
 if __name__ == "__main__":

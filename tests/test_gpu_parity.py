@@ -527,7 +527,8 @@ def _keypoints(n, seed, integer=False):
 
 
 @pytest.mark.parametrize("n_i,n_j,params", [(1500, 1500, ch.FamilyParams()), (900, 2100, ch.FamilyParams()),
-                                             (16384, 16384, ch.FamilyParams()), (1200, 1200, ch.FamilyParams(7, 100, 5, 42))])
+                                             (16384, 16384, ch.FamilyParams()), (1200, 1200, ch.FamilyParams(7, 100, 5, 42)),
+                                             (2000, 24577, ch.FamilyParams()), (1500, 13000, ch.FamilyParams(10, 96, 4, 99))])
 def test_guided_match_bit_exact(matcher, oracle, n_i, n_j, params):
     fam = ch.build_hash_family(params)
     fresh(matcher, fam)
