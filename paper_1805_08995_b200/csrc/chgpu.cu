@@ -904,24 +904,31 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
                     ctx->lists_cap = sb.queries * stride;
                 }
             }
-            const size_t act_stride = (size_t(sb.max_nq) + 7) & ~size_t(7);
-            if (ctx->act_cap < size_t(sb.tile_pairs) * act_stride || ctx->nact_cap < sb.tile_pairs) {
+            // active-query scratch: one slice of nq entries per (query image, tile) pair, packed (the list-scratch cap
+            // above bounds the sum over the sub-batch by 2^30 / (4 top_k) entries)
+            uint32_t ntp = 0;
+            size_t act_need = 0;
+            for (uint32_t k = 0; k < sb.count; ++k) {
+                const PairDesc& pd = descs[sb.first + k];
+                const std::vector<uint32_t>& ts = ctx->images[pd.slot_j].tile_slots;
+                const size_t nq = (size_t(ctx->images[pd.slot_i].dev.n) + 7) & ~size_t(7);
+                for (uint32_t t = 0; t < ts.size(); ++t) {
+                    b.h_tpairs[ntp++] = PairDesc{pd.slot_i, ts[t], pd.res_off, t * tp, t, k, uint32_t(act_need)};
+                    act_need += nq;
+                }
+            }
+            if (act_need > UINT32_MAX) return fail(ctx, CHGPU_EUNSUPPORTED, "tiled sub-batch too large (%zu active-query slots)", act_need);
+            if (ctx->act_cap < act_need || ctx->nact_cap < sb.tile_pairs) {
                 CK(cudaStreamSynchronize(ctx->compute));
                 cudaFree(ctx->d_act);
                 cudaFree(ctx->d_nact);
                 ctx->d_act = nullptr;
                 ctx->d_nact = nullptr;
                 ctx->act_cap = ctx->nact_cap = 0;
-                CK(cudaMalloc(&ctx->d_act, size_t(sb.tile_pairs) * act_stride * sizeof(uint16_t)));
+                CK(cudaMalloc(&ctx->d_act, std::max<size_t>(act_need, 8) * sizeof(uint16_t)));
                 CK(cudaMalloc(&ctx->d_nact, size_t(sb.tile_pairs) * sizeof(uint32_t)));
-                ctx->act_cap = size_t(sb.tile_pairs) * act_stride;
+                ctx->act_cap = std::max<size_t>(act_need, 8);
                 ctx->nact_cap = sb.tile_pairs;
-            }
-            uint32_t ntp = 0;
-            for (uint32_t k = 0; k < sb.count; ++k) {
-                const PairDesc& pd = descs[sb.first + k];
-                const std::vector<uint32_t>& ts = ctx->images[pd.slot_j].tile_slots;
-                for (uint32_t t = 0; t < ts.size(); ++t) b.h_tpairs[ntp++] = PairDesc{pd.slot_i, ts[t], pd.res_off, t * tp, t, k, 0u};
             }
             CK(cudaMemcpyAsync(b.d_tpairs, b.h_tpairs, size_t(ntp) * sizeof(PairDesc), cudaMemcpyHostToDevice, ctx->compute));
             CK(cudaMemsetAsync(ctx->d_gmin, 0xff, sb.queries * sizeof(uint32_t), ctx->compute));
@@ -939,7 +946,6 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
             P.nunits = ntp * chunks;
             P.act = ctx->d_act;
             P.nact = ctx->d_nact;
-            P.act_stride = uint32_t(act_stride);
             CK(launch_match_tiled(P, kModeTileMin, smem, ctx->prop.multiProcessorCount, ctx->compute, &grid));
             CK(launch_tile_compact(P, ntp, ctx->compute));
             CK(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), ctx->compute));

@@ -42,7 +42,7 @@ struct PairDesc {
     uint32_t tile_base;  // tiles: first point id of the tile inside its image
     uint32_t tile_idx;   // tiles: position of the tile's list in the per-query list scratch
     uint32_t pair_idx;   // position of the (whole-image) pair in its sub-batch: per-pair inputs such as fmats
-    uint32_t reserved;
+    uint32_t act_off;    // tiles: first entry of this (query image, tile) pair in the active-query scratch
 };
 
 struct DevStats {

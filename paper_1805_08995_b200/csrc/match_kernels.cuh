@@ -101,9 +101,8 @@ struct MatchParams {
     uint32_t* lists;            // per query: list_stride keys, tile t's top_k keys at [t * top_k, (t + 1) * top_k)
     uint32_t list_stride;
     uint32_t tile_points;       // point ids per tile
-    uint16_t* act;              // per (query image, tile) pair: the queries the top-k pass has to visit ...
+    uint16_t* act;              // per (query image, tile) pair, at PairDesc::act_off: the queries the top-k pass visits ...
     uint32_t* nact;             // ... and how many (tile_compact_kernel)
-    uint32_t act_stride;
 };
 
 // Train images too large for the shared-memory tile are matched tile by tile: every id range of
@@ -415,7 +414,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
         const uint32_t nq_unit = MODE == kModeTileTopK ? __ldg(P.nact + pair) : I.n;
         const uint32_t qc = (((nq_unit + P.chunks_per_pair - 1) / P.chunks_per_pair) + 31u) & ~31u;
         const uint32_t q0 = min(nq_unit, chunk * qc), q1 = min(nq_unit, q0 + qc);
-        const uint16_t* __restrict__ act = MODE == kModeTileTopK ? P.act + uint64_t(pair) * P.act_stride : nullptr;
+        const uint16_t* __restrict__ act = MODE == kModeTileTopK ? P.act + pd.act_off : nullptr;
         uint32_t qa_lane = 0;  // MODE 2: the query index behind batch position `lane`
         const uint16_t* __restrict__ ids = CH_IDS(J);
 
@@ -721,7 +720,7 @@ __global__ void tile_compact_kernel(const MatchParams P, uint32_t ntile_pairs) {
     if (tp >= ntile_pairs) return;
     const PairDesc pd = P.pairs[tp];
     const uint32_t nq = P.images[pd.slot_i].n;
-    uint16_t* __restrict__ out = P.act + uint64_t(tp) * P.act_stride;
+    uint16_t* __restrict__ out = P.act + pd.act_off;
     uint32_t count = 0;
     for (uint32_t q0 = 0; q0 < nq; q0 += 32) {
         const uint32_t q = q0 + lane;
