@@ -73,7 +73,7 @@ def measured_peak_hbm() -> tuple[float, str]:
 
 def recorded_instructions_per_query():
     """Warp instructions per query point of the match kernel, from the committed ncu --set full summary."""
-    p = ROOT / "profiles" / "r01k_match_kernel_ncu_full.json"
+    p = ROOT / "profiles" / "r01l_match_kernel_ncu_full.json"
     try:
         return float(json.loads(p.read_text())["kernels"][0]["warp_instructions_per_query"])
     except Exception:  # noqa: BLE001
@@ -379,7 +379,7 @@ def run_ours(args):
     roofline["on_chip"] = {"bound": "xu_popc", "achieved_gpopc_s": popc_rate / 1e9, "peak_gpopc_s": popc_peak / 1e9,
                            "frac": popc_rate / popc_peak,
                            "note": "lower bound on POPC work (padding lanes not counted); ncu pipe utilisations of the "
-                                   "committed capture: profiles/r01k_match_kernel_ncu_full.json"}
+                                   "committed capture: profiles/r01l_match_kernel_ncu_full.json"}
 
     # the limit the kernel actually runs into: warp-instruction issue slots (4 per clock per SM).  Instructions
     # per query come from the committed ncu capture of this kernel; the rate is this run's.
@@ -391,7 +391,7 @@ def run_ours(args):
             "bound": "issue_slots", "warp_instructions_per_query": ipq, "achieved_ginst_s": issue_rate / 1e9,
             "peak_ginst_s": issue_peak / 1e9, "frac": issue_rate / issue_peak,
             "note": "ncu of the same kernel: issue active 70 %, LSU data pipe 75 %, ALU 61 %, XU 50 % "
-                    "(profiles/r01k_match_kernel_ncu_full.json)"}
+                    "(profiles/r01l_match_kernel_ncu_full.json)"}
 
     # ---- e2e: host buffers in, host records out, every step ------------------------------------------
     e2e = None

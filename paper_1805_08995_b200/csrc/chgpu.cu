@@ -152,6 +152,7 @@ struct chgpu_ctx {
     std::vector<ImageRec> images;
     std::vector<uint32_t> free_slots;
     std::unordered_map<uint32_t, uint32_t> slot_of;
+    std::vector<uint32_t> slot_dense;  // slot_of for image ids < kDenseIds: pair lists resolve 2 ids per pair
     DevImage* d_images = nullptr;
     DevImage* h_images = nullptr;  // pinned mirror
     size_t images_cap = 0;
@@ -342,7 +343,19 @@ chgpu_status h2d(chgpu_ctx* ctx, void* dst, const void* src, size_t bytes) {
     return CHGPU_OK;
 }
 
+constexpr uint32_t kDenseIds = 1u << 22;
+void dense_set(chgpu_ctx* ctx, uint32_t image_id, uint32_t slot) {
+    if (image_id >= kDenseIds) return;
+    if (image_id >= ctx->slot_dense.size())
+        ctx->slot_dense.resize(std::max<size_t>(size_t(image_id) + 1, std::min<size_t>(kDenseIds, ctx->slot_dense.size() * 2 + 1024)), kNone);
+    ctx->slot_dense[image_id] = slot;
+}
+
 chgpu_status find_slot(chgpu_ctx* ctx, uint32_t image_id, uint32_t* slot) {
+    if (image_id < ctx->slot_dense.size() && ctx->slot_dense[image_id] != kNone) {
+        *slot = ctx->slot_dense[image_id];
+        return CHGPU_OK;
+    }
     const auto it = ctx->slot_of.find(image_id);
     if (it == ctx->slot_of.end()) return fail(ctx, CHGPU_ENOTFOUND, "image %u is not resident", image_id);
     *slot = it->second;
@@ -394,6 +407,7 @@ chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t
         CK(cudaStreamSynchronize(ctx->compute));
         release_slot(ctx, it->second);
         ctx->slot_of.erase(it);
+        dense_set(ctx, image_id, kNone);
     }
     const uint32_t m = ctx->fam.short_bits, L = ctx->fam.table_count;
     const uint32_t ntiles = tile_count_of(ctx, n), tp = tile_points_of(ctx);
@@ -454,6 +468,7 @@ chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t
         if (const chgpu_status s = publish_slot(ctx, tile_slots[k])) return s;
     }
     ctx->slot_of[image_id] = slot;
+    dense_set(ctx, image_id, slot);
     *slot_out = slot;
     return CHGPU_OK;
 }
@@ -1706,6 +1721,7 @@ chgpu_status chgpu_evict_image(chgpu_ctx* ctx, uint32_t image_id) {
     CK(cudaStreamSynchronize(ctx->compute));
     release_slot(ctx, slot);
     ctx->slot_of.erase(image_id);
+    dense_set(ctx, image_id, kNone);
     return CHGPU_OK;
 }
 
