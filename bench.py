@@ -73,21 +73,26 @@ def measured_peak_hbm() -> tuple[float, str]:
 
 def recorded_instructions_per_query():
     """Warp instructions per query point of the match kernel, from the committed ncu --set full summary."""
-    p = ROOT / "profiles" / "r01l_match_kernel_ncu_full.json"
+    files = sorted((ROOT / "profiles").glob("r*_match_kernel_ncu_full.json"))
     try:
-        return float(json.loads(p.read_text())["kernels"][0]["warp_instructions_per_query"])
+        return float(json.loads(files[-1].read_text())["kernels"][0]["warp_instructions_per_query"]), files[-1].name
     except Exception:  # noqa: BLE001
-        return None
+        return None, None
 
 
 def recorded_traffic():
-    """dram bytes per match-kernel launch from the committed ncu --set full capture, if any."""
-    p = ROOT / "profiles" / "traffic.json"
-    if p.exists():
-        try:
-            return json.loads(p.read_text())
-        except Exception:  # noqa: BLE001
-            return None
+    """dram bytes of one match-kernel launch and the pairs that launch held, from the latest committed ncu --set full
+    summary (profiles/r*_match_kernel_ncu_full.json; the capture's launch may be smaller than the bench's)."""
+    files = sorted((ROOT / "profiles").glob("r*_match_kernel_ncu_full.json"))
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    try:
+        k = json.loads(files[-1].read_text())["kernels"][0]
+        m = k["metrics"]
+        tot = sum(float(m[n]["value"]) * scale[m[n]["unit"]] for n in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        queries = float(m["smsp__inst_executed.sum"]["value"]) / float(k["warp_instructions_per_query"])
+        return {"dram_bytes_per_launch": tot, "queries_per_launch": queries, "source": files[-1].name}
+    except Exception:  # noqa: BLE001
+        return None
     return None
 
 
@@ -361,7 +366,10 @@ def run_ours(args):
     roofline = {
         "bound": "hbm", "kernel": "match_kernel<SMEM_TRAIN, L=6>", "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak, "peak_source": peak_src,
-        "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+        # dram bytes of one launch of this run's size: the captured launch scaled by its query count
+        "traffic": (traffic["dram_bytes_per_launch"] * (last["query_points"] / max(1, last["match_launches"])) /
+                    traffic["queries_per_launch"]) if traffic else None,
+        "traffic_source": (traffic or {}).get("source"),
         "algorithmic_bytes_per_pair": alg / npairs,
         "algorithmic_bytes_per_launch": alg / max(1, last["match_launches"]),
         "avg_launch_ms": kern_ms / max(1, match_launches),
@@ -379,11 +387,11 @@ def run_ours(args):
     roofline["on_chip"] = {"bound": "xu_popc", "achieved_gpopc_s": popc_rate / 1e9, "peak_gpopc_s": popc_peak / 1e9,
                            "frac": popc_rate / popc_peak,
                            "note": "lower bound on POPC work (padding lanes not counted); ncu pipe utilisations of the "
-                                   "committed capture: profiles/r01l_match_kernel_ncu_full.json"}
+                                   "committed capture (profiles/r*_match_kernel_ncu_full.json, latest)"}
 
     # the limit the kernel actually runs into: warp-instruction issue slots (4 per clock per SM).  Instructions
     # per query come from the committed ncu capture of this kernel; the rate is this run's.
-    ipq = recorded_instructions_per_query()
+    ipq, ipq_src = recorded_instructions_per_query()
     if ipq:
         issue_peak = props["sm_count"] * 4 * sm_mhz * 1e6
         issue_rate = ipq * last["query_points"] / (kern_ms_per_step * 1e-3)
@@ -391,7 +399,7 @@ def run_ours(args):
             "bound": "issue_slots", "warp_instructions_per_query": ipq, "achieved_ginst_s": issue_rate / 1e9,
             "peak_ginst_s": issue_peak / 1e9, "frac": issue_rate / issue_peak,
             "note": "ncu of the same kernel: issue active 70 %, LSU data pipe 75 %, ALU 61 %, XU 50 % "
-                    "(profiles/r01l_match_kernel_ncu_full.json)"}
+                    f"(profiles/{ipq_src})"}
 
     # ---- e2e: host buffers in, host records out, every step ------------------------------------------
     e2e = None

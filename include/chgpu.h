@@ -108,7 +108,7 @@ const char* chgpu_status_name(chgpu_status s);
 chgpu_status chgpu_get_device_props(chgpu_ctx* ctx, chgpu_device_props* out);
 chgpu_status chgpu_sync(chgpu_ctx* ctx);
 /* Tuning knob: upper bound on the sum of query points per sub-batch (one match-kernel launch);
- * 0 restores the default (16 Mi).  Results never depend on it. */
+ * 0 restores the default (32 Mi).  Results never depend on it. */
 chgpu_status chgpu_set_sub_batch_queries(chgpu_ctx* ctx, uint64_t max_queries);
 /* Pinned host memory for zero-staging uploads / result sinks. */
 chgpu_status chgpu_host_alloc(chgpu_ctx* ctx, size_t bytes, void** out);

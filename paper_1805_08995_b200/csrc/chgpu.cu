@@ -50,7 +50,7 @@ constexpr size_t kStageBytes = size_t(32) << 20;
 constexpr int kStageSlots = 2;
 constexpr uint32_t kHashQueueCap = 1u << 21;    // undecided dots per hash launch (16 MiB); ~110 per 8K-point image are expected
 constexpr uint32_t kHashBatchImages = 2048;     // images per hash launch
-constexpr uint64_t kSubBatchQueries = uint64_t(16) << 20;  // per sub-batch: sum of Nq (res 128 MiB, records <= 256 MiB)
+constexpr uint64_t kSubBatchQueries = uint64_t(32) << 20;  // per sub-batch: sum of Nq (res 256 MiB, records <= 512 MiB); the persistent grid pays its tail once per launch
 
 size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a; }
 

@@ -1,14 +1,18 @@
-# Evidence pass on the GPU box: bench (both arms), ncu launch list of the same command, ncu --set full of the
-# match kernel and of the filtered hash kernel.  Everything lands in gpurun_out/ under the tag given as $1.
+# Evidence pass on the GPU box: ncu --set full of the match kernel and of the filtered hash kernel (summarised into
+# profiles/ so that bench.py's issue-slot roofline uses this build's instruction count), bench (both arms), ncu launch
+# list of the same command.  Everything lands in gpurun_out/ under the tag given as $1.
 tag=${1:-r01x}
+ncu --set full --clock-control none --import-source on -k regex:match_kernel -s 3 -c 1 -f -o gpurun_out/${tag}_match \
+    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --images 200 --pairs 16384 > /dev/null 2>&1
+python scripts/ncu_summary.py gpurun_out/${tag}_match.ncu-rep profiles/${tag}_match_kernel_ncu_full.json 33554432
+cp profiles/${tag}_match_kernel_ncu_full.json gpurun_out/
+ncu --set full --clock-control none --import-source on -k regex:hash_filter_kernel -s 1 -c 1 -f -o gpurun_out/${tag}_hash \
+    python scripts/hash_bench.py --images 400 --reps 1 > /dev/null 2>&1
+python scripts/ncu_summary.py gpurun_out/${tag}_hash.ncu-rep gpurun_out/${tag}_hash_filter_kernel_ncu_full.json
 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
 python bench.py --impl reference > gpurun_out/${tag}_bench_reference_arm.json 2>> gpurun_out/${tag}_bench.err
 # the whole command, every launch (setup, warm-up step, timed step, one end-to-end step)
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches.csv \
     python bench.py --steps 1 --warmup 1 --no-cpu --e2e-steps 1 > gpurun_out/${tag}_bench_under_ncu.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:match_kernel -s 3 -c 1 -f -o gpurun_out/${tag}_match \
-    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --images 200 --pairs 16384 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:hash_filter_kernel -s 1 -c 1 -f -o gpurun_out/${tag}_hash \
-    python scripts/hash_bench.py --images 400 --reps 1 > /dev/null 2>&1
 python scripts/hash_bench.py > gpurun_out/${tag}_hash_bench.json
 tail -c 600 gpurun_out/${tag}_bench.json
