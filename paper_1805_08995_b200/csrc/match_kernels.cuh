@@ -733,6 +733,29 @@ __global__ void tile_compact_kernel(const MatchParams P, uint32_t ntile_pairs) {
     if (lane == 0) P.nact[tp] = count;
 }
 
+// Ascending bitonic sort of one value per lane (kNone sinks to the top lanes), and the last stage alone for a
+// sequence that is already bitonic.
+__device__ __forceinline__ uint32_t warp_bitonic_merge32(uint32_t v, uint32_t lane) {
+#pragma unroll
+    for (uint32_t j = 16; j > 0; j >>= 1) {
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, v, j);
+        v = (lane & j) == 0 ? min(v, o) : max(v, o);
+    }
+    return v;
+}
+__device__ __forceinline__ uint32_t warp_sort32(uint32_t v, uint32_t lane) {
+#pragma unroll
+    for (uint32_t k = 2; k < 32; k <<= 1) {
+#pragma unroll
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, v, j);
+            const bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
+            v = keep_min ? min(v, o) : max(v, o);
+        }
+    }
+    return warp_bitonic_merge32(v, lane);
+}
+
 constexpr int kMergeThreads = 256;
 constexpr uint32_t kMergeChunk = 1024;  // queries per CTA
 template <int kInstance>
@@ -749,22 +772,22 @@ __global__ void __launch_bounds__(kMergeThreads) tile_merge_kernel(const MatchPa
         uint32_t out_t = kNone, out_d = 0, n = 0, mykey = kNone;
         if ((__ldg(P.gmin + pd.res_off + q) >> 24) <= P.tau) {
             const uint32_t* __restrict__ list = P.lists + (pd.res_off + q) * P.list_stride;
+            // keys of different tiles differ in the id and a tile's list has no duplicates: a plain sort merges them.
+            // 32 entries per round, one per lane: sort the round, keep the 32 smallest of it and the running list
+            // (min(a[l], b[31 - l]) is bitonic), re-sort that with the last bitonic stage.
             bool cut = false;
             for (uint32_t e0 = 0; e0 < entries; e0 += 32) {
-                uint32_t key[1];
-                key[0] = e0 + lane < entries ? __ldg(list + e0 + lane) : kNone;
-                cut |= key[0] != kNone && (key[0] >> 24) > P.tau;
-                const uint32_t kth = __shfl_sync(FULL, mykey, P.top_k - 1);
-                uint32_t prev = __reduce_min_sync(FULL, key[0]);
-                if (prev > kth) continue;
-                const uint32_t old = mykey;
-                prev = min(prev, __shfl_sync(FULL, old, 0));
-                mykey = kNone;
-                for (uint32_t r = 0; r < P.top_k && prev != kNone; ++r) {
-                    if (lane == r) mykey = prev;
-                    prev = next_key(key, old, prev);
+                const uint32_t v = e0 + lane < entries ? __ldg(list + e0 + lane) : kNone;
+                cut |= v != kNone && (v >> 24) > P.tau;
+                const uint32_t sorted = warp_sort32(v, lane);
+                if (e0 == 0) {
+                    mykey = sorted;
+                } else {
+                    const uint32_t mirrored = __shfl_sync(FULL, sorted, 31u - lane);
+                    mykey = warp_bitonic_merge32(min(mykey, mirrored), lane);
                 }
             }
+            if (lane >= P.top_k) mykey = kNone;
             const bool anycut = __any_sync(FULL, cut);
             const uint32_t tot = __popc(__ballot_sync(FULL, mykey != kNone));
             const uint32_t s = __popc(__ballot_sync(FULL, mykey != kNone && (mykey >> 24) <= P.tau));
