@@ -343,6 +343,77 @@ inline std::vector<std::pair<std::uint32_t, std::uint32_t>> plan_guided(
 }
 
 // ---- batch interface: one device context ----------------------------------------------------------
+// ---- code cache ("CHCC") and centering fingerprint: hashing.hpp:134-157, hashing.cpp:151-272 ------------------
+// Files are byte-identical to the reference's and load in either implementation.
+inline std::uint64_t centering_fingerprint(const HashFamily& family) {
+    return chgpu_centering_fingerprint(family.centering.data());
+}
+
+inline void save_code_cache(const ImageCodes& codes, std::uint64_t centering_fp, const std::filesystem::path& path) {
+    const chgpu_family_params p = detail::to_c(codes.params);
+    std::vector<std::uint64_t> words(codes.longs.codes.size() * 2);
+    for (std::size_t i = 0; i < codes.longs.codes.size(); ++i) {
+        words[2 * i] = codes.longs.codes[i].words[0];
+        words[2 * i + 1] = codes.longs.codes[i].words[1];
+    }
+    const chgpu_status st = chgpu_save_code_cache(path.string().c_str(), &p, centering_fp,
+                                                  static_cast<std::uint32_t>(codes.longs.codes.size()),
+                                                  codes.shorts.values.data(), words.data());
+    if (st != CHGPU_OK) throw FeatureFileError(FeatureFileFault::Unwritable, path, 0, "");
+}
+
+struct CodeCacheHeader {  // hashing.hpp:146-150
+    FamilyParams params;
+    std::uint64_t centering_fp = 0;
+    std::uint32_t count = 0;
+};
+
+// Reads just the header; false on a missing file or foreign magic (hashing.cpp:208-226).
+inline bool read_code_cache_header(const std::filesystem::path& path, CodeCacheHeader& header) {
+    chgpu_family_params p{};
+    std::uint64_t fp = 0;
+    std::uint32_t count = 0;
+    if (chgpu_read_code_cache_header(path.string().c_str(), &p, &fp, &count) != CHGPU_OK) return false;
+    header.params = FamilyParams{p.short_bits, p.long_bits, p.table_count, p.seed};
+    header.centering_fp = fp;
+    header.count = count;
+    return true;
+}
+
+// Loads a cache; throws std::runtime_error if the echoed parameters or the fingerprint mismatch, FeatureFileError
+// for a missing / foreign / truncated file (hashing.cpp:228-272).
+inline ImageCodes load_code_cache(const std::filesystem::path& path, const FamilyParams& expected,
+                                  std::uint64_t expected_centering_fp) {
+    const chgpu_family_params p = detail::to_c(expected);
+    ImageCodes out;
+    std::vector<std::uint64_t> words;
+    std::uint32_t count = 0;
+    chgpu_file_fault fault = CHGPU_FAULT_NONE;
+    std::uint64_t off = 0;
+    chgpu_status st = chgpu_load_code_cache(path.string().c_str(), &p, expected_centering_fp, 0, &count, nullptr, nullptr,
+                                            &fault, &off);
+    if (st == CHGPU_ENOMEM) {  // the probe told us the count: now with room for the payload
+        out.shorts.values.resize(static_cast<std::size_t>(count) * expected.table_count);
+        words.resize(static_cast<std::size_t>(count) * 2);
+        st = chgpu_load_code_cache(path.string().c_str(), &p, expected_centering_fp, count, &count, out.shorts.values.data(),
+                                   words.data(), &fault, &off);
+    }
+    if (st == CHGPU_EFORMAT) throw FeatureFileError(static_cast<FeatureFileFault>(int(fault) - 1), path, off, "");
+    if (st == CHGPU_EMISMATCH) throw std::runtime_error(path.string() + ": code cache parameters mismatch active config");
+    if (st != CHGPU_OK) detail::raise(st, "load_code_cache");
+    out.params = expected;
+    out.shorts.short_bits = expected.short_bits;
+    out.shorts.table_count = expected.table_count;
+    out.shorts.point_count = count;
+    out.longs.long_bits = expected.long_bits;
+    out.longs.codes.resize(count);
+    for (std::uint32_t i = 0; i < count; ++i) {
+        out.longs.codes[i].words = {words[2 * i], words[2 * i + 1]};
+        out.longs.codes[i].bits = static_cast<std::uint16_t>(expected.long_bits);
+    }
+    return out;
+}
+
 struct MatchStats : chgpu_match_stats {};
 
 struct PairMatches {  // what the reference's sink receives (engine.cpp:145-160), one per pair

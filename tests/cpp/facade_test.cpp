@@ -172,6 +172,57 @@ static void host_checks(const std::filesystem::path& tmp) {
     }
     CHECK(throws<std::invalid_argument>([] { ch::plan_exhaustive(0, 1, 1); }));
 
+    // code cache (hashing.hpp:134-157): bytes identical to the oracle's file, round trip, header probe, the
+    // reference's error classes
+    {
+        ch::HashFamily fam = ch::build_hash_family(ch::FamilyParams{7, 70, 5, 11});
+        for (int x = 0; x < 128; ++x) fam.centering[x] = 100.0 + 0.25 * x;
+        fam.centering_set = true;
+        const std::uint64_t fp = ch::centering_fingerprint(fam);
+        std::uint64_t want_fp = 0;
+        CHECK(chor_centering_fingerprint(fam.centering.data(), &want_fp) == 0 && fp == want_fp);
+        ch::ImageCodes codes;
+        codes.params = fam.params;
+        codes.shorts.short_bits = 7;
+        codes.shorts.table_count = 5;
+        codes.shorts.point_count = 37;
+        codes.longs.long_bits = 70;
+        std::vector<std::uint64_t> words;
+        for (std::uint32_t p = 0; p < 37; ++p) {
+            for (std::uint32_t t = 0; t < 5; ++t) codes.shorts.values.push_back((p * 31 + t * 7) & 127);
+            ch::LongCode lc;
+            lc.words = {0x9e3779b97f4a7c15ull * (p + 1), (0xbf58476d1ce4e5b9ull * (p + 3)) & 0x3f};
+            lc.bits = 70;
+            codes.longs.codes.push_back(lc);
+            words.push_back(lc.words[0]);
+            words.push_back(lc.words[1]);
+        }
+        ch::save_code_cache(codes, fp, tmp / "c_ours.chcc");
+        const chor_family_params cp = to_chor(fam.params);
+        CHECK(chor_save_code_cache(&cp, fp, codes.shorts.values.data(), words.data(), 37, (tmp / "c_ref.chcc").string().c_str()) == 0);
+        CHECK(slurp(tmp / "c_ours.chcc") == slurp(tmp / "c_ref.chcc"));
+        ch::CodeCacheHeader hdr;
+        CHECK(ch::read_code_cache_header(tmp / "c_ref.chcc", hdr) && hdr.params == fam.params && hdr.centering_fp == fp &&
+              hdr.count == 37);
+        CHECK(!ch::read_code_cache_header(tmp / "no_such.chcc", hdr));
+        const ch::ImageCodes back = ch::load_code_cache(tmp / "c_ref.chcc", fam.params, fp);
+        CHECK(back.shorts.values == codes.shorts.values && back.shorts.point_count == 37 && back.longs.codes.size() == 37);
+        for (std::size_t p = 0; p < 37; ++p) CHECK(back.longs.codes[p].words == codes.longs.codes[p].words);
+        CHECK(throws<std::runtime_error>([&] { ch::load_code_cache(tmp / "c_ref.chcc", fam.params, fp + 1); }));
+        CHECK(throws<std::runtime_error>([&] { ch::load_code_cache(tmp / "c_ref.chcc", ch::FamilyParams{}, fp); }));
+        CHECK(throws<ch::FeatureFileError>([&] { ch::load_code_cache(tmp / "no_such.chcc", fam.params, fp); }));
+        std::string cut = slurp(tmp / "c_ref.chcc");
+        cut.resize(cut.size() - 9);
+        std::ofstream(tmp / "c_cut.chcc", std::ios::binary) << cut;
+        try {
+            ch::load_code_cache(tmp / "c_cut.chcc", fam.params, fp);
+            CHECK(false);
+        } catch (const ch::FeatureFileError& e) {
+            CHECK(e.fault() == ch::FeatureFileFault::Truncated);
+        }
+        CHECK(throws<ch::FeatureFileError>([&] { ch::save_code_cache(codes, fp, tmp / "no_such_dir" / "c.chcc"); }));
+    }
+
     // plan_guided: the accepted pairs (either order, duplicates collapse) in the exhaustive plan's order == the oracle's
     {
         std::vector<std::pair<std::uint32_t, std::uint32_t>> acc;
