@@ -1,0 +1,94 @@
+"""Randomised differential test: random hash families, match configurations, image sizes (empty to tiled) and
+descriptor distributions, unguided and epipolar-guided, against the CPU oracle — codes, records, statistics and
+ranked lists bit-exact.  Seeds are fixed: a failure names its case."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle_lib
+import paper_1805_08995_b200 as ch
+from paper_1805_08995_b200.synth import make_dataset
+from test_gpu_parity import fresh, put
+
+pytestmark = pytest.mark.gpu
+
+BASE = 9000
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    return oracle_lib.best()
+
+
+def random_case(seed):
+    rng = np.random.default_rng(seed)
+    m = int(rng.integers(1, 11))
+    n = int(rng.integers(m + 1, 129))
+    L = int(rng.integers(1, 9))
+    params = ch.FamilyParams(m, n, L, int(rng.integers(1, 1 << 30)))
+    top_k = int(rng.integers(2, 33))
+    cfg = ch.MatchConfig(top_k=top_k, hamming_threshold=int(rng.integers(0, n + 1)), ratio=float(rng.uniform(0.3, 0.99)),
+                         min_candidates_for_ratio=int(rng.integers(0, 12)), reduce_rounds=int(rng.integers(0, 8)))
+    sizes = [0, 1, 2, 31, 33, 200, 777, 1500, 3000, 4096, 9000, 11500, 14000]
+    weights = np.array([1, 1, 1, 1, 1, 4, 4, 4, 4, 3, 2, 2, 2], dtype=float)
+    n_i, n_j = (int(x) for x in rng.choice(sizes, 2, p=weights / weights.sum()))
+    shape = "sift" if rng.random() < 0.4 else "uniform"
+    return params, cfg, n_i, n_j, shape, rng
+
+
+# CHFUZZ_FIRST / CHFUZZ_COUNT widen the run (e.g. CHFUZZ_COUNT=1000 for a soak)
+SEEDS = range(int(os.environ.get("CHFUZZ_FIRST", "0")), int(os.environ.get("CHFUZZ_FIRST", "0")) + int(os.environ.get("CHFUZZ_COUNT", "40")))
+
+
+@pytest.mark.parametrize("seed", list(SEEDS))
+def test_random_case_matches_the_oracle(matcher, oracle, seed):
+    params, cfg, n_i, n_j, shape, rng = random_case(seed)
+    fam = ch.build_hash_family(params)
+    fresh(matcher, fam)
+    d = make_dataset(2, max(n_i, n_j, 1), seed=1000 + seed, shape=shape)
+    desc = [d[0][:n_i], d[1][:n_j]]
+    if n_i and n_j and rng.random() < 0.3:      # some exact duplicates across the pair and inside the train image
+        k = min(n_i, n_j, 20)
+        desc[1] = desc[1].copy()
+        desc[1][:k] = desc[0][:k]
+        desc[1][-k:] = desc[0][:k]
+    kp = [np.column_stack([np.floor(rng.uniform(0, 900, n)), rng.uniform(0, 700, n), np.full(n, 2.0), np.zeros(n)]).astype(np.float32)
+          for n in (n_i, n_j)]
+    cen = oracle.centering([x for x in desc if len(x)]) if n_i + n_j else np.zeros(128)
+    matcher.set_centering(cen)
+    for i in range(2):
+        put(matcher, BASE + i, desc[i], kp[i])
+    rr = cfg.reduce_rounds
+    matcher.hash([BASE, BASE + 1], rr)
+    codes = [oracle.compute_codes(params, fam.short_planes, fam.long_planes, cen, desc[i], rr) for i in range(2)]
+    for i in range(2):
+        c = matcher.codes(BASE + i)
+        assert np.array_equal(c.shorts, codes[i][0]) and np.array_equal(c.longs, codes[i][1]), (seed, "codes", i)
+    want, ws, wr, wc = oracle.match_pair(params, cfg, desc[0], *codes[0], desc[1], *codes[1], want_ranked=True)
+    offs, rec, st = matcher.match_pairs([(BASE, BASE + 1)], cfg)
+    assert np.array_equal(rec, want), (seed, params, cfg, n_i, n_j, shape)
+    assert (st["raw_candidates"], st["verified_queries"], st["distances"]) == \
+        (ws["raw_candidates"], ws["verified_queries"], ws["distances"]), seed
+    if n_i:
+        ranked, rc = matcher.ranked(BASE, BASE + 1, cfg)
+        assert np.array_equal(rc, wc[: len(rc)]), seed
+        for q in np.nonzero(rc)[0]:
+            assert np.array_equal(ranked[q, :rc[q]], wr[q, :rc[q]]), (seed, q)
+    # guided: a random fundamental matrix (sometimes degenerate for part of the queries) and band
+    if rng.random() < 0.5:
+        F = rng.normal(size=(3, 3))
+        F[:, 2] *= 300.0
+    else:
+        F = np.array([[1.0, 0.0, -float(rng.integers(0, 900))], [0.0, 0.0, 0.0], [0.0, 50.0, -20000.0]])
+    band = float(rng.choice([0.0, 5.0, 40.0, 300.0, 1e9]))
+    gw, gs, gr, gc = oracle.guided_match_pair(params, cfg, desc[0], kp[0], *codes[0], desc[1], kp[1], *codes[1], F, band,
+                                              want_ranked=True)
+    _, grec, gst = matcher.match_pairs_guided([(BASE, BASE + 1)], F[None], band, cfg)
+    assert np.array_equal(grec, gw), (seed, "guided", params, cfg, n_i, n_j, band)
+    assert (gst["verified_queries"], gst["distances"]) == (gs["verified_queries"], gs["distances"]), (seed, "guided stats")
+    if n_i:
+        ranked, rc = matcher.ranked_guided(BASE, BASE + 1, F, band, cfg)
+        assert np.array_equal(rc, gc[: len(rc)]), (seed, "guided counts")
+        for q in np.nonzero(rc)[0]:
+            assert np.array_equal(ranked[q, :rc[q]], gr[q, :rc[q]]), (seed, "guided ranked", q)
