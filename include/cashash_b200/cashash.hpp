@@ -14,7 +14,10 @@
 //     match output      save_matches / pair_file_name           include/cashash/feature_io.hpp:106,
 //                                                               include/cashash/engine.hpp:79
 //     guided match      guided_match_pair (F as 9 doubles)      include/cashash/geometry.hpp:86-89
-//     pair list         plan_exhaustive, plan_guided (flattened) include/cashash/scheduler.hpp:53-58
+//     pair list         plan_exhaustive, plan_guided (flattened, and as PairPlan over a Partition)
+//                                                               include/cashash/scheduler.hpp:53-58
+//     schedule          make_partition, residency_tasks, simulate_residency, auto_partition_sizing,
+//                       assign_workers                          include/cashash/scheduler.hpp:29-134
 //
 // A caller of the reference switches by including this header and `namespace cashash =
 // cashash_b200;`.  The free functions run on a process-wide default
@@ -340,6 +343,179 @@ inline std::vector<std::pair<std::uint32_t, std::uint32_t>> plan_guided(
     if (st != CHGPU_OK) detail::raise(st, "plan_guided");
     pairs.resize(n);
     return pairs;
+}
+
+// ---- scheduler.hpp types: partition, tasks, residency schedule --------------------------------------------------
+struct Partition {  // scheduler.hpp:14-27
+    std::uint32_t image_count = 0;
+    std::uint32_t block_images = 0;
+    std::uint32_t blocks_per_group = 0;
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> block_ranges;  // [first, last) image index per block
+    std::vector<std::vector<std::uint32_t>> group_blocks;               // block ids per group
+    std::vector<std::uint32_t> block_group_of;                          // group id per block
+
+    std::uint32_t block_count() const { return static_cast<std::uint32_t>(block_ranges.size()); }
+    std::uint32_t group_count() const { return static_cast<std::uint32_t>(group_blocks.size()); }
+    std::uint32_t block_size(std::uint32_t block) const { return block_ranges[block].second - block_ranges[block].first; }
+};
+
+inline Partition make_partition(std::uint32_t image_count, std::uint32_t block_images, std::uint32_t blocks_per_group) {
+    if (image_count == 0) throw std::invalid_argument("partition: empty manifest");  // scheduler.cpp:12
+    if (block_images == 0 || blocks_per_group == 0)
+        throw std::invalid_argument("partition: block_images and blocks_per_group must be >= 1");
+    Partition p;
+    p.image_count = image_count;
+    p.block_images = block_images;
+    p.blocks_per_group = blocks_per_group;
+    const std::uint32_t nblocks = (image_count + block_images - 1) / block_images;
+    p.group_blocks.resize((nblocks + blocks_per_group - 1) / blocks_per_group);
+    for (std::uint32_t b = 0; b < nblocks; ++b) {
+        const std::uint64_t last = std::min<std::uint64_t>(image_count, std::uint64_t(b + 1) * block_images);
+        p.block_ranges.emplace_back(b * block_images, static_cast<std::uint32_t>(last));
+        p.block_group_of.push_back(b / blocks_per_group);
+        p.group_blocks[b / blocks_per_group].push_back(b);
+    }
+    return p;
+}
+
+struct PlanTask {  // scheduler.hpp:36-40
+    std::uint32_t group_a = 0, group_b = 0;
+    std::uint32_t block_a = 0, block_b = 0;
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> pairs;
+};
+
+struct PairPlan {  // scheduler.hpp:42-46
+    std::vector<PlanTask> tasks;
+    std::size_t pair_count() const {
+        std::size_t n = 0;
+        for (const PlanTask& t : tasks) n += t.pairs.size();
+        return n;
+    }
+};
+
+namespace detail {
+inline PairPlan assemble_plan(const Partition& p, const std::vector<std::pair<std::uint32_t, std::uint32_t>>& flat,
+                              const std::uint32_t* accepted, std::uint64_t accepted_count, bool guided) {
+    std::uint32_t nt = 0;
+    std::uint32_t dummy[2] = {0, 0};
+    const std::uint32_t* acc = guided ? (accepted_count ? accepted : dummy) : nullptr;
+    chgpu_status st = chgpu_plan_tasks(p.image_count, p.block_images, p.blocks_per_group, acc, accepted_count, nullptr, &nt);
+    if (st != CHGPU_OK) raise(st, "plan");
+    std::vector<chgpu_plan_task> ts(nt);
+    if (nt) {
+        st = chgpu_plan_tasks(p.image_count, p.block_images, p.blocks_per_group, acc, accepted_count, ts.data(), &nt);
+        if (st != CHGPU_OK) raise(st, "plan");
+    }
+    PairPlan plan;
+    plan.tasks.resize(nt);
+    for (std::uint32_t t = 0; t < nt; ++t) {
+        PlanTask& out = plan.tasks[t];
+        out.group_a = ts[t].group_a;
+        out.group_b = ts[t].group_b;
+        out.block_a = ts[t].block_a;
+        out.block_b = ts[t].block_b;
+        out.pairs.assign(flat.begin() + static_cast<std::ptrdiff_t>(ts[t].first_pair),
+                         flat.begin() + static_cast<std::ptrdiff_t>(ts[t].first_pair + ts[t].npairs));
+    }
+    return plan;
+}
+}  // namespace detail
+
+// The reference's own signatures (scheduler.hpp:53-58): tasks with their pair lists.
+inline PairPlan plan_exhaustive(const Partition& p) {
+    return detail::assemble_plan(p, plan_exhaustive(p.image_count, p.block_images, p.blocks_per_group), nullptr, 0, false);
+}
+inline PairPlan plan_guided(const Partition& p, const std::vector<std::pair<std::uint32_t, std::uint32_t>>& accepted_pairs) {
+    return detail::assemble_plan(p, plan_guided(p.image_count, p.block_images, p.blocks_per_group, accepted_pairs),
+                                 reinterpret_cast<const std::uint32_t*>(accepted_pairs.data()), accepted_pairs.size(), true);
+}
+
+// assign_workers (scheduler.hpp:63-64): worker w runs tasks w, w + W, ...
+inline std::vector<std::vector<std::uint32_t>> assign_workers(const PairPlan& plan, std::uint32_t worker_count) {
+    if (worker_count == 0) throw std::invalid_argument("assign_workers: need >= 1 worker");
+    std::vector<std::vector<std::uint32_t>> lists(worker_count);
+    for (std::uint32_t t = 0; t < plan.tasks.size(); ++t) lists[t % worker_count].push_back(t);
+    return lists;
+}
+
+enum class ResidencyMode { Hashing, Matching };  // scheduler.hpp:68
+inline constexpr std::uint32_t residency_slot_limit(ResidencyMode mode) { return mode == ResidencyMode::Hashing ? 2u : 3u; }
+
+struct ResidencyTask {  // scheduler.hpp:77-81
+    std::vector<std::uint32_t> groups;
+    std::vector<std::uint32_t> blocks;
+    std::vector<std::uint32_t> block_groups;
+};
+
+inline std::vector<ResidencyTask> residency_tasks(const PairPlan& plan) {  // scheduler.hpp:83
+    std::vector<ResidencyTask> out;
+    out.reserve(plan.tasks.size());
+    for (const PlanTask& t : plan.tasks) {
+        ResidencyTask r;
+        r.groups = t.group_b != t.group_a ? std::vector<std::uint32_t>{t.group_a, t.group_b} : std::vector<std::uint32_t>{t.group_a};
+        r.blocks = t.block_b != t.block_a ? std::vector<std::uint32_t>{t.block_a, t.block_b} : std::vector<std::uint32_t>{t.block_a};
+        r.block_groups = t.block_b != t.block_a ? std::vector<std::uint32_t>{t.group_a, t.group_b} : std::vector<std::uint32_t>{t.group_a};
+        out.push_back(std::move(r));
+    }
+    return out;
+}
+
+inline std::vector<ResidencyTask> hashing_residency_tasks(const Partition& p) {  // scheduler.hpp:84
+    std::vector<ResidencyTask> out;
+    for (std::uint32_t b = 0; b < p.block_count(); ++b)
+        out.push_back(ResidencyTask{{p.block_group_of[b]}, {b}, {p.block_group_of[b]}});
+    return out;
+}
+
+enum class ActionKind { Load, Evict, Begin, Finish };  // scheduler.hpp:86
+enum class ResidencyLevel { Group, Block };            // scheduler.hpp:87
+
+struct ResidencyAction {  // scheduler.hpp:89-94
+    ActionKind kind = ActionKind::Load;
+    ResidencyLevel level = ResidencyLevel::Group;
+    std::uint32_t id = 0;
+    bool prefetch = false;
+};
+
+// simulate_residency (scheduler.hpp:124-125).  group_slots / block_slots = 0: the reference's limits for `mode`; a
+// device with room for more passes its own.  Throws std::logic_error where the reference does (a current load that
+// the limits cannot satisfy).
+inline std::vector<ResidencyAction> simulate_residency(const std::vector<ResidencyTask>& tasks, ResidencyMode mode,
+                                                       std::uint32_t group_slots = 0, std::uint32_t block_slots = 0) {
+    std::vector<chgpu_plan_task> ts(tasks.size());
+    for (std::size_t t = 0; t < tasks.size(); ++t) {
+        const ResidencyTask& r = tasks[t];
+        if (r.groups.empty() || r.blocks.empty() || r.groups.size() > 2 || r.blocks.size() > 2 ||
+            r.block_groups.size() != r.blocks.size())
+            throw std::invalid_argument("simulate_residency: a task names one or two groups and blocks");
+        ts[t].group_a = r.block_groups.front();
+        ts[t].group_b = r.block_groups.back();
+        ts[t].block_a = r.blocks.front();
+        ts[t].block_b = r.blocks.back();
+    }
+    const chgpu_residency_mode m = mode == ResidencyMode::Hashing ? CHGPU_RESIDENCY_HASHING : CHGPU_RESIDENCY_MATCHING;
+    std::uint64_t n = 0;
+    chgpu_status st = chgpu_simulate_residency(ts.data(), static_cast<std::uint32_t>(ts.size()), m, group_slots, block_slots,
+                                               nullptr, 0, &n);
+    if (st == CHGPU_EINVAL) throw std::logic_error("residency: current load blocked");
+    if (st != CHGPU_OK) detail::raise(st, "simulate_residency");
+    std::vector<chgpu_residency_action> raw(n);
+    if (n) chgpu_simulate_residency(ts.data(), static_cast<std::uint32_t>(ts.size()), m, group_slots, block_slots, raw.data(), n, &n);
+    std::vector<ResidencyAction> trace(n);
+    for (std::uint64_t i = 0; i < n; ++i)
+        trace[i] = ResidencyAction{static_cast<ActionKind>(raw[i].kind), static_cast<ResidencyLevel>(raw[i].level), raw[i].id,
+                                   raw[i].prefetch != 0};
+    return trace;
+}
+
+struct PartitionSizing {  // scheduler.hpp:129-132
+    std::uint32_t block_images = 1;
+    std::uint32_t blocks_per_group = 1;
+};
+inline PartitionSizing auto_partition_sizing(std::uint64_t mean_image_bytes, std::uint64_t memory_budget_bytes) {
+    PartitionSizing s;
+    chgpu_auto_partition_sizing(mean_image_bytes, memory_budget_bytes, &s.block_images, &s.blocks_per_group);
+    return s;
 }
 
 // ---- batch interface: one device context ----------------------------------------------------------

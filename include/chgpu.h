@@ -324,6 +324,92 @@ chgpu_status chgpu_plan_guided(uint32_t image_count, uint32_t block_images, uint
  * its train images hot (replaces assign_workers, scheduler.cpp:166-173). */
 void chgpu_shard_range(uint64_t npairs, uint32_t rank, uint32_t world, uint64_t* first, uint64_t* last);
 
+/* ---- block-pair tasks, residency schedule, out-of-core run -------------------------------- */
+/* The tasks behind the flat pair lists above (PlanTask, scheduler.hpp:36-43): task t covers pairs
+ * [first_pair, first_pair + npairs) of chgpu_plan_exhaustive (accepted == NULL) or chgpu_plan_guided (tasks left
+ * without a pair are dropped, scheduler.cpp:161).  tasks_out may be NULL to count. */
+typedef struct chgpu_plan_task {
+    uint32_t group_a, group_b;  /* parent groups of the two blocks */
+    uint32_t block_a, block_b;  /* block_a <= block_b; equal for the pairs inside one block */
+    uint64_t first_pair, npairs;
+} chgpu_plan_task;
+chgpu_status chgpu_plan_tasks(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group,
+                              const uint32_t* accepted /* nullable */, uint64_t accepted_count,
+                              chgpu_plan_task* tasks_out /* nullable */, uint32_t* ntasks_out);
+/* hashing_residency_tasks (scheduler.cpp:194-200): one task per block, in block order. */
+chgpu_status chgpu_hashing_tasks(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group,
+                                 chgpu_plan_task* tasks_out /* nullable */, uint32_t* ntasks_out);
+
+/* The two-line load / prefetch state machine (step_residency / simulate_residency, scheduler.cpp:226-345) run
+ * to completion over residency_tasks(plan) (scheduler.cpp:175-192).  Line 1 loads what the current task misses
+ * (evicting the resident item used farthest in the future), line 2 prefetches the nearest future group / block into
+ * free slots or over items needed strictly later, then the task begins and finishes.
+ * group_slots / block_slots: residency limit per level; 0 selects the reference's (CHGPU_RESIDENCY_HASHING: 2,
+ * CHGPU_RESIDENCY_MATCHING: 3, scheduler.hpp:70-72) and then the trace equals the reference's action for action.
+ * Larger limits are what a 180 GB device wants; a limit below what one task needs is CHGPU_EINVAL (the reference
+ * throws std::logic_error "current ... load blocked" at that point).
+ * actions_out may be NULL to count; CHGPU_ENOMEM with *nactions_out set when capacity is too small. */
+typedef enum chgpu_residency_mode { CHGPU_RESIDENCY_HASHING = 0, CHGPU_RESIDENCY_MATCHING = 1 } chgpu_residency_mode;
+typedef enum chgpu_action_kind { CHGPU_ACT_LOAD = 0, CHGPU_ACT_EVICT = 1, CHGPU_ACT_BEGIN = 2, CHGPU_ACT_FINISH = 3 } chgpu_action_kind;
+typedef enum chgpu_residency_level { CHGPU_LEVEL_GROUP = 0, CHGPU_LEVEL_BLOCK = 1 } chgpu_residency_level;
+typedef struct chgpu_residency_action {
+    uint32_t kind;      /* chgpu_action_kind */
+    uint32_t level;     /* chgpu_residency_level (Load / Evict) */
+    uint32_t id;        /* group / block id, or task index (Begin / Finish) */
+    uint32_t prefetch;  /* Load issued ahead of need (line 2) */
+} chgpu_residency_action;
+chgpu_status chgpu_simulate_residency(const chgpu_plan_task* tasks, uint32_t ntasks, chgpu_residency_mode mode,
+                                      uint32_t group_slots, uint32_t block_slots,
+                                      chgpu_residency_action* actions_out /* nullable */, uint64_t capacity,
+                                      uint64_t* nactions_out);
+/* auto_partition_sizing (scheduler.cpp:347-359): the device holds a quarter of the budget, three units per level. */
+void chgpu_auto_partition_sizing(uint64_t mean_image_bytes, uint64_t memory_budget_bytes, uint32_t* block_images,
+                                 uint32_t* blocks_per_group);
+/* The same rule with the numbers of this device: block_slots blocks share device_bytes (HBM left for images),
+ * group_slots groups share host_bytes (page cache the read-ahead may occupy); device_image_bytes is what one image
+ * occupies in HBM (descriptors, keypoints, codes, bucket index), file_image_bytes its CHFT file. */
+void chgpu_partition_sizing_for_device(uint64_t device_image_bytes, uint64_t file_image_bytes, uint64_t device_bytes,
+                                       uint64_t host_bytes, uint32_t block_slots, uint32_t group_slots,
+                                       uint32_t* block_images, uint32_t* blocks_per_group);
+
+/* Out-of-core run of a plan: the reference's execute_plan + ResidencyDriver (engine.cpp:252-456, :667-702) for
+ * datasets that do not fit in HBM at once.  The residency trace above is replayed on the calling thread:
+ *   Load group   read-ahead of the group's files into the host page cache (posix_fadvise WILLNEED; the pinned
+ *                ring of chgpu_load_chft_files is the staging level under it),
+ *   Load block   chgpu_load_chft_files of the block's files + chgpu_hash_images (hashing an 8K image costs 12 us,
+ *                less than reading its CHCC cache back would),
+ *   Evict block  chgpu_evict_image of its images;  Evict group: the pages are released (DONTNEED),
+ *   Begin task   chgpu_match_pairs_stream over the task's pairs; the sink sees plan-order pair indices.
+ * Never more than block_slots blocks are resident; at the end everything the run loaded is evicted again.  The run
+ * owns the context's image ids 0 .. image_count-1 (image id = index into paths).  Images whose file failed are
+ * reported in file_results (image_count entries) and their pairs are skipped without output, like the reference's
+ * invalid images (engine.cpp:799).  The family and the centering must be installed (chgpu_centering_pass_files).
+ * The sink is called on the calling thread, in plan order, with the pairs of the chunk (2 u32 per pair), their
+ * record offsets (npairs_chunk + 1, relative to records) and the records — the argument list of chgpu_sink_accept
+ * behind the task index; a nonzero return aborts the run. */
+typedef int (*chgpu_plan_sink_fn)(void* user, uint32_t task, const uint32_t* pairs, uint32_t npairs_chunk,
+                                  const uint64_t* offsets, const chgpu_match_record* records);
+typedef struct chgpu_streamed_stats {
+    uint64_t tasks, pairs, pairs_skipped, matches;
+    uint64_t block_loads, block_evictions, group_loads, group_evictions;
+    uint64_t images_loaded, bytes_read;
+    uint32_t max_resident_blocks, max_resident_groups;
+    double load_seconds, hash_seconds, match_seconds, wall_seconds;
+} chgpu_streamed_stats;
+chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths, uint32_t image_count,
+                                       uint32_t block_images, uint32_t blocks_per_group,
+                                       uint32_t group_slots, uint32_t block_slots,
+                                       const uint32_t* accepted /* nullable: exhaustive */, uint64_t accepted_count,
+                                       const chgpu_match_cfg* cfg, uint32_t io_threads, chgpu_plan_sink_fn sink /* nullable */,
+                                       void* user, chgpu_file_result* file_results /* nullable */,
+                                       chgpu_streamed_stats* stats /* nullable */);
+/* centering_pass (engine.cpp:545-559) without keeping anything resident: streams every file once through the
+ * loader in blocks of block_images (the 2-slot hashing schedule degenerates to load, sum, evict), applies the mean
+ * and returns it.  Files that fail are reported and left out of the mean, as the reference does. */
+chgpu_status chgpu_centering_pass_files(chgpu_ctx* ctx, const char* const* paths, uint32_t image_count,
+                                        uint32_t block_images, uint32_t io_threads,
+                                        chgpu_file_result* file_results /* nullable */, double* centering128_out /* nullable */);
+
 #ifdef __cplusplus
 }
 #endif

@@ -660,3 +660,215 @@ int chor_plan_guided(uint32_t image_count, uint32_t block_images, uint32_t block
 }
 
 }  // extern "C"
+
+// ---- residency schedule (scheduler.cpp:175-345) ---------------------------------------------------------------
+namespace {
+
+struct OTask {  // ResidencyTask, scheduler.hpp:77-81
+    std::vector<uint32_t> groups, blocks, block_groups;
+};
+
+// (block_a, block_b) of every task of the plan, by re-running the pair-list restatements above: a task's blocks are
+// the blocks of its first pair (every pair of a task lies in the same block pair, scheduler.cpp:47-75).
+int task_blocks(uint32_t K, uint32_t Np, uint32_t M, int has_accepted, const uint32_t* accepted, uint64_t accepted_count,
+                std::vector<std::pair<uint32_t, uint32_t>>& out) {
+    if (K == 0 || Np == 0 || M == 0) return 1;
+    const uint64_t cap = has_accepted ? accepted_count : static_cast<uint64_t>(K) * (K - 1) / 2;
+    std::vector<uint32_t> pairs(std::max<uint64_t>(cap, 1) * 2), sizes(static_cast<size_t>(K) * K + 4);
+    uint64_t np = 0;
+    uint32_t nt = 0;
+    const int rc = has_accepted ? chor_plan_guided(K, Np, M, accepted, accepted_count, pairs.data(), &np, sizes.data(), &nt)
+                                : chor_plan_exhaustive(K, Np, M, pairs.data(), &np, sizes.data(), &nt);
+    if (rc) return rc;
+    out.clear();
+    uint64_t at = 0;
+    for (uint32_t t = 0; t < nt; ++t) {
+        out.emplace_back(pairs[2 * at] / Np, pairs[2 * at + 1] / Np);
+        at += sizes[t];
+    }
+    return 0;
+}
+
+// Next task >= from that uses `id` at the given level, by scanning the task list (kNever if none).
+uint32_t scan_next_use(const std::vector<OTask>& tasks, bool block_level, uint32_t id, uint32_t from) {
+    for (uint32_t t = from; t < tasks.size(); ++t) {
+        const auto& v = block_level ? tasks[t].blocks : tasks[t].groups;
+        if (std::find(v.begin(), v.end(), id) != v.end()) return t;
+    }
+    return 0xffffffffu;
+}
+
+struct OAction {
+    uint32_t kind, level, id, prefetch;
+};
+
+// acquire (scheduler.cpp:226-247): free slot -> Load; else evict the resident item with the farthest next use
+// (ties: the smaller id), provided that use is strictly after need_at; else nothing can be done.
+bool o_acquire(const std::vector<OTask>& tasks, std::vector<uint32_t>& resident, bool block_level, uint32_t id,
+               uint32_t need_at, uint32_t limit, uint32_t cursor, bool prefetch, OAction& act) {
+    if (resident.size() < limit) {
+        resident.push_back(id);
+        act = {0u, block_level ? 1u : 0u, id, prefetch ? 1u : 0u};
+        return true;
+    }
+    bool have = false;
+    uint32_t victim = 0, far = 0;
+    for (uint32_t r : resident) {
+        const uint32_t u = scan_next_use(tasks, block_level, r, cursor);
+        if (u > far || (u == far && (!have || r < victim))) {
+            victim = r;
+            far = u;
+            have = true;
+        }
+    }
+    if (!have || far <= need_at) return false;
+    resident.erase(std::find(resident.begin(), resident.end(), victim));
+    act = {1u, block_level ? 1u : 0u, victim, 0u};
+    return true;
+}
+
+bool in(const std::vector<uint32_t>& v, uint32_t id) { return std::find(v.begin(), v.end(), id) != v.end(); }
+
+// simulate_residency (scheduler.cpp:339-345) = step_residency (:269-337) until the plan is exhausted.
+// Returns 2 where the reference throws std::logic_error.
+int o_simulate(const std::vector<OTask>& tasks, uint32_t limit, std::vector<OAction>& trace) {
+    std::vector<uint32_t> rg, rb;
+    uint32_t cursor = 0;
+    bool begun = false;
+    while (cursor < tasks.size()) {
+        const OTask& cur = tasks[cursor];
+        OAction act{};
+        bool acted = false;
+        if (!begun)  // line 1, groups
+            for (uint32_t g : cur.groups) {
+                if (in(rg, g)) continue;
+                if (!o_acquire(tasks, rg, false, g, cursor, limit, cursor, false, act)) return 2;
+                acted = true;
+                break;
+            }
+        if (!acted)  // line 2, groups
+            for (uint32_t t = cursor + 1; t < tasks.size() && !acted; ++t) {
+                bool all = true;
+                for (uint32_t g : tasks[t].groups) {
+                    if (in(rg, g)) continue;
+                    all = false;
+                    if (o_acquire(tasks, rg, false, g, t, limit, cursor, true, act)) {
+                        acted = true;
+                        break;
+                    }
+                }
+                if (!all) break;
+            }
+        if (!acted && !begun)  // line 1, blocks
+            for (uint32_t b : cur.blocks) {
+                if (in(rb, b)) continue;
+                if (!o_acquire(tasks, rb, true, b, cursor, limit, cursor, false, act)) return 2;
+                acted = true;
+                break;
+            }
+        if (!acted)  // line 2, blocks
+            for (uint32_t t = cursor + 1; t < tasks.size() && !acted; ++t) {
+                bool all = true, waits = false;
+                for (size_t i = 0; i < tasks[t].blocks.size(); ++i) {
+                    const uint32_t b = tasks[t].blocks[i];
+                    if (in(rb, b)) continue;
+                    all = false;
+                    if (!in(rg, tasks[t].block_groups[i])) {
+                        waits = true;
+                        break;
+                    }
+                    if (o_acquire(tasks, rb, true, b, t, limit, cursor, true, act)) {
+                        acted = true;
+                        break;
+                    }
+                }
+                if (!all || waits) break;
+            }
+        if (!acted) {
+            if (!begun) {
+                begun = true;
+                act = {2u, 1u, cursor, 0u};
+            } else {
+                act = {3u, 1u, cursor, 0u};
+                begun = false;
+                ++cursor;
+            }
+        }
+        trace.push_back(act);
+    }
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int chor_plan_task_blocks(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group, int has_accepted,
+                          const uint32_t* accepted, uint64_t accepted_count, uint32_t* tasks4_out, uint32_t* ntasks_out) {
+    std::vector<std::pair<uint32_t, uint32_t>> tb;
+    if (const int rc = task_blocks(image_count, block_images, blocks_per_group, has_accepted, accepted, accepted_count, tb))
+        return rc;
+    for (size_t t = 0; tasks4_out && t < tb.size(); ++t) {
+        tasks4_out[4 * t + 0] = tb[t].first / blocks_per_group;   // block_group_of, scheduler.cpp:24-31
+        tasks4_out[4 * t + 1] = tb[t].second / blocks_per_group;
+        tasks4_out[4 * t + 2] = tb[t].first;
+        tasks4_out[4 * t + 3] = tb[t].second;
+    }
+    *ntasks_out = static_cast<uint32_t>(tb.size());
+    return 0;
+}
+
+int chor_simulate_residency(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group, int mode,
+                            int has_accepted, const uint32_t* accepted, uint64_t accepted_count,
+                            uint32_t* actions4_out, uint64_t capacity, uint64_t* nactions_out) {
+    if (image_count == 0 || block_images == 0 || blocks_per_group == 0) return 1;
+    std::vector<OTask> tasks;
+    if (mode == 0) {  // hashing_residency_tasks, scheduler.cpp:194-200
+        const uint32_t nblocks = (image_count + block_images - 1) / block_images;
+        for (uint32_t b = 0; b < nblocks; ++b) tasks.push_back(OTask{{b / blocks_per_group}, {b}, {b / blocks_per_group}});
+    } else {  // residency_tasks, scheduler.cpp:175-192
+        std::vector<std::pair<uint32_t, uint32_t>> tb;
+        if (const int rc = task_blocks(image_count, block_images, blocks_per_group, has_accepted, accepted, accepted_count, tb))
+            return rc;
+        for (const auto& [ba, bb] : tb) {
+            OTask t;
+            const uint32_t ga = ba / blocks_per_group, gb = bb / blocks_per_group;
+            t.groups.push_back(ga);
+            if (gb != ga) t.groups.push_back(gb);
+            t.blocks.push_back(ba);
+            t.block_groups.push_back(ga);
+            if (bb != ba) {
+                t.blocks.push_back(bb);
+                t.block_groups.push_back(gb);
+            }
+            tasks.push_back(std::move(t));
+        }
+    }
+    std::vector<OAction> trace;
+    if (const int rc = o_simulate(tasks, mode == 0 ? 2u : 3u, trace)) return rc;  // residency_slot_limit, scheduler.hpp:70-72
+    for (size_t i = 0; actions4_out && i < trace.size() && i < capacity; ++i) {
+        actions4_out[4 * i + 0] = trace[i].kind;
+        actions4_out[4 * i + 1] = trace[i].level;
+        actions4_out[4 * i + 2] = trace[i].id;
+        actions4_out[4 * i + 3] = trace[i].prefetch;
+    }
+    *nactions_out = trace.size();
+    return 0;
+}
+
+int chor_auto_partition_sizing(uint64_t mean_image_bytes, uint64_t memory_budget_bytes, uint32_t* block_images,
+                               uint32_t* blocks_per_group) {
+    // scheduler.cpp:347-359: device arena = budget / 4, each level holds three of its units
+    const uint64_t per = mean_image_bytes ? mean_image_bytes : 1;
+    uint64_t bi = memory_budget_bytes / 4 / per / 3;
+    if (bi < 1) bi = 1;
+    uint64_t group_bytes = static_cast<uint32_t>(bi) * per;
+    if (group_bytes < 1) group_bytes = 1;
+    uint64_t bpg = memory_budget_bytes / group_bytes / 3;
+    if (bpg < 1) bpg = 1;
+    *block_images = static_cast<uint32_t>(bi);
+    *blocks_per_group = static_cast<uint32_t>(bpg);
+    return 0;
+}
+
+}  // extern "C"

@@ -145,6 +145,23 @@ int chor_plan_guided(uint32_t image_count, uint32_t block_images, uint32_t block
                      const uint32_t* accepted, uint64_t accepted_count, uint32_t* pairs_out, uint64_t* npairs_out,
                      uint32_t* task_sizes, uint32_t* ntasks_out);
 
+/* Block-pair tasks of the plan (PlanTask, scheduler.hpp:36-43) without their pair lists: 4 u32 per task
+ * (group_a, group_b, block_a, block_b).  has_accepted == 0: plan_exhaustive; else plan_guided over `accepted`. */
+int chor_plan_task_blocks(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group, int has_accepted,
+                          const uint32_t* accepted, uint64_t accepted_count, uint32_t* tasks4_out, uint32_t* ntasks_out);
+
+/* simulate_residency (scheduler.cpp:339-345) over residency_tasks(plan) (:175-192; mode 1 = Matching, 3 slots) or
+ * over hashing_residency_tasks(partition) (:194-200; mode 0 = Hashing, 2 slots; accepted ignored).  Actions as 4 u32
+ * each: kind (0 Load, 1 Evict, 2 Begin, 3 Finish), level (0 Group, 1 Block), id, prefetch.  actions4_out may be
+ * NULL to count.  Returns 2 (std::logic_error) when a current load is blocked. */
+int chor_simulate_residency(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group, int mode,
+                            int has_accepted, const uint32_t* accepted, uint64_t accepted_count,
+                            uint32_t* actions4_out, uint64_t capacity, uint64_t* nactions_out);
+
+/* auto_partition_sizing (scheduler.cpp:347-359). */
+int chor_auto_partition_sizing(uint64_t mean_image_bytes, uint64_t memory_budget_bytes, uint32_t* block_images,
+                               uint32_t* blocks_per_group);
+
 #ifdef __cplusplus
 }
 #endif

@@ -452,4 +452,65 @@ int chor_plan_guided(uint32_t image_count, uint32_t block_images, uint32_t block
     });
 }
 
+namespace {
+PairPlan plan_for(const Partition& part, int has_accepted, const uint32_t* accepted, uint64_t accepted_count) {
+    if (!has_accepted) return plan_exhaustive(part);
+    std::vector<std::pair<std::uint32_t, std::uint32_t>> acc(accepted_count);
+    for (uint64_t i = 0; i < accepted_count; ++i) acc[i] = {accepted[2 * i], accepted[2 * i + 1]};
+    return plan_guided(part, acc);
+}
+}  // namespace
+
+int chor_plan_task_blocks(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group, int has_accepted,
+                          const uint32_t* accepted, uint64_t accepted_count, uint32_t* tasks4_out, uint32_t* ntasks_out) {
+    return guarded([&] {
+        const PairPlan plan = plan_for(make_partition(image_count, block_images, blocks_per_group), has_accepted, accepted,
+                                       accepted_count);
+        uint32_t nt = 0;
+        for (const PlanTask& t : plan.tasks) {
+            if (tasks4_out) {
+                tasks4_out[4 * nt + 0] = t.group_a;
+                tasks4_out[4 * nt + 1] = t.group_b;
+                tasks4_out[4 * nt + 2] = t.block_a;
+                tasks4_out[4 * nt + 3] = t.block_b;
+            }
+            ++nt;
+        }
+        *ntasks_out = nt;
+    });
+}
+
+int chor_simulate_residency(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group, int mode,
+                            int has_accepted, const uint32_t* accepted, uint64_t accepted_count,
+                            uint32_t* actions4_out, uint64_t capacity, uint64_t* nactions_out) {
+    return guarded([&] {
+        const Partition part = make_partition(image_count, block_images, blocks_per_group);
+        const std::vector<ResidencyTask> tasks =
+            mode == 0 ? hashing_residency_tasks(part)
+                      : residency_tasks(plan_for(part, has_accepted, accepted, accepted_count));
+        const std::vector<ResidencyAction> trace =
+            simulate_residency(tasks, mode == 0 ? ResidencyMode::Hashing : ResidencyMode::Matching);
+        uint64_t n = 0;
+        for (const ResidencyAction& a : trace) {
+            if (actions4_out && n < capacity) {
+                actions4_out[4 * n + 0] = static_cast<uint32_t>(a.kind);
+                actions4_out[4 * n + 1] = static_cast<uint32_t>(a.level);
+                actions4_out[4 * n + 2] = a.id;
+                actions4_out[4 * n + 3] = a.prefetch ? 1u : 0u;
+            }
+            ++n;
+        }
+        *nactions_out = n;
+    });
+}
+
+int chor_auto_partition_sizing(uint64_t mean_image_bytes, uint64_t memory_budget_bytes, uint32_t* block_images,
+                               uint32_t* blocks_per_group) {
+    return guarded([&] {
+        const PartitionSizing s = auto_partition_sizing(mean_image_bytes, memory_budget_bytes);
+        *block_images = s.block_images;
+        *blocks_per_group = s.blocks_per_group;
+    });
+}
+
 }  // extern "C"

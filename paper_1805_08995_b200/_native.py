@@ -77,7 +77,30 @@ class DevicePropsC(C.Structure):
                 ("total_mem", C.c_size_t), ("free_mem", C.c_size_t), ("smem_per_block_optin", C.c_size_t)]
 
 
+class PlanTaskC(C.Structure):
+    _fields_ = [("group_a", C.c_uint32), ("group_b", C.c_uint32), ("block_a", C.c_uint32), ("block_b", C.c_uint32),
+                ("first_pair", C.c_uint64), ("npairs", C.c_uint64)]
+
+
+class ResidencyActionC(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("level", C.c_uint32), ("id", C.c_uint32), ("prefetch", C.c_uint32)]
+
+
+class StreamedStatsC(C.Structure):
+    _fields_ = [("tasks", C.c_uint64), ("pairs", C.c_uint64), ("pairs_skipped", C.c_uint64), ("matches", C.c_uint64),
+                ("block_loads", C.c_uint64), ("block_evictions", C.c_uint64), ("group_loads", C.c_uint64),
+                ("group_evictions", C.c_uint64), ("images_loaded", C.c_uint64), ("bytes_read", C.c_uint64),
+                ("max_resident_blocks", C.c_uint32), ("max_resident_groups", C.c_uint32),
+                ("load_seconds", C.c_double), ("hash_seconds", C.c_double), ("match_seconds", C.c_double),
+                ("wall_seconds", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
 SINK_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, u64p, C.POINTER(MatchRecordC))
+
+PLAN_SINK_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, u32p, C.c_uint32, u64p, C.POINTER(MatchRecordC))
 
 # name -> (restype, argtypes); every symbol include/chgpu.h declares
 SIGNATURES = {
@@ -147,6 +170,18 @@ SIGNATURES = {
     "chgpu_plan_exhaustive": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p, u64p]),
     "chgpu_plan_guided": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, u32p, C.c_uint64, u32p, u64p]),
     "chgpu_shard_range": (None, [C.c_uint64, C.c_uint32, C.c_uint32, u64p, u64p]),
+    "chgpu_plan_tasks": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint64, C.POINTER(PlanTaskC), u32p]),
+    "chgpu_hashing_tasks": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(PlanTaskC), u32p]),
+    "chgpu_simulate_residency": (C.c_int, [C.POINTER(PlanTaskC), C.c_uint32, C.c_int, C.c_uint32, C.c_uint32,
+                                           C.POINTER(ResidencyActionC), C.c_uint64, u64p]),
+    "chgpu_auto_partition_sizing": (None, [C.c_uint64, C.c_uint64, u32p, u32p]),
+    "chgpu_partition_sizing_for_device": (None, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
+                                                 u32p, u32p]),
+    "chgpu_match_plan_streamed": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                            C.c_uint32, C.c_void_p, C.c_uint64, C.POINTER(MatchCfgC), C.c_uint32, PLAN_SINK_FN,
+                                            C.c_void_p, C.POINTER(FileResultC), C.POINTER(StreamedStatsC)]),
+    "chgpu_centering_pass_files": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.c_uint32, C.c_uint32, C.c_uint32,
+                                             C.POINTER(FileResultC), f64p]),
 }
 
 _lib = None

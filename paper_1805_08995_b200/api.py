@@ -258,6 +258,82 @@ def plan_guided(image_count: int, block_images: int, blocks_per_group: int, acce
     return out[: n.value].copy()
 
 
+TASK_DTYPE = np.dtype([("group_a", "<u4"), ("group_b", "<u4"), ("block_a", "<u4"), ("block_b", "<u4"),
+                       ("first_pair", "<u8"), ("npairs", "<u8")])
+ACTION_DTYPE = np.dtype([("kind", "<u4"), ("level", "<u4"), ("id", "<u4"), ("prefetch", "<u4")])
+LOAD, EVICT, BEGIN, FINISH = range(4)   # ActionKind, scheduler.hpp:87
+GROUP, BLOCK = range(2)                 # ResidencyLevel, scheduler.hpp:88
+HASHING, MATCHING = range(2)            # ResidencyMode, scheduler.hpp:68
+
+
+def plan_tasks(image_count: int, block_images: int, blocks_per_group: int, accepted_pairs=None) -> np.ndarray:
+    """PlanTask list (scheduler.hpp:36-43) of plan_exhaustive (accepted_pairs None) or plan_guided, as TASK_DTYPE rows;
+    first_pair / npairs index the flat pair list of plan_exhaustive / plan_guided."""
+    lib = N.load()
+    acc = None if accepted_pairs is None else np.ascontiguousarray(accepted_pairs, dtype=np.uint32).reshape(-1, 2)
+    # a non-NULL pointer selects the guided plan even for an empty list
+    keep = None if acc is None else (acc if len(acc) else np.zeros((1, 2), np.uint32))
+    ptr = None if acc is None else keep.ctypes.data
+    cnt = 0 if acc is None else len(acc)
+    n = C.c_uint32(0)
+    st = lib.chgpu_plan_tasks(image_count, block_images, blocks_per_group, ptr, cnt, None, C.byref(n))
+    if st != N.OK:
+        _raise(st, "plan_tasks: bad partition, self pair or unknown image index")
+    tasks = np.zeros(n.value, dtype=TASK_DTYPE)
+    if n.value:
+        st = lib.chgpu_plan_tasks(image_count, block_images, blocks_per_group, ptr, cnt,
+                                  tasks.ctypes.data_as(C.POINTER(N.PlanTaskC)), C.byref(n))
+        if st != N.OK:
+            _raise(st, "plan_tasks")
+    return tasks
+
+
+def hashing_tasks(image_count: int, block_images: int, blocks_per_group: int) -> np.ndarray:
+    """hashing_residency_tasks (scheduler.cpp:194-200): one task per block."""
+    lib = N.load()
+    n = C.c_uint32(0)
+    st = lib.chgpu_hashing_tasks(image_count, block_images, blocks_per_group, None, C.byref(n))
+    if st != N.OK:
+        _raise(st, "hashing_tasks: bad partition")
+    tasks = np.zeros(n.value, dtype=TASK_DTYPE)
+    lib.chgpu_hashing_tasks(image_count, block_images, blocks_per_group, tasks.ctypes.data_as(C.POINTER(N.PlanTaskC)), C.byref(n))
+    return tasks
+
+
+def simulate_residency(tasks: np.ndarray, mode: int = MATCHING, group_slots: int = 0, block_slots: int = 0) -> np.ndarray:
+    """simulate_residency (scheduler.hpp:125): the whole action trace as ACTION_DTYPE rows.  Slots 0 = the reference's
+    limits (2 hashing / 3 matching).  ValueError when the limits cannot hold one task (reference: std::logic_error)."""
+    lib = N.load()
+    t = np.ascontiguousarray(tasks, dtype=TASK_DTYPE)
+    tp = t.ctypes.data_as(C.POINTER(N.PlanTaskC)) if len(t) else None
+    n = C.c_uint64(0)
+    st = lib.chgpu_simulate_residency(tp, len(t), mode, group_slots, block_slots, None, 0, C.byref(n))
+    if st != N.OK:
+        _raise(st, "residency: current load blocked (slot limit below what one task needs)")
+    acts = np.zeros(n.value, dtype=ACTION_DTYPE)
+    if n.value:
+        st = lib.chgpu_simulate_residency(tp, len(t), mode, group_slots, block_slots,
+                                          acts.ctypes.data_as(C.POINTER(N.ResidencyActionC)), n.value, C.byref(n))
+        if st != N.OK:
+            _raise(st, "simulate_residency")
+    return acts
+
+
+def auto_partition_sizing(mean_image_bytes: int, memory_budget_bytes: int) -> tuple[int, int]:
+    """auto_partition_sizing (scheduler.hpp:134): (block_images, blocks_per_group)."""
+    a, b = C.c_uint32(0), C.c_uint32(0)
+    N.load().chgpu_auto_partition_sizing(mean_image_bytes, memory_budget_bytes, C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
+def partition_sizing_for_device(device_image_bytes: int, file_image_bytes: int, device_bytes: int, host_bytes: int,
+                                block_slots: int = 3, group_slots: int = 3) -> tuple[int, int]:
+    a, b = C.c_uint32(0), C.c_uint32(0)
+    N.load().chgpu_partition_sizing_for_device(device_image_bytes, file_image_bytes, device_bytes, host_bytes, block_slots,
+                                               group_slots, C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
 def shard_range(npairs: int, rank: int, world: int) -> tuple[int, int]:
     a, b = C.c_uint64(0), C.c_uint64(0)
     N.load().chgpu_shard_range(npairs, rank, world, C.byref(a), C.byref(b))
@@ -422,6 +498,72 @@ class Matcher:
             else:
                 out.append(RuntimeError(f"{paths[i]}: status {r.status}"))
         return out, st.as_dict()
+
+    def _file_results(self, paths, res):
+        out = []
+        for i in range(len(paths)):
+            r = res[i]
+            if r.status == N.OK:
+                out.append(int(r.count))
+            elif r.status == N.EFORMAT:
+                out.append(FeatureFileError(f"{paths[i]}: fault {r.fault} at byte {r.fault_offset}", r.fault, r.fault_offset))
+            else:
+                out.append(RuntimeError(f"{paths[i]}: status {r.status}"))
+        return out
+
+    def centering_pass_files(self, paths, block_images: int, io_threads: int = 8):
+        """centering_pass (engine.cpp:545-559) streamed block by block, nothing left resident.  Returns
+        (centering, per-file results as in load_chft_files)."""
+        n = len(paths)
+        arr = (C.c_char_p * max(n, 1))(*[str(p).encode() for p in paths])
+        res = (N.FileResultC * max(n, 1))()
+        out = np.zeros(128, dtype=np.float64)
+        st = self.lib.chgpu_centering_pass_files(self.h, arr, n, block_images, io_threads, res, out.ctypes.data_as(N.f64p))
+        results = self._file_results(paths, res)
+        self._ck(st)
+        return out, results
+
+    def match_plan_streamed(self, paths, block_images: int, blocks_per_group: int, cfg: MatchConfig = MatchConfig(),
+                            accepted_pairs=None, group_slots: int = 0, block_slots: int = 0, io_threads: int = 8, sink=None):
+        """Out-of-core run of the exhaustive (accepted_pairs None) or guided plan over CHFT files
+        (chgpu_match_plan_streamed).  sink(task, pairs (k,2) u32, offsets (k+1) u64, records) is called in plan order.
+        Returns (stats dict, per-file results)."""
+        n = len(paths)
+        arr = (C.c_char_p * max(n, 1))(*[str(p).encode() for p in paths])
+        res = (N.FileResultC * max(n, 1))()
+        acc = None if accepted_pairs is None else np.ascontiguousarray(accepted_pairs, dtype=np.uint32).reshape(-1, 2)
+        keep = None if acc is None else (acc if len(acc) else np.zeros((1, 2), np.uint32))
+        c = cfg.c()
+        stats = N.StreamedStatsC()
+        err: list[BaseException] = []
+
+        def _cb(_user, task, pairs_p, count, offs_p, rec_p):
+            try:
+                if sink is None:
+                    return 0
+                pr = np.ctypeslib.as_array(pairs_p, shape=(count, 2)).copy()
+                offs = np.ctypeslib.as_array(offs_p, shape=(count + 1,))
+                total = int(offs[count] - offs[0])
+                if total:
+                    rec = np.frombuffer((N.MatchRecordC * total).from_address(C.addressof(rec_p.contents)),
+                                        dtype=RECORD_DTYPE)
+                else:
+                    rec = np.zeros(0, dtype=RECORD_DTYPE)
+                sink(int(task), pr, offs, rec)
+                return 0
+            except BaseException as e:  # noqa: BLE001 - propagate through the C frame
+                err.append(e)
+                return 1
+
+        cb = N.PLAN_SINK_FN(_cb)
+        st = self.lib.chgpu_match_plan_streamed(self.h, arr, n, block_images, blocks_per_group, group_slots, block_slots,
+                                                None if acc is None else keep.ctypes.data, 0 if acc is None else len(acc),
+                                                C.byref(c), io_threads, cb, None, res, C.byref(stats))
+        if err:
+            raise err[0]
+        results = self._file_results(paths, res)
+        self._ck(st)
+        return stats.as_dict(), results
 
     def evict(self, image_id: int):
         self._ck(self.lib.chgpu_evict_image(self.h, image_id))

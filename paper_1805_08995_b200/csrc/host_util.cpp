@@ -3,6 +3,7 @@
 // caller needs exactly one library for the whole matching path.
 
 #include "../../include/chgpu.h"
+#include "plan_tasks.hpp"
 
 #include <algorithm>
 #include <atomic>
@@ -234,59 +235,6 @@ void chgpu_pair_file_name(uint32_t image_i, uint32_t image_j, char* buf) {
     std::snprintf(buf, 48, "match_%06u_%06u.txt", image_i, image_j);
 }
 
-// Exhaustive plan in the reference's locality order (scheduler.cpp:99-142).  Blocks of
-// `block_images` consecutive images, groups of `blocks_per_group` consecutive blocks.  For
-// every anchor group: boustrophedon sweeps of (anchor block, partner block) against each
-// later group, then the anchor group's own block pairs as a chain that starts at the block
-// the sweep stopped on, then the pairs inside each block.
-extern "C++" {
-namespace {
-// The block-pair tasks of the exhaustive plan in plan order: cross(ba, bb) with ba < bb for two different blocks,
-// self(blk) for the pairs inside one block.
-template <class Cross, class Self>
-void for_each_plan_task(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group, Cross&& cross_task, Self&& self_task) {
-    const uint32_t nblocks = (image_count + block_images - 1) / block_images;
-    const uint32_t ngroups = (nblocks + blocks_per_group - 1) / blocks_per_group;
-    auto cross = [&](uint32_t ba, uint32_t bb) {
-        if (ba > bb) std::swap(ba, bb);
-        cross_task(ba, bb);
-    };
-    for (uint32_t g = 0; g < ngroups; ++g) {
-        const uint32_t a0 = g * blocks_per_group, an = std::min(nblocks, a0 + blocks_per_group) - a0;
-        uint32_t j = 0;
-        int jdir = +1;
-        for (uint32_t h = g + 1; h < ngroups; ++h) {
-            const uint32_t b0 = h * blocks_per_group, bn = std::min(nblocks, b0 + blocks_per_group) - b0;
-            uint32_t l = 0;
-            int ldir = +1;
-            for (uint32_t js = 0; js < an; ++js) {
-                for (uint32_t ls = 0; ls < bn; ++ls) {
-                    cross(a0 + j, b0 + l);
-                    if (ls + 1 < bn) l = uint32_t(int(l) + ldir);
-                }
-                ldir = -ldir;
-                if (js + 1 < an) j = uint32_t(int(j) + jdir);
-            }
-            jdir = -jdir;
-        }
-        // intra-group block pairs: vertex order = [j, others ascending]; row a pairs with the
-        // later vertices ascending on even rows, descending on odd rows
-        std::vector<uint32_t> order;
-        order.push_back(j);
-        for (uint32_t v = 0; v < an; ++v)
-            if (v != j) order.push_back(v);
-        for (uint32_t a = 0; a + 1 < an; ++a) {
-            if (a % 2 == 0)
-                for (uint32_t b = a + 1; b < an; ++b) cross(a0 + order[a], a0 + order[b]);
-            else
-                for (uint32_t b = an; b-- > a + 1;) cross(a0 + order[a], a0 + order[b]);
-        }
-        for (uint32_t blk = a0; blk < a0 + an; ++blk) self_task(blk);
-    }
-}
-}  // namespace
-}  // extern "C++"
-
 chgpu_status chgpu_plan_exhaustive(uint32_t image_count, uint32_t block_images, uint32_t blocks_per_group,
                                    uint32_t* pairs_out, uint64_t* npairs_out) {
     if (image_count == 0 || block_images == 0 || blocks_per_group == 0 || !npairs_out) return CHGPU_EINVAL;
@@ -300,7 +248,7 @@ chgpu_status chgpu_plan_exhaustive(uint32_t image_count, uint32_t block_images, 
         }
         ++np;
     };
-    for_each_plan_task(
+    chgpu::for_each_plan_task(
         image_count, block_images, blocks_per_group,
         [&](uint32_t ba, uint32_t bb) {
             for (uint32_t a = block_lo(ba); a < block_hi(ba); ++a)
@@ -345,7 +293,7 @@ chgpu_status chgpu_plan_guided(uint32_t image_count, uint32_t block_images, uint
             ++np;
         }
     };
-    for_each_plan_task(
+    chgpu::for_each_plan_task(
         image_count, block_images, blocks_per_group, [&](uint32_t ba, uint32_t bb) { emit_bucket(uint64_t(ba) * nblocks + bb); },
         [&](uint32_t blk) { emit_bucket(uint64_t(blk) * nblocks + blk); });
     *npairs_out = np;

@@ -172,6 +172,46 @@ static void host_checks(const std::filesystem::path& tmp) {
     }
     CHECK(throws<std::invalid_argument>([] { ch::plan_exhaustive(0, 1, 1); }));
 
+    // scheduler.hpp:29-134 through the facade: partition, tasks with their pairs, residency traces, sizing
+    {
+        const ch::Partition part = ch::make_partition(23, 4, 3);
+        CHECK(part.block_count() == 6 && part.group_count() == 2 && part.block_size(5) == 3 && part.block_group_of[4] == 1);
+        const ch::PairPlan plan = ch::plan_exhaustive(part);
+        CHECK(plan.pair_count() == 23 * 22 / 2);
+        std::size_t at = 0;
+        for (const ch::PlanTask& t : plan.tasks) {
+            CHECK(t.block_a <= t.block_b && t.group_a == part.block_group_of[t.block_a] && t.group_b == part.block_group_of[t.block_b]);
+            for (const auto& pr : t.pairs) {
+                CHECK(pr == pairs[at] && pr.first / 4 == t.block_a && pr.second / 4 == t.block_b);
+                ++at;
+            }
+        }
+        const auto rtasks = ch::residency_tasks(plan);
+        const auto trace = ch::simulate_residency(rtasks, ch::ResidencyMode::Matching);
+        std::uint64_t want_n = 0;
+        CHECK(chor_simulate_residency(23, 4, 3, 1, 0, nullptr, 0, nullptr, 0, &want_n) == 0 && want_n == trace.size());
+        std::vector<std::uint32_t> want(want_n * 4);
+        CHECK(chor_simulate_residency(23, 4, 3, 1, 0, nullptr, 0, want.data(), want_n, &want_n) == 0);
+        for (std::size_t i = 0; i < trace.size(); ++i)
+            CHECK(std::uint32_t(trace[i].kind) == want[4 * i] && std::uint32_t(trace[i].level) == want[4 * i + 1] &&
+                  trace[i].id == want[4 * i + 2] && std::uint32_t(trace[i].prefetch) == want[4 * i + 3]);
+        const auto htrace = ch::simulate_residency(ch::hashing_residency_tasks(part), ch::ResidencyMode::Hashing);
+        CHECK(chor_simulate_residency(23, 4, 3, 0, 0, nullptr, 0, nullptr, 0, &want_n) == 0 && want_n == htrace.size());
+        CHECK(ch::residency_slot_limit(ch::ResidencyMode::Hashing) == 2 && ch::residency_slot_limit(ch::ResidencyMode::Matching) == 3);
+        CHECK(throws<std::logic_error>([&] { ch::simulate_residency(rtasks, ch::ResidencyMode::Matching, 3, 1); }));
+        const ch::PairPlan guided = ch::plan_guided(part, {{3, 1}, {1, 3}, {20, 2}, {7, 6}});
+        CHECK(guided.tasks.size() == 3 && guided.pair_count() == 3);
+        CHECK(throws<std::invalid_argument>([&] { ch::plan_guided(part, {{3, 3}}); }));
+        const auto lanes = ch::assign_workers(plan, 4);
+        CHECK(lanes.size() == 4 && lanes[1][0] == 1 && lanes[1][1] == 5);
+        CHECK(throws<std::invalid_argument>([&] { ch::assign_workers(plan, 0); }));
+        std::uint32_t bi = 0, bpg = 0;
+        CHECK(chor_auto_partition_sizing(1179664, 64ull << 30, &bi, &bpg) == 0);
+        const ch::PartitionSizing sz = ch::auto_partition_sizing(1179664, 64ull << 30);
+        CHECK(sz.block_images == bi && sz.blocks_per_group == bpg);
+        CHECK(throws<std::invalid_argument>([] { ch::make_partition(0, 1, 1); }));
+    }
+
     // code cache (hashing.hpp:134-157): bytes identical to the oracle's file, round trip, header probe, the
     // reference's error classes
     {

@@ -106,6 +106,23 @@ def main() -> None:
         guided[f"pairs_{k}_{np_}_{m}"] = pairs
         guided[f"sizes_{k}_{np_}_{m}"] = sizes
     np.savez_compressed(OUT / "plans_guided.npz", **guided)
+    # ---- residency schedule (scheduler.cpp:175-345): task blocks and full action traces -----------------------------
+    res = {}
+    rng = np.random.default_rng(29)
+    for (k, np_, m) in ((10, 3, 2), (23, 2, 3), (40, 3, 4), (64, 5, 4), (9, 1, 4), (5, 8, 3), (31, 4, 1)):
+        key = f"{k}_{np_}_{m}"
+        res[f"tasks_{key}"] = ref.plan_task_blocks(k, np_, m)
+        res[f"trace_match_{key}"] = ref.simulate_residency(k, np_, m, 1)
+        res[f"trace_hash_{key}"] = ref.simulate_residency(k, np_, m, 0)
+        acc = rng.integers(0, k, (3 * k, 2)).astype(np.uint32)
+        acc = acc[acc[:, 0] != acc[:, 1]]
+        res[f"accepted_{key}"] = acc
+        res[f"tasks_guided_{key}"] = ref.plan_task_blocks(k, np_, m, acc)
+        res[f"trace_guided_{key}"] = ref.simulate_residency(k, np_, m, 1, acc)
+    sizing_in = np.array([[1179664, 64 << 30], [0, 0], [1, 10], [1565464, 180 << 30], [144, 1 << 20], [10**6, 10**6]], dtype=np.uint64)
+    res["sizing_in"] = sizing_in
+    res["sizing_out"] = np.array([ref.auto_partition_sizing(int(a), int(b)) for a, b in sizing_in], dtype=np.uint32)
+    np.savez_compressed(OUT / "residency.npz", **res)
     # ---- code cache written by the reference (hashing.cpp:184-206) for image 0 of the small dataset --
     cache = {"centering_fp": np.uint64(ref.centering_fingerprint(centering))}
     with tempfile.TemporaryDirectory() as td:

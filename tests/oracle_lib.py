@@ -66,6 +66,9 @@ class Oracle:
             "chor_time_match_pairs": [P, P, P, P, P, P, P, U32, U32, P, P],
             "chor_plan_exhaustive": [U32, U32, U32, P, P, P, P],
             "chor_plan_guided": [U32, U32, U32, P, C.c_uint64, P, P, P, P],
+            "chor_plan_task_blocks": [U32, U32, U32, C.c_int, P, C.c_uint64, P, P],
+            "chor_simulate_residency": [U32, U32, U32, C.c_int, C.c_int, P, C.c_uint64, P, C.c_uint64, P],
+            "chor_auto_partition_sizing": [C.c_uint64, C.c_uint64, P, P],
             "chor_centering_fingerprint": [P, P],
             "chor_save_code_cache": [P, U64, P, P, U32, C.c_char_p],
             "chor_load_code_cache": [C.c_char_p, P, U64, U32, P, P, P, P, P],
@@ -267,6 +270,35 @@ class Oracle:
         self._check(self.lib.chor_plan_guided(image_count, block_images, blocks_per_group, acc.ctypes.data, C.c_uint64(len(acc)),
                                               pairs.ctypes.data, C.byref(n), sizes.ctypes.data, C.byref(nt)), "plan_guided")
         return pairs[: n.value].copy(), sizes[: nt.value].copy()
+
+    def plan_task_blocks(self, image_count: int, block_images: int, blocks_per_group: int, accepted=None):
+        """(ntasks, 4) u32: group_a, group_b, block_a, block_b of every PlanTask."""
+        acc = None if accepted is None else np.ascontiguousarray(accepted, dtype=np.uint32).reshape(-1, 2)
+        nt = C.c_uint32(0)
+        cap = image_count * image_count + 4
+        out = np.zeros((cap, 4), dtype=np.uint32)
+        self._check(self.lib.chor_plan_task_blocks(image_count, block_images, blocks_per_group, 0 if acc is None else 1,
+                                                   None if acc is None or not len(acc) else acc.ctypes.data,
+                                                   C.c_uint64(0 if acc is None else len(acc)), out.ctypes.data, C.byref(nt)),
+                    "plan_task_blocks")
+        return out[: nt.value].copy()
+
+    def simulate_residency(self, image_count: int, block_images: int, blocks_per_group: int, mode: int, accepted=None):
+        """(nactions, 4) u32: kind, level, id, prefetch (simulate_residency over the plan's residency tasks)."""
+        acc = None if accepted is None else np.ascontiguousarray(accepted, dtype=np.uint32).reshape(-1, 2)
+        args = (image_count, block_images, blocks_per_group, mode, 0 if acc is None else 1,
+                None if acc is None or not len(acc) else acc.ctypes.data, C.c_uint64(0 if acc is None else len(acc)))
+        n = C.c_uint64(0)
+        self._check(self.lib.chor_simulate_residency(*args, None, C.c_uint64(0), C.byref(n)), "simulate_residency")
+        out = np.zeros((max(n.value, 1), 4), dtype=np.uint32)
+        self._check(self.lib.chor_simulate_residency(*args, out.ctypes.data, C.c_uint64(n.value), C.byref(n)), "simulate_residency")
+        return out[: n.value].copy()
+
+    def auto_partition_sizing(self, mean_image_bytes: int, memory_budget_bytes: int):
+        a, b = C.c_uint32(0), C.c_uint32(0)
+        self._check(self.lib.chor_auto_partition_sizing(C.c_uint64(mean_image_bytes), C.c_uint64(memory_budget_bytes),
+                                                        C.byref(a), C.byref(b)), "auto_partition_sizing")
+        return a.value, b.value
 
     def time_match_pairs(self, params, cfg, descs, shorts, longs, pairs, threads: int):
         """descs/shorts/longs: lists of per-image arrays.  Returns (seconds, total matches)."""
