@@ -169,7 +169,22 @@ typedef struct chgpu_load_stats {
 chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, const uint32_t* image_ids, uint32_t count,
                                    uint32_t io_threads, int accumulate_centering, chgpu_file_result* results,
                                    chgpu_load_stats* stats /* nullable */);
+/* Background form of the loader, for overlapping the load of the NEXT block with the matching of the current task
+ * (the two-line exchange of PAPER.md:73-94; the loader thread of engine.cpp:414-442).  _begin starts the reader
+ * threads into a deeper pinned ring (paths and ids are copied) and returns at once; while the job is open every
+ * chgpu_match_pairs* call on this context moves it forward between its sub-batches — files the readers have
+ * finished are sent with cudaMemcpyAsync and split on the device, under the match kernels already launched, all on
+ * the calling thread (a context stays thread-compatible).  _end handles what is left, drains and reports per file
+ * like chgpu_load_chft_files (results: count entries, nullable).  The images become usable after _end.  One job
+ * per context; other loads are CHGPU_ELOGIC while it is open. */
+chgpu_status chgpu_load_chft_files_begin(chgpu_ctx* ctx, const char* const* paths, const uint32_t* image_ids, uint32_t count,
+                                         uint32_t io_threads, int accumulate_centering);
+chgpu_status chgpu_load_chft_files_end(chgpu_ctx* ctx, chgpu_file_result* results /* nullable */,
+                                       chgpu_load_stats* stats /* nullable */);
 chgpu_status chgpu_evict_image(chgpu_ctx* ctx, uint32_t image_id);
+/* Batch form (block eviction, engine.cpp:420-441): one drain of the streams for the whole list.  Ids that are not
+ * resident are skipped and reported as CHGPU_ENOTFOUND after the rest has been released. */
+chgpu_status chgpu_evict_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32_t count);
 chgpu_status chgpu_image_points(chgpu_ctx* ctx, uint32_t image_id, uint32_t* n);
 chgpu_status chgpu_download_descriptors(chgpu_ctx* ctx, uint32_t image_id, uint8_t* desc, float* keypoints);
 
@@ -354,7 +369,7 @@ typedef enum chgpu_action_kind { CHGPU_ACT_LOAD = 0, CHGPU_ACT_EVICT = 1, CHGPU_
 typedef enum chgpu_residency_level { CHGPU_LEVEL_GROUP = 0, CHGPU_LEVEL_BLOCK = 1 } chgpu_residency_level;
 typedef struct chgpu_residency_action {
     uint32_t kind;      /* chgpu_action_kind */
-    uint32_t level;     /* chgpu_residency_level (Load / Evict) */
+    uint32_t level;     /* chgpu_residency_level; meaningful for Load / Evict */
     uint32_t id;        /* group / block id, or task index (Begin / Finish) */
     uint32_t prefetch;  /* Load issued ahead of need (line 2) */
 } chgpu_residency_action;
@@ -379,7 +394,10 @@ void chgpu_partition_sizing_for_device(uint64_t device_image_bytes, uint64_t fil
  *   Load block   chgpu_load_chft_files of the block's files + chgpu_hash_images (hashing an 8K image costs 12 us,
  *                less than reading its CHCC cache back would),
  *   Evict block  chgpu_evict_image of its images;  Evict group: the pages are released (DONTNEED),
- *   Begin task   chgpu_match_pairs_stream over the task's pairs; the sink sees plan-order pair indices.
+ *   Begin task   chgpu_match_pairs_stream over the task's pairs.  What the schedule prefetches between Begin and
+ *                Finish of a task (its line 2) is opened as a background load (chgpu_load_chft_files_begin) before
+ *                the match call and completed behind it, so the H2D copies of the next block run under the match
+ *                kernels of the current one; CHGPU_STREAM_NO_OVERLAP=1 replays strictly in trace order (A/B).
  * Never more than block_slots blocks are resident; at the end everything the run loaded is evicted again.  The run
  * owns the context's image ids 0 .. image_count-1 (image id = index into paths).  Images whose file failed are
  * reported in file_results (image_count entries) and their pairs are skipped without output, like the reference's
@@ -393,6 +411,7 @@ typedef struct chgpu_streamed_stats {
     uint64_t tasks, pairs, pairs_skipped, matches;
     uint64_t block_loads, block_evictions, group_loads, group_evictions;
     uint64_t images_loaded, bytes_read;
+    uint64_t background_block_loads; /* of block_loads: opened before a task's match call and completed behind it */
     uint32_t max_resident_blocks, max_resident_groups;
     double load_seconds, hash_seconds, match_seconds, wall_seconds;
 } chgpu_streamed_stats;

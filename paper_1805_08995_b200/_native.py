@@ -90,6 +90,7 @@ class StreamedStatsC(C.Structure):
     _fields_ = [("tasks", C.c_uint64), ("pairs", C.c_uint64), ("pairs_skipped", C.c_uint64), ("matches", C.c_uint64),
                 ("block_loads", C.c_uint64), ("block_evictions", C.c_uint64), ("group_loads", C.c_uint64),
                 ("group_evictions", C.c_uint64), ("images_loaded", C.c_uint64), ("bytes_read", C.c_uint64),
+                ("background_block_loads", C.c_uint64),
                 ("max_resident_blocks", C.c_uint32), ("max_resident_groups", C.c_uint32),
                 ("load_seconds", C.c_double), ("hash_seconds", C.c_double), ("match_seconds", C.c_double),
                 ("wall_seconds", C.c_double)]
@@ -128,7 +129,10 @@ SIGNATURES = {
                                     C.POINTER(C.c_int), u64p]),
     "chgpu_load_chft_files": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), u32p, C.c_uint32, C.c_uint32, C.c_int,
                                         C.POINTER(FileResultC), C.POINTER(LoadStatsC)]),
+    "chgpu_load_chft_files_begin": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), u32p, C.c_uint32, C.c_uint32, C.c_int]),
+    "chgpu_load_chft_files_end": (C.c_int, [C.c_void_p, C.POINTER(FileResultC), C.POINTER(LoadStatsC)]),
     "chgpu_evict_image": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "chgpu_evict_images": (C.c_int, [C.c_void_p, u32p, C.c_uint32]),
     "chgpu_image_points": (C.c_int, [C.c_void_p, C.c_uint32, u32p]),
     "chgpu_download_descriptors": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
     "chgpu_set_hash_mode": (C.c_int, [C.c_void_p, C.c_int]),

@@ -568,6 +568,29 @@ class Matcher:
     def evict(self, image_id: int):
         self._ck(self.lib.chgpu_evict_image(self.h, image_id))
 
+    def load_chft_files_begin(self, paths, image_ids, io_threads: int = 8, accumulate_centering: bool = False):
+        """Background load (chgpu_load_chft_files_begin): returns at once; match calls on this Matcher move it forward."""
+        n = len(paths)
+        arr = (C.c_char_p * max(n, 1))(*[str(p).encode() for p in paths])
+        ids = np.ascontiguousarray(image_ids, dtype=np.uint32)
+        assert len(ids) == n
+        self._bg_paths = list(paths)
+        self._ck(self.lib.chgpu_load_chft_files_begin(self.h, arr, ids.ctypes.data_as(N.u32p), n, io_threads,
+                                                      1 if accumulate_centering else 0))
+
+    def load_chft_files_end(self):
+        """Completes the background load: (results, stats) as load_chft_files returns them."""
+        paths = getattr(self, "_bg_paths", [])
+        res = (N.FileResultC * max(len(paths), 1))()
+        st = N.LoadStatsC()
+        self._ck(self.lib.chgpu_load_chft_files_end(self.h, res, C.byref(st)))
+        self._bg_paths = []
+        return self._file_results(paths, res), st.as_dict()
+
+    def evict_many(self, image_ids):
+        ids = np.ascontiguousarray(image_ids, dtype=np.uint32)
+        self._ck(self.lib.chgpu_evict_images(self.h, ids.ctypes.data_as(N.u32p), len(ids)))
+
     def points(self, image_id: int) -> int:
         n = C.c_uint32(0)
         self._ck(self.lib.chgpu_image_points(self.h, image_id, C.byref(n)))

@@ -141,6 +141,8 @@ struct MatchBuffers {
 
 }  // namespace
 
+struct chgpu_load_job;
+
 struct chgpu_ctx {
     int device = 0;
     cudaDeviceProp prop{};
@@ -208,6 +210,7 @@ struct chgpu_ctx {
     size_t load_pinned_slot = 0, load_pinned_slots = 0;
     std::vector<std::pair<char*, size_t>> load_scratch;
     uint64_t sub_batch_queries = kSubBatchQueries;
+    chgpu_load_job* load_job = nullptr;  // background load opened by chgpu_load_chft_files_begin
 };
 
 namespace {
@@ -695,6 +698,8 @@ chgpu_status ensure_host_records(chgpu_ctx* ctx, MatchBuffers& b, size_t need) {
     return CHGPU_OK;
 }
 
+void load_pump(chgpu_load_job* job, bool block);  // streaming loader, below
+
 struct MatchRun {
     const uint32_t* pairs;
     uint32_t npairs;
@@ -985,10 +990,14 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
         st.total_launches += 3;
         // the result scratch d_res is shared: the next match kernel must not start before this
         // sub-batch's compaction, which stream order on `compute` already guarantees.
+        // a background load (chgpu_load_chft_files_begin) moves forward under the kernels just launched
+        if (ctx->load_job) load_pump(ctx->load_job, false);
         if (s >= 1)
             if (const chgpu_status e = finish(s - 1)) return e;
     }
+    if (ctx->load_job) load_pump(ctx->load_job, false);
     if (const chgpu_status e = finish(subs.size() - 1)) return e;
+    if (ctx->load_job) load_pump(ctx->load_job, false);
 
     CK(cudaEventRecord(ctx->ev_t1, ctx->compute));
     CK(cudaMemcpyAsync(ctx->h_stats, ctx->d_stats, sizeof(DevStats), cudaMemcpyDeviceToHost, ctx->compute));
@@ -1083,6 +1092,7 @@ chgpu_status chgpu_create(int device, chgpu_ctx** out) {
 void chgpu_destroy(chgpu_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    chgpu_load_chft_files_end(ctx, nullptr, nullptr);  // a background load left open
     cudaDeviceSynchronize();
     ctx->arena.destroy();
     for (MatchBuffers& b : ctx->mb) {
@@ -1394,6 +1404,7 @@ chgpu_status chgpu_upload_chft(chgpu_ctx* ctx, uint32_t image_id, const void* bl
 }
 
 // ---- streaming loader: disk -> pinned ring -> HBM ---------------------------------------------------
+extern "C++" {
 namespace {
 
 // Every slot has its own lock and condition variables: the issue thread wakes exactly the reader that waits for
@@ -1485,25 +1496,78 @@ void loader_thread(LoadRing* ring, const char* const* paths, uint32_t count) {
 
 }  // namespace
 
-chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, const uint32_t* image_ids, uint32_t count,
-                                   uint32_t io_threads, int accumulate_centering, chgpu_file_result* results,
-                                   chgpu_load_stats* stats) {
-    if (!ctx || (count && (!paths || !image_ids || !results))) return CHGPU_EINVAL;
-    DeviceGuard guard(ctx->device);
-    if (!ctx->has_family)
-        return fail(ctx, CHGPU_ELOGIC, "chgpu_set_family must precede image uploads (block layout depends on m, L)");
+// One streaming load in progress.  The issue side is a state machine the owning thread pumps: load_pump(block = true)
+// is the classic loop (wait for the next file, send it); load_pump(block = false) sends whatever the readers have
+// finished and returns — chgpu_match_pairs* calls it between sub-batches while a background job is open, so the
+// H2D copies of the next block run under the match kernels of the current task (the paper's exchange).
+struct chgpu_load_job {
+    chgpu_ctx* ctx = nullptr;
+    std::vector<std::string> path_store;
+    std::vector<const char*> paths;
+    std::vector<uint32_t> image_ids;
+    std::vector<chgpu_file_result> results;
+    uint32_t count = 0, io_threads = 0;
+    bool sums = false;
+    LoadRing ring;
+    size_t S = 0;
+    struct Scratch {
+        char* ptr = nullptr;
+        size_t cap = 0;
+        cudaEvent_t split_done = nullptr;
+        bool used = false;
+    };
+    std::vector<Scratch> scratch;  // device-side raw (AoS) ring
+    std::vector<std::thread> readers;
+    std::deque<uint32_t> in_flight;  // files whose H2D was issued, oldest first (copies complete in this order)
+    uint32_t next = 0;               // next file the issue side handles
+    uint32_t pub_lo = UINT32_MAX, pub_hi = 0;  // image-table range to publish when the batch is in
     chgpu_load_stats st{};
-    if (count == 0) {
-        if (stats) *stats = st;
-        return CHGPU_OK;
+    chgpu_status rc = CHGPU_OK;
+    std::chrono::steady_clock::time_point wall0;
+    double t_wait = 0, t_alloc = 0, t_issue = 0;
+};
+
+namespace {
+
+void load_poll_copies(chgpu_load_job* job) {  // slots whose H2D completed go back to the readers
+    LoadRing& ring = job->ring;
+    const size_t S = job->S;
+    size_t done = 0;
+    while (done < job->in_flight.size() && cudaEventQuery(ring.slots[job->in_flight[done] % S].copied) == cudaSuccess) ++done;
+    for (size_t k = 0; k < done; ++k) {
+        LoadSlot& s = ring.slots[job->in_flight[k] % S];
+        {
+            std::lock_guard<std::mutex> lock(s.mu);
+            s.in_flight = false;
+            s.state = LoadSlot::Free;
+            s.turn = s.file + uint32_t(S);
+        }
+        s.cv_free.notify_one();
     }
+    job->in_flight.erase(job->in_flight.begin(), job->in_flight.begin() + done);
+}
+
+// ring_slots pinned slots (>= 8, >= 2 per reader), scratch_slots device staging buffers.
+chgpu_status load_start(chgpu_ctx* ctx, const char* const* paths, const uint32_t* image_ids, uint32_t count, uint32_t io_threads,
+                        bool sums, size_t ring_slots, size_t scratch_slots, chgpu_load_job** out) {
+    std::unique_ptr<chgpu_load_job> job(new chgpu_load_job);
+    job->ctx = ctx;
+    job->count = count;
+    job->sums = sums;
+    job->path_store.reserve(count);
+    for (uint32_t i = 0; i < count; ++i) job->path_store.emplace_back(paths[i] ? paths[i] : "");
+    for (uint32_t i = 0; i < count; ++i) job->paths.push_back(job->path_store[i].c_str());
+    job->image_ids.assign(image_ids, image_ids + count);
+    job->results.assign(count, chgpu_file_result{});
     io_threads = std::max<uint32_t>(1, std::min<uint32_t>(io_threads ? io_threads : 4, 64));
-    const size_t S = std::max<size_t>(8, 2 * size_t(io_threads));
+    job->io_threads = io_threads;
+    const size_t S = std::max<size_t>(std::max<size_t>(8, 2 * size_t(io_threads)), ring_slots);
+    job->S = S;
     // Pinned ring buffers and device staging live in the context: cudaMallocHost / cudaMalloc cost milliseconds
     // and take the driver lock, so they are sized up front (first file + 12 %) on this thread and only a later,
     // larger file makes a reader grow its slot.
     size_t guess = size_t(2) << 20;
-    if (FILE* f0 = std::fopen(paths[0], "rb")) {
+    if (FILE* f0 = std::fopen(job->paths[0], "rb")) {
         std::fseek(f0, 0, SEEK_END);
         const long sz = std::ftell(f0);
         std::fclose(f0);
@@ -1521,7 +1585,7 @@ chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, con
         ctx->load_pinned_slots = S;
         ctx->load_pinned_slot = guess;
     }
-    LoadRing ring;
+    LoadRing& ring = job->ring;
     ring.slots.reset(new LoadSlot[S]);
     ring.nslots = S;
     for (size_t k = 0; k < S; ++k) {
@@ -1532,64 +1596,58 @@ chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, con
             return fail(ctx, CHGPU_ECUDA, "loader: event creation failed");
     }
     // device-side raw (AoS) scratch ring: deep enough that waiting for a split kernel never stalls the issue loop
-    constexpr size_t kScratch = 8;
-    struct Scratch {
-        char* ptr = nullptr;
-        size_t cap = 0;
-        cudaEvent_t split_done = nullptr;
-        bool used = false;
-    } scratch[kScratch];
-    if (ctx->load_scratch.size() < kScratch) ctx->load_scratch.resize(kScratch, {nullptr, 0});
-    for (size_t k = 0; k < kScratch; ++k) {
-        scratch[k].ptr = ctx->load_scratch[k].first;
-        scratch[k].cap = ctx->load_scratch[k].second;
-        cudaEventCreateWithFlags(&scratch[k].split_done, cudaEventDisableTiming);
+    const size_t nscratch = std::max<size_t>(8, scratch_slots);
+    if (ctx->load_scratch.size() < nscratch) ctx->load_scratch.resize(nscratch, {nullptr, 0});
+    job->scratch.resize(nscratch);
+    for (size_t k = 0; k < nscratch; ++k) {
+        job->scratch[k].ptr = ctx->load_scratch[k].first;
+        job->scratch[k].cap = ctx->load_scratch[k].second;
+        cudaEventCreateWithFlags(&job->scratch[k].split_done, cudaEventDisableTiming);
     }
-    uint32_t pub_lo = UINT32_MAX, pub_hi = 0;  // image-table range to publish when the batch is in
+    job->wall0 = std::chrono::steady_clock::now();
+    for (uint32_t t = 0; t < io_threads; ++t) job->readers.emplace_back(loader_thread, &job->ring, job->paths.data(), count);
+    *out = job.release();
+    return CHGPU_OK;
+}
 
-    const auto wall0 = std::chrono::steady_clock::now();
-    std::vector<std::thread> readers;
-    for (uint32_t t = 0; t < io_threads; ++t) readers.emplace_back(loader_thread, &ring, paths, count);
-
-    chgpu_status rc = CHGPU_OK;
-    std::deque<uint32_t> in_flight;  // files whose H2D was issued, oldest first (copies complete in this order)
-    auto poll_copies = [&]() {       // slots whose H2D completed go back to the readers
-        size_t done = 0;
-        while (done < in_flight.size() && cudaEventQuery(ring.slots[in_flight[done] % S].copied) == cudaSuccess) ++done;
-        for (size_t k = 0; k < done; ++k) {
-            LoadSlot& s = ring.slots[in_flight[k] % S];
-            {
-                std::lock_guard<std::mutex> lock(s.mu);
-                s.in_flight = false;
-                s.state = LoadSlot::Free;
-                s.turn = s.file + uint32_t(S);
-            }
-            s.cv_free.notify_one();
-        }
-        in_flight.erase(in_flight.begin(), in_flight.begin() + done);
-    };
-    const bool trace = getenv("CHGPU_LOADER_TRACE") != nullptr;
-    double t_wait = 0, t_alloc = 0, t_issue = 0;
+// Sends files to the device in list order.  block: until every file has been handled; otherwise until the next file
+// is not in its pinned slot yet or its device staging buffer is still waiting for an earlier split kernel.
+void load_pump(chgpu_load_job* job, bool block) {
+    chgpu_ctx* ctx = job->ctx;
+    LoadRing& ring = job->ring;
+    const size_t S = job->S, nscratch = job->scratch.size();
     auto now = [] { return std::chrono::steady_clock::now(); };
     auto secs = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
         return std::chrono::duration<double>(b - a).count();
     };
-    for (uint32_t i = 0; i < count && rc == CHGPU_OK; ++i) {
+    chgpu_load_stats& st = job->st;
+    while (job->next < job->count && job->rc == CHGPU_OK) {
+        const uint32_t i = job->next;
         LoadSlot& s = ring.slots[i % S];
+        chgpu_load_job::Scratch& sc = job->scratch[i % nscratch];
         const auto tw0 = now();
         {
             std::unique_lock<std::mutex> lock(s.mu);
             while (!(s.state == LoadSlot::Ready && s.file == i)) {
                 lock.unlock();
-                poll_copies();
+                load_poll_copies(job);
+                if (!block) return;
                 lock.lock();
                 if (s.state == LoadSlot::Ready && s.file == i) break;
                 s.cv_ready.wait_for(lock, std::chrono::microseconds(50));
             }
         }
+        if (sc.used) {  // its previous split kernel has to have consumed it
+            if (block) cudaEventSynchronize(sc.split_done);
+            else if (cudaEventQuery(sc.split_done) != cudaSuccess) {
+                cudaGetLastError();
+                return;
+            }
+        }
+        job->next = i + 1;
         const auto tw1 = now();
-        t_wait += secs(tw0, tw1);
-        chgpu_file_result& r = results[i];
+        job->t_wait += secs(tw0, tw1);
+        chgpu_file_result& r = job->results[i];
         r = chgpu_file_result{};
         auto release_slot = [&]() {
             {
@@ -1619,19 +1677,17 @@ chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, con
         if (s.bytes < 16 + raw_bytes) { bad(CHGPU_FAULT_TRUNCATED, s.bytes); continue; }
 
         uint32_t slot_img;
-        if (const chgpu_status e = alloc_image(ctx, image_ids[i], n, &slot_img)) {
+        if (const chgpu_status e = alloc_image(ctx, job->image_ids[i], n, &slot_img)) {
             r.status = e;
             ++st.files_failed;
             release_slot();
-            if (e == CHGPU_ENOMEM || e == CHGPU_ECUDA) rc = e;  // device trouble ends the batch; bad input does not
+            if (e == CHGPU_ENOMEM || e == CHGPU_ECUDA) job->rc = e;  // device trouble ends the batch; bad input does not
             continue;
         }
         ImageRec& img = ctx->images[slot_img];
         const auto tw2 = now();
-        t_alloc += secs(tw1, tw2);
+        job->t_alloc += secs(tw1, tw2);
         if (n) {
-            Scratch& sc = scratch[i % kScratch];
-            if (sc.used) cudaEventSynchronize(sc.split_done);  // its previous split kernel has consumed it
             if (sc.cap < raw_bytes) {
                 if (sc.ptr) cudaFree(sc.ptr);
                 sc.ptr = nullptr;
@@ -1639,7 +1695,7 @@ chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, con
                 const size_t cap = std::max<size_t>(raw_bytes + raw_bytes / 8, size_t(2) << 20);
                 if (cudaMalloc(reinterpret_cast<void**>(&sc.ptr), cap) != cudaSuccess) {
                     cudaGetLastError();
-                    rc = fail(ctx, CHGPU_ENOMEM, "loader: device staging of %zu bytes", cap);
+                    job->rc = fail(ctx, CHGPU_ENOMEM, "loader: device staging of %zu bytes", cap);
                     release_slot();
                     break;
                 }
@@ -1648,9 +1704,9 @@ chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, con
             cudaMemcpyAsync(sc.ptr, s.buf + 16, raw_bytes, cudaMemcpyHostToDevice, ctx->copy);
             cudaEventRecord(s.copied, ctx->copy);
             s.in_flight = true;
-            in_flight.push_back(i);
+            job->in_flight.push_back(i);
             cudaStreamWaitEvent(ctx->compute, s.copied, 0);
-            if (accumulate_centering) {  // one launch: AoS -> SoA split with the column sums folded in
+            if (job->sums) {  // one launch: AoS -> SoA split with the column sums folded in
                 const uint32_t blocks = std::max(1u, std::min((n + 127u) / 128u, 2u * uint32_t(ctx->prop.multiProcessorCount)));
                 chft_split_sums_kernel<<<blocks, kSplitSumThreads, 0, ctx->compute>>>(
                     reinterpret_cast<const uint4*>(sc.ptr), n, reinterpret_cast<uint4*>(const_cast<uint8_t*>(img.dev.desc)),
@@ -1669,47 +1725,110 @@ chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, con
         }
         // the kernels above take pointers, not table entries: the table is published once, behind the loop
         ctx->h_images[slot_img] = ctx->images[slot_img].dev;
-        pub_lo = std::min(pub_lo, slot_img);
-        pub_hi = std::max(pub_hi, slot_img);
+        job->pub_lo = std::min(job->pub_lo, slot_img);
+        job->pub_hi = std::max(job->pub_hi, slot_img);
         r.status = CHGPU_OK;
         r.count = n;
         ++st.files_ok;
         st.points += n;
-        poll_copies();
-        t_issue += secs(tw2, now());
+        load_poll_copies(job);
+        job->t_issue += secs(tw2, now());
     }
-    if (trace)
+}
+
+// Handles what is left, publishes the image table, drains, joins the readers and frees the job.
+chgpu_status load_finish(chgpu_load_job* job, chgpu_file_result* results, chgpu_load_stats* stats) {
+    chgpu_ctx* ctx = job->ctx;
+    LoadRing& ring = job->ring;
+    const size_t S = job->S;
+    load_pump(job, true);
+    if (getenv("CHGPU_LOADER_TRACE") != nullptr)
         fprintf(stderr, "chgpu loader: %u files, issue thread waited %.3f s for readers, %.3f s in alloc_image, %.3f s issuing\n",
-                count, t_wait, t_alloc, t_issue);
-    // drain
-    if (rc != CHGPU_OK) ring.abort.store(true);
-    if (pub_lo <= pub_hi)
-        cudaMemcpyAsync(ctx->d_images + pub_lo, ctx->h_images + pub_lo, size_t(pub_hi - pub_lo + 1) * sizeof(DevImage),
-                        cudaMemcpyHostToDevice, ctx->copy);
+                job->count, job->t_wait, job->t_alloc, job->t_issue);
+    if (job->rc != CHGPU_OK) ring.abort.store(true);
+    if (job->pub_lo <= job->pub_hi)
+        cudaMemcpyAsync(ctx->d_images + job->pub_lo, ctx->h_images + job->pub_lo,
+                        size_t(job->pub_hi - job->pub_lo + 1) * sizeof(DevImage), cudaMemcpyHostToDevice, ctx->copy);
     cudaStreamSynchronize(ctx->copy);
     cudaStreamSynchronize(ctx->compute);
-    poll_copies();
+    load_poll_copies(job);
     ring.abort.store(true);
     for (size_t k = 0; k < S; ++k) {
         { std::lock_guard<std::mutex> lock(ring.slots[k].mu); }
         ring.slots[k].cv_free.notify_all();
     }
-    for (std::thread& t : readers) t.join();
+    for (std::thread& t : job->readers) t.join();
     const cudaError_t last = cudaGetLastError();
     for (size_t k = 0; k < S; ++k) {
         if (ring.slots[k].own) cudaFreeHost(ring.slots[k].buf);  // a reader outgrew its share of the region
         cudaEventDestroy(ring.slots[k].copied);
     }
-    for (size_t k = 0; k < kScratch; ++k) {
-        ctx->load_scratch[k] = {scratch[k].ptr, scratch[k].cap};
-        cudaEventDestroy(scratch[k].split_done);
+    for (size_t k = 0; k < job->scratch.size(); ++k) {
+        ctx->load_scratch[k] = {job->scratch[k].ptr, job->scratch[k].cap};
+        cudaEventDestroy(job->scratch[k].split_done);
     }
+    chgpu_load_stats st = job->st;
     st.bytes_read = ring.bytes_read;
     st.read_seconds = ring.read_seconds;
-    st.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    st.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - job->wall0).count();
+    if (results) std::copy(job->results.begin(), job->results.end(), results);
     if (stats) *stats = st;
+    const chgpu_status rc = job->rc;
+    delete job;
     if (rc == CHGPU_OK && last != cudaSuccess) return fail(ctx, CHGPU_ECUDA, "loader: %s", cudaGetErrorString(last));
     return rc;
+}
+
+}  // namespace
+}  // extern "C++"
+
+chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, const uint32_t* image_ids, uint32_t count,
+                                   uint32_t io_threads, int accumulate_centering, chgpu_file_result* results,
+                                   chgpu_load_stats* stats) {
+    if (!ctx || (count && (!paths || !image_ids || !results))) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    if (!ctx->has_family)
+        return fail(ctx, CHGPU_ELOGIC, "chgpu_set_family must precede image uploads (block layout depends on m, L)");
+    if (ctx->load_job) return fail(ctx, CHGPU_ELOGIC, "a background load is open (chgpu_load_chft_files_end first)");
+    if (count == 0) {
+        if (stats) *stats = chgpu_load_stats{};
+        return CHGPU_OK;
+    }
+    chgpu_load_job* job = nullptr;
+    if (const chgpu_status s = load_start(ctx, paths, image_ids, count, io_threads, accumulate_centering != 0, 0, 0, &job)) return s;
+    return load_finish(job, results, stats);
+}
+
+chgpu_status chgpu_load_chft_files_begin(chgpu_ctx* ctx, const char* const* paths, const uint32_t* image_ids, uint32_t count,
+                                         uint32_t io_threads, int accumulate_centering) {
+    if (!ctx || (count && (!paths || !image_ids))) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    if (!ctx->has_family)
+        return fail(ctx, CHGPU_ELOGIC, "chgpu_set_family must precede image uploads (block layout depends on m, L)");
+    if (ctx->load_job) return fail(ctx, CHGPU_ELOGIC, "a background load is already open");
+    if (count == 0) return CHGPU_OK;
+    // a ring deep enough that one pump per match-kernel launch keeps the copy engine fed (<= 192 files, <= 512 MiB)
+    size_t first_bytes = size_t(2) << 20;
+    if (FILE* f0 = std::fopen(paths[0], "rb")) {
+        std::fseek(f0, 0, SEEK_END);
+        const long sz = std::ftell(f0);
+        std::fclose(f0);
+        if (sz > 0) first_bytes = std::max(first_bytes, size_t(sz));
+    }
+    const size_t deep = std::max<size_t>(16, std::min<size_t>(std::min<size_t>(count, 192), (size_t(512) << 20) / first_bytes));
+    return load_start(ctx, paths, image_ids, count, io_threads, accumulate_centering != 0, deep, deep, &ctx->load_job);
+}
+
+chgpu_status chgpu_load_chft_files_end(chgpu_ctx* ctx, chgpu_file_result* results, chgpu_load_stats* stats) {
+    if (!ctx) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    if (!ctx->load_job) {
+        if (stats) *stats = chgpu_load_stats{};
+        return CHGPU_OK;
+    }
+    chgpu_load_job* job = ctx->load_job;
+    ctx->load_job = nullptr;
+    return load_finish(job, results, stats);
 }
 
 chgpu_status chgpu_evict_image(chgpu_ctx* ctx, uint32_t image_id) {
@@ -1723,6 +1842,27 @@ chgpu_status chgpu_evict_image(chgpu_ctx* ctx, uint32_t image_id) {
     ctx->slot_of.erase(image_id);
     dense_set(ctx, image_id, kNone);
     return CHGPU_OK;
+}
+
+chgpu_status chgpu_evict_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32_t count) {
+    if (!ctx || (count && !image_ids)) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    if (count == 0) return CHGPU_OK;
+    // one drain for the whole list: no kernel or copy still reads the blocks that go back to the arena
+    CK(cudaStreamSynchronize(ctx->copy));
+    CK(cudaStreamSynchronize(ctx->compute));
+    chgpu_status rc = CHGPU_OK;
+    for (uint32_t i = 0; i < count; ++i) {
+        uint32_t slot;
+        if (find_slot(ctx, image_ids[i], &slot) != CHGPU_OK) {
+            rc = CHGPU_ENOTFOUND;  // reported after the rest of the list has been released
+            continue;
+        }
+        release_slot(ctx, slot);
+        ctx->slot_of.erase(image_ids[i]);
+        dense_set(ctx, image_ids[i], kNone);
+    }
+    return rc;
 }
 
 chgpu_status chgpu_image_points(chgpu_ctx* ctx, uint32_t image_id, uint32_t* n) {

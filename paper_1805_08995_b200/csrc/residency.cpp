@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <vector>
@@ -271,11 +272,17 @@ struct Replay {
         std::vector<uint32_t> ids(cnt);
         for (uint32_t i = 0; i < cnt; ++i) ids[i] = lo + i;
         chgpu_load_stats ls{};
-        auto t0 = std::chrono::steady_clock::now();
+        const auto t0 = std::chrono::steady_clock::now();
         const chgpu_status s = chgpu_load_chft_files(ctx, paths + lo, ids.data(), cnt, io_threads, centering_only ? 1 : 0,
                                                      results.data() + lo, &ls);
         st.load_seconds += seconds_since(t0);
         st.bytes_read += ls.bytes_read;
+        return adopt_block(b, s);
+    }
+
+    // The block's files are on the device (results[] filled in): book-keeping + hash build of the images that made it.
+    chgpu_status adopt_block(uint32_t b, chgpu_status load_status) {
+        const uint32_t lo = part.lo(b), cnt = part.size(b);
         block_resident[b] = 1;
         std::vector<uint32_t> good;
         for (uint32_t i = 0; i < cnt; ++i)
@@ -284,9 +291,9 @@ struct Replay {
                 ok[lo + i] = 1;
             }
         st.images_loaded += good.size();
-        if (s != CHGPU_OK) return s;
+        if (load_status != CHGPU_OK) return load_status;
         if (!centering_only && !good.empty()) {
-            t0 = std::chrono::steady_clock::now();
+            const auto t0 = std::chrono::steady_clock::now();
             const chgpu_status h = chgpu_hash_images(ctx, good.data(), uint32_t(good.size()), 3);
             if (h == CHGPU_OK) chgpu_sync(ctx);
             st.hash_seconds += seconds_since(t0);
@@ -297,13 +304,57 @@ struct Replay {
         return CHGPU_OK;
     }
 
+    // Line 2 of the exchange: the blocks the schedule prefetches while task t runs are opened as ONE background load
+    // before the task's match call (which moves it forward between its sub-batches) and adopted when the task finishes.
+    std::vector<uint32_t> background;  // blocks of the open background load, in load order
+    chgpu_status begin_background(const std::vector<uint32_t>& blocks) {
+        if (blocks.empty()) return CHGPU_OK;
+        std::vector<const char*> ps;
+        std::vector<uint32_t> ids;
+        for (const uint32_t b : blocks)
+            for (uint32_t i = part.lo(b); i < part.hi(b); ++i) {
+                ps.push_back(paths[i]);
+                ids.push_back(i);
+            }
+        const auto t0 = std::chrono::steady_clock::now();
+        const chgpu_status s = chgpu_load_chft_files_begin(ctx, ps.data(), ids.data(), uint32_t(ids.size()), io_threads, 0);
+        st.load_seconds += seconds_since(t0);
+        if (s == CHGPU_OK) background = blocks;
+        return s;
+    }
+    chgpu_status end_background() {
+        if (background.empty()) return CHGPU_OK;
+        size_t total = 0;
+        for (const uint32_t b : background) total += part.size(b);
+        std::vector<chgpu_file_result> res(total);
+        chgpu_load_stats ls{};
+        const auto t0 = std::chrono::steady_clock::now();
+        const chgpu_status s = chgpu_load_chft_files_end(ctx, res.data(), &ls);
+        st.load_seconds += seconds_since(t0);  // what the task could not hide
+        st.bytes_read += ls.bytes_read;
+        size_t at = 0;
+        chgpu_status rc = s;
+        const std::vector<uint32_t> blocks = background;
+        background.clear();
+        for (const uint32_t b : blocks) {
+            std::copy(res.begin() + at, res.begin() + at + part.size(b), results.begin() + part.lo(b));
+            at += part.size(b);
+            const chgpu_status a = adopt_block(b, s);
+            if (rc == CHGPU_OK) rc = a;
+            ++st.background_block_loads;
+        }
+        return rc;
+    }
+
     void evict_block(uint32_t b, bool count) {
         if (!block_resident[b]) return;
+        std::vector<uint32_t> ids;
         for (uint32_t i = part.lo(b); i < part.hi(b); ++i)
             if (ok[i]) {
-                chgpu_evict_image(ctx, i);
+                ids.push_back(i);
                 ok[i] = 0;
             }
+        chgpu_evict_images(ctx, ids.data(), uint32_t(ids.size()));
         block_resident[b] = 0;
         if (count) {
             ++st.block_evictions;
@@ -457,6 +508,8 @@ chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths,
     chgpu_status rc = CHGPU_OK;
     std::vector<uint32_t> pairs;
     chgpu_residency_action act;
+    const char* no_overlap = std::getenv("CHGPU_STREAM_NO_OVERLAP");  // A/B switch: replay strictly in trace order
+    const bool overlap = !(no_overlap && no_overlap[0] == '1');
     while (rc == CHGPU_OK && m.step(act)) {
         if (act.kind == CHGPU_ACT_LOAD) {
             if (act.level == CHGPU_LEVEL_GROUP) rp.group_hint(act.id, true);
@@ -467,6 +520,27 @@ chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths,
         } else if (act.kind == CHGPU_ACT_BEGIN) {
             const chgpu_plan_task& t = tasks[act.id];
             ++rp.st.tasks;
+            // The schedule's line 2: everything it does between Begin and Finish of this task is prefetching for later
+            // tasks.  Evictions and page-cache hints happen now (the victims are not this task's blocks), the block
+            // loads run in the background of the task's match call.
+            std::vector<uint32_t> prefetch;
+            bool finished = false;
+            if (overlap) {
+                chgpu_residency_action nx;
+                while (m.step(nx)) {
+                    if (nx.kind == CHGPU_ACT_FINISH) {
+                        finished = true;
+                        break;
+                    }
+                    if (nx.level == CHGPU_LEVEL_GROUP) rp.group_hint(nx.id, nx.kind == CHGPU_ACT_LOAD);
+                    else if (nx.kind == CHGPU_ACT_LOAD) prefetch.push_back(nx.id);
+                    else if (std::find(prefetch.begin(), prefetch.end(), nx.id) != prefetch.end())
+                        prefetch.erase(std::find(prefetch.begin(), prefetch.end(), nx.id));
+                    else rp.evict_block(nx.id, true);
+                }
+                rc = rp.begin_background(prefetch);
+                if (rc != CHGPU_OK) break;
+            }
             // the task's pairs in plan order (scheduler.cpp:47-75), images that failed to load left out
             pairs.clear();
             uint64_t skipped = 0;
@@ -509,8 +583,14 @@ chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths,
             }
             if (rc == CHGPU_OK) flush(true);
             rp.st.pairs_skipped += skipped;
+            if (overlap) {
+                const chgpu_status e = rp.end_background();
+                if (rc == CHGPU_OK) rc = e;
+                (void)finished;
+            }
         }
     }
+    chgpu_load_chft_files_end(ctx, nullptr, nullptr);  // an error path may have left the background load open
     if (rc == CHGPU_OK && m.blocked) rc = CHGPU_EINVAL;  // slot limits below what one task needs
     rp.evict_all();
     rp.st.wall_seconds = seconds_since(wall0);

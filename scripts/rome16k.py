@@ -19,6 +19,45 @@ sys.path.insert(0, str(ROOT))
 import paper_1805_08995_b200 as ch  # noqa: E402
 
 
+def streamed(args, paths, accepted, K, n, write_s):
+    """The same workload with bounded residency: centering pass over the files, then the guided plan replayed under
+    the residency schedule (Load / Evict of blocks, matching task by task)."""
+    with ch.Matcher(0) as m:
+        m.set_family(ch.build_hash_family(ch.FamilyParams()))
+        t0 = time.perf_counter()
+        _, res = m.centering_pass_files(paths, args.block_images, io_threads=args.io_threads)
+        assert all(r == n for r in res)
+        t1 = time.perf_counter()
+        got = {"records": 0, "pairs": 0, "peak_used": 0}
+
+        def sink(task, pr, offs, recs):
+            got["records"] += len(recs)
+            got["pairs"] += len(pr)
+
+        st, res = m.match_plan_streamed(paths, args.block_images, args.blocks_per_group, ch.MatchConfig(), accepted_pairs=accepted,
+                                        group_slots=args.group_slots, block_slots=args.block_slots, io_threads=args.io_threads,
+                                        sink=sink)
+        t2 = time.perf_counter()
+        assert got["records"] == st["matches"] and got["pairs"] == st["pairs"]
+        props = m.device_props()
+    tasks = ch.plan_tasks(K, args.block_images, args.blocks_per_group, accepted)
+    line = {
+        "workload": f"BASELINE configs[3] Rome16K-shaped, OUT OF CORE: {K} images x {n} descriptors from CHFT files, (i,i+d) "
+                    f"d=1..{args.neighbors}; blocks of {args.block_images} images, {args.block_slots} block slots",
+        "images": K, "pairs": int(st["pairs"]), "tasks": len(tasks), "file_bytes": int(K * (16 + 144 * n)),
+        "dataset_write_s": write_s,
+        "centering_pass": {"seconds": t1 - t0, "GB_per_s": K * (16 + 144 * n) / (t1 - t0) / 1e9},
+        "streamed_run": {"seconds": t2 - t1, "pairs_per_s": st["pairs"] / (t2 - t1), **st},
+        "resident_bound_GB": args.block_slots * args.block_images * 1_565_464 / 1e9,
+        "end_to_end": {"seconds": t2 - t0, "pairs_per_s": st["pairs"] / (t2 - t0)},
+        "device": props["name"], "hbm_in_use_after_GB": (props["total_mem"] - props["free_mem"]) / 1e9,
+    }
+    print(json.dumps(line), flush=True)
+    if not args.keep:
+        for p in paths:
+            p.unlink()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--images", type=int, default=2048)
@@ -27,6 +66,13 @@ def main():
     ap.add_argument("--dir", default="/tmp/rome16k_shaped")
     ap.add_argument("--io-threads", type=int, default=16)
     ap.add_argument("--keep", action="store_true")
+    ap.add_argument("--streamed", action="store_true",
+                    help="out-of-core run (chgpu_match_plan_streamed): at most --block-slots blocks of --block-images images "
+                         "resident, loads / evictions by the residency schedule")
+    ap.add_argument("--block-images", type=int, default=1024)
+    ap.add_argument("--blocks-per-group", type=int, default=4)
+    ap.add_argument("--block-slots", type=int, default=3)
+    ap.add_argument("--group-slots", type=int, default=3)
     args = ap.parse_args()
     d = Path(args.dir)
     d.mkdir(parents=True, exist_ok=True)
@@ -53,9 +99,11 @@ def main():
                     f.write(rec.tobytes())
             paths.append(p)
     write_s = time.perf_counter() - t0
-    pairs = np.array([(i, i + dd) for i in range(K) for dd in range(1, args.neighbors + 1) if i + dd < K], dtype=np.uint32)
+    pairs_list = pairs = np.array([(i, i + dd) for i in range(K) for dd in range(1, args.neighbors + 1) if i + dd < K], dtype=np.uint32)
     pairs = ch.plan_guided(K, 50, 4, pairs)  # the reference's traversal order restricted to this list (scheduler.cpp:144-164)
 
+    if args.streamed:
+        return streamed(args, paths, pairs_list, K, n, write_s)
     with ch.Matcher(0) as m:
         m.set_family(ch.build_hash_family(ch.FamilyParams()))
         ids = np.arange(K, dtype=np.uint32)

@@ -236,8 +236,10 @@ def resident_reference(matcher, desc, pairs, cfg, centering, base_id=70000):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("guided", [False, True])
-def test_streamed_run_equals_resident_run(matcher, restatement, tmp_path, guided):
+@pytest.mark.parametrize("guided,overlap", [(False, True), (True, True), (False, False)])
+def test_streamed_run_equals_resident_run(matcher, restatement, tmp_path, monkeypatch, guided, overlap):
+    if not overlap:
+        monkeypatch.setenv("CHGPU_STREAM_NO_OVERLAP", "1")  # strictly in trace order
     sizes = [900, 1200, 700, 1500, 1, 1000, 0, 800, 1100, 950, 1300, 600, 1000, 1024, 990, 870, 1250, 640, 1111, 905, 1000, 333, 1500]
     desc, paths = write_dataset(tmp_path, sizes, seed=41)
     k, np_, m = len(sizes), 3, 2
@@ -273,6 +275,8 @@ def test_streamed_run_equals_resident_run(matcher, restatement, tmp_path, guided
     assert stats["block_loads"] == int(np.sum((trace["kind"] == api.LOAD) & (trace["level"] == api.BLOCK)))
     assert stats["block_evictions"] == int(np.sum((trace["kind"] == api.EVICT) & (trace["level"] == api.BLOCK)))
     assert stats["block_loads"] > (k + np_ - 1) // np_ or guided  # blocks really were re-loaded: the run was out of core
+    prefetched = int(np.sum((trace["kind"] == api.LOAD) & (trace["level"] == api.BLOCK) & (trace["prefetch"] == 1)))
+    assert stats["background_block_loads"] == (prefetched if overlap else 0)  # line 2 runs behind the match calls
     assert np.array_equal(np.concatenate(got_pairs), flat)  # plan order
     # nothing is left behind on the device
     for i in range(k):
@@ -319,3 +323,45 @@ def test_streamed_run_more_slots_and_failed_files(matcher, tmp_path):
     # one block slot cannot hold a cross task
     with pytest.raises(ValueError):
         matcher.match_plan_streamed(paths, np_, m, cfg, group_slots=3, block_slots=1)
+
+
+@pytest.mark.gpu
+def test_background_load_under_match_calls(matcher, tmp_path):
+    """chgpu_load_chft_files_begin / _end: a load opened before match calls completes behind them (the calls pump it
+    between sub-batches); images, per-file faults and match results are those of the blocking loader."""
+    sizes = [1500, 900, 0, 2048, 700, 1200, 1, 3000, 800, 1000, 640, 5000, 900, 1100, 30, 2500]
+    desc, paths = write_dataset(tmp_path, sizes, seed=47)
+    paths[4] = tmp_path / "absent.chft"
+    fam = ch.build_hash_family(ch.FamilyParams())
+    matcher.set_family(fam)
+    cfg = ch.MatchConfig()
+    first, rest = list(range(0, 6)), list(range(6, len(sizes)))
+    ids = [81000 + i for i in range(len(sizes))]
+    res, _ = matcher.load_chft_files([paths[i] for i in first], [ids[i] for i in first], io_threads=2)
+    assert isinstance(res[4], ch.FeatureFileError) and [r for i, r in enumerate(res) if i != 4] == [sizes[i] for i in first if i != 4]
+    live = [i for i in first if i != 4]
+    matcher.set_centering(np.full(128, 127.5))
+    matcher.hash([ids[i] for i in live])
+    pairs = np.array([(ids[a], ids[b]) for a in live for b in live if a < b], dtype=np.uint32)
+    matcher.set_sub_batch_queries(2048)  # many sub-batches: many pumps
+    try:
+        want = matcher.match_pairs(pairs, cfg)
+        matcher.load_chft_files_begin([paths[i] for i in rest], [ids[i] for i in rest], io_threads=3)
+        with pytest.raises(ch.LogicError):
+            matcher.load_chft_files([paths[0]], [99999])  # one job per context
+        got = matcher.match_pairs(pairs, cfg)
+        res, stats = matcher.load_chft_files_end()
+    finally:
+        matcher.set_sub_batch_queries(0)
+    assert res == [sizes[i] for i in rest] and stats["files_ok"] == len(rest)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+    for i in rest:
+        d, _ = matcher.descriptors(ids[i])
+        assert np.array_equal(d, desc[i])
+    matcher.hash([ids[i] for i in rest])
+    a, b = matcher.match_pairs([(ids[7], ids[11])], cfg)[:2]
+    assert len(b) > 100
+    assert matcher.load_chft_files_end() == ([], matcher.load_chft_files_end()[1])  # nothing open: a no-op
+    matcher.evict_many([ids[i] for i in live + rest])
+    with pytest.raises(KeyError):
+        matcher.points(ids[7])
