@@ -764,6 +764,73 @@ public:
         ck(st);
     }
 
+    // centering_pass (engine.cpp:545-559) over CHFT files, block by block, nothing left resident; files that fail are
+    // reported in `failures` (what() of the FeatureFileError the reference would have collected) and left out.
+    std::array<double, kDescriptorDim> centering_pass_files(const std::vector<std::filesystem::path>& files,
+                                                             std::uint32_t block_images, std::uint32_t io_threads = 8,
+                                                             std::vector<std::string>* failures = nullptr) {
+        std::vector<std::string> store;
+        std::vector<const char*> cpaths;
+        for (const auto& f : files) store.push_back(f.string());
+        for (const auto& f : store) cpaths.push_back(f.c_str());
+        std::vector<chgpu_file_result> res(files.size());
+        std::array<double, kDescriptorDim> c{};
+        const chgpu_status st = chgpu_centering_pass_files(ctx_, cpaths.data(), static_cast<std::uint32_t>(files.size()),
+                                                           block_images, io_threads, res.data(), c.data());
+        collect_failures(files, res, failures);
+        if (st == CHGPU_EINVAL) throw std::invalid_argument("centering: no descriptors in the stream");  // hashing.cpp:60
+        ck(st);
+        return c;
+    }
+
+    // Out-of-core run of a plan (execute_plan + ResidencyDriver, engine.cpp:252-456, :667-702): at most block_slots
+    // blocks of block_images images resident (0 = the reference's 3), the next block loading behind the current task.
+    // sink(task, pairs, offsets (k+1), records) per chunk, in plan order.  accepted == nullptr: the exhaustive plan.
+    using PlanSink = std::function<void(std::uint32_t, std::span<const std::pair<std::uint32_t, std::uint32_t>>,
+                                        std::span<const std::uint64_t>, std::span<const MatchRecord>)>;
+    chgpu_streamed_stats match_plan_streamed(const std::vector<std::filesystem::path>& files, const Partition& partition,
+                                             const MatchConfig& cfg, const PlanSink& sink,
+                                             const std::vector<std::pair<std::uint32_t, std::uint32_t>>* accepted = nullptr,
+                                             std::uint32_t group_slots = 0, std::uint32_t block_slots = 0,
+                                             std::uint32_t io_threads = 8, std::vector<std::string>* failures = nullptr) {
+        if (partition.image_count != files.size()) throw std::invalid_argument("match_plan_streamed: one file per image");
+        std::vector<std::string> store;
+        std::vector<const char*> cpaths;
+        for (const auto& f : files) store.push_back(f.string());
+        for (const auto& f : store) cpaths.push_back(f.c_str());
+        std::vector<chgpu_file_result> res(files.size());
+        const chgpu_match_cfg c = detail::to_c(cfg);
+        struct Thunk {
+            const PlanSink* sink;
+            std::exception_ptr error;
+        } thunk{&sink, nullptr};
+        auto trampoline = [](void* user, std::uint32_t task, const std::uint32_t* pairs, std::uint32_t count,
+                             const std::uint64_t* offs, const chgpu_match_record* rec) -> int {
+            Thunk* t = static_cast<Thunk*>(user);
+            try {
+                if (*t->sink)
+                    (*t->sink)(task, {reinterpret_cast<const std::pair<std::uint32_t, std::uint32_t>*>(pairs), count},
+                               {offs, static_cast<std::size_t>(count) + 1},
+                               {reinterpret_cast<const MatchRecord*>(rec), static_cast<std::size_t>(offs[count])});
+                return 0;
+            } catch (...) {
+                t->error = std::current_exception();
+                return 1;
+            }
+        };
+        static const std::uint32_t none[2] = {0, 0};
+        const std::uint32_t* acc = !accepted ? nullptr : (accepted->empty() ? none : reinterpret_cast<const std::uint32_t*>(accepted->data()));
+        chgpu_streamed_stats stats{};
+        const chgpu_status st = chgpu_match_plan_streamed(
+            ctx_, cpaths.data(), partition.image_count, partition.block_images, partition.blocks_per_group, group_slots, block_slots,
+            acc, accepted ? accepted->size() : 0, &c, io_threads, trampoline, &thunk, res.data(), &stats);
+        if (thunk.error) std::rethrow_exception(thunk.error);
+        collect_failures(files, res, failures);
+        if (st == CHGPU_EINVAL) throw std::invalid_argument("match_plan_streamed: bad pair list, or slot limits below what one task needs");
+        ck(st);
+        return stats;
+    }
+
     // epipolar-guided pair list (guided_match_pair, geometry.cpp:234-250): one row-major 3x3 F per pair
     std::vector<PairMatches> match_pairs_guided(std::span<const std::pair<std::uint32_t, std::uint32_t>> pairs,
                                                 std::span<const std::array<double, 9>> fmats, double band_px,
@@ -796,6 +863,18 @@ public:
 private:
     void ck(chgpu_status st) const {
         if (st != CHGPU_OK) detail::raise(st, chgpu_last_error(ctx_));
+    }
+    // per-file outcomes of a streamed load as the strings the reference collects (engine.cpp:315-318)
+    static void collect_failures(const std::vector<std::filesystem::path>& files, const std::vector<chgpu_file_result>& res,
+                                 std::vector<std::string>* failures) {
+        if (!failures) return;
+        for (std::size_t i = 0; i < files.size(); ++i) {
+            if (res[i].status == CHGPU_OK) continue;
+            if (res[i].status == CHGPU_EFORMAT)
+                failures->push_back(FeatureFileError(static_cast<FeatureFileFault>(res[i].fault - 1), files[i], res[i].fault_offset, "").what());
+            else
+                failures->push_back(files[i].string() + ": " + chgpu_status_name(static_cast<chgpu_status>(res[i].status)));
+        }
     }
     chgpu_ctx* ctx_ = nullptr;
     FamilyParams params_{};

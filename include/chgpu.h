@@ -171,10 +171,10 @@ chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, con
                                    chgpu_load_stats* stats /* nullable */);
 /* Background form of the loader, for overlapping the load of the NEXT block with the matching of the current task
  * (the two-line exchange of PAPER.md:73-94; the loader thread of engine.cpp:414-442).  _begin starts the reader
- * threads into a deeper pinned ring (paths and ids are copied) and returns at once; while the job is open every
- * chgpu_match_pairs* call on this context moves it forward between its sub-batches — files the readers have
- * finished are sent with cudaMemcpyAsync and split on the device, under the match kernels already launched, all on
- * the calling thread (a context stays thread-compatible).  _end handles what is left, drains and reports per file
+ * threads (paths and ids are copied) and returns at once; while the job is open every chgpu_match_pairs* call on
+ * this context moves it forward wherever it would otherwise sleep on the device — files the readers have finished
+ * are sent with cudaMemcpyAsync under the match kernels already launched and split behind them, all on the calling
+ * thread (a context stays thread-compatible).  _end handles what is left, drains and reports per file
  * like chgpu_load_chft_files (results: count entries, nullable).  The images become usable after _end.  One job
  * per context; other loads are CHGPU_ELOGIC while it is open. */
 chgpu_status chgpu_load_chft_files_begin(chgpu_ctx* ctx, const char* const* paths, const uint32_t* image_ids, uint32_t count,
@@ -414,6 +414,7 @@ typedef struct chgpu_streamed_stats {
     uint64_t background_block_loads; /* of block_loads: opened before a task's match call and completed behind it */
     uint32_t max_resident_blocks, max_resident_groups;
     double load_seconds, hash_seconds, match_seconds, wall_seconds;
+    double evict_seconds, hint_seconds; /* block evictions; page-cache hints of the group level */
 } chgpu_streamed_stats;
 chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths, uint32_t image_count,
                                        uint32_t block_images, uint32_t blocks_per_group,

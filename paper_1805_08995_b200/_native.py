@@ -93,7 +93,7 @@ class StreamedStatsC(C.Structure):
                 ("background_block_loads", C.c_uint64),
                 ("max_resident_blocks", C.c_uint32), ("max_resident_groups", C.c_uint32),
                 ("load_seconds", C.c_double), ("hash_seconds", C.c_double), ("match_seconds", C.c_double),
-                ("wall_seconds", C.c_double)]
+                ("wall_seconds", C.c_double), ("evict_seconds", C.c_double), ("hint_seconds", C.c_double)]
 
     def as_dict(self) -> dict:
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -147,6 +147,7 @@ struct chgpu_ctx {
     int device = 0;
     cudaDeviceProp prop{};
     cudaStream_t compute = nullptr, copy = nullptr;
+    cudaStream_t load = nullptr;  // H2D of background loads: runs beside the result copies (D2H on `copy`)
     cudaEvent_t ev_upload = nullptr, ev_compute = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
     std::string err;
 
@@ -211,6 +212,8 @@ struct chgpu_ctx {
     std::vector<std::pair<char*, size_t>> load_scratch;
     uint64_t sub_batch_queries = kSubBatchQueries;
     chgpu_load_job* load_job = nullptr;  // background load opened by chgpu_load_chft_files_begin
+    char* load_region = nullptr;         // its device staging, one allocation cut into slices
+    size_t load_region_bytes = 0;
 };
 
 namespace {
@@ -799,10 +802,28 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
     float match_ms = 0.f;
     uint64_t delivered_records = 0;
 
+    // While a background load is open this thread does not sleep on the device: it keeps the loader's issue side going
+    // (files the readers finished -> cudaMemcpyAsync on the load stream) under the match kernels and the result copies.
+    auto sync_copy = [&]() -> cudaError_t {
+        while (ctx->load_job) {
+            const cudaError_t q = cudaStreamQuery(ctx->copy);
+            if (q != cudaErrorNotReady) return q;
+            load_pump(ctx->load_job, false);
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
+        return cudaStreamSynchronize(ctx->copy);
+    };
     // finishes sub-batch s (already launched into mb[s & 1]): D2H + delivery
     auto finish = [&](size_t s) -> chgpu_status {
         MatchBuffers& b = ctx->mb[s & 1];
         const SubBatch& sb = subs[s];
+        while (ctx->load_job) {
+            const cudaError_t q = cudaEventQuery(b.ev_done);
+            if (q == cudaSuccess) break;
+            if (q != cudaErrorNotReady) CK(q);
+            load_pump(ctx->load_job, false);
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
         CK(cudaEventSynchronize(b.ev_done));
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, b.ev_k0, b.ev_k1));
@@ -810,7 +831,7 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
         if (!host_side) return CHGPU_OK;
         CK(cudaMemcpyAsync(b.h_offsets, b.d_offsets, (size_t(sb.count) + 1) * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, ctx->copy));
-        CK(cudaStreamSynchronize(ctx->copy));
+        CK(sync_copy());
         const uint64_t total = b.h_offsets[sb.count];
         if (run.mode == SinkMode::Host) {
             for (uint32_t k = 0; k < sb.count; ++k) run.offsets[sb.first + k + 1] = delivered_records + b.h_offsets[k + 1];
@@ -819,13 +840,13 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
             } else if (total) {
                 CK(cudaMemcpyAsync(run.records + delivered_records, b.d_records, total * sizeof(uint4),
                                    cudaMemcpyDeviceToHost, ctx->copy));
-                CK(cudaStreamSynchronize(ctx->copy));
+                CK(sync_copy());
             }
         } else {
             if (const chgpu_status e = ensure_host_records(ctx, b, std::max<uint64_t>(total, 1))) return e;
             if (total) {
                 CK(cudaMemcpyAsync(b.h_records, b.d_records, total * sizeof(uint4), cudaMemcpyDeviceToHost, ctx->copy));
-                CK(cudaStreamSynchronize(ctx->copy));
+                CK(sync_copy());
             }
             if (run.sink) {
                 static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "offset width");
@@ -1065,6 +1086,7 @@ chgpu_status chgpu_create(int device, chgpu_ctx** out) {
     bool ok = true;
     ok &= cudaStreamCreateWithFlags(&ctx->compute, cudaStreamNonBlocking) == cudaSuccess;
     ok &= cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) == cudaSuccess;
+    ok &= cudaStreamCreateWithFlags(&ctx->load, cudaStreamNonBlocking) == cudaSuccess;
     ok &= cudaEventCreateWithFlags(&ctx->ev_upload, cudaEventDisableTiming) == cudaSuccess;
     ok &= cudaEventCreateWithFlags(&ctx->ev_compute, cudaEventDisableTiming) == cudaSuccess;
     ok &= cudaEventCreate(&ctx->ev_t0) == cudaSuccess;
@@ -1112,6 +1134,7 @@ void chgpu_destroy(chgpu_ctx* ctx) {
     cudaFree(ctx->d_stats); cudaFreeHost(ctx->h_stats); cudaFree(ctx->d_counter); cudaFree(ctx->d_slots);
     cudaFree(ctx->d_dbg); cudaFree(ctx->d_gmin); cudaFree(ctx->d_gdone); cudaFree(ctx->d_lists); cudaFree(ctx->d_act); cudaFree(ctx->d_nact);
     cudaFreeHost(ctx->load_pinned);
+    cudaFree(ctx->load_region);
     for (auto& b : ctx->load_scratch) cudaFree(b.first);
     cudaFree(ctx->d_planes_t); cudaFree(ctx->d_bias); cudaFree(ctx->d_hnorm); cudaFree(ctx->d_hq);
     cudaFree(ctx->d_hq_count); cudaFree(ctx->d_hstats);
@@ -1121,6 +1144,7 @@ void chgpu_destroy(chgpu_ctx* ctx) {
     if (ctx->ev_t1) cudaEventDestroy(ctx->ev_t1);
     if (ctx->compute) cudaStreamDestroy(ctx->compute);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
+    if (ctx->load) cudaStreamDestroy(ctx->load);
     cudaGetLastError();
     delete ctx;
 }
@@ -1515,8 +1539,17 @@ struct chgpu_load_job {
         size_t cap = 0;
         cudaEvent_t split_done = nullptr;
         bool used = false;
+        bool own = true;  // its own cudaMalloc (kept by the context between calls); false: a slice of the staging region
+        bool outgrown = false;  // region mode: a private buffer for a file larger than a slice, freed with the job
+        // region mode: the split kernel of the file it holds is launched later (load_flush_splits)
+        bool split_pending = false;
+        uint32_t n = 0;
+        uint8_t* dst_desc = nullptr;
+        float4* dst_kp = nullptr;
     };
     std::vector<Scratch> scratch;  // device-side raw (AoS) ring
+    bool region_mode = false;
+    cudaEvent_t last_copied = nullptr;  // region mode: event of the latest H2D copy
     std::vector<std::thread> readers;
     std::deque<uint32_t> in_flight;  // files whose H2D was issued, oldest first (copies complete in this order)
     uint32_t next = 0;               // next file the issue side handles
@@ -1597,17 +1630,68 @@ chgpu_status load_start(chgpu_ctx* ctx, const char* const* paths, const uint32_t
     }
     // device-side raw (AoS) scratch ring: deep enough that waiting for a split kernel never stalls the issue loop
     const size_t nscratch = std::max<size_t>(8, scratch_slots);
-    if (ctx->load_scratch.size() < nscratch) ctx->load_scratch.resize(nscratch, {nullptr, 0});
     job->scratch.resize(nscratch);
-    for (size_t k = 0; k < nscratch; ++k) {
-        job->scratch[k].ptr = ctx->load_scratch[k].first;
-        job->scratch[k].cap = ctx->load_scratch[k].second;
-        cudaEventCreateWithFlags(&job->scratch[k].split_done, cudaEventDisableTiming);
+    if (scratch_slots == 0) {
+        if (ctx->load_scratch.size() < nscratch) ctx->load_scratch.resize(nscratch, {nullptr, 0});
+        for (size_t k = 0; k < nscratch; ++k) {
+            job->scratch[k].ptr = ctx->load_scratch[k].first;
+            job->scratch[k].cap = ctx->load_scratch[k].second;
+        }
+    } else {
+        // background loads: one region, allocated now while the device is idle (a cudaMalloc issued under a running
+        // kernel waits for it) and cut into slices
+        if (ctx->load_region_bytes < nscratch * guess) {
+            CK(cudaStreamSynchronize(ctx->compute));
+            cudaFree(ctx->load_region);
+            ctx->load_region = nullptr;
+            ctx->load_region_bytes = 0;
+            if (cudaMalloc(reinterpret_cast<void**>(&ctx->load_region), nscratch * guess) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(ctx, CHGPU_ENOMEM, "loader: %zu bytes of device staging", nscratch * guess);
+            }
+            ctx->load_region_bytes = nscratch * guess;
+        }
+        job->region_mode = true;
+        for (size_t k = 0; k < nscratch; ++k) {
+            job->scratch[k].ptr = ctx->load_region + k * guess;
+            job->scratch[k].cap = guess;
+            job->scratch[k].own = false;
+        }
     }
+    for (size_t k = 0; k < nscratch; ++k) cudaEventCreateWithFlags(&job->scratch[k].split_done, cudaEventDisableTiming);
     job->wall0 = std::chrono::steady_clock::now();
     for (uint32_t t = 0; t < io_threads; ++t) job->readers.emplace_back(loader_thread, &job->ring, job->paths.data(), count);
     *out = job.release();
     return CHGPU_OK;
+}
+
+// AoS -> SoA split of the file a staging buffer holds (with the centering sums folded in when the job collects them).
+void load_launch_split(chgpu_load_job* job, chgpu_load_job::Scratch& sc) {
+    chgpu_ctx* ctx = job->ctx;
+    const uint32_t n = sc.n;
+    if (job->sums) {
+        const uint32_t blocks = std::max(1u, std::min((n + 127u) / 128u, 2u * uint32_t(ctx->prop.multiProcessorCount)));
+        chft_split_sums_kernel<<<blocks, kSplitSumThreads, 0, ctx->compute>>>(reinterpret_cast<const uint4*>(sc.ptr), n,
+                                                                             reinterpret_cast<uint4*>(sc.dst_desc),
+                                                                             reinterpret_cast<uint4*>(sc.dst_kp), ctx->d_sums);
+    } else {
+        const uint32_t blocks = uint32_t(std::min<uint64_t>((uint64_t(n) * 9 + 255) / 256, 8u * ctx->prop.multiProcessorCount));
+        chft_split_kernel<<<blocks, 256, 0, ctx->compute>>>(reinterpret_cast<const uint4*>(sc.ptr), n,
+                                                           reinterpret_cast<uint4*>(sc.dst_desc), reinterpret_cast<uint4*>(sc.dst_kp));
+    }
+    cudaEventRecord(sc.split_done, ctx->compute);
+    sc.used = true;
+    sc.split_pending = false;
+}
+
+// Region mode: launches the split kernels held back so far (behind the copies issued so far).
+void load_flush_splits(chgpu_load_job* job) {
+    bool any = false;
+    for (auto& sc : job->scratch) any = any || sc.split_pending;
+    if (!any) return;
+    if (job->last_copied) cudaStreamWaitEvent(job->ctx->compute, job->last_copied, 0);  // copies complete in issue order
+    for (auto& sc : job->scratch)
+        if (sc.split_pending) load_launch_split(job, sc);
 }
 
 // Sends files to the device in list order.  block: until every file has been handled; otherwise until the next file
@@ -1638,6 +1722,7 @@ void load_pump(chgpu_load_job* job, bool block) {
             }
         }
         if (sc.used) {  // its previous split kernel has to have consumed it
+            if (sc.split_pending) load_flush_splits(job);  // (a job with more files than staging buffers)
             if (block) cudaEventSynchronize(sc.split_done);
             else if (cudaEventQuery(sc.split_done) != cudaSuccess) {
                 cudaGetLastError();
@@ -1689,7 +1774,7 @@ void load_pump(chgpu_load_job* job, bool block) {
         job->t_alloc += secs(tw1, tw2);
         if (n) {
             if (sc.cap < raw_bytes) {
-                if (sc.ptr) cudaFree(sc.ptr);
+                if (sc.ptr && sc.own) cudaFree(sc.ptr);
                 sc.ptr = nullptr;
                 sc.cap = 0;
                 const size_t cap = std::max<size_t>(raw_bytes + raw_bytes / 8, size_t(2) << 20);
@@ -1700,26 +1785,28 @@ void load_pump(chgpu_load_job* job, bool block) {
                     break;
                 }
                 sc.cap = cap;
+                sc.own = true;
+                sc.outgrown = !job->region_mode ? false : true;
             }
-            cudaMemcpyAsync(sc.ptr, s.buf + 16, raw_bytes, cudaMemcpyHostToDevice, ctx->copy);
-            cudaEventRecord(s.copied, ctx->copy);
+            cudaStream_t h2d_stream = job->region_mode ? ctx->load : ctx->copy;
+            cudaMemcpyAsync(sc.ptr, s.buf + 16, raw_bytes, cudaMemcpyHostToDevice, h2d_stream);
+            cudaEventRecord(s.copied, h2d_stream);
             s.in_flight = true;
             job->in_flight.push_back(i);
-            cudaStreamWaitEvent(ctx->compute, s.copied, 0);
-            if (job->sums) {  // one launch: AoS -> SoA split with the column sums folded in
-                const uint32_t blocks = std::max(1u, std::min((n + 127u) / 128u, 2u * uint32_t(ctx->prop.multiProcessorCount)));
-                chft_split_sums_kernel<<<blocks, kSplitSumThreads, 0, ctx->compute>>>(
-                    reinterpret_cast<const uint4*>(sc.ptr), n, reinterpret_cast<uint4*>(const_cast<uint8_t*>(img.dev.desc)),
-                    reinterpret_cast<uint4*>(const_cast<float4*>(img.dev.kp)), ctx->d_sums);
-                ctx->sum_count += n;
+            sc.n = n;
+            sc.dst_desc = const_cast<uint8_t*>(img.dev.desc);
+            sc.dst_kp = const_cast<float4*>(img.dev.kp);
+            if (job->sums) ctx->sum_count += n;
+            if (job->region_mode) {
+                // A background load sends the bytes now and splits them later, in one go: hundreds of tiny launches
+                // queued behind a running match kernel would fill the launch queue and stall this thread.
+                sc.split_pending = true;
+                sc.used = true;
+                job->last_copied = s.copied;
             } else {
-                const uint32_t blocks = uint32_t(std::min<uint64_t>((uint64_t(n) * 9 + 255) / 256, 8u * ctx->prop.multiProcessorCount));
-                chft_split_kernel<<<blocks, 256, 0, ctx->compute>>>(reinterpret_cast<const uint4*>(sc.ptr), n,
-                                                                   reinterpret_cast<uint4*>(const_cast<uint8_t*>(img.dev.desc)),
-                                                                   reinterpret_cast<uint4*>(const_cast<float4*>(img.dev.kp)));
+                cudaStreamWaitEvent(ctx->compute, s.copied, 0);
+                load_launch_split(job, sc);
             }
-            cudaEventRecord(sc.split_done, ctx->compute);
-            sc.used = true;
         } else {
             release_slot();
         }
@@ -1742,6 +1829,7 @@ chgpu_status load_finish(chgpu_load_job* job, chgpu_file_result* results, chgpu_
     LoadRing& ring = job->ring;
     const size_t S = job->S;
     load_pump(job, true);
+    load_flush_splits(job);
     if (getenv("CHGPU_LOADER_TRACE") != nullptr)
         fprintf(stderr, "chgpu loader: %u files, issue thread waited %.3f s for readers, %.3f s in alloc_image, %.3f s issuing\n",
                 job->count, job->t_wait, job->t_alloc, job->t_issue);
@@ -1749,6 +1837,7 @@ chgpu_status load_finish(chgpu_load_job* job, chgpu_file_result* results, chgpu_
     if (job->pub_lo <= job->pub_hi)
         cudaMemcpyAsync(ctx->d_images + job->pub_lo, ctx->h_images + job->pub_lo,
                         size_t(job->pub_hi - job->pub_lo + 1) * sizeof(DevImage), cudaMemcpyHostToDevice, ctx->copy);
+    cudaStreamSynchronize(ctx->load);
     cudaStreamSynchronize(ctx->copy);
     cudaStreamSynchronize(ctx->compute);
     load_poll_copies(job);
@@ -1764,7 +1853,8 @@ chgpu_status load_finish(chgpu_load_job* job, chgpu_file_result* results, chgpu_
         cudaEventDestroy(ring.slots[k].copied);
     }
     for (size_t k = 0; k < job->scratch.size(); ++k) {
-        ctx->load_scratch[k] = {job->scratch[k].ptr, job->scratch[k].cap};
+        if (!job->region_mode) ctx->load_scratch[k] = {job->scratch[k].ptr, job->scratch[k].cap};
+        else if (job->scratch[k].outgrown) cudaFree(job->scratch[k].ptr);
         cudaEventDestroy(job->scratch[k].split_done);
     }
     chgpu_load_stats st = job->st;
@@ -1807,7 +1897,9 @@ chgpu_status chgpu_load_chft_files_begin(chgpu_ctx* ctx, const char* const* path
         return fail(ctx, CHGPU_ELOGIC, "chgpu_set_family must precede image uploads (block layout depends on m, L)");
     if (ctx->load_job) return fail(ctx, CHGPU_ELOGIC, "a background load is already open");
     if (count == 0) return CHGPU_OK;
-    // a ring deep enough that one pump per match-kernel launch keeps the copy engine fed (<= 192 files, <= 512 MiB)
+    // The split kernels queue behind the match kernel that is running, so a file's device staging buffer stays busy
+    // for up to one launch (~15 ms): the staging ring holds what the copy engine delivers in that time (<= 1,024
+    // files, <= 1.5 GiB); the pinned ring frees its slots as the copies complete and needs no more than usual.
     size_t first_bytes = size_t(2) << 20;
     if (FILE* f0 = std::fopen(paths[0], "rb")) {
         std::fseek(f0, 0, SEEK_END);
@@ -1815,8 +1907,8 @@ chgpu_status chgpu_load_chft_files_begin(chgpu_ctx* ctx, const char* const* path
         std::fclose(f0);
         if (sz > 0) first_bytes = std::max(first_bytes, size_t(sz));
     }
-    const size_t deep = std::max<size_t>(16, std::min<size_t>(std::min<size_t>(count, 192), (size_t(512) << 20) / first_bytes));
-    return load_start(ctx, paths, image_ids, count, io_threads, accumulate_centering != 0, deep, deep, &ctx->load_job);
+    const size_t staging = std::max<size_t>(16, std::min<size_t>(std::min<size_t>(count, 1024), (size_t(1536) << 20) / first_bytes));
+    return load_start(ctx, paths, image_ids, count, io_threads, accumulate_centering != 0, 64, staging, &ctx->load_job);
 }
 
 chgpu_status chgpu_load_chft_files_end(chgpu_ctx* ctx, chgpu_file_result* results, chgpu_load_stats* stats) {

@@ -233,9 +233,20 @@ __device__ __forceinline__ uint32_t first_key(const uint32_t (&key)[SLOTS], uint
 template <int SLOTS>
 __device__ __forceinline__ uint32_t next_key(const uint32_t (&key)[SLOTS], uint32_t extra, uint32_t prev) {
     const uint32_t nb = ~prev;  // -(prev + 1)
+#ifndef CHGPU_SERIAL_PULL
+    // two independent min chains (half the dependency depth, one more instruction: +0.3 % measured)
+    uint32_t acc = extra + nb, acc2 = key[0] + nb;
+#pragma unroll
+    for (int i = 1; i < SLOTS; ++i) {
+        if (i & 1) acc = min(acc, key[i] + nb);
+        else acc2 = min(acc2, key[i] + nb);
+    }
+    acc = min(acc, acc2);
+#else
     uint32_t acc = extra + nb;
 #pragma unroll
     for (int i = 0; i < SLOTS; ++i) acc = min(acc, key[i] + nb);
+#endif
     const uint32_t g = __reduce_min_sync(0xffffffffu, acc);
     return g >= nb - 1u ? kNone : g - nb;
 }

@@ -348,6 +348,7 @@ struct Replay {
 
     void evict_block(uint32_t b, bool count) {
         if (!block_resident[b]) return;
+        const auto t0 = std::chrono::steady_clock::now();
         std::vector<uint32_t> ids;
         for (uint32_t i = part.lo(b); i < part.hi(b); ++i)
             if (ok[i]) {
@@ -355,6 +356,7 @@ struct Replay {
                 ok[i] = 0;
             }
         chgpu_evict_images(ctx, ids.data(), uint32_t(ids.size()));
+        st.evict_seconds += seconds_since(t0);
         block_resident[b] = 0;
         if (count) {
             ++st.block_evictions;
@@ -363,6 +365,7 @@ struct Replay {
     }
 
     void group_hint(uint32_t g, bool load) {
+        const auto t0 = std::chrono::steady_clock::now();
         const uint32_t b0 = g * part.blocks_per_group, b1 = std::min(part.nblocks, b0 + part.blocks_per_group);
         for (uint32_t i = part.lo(b0); i < part.hi(b1 - 1); ++i)
             advise_file(paths[i], load ? POSIX_FADV_WILLNEED : POSIX_FADV_DONTNEED);
@@ -373,6 +376,7 @@ struct Replay {
             ++st.group_evictions;
             --resident_groups;
         }
+        st.hint_seconds += seconds_since(t0);
     }
 
     void evict_all() {
@@ -510,35 +514,26 @@ chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths,
     chgpu_residency_action act;
     const char* no_overlap = std::getenv("CHGPU_STREAM_NO_OVERLAP");  // A/B switch: replay strictly in trace order
     const bool overlap = !(no_overlap && no_overlap[0] == '1');
+    std::vector<uint32_t> pending;  // prefetched blocks whose load waits for the next Begin
     while (rc == CHGPU_OK && m.step(act)) {
         if (act.kind == CHGPU_ACT_LOAD) {
             if (act.level == CHGPU_LEVEL_GROUP) rp.group_hint(act.id, true);
+            else if (overlap && act.prefetch) pending.push_back(act.id);  // for a later task: behind the next match call
             else rc = rp.load_block(act.id);
         } else if (act.kind == CHGPU_ACT_EVICT) {
             if (act.level == CHGPU_LEVEL_GROUP) rp.group_hint(act.id, false);
-            else rp.evict_block(act.id, true);
+            else if (std::find(pending.begin(), pending.end(), act.id) != pending.end()) {
+                pending.erase(std::find(pending.begin(), pending.end(), act.id));  // evicted before it was ever loaded
+            } else rp.evict_block(act.id, true);
         } else if (act.kind == CHGPU_ACT_BEGIN) {
             const chgpu_plan_task& t = tasks[act.id];
             ++rp.st.tasks;
-            // The schedule's line 2: everything it does between Begin and Finish of this task is prefetching for later
-            // tasks.  Evictions and page-cache hints happen now (the victims are not this task's blocks), the block
-            // loads run in the background of the task's match call.
-            std::vector<uint32_t> prefetch;
-            bool finished = false;
-            if (overlap) {
-                chgpu_residency_action nx;
-                while (m.step(nx)) {
-                    if (nx.kind == CHGPU_ACT_FINISH) {
-                        finished = true;
-                        break;
-                    }
-                    if (nx.level == CHGPU_LEVEL_GROUP) rp.group_hint(nx.id, nx.kind == CHGPU_ACT_LOAD);
-                    else if (nx.kind == CHGPU_ACT_LOAD) prefetch.push_back(nx.id);
-                    else if (std::find(prefetch.begin(), prefetch.end(), nx.id) != prefetch.end())
-                        prefetch.erase(std::find(prefetch.begin(), prefetch.end(), nx.id));
-                    else rp.evict_block(nx.id, true);
-                }
-                rc = rp.begin_background(prefetch);
+            // Line 2 of the exchange: the prefetches the schedule issued since the last task (their evictions are done, their
+            // loads were held back) are opened as one background load that this task's match call moves forward; the
+            // reference's loader thread does the same while its workers run the task (engine.cpp:414-442, :679-696).
+            if (!pending.empty()) {
+                rc = rp.begin_background(pending);
+                pending.clear();
                 if (rc != CHGPU_OK) break;
             }
             // the task's pairs in plan order (scheduler.cpp:47-75), images that failed to load left out
@@ -583,10 +578,9 @@ chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths,
             }
             if (rc == CHGPU_OK) flush(true);
             rp.st.pairs_skipped += skipped;
-            if (overlap) {
+            {
                 const chgpu_status e = rp.end_background();
                 if (rc == CHGPU_OK) rc = e;
-                (void)finished;
             }
         }
     }

@@ -464,6 +464,44 @@ static void device_checks(const std::filesystem::path& tmp) {
         }
         CHECK(throws<std::out_of_range>([&] { m.codes(12345); }));
 
+        // out-of-core run of the same plan from CHFT files: blocks of one image, three slots (the reference's limit),
+        // the next block loading behind the current task — the same records, in plan order
+        {
+            std::vector<std::filesystem::path> files;
+            for (std::uint32_t i = 0; i < sets.size(); ++i) {
+                files.push_back(tmp / ("ooc_" + std::to_string(i) + ".chft"));
+                ch::save_features(sets[i], files.back());
+            }
+            ch::Matcher oc(0);
+            oc.set_family(fam2);
+            std::vector<std::string> failures;
+            CHECK(oc.centering_pass_files(files, 2, 2, &failures) == fam.centering && failures.empty());
+            const ch::Partition part = ch::make_partition(std::uint32_t(sets.size()), 1, 2);
+            std::vector<std::pair<std::uint32_t, std::uint32_t>> seen;
+            std::vector<std::vector<ch::MatchRecord>> recs;
+            const chgpu_streamed_stats ss = oc.match_plan_streamed(
+                files, part, {},
+                [&](std::uint32_t, std::span<const std::pair<std::uint32_t, std::uint32_t>> pr, std::span<const std::uint64_t> offs,
+                    std::span<const ch::MatchRecord> rec) {
+                    for (std::size_t k = 0; k < pr.size(); ++k) {
+                        seen.push_back(pr[k]);
+                        recs.emplace_back(rec.begin() + offs[k], rec.begin() + offs[k + 1]);
+                    }
+                },
+                nullptr, 0, 0, 2, &failures);
+            const auto plan1 = ch::plan_exhaustive(std::uint32_t(sets.size()), 1, 2);
+            CHECK(failures.empty() && seen == plan1 && ss.pairs == plan1.size() && ss.max_resident_blocks <= 3);
+            CHECK(ss.block_loads > sets.size() - 1 && ss.background_block_loads > 0);
+            for (std::size_t k = 0; k < seen.size(); ++k)
+                CHECK(recs[k] == oracle_match(fam, {}, sets[seen[k].first], ocodes[seen[k].first], sets[seen[k].second], ocodes[seen[k].second]));
+            CHECK(throws<std::out_of_range>([&] { oc.codes(0); }));  // nothing stays resident
+            std::filesystem::remove(files[1]);
+            failures.clear();
+            const chgpu_streamed_stats s2 = oc.match_plan_streamed(files, part, {}, nullptr, nullptr, 0, 0, 2, &failures);
+            CHECK(failures.size() >= 1 && s2.pairs_skipped == sets.size() - 1 && s2.pairs == plan1.size() - (sets.size() - 1));
+            CHECK(throws<std::invalid_argument>([&] { oc.match_plan_streamed(files, part, {}, nullptr, nullptr, 3, 1); }));
+        }
+
         // several lanes (here: three contexts on the one GPU): replicated working set, sharded pair list,
         // partial centering sums exchanged on the host — the same records in the same order
         const int devs[3] = {0, 0, 0};

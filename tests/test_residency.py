@@ -220,6 +220,18 @@ def write_dataset(tmp_path, sizes, seed):
     return desc, paths
 
 
+def fresh(matcher, family):
+    """Drops what earlier GPU test modules left resident on the shared context and installs `family`."""
+    for img in list(getattr(matcher, "_test_ids", set())):
+        try:
+            matcher.evict(img)
+        except KeyError:
+            pass
+    matcher._test_ids = set()
+    matcher.set_family(family)
+    matcher.set_sub_batch_queries(0)
+
+
 def resident_reference(matcher, desc, pairs, cfg, centering, base_id=70000):
     """The same pairs on the ordinary resident path (parity-tested against the oracle in test_gpu_parity.py)."""
     ids = [base_id + i for i in range(len(desc))]
@@ -244,7 +256,7 @@ def test_streamed_run_equals_resident_run(matcher, restatement, tmp_path, monkey
     desc, paths = write_dataset(tmp_path, sizes, seed=41)
     k, np_, m = len(sizes), 3, 2
     fam = ch.build_hash_family(ch.FamilyParams())
-    matcher.set_family(fam)
+    fresh(matcher, fam)
     cfg = ch.MatchConfig()
     want_centering = restatement.centering(desc)
     centering, results = matcher.centering_pass_files(paths, block_images=4, io_threads=3)
@@ -296,7 +308,7 @@ def test_streamed_run_more_slots_and_failed_files(matcher, tmp_path):
     paths[5].write_bytes(good[: 16 + 144 * 100 + 7])  # truncated payload
     paths[9] = tmp_path / "missing.chft"
     fam = ch.build_hash_family(ch.FamilyParams())
-    matcher.set_family(fam)
+    fresh(matcher, fam)
     cfg = ch.MatchConfig()
     centering, results = matcher.centering_pass_files(paths, block_images=5, io_threads=2)
     assert isinstance(results[5], ch.FeatureFileError) and results[5].fault == "Truncated"
@@ -333,7 +345,7 @@ def test_background_load_under_match_calls(matcher, tmp_path):
     desc, paths = write_dataset(tmp_path, sizes, seed=47)
     paths[4] = tmp_path / "absent.chft"
     fam = ch.build_hash_family(ch.FamilyParams())
-    matcher.set_family(fam)
+    fresh(matcher, fam)
     cfg = ch.MatchConfig()
     first, rest = list(range(0, 6)), list(range(6, len(sizes)))
     ids = [81000 + i for i in range(len(sizes))]
