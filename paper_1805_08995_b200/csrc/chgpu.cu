@@ -214,6 +214,11 @@ struct chgpu_ctx {
     chgpu_load_job* load_job = nullptr;  // background load opened by chgpu_load_chft_files_begin
     char* load_region = nullptr;         // its device staging, one allocation cut into slices
     size_t load_region_bytes = 0;
+    SplitJob* h_split_jobs = nullptr;    // pinned / device list for the batched split of a background load
+    SplitJob* d_split_jobs = nullptr;
+    size_t split_jobs_cap = 0;
+    cudaEvent_t ev_split_jobs = nullptr;
+    bool split_jobs_busy = false;
 };
 
 namespace {
@@ -1087,6 +1092,7 @@ chgpu_status chgpu_create(int device, chgpu_ctx** out) {
     ok &= cudaStreamCreateWithFlags(&ctx->compute, cudaStreamNonBlocking) == cudaSuccess;
     ok &= cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) == cudaSuccess;
     ok &= cudaStreamCreateWithFlags(&ctx->load, cudaStreamNonBlocking) == cudaSuccess;
+    ok &= cudaEventCreateWithFlags(&ctx->ev_split_jobs, cudaEventDisableTiming) == cudaSuccess;
     ok &= cudaEventCreateWithFlags(&ctx->ev_upload, cudaEventDisableTiming) == cudaSuccess;
     ok &= cudaEventCreateWithFlags(&ctx->ev_compute, cudaEventDisableTiming) == cudaSuccess;
     ok &= cudaEventCreate(&ctx->ev_t0) == cudaSuccess;
@@ -1135,6 +1141,9 @@ void chgpu_destroy(chgpu_ctx* ctx) {
     cudaFree(ctx->d_dbg); cudaFree(ctx->d_gmin); cudaFree(ctx->d_gdone); cudaFree(ctx->d_lists); cudaFree(ctx->d_act); cudaFree(ctx->d_nact);
     cudaFreeHost(ctx->load_pinned);
     cudaFree(ctx->load_region);
+    cudaFreeHost(ctx->h_split_jobs);
+    cudaFree(ctx->d_split_jobs);
+    if (ctx->ev_split_jobs) cudaEventDestroy(ctx->ev_split_jobs);
     for (auto& b : ctx->load_scratch) cudaFree(b.first);
     cudaFree(ctx->d_planes_t); cudaFree(ctx->d_bias); cudaFree(ctx->d_hnorm); cudaFree(ctx->d_hq);
     cudaFree(ctx->d_hq_count); cudaFree(ctx->d_hstats);
@@ -1249,7 +1258,7 @@ chgpu_status chgpu_centering_reset(chgpu_ctx* ctx) {
 chgpu_status chgpu_centering_add_image(chgpu_ctx* ctx, uint32_t image_id) {
     if (!ctx) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
-    uint32_t slot;
+    uint32_t slot = 0;
     if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
     const DevImage& d = ctx->images[slot].dev;
     if (d.n == 0) return CHGPU_OK;
@@ -1332,7 +1341,7 @@ chgpu_status chgpu_upload_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, c
                                 const float* keypoints) {
     if (!ctx || (n && !desc)) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
-    uint32_t slot;
+    uint32_t slot = 0;
     if (const chgpu_status s = alloc_image(ctx, image_id, n, &slot)) return s;
     if (const chgpu_status s = order_copy_after_compute(ctx)) return s;
     ImageRec& r = ctx->images[slot];
@@ -1355,7 +1364,7 @@ chgpu_status chgpu_upload_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint
     const bool pinned = n == 0 || (is_pinned(desc) && (!keypoints || is_pinned(keypoints)));
     uint32_t lo = UINT32_MAX, hi = 0;
     for (uint32_t i = 0; i < count; ++i) {
-        uint32_t slot;
+        uint32_t slot = 0;
         if (const chgpu_status s = alloc_image(ctx, image_ids[i], n, &slot)) return s;
         ImageRec& r = ctx->images[slot];
         const uint8_t* d = desc + size_t(i) * n * kDim;
@@ -1402,7 +1411,7 @@ chgpu_status chgpu_upload_chft(chgpu_ctx* ctx, uint32_t image_id, const void* bl
     if (nbytes < expected) return bad(CHGPU_FAULT_TRUNCATED, nbytes, "truncated payload");
     if (count_out) *count_out = count;
 
-    uint32_t slot;
+    uint32_t slot = 0;
     if (const chgpu_status s = alloc_image(ctx, image_id, count, &slot)) return s;
     ImageRec& r = ctx->images[slot];
     if (count) {
@@ -1550,6 +1559,7 @@ struct chgpu_load_job {
     std::vector<Scratch> scratch;  // device-side raw (AoS) ring
     bool region_mode = false;
     cudaEvent_t last_copied = nullptr;  // region mode: event of the latest H2D copy
+    cudaEvent_t ev_flush = nullptr;     // region mode: recorded behind the latest batched split
     std::vector<std::thread> readers;
     std::deque<uint32_t> in_flight;  // files whose H2D was issued, oldest first (copies complete in this order)
     uint32_t next = 0;               // next file the issue side handles
@@ -1658,7 +1668,10 @@ chgpu_status load_start(chgpu_ctx* ctx, const char* const* paths, const uint32_t
             job->scratch[k].own = false;
         }
     }
-    for (size_t k = 0; k < nscratch; ++k) cudaEventCreateWithFlags(&job->scratch[k].split_done, cudaEventDisableTiming);
+    // (region mode: one event behind each batched split covers every buffer it consumed)
+    if (job->region_mode) cudaEventCreateWithFlags(&job->ev_flush, cudaEventDisableTiming);
+    else
+        for (size_t k = 0; k < nscratch; ++k) cudaEventCreateWithFlags(&job->scratch[k].split_done, cudaEventDisableTiming);
     job->wall0 = std::chrono::steady_clock::now();
     for (uint32_t t = 0; t < io_threads; ++t) job->readers.emplace_back(loader_thread, &job->ring, job->paths.data(), count);
     *out = job.release();
@@ -1679,7 +1692,7 @@ void load_launch_split(chgpu_load_job* job, chgpu_load_job::Scratch& sc) {
         chft_split_kernel<<<blocks, 256, 0, ctx->compute>>>(reinterpret_cast<const uint4*>(sc.ptr), n,
                                                            reinterpret_cast<uint4*>(sc.dst_desc), reinterpret_cast<uint4*>(sc.dst_kp));
     }
-    cudaEventRecord(sc.split_done, ctx->compute);
+    cudaEventRecord(job->region_mode ? job->ev_flush : sc.split_done, ctx->compute);
     sc.used = true;
     sc.split_pending = false;
 }
@@ -1689,9 +1702,57 @@ void load_flush_splits(chgpu_load_job* job) {
     bool any = false;
     for (auto& sc : job->scratch) any = any || sc.split_pending;
     if (!any) return;
-    if (job->last_copied) cudaStreamWaitEvent(job->ctx->compute, job->last_copied, 0);  // copies complete in issue order
+    chgpu_ctx* ctx = job->ctx;
+    if (job->last_copied) cudaStreamWaitEvent(ctx->compute, job->last_copied, 0);  // copies complete in issue order
+    if (job->sums) {  // (the fused split + sums kernel stays one launch per file)
+        for (auto& sc : job->scratch)
+            if (sc.split_pending) load_launch_split(job, sc);
+        return;
+    }
+    // one launch for all of them: the job list travels through a pinned array kept by the context
+    size_t np = 0;
+    for (auto& sc : job->scratch) np += sc.split_pending ? 1 : 0;
+    if (ctx->split_jobs_cap < np) {
+        cudaStreamSynchronize(ctx->compute);
+        cudaFreeHost(ctx->h_split_jobs);
+        cudaFree(ctx->d_split_jobs);
+        ctx->h_split_jobs = nullptr;
+        ctx->d_split_jobs = nullptr;
+        ctx->split_jobs_cap = 0;
+        const size_t cap = std::max<size_t>(np, 1024);
+        if (cudaMallocHost(reinterpret_cast<void**>(&ctx->h_split_jobs), cap * sizeof(SplitJob)) != cudaSuccess ||
+            cudaMalloc(reinterpret_cast<void**>(&ctx->d_split_jobs), cap * sizeof(SplitJob)) != cudaSuccess) {
+            cudaGetLastError();
+            for (auto& sc : job->scratch)  // no room for the list: one launch per file
+                if (sc.split_pending) load_launch_split(job, sc);
+            return;
+        }
+        ctx->split_jobs_cap = cap;
+    } else if (ctx->split_jobs_busy) {
+        cudaEventSynchronize(ctx->ev_split_jobs);  // the previous list has been read
+    }
+    uint32_t max_n = 0;
+    size_t k = 0;
     for (auto& sc : job->scratch)
-        if (sc.split_pending) load_launch_split(job, sc);
+        if (sc.split_pending) {
+            ctx->h_split_jobs[k++] = SplitJob{reinterpret_cast<const uint4*>(sc.ptr), reinterpret_cast<uint4*>(sc.dst_desc),
+                                              reinterpret_cast<uint4*>(sc.dst_kp), sc.n, 0u};
+            max_n = std::max(max_n, sc.n);
+        }
+    cudaMemcpyAsync(ctx->d_split_jobs, ctx->h_split_jobs, np * sizeof(SplitJob), cudaMemcpyHostToDevice, ctx->compute);
+    cudaEventRecord(ctx->ev_split_jobs, ctx->compute);
+    ctx->split_jobs_busy = true;
+    const uint32_t bx = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>((uint64_t(max_n) * 9 + 255) / 256, 32)));
+    for (size_t first = 0; first < np; first += 65535) {  // gridDim.y limit
+        const uint32_t cnt = uint32_t(std::min<size_t>(65535, np - first));
+        chft_split_batch_kernel<<<dim3(bx, cnt), 256, 0, ctx->compute>>>(ctx->d_split_jobs + first);
+    }
+    cudaEventRecord(job->ev_flush, ctx->compute);
+    for (auto& sc : job->scratch)
+        if (sc.split_pending) {
+            sc.used = true;
+            sc.split_pending = false;
+        }
 }
 
 // Sends files to the device in list order.  block: until every file has been handled; otherwise until the next file
@@ -1723,8 +1784,9 @@ void load_pump(chgpu_load_job* job, bool block) {
         }
         if (sc.used) {  // its previous split kernel has to have consumed it
             if (sc.split_pending) load_flush_splits(job);  // (a job with more files than staging buffers)
-            if (block) cudaEventSynchronize(sc.split_done);
-            else if (cudaEventQuery(sc.split_done) != cudaSuccess) {
+            cudaEvent_t consumed = job->region_mode ? job->ev_flush : sc.split_done;
+            if (block) cudaEventSynchronize(consumed);
+            else if (cudaEventQuery(consumed) != cudaSuccess) {
                 cudaGetLastError();
                 return;
             }
@@ -1828,11 +1890,15 @@ chgpu_status load_finish(chgpu_load_job* job, chgpu_file_result* results, chgpu_
     chgpu_ctx* ctx = job->ctx;
     LoadRing& ring = job->ring;
     const size_t S = job->S;
+    const uint32_t left = job->count - job->next;
+    const auto tf0 = std::chrono::steady_clock::now();
     load_pump(job, true);
     load_flush_splits(job);
     if (getenv("CHGPU_LOADER_TRACE") != nullptr)
-        fprintf(stderr, "chgpu loader: %u files, issue thread waited %.3f s for readers, %.3f s in alloc_image, %.3f s issuing\n",
-                job->count, job->t_wait, job->t_alloc, job->t_issue);
+        fprintf(stderr, "chgpu loader: %u files (%u left for the final pump, %.3f s), issue thread waited %.3f s for readers, "
+                "%.3f s in alloc_image, %.3f s issuing, %.3f s since start\n",
+                job->count, left, std::chrono::duration<double>(std::chrono::steady_clock::now() - tf0).count(), job->t_wait,
+                job->t_alloc, job->t_issue, std::chrono::duration<double>(std::chrono::steady_clock::now() - job->wall0).count());
     if (job->rc != CHGPU_OK) ring.abort.store(true);
     if (job->pub_lo <= job->pub_hi)
         cudaMemcpyAsync(ctx->d_images + job->pub_lo, ctx->h_images + job->pub_lo,
@@ -1855,8 +1921,9 @@ chgpu_status load_finish(chgpu_load_job* job, chgpu_file_result* results, chgpu_
     for (size_t k = 0; k < job->scratch.size(); ++k) {
         if (!job->region_mode) ctx->load_scratch[k] = {job->scratch[k].ptr, job->scratch[k].cap};
         else if (job->scratch[k].outgrown) cudaFree(job->scratch[k].ptr);
-        cudaEventDestroy(job->scratch[k].split_done);
+        if (job->scratch[k].split_done) cudaEventDestroy(job->scratch[k].split_done);
     }
+    if (job->ev_flush) cudaEventDestroy(job->ev_flush);
     chgpu_load_stats st = job->st;
     st.bytes_read = ring.bytes_read;
     st.read_seconds = ring.read_seconds;
@@ -1926,7 +1993,7 @@ chgpu_status chgpu_load_chft_files_end(chgpu_ctx* ctx, chgpu_file_result* result
 chgpu_status chgpu_evict_image(chgpu_ctx* ctx, uint32_t image_id) {
     if (!ctx) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
-    uint32_t slot;
+    uint32_t slot = 0;
     if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
     CK(cudaStreamSynchronize(ctx->copy));
     CK(cudaStreamSynchronize(ctx->compute));
@@ -1945,7 +2012,7 @@ chgpu_status chgpu_evict_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint3
     CK(cudaStreamSynchronize(ctx->compute));
     chgpu_status rc = CHGPU_OK;
     for (uint32_t i = 0; i < count; ++i) {
-        uint32_t slot;
+        uint32_t slot = 0;
         if (find_slot(ctx, image_ids[i], &slot) != CHGPU_OK) {
             rc = CHGPU_ENOTFOUND;  // reported after the rest of the list has been released
             continue;
@@ -1959,7 +2026,7 @@ chgpu_status chgpu_evict_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint3
 
 chgpu_status chgpu_image_points(chgpu_ctx* ctx, uint32_t image_id, uint32_t* n) {
     if (!ctx || !n) return CHGPU_EINVAL;
-    uint32_t slot;
+    uint32_t slot = 0;
     if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
     *n = ctx->images[slot].dev.n;
     return CHGPU_OK;
@@ -1968,7 +2035,7 @@ chgpu_status chgpu_image_points(chgpu_ctx* ctx, uint32_t image_id, uint32_t* n) 
 chgpu_status chgpu_download_descriptors(chgpu_ctx* ctx, uint32_t image_id, uint8_t* desc, float* keypoints) {
     if (!ctx) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
-    uint32_t slot;
+    uint32_t slot = 0;
     if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
     if (const chgpu_status s = chgpu_sync(ctx)) return s;
     const DevImage& d = ctx->images[slot].dev;
@@ -2027,7 +2094,7 @@ chgpu_status chgpu_hash_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32
 chgpu_status chgpu_download_codes(chgpu_ctx* ctx, uint32_t image_id, uint32_t* shorts, uint64_t* longs) {
     if (!ctx) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
-    uint32_t slot;
+    uint32_t slot = 0;
     if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
     const DevImage& d = ctx->images[slot].dev;
     if (!(d.flags & 1u)) return fail(ctx, CHGPU_ELOGIC, "image %u: codes not computed", image_id);
@@ -2041,7 +2108,7 @@ chgpu_status chgpu_download_codes(chgpu_ctx* ctx, uint32_t image_id, uint32_t* s
 chgpu_status chgpu_upload_codes(chgpu_ctx* ctx, uint32_t image_id, const uint32_t* shorts, const uint64_t* longs) {
     if (!ctx || !shorts || !longs) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
-    uint32_t slot;
+    uint32_t slot = 0;
     if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
     ImageRec& r = ctx->images[slot];
     const uint32_t n = r.dev.n, L = ctx->fam.table_count, m = ctx->fam.short_bits;
@@ -2067,7 +2134,7 @@ chgpu_status chgpu_upload_codes(chgpu_ctx* ctx, uint32_t image_id, const uint32_
 chgpu_status chgpu_download_bucket_index(chgpu_ctx* ctx, uint32_t image_id, uint32_t* offsets, uint32_t* points) {
     if (!ctx) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
-    uint32_t slot;
+    uint32_t slot = 0;
     if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
     const DevImage& d = ctx->images[slot].dev;
     if (!(d.flags & 1u)) return fail(ctx, CHGPU_ELOGIC, "image %u: codes not computed", image_id);
@@ -2087,7 +2154,7 @@ chgpu_status chgpu_download_bucket_index(chgpu_ctx* ctx, uint32_t image_id, uint
 chgpu_status chgpu_image_save_code_cache(chgpu_ctx* ctx, uint32_t image_id, const char* path) {
     if (!ctx || !path) return CHGPU_EINVAL;
     if (!ctx->has_centering) return fail(ctx, CHGPU_ELOGIC, "code cache: centering has not been set");
-    uint32_t slot;
+    uint32_t slot = 0;
     if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
     const uint32_t n = ctx->images[slot].dev.n;
     std::vector<uint32_t> shorts(size_t(n) * ctx->fam.table_count);
@@ -2103,7 +2170,7 @@ chgpu_status chgpu_image_load_code_cache(chgpu_ctx* ctx, uint32_t image_id, cons
                                          uint64_t* fault_offset) {
     if (!ctx || !path) return CHGPU_EINVAL;
     if (!ctx->has_centering) return fail(ctx, CHGPU_ELOGIC, "code cache: centering has not been set");
-    uint32_t slot;
+    uint32_t slot = 0;
     if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
     const uint32_t n = ctx->images[slot].dev.n;
     std::vector<uint32_t> shorts(std::max<size_t>(1, size_t(n) * ctx->fam.table_count));

@@ -24,6 +24,26 @@ __global__ void chft_split_kernel(const uint4* __restrict__ records, uint32_t n,
     }
 }
 
+// The same split over a list of blobs in one launch (background loads split a whole block at once):
+// blockIdx.y = file, blockIdx.x strides over its 16-byte chunks.
+struct SplitJob {
+    const uint4* records;
+    uint4* desc;
+    uint4* kp;
+    uint32_t n;
+    uint32_t pad;
+};
+__global__ void chft_split_batch_kernel(const SplitJob* __restrict__ jobs) {
+    const SplitJob j = jobs[blockIdx.y];
+    const uint64_t total = uint64_t(j.n) * 9;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t p = uint32_t(i / 9), c = uint32_t(i % 9);
+        const uint4 v = __ldg(j.records + i);
+        if (c == 0) j.kp[p] = v;
+        else j.desc[uint64_t(p) * 8 + (c - 1)] = v;
+    }
+}
+
 // K0 fused with the centering sums (the streaming loader's per-file kernel): blocks of 288 threads = 32 records
 // x 9 chunks, so a thread keeps its chunk position while it strides over the records and can hold the 16 column
 // sums of its descriptor chunk in registers; one shared-memory and one global (u64) atomic pass per block.

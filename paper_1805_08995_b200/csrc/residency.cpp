@@ -519,18 +519,32 @@ chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths,
         if (act.kind == CHGPU_ACT_LOAD) {
             if (act.level == CHGPU_LEVEL_GROUP) rp.group_hint(act.id, true);
             else if (overlap && act.prefetch) pending.push_back(act.id);  // for a later task: behind the next match call
-            else rc = rp.load_block(act.id);
+            else {
+                rc = rp.end_background();  // (one load at a time per context)
+                if (rc == CHGPU_OK) rc = rp.load_block(act.id);
+            }
         } else if (act.kind == CHGPU_ACT_EVICT) {
             if (act.level == CHGPU_LEVEL_GROUP) rp.group_hint(act.id, false);
             else if (std::find(pending.begin(), pending.end(), act.id) != pending.end()) {
                 pending.erase(std::find(pending.begin(), pending.end(), act.id));  // evicted before it was ever loaded
-            } else rp.evict_block(act.id, true);
+            } else {
+                if (std::find(rp.background.begin(), rp.background.end(), act.id) != rp.background.end()) rc = rp.end_background();
+                rp.evict_block(act.id, true);
+            }
         } else if (act.kind == CHGPU_ACT_BEGIN) {
             const chgpu_plan_task& t = tasks[act.id];
             ++rp.st.tasks;
             // Line 2 of the exchange: the prefetches the schedule issued since the last task (their evictions are done, their
             // loads were held back) are opened as one background load that this task's match call moves forward; the
             // reference's loader thread does the same while its workers run the task (engine.cpp:414-442, :679-696).
+            // The open load stays open across tasks that do not need its blocks (a short task hides little; the next
+            // long one hides the rest) and is completed when a task needs one of them or the next load has to start.
+            const bool needs_open = std::find(rp.background.begin(), rp.background.end(), t.block_a) != rp.background.end() ||
+                                    std::find(rp.background.begin(), rp.background.end(), t.block_b) != rp.background.end();
+            if (needs_open || !pending.empty()) {
+                rc = rp.end_background();
+                if (rc != CHGPU_OK) break;
+            }
             if (!pending.empty()) {
                 rc = rp.begin_background(pending);
                 pending.clear();
@@ -578,11 +592,11 @@ chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths,
             }
             if (rc == CHGPU_OK) flush(true);
             rp.st.pairs_skipped += skipped;
-            {
-                const chgpu_status e = rp.end_background();
-                if (rc == CHGPU_OK) rc = e;
-            }
         }
+    }
+    {
+        const chgpu_status e = rp.end_background();
+        if (rc == CHGPU_OK) rc = e;
     }
     chgpu_load_chft_files_end(ctx, nullptr, nullptr);  // an error path may have left the background load open
     if (rc == CHGPU_OK && m.blocked) rc = CHGPU_EINVAL;  // slot limits below what one task needs

@@ -6,3 +6,6 @@ for tool in memcheck racecheck synccheck; do
   echo "== $tool"
   timeout 1500 compute-sanitizer --tool $tool --print-limit 5 python -m pytest $FILES -m gpu -x -q -k "$SEL" 2>&1 | grep -E "COMPUTE-SANITIZER|passed|failed|SUMMARY|Error|hazard" | head -20
 done
+# round r01n: residency replay, background loads (deferred splits on the load stream), batch eviction
+echo "== memcheck (residency / background loads)"
+timeout 1500 compute-sanitizer --tool memcheck --print-limit 5 python -m pytest tests/test_residency.py tests/test_loader.py -m gpu -x -q 2>&1 | grep -E "COMPUTE-SANITIZER|passed|failed|SUMMARY|Error" | head -20
