@@ -382,10 +382,20 @@ def run_ours(args):
     # (4 per raw candidate, 16 lanes/clk/SM on the XU pipe); DESIGN.md section 4
     props = m.device_props()
     sm_mhz = clocks.get("sm_mhz") or 1965.0
-    popc_peak = props["sm_count"] * 16 * sm_mhz * 1e6
+    # measured peaks of this pool's B200 (scripts/onchip_probe.cu -> profiles/onchip_peaks.json): POPC 15.9 /clk/SM,
+    # integer ALU pipe 2 warp instructions /clk/SM (half rate), LDS.128 1.9 wavefronts /clk/SM
+    probe = None
+    try:
+        probe = json.loads((ROOT / "profiles" / "onchip_peaks.json").read_text())
+    except (OSError, ValueError):
+        pass
+    popc_per_clk = probe["popc_per_clk_per_sm_at_max_clock"] if probe else 16.0
+    popc_peak = props["sm_count"] * popc_per_clk * sm_mhz * 1e6
     popc_rate = 4.0 * last["raw_candidates"] / (kern_ms_per_step * 1e-3)
     roofline["on_chip"] = {"bound": "xu_popc", "achieved_gpopc_s": popc_rate / 1e9, "peak_gpopc_s": popc_peak / 1e9,
                            "frac": popc_rate / popc_peak,
+                           "peak_source": "measured (profiles/onchip_peaks.json)" if probe else "16 lanes/clk/SM (assumed)",
+                           "measured_peaks": probe,
                            "note": "lower bound on POPC work (padding lanes not counted); ncu pipe utilisations of the "
                                    "committed capture (profiles/r*_match_kernel_ncu_full.json, latest)"}
 
