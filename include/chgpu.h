@@ -416,9 +416,18 @@ typedef struct chgpu_streamed_stats {
     double load_seconds, hash_seconds, match_seconds, wall_seconds;
     double evict_seconds, hint_seconds; /* block evictions; page-cache hints of the group level */
 } chgpu_streamed_stats;
+/* Task order of a streamed run.  REFERENCE: the plan's own order (scheduler.cpp:99-164).  REUSE: the same tasks in an
+ * order chosen for descriptor reuse in HBM — always the pending task that needs the fewest block loads given what
+ * is resident (ties: plan order), evicting the block with the fewest tasks left.  The reference's traversal is
+ * built for all-pairs plans; on a banded pair list (k nearest neighbours) it comes back to blocks it has dropped,
+ * and REUSE loads every block once.  Results per pair are the same; only the order of the sink calls changes. */
+typedef enum chgpu_task_order { CHGPU_ORDER_REFERENCE = 0, CHGPU_ORDER_REUSE = 1 } chgpu_task_order;
+/* order_out: ntasks task indices.  Plans of more than 2^18 tasks are returned in plan order. */
+chgpu_status chgpu_order_tasks_for_reuse(const chgpu_plan_task* tasks, uint32_t ntasks, uint32_t block_slots,
+                                         uint32_t* order_out);
 chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths, uint32_t image_count,
                                        uint32_t block_images, uint32_t blocks_per_group,
-                                       uint32_t group_slots, uint32_t block_slots,
+                                       uint32_t group_slots, uint32_t block_slots, chgpu_task_order task_order,
                                        const uint32_t* accepted /* nullable: exhaustive */, uint64_t accepted_count,
                                        const chgpu_match_cfg* cfg, uint32_t io_threads, chgpu_plan_sink_fn sink /* nullable */,
                                        void* user, chgpu_file_result* file_results /* nullable */,

@@ -319,6 +319,21 @@ def simulate_residency(tasks: np.ndarray, mode: int = MATCHING, group_slots: int
     return acts
 
 
+ORDER_REFERENCE, ORDER_REUSE = range(2)  # chgpu_task_order
+
+
+def order_tasks_for_reuse(tasks: np.ndarray, block_slots: int = 3) -> np.ndarray:
+    """Task indices in the order chgpu_match_plan_streamed(task_order=ORDER_REUSE) executes them."""
+    t = np.ascontiguousarray(tasks, dtype=TASK_DTYPE)
+    out = np.zeros(len(t), dtype=np.uint32)
+    if len(t):
+        st = N.load().chgpu_order_tasks_for_reuse(t.ctypes.data_as(C.POINTER(N.PlanTaskC)), len(t), block_slots,
+                                                  out.ctypes.data_as(N.u32p))
+        if st != N.OK:
+            _raise(st, "order_tasks_for_reuse")
+    return out
+
+
 def auto_partition_sizing(mean_image_bytes: int, memory_budget_bytes: int) -> tuple[int, int]:
     """auto_partition_sizing (scheduler.hpp:134): (block_images, blocks_per_group)."""
     a, b = C.c_uint32(0), C.c_uint32(0)
@@ -524,9 +539,11 @@ class Matcher:
         return out, results
 
     def match_plan_streamed(self, paths, block_images: int, blocks_per_group: int, cfg: MatchConfig = MatchConfig(),
-                            accepted_pairs=None, group_slots: int = 0, block_slots: int = 0, io_threads: int = 8, sink=None):
+                            accepted_pairs=None, group_slots: int = 0, block_slots: int = 0, io_threads: int = 8, sink=None,
+                            task_order: int = 0):
         """Out-of-core run of the exhaustive (accepted_pairs None) or guided plan over CHFT files
-        (chgpu_match_plan_streamed).  sink(task, pairs (k,2) u32, offsets (k+1) u64, records) is called in plan order.
+        (chgpu_match_plan_streamed).  sink(task, pairs (k,2) u32, offsets (k+1) u64, records) is called in execution order
+        (plan order, or the reuse order with task_order=ORDER_REUSE; `task` is always the plan's task index).
         Returns (stats dict, per-file results)."""
         n = len(paths)
         arr = (C.c_char_p * max(n, 1))(*[str(p).encode() for p in paths])
@@ -556,7 +573,7 @@ class Matcher:
                 return 1
 
         cb = N.PLAN_SINK_FN(_cb)
-        st = self.lib.chgpu_match_plan_streamed(self.h, arr, n, block_images, blocks_per_group, group_slots, block_slots,
+        st = self.lib.chgpu_match_plan_streamed(self.h, arr, n, block_images, blocks_per_group, group_slots, block_slots, task_order,
                                                 None if acc is None else keep.ctypes.data, 0 if acc is None else len(acc),
                                                 C.byref(c), io_threads, cb, None, res, C.byref(stats))
         if err:

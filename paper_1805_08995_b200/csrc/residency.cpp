@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -240,6 +241,79 @@ struct Machine {
     }
 };
 
+// Greedy order for reuse: always the pending task that needs the fewest block loads given what is resident (ties:
+// plan order); a block that has to go is the resident one with the fewest tasks left.
+void order_for_reuse(const chgpu_plan_task* tasks, uint32_t n, uint32_t slots, std::vector<uint32_t>& order) {
+    order.clear();
+    order.reserve(n);
+    if (n > (1u << 18) || slots < 2) {
+        for (uint32_t t = 0; t < n; ++t) order.push_back(t);
+        return;
+    }
+    uint32_t nblocks = 0;
+    for (uint32_t t = 0; t < n; ++t) nblocks = std::max(nblocks, std::max(tasks[t].block_a, tasks[t].block_b) + 1);
+    std::vector<std::vector<uint32_t>> of_block(nblocks);  // ascending task indices
+    std::vector<uint32_t> left(nblocks, 0), head(nblocks, 0);
+    for (uint32_t t = 0; t < n; ++t) {
+        of_block[tasks[t].block_a].push_back(t);
+        ++left[tasks[t].block_a];
+        if (tasks[t].block_b != tasks[t].block_a) {
+            of_block[tasks[t].block_b].push_back(t);
+            ++left[tasks[t].block_b];
+        }
+    }
+    std::vector<uint8_t> done(n, 0), is_res(nblocks, 0);
+    std::vector<uint32_t> resident;
+    uint32_t first_pending = 0;
+    auto missing = [&](uint32_t t) { return (is_res[tasks[t].block_a] ? 0 : 1) + (tasks[t].block_b != tasks[t].block_a && !is_res[tasks[t].block_b] ? 1 : 0); };
+    for (uint32_t step = 0; step < n; ++step) {
+        // best pending task among those touching a resident block; else the first pending task of the plan
+        uint32_t best = kNever, best_missing = 3;
+        for (const uint32_t r : resident) {
+            auto& list = of_block[r];
+            while (head[r] < list.size() && done[list[head[r]]]) ++head[r];
+            for (uint32_t k = head[r]; k < list.size(); ++k) {
+                const uint32_t t = list[k];
+                if (done[t]) continue;
+                const uint32_t ms = missing(t);
+                if (ms < best_missing || (ms == best_missing && t < best)) {
+                    best = t;
+                    best_missing = ms;
+                }
+                if (ms == 0) break;  // lists ascend: the first fully resident task of this block is its best
+            }
+        }
+        if (best == kNever) {
+            while (done[first_pending]) ++first_pending;
+            best = first_pending;
+        }
+        const uint32_t need[2] = {tasks[best].block_a, tasks[best].block_b};
+        for (const uint32_t b : need) {
+            if (is_res[b]) continue;
+            if (resident.size() >= slots) {
+                uint32_t victim = kNever, fewest = kNever;
+                for (const uint32_t r : resident) {
+                    if (r == need[0] || r == need[1]) continue;
+                    if (left[r] < fewest || (left[r] == fewest && r < victim)) {
+                        victim = r;
+                        fewest = left[r];
+                    }
+                }
+                if (victim != kNever) {
+                    resident.erase(std::find(resident.begin(), resident.end(), victim));
+                    is_res[victim] = 0;
+                }
+            }
+            resident.push_back(b);
+            is_res[b] = 1;
+        }
+        done[best] = 1;
+        --left[need[0]];
+        if (need[1] != need[0]) --left[need[1]];
+        order.push_back(best);
+    }
+}
+
 uint32_t default_limit(chgpu_residency_mode mode) { return mode == CHGPU_RESIDENCY_HASHING ? 2u : 3u; }
 
 double seconds_since(std::chrono::steady_clock::time_point t0) {
@@ -364,11 +438,17 @@ struct Replay {
         }
     }
 
+    // Group level of the exchange: the page cache.  The hints are pure host work (open / posix_fadvise / close per
+    // file), so they run on a helper thread; hint_seconds counts only what the replay had to wait for.
+    std::vector<std::thread> hint_threads;
     void group_hint(uint32_t g, bool load) {
         const auto t0 = std::chrono::steady_clock::now();
         const uint32_t b0 = g * part.blocks_per_group, b1 = std::min(part.nblocks, b0 + part.blocks_per_group);
-        for (uint32_t i = part.lo(b0); i < part.hi(b1 - 1); ++i)
-            advise_file(paths[i], load ? POSIX_FADV_WILLNEED : POSIX_FADV_DONTNEED);
+        const uint32_t lo = part.lo(b0), hi = part.hi(b1 - 1);
+        const char* const* ps = paths;
+        hint_threads.emplace_back([ps, lo, hi, load] {
+            for (uint32_t i = lo; i < hi; ++i) advise_file(ps[i], load ? POSIX_FADV_WILLNEED : POSIX_FADV_DONTNEED);
+        });
         if (load) {
             ++st.group_loads;
             st.max_resident_groups = std::max(st.max_resident_groups, ++resident_groups);
@@ -376,6 +456,12 @@ struct Replay {
             ++st.group_evictions;
             --resident_groups;
         }
+        st.hint_seconds += seconds_since(t0);
+    }
+    void join_hints() {
+        const auto t0 = std::chrono::steady_clock::now();
+        for (std::thread& t : hint_threads) t.join();
+        hint_threads.clear();
         st.hint_seconds += seconds_since(t0);
     }
 
@@ -459,6 +545,15 @@ chgpu_status chgpu_simulate_residency(const chgpu_plan_task* tasks, uint32_t nta
     return CHGPU_OK;
 }
 
+chgpu_status chgpu_order_tasks_for_reuse(const chgpu_plan_task* tasks, uint32_t ntasks, uint32_t block_slots,
+                                         uint32_t* order_out) {
+    if ((ntasks && (!tasks || !order_out))) return CHGPU_EINVAL;
+    std::vector<uint32_t> order;
+    order_for_reuse(tasks, ntasks, block_slots ? block_slots : 3u, order);
+    std::copy(order.begin(), order.end(), order_out);
+    return CHGPU_OK;
+}
+
 void chgpu_auto_partition_sizing(uint64_t mean_image_bytes, uint64_t memory_budget_bytes, uint32_t* block_images,
                                  uint32_t* blocks_per_group) {
     const uint64_t per_image = std::max<uint64_t>(1, mean_image_bytes);
@@ -482,8 +577,9 @@ void chgpu_partition_sizing_for_device(uint64_t device_image_bytes, uint64_t fil
 
 chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths, uint32_t image_count,
                                        uint32_t block_images, uint32_t blocks_per_group, uint32_t group_slots,
-                                       uint32_t block_slots, const uint32_t* accepted, uint64_t accepted_count,
-                                       const chgpu_match_cfg* cfg, uint32_t io_threads, chgpu_plan_sink_fn sink, void* user,
+                                       uint32_t block_slots, chgpu_task_order task_order, const uint32_t* accepted,
+                                       uint64_t accepted_count, const chgpu_match_cfg* cfg, uint32_t io_threads,
+                                       chgpu_plan_sink_fn sink, void* user,
                                        chgpu_file_result* file_results, chgpu_streamed_stats* stats) {
     if (!ctx || !paths || !cfg || image_count == 0 || block_images == 0 || blocks_per_group == 0) return CHGPU_EINVAL;
     if (accepted_count && !accepted) return CHGPU_EINVAL;
@@ -505,6 +601,17 @@ chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths,
         if (const chgpu_status s = key_accepted(p, accepted, accepted_count, keyed)) return s;
     std::vector<chgpu_plan_task> tasks;
     build_tasks(p, guided ? &keyed : nullptr, tasks);
+    // plan index of every task of the run, in the order it is executed
+    std::vector<uint32_t> plan_index(tasks.size());
+    for (uint32_t t = 0; t < tasks.size(); ++t) plan_index[t] = t;
+    if (task_order == CHGPU_ORDER_REUSE) {
+        order_for_reuse(tasks.data(), uint32_t(tasks.size()), block_slots ? block_slots : 3u, plan_index);
+        std::vector<chgpu_plan_task> permuted(tasks.size());
+        for (uint32_t k = 0; k < tasks.size(); ++k) permuted[k] = tasks[plan_index[k]];
+        tasks.swap(permuted);
+    } else if (task_order != CHGPU_ORDER_REFERENCE) {
+        return CHGPU_EINVAL;
+    }
 
     Machine m;
     m.init(tasks.data(), uint32_t(tasks.size()), group_slots ? group_slots : 3u, block_slots ? block_slots : 3u);
@@ -564,7 +671,7 @@ chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths,
             auto flush = [&](bool final) {
                 const uint64_t np = pairs.size() / 2;
                 if (np == 0 || (!final && np < kPairsPerCall)) return;
-                SinkAdapter ad{sink, user, act.id, pairs.data(), 0};
+                SinkAdapter ad{sink, user, plan_index[act.id], pairs.data(), 0};
                 chgpu_match_stats ms{};
                 const auto t0 = std::chrono::steady_clock::now();
                 rc = chgpu_match_pairs_stream(ctx, pairs.data(), uint32_t(np), cfg, sink_adapter, &ad, &ms);
@@ -601,6 +708,7 @@ chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths,
     chgpu_load_chft_files_end(ctx, nullptr, nullptr);  // an error path may have left the background load open
     if (rc == CHGPU_OK && m.blocked) rc = CHGPU_EINVAL;  // slot limits below what one task needs
     rp.evict_all();
+    rp.join_hints();
     rp.st.wall_seconds = seconds_since(wall0);
     if (file_results) std::copy(rp.results.begin(), rp.results.end(), file_results);
     if (stats) *stats = rp.st;
@@ -635,6 +743,7 @@ chgpu_status chgpu_centering_pass_files(chgpu_ctx* ctx, const char* const* paths
         else if (act.kind == CHGPU_ACT_EVICT) rp.evict_block(act.id, true);
     }
     rp.evict_all();
+    rp.join_hints();
     if (file_results) std::copy(rp.results.begin(), rp.results.end(), file_results);
     if (rc != CHGPU_OK) return rc;
     return chgpu_centering_apply(ctx, centering128_out);  // CHGPU_EINVAL when no descriptor was seen (hashing.cpp:60)

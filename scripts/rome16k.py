@@ -36,14 +36,14 @@ def streamed(args, paths, accepted, K, n, write_s):
 
         st, res = m.match_plan_streamed(paths, args.block_images, args.blocks_per_group, ch.MatchConfig(), accepted_pairs=accepted,
                                         group_slots=args.group_slots, block_slots=args.block_slots, io_threads=args.io_threads,
-                                        sink=sink)
+                                        sink=sink, task_order=1 if args.reuse_order else 0)
         t2 = time.perf_counter()
         assert got["records"] == st["matches"] and got["pairs"] == st["pairs"]
         props = m.device_props()
     tasks = ch.plan_tasks(K, args.block_images, args.blocks_per_group, accepted)
     line = {
         "workload": f"BASELINE configs[3] Rome16K-shaped, OUT OF CORE: {K} images x {n} descriptors from CHFT files, (i,i+d) "
-                    f"d=1..{args.neighbors}; blocks of {args.block_images} images, {args.block_slots} block slots",
+                    f"d=1..{args.neighbors}; blocks of {args.block_images} images, {args.block_slots} block slots, " + ("reuse order" if args.reuse_order else "plan order"),
         "images": K, "pairs": int(st["pairs"]), "tasks": len(tasks), "file_bytes": int(K * (16 + 144 * n)),
         "dataset_write_s": write_s,
         "centering_pass": {"seconds": t1 - t0, "GB_per_s": K * (16 + 144 * n) / (t1 - t0) / 1e9},
@@ -73,6 +73,7 @@ def main():
     ap.add_argument("--blocks-per-group", type=int, default=4)
     ap.add_argument("--block-slots", type=int, default=3)
     ap.add_argument("--group-slots", type=int, default=3)
+    ap.add_argument("--reuse-order", action="store_true", help="execute the tasks in the reuse order (CHGPU_ORDER_REUSE)")
     args = ap.parse_args()
     d = Path(args.dir)
     d.mkdir(parents=True, exist_ok=True)

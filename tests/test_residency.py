@@ -377,3 +377,64 @@ def test_background_load_under_match_calls(matcher, tmp_path):
     matcher.evict_many([ids[i] for i in live + rest])
     with pytest.raises(KeyError):
         matcher.points(ids[7])
+
+
+# ---- task order for descriptor reuse (CHGPU_ORDER_REUSE) ---------------------------------------------------------
+def block_loads(tasks, order, slots):
+    trace = api.simulate_residency(tasks[order], api.MATCHING, group_slots=max(slots, 3), block_slots=slots)
+    return int(np.sum((trace["kind"] == api.LOAD) & (trace["level"] == api.BLOCK)))
+
+
+def test_reuse_order_is_a_permutation_and_saves_loads_on_banded_plans():
+    # a k-nearest-neighbour list (the Rome16K-shaped config): pairs (i, i + d), d <= 30, blocks of 64 images
+    k, np_, m = 1024, 64, 4
+    acc = np.array([(i, i + d) for i in range(k) for d in range(1, 31) if i + d < k], dtype=np.uint32)
+    tasks = api.plan_tasks(k, np_, m, acc)
+    nblocks = k // np_
+    for slots in (3, 4, 6):
+        order = api.order_tasks_for_reuse(tasks, slots)
+        assert sorted(order.tolist()) == list(range(len(tasks)))
+        plan_loads = block_loads(tasks, np.arange(len(tasks)), slots)
+        reuse_loads = block_loads(tasks, order, slots)
+        # every block once (one more where the walk starts inside the band and has to come back for the other half);
+        # the reference traversal returns to blocks it has dropped
+        assert nblocks <= reuse_loads <= nblocks + 1 and reuse_loads < plan_loads, (slots, reuse_loads, plan_loads)
+    # exhaustive plans: never worse than the reference's serpentine on these shapes, and still a permutation
+    for (k, np_, m, slots) in ((40, 4, 2, 3), (64, 4, 4, 3), (60, 5, 3, 4), (23, 2, 3, 3)):
+        tasks = api.plan_tasks(k, np_, m)
+        order = api.order_tasks_for_reuse(tasks, slots)
+        assert sorted(order.tolist()) == list(range(len(tasks)))
+        assert block_loads(tasks, order, slots) <= block_loads(tasks, np.arange(len(tasks)), slots) * 1.05
+    assert len(api.order_tasks_for_reuse(api.plan_tasks(1, 1, 1), 3)) == 0
+
+
+@pytest.mark.gpu
+def test_streamed_run_in_reuse_order(matcher, tmp_path):
+    sizes = [700 + 37 * (i % 9) for i in range(40)]
+    desc, paths = write_dataset(tmp_path, sizes, seed=53)
+    fam = ch.build_hash_family(ch.FamilyParams())
+    fresh(matcher, fam)
+    cfg = ch.MatchConfig()
+    centering, _ = matcher.centering_pass_files(paths, block_images=8, io_threads=2)
+    k, np_, m = len(sizes), 4, 2
+    acc = np.array([(i, i + d) for i in range(k) for d in range(1, 7) if i + d < k], dtype=np.uint32)
+    flat = api.plan_guided(k, np_, m, acc)
+    runs = {}
+    for order in (api.ORDER_REFERENCE, api.ORDER_REUSE):
+        got = {}
+
+        def sink(task, pairs, offs, rec):
+            o = offs.astype(np.int64) - int(offs[0])
+            for i, (a, b) in enumerate(pairs):
+                got[(int(a), int(b))] = rec[o[i]:o[i + 1]].copy()
+
+        stats, _ = matcher.match_plan_streamed(paths, np_, m, cfg, accepted_pairs=acc, io_threads=2, sink=sink, task_order=order)
+        assert stats["pairs"] == len(flat) and stats["max_resident_blocks"] <= 3
+        runs[order] = (stats, got)
+    assert (k + np_ - 1) // np_ <= runs[api.ORDER_REUSE][0]["block_loads"] <= (k + np_ - 1) // np_ + 1
+    assert runs[api.ORDER_REUSE][0]["block_loads"] < runs[api.ORDER_REFERENCE][0]["block_loads"]
+    assert set(runs[0][1]) == set(runs[1][1]) == {(int(a), int(b)) for a, b in flat}
+    for key, rec in runs[0][1].items():
+        assert np.array_equal(rec, runs[1][1][key])
+    with pytest.raises(ValueError):
+        matcher.match_plan_streamed(paths, np_, m, cfg, task_order=7)
