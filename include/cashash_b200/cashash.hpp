@@ -793,7 +793,8 @@ public:
                                              const std::vector<std::pair<std::uint32_t, std::uint32_t>>* accepted = nullptr,
                                              std::uint32_t group_slots = 0, std::uint32_t block_slots = 0,
                                              std::uint32_t io_threads = 8, std::vector<std::string>* failures = nullptr,
-                                             chgpu_task_order task_order = CHGPU_ORDER_REFERENCE) {
+                                             chgpu_task_order task_order = CHGPU_ORDER_REFERENCE, std::uint32_t shard = 0,
+                                             std::uint32_t shards = 1) {
         if (partition.image_count != files.size()) throw std::invalid_argument("match_plan_streamed: one file per image");
         std::vector<std::string> store;
         std::vector<const char*> cpaths;
@@ -824,7 +825,7 @@ public:
         chgpu_streamed_stats stats{};
         const chgpu_status st = chgpu_match_plan_streamed(
             ctx_, cpaths.data(), partition.image_count, partition.block_images, partition.blocks_per_group, group_slots, block_slots,
-            task_order, acc, accepted ? accepted->size() : 0, &c, io_threads, trampoline, &thunk, res.data(), &stats);
+            task_order, shard, shards, acc, accepted ? accepted->size() : 0, &c, io_threads, trampoline, &thunk, res.data(), &stats);
         if (thunk.error) std::rethrow_exception(thunk.error);
         collect_failures(files, res, failures);
         if (st == CHGPU_EINVAL) throw std::invalid_argument("match_plan_streamed: bad pair list, or slot limits below what one task needs");

@@ -425,9 +425,17 @@ typedef enum chgpu_task_order { CHGPU_ORDER_REFERENCE = 0, CHGPU_ORDER_REUSE = 1
 /* order_out: ntasks task indices.  Plans of more than 2^18 tasks are returned in plan order. */
 chgpu_status chgpu_order_tasks_for_reuse(const chgpu_plan_task* tasks, uint32_t ntasks, uint32_t block_slots,
                                          uint32_t* order_out);
+/* Multi-GPU form of a streamed run: the executed task sequence (plan order, or `order` from
+ * chgpu_order_tasks_for_reuse) is cut into `shards` contiguous ranges of about equal pair counts — contiguous, so a
+ * worker keeps the block locality of the sequence (assign_workers' round robin, scheduler.cpp:166-173, would hand
+ * every worker every block).  first_out[s] .. first_out[s + 1] are the positions of worker s; shards + 1 entries. */
+chgpu_status chgpu_shard_tasks(const chgpu_plan_task* tasks, const uint32_t* order /* nullable: plan order */,
+                               uint32_t ntasks, uint32_t shards, uint32_t* first_out);
+/* `shard` of `shards` (0 of 0 or 1: the whole plan): one call per GPU / process, each with its own context. */
 chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths, uint32_t image_count,
                                        uint32_t block_images, uint32_t blocks_per_group,
                                        uint32_t group_slots, uint32_t block_slots, chgpu_task_order task_order,
+                                       uint32_t shard, uint32_t shards,
                                        const uint32_t* accepted /* nullable: exhaustive */, uint64_t accepted_count,
                                        const chgpu_match_cfg* cfg, uint32_t io_threads, chgpu_plan_sink_fn sink /* nullable */,
                                        void* user, chgpu_file_result* file_results /* nullable */,

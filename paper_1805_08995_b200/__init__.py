@@ -11,6 +11,6 @@ from .api import (  # noqa: F401
     CacheMismatchError, centering_fingerprint, load_centering_file, load_code_cache, read_code_cache_header,
     save_centering_file, save_code_cache, MatchFileSink,
     plan_tasks, hashing_tasks, simulate_residency, auto_partition_sizing, partition_sizing_for_device,
-    TASK_DTYPE, ACTION_DTYPE, order_tasks_for_reuse, ORDER_REFERENCE, ORDER_REUSE,
+    TASK_DTYPE, ACTION_DTYPE, order_tasks_for_reuse, ORDER_REFERENCE, ORDER_REUSE, shard_tasks,
 )
 from .synth import make_dataset  # noqa: F401

@@ -182,8 +182,9 @@ SIGNATURES = {
     "chgpu_partition_sizing_for_device": (None, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
                                                  u32p, u32p]),
     "chgpu_order_tasks_for_reuse": (C.c_int, [C.POINTER(PlanTaskC), C.c_uint32, C.c_uint32, u32p]),
+    "chgpu_shard_tasks": (C.c_int, [C.POINTER(PlanTaskC), u32p, C.c_uint32, C.c_uint32, u32p]),
     "chgpu_match_plan_streamed": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
-                                            C.c_uint32, C.c_int, C.c_void_p, C.c_uint64, C.POINTER(MatchCfgC), C.c_uint32, PLAN_SINK_FN,
+                                            C.c_uint32, C.c_int, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint64, C.POINTER(MatchCfgC), C.c_uint32, PLAN_SINK_FN,
                                             C.c_void_p, C.POINTER(FileResultC), C.POINTER(StreamedStatsC)]),
     "chgpu_centering_pass_files": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.c_uint32, C.c_uint32, C.c_uint32,
                                              C.POINTER(FileResultC), f64p]),

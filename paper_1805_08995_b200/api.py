@@ -334,6 +334,18 @@ def order_tasks_for_reuse(tasks: np.ndarray, block_slots: int = 3) -> np.ndarray
     return out
 
 
+def shard_tasks(tasks: np.ndarray, shards: int, order=None) -> np.ndarray:
+    """Positions (shards + 1) cutting the executed task sequence into contiguous ranges of about equal pair counts."""
+    t = np.ascontiguousarray(tasks, dtype=TASK_DTYPE)
+    o = None if order is None else np.ascontiguousarray(order, dtype=np.uint32)
+    out = np.zeros(shards + 1, dtype=np.uint32)
+    st = N.load().chgpu_shard_tasks(t.ctypes.data_as(C.POINTER(N.PlanTaskC)) if len(t) else None,
+                                    None if o is None else o.ctypes.data_as(N.u32p), len(t), shards, out.ctypes.data_as(N.u32p))
+    if st != N.OK:
+        _raise(st, "shard_tasks: shards must be >= 1")
+    return out
+
+
 def auto_partition_sizing(mean_image_bytes: int, memory_budget_bytes: int) -> tuple[int, int]:
     """auto_partition_sizing (scheduler.hpp:134): (block_images, blocks_per_group)."""
     a, b = C.c_uint32(0), C.c_uint32(0)
@@ -540,7 +552,7 @@ class Matcher:
 
     def match_plan_streamed(self, paths, block_images: int, blocks_per_group: int, cfg: MatchConfig = MatchConfig(),
                             accepted_pairs=None, group_slots: int = 0, block_slots: int = 0, io_threads: int = 8, sink=None,
-                            task_order: int = 0):
+                            task_order: int = 0, shard: int = 0, shards: int = 1):
         """Out-of-core run of the exhaustive (accepted_pairs None) or guided plan over CHFT files
         (chgpu_match_plan_streamed).  sink(task, pairs (k,2) u32, offsets (k+1) u64, records) is called in execution order
         (plan order, or the reuse order with task_order=ORDER_REUSE; `task` is always the plan's task index).
@@ -574,6 +586,7 @@ class Matcher:
 
         cb = N.PLAN_SINK_FN(_cb)
         st = self.lib.chgpu_match_plan_streamed(self.h, arr, n, block_images, blocks_per_group, group_slots, block_slots, task_order,
+                                                shard, shards,
                                                 None if acc is None else keep.ctypes.data, 0 if acc is None else len(acc),
                                                 C.byref(c), io_threads, cb, None, res, C.byref(stats))
         if err:

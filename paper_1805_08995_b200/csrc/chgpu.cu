@@ -1601,7 +1601,11 @@ chgpu_status load_start(chgpu_ctx* ctx, const char* const* paths, const uint32_t
     for (uint32_t i = 0; i < count; ++i) job->path_store.emplace_back(paths[i] ? paths[i] : "");
     for (uint32_t i = 0; i < count; ++i) job->paths.push_back(job->path_store[i].c_str());
     job->image_ids.assign(image_ids, image_ids + count);
-    job->results.assign(count, chgpu_file_result{});
+    {
+        chgpu_file_result not_reached{};
+        not_reached.status = CHGPU_ECUDA;  // a batch that device trouble ends early leaves the rest unloaded, not "ok"
+        job->results.assign(count, not_reached);
+    }
     io_threads = std::max<uint32_t>(1, std::min<uint32_t>(io_threads ? io_threads : 4, 64));
     job->io_threads = io_threads;
     const size_t S = std::max<size_t>(std::max<size_t>(8, 2 * size_t(io_threads)), ring_slots);

@@ -314,6 +314,22 @@ void order_for_reuse(const chgpu_plan_task* tasks, uint32_t n, uint32_t slots, s
     }
 }
 
+// Contiguous ranges of the executed sequence, balanced by pair count: worker s gets positions [first[s], first[s + 1]).
+void shard_sequence(const chgpu_plan_task* tasks, const uint32_t* order, uint32_t n, uint32_t shards, std::vector<uint32_t>& first) {
+    shards = std::max<uint32_t>(1, shards);
+    uint64_t total = 0;
+    for (uint32_t k = 0; k < n; ++k) total += tasks[order ? order[k] : k].npairs;
+    first.assign(shards + 1, n);
+    first[0] = 0;
+    uint64_t acc = 0;
+    uint32_t s = 1;
+    for (uint32_t k = 0; k < n && s < shards; ++k) {
+        acc += tasks[order ? order[k] : k].npairs;
+        // the boundary after position k belongs to every worker whose share of the pairs is complete by now
+        while (s < shards && acc * shards >= total * s) first[s++] = k + 1;
+    }
+}
+
 uint32_t default_limit(chgpu_residency_mode mode) { return mode == CHGPU_RESIDENCY_HASHING ? 2u : 3u; }
 
 double seconds_since(std::chrono::steady_clock::time_point t0) {
@@ -554,6 +570,15 @@ chgpu_status chgpu_order_tasks_for_reuse(const chgpu_plan_task* tasks, uint32_t 
     return CHGPU_OK;
 }
 
+chgpu_status chgpu_shard_tasks(const chgpu_plan_task* tasks, const uint32_t* order, uint32_t ntasks, uint32_t shards,
+                               uint32_t* first_out) {
+    if ((ntasks && !tasks) || !first_out || shards == 0) return CHGPU_EINVAL;
+    std::vector<uint32_t> first;
+    shard_sequence(tasks, order, ntasks, shards, first);
+    std::copy(first.begin(), first.end(), first_out);
+    return CHGPU_OK;
+}
+
 void chgpu_auto_partition_sizing(uint64_t mean_image_bytes, uint64_t memory_budget_bytes, uint32_t* block_images,
                                  uint32_t* blocks_per_group) {
     const uint64_t per_image = std::max<uint64_t>(1, mean_image_bytes);
@@ -577,7 +602,8 @@ void chgpu_partition_sizing_for_device(uint64_t device_image_bytes, uint64_t fil
 
 chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths, uint32_t image_count,
                                        uint32_t block_images, uint32_t blocks_per_group, uint32_t group_slots,
-                                       uint32_t block_slots, chgpu_task_order task_order, const uint32_t* accepted,
+                                       uint32_t block_slots, chgpu_task_order task_order, uint32_t shard, uint32_t shards,
+                                       const uint32_t* accepted,
                                        uint64_t accepted_count, const chgpu_match_cfg* cfg, uint32_t io_threads,
                                        chgpu_plan_sink_fn sink, void* user,
                                        chgpu_file_result* file_results, chgpu_streamed_stats* stats) {
@@ -611,6 +637,13 @@ chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths,
         tasks.swap(permuted);
     } else if (task_order != CHGPU_ORDER_REFERENCE) {
         return CHGPU_EINVAL;
+    }
+    if (shards > 1) {  // this worker's contiguous range of the executed sequence
+        if (shard >= shards) return CHGPU_EINVAL;
+        std::vector<uint32_t> first;
+        shard_sequence(tasks.data(), nullptr, uint32_t(tasks.size()), shards, first);
+        tasks.assign(tasks.begin() + first[shard], tasks.begin() + first[shard + 1]);
+        plan_index.assign(plan_index.begin() + first[shard], plan_index.begin() + first[shard + 1]);
     }
 
     Machine m;

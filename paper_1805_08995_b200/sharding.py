@@ -22,7 +22,8 @@ import os
 
 import numpy as np
 
-from .api import RECORD_DTYPE, MatchConfig, shard_range
+from .api import (ORDER_REFERENCE, ORDER_REUSE, RECORD_DTYPE, MatchConfig, order_tasks_for_reuse, plan_exhaustive, plan_guided,
+                  plan_tasks, shard_range, shard_tasks)
 
 
 class Comm:
@@ -137,6 +138,52 @@ class ShardedJob:
         offsets = np.zeros(len(all_counts) + 1, dtype=np.uint64)
         np.cumsum(all_counts, out=offsets[1:])
         return offsets, np.concatenate([p[1] for p in parts])
+
+
+def streamed_shard_pairs(image_count: int, block_images: int, blocks_per_group: int, rank: int, world: int, accepted_pairs=None,
+                         task_order: int = ORDER_REFERENCE, block_slots: int = 3):
+    """Host mirror of the split chgpu_match_plan_streamed(shard=rank, shards=world) makes: (plan task indices, pairs) this
+    rank executes, in execution order — a contiguous range of the (optionally reuse-ordered) task sequence, balanced by
+    pair count, so a rank keeps the block locality of the sequence."""
+    tasks = plan_tasks(image_count, block_images, blocks_per_group, accepted_pairs)
+    flat = plan_exhaustive(image_count, block_images, blocks_per_group) if accepted_pairs is None else plan_guided(
+        image_count, block_images, blocks_per_group, accepted_pairs)
+    order = order_tasks_for_reuse(tasks, block_slots) if task_order == ORDER_REUSE else np.arange(len(tasks), dtype=np.uint32)
+    first = shard_tasks(tasks, world, order)
+    mine = order[int(first[rank]):int(first[rank + 1])]
+    chunks = [flat[int(tasks["first_pair"][t]):int(tasks["first_pair"][t] + tasks["npairs"][t])] for t in mine]
+    pairs = np.concatenate(chunks) if chunks else np.zeros((0, 2), np.uint32)
+    return mine, pairs
+
+
+class StreamedShardedJob:
+    """Out-of-core matching of one dataset of CHFT files over `comm.world` GPUs: every rank streams the centering
+    pass over its share of the files (exact u64 sums, exchanged once: 1 KB), then runs its contiguous range of the task
+    sequence with chgpu_match_plan_streamed(shard=rank, shards=world).  No data-path collective."""
+
+    def __init__(self, engine, comm: Comm):
+        self.engine = engine
+        self.comm = comm
+
+    def set_centering(self, paths, block_images: int, io_threads: int = 8) -> np.ndarray:
+        e, c = self.engine, self.comm
+        mine = list(paths[c.rank::c.world])
+        e.centering_reset()
+        if mine:
+            e.centering_pass_files(mine, block_images, io_threads)  # leaves this rank's sums in the accumulator
+        sums, count = e.centering_sums()
+        packed = np.concatenate([np.asarray(sums, dtype=np.uint64), np.array([count], dtype=np.uint64)])
+        others = c.sum_u64(packed) - packed
+        if c.world > 1:
+            e.centering_add_sums(others[:128], int(others[128]))
+        return e.centering_apply()
+
+    def match(self, paths, block_images: int, blocks_per_group: int, cfg: MatchConfig = MatchConfig(), accepted_pairs=None,
+              block_slots: int = 0, task_order: int = ORDER_REUSE, io_threads: int = 8, sink=None):
+        stats, results = self.engine.match_plan_streamed(paths, block_images, blocks_per_group, cfg, accepted_pairs=accepted_pairs,
+                                                         block_slots=block_slots, io_threads=io_threads, sink=sink,
+                                                         task_order=task_order, shard=self.comm.rank, shards=self.comm.world)
+        return stats, results
 
 
 class CollectingSink:

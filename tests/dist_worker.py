@@ -14,7 +14,7 @@ sys.path.insert(0, str(ROOT / "tests"))
 
 import oracle_lib  # noqa: E402
 import paper_1805_08995_b200 as ch  # noqa: E402
-from paper_1805_08995_b200.sharding import CollectingSink, Comm, ShardedJob  # noqa: E402
+from paper_1805_08995_b200.sharding import CollectingSink, Comm, ShardedJob, streamed_shard_pairs  # noqa: E402
 
 
 class OracleEngine:
@@ -95,6 +95,10 @@ def main():
     if comm.rank == 0:
         offsets, recs = gathered
         np.savez(out / "gathered.npz", offsets=offsets, records=recs, pairs=pairs)
+    # the split of an out-of-core (streamed) run: this rank's contiguous range of the task sequence, both orders
+    for name, order in (("plan", ch.ORDER_REFERENCE), ("reuse", ch.ORDER_REUSE)):
+        tasks_mine, pairs_mine = streamed_shard_pairs(images, 2, 2, comm.rank, comm.world, task_order=order)
+        np.savez(out / f"streamed_{name}_rank{comm.rank}.npz", tasks=tasks_mine, pairs=pairs_mine)
     comm.barrier()
     dist.destroy_process_group()
 

@@ -438,3 +438,66 @@ def test_streamed_run_in_reuse_order(matcher, tmp_path):
         assert np.array_equal(rec, runs[1][1][key])
     with pytest.raises(ValueError):
         matcher.match_plan_streamed(paths, np_, m, cfg, task_order=7)
+
+
+# ---- sharding a streamed run over workers (one process / context per GPU) ------------------------------------------
+def test_shard_tasks_contiguous_and_balanced():
+    k, np_, m = 1024, 64, 4
+    acc = np.array([(i, i + d) for i in range(k) for d in range(1, 31) if i + d < k], dtype=np.uint32)
+    for tasks, order in ((api.plan_tasks(k, np_, m, acc), None), (api.plan_tasks(k, np_, m, acc), "reuse"), (api.plan_tasks(48, 4, 3), None)):
+        o = api.order_tasks_for_reuse(tasks, 3) if order == "reuse" else None
+        seq = tasks if o is None else tasks[o]
+        total = int(seq["npairs"].sum())
+        for shards in (1, 2, 3, 8, len(tasks) + 5):
+            first = api.shard_tasks(tasks, shards, o)
+            assert first[0] == 0 and first[-1] == len(tasks) and np.all(np.diff(first.astype(np.int64)) >= 0)
+            per = [int(seq["npairs"][first[i]:first[i + 1]].sum()) for i in range(shards)]
+            assert sum(per) == total
+            if shards <= 8:  # no worker exceeds its share by more than one task
+                assert max(per) <= total / shards + int(seq["npairs"].max())
+    with pytest.raises(ValueError):
+        api.shard_tasks(api.plan_tasks(10, 2, 2), 0)
+
+
+@pytest.mark.gpu
+def test_streamed_shards_cover_the_plan(matcher, tmp_path):
+    sizes = [600 + 41 * (i % 7) for i in range(24)]
+    desc, paths = write_dataset(tmp_path, sizes, seed=59)
+    fam = ch.build_hash_family(ch.FamilyParams())
+    fresh(matcher, fam)
+    cfg = ch.MatchConfig()
+    matcher.centering_pass_files(paths, block_images=6, io_threads=2)
+    k, np_, m = len(sizes), 3, 2
+    flat = api.plan_exhaustive(k, np_, m)
+    whole = {}
+    matcher.match_plan_streamed(paths, np_, m, cfg, io_threads=2, task_order=api.ORDER_REUSE,
+                                sink=lambda t, p, o, r: whole.update({(int(a), int(b)): r[int(o[i] - o[0]):int(o[i + 1] - o[0])].copy()
+                                                                      for i, (a, b) in enumerate(p)}))
+    assert set(whole) == {(int(a), int(b)) for a, b in flat}
+    parts, pairs_seen = {}, 0
+    for shard in range(3):  # what three GPUs would run, here one after the other on the one context
+        stats, _ = matcher.match_plan_streamed(paths, np_, m, cfg, io_threads=2, task_order=api.ORDER_REUSE, shard=shard, shards=3,
+                                               sink=lambda t, p, o, r: parts.update({(int(a), int(b)): r[int(o[i] - o[0]):int(o[i + 1] - o[0])].copy()
+                                                                                     for i, (a, b) in enumerate(p)}))
+        assert 0 < stats["pairs"] < len(flat)
+        pairs_seen += stats["pairs"]
+    assert pairs_seen == len(flat) and set(parts) == set(whole)  # every pair exactly once over the shards
+    for key, rec in whole.items():
+        assert np.array_equal(rec, parts[key])
+    with pytest.raises(ValueError):
+        matcher.match_plan_streamed(paths, np_, m, cfg, shard=3, shards=3)
+
+
+@pytest.mark.gpu
+def test_streamed_sharded_job_single_rank(matcher, restatement, tmp_path):
+    from paper_1805_08995_b200.sharding import Comm, StreamedShardedJob
+    sizes = [500 + 29 * (i % 5) for i in range(12)]
+    desc, paths = write_dataset(tmp_path, sizes, seed=61)
+    fresh(matcher, ch.build_hash_family(ch.FamilyParams()))
+    job = StreamedShardedJob(matcher, Comm(0, 1))
+    cen = job.set_centering(paths, block_images=5, io_threads=2)
+    assert np.array_equal(cen, restatement.centering(desc))
+    seen = []
+    stats, results = job.match(paths, 3, 2, ch.MatchConfig(), io_threads=2, sink=lambda t, p, o, r: seen.append(p))
+    assert results == sizes and stats["pairs"] == 12 * 11 // 2
+    assert sorted(map(tuple, np.concatenate(seen).tolist())) == sorted(map(tuple, api.plan_exhaustive(12, 3, 2).tolist()))

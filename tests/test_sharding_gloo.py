@@ -62,3 +62,14 @@ def test_sharded_job_is_worker_invariant(tmp_path, single_process_truth, world):
     assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
     sizes = [b - a for a, b in spans]
     assert max(sizes) - min(sizes) <= 1
+
+    # streamed (out-of-core) split: contiguous task ranges per rank, every pair exactly once, in both task orders
+    from paper_1805_08995_b200 import api
+    tasks = api.plan_tasks(IMAGES, 2, 2)
+    for name in ("plan", "reuse"):
+        parts = [np.load(tmp_path / f"streamed_{name}_rank{r}.npz") for r in range(world)]
+        seq = np.concatenate([p["tasks"] for p in parts])
+        want = np.arange(len(tasks)) if name == "plan" else api.order_tasks_for_reuse(tasks, 3)
+        assert np.array_equal(seq, want)
+        got = np.concatenate([p["pairs"] for p in parts])
+        assert sorted(map(tuple, got.tolist())) == sorted(map(tuple, pairs.tolist()))
