@@ -56,43 +56,61 @@ __device__ __forceinline__ unsigned long long mix64_dev(unsigned long long x) {
 }
 
 // One CTA per pair: ordered compaction of the per-query scratch into MatchRecord{u32 q, u32 t, f64 d^2}
-// (feature_io.hpp:51-57), ascending q, at most one per query (matcher.cpp:191-192).
-__global__ void compact_kernel(const PairDesc* __restrict__ pairs, const DevImage* __restrict__ images,
-                               const uint2* __restrict__ res, const unsigned long long* __restrict__ offsets,
-                               uint4* __restrict__ records, uint32_t first_pair_global, DevStats* stats) {
+// (feature_io.hpp:51-57), ascending q, at most one per query (matcher.cpp:191-192).  A thread owns kCompactPer
+// consecutive queries, so a pass over 8,192 queries is one warp scan + one scan over the warps (three barriers)
+// and every thread has its loads in flight at once.
+constexpr int kCompactPer = 8;
+__global__ void __launch_bounds__(1024) compact_kernel(const PairDesc* __restrict__ pairs, const DevImage* __restrict__ images,
+                                                       const uint2* __restrict__ res, const unsigned long long* __restrict__ offsets,
+                                                       uint4* __restrict__ records, uint32_t first_pair_global, DevStats* stats) {
     __shared__ uint32_t s_warp[32];
-    __shared__ uint32_t s_base;
-    const uint32_t pair = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t pair = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const PairDesc pd = pairs[pair];
     const uint32_t nq = images[pd.slot_i].n;
-    if (tid == 0) s_base = 0;
-    __syncthreads();
     uint4* out = records + offsets[pair];
+    const uint2* __restrict__ in = res + pd.res_off;
     unsigned long long csum = 0;
-    for (uint32_t q0 = 0; q0 < nq; q0 += blockDim.x) {
-        const uint32_t q = q0 + tid;
-        uint2 r = make_uint2(kNone, 0);
-        if (q < nq) r = res[pd.res_off + q];
-        const bool hit = r.x != kNone;
-        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-        if (lane == 0) s_warp[warp] = __popc(bal);
+    uint32_t base = 0;  // records written by earlier passes (every thread keeps its own copy)
+    for (uint32_t q0 = 0; q0 < nq; q0 += blockDim.x * kCompactPer) {
+        const uint32_t qa = q0 + tid * kCompactPer;
+        uint2 r[kCompactPer];
+        uint32_t mask = 0;
+#pragma unroll
+        for (int k = 0; k < kCompactPer; ++k) {
+            r[k] = qa + k < nq ? __ldcs(in + qa + k) : make_uint2(kNone, 0u);
+            if (r[k].x != kNone) mask |= 1u << k;
+        }
+        const uint32_t cnt = __popc(mask);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, incl, d);
+            if (int(lane) >= d) incl += u;
+        }
+        if (lane == 31) s_warp[warp] = incl;
         __syncthreads();
-        uint32_t before = s_base;
-        for (uint32_t w = 0; w < warp; ++w) before += s_warp[w];
-        if (hit) {
-            const uint32_t pos = before + __popc(bal & ((1u << lane) - 1u));
-            const unsigned long long db = (unsigned long long)__double_as_longlong(double(r.y));
-            out[pos] = make_uint4(q, r.x, uint32_t(db), uint32_t(db >> 32));
-            csum += mix64_dev(mix64_dev((unsigned long long)(first_pair_global + pair) << 32 | q) ^
-                              ((unsigned long long)r.x << 32 | r.y));
+        if (warp == 0) {
+            uint32_t w = lane < nwarps ? s_warp[lane] : 0u;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, w, d);
+                if (int(lane) >= d) w += u;
+            }
+            s_warp[lane] = w;  // inclusive over the warps
         }
         __syncthreads();
-        if (tid == 0) {
-            uint32_t tot = 0;
-            for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) tot += s_warp[w];
-            s_base += tot;
-        }
-        __syncthreads();
+        uint32_t pos = base + (warp ? s_warp[warp - 1] : 0u) + incl - cnt;
+        base += s_warp[31];
+#pragma unroll
+        for (int k = 0; k < kCompactPer; ++k)
+            if (mask & (1u << k)) {
+                const uint32_t q = qa + k;
+                const unsigned long long db = (unsigned long long)__double_as_longlong(double(r[k].y));
+                out[pos++] = make_uint4(q, r[k].x, uint32_t(db), uint32_t(db >> 32));
+                csum += mix64_dev(mix64_dev((unsigned long long)(first_pair_global + pair) << 32 | q) ^
+                                  ((unsigned long long)r[k].x << 32 | r[k].y));
+            }
+        __syncthreads();  // s_warp is rewritten by the next pass
     }
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, d);
