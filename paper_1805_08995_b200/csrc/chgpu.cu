@@ -1008,7 +1008,7 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
         }
         scan_counts_kernel<<<1, 1024, 0, ctx->compute>>>(b.d_counts, sb.count, b.d_offsets, ctx->d_stats);
         CK(cudaGetLastError());
-        compact_kernel<<<sb.count, 1024, 0, ctx->compute>>>(b.d_pairs, ctx->d_images, ctx->d_res, b.d_offsets,
+        compact_kernel<<<sb.count, kCompactThreads, 0, ctx->compute>>>(b.d_pairs, ctx->d_images, ctx->d_res, b.d_offsets,
                                                             b.d_records, sb.first, ctx->d_stats);
         CK(cudaGetLastError());
         CK(cudaEventRecord(b.ev_done, ctx->compute));

@@ -57,10 +57,19 @@ __device__ __forceinline__ unsigned long long mix64_dev(unsigned long long x) {
 
 // One CTA per pair: ordered compaction of the per-query scratch into MatchRecord{u32 q, u32 t, f64 d^2}
 // (feature_io.hpp:51-57), ascending q, at most one per query (matcher.cpp:191-192).  A thread owns kCompactPer
-// consecutive queries, so a pass over 8,192 queries is one warp scan + one scan over the warps (three barriers)
-// and every thread has its loads in flight at once.
-constexpr int kCompactPer = 8;
-__global__ void __launch_bounds__(1024) compact_kernel(const PairDesc* __restrict__ pairs, const DevImage* __restrict__ images,
+// consecutive queries, so a pass over kCompactThreads * kCompactPer queries is one warp scan + one scan over the warps
+// (three barriers) with every thread's loads in flight at once.  Measured per 4,096 pairs of 8,192 queries (scripts/exp4.sh):
+// 512 x 4: 98 us, 256 x 4: 99, 512 x 2: 109, 1024 x 4: 114, 512 x 8: 129, 1024 x 8: 168, 512 x 16: 194 (the old one-query-per-
+// thread kernel with serial scans: 329).
+#ifndef CHGPU_COMPACT_PER
+#define CHGPU_COMPACT_PER 4
+#endif
+#ifndef CHGPU_COMPACT_THREADS
+#define CHGPU_COMPACT_THREADS 512
+#endif
+constexpr int kCompactPer = CHGPU_COMPACT_PER;
+constexpr int kCompactThreads = CHGPU_COMPACT_THREADS;
+__global__ void __launch_bounds__(kCompactThreads) compact_kernel(const PairDesc* __restrict__ pairs, const DevImage* __restrict__ images,
                                                        const uint2* __restrict__ res, const unsigned long long* __restrict__ offsets,
                                                        uint4* __restrict__ records, uint32_t first_pair_global, DevStats* stats) {
     __shared__ uint32_t s_warp[32];
@@ -100,7 +109,7 @@ __global__ void __launch_bounds__(1024) compact_kernel(const PairDesc* __restric
         }
         __syncthreads();
         uint32_t pos = base + (warp ? s_warp[warp - 1] : 0u) + incl - cnt;
-        base += s_warp[31];
+        base += s_warp[nwarps - 1];
 #pragma unroll
         for (int k = 0; k < kCompactPer; ++k)
             if (mask & (1u << k)) {
