@@ -751,6 +751,18 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
     std::vector<SubBatch> subs;
     {
         SubBatch cur{0, 0, 0, 0, 0, false, 0, 0};
+        // The persistent grid hands out one unit per pair: a sub-batch whose pair count is a multiple of the CTA count
+        // ends with every SM busy (4,096 pairs on 148 SMs leave 48 of them idle for the last unit: ~1 % of a launch).
+        uint32_t pairs_cap = 1u << 20;
+        {
+            uint32_t s0;
+            const char* no_round = getenv("CHGPU_NO_SUBBATCH_ROUNDING");
+            if (!(no_round && no_round[0] == '1') && find_slot(ctx, run.pairs[0], &s0) == CHGPU_OK && ctx->images[s0].dev.n) {
+                const uint64_t fit = ctx->sub_batch_queries / ctx->images[s0].dev.n;
+                const uint64_t sms = uint64_t(ctx->prop.multiProcessorCount);
+                if (fit >= 4 * sms) pairs_cap = uint32_t(std::min<uint64_t>(fit / sms * sms, 1u << 20));
+            }
+        }
         for (uint32_t k = 0; k < npairs; ++k) {
             uint32_t si, sj;
             if (const chgpu_status s = find_slot(ctx, run.pairs[2 * k], &si)) return s;
@@ -762,7 +774,7 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
                             run.pairs[2 * k], run.pairs[2 * k + 1]);
             const uint32_t tiles = uint32_t(ctx->images[sj].tile_slots.size());
             const bool tiled = tiles != 0;
-            if (cur.count && (cur.queries + I.n > ctx->sub_batch_queries || cur.count >= (1u << 20) || tiled != cur.tiled ||
+            if (cur.count && (cur.queries + I.n > ctx->sub_batch_queries || cur.count >= pairs_cap || tiled != cur.tiled ||
                               (tiled && (cur.queries + I.n) * std::max(cur.max_tiles, tiles) * run.cfg.top_k * 4 > kTileListBytes))) {
                 subs.push_back(cur);
                 cur = SubBatch{k, 0, 0, 0, 0, false, 0, 0};
