@@ -4,7 +4,7 @@
 tag=${1:-r01x}
 ncu --set full --clock-control none --import-source on -k regex:match_kernel -s 3 -c 1 -f -o gpurun_out/${tag}_match \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --images 200 --pairs 16384 > /dev/null 2>&1
-python scripts/ncu_summary.py gpurun_out/${tag}_match.ncu-rep profiles/${tag}_match_kernel_ncu_full.json 33554432
+python scripts/ncu_summary.py gpurun_out/${tag}_match.ncu-rep profiles/${tag}_match_kernel_ncu_full.json 32735232  # 3,996 pairs (27 x 148 SMs) x 8,192 queries per launch
 cp profiles/${tag}_match_kernel_ncu_full.json gpurun_out/
 ncu --set full --clock-control none --import-source on -k regex:hash_filter_kernel -s 1 -c 1 -f -o gpurun_out/${tag}_hash \
     python scripts/hash_bench.py --images 400 --reps 1 > /dev/null 2>&1
