@@ -155,7 +155,7 @@ struct BandFilter {
         const double x = kp_i[4 * static_cast<size_t>(q)], y = kp_i[4 * static_cast<size_t>(q) + 1];
         const double a = (F[0] * x + F[1] * y) + F[2];  // epipolar_line: l = F (x, y, 1)^T  (geometry.cpp:98-101)
         const double b = (F[3] * x + F[4] * y) + F[5];
-        const double c = (F[6] * x + F[7] * y) + F[8];
+        const double c = F[6] * x + (F[7] * y + F[8]);   // (association order: see chor.h)
         if (a == 0.0 && b == 0.0) return false;  // EpipolarLine::degenerate, geometry.hpp:28
         const double inv_norm = 1.0 / std::sqrt(a * a + b * b);
         std::erase_if(cands, [&](uint32_t idx) {

@@ -95,9 +95,17 @@ int chor_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
  * matcher.cpp:205-210): between candidate lookup and ranking the candidates of query q are cut to those
  * within band_px of the epipolar line l = F (x_q, y_q, 1)^T; a degenerate line (a == b == 0) leaves the
  * query unguided.  kp_*: n x 4 f32 (x, y, scale, orientation); F: 9 doubles, row-major.
- * The line is evaluated as l_i = (F[i][0]*x + F[i][1]*y) + F[i][2] in fp64 without contraction (the
- * reference forms it with an Eigen 3x3 * 3x1 product whose association order is not pinned here: Eigen is
- * absent from this image, so geometry.cpp cannot be compiled).  In oracle/_ref everything but that line is
+ * The line is evaluated in fp64 without contraction as
+ *     a = (F00 x + F01 y) + F02,   b = (F10 x + F11 y) + F12,   c = F20 x + (F21 y + F22).
+ * The reference forms it as an Eigen product, Matrix3d * Vector3d (geometry.cpp:98-101), and Eigen is absent from
+ * this image (geometry.cpp cannot be compiled), so the order is RESTATED from Eigen >= 3.3's published evaluation
+ * of that expression, not checked against a build: a 3 x 3 by 3 x 1 product is coefficient-based (sizes below the
+ * GEMV threshold); the assignment to a Vector3d is a linear vectorised traversal, completely unrolled (unaligned
+ * vectorisation is on by default): coefficients 0-1 as one Packet2d accumulated over the depth in order,
+ * pmadd = padd(pmul(.,.), .) without FMA on baseline x86-64, i.e. (F.0 x + F.1 y) + F.2; the odd coefficient 2 as
+ * lhs.row(2).cwiseProduct(rhs).sum(), whose 3-term reduction is unrolled by halves: c0 + (c1 + c2).
+ * Parity for candidates within one ulp of the band edge stays UNPINNED until an Eigen build confirms this.
+ * In oracle/_ref everything but that line is
  * the reference's own code (match_pair_filtered with this filter). */
 int chor_guided_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
                            const uint8_t* desc_i, const float* kp_i, uint32_t n_i, const uint32_t* shorts_i,

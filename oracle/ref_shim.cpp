@@ -296,7 +296,7 @@ int chor_guided_match_pair(const chor_family_params* p, const chor_match_cfg* cf
             const double x = kp.x, y = kp.y;
             const double a = (F[0] * x + F[1] * y) + F[2];
             const double b = (F[3] * x + F[4] * y) + F[5];
-            const double c = (F[6] * x + F[7] * y) + F[8];
+            const double c = F[6] * x + (F[7] * y + F[8]);  // (association order: see chor.h)
             if (a == 0.0 && b == 0.0) return false;
             const double inv_norm = 1.0 / std::sqrt(a * a + b * b);
             std::erase_if(candidates, [&](std::uint32_t idx) {

@@ -303,7 +303,8 @@ __device__ __forceinline__ EpiLine epipolar_band(const double* __restrict__ F, f
     EpiLine l;
     l.a = __dadd_rn(__dadd_rn(__dmul_rn(__ldg(F + 0), x), __dmul_rn(__ldg(F + 1), y)), __ldg(F + 2));
     l.b = __dadd_rn(__dadd_rn(__dmul_rn(__ldg(F + 3), x), __dmul_rn(__ldg(F + 4), y)), __ldg(F + 5));
-    l.c = __dadd_rn(__dadd_rn(__dmul_rn(__ldg(F + 6), x), __dmul_rn(__ldg(F + 7), y)), __ldg(F + 8));
+    // third component: the order Eigen >= 3.3 gives it (see oracle/chor.h): F20 x + (F21 y + F22)
+    l.c = __dadd_rn(__dmul_rn(__ldg(F + 6), x), __dadd_rn(__dmul_rn(__ldg(F + 7), y), __ldg(F + 8)));
     l.active = !(l.a == 0.0 && l.b == 0.0);
     l.inv_norm = l.active ? __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__dmul_rn(l.a, l.a), __dmul_rn(l.b, l.b)))) : 0.0;
     return l;
