@@ -437,6 +437,39 @@ def test_pair_list_batching_is_invariant(matcher, oracle, default_family):
         matcher.match_pairs(pairs, cfg, capacity=10)
 
 
+def test_sub_batches_rounded_to_the_sm_count(matcher, default_family, monkeypatch):
+    """A sub-batch holds a multiple of the SM count of pairs (one unit per pair in the persistent grid); where the cut
+    falls never changes a record."""
+    fresh(matcher, default_family)
+    k, n = 36, 256
+    d = make_dataset(k, n, seed=93)
+    matcher.centering_reset()
+    for i in range(k):
+        put(matcher, BASE + i, d[i])
+        matcher.centering_add(BASE + i)
+    matcher.centering_apply()
+    matcher.hash([BASE + i for i in range(k)])
+    pairs = ch.plan_exhaustive(k, 4, 3) + BASE  # 630 pairs
+    cfg = ch.MatchConfig()
+    sms = matcher.device_props()["sm_count"]
+    offs, rec, st = matcher.match_pairs(pairs, cfg)
+    assert st["match_launches"] == 1
+    try:
+        matcher.set_sub_batch_queries((4 * sms + 5) * n)  # room for 4 * sms + 5 pairs: the cut moves down to 4 * sms
+        chunks = []
+        st2 = matcher.match_pairs_stream(pairs, cfg, lambda first, o, r: chunks.append((first, len(o) - 1, r.copy())))
+        want_first = list(range(0, len(pairs), 4 * sms))
+        assert [c[0] for c in chunks] == want_first and chunks[0][1] == min(4 * sms, len(pairs))
+        assert np.array_equal(np.concatenate([c[2] for c in chunks]), rec)
+        monkeypatch.setenv("CHGPU_NO_SUBBATCH_ROUNDING", "1")
+        chunks2 = []
+        matcher.match_pairs_stream(pairs, cfg, lambda first, o, r: chunks2.append((first, len(o) - 1, r.copy())))
+        assert [c[0] for c in chunks2] == list(range(0, len(pairs), 4 * sms + 5))
+        assert np.array_equal(np.concatenate([c[2] for c in chunks2]), rec)
+    finally:
+        matcher.set_sub_batch_queries(0)
+
+
 def test_config2_properties_full_size(matcher, default_family):
     """BASELINE config 2 (100 images x 4,096 descriptors, 4,950 pairs) through the pair-list path;
     checked with properties that need no oracle run."""
