@@ -351,6 +351,7 @@ struct Replay {
     Partition part;
     uint32_t io_threads;
     bool centering_only;  // hashing schedule: blocks are summed into the centering accumulator, nothing is matched
+    int reduce_rounds = 3;  // N_r of the hash build (MatchConfig::reduce_rounds, matcher.hpp:14-23)
     std::vector<chgpu_file_result> results;
     std::vector<uint8_t> ok;  // image loaded and (matching runs) hashed
     std::vector<uint8_t> block_resident;
@@ -384,7 +385,7 @@ struct Replay {
         if (load_status != CHGPU_OK) return load_status;
         if (!centering_only && !good.empty()) {
             const auto t0 = std::chrono::steady_clock::now();
-            const chgpu_status h = chgpu_hash_images(ctx, good.data(), uint32_t(good.size()), 3);
+            const chgpu_status h = chgpu_hash_images(ctx, good.data(), uint32_t(good.size()), reduce_rounds);
             if (h == CHGPU_OK) chgpu_sync(ctx);
             st.hash_seconds += seconds_since(t0);
             if (h != CHGPU_OK) return h;
@@ -616,6 +617,8 @@ chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths,
     rp.part = Partition{image_count, block_images, blocks_per_group, (image_count + block_images - 1) / block_images};
     rp.io_threads = io_threads;
     rp.centering_only = false;
+    if (cfg->reduce_rounds < 0 || cfg->reduce_rounds > 7) return CHGPU_EINVAL;  // hashing.hpp:28-29
+    rp.reduce_rounds = cfg->reduce_rounds;
     rp.results.assign(image_count, chgpu_file_result{});
     rp.ok.assign(image_count, 0);
     rp.block_resident.assign(rp.part.nblocks, 0);
