@@ -50,6 +50,7 @@ constexpr size_t kStageBytes = size_t(32) << 20;
 constexpr int kStageSlots = 2;
 constexpr uint32_t kHashQueueCap = 1u << 21;    // undecided dots per hash launch (16 MiB); ~110 per 8K-point image are expected
 constexpr uint32_t kHashBatchImages = 2048;     // images per hash launch
+constexpr size_t kSinkChunkEntries = size_t(2) << 20;  // records per pinned delivery buffer of the streaming sink (32 MiB)
 constexpr uint64_t kSubBatchQueries = uint64_t(32) << 20;  // per sub-batch: sum of Nq (res 256 MiB, records <= 512 MiB); the persistent grid pays its tail once per launch
 
 size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a; }
@@ -149,6 +150,7 @@ struct chgpu_ctx {
     cudaStream_t compute = nullptr, copy = nullptr;
     cudaStream_t load = nullptr;  // H2D of background loads: runs beside the result copies (D2H on `copy`)
     cudaEvent_t ev_upload = nullptr, ev_compute = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+    cudaEvent_t ev_chunk[2] = {nullptr, nullptr};  // D2H of a result chunk into mb[j].h_records complete
     std::string err;
 
     Arena arena;
@@ -697,7 +699,7 @@ chgpu_status ensure_match_buffers(chgpu_ctx* ctx, MatchBuffers& b, const SubBatc
 chgpu_status ensure_host_records(chgpu_ctx* ctx, MatchBuffers& b, size_t need) {
     if (need <= b.h_records_cap) return CHGPU_OK;
     if (b.h_records) cudaFreeHost(b.h_records);
-    size_t cap = std::max<size_t>(b.h_records_cap * 2, size_t(4) << 20);
+    size_t cap = std::max<size_t>(b.h_records_cap * 2, kSinkChunkEntries);
     while (cap < need) cap *= 2;
     b.h_records = nullptr;
     b.h_records_cap = 0;
@@ -860,15 +862,49 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
                 CK(sync_copy());
             }
         } else {
-            if (const chgpu_status e = ensure_host_records(ctx, b, std::max<uint64_t>(total, 1))) return e;
-            if (total) {
-                CK(cudaMemcpyAsync(b.h_records, b.d_records, total * sizeof(uint4), cudaMemcpyDeviceToHost, ctx->copy));
-                CK(sync_copy());
-            }
-            if (run.sink) {
-                static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "offset width");
-                if (run.sink(run.user, sb.first, sb.count, reinterpret_cast<const uint64_t*>(b.h_offsets), b.h_records) != 0)
-                    return fail(ctx, CHGPU_EINVAL, "sink aborted at pair %u", sb.first);
+            // Stream mode: the sub-batch reaches the sink in chunks of whole pairs through two pinned buffers of
+            // kSinkChunkEntries records (32 MiB each, allocated once): no sub-batch-sized pinned allocation stalls the
+            // first launches of a cold run (cudaMallocHost pins ~2.5 GB/s), and chunk i + 1 travels while the sink has chunk i.
+            const unsigned long long* ho = b.h_offsets;
+            auto chunk_end = [&](uint32_t k0) {
+                uint32_t k1 = k0 + 1;
+                while (k1 < sb.count && ho[k1 + 1] - ho[k0] <= kSinkChunkEntries) ++k1;
+                return k1;
+            };
+            auto issue = [&](uint32_t k0, uint32_t k1, int j) -> chgpu_status {
+                const uint64_t cnt = ho[k1] - ho[k0];
+                if (const chgpu_status e = ensure_host_records(ctx, ctx->mb[j], std::max<uint64_t>(cnt, 1))) return e;
+                if (cnt)
+                    CK(cudaMemcpyAsync(ctx->mb[j].h_records, b.d_records + ho[k0], cnt * sizeof(uint4), cudaMemcpyDeviceToHost, ctx->copy));
+                CK(cudaEventRecord(ctx->ev_chunk[j], ctx->copy));
+                return CHGPU_OK;
+            };
+            std::vector<uint64_t> rel;
+            uint32_t k0 = 0, k1 = chunk_end(0);
+            int j = 0;
+            if (const chgpu_status e = issue(k0, k1, j)) return e;
+            while (k0 < sb.count) {
+                const uint32_t n0 = k1, n1 = n0 < sb.count ? chunk_end(n0) : n0;
+                if (n0 < sb.count)
+                    if (const chgpu_status e = issue(n0, n1, j ^ 1)) return e;
+                while (ctx->load_job) {  // (keeps a background load going instead of sleeping on the copy)
+                    const cudaError_t q = cudaEventQuery(ctx->ev_chunk[j]);
+                    if (q == cudaSuccess) break;
+                    if (q != cudaErrorNotReady) CK(q);
+                    load_pump(ctx->load_job, false);
+                    std::this_thread::sleep_for(std::chrono::microseconds(20));
+                }
+                CK(cudaEventSynchronize(ctx->ev_chunk[j]));
+                if (run.sink) {
+                    static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "offset width");
+                    rel.resize(size_t(k1 - k0) + 1);
+                    for (uint32_t i = 0; i <= k1 - k0; ++i) rel[i] = ho[k0 + i] - ho[k0];
+                    if (run.sink(run.user, sb.first + k0, k1 - k0, rel.data(), ctx->mb[j].h_records) != 0)
+                        return fail(ctx, CHGPU_EINVAL, "sink aborted at pair %u", sb.first + k0);
+                }
+                k0 = n0;
+                k1 = n1;
+                j ^= 1;
             }
         }
         delivered_records += total;
@@ -1105,6 +1141,7 @@ chgpu_status chgpu_create(int device, chgpu_ctx** out) {
     ok &= cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) == cudaSuccess;
     ok &= cudaStreamCreateWithFlags(&ctx->load, cudaStreamNonBlocking) == cudaSuccess;
     ok &= cudaEventCreateWithFlags(&ctx->ev_split_jobs, cudaEventDisableTiming) == cudaSuccess;
+    for (cudaEvent_t& e : ctx->ev_chunk) ok &= cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
     ok &= cudaEventCreateWithFlags(&ctx->ev_upload, cudaEventDisableTiming) == cudaSuccess;
     ok &= cudaEventCreateWithFlags(&ctx->ev_compute, cudaEventDisableTiming) == cudaSuccess;
     ok &= cudaEventCreate(&ctx->ev_t0) == cudaSuccess;
@@ -1156,6 +1193,8 @@ void chgpu_destroy(chgpu_ctx* ctx) {
     cudaFreeHost(ctx->h_split_jobs);
     cudaFree(ctx->d_split_jobs);
     if (ctx->ev_split_jobs) cudaEventDestroy(ctx->ev_split_jobs);
+    for (cudaEvent_t e : ctx->ev_chunk)
+        if (e) cudaEventDestroy(e);
     for (auto& b : ctx->load_scratch) cudaFree(b.first);
     cudaFree(ctx->d_planes_t); cudaFree(ctx->d_bias); cudaFree(ctx->d_hnorm); cudaFree(ctx->d_hq);
     cudaFree(ctx->d_hq_count); cudaFree(ctx->d_hstats);
