@@ -574,6 +574,8 @@ chgpu_status chgpu_order_tasks_for_reuse(const chgpu_plan_task* tasks, uint32_t 
 chgpu_status chgpu_shard_tasks(const chgpu_plan_task* tasks, const uint32_t* order, uint32_t ntasks, uint32_t shards,
                                uint32_t* first_out) {
     if ((ntasks && !tasks) || !first_out || shards == 0) return CHGPU_EINVAL;
+    for (uint32_t k = 0; order && k < ntasks; ++k)
+        if (order[k] >= ntasks) return CHGPU_EINVAL;
     std::vector<uint32_t> first;
     shard_sequence(tasks, order, ntasks, shards, first);
     std::copy(first.begin(), first.end(), first_out);
