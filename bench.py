@@ -3,9 +3,12 @@
 
 Workload (BASELINE.json configs[2]): exhaustive matching of 1,000 synthetic images x 8,192
 descriptors = 499,500 pairs, in the reference's plan order (plan_exhaustive, N_p=50, M=4).  One
-STEP = one pass over the whole pair list on one GPU.  With N GPUs every rank owns its own
-1,000-image dataset (seed + rank) and runs the same pass — weak scaling, no data-path collective
-(SURVEY.md §8e); value = N * pairs / max-over-ranks time.
+STEP = one pass over the whole pair list.  With N GPUs (`--gpus N`: bench.py launches the N ranks
+itself, one process per GPU, or runs as one rank of a torchrun launch of the same size) the ONE pair
+list is cut into N contiguous, work-balanced shards (chgpu_shard_pairs_weighted) — strong scaling, no
+data-path collective: every rank uploads and hashes only the images its shard touches,
+the dataset centering is exchanged as 128 u64 sums + a count, value = pairs / max-over-ranks time.
+`--weak` gives every rank its own 1,000-image dataset instead (N independent jobs).
 
     value     device-resident: descriptors, codes and bucket indices already in HBM; timed =
               match kernels + ordered compaction into MatchRecords in device memory
@@ -40,7 +43,7 @@ METRIC = "image pairs matched/sec @8K SIFT/img"
 UNIT = "pairs/s"
 
 
-def parse_args():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
@@ -56,9 +59,9 @@ def parse_args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the baseline sample")
     ap.add_argument("--seed", type=int, default=7)
-    ap.add_argument("--strong", action="store_true",
-                    help="strong scaling: ONE dataset, the pair list sharded over the ranks (default: weak, one dataset per rank)")
-    return ap.parse_args()
+    ap.add_argument("--strong", action="store_true", help="(default for --gpus > 1) ONE dataset, the pair list sharded over the ranks")
+    ap.add_argument("--weak", action="store_true", help="weak scaling: one private dataset per rank (N independent jobs)")
+    return ap.parse_args(argv)
 
 
 def measured_peak_hbm() -> tuple[float, str]:
@@ -238,13 +241,13 @@ def run_reference_arm(args):
     t0 = time.perf_counter()
     total = 0.0
     for _ in range(args.steps):
-        sec, _ = run()
+        sec, _, _ = run()
         total += sec
     wall = time.perf_counter() - t0
     value = info["sample_pairs"] * args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8/u64 popcount + exact integer distances (fp64 ratio test)", "data": "synthetic",
         "config": workload_config(args, len(pairs)),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": info["kind"], "sample": info["sample"]},
@@ -254,60 +257,88 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(args, npairs: int) -> dict:
+def workload_config(args, npairs: int, world: int = 1, strong: bool = True) -> dict:
+    per = (f"{npairs} pairs per step, ONE list sharded over {world} GPUs" if strong and world > 1
+           else f"{npairs} pairs per step per GPU")
     return {
         "workload": f"BASELINE configs[2]: exhaustive matching of {args.images} images x {args.points} descriptors "
-                    f"({npairs} pairs per step per GPU, reference plan order N_p={args.block_images} M={args.blocks_per_group})",
-        "images": args.images, "points_per_image": args.points, "pairs_per_step_per_gpu": npairs,
+                    f"({per}, reference plan order N_p={args.block_images} M={args.blocks_per_group})",
+        "images": args.images, "points_per_image": args.points,
+        "pairs_per_step": npairs if strong else npairs * world, "pairs_per_step_per_gpu": npairs if not strong else None,
         "family": "m=8 L=6 n=128 seed=1", "match": "k=10 tau=40 ratio=0.8 min_cand=2 N_r=3",
-        "synthetic": "uniform u8 descriptors, 30% sigma=8 twins of a shared pool (SURVEY 8d), seed 7 + rank",
+        "synthetic": "uniform u8 descriptors, 30% sigma=8 twins of a shared pool (SURVEY 8d), seed 7" + ("" if strong else " + rank"),
         "l2": "resident working set (1.47 MB/image) is larger than the 126 MB L2; no flush needed",
-        "parallelism": "pair-list sharding, one process per GPU, no collective",
+        "parallelism": ("one process per GPU; the pair list in contiguous work-balanced shards (chgpu_shard_pairs_weighted); "
+                        "no data-path collective; 1 KB centering exchange + timing reductions only"),
     }
+
+
+# Test hook (tests/bench_worker.py): an engine with ch.Matcher's method names and the torch.distributed backend to
+# use with it.  The product path leaves both alone: ch.Matcher on cuda:LOCAL_RANK, NCCL.
+ENGINE_FACTORY = None
+DIST_BACKEND = "nccl"
+
+
+def runs_of(ids) -> list[tuple[int, int]]:
+    """Sorted unique ids as [start, stop) runs of consecutive values (contiguous slices of the pinned dataset)."""
+    ids = np.unique(np.asarray(ids, dtype=np.int64))
+    if len(ids) == 0:
+        return []
+    cut = np.flatnonzero(np.diff(ids) != 1) + 1
+    starts = np.concatenate([[0], cut])
+    stops = np.concatenate([cut, [len(ids)]])
+    return [(int(ids[a]), int(ids[b - 1]) + 1) for a, b in zip(starts, stops)]
 
 
 def run_ours(args):
     rank, local, world = dist_env()
     import torch
     import paper_1805_08995_b200 as ch
+    from paper_1805_08995_b200.sharding import Comm
 
-    if not torch.cuda.is_available():
-        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
-    torch.cuda.set_device(local)
+    gpu = ENGINE_FACTORY is None
+    if gpu:
+        if not torch.cuda.is_available():
+            raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+        if local >= torch.cuda.device_count():
+            raise SystemExit(f"bench.py: rank {rank} wants cuda:{local} but only {torch.cuda.device_count()} device(s) are visible")
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local) if gpu else torch.device("cpu")
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if gpu:
+            dist.init_process_group(DIST_BACKEND, device_id=dev)
+        else:
+            dist.init_process_group(DIST_BACKEND)
+    comm = Comm(rank, world)  # host-side exchange (gloo group): centering sums, per-rank report
+    strong = world > 1 and not args.weak
 
     def barrier():
         if world > 1:
             import torch.distributed as dist
             dist.barrier()
-        torch.cuda.synchronize()
+        if gpu:
+            torch.cuda.synchronize()
 
-    def max_over_ranks(x: float) -> float:
+    def reduce_ranks(x: float, op: str) -> float:
         if world == 1:
             return x
         import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
         return float(t.item())
 
-    def sum_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
-
-    pairs = pair_list(args)
-    if args.strong and world > 1:
-        # one job, sharded: contiguous range of the plan per rank (chgpu_shard_range); every rank keeps the
-        # whole 1.5 GB dataset resident, so centering needs no exchange here (sharding.py has the general form)
-        a, b = ch.shard_range(len(pairs), rank, world)
-        pairs = np.ascontiguousarray(pairs[a:b])
+    all_pairs = pair_list(args)
+    shard_weights = None
+    if strong:
+        # ONE job: contiguous ranges of the plan balanced by work (queries x train points), so a rank keeps the
+        # plan's block locality (assign_workers' round robin, scheduler.cpp:166-173, would hand every rank every block)
+        first, shard_weights = ch.shard_pairs_weighted(all_pairs, np.full(args.images, args.points, np.uint32), world)
+        pairs = np.ascontiguousarray(all_pairs[int(first[rank]):int(first[rank + 1])])
+    else:
+        pairs = all_pairs
     npairs = len(pairs)
-    m = ch.Matcher(local)
+    m = ch.Matcher(local) if gpu else ENGINE_FACTORY(local)
     params = ch.FamilyParams()
     fam = ch.build_hash_family(params)
     m.set_family(fam)
@@ -315,27 +346,44 @@ def run_ours(args):
 
     # host dataset in pinned memory (what a loader thread would fill from CHFT files)
     desc = m.pinned_empty((args.images, args.points, 128), np.uint8)
-    ch.make_dataset(args.images, args.points, seed=args.seed + (0 if args.strong else rank), out=desc)
-    ids = np.arange(args.images, dtype=np.uint32)
+    ch.make_dataset(args.images, args.points, seed=args.seed + (rank if (world > 1 and not strong) else 0), out=desc)
+    needed = np.unique(pairs).astype(np.uint32) if strong else np.arange(args.images, dtype=np.uint32)
+    # centering is a property of the whole dataset (hashing.cpp:52-70): strong-mode ranks sum a contiguous share of
+    # the images each and exchange 128 u64 sums + a count; weak-mode ranks own their whole dataset
+    own_a, own_b = ch.shard_range(args.images, rank, world) if strong else (0, args.images)
+    owned = np.arange(own_a, own_b, dtype=np.uint32)
+    resident = np.union1d(needed, owned).astype(np.uint32)
+    only_centering = np.setdiff1d(owned, needed).astype(np.uint32)
+    h2d_bytes = int(len(resident)) * args.points * 128
 
     def load_and_hash():
-        m.upload_many(ids, desc)
+        for a, b in runs_of(resident):
+            m.upload_many(np.arange(a, b, dtype=np.uint32), desc[a:b])
         m.centering_reset()
-        m.centering_add_many(ids)
-        m.centering_apply()
-        m.hash(ids)
+        m.centering_add_many(owned)
+        if strong:
+            sums, count = m.centering_sums()
+            packed = np.concatenate([np.asarray(sums, np.uint64), np.array([count], np.uint64)])
+            others = comm.sum_u64(packed) - packed
+            m.centering_add_sums(others[:128], int(others[128]))
+        cen = m.centering_apply()
+        if len(only_centering):
+            m.evict_many(only_centering)
+        m.hash(needed)
+        return cen
 
     t0 = time.perf_counter()
-    load_and_hash()
+    centering = load_and_hash()
     m.sync()
     setup_s = time.perf_counter() - t0
 
     # ---- value: device-resident matching pass ------------------------------------------------------
     for _ in range(args.warmup):
         m.match_pairs_device(pairs, cfg)
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local) if gpu else None
     barrier()
-    sampler.start()
+    if sampler:
+        sampler.start()
     t0 = time.perf_counter()
     dev_ms = 0.0
     kern_ms = 0.0
@@ -350,35 +398,37 @@ def run_ours(args):
         match_launches += last["match_launches"]
     barrier()
     wall_s = time.perf_counter() - t0
-    clocks = sampler.stop()
-    dev_ms = max_over_ranks(dev_ms)
-    wall_s = max_over_ranks(wall_s)
+    clocks = sampler.stop() if sampler else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no GPU engine (test stand-in)"]}
+    my_dev_ms = dev_ms
+    dev_ms = reduce_ranks(dev_ms, "max")
+    wall_s = reduce_ranks(wall_s, "max")
     ms_per_step = dev_ms / args.steps
-    total_pairs = sum_over_ranks(float(npairs))  # weak: world x list; strong: the one list
+    total_pairs = reduce_ranks(float(npairs), "sum")  # strong: the one list; weak: world x list
     value = total_pairs / (ms_per_step * 1e-3)
+    total_launches = reduce_ranks(float(launches), "sum")
 
-    # ---- roofline of the match kernel --------------------------------------------------------------
+    # ---- roofline of the match kernel (this rank's launches; rank 0 reports) ----------------------------
     peak, peak_src = measured_peak_hbm()
     alg = algorithmic_bytes(last, params.short_bits, params.table_count)
-    kern_ms_per_step = kern_ms / args.steps
+    kern_ms_per_step = max(kern_ms / args.steps, 1e-9)
     achieved = alg / (kern_ms_per_step * 1e-3) / 1e9
     traffic = recorded_traffic()
     roofline = {
-        "bound": "hbm", "kernel": "match_kernel<SMEM_TRAIN, L=6>", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "bound": "hbm", "kernel": last.get("kernel", "match_kernel<SMEM_TRAIN, L=6>"), "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak, "peak_source": peak_src,
         # dram bytes of one launch of this run's size: the captured launch scaled by its query count
         "traffic": (traffic["dram_bytes_per_launch"] * (last["query_points"] / max(1, last["match_launches"])) /
                     traffic["queries_per_launch"]) if traffic else None,
         "traffic_source": (traffic or {}).get("source"),
-        "algorithmic_bytes_per_pair": alg / npairs,
+        "algorithmic_bytes_per_pair": alg / max(1, npairs),
         "algorithmic_bytes_per_launch": alg / max(1, last["match_launches"]),
         "avg_launch_ms": kern_ms / max(1, match_launches),
-        "kernel_share_of_step": kern_ms / dev_ms if dev_ms else None,
-        "note": "candidate gathers (20 B x R, 88% of the algorithmic bytes) are served from shared memory, "
-                "so frac may exceed 1; see DESIGN.md for the on-chip (POPC / LDS) bounds",
+        "kernel_share_of_step": kern_ms / my_dev_ms if my_dev_ms else None,
+        "note": "candidate gathers (20 B x R, 88% of the algorithmic bytes) are served on chip, "
+                "so frac may exceed 1; see DESIGN.md for the on-chip (POPC / issue / tensor) bounds",
     }
 
-    # on-chip bound of the same kernel: POPC is the one quarter-rate instruction the scan cannot avoid
+    # on-chip bound of the SIMT scan: POPC is the one quarter-rate instruction it cannot avoid
     # (4 per raw candidate, 16 lanes/clk/SM on the XU pipe); DESIGN.md section 4
     props = m.device_props()
     sm_mhz = clocks.get("sm_mhz") or 1965.0
@@ -396,7 +446,8 @@ def run_ours(args):
                            "frac": popc_rate / popc_peak,
                            "peak_source": "measured (profiles/onchip_peaks.json)" if probe else "16 lanes/clk/SM (assumed)",
                            "measured_peaks": probe,
-                           "note": "lower bound on POPC work (padding lanes not counted); ncu pipe utilisations of the "
+                           "note": "Hamming evaluations the reference's algorithm needs (4 POPC-equivalents per raw candidate) "
+                                   "against the XU pipe's POPC peak; ncu pipe utilisations of the "
                                    "committed capture (profiles/r*_match_kernel_ncu_full.json, latest)"}
 
     # the limit the kernel actually runs into: warp-instruction issue slots (4 per clock per SM).  Instructions
@@ -408,8 +459,7 @@ def run_ours(args):
         roofline["on_chip"]["issue"] = {
             "bound": "issue_slots", "warp_instructions_per_query": ipq, "achieved_ginst_s": issue_rate / 1e9,
             "peak_ginst_s": issue_peak / 1e9, "frac": issue_rate / issue_peak,
-            "note": "ncu of the same kernel: issue active 70 %, LSU data pipe 75 %, ALU 61 %, XU 50 % "
-                    f"(profiles/{ipq_src})"}
+            "note": f"instructions per query from the committed ncu capture (profiles/{ipq_src})"}
 
     # ---- e2e: host buffers in, host records out, every step ------------------------------------------
     e2e = None
@@ -434,14 +484,16 @@ def run_ours(args):
             st = e2e_step()
             e2e_launches += st["total_launches"]
         barrier()
-        e2e_s = max_over_ranks(time.perf_counter() - t0) / args.e2e_steps
+        e2e_s = reduce_ranks(time.perf_counter() - t0, "max") / args.e2e_steps
         assert got["records"] == st["matches"]
         e2e = {
             "value": total_pairs / e2e_s, "unit": UNIT,
-            "h2d_bytes_per_step": int(desc.nbytes + npairs * 16),
-            "d2h_bytes_per_step": int(st["matches"] * 16 + (npairs + st["match_launches"]) * 8),
+            "h2d_bytes_per_step": int(reduce_ranks(float(h2d_bytes + npairs * 16), "sum")),
+            "d2h_bytes_per_step": int(reduce_ranks(float(st["matches"] * 16 + (npairs + st["match_launches"]) * 8), "sum")),
             "steps": args.e2e_steps, "ms_per_step": 1e3 * e2e_s,
-            "includes": "H2D descriptors from pinned host, centering sums, hash + bucket build, match, D2H of all MatchRecords to the sink",
+            "includes": "H2D descriptors from pinned host (the images the shard touches), centering sums"
+                        + (" + their 1 KB exchange" if strong else "") +
+                        ", hash + bucket build, match, D2H of all MatchRecords to the sink",
         }
 
     # ---- CPU baseline (rank 0, N=1 only) ----------------------------------------------------------------
@@ -451,26 +503,44 @@ def run_ours(args):
             c = m.codes(i)
             return c.shorts, c.longs
         run, info = cpu_sample(args, pairs, desc, codes_from=gpu_codes)
-        sec, cpu_matches = run()
+        sec, cpu_matches, cpu_checksum = run()
         cpu = {"value": info["sample_pairs"] / sec, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
                "sample": info["sample"], "seconds": sec}
-        # the sample doubles as a parity check: same number of matches on the same pairs
+        # the sample doubles as a parity check at config-3 size: EVERY record of the sample, through the
+        # order-independent checksum the compaction kernel accumulates on the device (not just a match count)
         st = m.match_pairs_device(pairs[: info["sample_pairs"]], cfg)
         cpu["gpu_matches_on_sample"] = st["matches"]
         cpu["cpu_matches_on_sample"] = cpu_matches
-        assert st["matches"] == cpu_matches, "GPU and CPU reference disagree on the sample"
+        cpu["records_checksum_equal"] = bool(st["records_checksum"] == cpu_checksum)
+        cpu["records_checksum"] = f"{cpu_checksum:#018x}"
+        assert st["matches"] == cpu_matches, "GPU and CPU reference disagree on the sample (match count)"
+        assert st["records_checksum"] == cpu_checksum, "GPU and CPU reference disagree on the sample (records checksum)"
 
-    total_matches = sum_over_ranks(float(last["matches"]))
+    total_matches = reduce_ranks(float(last["matches"]), "sum")
+    report = {"rank": rank, "gpu": local, "pairs": npairs, "images_resident": int(len(needed)),
+              "ms_per_step": my_dev_ms / args.steps, "match_kernel_ms_per_step": kern_ms / args.steps,
+              "clocks": clocks, "centering_fingerprint": f"{ch.centering_fingerprint(centering):#018x}"}
+    reports = comm.gather(report)
     if rank == 0:
+        fps = {r["centering_fingerprint"] for r in reports}
+        assert (len(fps) == 1) or not strong, f"ranks disagree on the dataset centering: {fps}"
+        worst = max(reports, key=lambda r: r["ms_per_step"])
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+            "scaling": "strong" if (strong or world == 1) else "weak", "vs_baseline": None,
             "dtype": "u8/u32 popcount + exact integer distances (fp64 ratio test; hashing: fp32 filter + exact fp64 re-evaluation)",
-            "data": "synthetic", "config": workload_config(args, npairs), "roofline": roofline, "cpu_baseline": cpu,
-            "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "data": "synthetic", "config": workload_config(args, len(all_pairs), world, strong or world == 1),
+            "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": int(total_launches), "clocks": worst["clocks"],
             "wall_ms_per_step": 1e3 * wall_s / args.steps, "setup_s": setup_s,
-            "matches_per_step": total_matches, "device": m.device_props()["name"],
+            "matches_per_step": total_matches, "device": props["name"],
+            "ranks": reports,
+            "shard_work": ({"weights": [int(w) for w in shard_weights],
+                            "max_over_min": float(max(shard_weights)) / float(max(1, min(shard_weights)))}
+                           if shard_weights is not None else None),
+            "collectives": ("none on the data path; torch.distributed: barrier + max/sum of scalars "
+                            f"({DIST_BACKEND}), 1 KB centering exchange + per-rank report (gloo, host side)") if world > 1 else "none",
         }
         print(json.dumps(line), flush=True)
     m.close()
@@ -479,13 +549,45 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def main():
-    args = parse_args()
+def free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n: int, argv: list[str], script: str | None = None, check_devices: bool = True) -> int:
+    """`bench.py --gpus N` without a launcher: become the launcher.  One process per GPU through torch.distributed.run
+    (rank r -> cuda:r via LOCAL_RANK), rendezvous on 127.0.0.1.  Fails loudly when the box has fewer than N GPUs."""
+    if check_devices:
+        import torch
+        have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        if have < n:
+            print(f"bench.py: --gpus {n} asked for, {have} CUDA device(s) visible; refusing to time fewer GPUs than reported",
+                  file=sys.stderr)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), script or str(Path(__file__).resolve()), *argv]
+    return subprocess.call(cmd)
+
+
+def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
+    args = parse_args(argv)
+    launched = "WORLD_SIZE" in os.environ
     if args.impl == "reference":
-        run_reference_arm(args)
-    else:
-        run_ours(args)
+        run_reference_arm(args)  # rank 0 alone runs and prints; other ranks of a torchrun launch exit 0 without work
+        return 0
+    if not launched and args.gpus > 1:
+        return spawn_ranks(args.gpus, argv)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but the launcher started {world} rank(s) (WORLD_SIZE); they must agree",
+              file=sys.stderr)
+        return 2
+    run_ours(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -1096,7 +1096,7 @@ inline std::vector<MatchRecord> guided_match_pair(const FeatureSet& fs_i, const 
 }
 
 // Several GPUs of one box from one process: one Matcher (context) and one host thread per lane, the working set
-// replicated on every lane, the pair list cut into contiguous shards of the plan (chgpu_shard_range), results
+// replicated on every lane, the pair list cut into contiguous, work-balanced shards of the plan (chgpu_shard_pairs_weighted), results
 // gathered in pair order on the host.  No device-to-device traffic: pairs are independent.  The
 // reference's counterpart is its W worker threads over one in-memory arena (execute_plan, engine.cpp:667-702);
 // paper_1805_08995_b200/sharding.py is the same protocol with one process per GPU.
@@ -1150,10 +1150,21 @@ public:
         const std::size_t G = lanes_.size();
         std::vector<std::vector<PairMatches>> part(G);
         std::vector<MatchStats> st(G);
+        // contiguous shards of about equal WORK (chgpu_pair_weight: queries x train points), not pair count:
+        // datasets mix 1K- and 32K-point images and a 32K x 32K pair costs ~1000 x a 1K x 1K one
+        std::uint32_t max_id = 0;
+        for (const auto& p : pairs) max_id = std::max({max_id, p.first, p.second});
+        std::vector<std::uint32_t> points(pairs.empty() ? 0 : std::size_t(max_id) + 1, 0);
+        for (const auto& p : pairs)
+            for (const std::uint32_t id : {p.first, p.second})
+                if (points[id] == 0) ck_lane(0, chgpu_image_points(lanes_[0]->handle(), id, &points[id]));
+        std::vector<std::uint64_t> first(G + 1, 0);
+        static_assert(sizeof(std::pair<std::uint32_t, std::uint32_t>) == 8, "pair list is passed as 2 x u32 per pair");
+        ck_lane(0, chgpu_shard_pairs_weighted(reinterpret_cast<const std::uint32_t*>(pairs.data()), pairs.size(), points.data(),
+                                              static_cast<std::uint32_t>(points.size()), static_cast<std::uint32_t>(G),
+                                              first.data(), nullptr));
         each_lane([&](std::size_t k) {
-            std::uint64_t first = 0, last = 0;
-            chgpu_shard_range(pairs.size(), static_cast<std::uint32_t>(k), static_cast<std::uint32_t>(G), &first, &last);
-            part[k] = lanes_[k]->match_pairs(pairs.subspan(first, last - first), cfg, &st[k]);
+            part[k] = lanes_[k]->match_pairs(pairs.subspan(first[k], first[k + 1] - first[k]), cfg, &st[k]);
         });
         std::vector<PairMatches> out;
         out.reserve(pairs.size());

@@ -337,7 +337,17 @@ chgpu_status chgpu_plan_guided(uint32_t image_count, uint32_t block_images, uint
                                const uint32_t* accepted, uint64_t accepted_count, uint32_t* pairs_out, uint64_t* npairs_out);
 /* Shard [0,npairs) for rank `rank` of `world`: contiguous ranges of the plan, so each GPU keeps
  * its train images hot (replaces assign_workers, scheduler.cpp:166-173). */
-void chgpu_shard_range(uint64_t npairs, uint32_t rank, uint32_t world, uint64_t* first, uint64_t* last);
+chgpu_status chgpu_shard_range(uint64_t npairs, uint32_t rank, uint32_t world, uint64_t* first, uint64_t* last);
+/* The work model of one pair for load balancing: queries x (train points + a constant for the per-query
+ * lookup / ranking overhead).  Candidates per query grow linearly with the train image, so a
+ * 32K x 32K pair weighs ~16 x an 8K x 8K pair and ~1000 x a 1K x 1K one; pair COUNT balances only uniform datasets. */
+uint64_t chgpu_pair_weight(uint32_t query_points, uint32_t train_points);
+/* Work-balanced form of chgpu_shard_range for datasets of mixed image sizes: the pair list is cut into `shards`
+ * contiguous ranges of about equal total chgpu_pair_weight.  points_per_image[i] = descriptors of image i
+ * (every index in `pairs` must be < image_count).  first_out: shards + 1 positions; shard s owns
+ * [first_out[s], first_out[s + 1]).  weights_out (nullable, `shards` entries) receives the weight of every shard. */
+chgpu_status chgpu_shard_pairs_weighted(const uint32_t* pairs, uint64_t npairs, const uint32_t* points_per_image,
+                                        uint32_t image_count, uint32_t shards, uint64_t* first_out, uint64_t* weights_out);
 
 /* ---- block-pair tasks, residency schedule, out-of-core run -------------------------------- */
 /* The tasks behind the flat pair lists above (PlanTask, scheduler.hpp:36-43): task t covers pairs
@@ -431,6 +441,12 @@ chgpu_status chgpu_order_tasks_for_reuse(const chgpu_plan_task* tasks, uint32_t 
  * every worker every block).  first_out[s] .. first_out[s + 1] are the positions of worker s; shards + 1 entries. */
 chgpu_status chgpu_shard_tasks(const chgpu_plan_task* tasks, const uint32_t* order /* nullable: plan order */,
                                uint32_t ntasks, uint32_t shards, uint32_t* first_out);
+/* The same cut balanced by WORK instead of pair count: task_weights[t] = sum of chgpu_pair_weight over the pairs of
+ * task t (chgpu_task_weights computes them from the flat pair list the tasks index). */
+chgpu_status chgpu_shard_tasks_weighted(const chgpu_plan_task* tasks, const uint32_t* order /* nullable */, uint32_t ntasks,
+                                        const uint64_t* task_weights, uint32_t shards, uint32_t* first_out);
+chgpu_status chgpu_task_weights(const chgpu_plan_task* tasks, uint32_t ntasks, const uint32_t* pairs, uint64_t npairs,
+                                const uint32_t* points_per_image, uint32_t image_count, uint64_t* task_weights_out);
 /* `shard` of `shards` (0 of 0 or 1: the whole plan): one call per GPU / process, each with its own context. */
 chgpu_status chgpu_match_plan_streamed(chgpu_ctx* ctx, const char* const* paths, uint32_t image_count,
                                        uint32_t block_images, uint32_t blocks_per_group,

@@ -514,9 +514,9 @@ int chor_time_match_pairs(const chor_family_params* p, const chor_match_cfg* cfg
                           const uint8_t* const* desc, const uint32_t* counts,
                           const uint32_t* const* shorts, const uint64_t* const* longs,
                           const uint32_t* pairs, uint32_t npairs, uint32_t threads,
-                          double* seconds, uint64_t* total_matches) {
+                          double* seconds, uint64_t* total_matches, uint64_t* records_checksum) {
     if (threads == 0) return 1;
-    std::vector<uint64_t> per_thread(threads, 0);
+    std::vector<uint64_t> per_thread(threads, 0), per_thread_sum(threads, 0);
     std::vector<int> rc(threads, 0);
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<std::thread> pool;
@@ -532,17 +532,21 @@ int chor_time_match_pairs(const chor_family_params* p, const chor_match_cfg* cfg
                                               nullptr, nullptr);
                 if (r != 0) rc[w] = r;
                 per_thread[w] += n;
+                for (uint32_t i = 0; i < n; ++i)
+                    per_thread_sum[w] += chor_record_checksum(k, rec[i].query_index, rec[i].train_index, rec[i].distance_sq);
             }
         });
     }
     for (auto& t : pool) t.join();
     *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    uint64_t total = 0;
+    uint64_t total = 0, sum = 0;
     for (uint32_t w = 0; w < threads; ++w) {
         total += per_thread[w];
+        sum += per_thread_sum[w];
         if (rc[w] != 0) return rc[w];
     }
     *total_matches = total;
+    if (records_checksum) *records_checksum = sum;
     return 0;
 }
 

@@ -133,12 +133,25 @@ int chor_save_matches(const char* id_i, const char* id_j, const chor_match_recor
 
 /* CPU throughput probe for bench.py: runs match_pair over pairs[2*npairs] of a dataset held as
  * arrays of per-image pointers, on `threads` std::threads each taking a disjoint strided slice
- * (the reference's worker model, engine.cpp:686).  Returns wall seconds and total matches. */
+ * (the reference's worker model, engine.cpp:686).  Returns wall seconds, total matches and (optional) the
+ * order-independent checksum of all records the GPU path's compaction kernel accumulates
+ * (sum over records of mix(mix(k << 32 | query) ^ (train << 32 | d^2)), k = position of the pair in `pairs`,
+ * mix = the splitmix64 finaliser), so a bench sample compares every record, not a count. */
 int chor_time_match_pairs(const chor_family_params* p, const chor_match_cfg* cfg,
                           const uint8_t* const* desc, const uint32_t* counts,
                           const uint32_t* const* shorts, const uint64_t* const* longs,
                           const uint32_t* pairs, uint32_t npairs, uint32_t threads,
-                          double* seconds, uint64_t* total_matches);
+                          double* seconds, uint64_t* total_matches, uint64_t* records_checksum);
+/* The per-record term of that checksum. */
+static inline uint64_t chor_checksum_mix(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+static inline uint64_t chor_record_checksum(uint64_t pair_position, uint32_t query, uint32_t train, double distance_sq) {
+    return chor_checksum_mix(chor_checksum_mix(pair_position << 32 | query) ^ ((uint64_t)train << 32 | (uint64_t)distance_sq));
+}
 
 /* Flattened pair list of plan_exhaustive (scheduler.cpp:99-142) in task order; pairs_out holds
  * image_count*(image_count-1) u32.  task_sizes (optional) receives the pair count of every task,

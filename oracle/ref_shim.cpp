@@ -368,7 +368,7 @@ int chor_time_match_pairs(const chor_family_params* p, const chor_match_cfg* cfg
                           const uint8_t* const* desc, const uint32_t* counts,
                           const uint32_t* const* shorts, const uint64_t* const* longs,
                           const uint32_t* pairs, uint32_t npairs, uint32_t threads,
-                          double* seconds, uint64_t* total_matches) {
+                          double* seconds, uint64_t* total_matches, uint64_t* records_checksum) {
     if (threads == 0) return 1;
     return guarded([&] {
         const FamilyParams fp = to_params(*p);
@@ -387,21 +387,26 @@ int chor_time_match_pairs(const chor_family_params* p, const chor_match_cfg* cfg
             cs[a] = to_codes(fp, shorts[a], longs[a], counts[a]);
             have[a] = 1;
         }
-        std::vector<uint64_t> per_thread(threads, 0);
+        std::vector<uint64_t> per_thread(threads, 0), per_thread_sum(threads, 0);
         const auto t0 = std::chrono::steady_clock::now();
         std::vector<std::thread> pool;
         for (uint32_t w = 0; w < threads; ++w)
             pool.emplace_back([&, w] {
                 for (uint32_t k = w; k < npairs; k += threads) {
                     const uint32_t a = pairs[2 * k], b = pairs[2 * k + 1];
-                    per_thread[w] += match_pair(fs[a], fs[b], cs[a], cs[b], mc).size();
+                    const std::vector<MatchRecord> rec = match_pair(fs[a], fs[b], cs[a], cs[b], mc);
+                    per_thread[w] += rec.size();
+                    for (const MatchRecord& r : rec)  // a few thousand mixes per 80 ms pair: not measurable
+                        per_thread_sum[w] += chor_record_checksum(k, r.query_index, r.train_index, r.distance_sq);
                 }
             });
         for (auto& t : pool) t.join();
         *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        uint64_t total = 0;
+        uint64_t total = 0, sum = 0;
         for (uint64_t v : per_thread) total += v;
+        for (uint64_t v : per_thread_sum) sum += v;
         *total_matches = total;
+        if (records_checksum) *records_checksum = sum;
     });
 }
 

@@ -12,5 +12,6 @@ from .api import (  # noqa: F401
     save_centering_file, save_code_cache, MatchFileSink,
     plan_tasks, hashing_tasks, simulate_residency, auto_partition_sizing, partition_sizing_for_device,
     TASK_DTYPE, ACTION_DTYPE, order_tasks_for_reuse, ORDER_REFERENCE, ORDER_REUSE, shard_tasks,
+    shard_pairs_weighted, task_weights, pair_weight,
 )
 from .synth import make_dataset  # noqa: F401

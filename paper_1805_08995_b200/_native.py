@@ -173,7 +173,9 @@ SIGNATURES = {
     "chgpu_pair_file_name": (None, [C.c_uint32, C.c_uint32, C.c_char_p]),
     "chgpu_plan_exhaustive": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p, u64p]),
     "chgpu_plan_guided": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, u32p, C.c_uint64, u32p, u64p]),
-    "chgpu_shard_range": (None, [C.c_uint64, C.c_uint32, C.c_uint32, u64p, u64p]),
+    "chgpu_shard_range": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, u64p, u64p]),
+    "chgpu_pair_weight": (C.c_uint64, [C.c_uint32, C.c_uint32]),
+    "chgpu_shard_pairs_weighted": (C.c_int, [u32p, C.c_uint64, u32p, C.c_uint32, C.c_uint32, u64p, u64p]),
     "chgpu_plan_tasks": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint64, C.POINTER(PlanTaskC), u32p]),
     "chgpu_hashing_tasks": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(PlanTaskC), u32p]),
     "chgpu_simulate_residency": (C.c_int, [C.POINTER(PlanTaskC), C.c_uint32, C.c_int, C.c_uint32, C.c_uint32,
@@ -183,6 +185,8 @@ SIGNATURES = {
                                                  u32p, u32p]),
     "chgpu_order_tasks_for_reuse": (C.c_int, [C.POINTER(PlanTaskC), C.c_uint32, C.c_uint32, u32p]),
     "chgpu_shard_tasks": (C.c_int, [C.POINTER(PlanTaskC), u32p, C.c_uint32, C.c_uint32, u32p]),
+    "chgpu_shard_tasks_weighted": (C.c_int, [C.POINTER(PlanTaskC), u32p, C.c_uint32, u64p, C.c_uint32, u32p]),
+    "chgpu_task_weights": (C.c_int, [C.POINTER(PlanTaskC), C.c_uint32, u32p, C.c_uint64, u32p, C.c_uint32, u64p]),
     "chgpu_match_plan_streamed": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p), C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                             C.c_uint32, C.c_int, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint64, C.POINTER(MatchCfgC), C.c_uint32, PLAN_SINK_FN,
                                             C.c_void_p, C.POINTER(FileResultC), C.POINTER(StreamedStatsC)]),

@@ -334,13 +334,21 @@ def order_tasks_for_reuse(tasks: np.ndarray, block_slots: int = 3) -> np.ndarray
     return out
 
 
-def shard_tasks(tasks: np.ndarray, shards: int, order=None) -> np.ndarray:
-    """Positions (shards + 1) cutting the executed task sequence into contiguous ranges of about equal pair counts."""
+def shard_tasks(tasks: np.ndarray, shards: int, order=None, weights=None) -> np.ndarray:
+    """Positions (shards + 1) cutting the executed task sequence into contiguous ranges of about equal pair counts,
+    or of about equal work when `weights` (task_weights) is given."""
     t = np.ascontiguousarray(tasks, dtype=TASK_DTYPE)
     o = None if order is None else np.ascontiguousarray(order, dtype=np.uint32)
     out = np.zeros(shards + 1, dtype=np.uint32)
-    st = N.load().chgpu_shard_tasks(t.ctypes.data_as(C.POINTER(N.PlanTaskC)) if len(t) else None,
-                                    None if o is None else o.ctypes.data_as(N.u32p), len(t), shards, out.ctypes.data_as(N.u32p))
+    tp = t.ctypes.data_as(C.POINTER(N.PlanTaskC)) if len(t) else None
+    op = None if o is None else o.ctypes.data_as(N.u32p)
+    if weights is not None:
+        w = np.ascontiguousarray(weights, dtype=np.uint64)
+        if len(w) != len(t):
+            raise ValueError("shard_tasks: one weight per task")
+        st = N.load().chgpu_shard_tasks_weighted(tp, op, len(t), w.ctypes.data_as(N.u64p), shards, out.ctypes.data_as(N.u32p))
+    else:
+        st = N.load().chgpu_shard_tasks(tp, op, len(t), shards, out.ctypes.data_as(N.u32p))
     if st != N.OK:
         _raise(st, "shard_tasks: shards must be >= 1")
     return out
@@ -363,8 +371,43 @@ def partition_sizing_for_device(device_image_bytes: int, file_image_bytes: int, 
 
 def shard_range(npairs: int, rank: int, world: int) -> tuple[int, int]:
     a, b = C.c_uint64(0), C.c_uint64(0)
-    N.load().chgpu_shard_range(npairs, rank, world, C.byref(a), C.byref(b))
+    st = N.load().chgpu_shard_range(npairs, rank, world, C.byref(a), C.byref(b))
+    if st != N.OK:
+        _raise(st, f"shard_range: rank {rank} is not below world {world}")
     return a.value, b.value
+
+
+def pair_weight(query_points: int, train_points: int) -> int:
+    """The work model of one pair that the weighted sharding balances (chgpu_pair_weight)."""
+    return int(N.load().chgpu_pair_weight(query_points, train_points))
+
+
+def shard_pairs_weighted(pairs: np.ndarray, points_per_image, shards: int) -> tuple[np.ndarray, np.ndarray]:
+    """Work-balanced contiguous cut of a pair list for datasets of mixed image sizes: (first[shards + 1],
+    weight per shard).  Shard s owns pairs[first[s]:first[s + 1]]."""
+    pr = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
+    pts = np.ascontiguousarray(points_per_image, dtype=np.uint32)
+    first = np.zeros(shards + 1, dtype=np.uint64)
+    weights = np.zeros(max(shards, 1), dtype=np.uint64)
+    st = N.load().chgpu_shard_pairs_weighted(pr.ctypes.data_as(N.u32p) if len(pr) else None, len(pr), pts.ctypes.data_as(N.u32p),
+                                             len(pts), shards, first.ctypes.data_as(N.u64p), weights.ctypes.data_as(N.u64p))
+    if st != N.OK:
+        _raise(st, "shard_pairs_weighted: shards must be >= 1 and every pair index below len(points_per_image)")
+    return first, weights
+
+
+def task_weights(tasks: np.ndarray, pairs: np.ndarray, points_per_image) -> np.ndarray:
+    """Work per plan task: sum of pair_weight over the task's pairs of the flat list the tasks index."""
+    t = np.ascontiguousarray(tasks, dtype=TASK_DTYPE)
+    pr = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
+    pts = np.ascontiguousarray(points_per_image, dtype=np.uint32)
+    out = np.zeros(len(t), dtype=np.uint64)
+    st = N.load().chgpu_task_weights(t.ctypes.data_as(C.POINTER(N.PlanTaskC)) if len(t) else None, len(t),
+                                     pr.ctypes.data_as(N.u32p) if len(pr) else None, len(pr), pts.ctypes.data_as(N.u32p), len(pts),
+                                     out.ctypes.data_as(N.u64p))
+    if st != N.OK:
+        _raise(st, "task_weights")
+    return out
 
 
 class Matcher:

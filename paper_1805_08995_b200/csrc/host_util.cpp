@@ -463,12 +463,58 @@ chgpu_status chgpu_load_centering_file(const char* path, chgpu_family_params* p,
     return CHGPU_OK;
 }
 
-void chgpu_shard_range(uint64_t npairs, uint32_t rank, uint32_t world, uint64_t* first, uint64_t* last) {
+chgpu_status chgpu_shard_range(uint64_t npairs, uint32_t rank, uint32_t world, uint64_t* first, uint64_t* last) {
+    if (!first || !last) return CHGPU_EINVAL;
     if (world == 0) world = 1;
+    if (rank >= world) {
+        *first = *last = npairs;
+        return CHGPU_EINVAL;
+    }
     const uint64_t base = npairs / world, rem = npairs % world;
     const uint64_t f = uint64_t(rank) * base + std::min<uint64_t>(rank, rem);
     *first = f;
     *last = f + base + (rank < rem ? 1 : 0);
+    return CHGPU_OK;
+}
+
+uint64_t chgpu_pair_weight(uint32_t query_points, uint32_t train_points) {
+    return uint64_t(query_points) * (uint64_t(train_points) + 512u);
+}
+
+chgpu_status chgpu_shard_pairs_weighted(const uint32_t* pairs, uint64_t npairs, const uint32_t* points_per_image,
+                                        uint32_t image_count, uint32_t shards, uint64_t* first_out, uint64_t* weights_out) {
+    if ((npairs && !pairs) || !points_per_image || !first_out || shards == 0) return CHGPU_EINVAL;
+    for (uint64_t k = 0; k < 2 * npairs; ++k)
+        if (pairs[k] >= image_count) return CHGPU_EINVAL;
+    // 128-bit products: a Rome16K-sized list of 32K-point images sums to ~2^59 before the multiplication by `shards`
+    unsigned __int128 total = 0;
+    for (uint64_t k = 0; k < npairs; ++k) total += chgpu_pair_weight(points_per_image[pairs[2 * k]], points_per_image[pairs[2 * k + 1]]);
+    for (uint32_t s = 0; s <= shards; ++s) first_out[s] = npairs;
+    first_out[0] = 0;
+    unsigned __int128 acc = 0;
+    uint32_t s = 1;
+    for (uint64_t k = 0; k < npairs && s < shards; ++k) {
+        const uint64_t w = chgpu_pair_weight(points_per_image[pairs[2 * k]], points_per_image[pairs[2 * k + 1]]);
+        // cut in front of the pair that would carry the shard past its share, unless stopping short is the worse miss
+        const unsigned __int128 target = total * s;
+        if ((acc + w) * shards > target) {
+            const unsigned __int128 over = (acc + w) * shards - target, under = target - acc * shards;
+            if (acc * shards >= target || over > under) {
+                first_out[s++] = k;
+                --k;  // the same pair is looked at again for the next boundary
+                continue;
+            }
+        }
+        acc += w;
+    }
+    if (weights_out)
+        for (uint32_t r = 0; r < shards; ++r) {
+            uint64_t w = 0;
+            for (uint64_t k = first_out[r]; k < first_out[r + 1]; ++k)
+                w += chgpu_pair_weight(points_per_image[pairs[2 * k]], points_per_image[pairs[2 * k + 1]]);
+            weights_out[r] = w;
+        }
+    return CHGPU_OK;
 }
 
 }  // extern "C"

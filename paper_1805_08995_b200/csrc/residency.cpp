@@ -315,16 +315,33 @@ void order_for_reuse(const chgpu_plan_task* tasks, uint32_t n, uint32_t slots, s
 }
 
 // Contiguous ranges of the executed sequence, balanced by pair count: worker s gets positions [first[s], first[s + 1]).
-void shard_sequence(const chgpu_plan_task* tasks, const uint32_t* order, uint32_t n, uint32_t shards, std::vector<uint32_t>& first) {
+// `weights` (nullable): work per task (chgpu_task_weights) instead of its pair count.
+void shard_sequence(const chgpu_plan_task* tasks, const uint32_t* order, uint32_t n, uint32_t shards, std::vector<uint32_t>& first,
+                    const uint64_t* weights = nullptr) {
     shards = std::max<uint32_t>(1, shards);
-    uint64_t total = 0;
-    for (uint32_t k = 0; k < n; ++k) total += tasks[order ? order[k] : k].npairs;
+    auto weight = [&](uint32_t k) -> uint64_t {
+        const uint32_t t = order ? order[k] : k;
+        return weights ? weights[t] : tasks[t].npairs;
+    };
+    unsigned __int128 total = 0;
+    for (uint32_t k = 0; k < n; ++k) total += weight(k);
     first.assign(shards + 1, n);
     first[0] = 0;
-    uint64_t acc = 0;
+    unsigned __int128 acc = 0;
     uint32_t s = 1;
     for (uint32_t k = 0; k < n && s < shards; ++k) {
-        acc += tasks[order ? order[k] : k].npairs;
+        const unsigned __int128 w = weight(k);
+        if (weights) {
+            // weighted: tasks differ by orders of magnitude, so a boundary goes to whichever side of task k misses the
+            // worker's share by less
+            while (s < shards && (acc + w) * shards >= total * s) {
+                const unsigned __int128 target = total * s, before = acc * shards, after = (acc + w) * shards;
+                first[s++] = (before >= target || target - before < after - target) ? k : k + 1;
+            }
+            acc += w;
+            continue;
+        }
+        acc += w;
         // the boundary after position k belongs to every worker whose share of the pairs is complete by now
         while (s < shards && acc * shards >= total * s) first[s++] = k + 1;
     }
@@ -579,6 +596,33 @@ chgpu_status chgpu_shard_tasks(const chgpu_plan_task* tasks, const uint32_t* ord
     std::vector<uint32_t> first;
     shard_sequence(tasks, order, ntasks, shards, first);
     std::copy(first.begin(), first.end(), first_out);
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_shard_tasks_weighted(const chgpu_plan_task* tasks, const uint32_t* order, uint32_t ntasks,
+                                        const uint64_t* task_weights, uint32_t shards, uint32_t* first_out) {
+    if ((ntasks && (!tasks || !task_weights)) || !first_out || shards == 0) return CHGPU_EINVAL;
+    for (uint32_t k = 0; order && k < ntasks; ++k)
+        if (order[k] >= ntasks) return CHGPU_EINVAL;
+    std::vector<uint32_t> first;
+    shard_sequence(tasks, order, ntasks, shards, first, task_weights);
+    std::copy(first.begin(), first.end(), first_out);
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_task_weights(const chgpu_plan_task* tasks, uint32_t ntasks, const uint32_t* pairs, uint64_t npairs,
+                                const uint32_t* points_per_image, uint32_t image_count, uint64_t* task_weights_out) {
+    if ((ntasks && (!tasks || !task_weights_out)) || (npairs && !pairs) || !points_per_image) return CHGPU_EINVAL;
+    for (uint32_t t = 0; t < ntasks; ++t) {
+        if (tasks[t].first_pair + tasks[t].npairs > npairs) return CHGPU_EINVAL;
+        uint64_t w = 0;
+        for (uint64_t k = tasks[t].first_pair; k < tasks[t].first_pair + tasks[t].npairs; ++k) {
+            const uint32_t a = pairs[2 * k], b = pairs[2 * k + 1];
+            if (a >= image_count || b >= image_count) return CHGPU_EINVAL;
+            w += chgpu_pair_weight(points_per_image[a], points_per_image[b]);
+        }
+        task_weights_out[t] = w;
+    }
     return CHGPU_OK;
 }
 

@@ -63,7 +63,7 @@ class Oracle:
             "chor_brute_force_match": [P, U32, P, U32, D, P, P],
             "chor_guided_match_pair": [P, P, P, P, U32, P, P, P, P, U32, P, P, P, D, P, P, P, P, P],
             "chor_save_matches": [C.c_char_p, C.c_char_p, P, U32, C.c_char_p],
-            "chor_time_match_pairs": [P, P, P, P, P, P, P, U32, U32, P, P],
+            "chor_time_match_pairs": [P, P, P, P, P, P, P, U32, U32, P, P, P],
             "chor_plan_exhaustive": [U32, U32, U32, P, P, P, P],
             "chor_plan_guided": [U32, U32, U32, P, C.c_uint64, P, P, P, P],
             "chor_plan_task_blocks": [U32, U32, U32, C.c_int, P, C.c_uint64, P, P],
@@ -301,7 +301,8 @@ class Oracle:
         return a.value, b.value
 
     def time_match_pairs(self, params, cfg, descs, shorts, longs, pairs, threads: int):
-        """descs/shorts/longs: lists of per-image arrays.  Returns (seconds, total matches)."""
+        """descs/shorts/longs: lists of per-image arrays.  Returns (seconds, total matches, records checksum):
+        the checksum is the order-independent one the GPU compaction kernel reports (stats["records_checksum"])."""
         p, c = self._fp(params), self._cfg(cfg)
         k = len(descs)
         keep = []
@@ -319,10 +320,11 @@ class Oracle:
         pr = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)
         sec = C.c_double(0)
         tot = C.c_uint64(0)
+        csum = C.c_uint64(0)
         self._check(self.lib.chor_time_match_pairs(C.byref(p), C.byref(c), dptr, counts.ctypes.data, sptr, lptr,
-                                                   pr.ctypes.data, len(pr), threads, C.byref(sec), C.byref(tot)),
+                                                   pr.ctypes.data, len(pr), threads, C.byref(sec), C.byref(tot), C.byref(csum)),
                     "time_match_pairs")
-        return sec.value, tot.value
+        return sec.value, tot.value, csum.value
 
 
 def restatement() -> Oracle:

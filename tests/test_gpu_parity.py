@@ -516,6 +516,37 @@ def test_config2_properties_full_size(matcher, default_family):
     assert len(ab & ba) > 0.9 * min(len(ab), len(ba))
 
 
+def test_config2_full_size_records_equal_the_oracle(matcher, oracle, default_family):
+    """BASELINE config 2 at full size against the ORACLE: all 4,950 pairs of 100 x 4,096 descriptors are matched by the CPU
+    reference (all host threads) and every record is compared through the order-independent checksum the compaction
+    kernel accumulates on the device — pair position, query, train index and distance of all ~6 M records."""
+    import os
+    fresh(matcher, default_family)
+    k, n = 100, 4096
+    d = make_dataset(k, n, seed=7)
+    ids = np.arange(BASE, BASE + k, dtype=np.uint32)
+    matcher.upload_many(ids, np.ascontiguousarray(d))
+    matcher.centering_reset()
+    matcher.centering_add_many(ids)
+    cen = matcher.centering_apply()
+    matcher.hash(ids)
+    codes = [matcher.codes(int(i)) for i in ids]
+    p = default_family.params
+    for i in (0, 37, 99):  # the device codes the oracle run is fed are the oracle's own (bit-exact hash build)
+        s, l = oracle.compute_codes(p, default_family.short_planes, default_family.long_planes, cen, d[i])
+        assert np.array_equal(codes[i].shorts, s) and np.array_equal(codes[i].longs, l)
+    pairs = ch.plan_exhaustive(k, 10, 4)
+    cfg = ch.MatchConfig()
+    sec, cpu_matches, cpu_checksum = oracle.time_match_pairs(p, cfg, [d[i] for i in range(k)], [c.shorts for c in codes],
+                                                              [c.longs for c in codes], pairs, os.cpu_count() or 1)
+    st = matcher.match_pairs_device(pairs + BASE, cfg)
+    assert st["pairs"] == 4950 and st["matches"] == cpu_matches
+    assert st["records_checksum"] == cpu_checksum
+    # and the host delivery of the same run carries the same records
+    offs, rec, _ = matcher.match_pairs(pairs + BASE, cfg)
+    assert host_checksum(offs, rec) == cpu_checksum
+
+
 def test_save_matches_from_device_results(matcher, oracle, default_family, tmp_path):
     fresh(matcher, default_family)
     d = make_dataset(2, 500, seed=101)

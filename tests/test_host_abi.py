@@ -147,3 +147,46 @@ def test_save_matches_is_byte_identical(golden, restatement):
             ch.save_matches("x", "y", odd, Path(td) / "no_such_dir" / "f.txt")
     assert ch.pair_file_name(3, 41) == "match_000003_000041.txt"      # engine.cpp:724-728
     assert ch.pair_file_name(1234567, 2) == "match_1234567_000002.txt"
+
+
+# ---- work-balanced sharding (datasets of mixed image sizes) -------------------------------------------
+def test_weighted_sharding_balances_work_not_pair_count():
+    rng = np.random.default_rng(5)
+    images = 240
+    points = rng.choice(np.array([1024, 8192, 32768], dtype=np.uint32), size=images, p=[0.5, 0.4, 0.1])
+    pairs = ch.plan_exhaustive(images, 16, 3)
+    w = np.array([ch.pair_weight(int(points[a]), int(points[b])) for a, b in pairs], dtype=np.uint64)
+    for shards in (2, 3, 4, 8):
+        first, weights = ch.shard_pairs_weighted(pairs, points, shards)
+        assert first[0] == 0 and first[-1] == len(pairs) and np.all(np.diff(first.astype(np.int64)) >= 0)
+        mine = [int(w[int(first[s]):int(first[s + 1])].sum()) for s in range(shards)]
+        assert mine == [int(x) for x in weights] and sum(mine) == int(w.sum())
+        assert max(mine) / min(mine) <= 1.05, (shards, mine)
+        # the pair-count split of the same list is far from balanced on this dataset
+        by_count = [int(w[a:b].sum()) for a, b in (ch.shard_range(len(pairs), r, shards) for r in range(shards))]
+        assert max(by_count) / min(by_count) > max(mine) / min(mine)
+    # tasks: the same balance one level up (out-of-core runs shard the task sequence)
+    tasks = ch.plan_tasks(images, 16, 3)
+    tw = ch.task_weights(tasks, pairs, points)
+    assert int(tw.sum()) == int(w.sum())
+    for shards in (2, 4):
+        cut = ch.shard_tasks(tasks, shards, weights=tw)
+        work = [int(tw[int(cut[s]):int(cut[s + 1])].sum()) for s in range(shards)]
+        plain = ch.shard_tasks(tasks, shards)
+        plain_work = [int(tw[int(plain[s]):int(plain[s + 1])].sum()) for s in range(shards)]
+        assert max(work) / min(work) <= max(plain_work) / min(plain_work) + 1e-9
+    # uniform datasets: identical to the pair-count split up to one pair
+    first, _ = ch.shard_pairs_weighted(pairs, np.full(images, 4096, np.uint32), 4)
+    for r in range(4):
+        a, b = ch.shard_range(len(pairs), r, 4)
+        assert abs(int(first[r]) - a) <= 1 and abs(int(first[r + 1]) - b) <= 1
+
+
+def test_shard_arguments_are_validated():
+    with pytest.raises(ValueError):
+        ch.shard_range(10, 3, 3)  # rank must be below world
+    with pytest.raises(ValueError):
+        ch.shard_pairs_weighted(np.array([[0, 5]], np.uint32), np.array([10, 10], np.uint32), 2)  # index beyond the image table
+    with pytest.raises(ValueError):
+        ch.shard_pairs_weighted(np.array([[0, 1]], np.uint32), np.array([10, 10], np.uint32), 0)
+    assert ch.shard_range(10, 0, 1) == (0, 10)

@@ -376,3 +376,37 @@ def test_guided_restatement_equals_reference(restatement, reference):
             assert np.array_equal(a[2][q, :a[3][q]], b[2][q, :b[3][q]])
         sizes.append(len(a[0]))
     assert sizes[0] == len(base) == sizes[4] and sizes[3] == 0 and 0 < sizes[1] < sizes[0]
+
+
+# ---- the order-independent records checksum (bench.py's and the full-size GPU tests' comparison) ------------
+def _mix64(x):
+    x = (x + np.uint64(0x9e3779b97f4a7c15))
+    x = (x ^ (x >> np.uint64(30))) * np.uint64(0xbf58476d1ce4e5b9)
+    x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94d049bb133111eb)
+    return x ^ (x >> np.uint64(31))
+
+
+@pytest.mark.parametrize("which", ["restatement", "reference"])
+def test_time_match_pairs_checksum_is_the_device_checksum_definition(which, request):
+    """chor_time_match_pairs' checksum, from both oracles, equals the formula compact_kernel implements
+    (compact_kernels.cuh; tests/test_gpu_parity.py::host_checksum) evaluated over match_pair's own records."""
+    import paper_1805_08995_b200 as ch
+    orc = request.getfixturevalue(which)
+    fam = ch.build_hash_family(FamilyParams())
+    d = make_dataset(5, 700, seed=23)
+    cen = orc.centering([d[i] for i in range(5)])
+    codes = [orc.compute_codes(fam.params, fam.short_planes, fam.long_planes, cen, d[i]) for i in range(5)]
+    pairs = ch.plan_exhaustive(5, 2, 2)
+    cfg = MatchConfig()
+    want, total = np.uint64(0), 0
+    with np.errstate(over="ignore"):
+        for k, (a, b) in enumerate(pairs):
+            rec, _ = orc.match_pair(fam.params, cfg, d[a], *codes[a], d[b], *codes[b])
+            total += len(rec)
+            ka = (np.uint64(k) << np.uint64(32)) | rec["query_index"].astype(np.uint64)
+            kb = (rec["train_index"].astype(np.uint64) << np.uint64(32)) | rec["distance_sq"].astype(np.uint64)
+            want = want + np.sum(_mix64(_mix64(ka) ^ kb), dtype=np.uint64)
+    for threads in (1, 3):
+        sec, n, csum = orc.time_match_pairs(fam.params, cfg, [d[i] for i in range(5)], [c[0] for c in codes],
+                                            [c[1] for c in codes], pairs, threads)
+        assert n == total > 0 and csum == int(want) and sec > 0
