@@ -526,6 +526,7 @@ def test_config2_full_size_records_equal_the_oracle(matcher, oracle, default_fam
     d = make_dataset(k, n, seed=7)
     ids = np.arange(BASE, BASE + k, dtype=np.uint32)
     matcher.upload_many(ids, np.ascontiguousarray(d))
+    matcher._test_ids.update(int(i) for i in ids)
     matcher.centering_reset()
     matcher.centering_add_many(ids)
     cen = matcher.centering_apply()
