@@ -33,9 +33,10 @@
 //                        a warp-wide REDUX.MIN picks the winner.  The threshold tau and the
 //                        re-rank fallback (matcher.cpp:176-189) only decide where the pulling
 //                        stops, so no histogram has to be stored.
-//   4. verification    : 2 lanes per candidate row, __vabsdiffu4 + __dp4a (exact u32 squared
-//                        distance), best / second with rank-order tie-break, Lowe ratio in
-//                        fp64 exactly as matcher.cpp:115-137.
+//   4. verification    : 7 candidate rows and the query row as one 8 x 128 u8 matrix, its Gram
+//                        matrix on the integer tensor-core path (mma.sync m16n8k16 u8, exact s32):
+//                        |t - q|^2 = G[r][r] - 2 G[r][q] + G[q][q]; best / second with rank-order
+//                        tie-break, Lowe ratio in fp64 exactly as matcher.cpp:115-137.
 //
 // Results go to a per-query scratch (train id, d^2); compact_kernel (compact_kernels.cuh) turns
 // them into the reference's MatchRecord stream, ascending query index inside every pair.
@@ -316,7 +317,8 @@ __device__ __forceinline__ uint32_t band_filter(uint32_t key, const EpiLine& l, 
     return d > band_px ? kNone : key;
 }
 
-// Verification of a ranked list (euclidean_verify, matcher.cpp:115-137): lane r holds the r-th ranked key
+#ifdef CHGPU_VERIFY_SIMT
+// SIMT form of the verification (A/B switch -DCHGPU_VERIFY_SIMT; the default is the tensor-core form below): lane r holds the r-th ranked key
 // (id in the low 24 bits), n >= 2 entries.  kVerifyLanes lanes per candidate row (128 / kVerifyLanes bytes
 // each), 32 / kVerifyLanes rows per round; exact u32 squared distances; best = smallest d^2 with ties to the
 // earlier rank (strict '<' in the reference loop); Lowe ratio in fp64 with the reference's operand order.
@@ -358,6 +360,85 @@ __device__ __forceinline__ bool verify_ranked(const uint8_t* __restrict__ desc_i
     }
     return false;
 }
+#else
+// One tensor-core step of the verification: D(16x8, s32) += A(16x16, u8, row) * B(16x8, u8, col)
+// (warp-level mma.sync; SASS IMMA.16816.U8.U8).
+__device__ __forceinline__ void mma_u8_16816(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+    asm("mma.sync.aligned.m16n8k16.row.col.s32.u8.u8.s32 {%0, %1, %2, %3}, {%4, %5}, {%6}, {%0, %1, %2, %3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a0), "r"(a1), "r"(b0));
+}
+// Gram matrix of 8 descriptor rows, one row per fragment group g, thread t of the group holding bytes [32 t, 32 t + 32)
+// of its row as two LDG.128 results.  The fragment registers of mma.sync are taken as loaded (no repacking): an A
+// pair (a0 | a1) is an even / odd word pair of ONE row, so fragment row g is the row's even words E_g and fragment
+// row g + 8 its odd words O_g; with B = the even word the upper half of D accumulates E_g . E_c, with B = the odd word
+// the lower half accumulates O_g . O_c (the other halves are mixed products nobody reads).  The K order is free as
+// long as A and B agree.  After the 8 steps  G[g][c] = e[c & 1] + o[2 + (c & 1)]  in thread t == c >> 1.
+__device__ __forceinline__ void gram8_u8(int (&e)[4], int (&o)[4], const uint4& x0, const uint4& x1) {
+    mma_u8_16816(e, x0.x, x0.y, x0.x);
+    mma_u8_16816(o, x0.x, x0.y, x0.y);
+    mma_u8_16816(e, x0.z, x0.w, x0.z);
+    mma_u8_16816(o, x0.z, x0.w, x0.w);
+    mma_u8_16816(e, x1.x, x1.y, x1.x);
+    mma_u8_16816(o, x1.x, x1.y, x1.y);
+    mma_u8_16816(e, x1.z, x1.w, x1.z);
+    mma_u8_16816(o, x1.z, x1.w, x1.w);
+}
+
+// Verification of a ranked list (euclidean_verify, matcher.cpp:115-137): lane r holds the r-th ranked key
+// (id in the low 24 bits), n >= 2 entries.  Exact u32 squared distances; best = smallest d^2 with ties to the
+// earlier rank (strict '<' in the reference loop); Lowe ratio in fp64 with the reference's operand order.
+//
+// The distances come from the integer tensor-core path: 7 candidate rows and the query row (row 7) form an
+// 8 x 128 u8 matrix X; its Gram matrix G = X X^T (u8 x u8 -> s32, every product and sum exact) holds all three
+// terms of |x_r - q|^2 = G[r][r] - 2 G[r][7] + G[7][7].  Two such tiles (14 candidates) per round, their four
+// row loads per thread in flight together.  The thread that holds G[r][r] (t == r >> 1) fetches G[r][7] from
+// thread 3 of its group and keeps (d^2 << 8 | rank) of its candidates; best and second come out of two
+// warp-wide minima over those, so the distances never have to be moved to "their" lane.
+__device__ __forceinline__ bool verify_ranked(const uint8_t* __restrict__ desc_i, const uint8_t* __restrict__ desc_j,
+                                              uint32_t q, uint32_t n, uint32_t mykey, uint32_t lane, double ratio_sq,
+                                              uint32_t& out_t, uint32_t& out_d) {
+    constexpr uint32_t FULL = 0xffffffffu;
+    const uint32_t g = lane >> 2, t = lane & 3;  // fragment coordinates: row of the tile, 32-byte slice of the row
+    const uint4* __restrict__ qrow = reinterpret_cast<const uint4*>(desc_i + uint64_t(q) * kDim) + t * 2;
+    const bool own = g != 7 && t == (g >> 1);  // this thread receives G[g][g] of both tiles
+    uint32_t m1 = kNone, m2 = kNone;           // smallest and second smallest (d^2 << 8 | rank) seen by this thread
+    for (uint32_t j0 = 0; j0 < n; j0 += 14) {
+        // tile A: candidates j0 .. j0 + 6, tile B: j0 + 7 .. j0 + 13 (past the end: the last one again)
+        const uint32_t ra = j0 + g, rb = ra + 7;
+        const uint32_t ia = __shfl_sync(FULL, mykey, min(ra, n - 1)) & 0xffffffu;
+        const uint32_t ib = __shfl_sync(FULL, mykey, min(rb, n - 1)) & 0xffffffu;
+        const uint4* __restrict__ pa = g == 7 ? qrow : reinterpret_cast<const uint4*>(desc_j + uint64_t(ia) * kDim) + t * 2;
+        const uint4* __restrict__ pb = g == 7 ? qrow : reinterpret_cast<const uint4*>(desc_j + uint64_t(ib) * kDim) + t * 2;
+        const uint4 a0 = __ldg(pa), a1 = __ldg(pa + 1), b0 = __ldg(pb), b1 = __ldg(pb + 1);
+        int ea[4] = {0, 0, 0, 0}, oa[4] = {0, 0, 0, 0}, eb[4] = {0, 0, 0, 0}, ob[4] = {0, 0, 0, 0};
+        gram8_u8(ea, oa, a0, a1);
+        gram8_u8(eb, ob, b0, b1);
+        const int a_even = ea[0] + oa[2], a_odd = ea[1] + oa[3];  // G_A[g][2t], G_A[g][2t+1]
+        const int b_even = eb[0] + ob[2], b_odd = eb[1] + ob[3];
+        const int cross_a = __shfl_sync(FULL, a_odd, lane | 3u), cross_b = __shfl_sync(FULL, b_odd, lane | 3u);  // G[g][7]
+        const int qq = __shfl_sync(FULL, a_odd, 31);                                                             // G[7][7]
+        const int diag_a = (g & 1) ? a_odd : a_even, diag_b = (g & 1) ? b_odd : b_even;
+        const uint32_t da = uint32_t(diag_a + qq - 2 * cross_a), db = uint32_t(diag_b + qq - 2 * cross_b);
+        const uint32_t pka = (own && ra < n) ? ((da << 8) | ra) : kNone;
+        const uint32_t pkb = (own && rb < n) ? ((db << 8) | rb) : kNone;
+        m2 = min(m2, max(m1, pka));
+        m1 = min(m1, pka);
+        m2 = min(m2, max(m1, pkb));
+        m1 = min(m1, pkb);
+    }
+    const uint32_t bestp = __reduce_min_sync(FULL, m1);
+    const uint32_t secondp = __reduce_min_sync(FULL, m1 == bestp ? m2 : m1);
+    const uint32_t bl = bestp & 0xffu, best = bestp >> 8, second = secondp >> 8;
+    const uint32_t bid = __shfl_sync(FULL, mykey, bl) & 0xffffffu;
+    if (second != 0u && double(best) < __dmul_rn(ratio_sq, double(second))) {
+        out_t = bid;
+        out_d = best;
+        return true;
+    }
+    return false;
+}
+#endif
 
 // LT = number of table slots unrolled in registers (>= L); EXACT: L == LT, no per-table guards;
 // GUIDED: the epipolar band filter above is applied to every candidate.
@@ -384,6 +465,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
     asm volatile("" : "+r"(s_stage));
     constexpr uint32_t kRec = stage_record_bytes(LT), kAdj = 32u + uint32_t(LT) * 8u;
     const uint32_t le_mask = (2u << lane) - 1u;  // lanes <= this one
+    const bool dbg = MODE == kModeMatch && P.dbg_ranked != nullptr;  // parity tests only: one predicate, not a pointer test per query
 
     if (SMEM_TRAIN && tid == 0) {
         mbar_init(&s_bar, 1);
@@ -684,7 +766,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     if (MODE == kModeTileMin && lane == 0) atomicOr(P.gdone + pd.res_off + q, 1ull << pd.tile_idx);
                 }
 
-                if (MODE == kModeMatch && P.dbg_ranked != nullptr) {
+                if (dbg) {
                     if (lane < n) P.dbg_ranked[uint64_t(q) * P.top_k + lane] = mykey & 0xffffffu;
                     if (lane == 0) P.dbg_count[q] = n;
                 }
