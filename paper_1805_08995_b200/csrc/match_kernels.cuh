@@ -643,9 +643,15 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                         for (int t = 0; t < LT; ++t)
                             if (hdr.x & (0x100u << t)) key[t] = kNone;
                     }
-#pragma unroll
-                    for (int s = 0; s < kOverSlots; ++s)
-                        if (uint32_t(s) * 32u < tover) key[LT + s] = key_of<SMEM_TRAIN>(key[LT + s], ql, s_long, J.longs);
+                    // nested: half of the queries have at most one overflow step and leave through one branch
+                    if (tover != 0) {
+                        key[LT] = key_of<SMEM_TRAIN>(key[LT], ql, s_long, J.longs);
+                        if (kOverSlots > 1 && tover > 32u) {
+                            key[LT + 1] = key_of<SMEM_TRAIN>(key[LT + 1], ql, s_long, J.longs);
+                            if (kOverSlots > 2 && tover > 64u)
+                                key[LT + kOverSlots - 1] = key_of<SMEM_TRAIN>(key[LT + kOverSlots - 1], ql, s_long, J.longs);
+                        }
+                    }
                     // ---- 3. ranking: pull straight out of the slots -------------------------------
                     uint32_t k0 = first_key(key, kNone);
                     if (GUIDED && (MODE == kModeTileTopK || (k0 >> 24) <= P.tau)) {
