@@ -641,6 +641,7 @@ cudaError_t launch_match(chgpu_ctx* ctx, MatchParams& P, bool smem_train, uint32
     P.smem_long_bytes = smem_train ? std::max<uint32_t>(max_nt * 16u, 16u) : 0u;
     const size_t smem = smem_train ? size_t(P.smem_long_bytes) + offs_smem_bytes(ctx) + stage_smem_bytes(ctx, guided)
                                    : stage_smem_bytes(ctx, guided);
+    if (P.dbg_ranked != nullptr) return launch_match_dbg(P, smem_train, smem, sms, ctx->compute, grid);
     if (guided) return launch_match_guided(P, smem_train, smem, sms, ctx->compute, grid);
     return smem_train ? launch_match_smem(P, smem, sms, ctx->compute, grid)
                       : launch_match_global(P, smem, sms, ctx->compute, grid);

@@ -33,10 +33,11 @@
 //                        a warp-wide REDUX.MIN picks the winner.  The threshold tau and the
 //                        re-rank fallback (matcher.cpp:176-189) only decide where the pulling
 //                        stops, so no histogram has to be stored.
-//   4. verification    : 7 candidate rows and the query row as one 8 x 128 u8 matrix, its Gram
-//                        matrix on the integer tensor-core path (mma.sync m16n8k16 u8, exact s32):
-//                        |t - q|^2 = G[r][r] - 2 G[r][q] + G[q][q]; best / second with rank-order
-//                        tie-break, Lowe ratio in fp64 exactly as matcher.cpp:115-137.
+//   4. verification    : 4 lanes per candidate row, __vabsdiffu4 + __dp4a (exact u32 squared
+//                        distance), best / second with rank-order tie-break, Lowe ratio in
+//                        fp64 exactly as matcher.cpp:115-137.  (-DCHGPU_VERIFY_MMA: the same distances
+//                        from a Gram matrix on the integer tensor-core path, mma.sync m16n8k16 u8;
+//                        measured slower, kept as an A/B switch.)
 //
 // Results go to a per-query scratch (train id, d^2); compact_kernel (compact_kernels.cuh) turns
 // them into the reference's MatchRecord stream, ascending query index inside every pair.
@@ -66,6 +67,9 @@ __device__ __forceinline__ void static_for(F&& f) {
 #endif
 #ifndef CHGPU_VERIFY_LANES
 #define CHGPU_VERIFY_LANES 4
+#endif
+#ifndef CHGPU_VERIFY_TILES
+#define CHGPU_VERIFY_TILES 2  // tensor-core verification: 7-candidate tiles per round (1 or 2)
 #endif
 constexpr int kMatchThreads = CHGPU_MATCH_THREADS;
 constexpr uint32_t kVerifyLanes = CHGPU_VERIFY_LANES;  // lanes per descriptor row in the verification (2, 4 or 8)
@@ -317,8 +321,9 @@ __device__ __forceinline__ uint32_t band_filter(uint32_t key, const EpiLine& l, 
     return d > band_px ? kNone : key;
 }
 
-#ifdef CHGPU_VERIFY_SIMT
-// SIMT form of the verification (A/B switch -DCHGPU_VERIFY_SIMT; the default is the tensor-core form below): lane r holds the r-th ranked key
+#ifndef CHGPU_VERIFY_MMA
+// Verification of a ranked list (euclidean_verify, matcher.cpp:115-137), SIMT form (the default; the tensor-core
+// form below, -DCHGPU_VERIFY_MMA, issues 14 fewer instructions per query and is 2.4 % SLOWER on the B200: DESIGN.md): lane r holds the r-th ranked key
 // (id in the low 24 bits), n >= 2 entries.  kVerifyLanes lanes per candidate row (128 / kVerifyLanes bytes
 // each), 32 / kVerifyLanes rows per round; exact u32 squared distances; best = smallest d^2 with ties to the
 // earlier rank (strict '<' in the reference loop); Lowe ratio in fp64 with the reference's operand order.
@@ -403,6 +408,7 @@ __device__ __forceinline__ bool verify_ranked(const uint8_t* __restrict__ desc_i
     const uint4* __restrict__ qrow = reinterpret_cast<const uint4*>(desc_i + uint64_t(q) * kDim) + t * 2;
     const bool own = g != 7 && t == (g >> 1);  // this thread receives G[g][g] of both tiles
     uint32_t m1 = kNone, m2 = kNone;           // smallest and second smallest (d^2 << 8 | rank) seen by this thread
+#if CHGPU_VERIFY_TILES == 2
     for (uint32_t j0 = 0; j0 < n; j0 += 14) {
         // tile A: candidates j0 .. j0 + 6, tile B: j0 + 7 .. j0 + 13 (past the end: the last one again)
         const uint32_t ra = j0 + g, rb = ra + 7;
@@ -427,6 +433,24 @@ __device__ __forceinline__ bool verify_ranked(const uint8_t* __restrict__ desc_i
         m2 = min(m2, max(m1, pkb));
         m1 = min(m1, pkb);
     }
+#else
+    for (uint32_t j0 = 0; j0 < n; j0 += 7) {  // one tile per round: candidates j0 .. j0 + 6
+        const uint32_t ra = j0 + g;
+        const uint32_t ia = __shfl_sync(FULL, mykey, min(ra, n - 1)) & 0xffffffu;
+        const uint4* __restrict__ pa = g == 7 ? qrow : reinterpret_cast<const uint4*>(desc_j + uint64_t(ia) * kDim) + t * 2;
+        const uint4 a0 = __ldg(pa), a1 = __ldg(pa + 1);
+        int ea[4] = {0, 0, 0, 0}, oa[4] = {0, 0, 0, 0};
+        gram8_u8(ea, oa, a0, a1);
+        const int a_even = ea[0] + oa[2], a_odd = ea[1] + oa[3];
+        const int cross_a = __shfl_sync(FULL, a_odd, lane | 3u);
+        const int qq = __shfl_sync(FULL, a_odd, 31);
+        const int diag_a = (g & 1) ? a_odd : a_even;
+        const uint32_t da = uint32_t(diag_a + qq - 2 * cross_a);
+        const uint32_t pka = (own && ra < n) ? ((da << 8) | ra) : kNone;
+        m2 = min(m2, max(m1, pka));
+        m1 = min(m1, pka);
+    }
+#endif
     const uint32_t bestp = __reduce_min_sync(FULL, m1);
     const uint32_t secondp = __reduce_min_sync(FULL, m1 == bestp ? m2 : m1);
     const uint32_t bl = bestp & 0xffu, best = bestp >> 8, second = secondp >> 8;
@@ -442,7 +466,9 @@ __device__ __forceinline__ bool verify_ranked(const uint8_t* __restrict__ desc_i
 
 // LT = number of table slots unrolled in registers (>= L); EXACT: L == LT, no per-table guards;
 // GUIDED: the epipolar band filter above is applied to every candidate.
-template <bool SMEM_TRAIN, int LT, bool EXACT, bool GUIDED, int MODE = kModeMatch>
+// DBG: the parity tests' ranked-list output (dbg_ranked / dbg_count); a separate instantiation so that production launches
+// carry no per-query pointer test.
+template <bool SMEM_TRAIN, int LT, bool EXACT, bool GUIDED, int MODE = kModeMatch, bool DBG = false>
 __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchParams P) {
     extern __shared__ __align__(16) unsigned char s_raw[];  // [train codes | bucket offsets | lookup staging]
     __shared__ unsigned int s_unit;
@@ -465,7 +491,6 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
     asm volatile("" : "+r"(s_stage));
     constexpr uint32_t kRec = stage_record_bytes(LT), kAdj = 32u + uint32_t(LT) * 8u;
     const uint32_t le_mask = (2u << lane) - 1u;  // lanes <= this one
-    const bool dbg = MODE == kModeMatch && P.dbg_ranked != nullptr;  // parity tests only: one predicate, not a pointer test per query
 
     if (SMEM_TRAIN && tid == 0) {
         mbar_init(&s_bar, 1);
@@ -772,7 +797,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     if (MODE == kModeTileMin && lane == 0) atomicOr(P.gdone + pd.res_off + q, 1ull << pd.tile_idx);
                 }
 
-                if (dbg) {
+                if (DBG && MODE == kModeMatch) {
                     if (lane < n) P.dbg_ranked[uint64_t(q) * P.top_k + lane] = mykey & 0xffffffu;
                     if (lane == 0) P.dbg_count[q] = n;
                 }

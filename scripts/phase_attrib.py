@@ -47,24 +47,58 @@ def sass_lines(lib, kernel):
             return out
     raise SystemExit('kernel not found in ' + lib)
 
+SRC = os.path.join(os.path.dirname(os.path.abspath(__file__)), '..', 'paper_1805_08995_b200', 'csrc', 'match_kernels.cuh')
+MARKS = [  # (first line containing the text, phase of the lines from there on)
+    ('void __launch_bounds__(kMatchThreads, 1) match_kernel', 'other'),
+    ('for (;;) {', 'unit'),
+    ('auto lookup_batch = ', 'lookup'),
+    ('auto load_ids = ', 'ids'),
+    ('uint32_t idn[LT];', 'loop'),
+    ('} else if (tover <= 32u * kOverSlots) {', 'scan'),
+    ('// ---- 3. ranking', 'rank'),
+    ('// ---- long buckets', 'longbuckets'),
+    ('if (MODE != kModeMatch && emit) {', 'emit_dbg'),
+    ('// ---- 4. verification', 'verify'),
+    ('// batch boundary', 'loop'),
+    ('st_raw = __reduce_add_sync', 'unit'),
+]
+_ranges = None
+KERNEL_FIRST = KERNEL_LAST = 0
+
+
+def _load_ranges():
+    global _ranges, KERNEL_FIRST, KERNEL_LAST
+    lines = open(SRC).read().splitlines()
+    starts, at = [], 0
+    for text, ph in MARKS:
+        at = next(i for i in range(at, len(lines)) if text in lines[i])
+        starts.append((at + 1, ph))
+    end = next(i for i in range(at, len(lines)) if lines[i].startswith('}')) + 1
+    KERNEL_FIRST, KERNEL_LAST = starts[0][0], end
+    special = {}
+    for i in range(starts[-2][0], starts[-1][0]):  # the loop tail calls the lookup and the id prefetch
+        if 'lookup_batch(' in lines[i - 1]: special[i] = 'lookup'
+        if 'load_ids(' in lines[i - 1]: special[i] = 'ids'
+    for i in range(starts[4][0], starts[5][0]):    # ... and so does the loop head
+        if 'lookup_batch(' in lines[i - 1]: special[i] = 'lookup'
+        if 'load_ids(' in lines[i - 1]: special[i] = 'ids'
+    _ranges = (starts, end, special)
+
+
 def phase_of(line):
-    if line is None: return 'other'
-    if 443 <= line <= 491: return 'lookup'
-    if 494 <= line <= 500: return 'ids'
-    if 395 <= line <= 433 or 435 <= line <= 438: return 'unit'
-    if line in (505, 703): return 'lookup'
-    if line in (506, 704, 519): return 'ids'
-    if 502 <= line <= 529 or 700 <= line <= 706: return 'loop'
-    if 531 <= line <= 566: return 'scan'
-    if 568 <= line <= 610: return 'rank'
-    if 611 <= line <= 679: return 'longbuckets'
-    if 681 <= line <= 690: return 'emit_dbg'
-    if 693 <= line <= 698: return 'verify'
-    if 709 <= line <= 717: return 'unit'
-    return 'other'
+    if _ranges is None: _load_ranges()
+    starts, end, special = _ranges
+    if line is None or line < starts[0][0] or line > end: return 'other'
+    if line in special: return special[line]
+    ph = 'other'
+    for first, name in starts:
+        if line >= first: ph = name
+    return ph
+
 
 def main():
     src, lib, kernel, nq = sys.argv[1], sys.argv[2], sys.argv[3], float(sys.argv[4])
+    _load_ranges()
     table = sass_lines(lib, kernel)
     rows = list(csv.reader(open(src)))
     hdr_i = next(i for i, r in enumerate(rows) if r and r[0] == 'Address')
@@ -84,11 +118,11 @@ def main():
         # outermost line in match_kernels.cuh inside the kernel body (>= 365); else innermost known
         outer = None
         for f, l, inl in chain:
-            if f == 'match_kernels.cuh' and inl is None and l >= 365 and l <= 718:
+            if f == 'match_kernels.cuh' and inl is None and KERNEL_FIRST <= l <= KERNEL_LAST:
                 outer = l
         if outer is None:
             for f, l, inl in chain:
-                if inl is not None and 365 <= inl <= 718: outer = inl
+                if inl is not None and KERNEL_FIRST <= inl <= KERNEL_LAST: outer = inl
         ph = phase_of(outer)
         op = text.split()[0] if not text.startswith('@') else text.split()[1]
         op = op.split('.')[0]
