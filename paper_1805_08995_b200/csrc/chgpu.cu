@@ -116,6 +116,9 @@ struct ImageRec {
     size_t block_bytes = 0;
     uint32_t image_id = 0;
     bool used = false;
+    // centering generation the codes were computed under (chgpu_hash_images, verified code caches); 0 = codes supplied
+    // by the caller (chgpu_upload_codes), not tied to the context's centering
+    uint32_t hash_gen = 0;
     // id-range tiles of an image too large for the match kernel's shared-memory tile: hidden slots of the
     // image table whose DevImages are slices of this block with their own bucket index (local point ids)
     std::vector<uint32_t> tile_slots;
@@ -169,6 +172,7 @@ struct chgpu_ctx {
 
     // family
     bool has_family = false, has_centering = false;
+    uint32_t centering_gen = 1;  // bumped when a DIFFERENT centering vector is installed: codes hashed before are stale
     chgpu_family_params fam{};
     double* d_planes = nullptr;
     double* d_centering = nullptr;
@@ -733,7 +737,22 @@ struct MatchRun {
     uint32_t* dbg_count = nullptr;
 };
 
+chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_out);
+
+// A failure in the middle of a pair list (an aborting sink, a CUDA error, an allocation that fails) returns while the
+// next sub-batch is still queued on the streams: drain them before handing the status back, so that the buffers the
+// next call reuses (pair table, result scratch, pinned chunks) have no reader or writer left and the context stays usable.
 chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_out) {
+    const chgpu_status s = run_match_impl(ctx, run, stats_out);
+    if (s != CHGPU_OK) {
+        cudaStreamSynchronize(ctx->compute);
+        cudaStreamSynchronize(ctx->copy);
+        cudaGetLastError();
+    }
+    return s;
+}
+
+chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_out) {
     DeviceGuard guard(ctx->device);
     if (!ctx->has_family) return fail(ctx, CHGPU_ELOGIC, "no hash family installed");
     const char* why = nullptr;
@@ -775,6 +794,10 @@ chgpu_status run_match(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_o
             if (!(I.flags & 1u) || !(J.flags & 1u))
                 return fail(ctx, CHGPU_ELOGIC, "pair (%u,%u): codes not computed (call chgpu_hash_images first)",
                             run.pairs[2 * k], run.pairs[2 * k + 1]);
+            const uint32_t gi = ctx->images[si].hash_gen, gj = ctx->images[sj].hash_gen;
+            if ((gi && gi != ctx->centering_gen) || (gj && gj != ctx->centering_gen))
+                return fail(ctx, CHGPU_ELOGIC, "pair (%u,%u): codes were computed under a centering that has been replaced "
+                            "(call chgpu_hash_images again)", run.pairs[2 * k], run.pairs[2 * k + 1]);
             const uint32_t tiles = uint32_t(ctx->images[sj].tile_slots.size());
             const bool tiled = tiles != 0;
             if (cur.count && (cur.queries + I.n > ctx->sub_batch_queries || cur.count >= pairs_cap || tiled != cur.tiled ||
@@ -1372,6 +1395,10 @@ chgpu_status chgpu_set_centering(chgpu_ctx* ctx, const double* centering128) {
     DeviceGuard guard(ctx->device);
     CK(cudaStreamSynchronize(ctx->compute));
     CK(cudaMemcpy(ctx->d_centering, centering128, 128 * sizeof(double), cudaMemcpyHostToDevice));
+    // The reference's HashFamily does not change once centered (hashing.cpp:59-64) and its code caches carry the
+    // centering fingerprint for that reason: codes hashed here under another vector must not meet codes hashed under
+    // this one.  They stay resident but run_match refuses them until they are hashed again.
+    if (ctx->has_centering && memcmp(ctx->h_centering, centering128, sizeof(ctx->h_centering)) != 0) ++ctx->centering_gen;
     memcpy(ctx->h_centering, centering128, sizeof(ctx->h_centering));
     ctx->has_centering = true;
     return refresh_hash_filter(ctx);
@@ -2132,14 +2159,22 @@ chgpu_status chgpu_hash_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32
                 if (mx) CK(launch_hash_filtered(ctx, ctx->d_slots + first, cnt, mx, reduce_rounds));
             }
         } else {
-            CK(launch_hash_exact(ctx, dim3((max_n + kHashTilePoints - 1) / kHashTilePoints, count), ctx->d_slots,
-                                 reduce_rounds, false));
+            // gridDim.y holds at most 65,535 images: same chunks as the filtered path
+            for (uint32_t first = 0; first < count; first += kHashBatchImages) {
+                const uint32_t cnt = std::min(kHashBatchImages, count - first);
+                uint32_t mx = 0;
+                for (uint32_t i = 0; i < cnt; ++i) mx = std::max(mx, ctx->images[slots[first + i]].dev.n);
+                if (mx)
+                    CK(launch_hash_exact(ctx, dim3((mx + kHashTilePoints - 1) / kHashTilePoints, cnt), ctx->d_slots + first,
+                                         reduce_rounds, false));
+            }
         }
     }
     if (const chgpu_status s = launch_bucket_build(ctx, uint32_t(all.size()))) return s;
     for (const uint32_t sl : all) {
         ImageRec& r = ctx->images[sl];
         r.dev.flags |= 1u;
+        r.hash_gen = ctx->centering_gen;
         ctx->h_images[sl] = r.dev;
     }
     // flags live only on the host mirror and in the device table; kernels never read them, so
@@ -2182,6 +2217,7 @@ chgpu_status chgpu_upload_codes(chgpu_ctx* ctx, uint32_t image_id, const uint32_
     CK(cudaStreamSynchronize(ctx->compute));
     for (const uint32_t sl : all) {
         ctx->images[sl].dev.flags |= 1u;
+        ctx->images[sl].hash_gen = 0;
         ctx->h_images[sl] = ctx->images[sl].dev;
     }
     return CHGPU_OK;
@@ -2238,7 +2274,9 @@ chgpu_status chgpu_image_load_code_cache(chgpu_ctx* ctx, uint32_t image_id, cons
     if (s == CHGPU_ENOMEM || (s == CHGPU_OK && count != n))  // cache_is_current also compares the point count (engine.cpp:581)
         return fail(ctx, CHGPU_EMISMATCH, "%s: code cache holds %u points, image %u has %u", path, count, image_id, n);
     if (s != CHGPU_OK) return fail(ctx, s, "%s: unreadable code cache", path);
-    return chgpu_upload_codes(ctx, image_id, shorts.data(), longs.data());
+    if (const chgpu_status u = chgpu_upload_codes(ctx, image_id, shorts.data(), longs.data())) return u;
+    ctx->images[slot].hash_gen = ctx->centering_gen;  // the cache's centering fingerprint equals the installed vector's
+    return CHGPU_OK;
 }
 
 // ---- match --------------------------------------------------------------------------------------

@@ -392,6 +392,7 @@ struct Replay {
     chgpu_status adopt_block(uint32_t b, chgpu_status load_status) {
         const uint32_t lo = part.lo(b), cnt = part.size(b);
         block_resident[b] = 1;
+        ++resident_blocks;  // counted together with the flag: an eviction after a failed load or hash must not underflow it
         std::vector<uint32_t> good;
         for (uint32_t i = 0; i < cnt; ++i)
             if (results[lo + i].status == CHGPU_OK) {
@@ -408,7 +409,7 @@ struct Replay {
             if (h != CHGPU_OK) return h;
         }
         ++st.block_loads;
-        st.max_resident_blocks = std::max(st.max_resident_blocks, ++resident_blocks);
+        st.max_resident_blocks = std::max(st.max_resident_blocks, resident_blocks);
         return CHGPU_OK;
     }
 

@@ -638,3 +638,95 @@ def test_guided_match_bit_exact(matcher, oracle, n_i, n_j, params):
     assert np.array_equal(rec[offs[2]:offs[3]], base)
     with pytest.raises(ValueError):
         matcher.match_pairs_guided([(BASE, BASE + 1)], F[None], -1.0, cfg)
+
+
+# ---- failure paths ----------------------------------------------------------------------------------
+def test_failed_pair_list_leaves_the_context_usable(matcher, default_family):
+    """A sink that aborts, and a record capacity that runs out, in the MIDDLE of a multi-sub-batch pair list
+    (chgpu.cu run_match: the next sub-batch is already queued when the failure is seen): the call reports the failure,
+    and the same context then delivers exactly the records of an undisturbed run."""
+    fresh(matcher, default_family)
+    n_img, n_pts = 12, 700
+    ds = make_dataset(n_img, n_pts, seed=31)
+    for i, d in enumerate(ds):
+        put(matcher, BASE + i, d)
+    ids = [BASE + i for i in range(n_img)]
+    matcher.centering_reset()
+    matcher.centering_add_many(ids)
+    matcher.centering_apply()
+    matcher.hash(ids)
+    pairs = [(BASE + i, BASE + j) for i in range(n_img) for j in range(i + 1, n_img)]  # 66 pairs
+    cfg = ch.MatchConfig()
+    matcher.set_sub_batch_queries(5 * n_pts)  # 5 pairs per sub-batch: 14 sub-batches
+    try:
+        offs0, rec0, st0 = matcher.match_pairs(pairs, cfg)
+        want = host_checksum(offs0, rec0)
+        assert st0["match_launches"] >= 10 and len(rec0) > 0
+
+        class Abort(Exception):
+            pass
+
+        calls = []
+
+        def bad_sink(first, offs, rec):
+            calls.append(first)
+            if len(calls) == 3:
+                raise Abort()
+
+        with pytest.raises(Abort):
+            matcher.match_pairs_stream(pairs, cfg, bad_sink)
+        assert len(calls) == 3
+
+        # capacity exhausted mid-list: the status says so and `total` is still the full count
+        with pytest.raises(MemoryError):
+            matcher.match_pairs(pairs, cfg, capacity=len(rec0) // 2)
+
+        got = []
+        matcher.match_pairs_stream(pairs, cfg, lambda first, offs, rec: got.append((first, offs.copy(), rec.copy())))
+        assert [g[0] for g in got] == sorted(g[0] for g in got)
+        rec = np.concatenate([g[2] for g in got])
+        assert len(rec) == len(rec0) and np.array_equal(rec, rec0)
+        offs1, rec1, st1 = matcher.match_pairs(pairs, cfg)
+        assert np.array_equal(offs1, offs0) and np.array_equal(rec1, rec0) and host_checksum(offs1, rec1) == want
+        assert st1["matches"] == st0["matches"]
+    finally:
+        matcher.set_sub_batch_queries(0)
+
+
+def test_replaced_centering_invalidates_hashed_codes(matcher, oracle, default_family):
+    """Codes hashed under one centering must not meet codes hashed under another (the reference's HashFamily is
+    fixed once centered, hashing.cpp:59-64; its code caches carry the centering fingerprint): after
+    chgpu_set_centering installs a different vector, images hashed before are refused until they are hashed again;
+    re-installing the SAME vector changes nothing; uploaded codes are the caller's and stay valid."""
+    fresh(matcher, default_family)
+    ds = make_dataset(3, 300, seed=5)
+    for i, d in enumerate(ds):
+        put(matcher, BASE + i, d)
+    ids = [BASE, BASE + 1, BASE + 2]
+    cen_a = oracle.centering(list(ds))
+    cen_b = cen_a + 0.25
+    matcher.set_centering(cen_a)
+    matcher.hash(ids)
+    cfg = ch.MatchConfig()
+    offs_a, rec_a, _ = matcher.match_pairs([(BASE, BASE + 1)], cfg)
+    matcher.set_centering(cen_a.copy())                     # same vector: still valid
+    matcher.match_pairs([(BASE, BASE + 1)], cfg)
+    matcher.set_centering(cen_b)
+    with pytest.raises(ch.LogicError):
+        matcher.match_pairs([(BASE, BASE + 1)], cfg)
+    matcher.hash([BASE])                                    # one side re-hashed is not enough
+    with pytest.raises(ch.LogicError):
+        matcher.match_pairs([(BASE, BASE + 1)], cfg)
+    matcher.upload_codes(BASE + 2, matcher.codes(BASE + 2))  # caller-supplied codes are not tied to the centering
+    matcher.match_pairs([(BASE, BASE + 2)], cfg)
+    matcher.hash([BASE + 1])
+    offs_b, rec_b, _ = matcher.match_pairs([(BASE, BASE + 1)], cfg)
+    fam = default_family
+    for k, img in enumerate((BASE, BASE + 1)):
+        s, l = oracle_codes(oracle, fam, cen_b, ds[k])
+        got = matcher.codes(img)
+        assert np.array_equal(got.shorts, s) and np.array_equal(got.longs, l)
+    matcher.set_centering(cen_a)
+    matcher.hash(ids)
+    offs_c, rec_c, _ = matcher.match_pairs([(BASE, BASE + 1)], cfg)
+    assert np.array_equal(offs_c, offs_a) and np.array_equal(rec_c, rec_a)
