@@ -27,6 +27,12 @@
 //
 // There is no CPU fallback: every function that computes goes through libchgpu.so and throws
 // std::runtime_error when no sm_100 device is present.
+//
+// Parameter envelope.  The reference accepts short_bits <= 32, any table_count >= 1, any top_k >= 2 and any
+// image size (hashing.cpp:30-36, matcher.cpp:9-17); the device path holds short_bits <= 12, table_count <= 8,
+// top_k <= 32 and <= 65,536 points per image (kDeviceMax* below; chgpu.h).  Arguments that are valid for the
+// reference but outside that envelope throw `UnsupportedOnDevice` (a std::runtime_error) — never a wrong result
+// and never one of the reference's own exception classes, so a caller can tell "not offered here" from "invalid".
 #pragma once
 
 #include <algorithm>
@@ -56,6 +62,17 @@ inline constexpr int kMaxReduceRounds = 7;
 inline constexpr int kDefaultReduceRounds = 3;
 inline constexpr std::size_t kFeatureFileHeaderBytes = 16;
 inline constexpr std::size_t kFeatureRecordBytes = 16 + kDescriptorDim;
+// the device path's parameter envelope (include/chgpu.h); beyond it: UnsupportedOnDevice
+inline constexpr std::uint32_t kDeviceMaxShortBits = 12;
+inline constexpr std::uint32_t kDeviceMaxTables = 8;
+inline constexpr std::uint32_t kDeviceMaxTopK = 32;
+inline constexpr std::uint32_t kDeviceMaxPoints = 65536;
+
+// Arguments the reference accepts and the device path does not hold (see the header comment).
+class UnsupportedOnDevice : public std::runtime_error {
+public:
+    explicit UnsupportedOnDevice(const std::string& what) : std::runtime_error(what) {}
+};
 
 // ---- feature_io.hpp types ---------------------------------------------------------------------
 struct Keypoint {  // feature_io.hpp:16-23
@@ -218,6 +235,7 @@ inline chgpu_match_cfg to_c(const MatchConfig& m) {
         case CHGPU_ELOGIC: throw std::logic_error(msg);
         case CHGPU_ENOMEM: throw std::bad_alloc();
         case CHGPU_ENOTFOUND: throw std::out_of_range(msg);
+        case CHGPU_EUNSUPPORTED: throw UnsupportedOnDevice(msg);
         default: throw std::runtime_error(msg + " [" + chgpu_status_name(st) + "]");
     }
 }
@@ -1132,12 +1150,12 @@ public:
             ck_lane(k, chgpu_centering_get_sums(lanes_[k]->handle(), part[k].data(), &cnt[k]));
         });
         for (std::size_t k = 0; k < G; ++k) {
-            for (int x = 0; x < kDescriptorDim; ++x) total[x] += part[k][x];
+            for (std::size_t x = 0; x < kDescriptorDim; ++x) total[x] += part[k][x];
             count += cnt[k];
         }
         if (count == 0) throw std::invalid_argument("set_centering: no descriptors");
         std::array<double, kDescriptorDim> c{};
-        for (int x = 0; x < kDescriptorDim; ++x) c[x] = static_cast<double>(total[x]) / static_cast<double>(count);
+        for (std::size_t x = 0; x < kDescriptorDim; ++x) c[x] = static_cast<double>(total[x]) / static_cast<double>(count);
         for (std::size_t k = 0; k < G; ++k) ck_lane(k, chgpu_set_centering(lanes_[k]->handle(), c.data()));
         return c;
     }

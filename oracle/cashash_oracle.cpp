@@ -143,6 +143,11 @@ struct Ranker {
     }
 };
 
+// Association order of the third line component (see chor.h): 0 = F20 x + (F21 y + F22), the order restated from
+// Eigen's evaluators; 1 = (F20 x + F21 y) + F22, the other order a build of geometry.cpp:98-101 could produce.
+// tests/test_oracle.py measures how often the two disagree on a candidate (chor_set_line_order).
+int g_line_order = 0;
+
 // Epipolar band filter of guided_match_pair (geometry.cpp:234-250).
 struct BandFilter {
     const float* kp_i;  // n_i x 4
@@ -155,7 +160,8 @@ struct BandFilter {
         const double x = kp_i[4 * static_cast<size_t>(q)], y = kp_i[4 * static_cast<size_t>(q) + 1];
         const double a = (F[0] * x + F[1] * y) + F[2];  // epipolar_line: l = F (x, y, 1)^T  (geometry.cpp:98-101)
         const double b = (F[3] * x + F[4] * y) + F[5];
-        const double c = F[6] * x + (F[7] * y + F[8]);   // (association order: see chor.h)
+        const double c = g_line_order == 0 ? F[6] * x + (F[7] * y + F[8])    // (association order: see chor.h)
+                                           : (F[6] * x + F[7] * y) + F[8];
         if (a == 0.0 && b == 0.0) return false;  // EpipolarLine::degenerate, geometry.hpp:28
         const double inv_norm = 1.0 / std::sqrt(a * a + b * b);
         std::erase_if(cands, [&](uint32_t idx) {
@@ -367,6 +373,8 @@ int chor_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
     return match_pair_impl(*p, *cfg, desc_i, n_i, shorts_i, longs_i, desc_j, n_j, shorts_j, longs_j,
                            records, record_count, stats, ranked, ranked_count);
 }
+
+void chor_set_line_order(int order) { g_line_order = order ? 1 : 0; }
 
 int chor_guided_match_pair(const chor_family_params* p, const chor_match_cfg* cfg,
                            const uint8_t* desc_i, const float* kp_i, uint32_t n_i, const uint32_t* shorts_i,

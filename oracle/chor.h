@@ -114,6 +114,10 @@ int chor_guided_match_pair(const chor_family_params* p, const chor_match_cfg* cf
                            chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
                            uint32_t* ranked, uint32_t* ranked_count);
 
+/* Association order of the line's third component used by chor_guided_match_pair of THIS library (the restatement):
+ * 0 (default) F20 x + (F21 y + F22); 1 (F20 x + F21 y) + F22.  Test instrumentation for the bound on row f4. */
+void chor_set_line_order(int order);
+
 int chor_brute_force_match(const uint8_t* desc_i, uint32_t n_i, const uint8_t* desc_j, uint32_t n_j,
                            double ratio, chor_match_record* records, uint32_t* record_count);
 

@@ -373,6 +373,20 @@ static void device_checks(const std::filesystem::path& tmp) {
         bad = {};
         bad.hamming_threshold = 129;
         CHECK(throws<std::invalid_argument>([&] { ch::match_pair(sets[0], sets[1], codes[0], codes[1], bad); }));
+        // valid for the reference, outside the device envelope: a distinct exception, at the first value beyond it
+        ch::MatchConfig wide;
+        wide.top_k = ch::kDeviceMaxTopK + 1;
+        CHECK(throws<ch::UnsupportedOnDevice>([&] { ch::match_pair(sets[0], sets[1], codes[0], codes[1], wide); }));
+        wide.top_k = ch::kDeviceMaxTopK;  // the last value inside it works
+        CHECK(!throws<ch::UnsupportedOnDevice>([&] { ch::match_pair(sets[0], sets[1], codes[0], codes[1], wide); }));
+        ch::FamilyParams fp13;
+        fp13.short_bits = ch::kDeviceMaxShortBits + 1;
+        const ch::HashFamily fam13 = ch::build_hash_family(fp13);  // host-side: the family itself is legal
+        CHECK(throws<ch::UnsupportedOnDevice>([&] { ch::Matcher m13; m13.set_family(fam13); }));
+        ch::FamilyParams fp9;
+        fp9.table_count = ch::kDeviceMaxTables + 1;
+        const ch::HashFamily fam9 = ch::build_hash_family(fp9);
+        CHECK(throws<ch::UnsupportedOnDevice>([&] { ch::Matcher m9; m9.set_family(fam9); }));
     }
 
     // guided_match_pair (geometry.hpp:86-89): the epipolar band between lookup and ranking

@@ -186,6 +186,11 @@ class Oracle:
             return out, stats.as_dict(), ranked[:ni], rcount[:ni]
         return out, stats.as_dict()
 
+    def set_line_order(self, order: int) -> None:
+        """Restatement only: association order of the epipolar line's third component (chor.h)."""
+        self.lib.chor_set_line_order.restype = None
+        self.lib.chor_set_line_order(C.c_int(order))
+
     def guided_match_pair(self, params, cfg, desc_i, kp_i, shorts_i, longs_i, desc_j, kp_j, shorts_j, longs_j, F, band_px,
                           want_ranked=False):
         p, c = self._fp(params), self._cfg(cfg)

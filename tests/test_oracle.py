@@ -378,6 +378,78 @@ def test_guided_restatement_equals_reference(restatement, reference):
     assert sizes[0] == len(base) == sizes[4] and sizes[3] == 0 and 0 < sizes[1] < sizes[0]
 
 
+def _band_distances(F, kp_i, kp_j, order):
+    """|a x' + b y' + c| / sqrt(a^2 + b^2) for every (query, train point), fp64, one rounding per operation, in the
+    operation order of the band filter (geometry.cpp:238-248) with the line's third component associated either way."""
+    x, y = kp_i[:, 0].astype(np.float64), kp_i[:, 1].astype(np.float64)
+    a = (F[0, 0] * x + F[0, 1] * y) + F[0, 2]
+    b = (F[1, 0] * x + F[1, 1] * y) + F[1, 2]
+    c = F[2, 0] * x + (F[2, 1] * y + F[2, 2]) if order == 0 else (F[2, 0] * x + F[2, 1] * y) + F[2, 2]
+    live = ~((a == 0.0) & (b == 0.0))
+    with np.errstate(divide="ignore", invalid="ignore"):
+        inv = 1.0 / np.sqrt(a * a + b * b)
+        tx, ty = kp_j[:, 0].astype(np.float64), kp_j[:, 1].astype(np.float64)
+        d = np.abs((a[:, None] * tx[None, :] + b[:, None] * ty[None, :]) + c[:, None]) * inv[:, None]
+    return d, live
+
+
+def test_guided_line_order_bound(restatement):
+    """Row f4 is pinned up to ONE unverifiable fact: the association order of l(2) = F20 x + F21 y + F22 inside
+    Eigen's Matrix3d * Vector3d (geometry.cpp:98-101; no Eigen in this image).  This bounds what that fact can change:
+    over a fuzz corpus of fundamental matrices, keypoints and bands, (1) count the (query, candidate) decisions that
+    differ between the two possible orders and the candidates within 4 ulp of the band edge under either, and (2) run
+    the whole guided match under both orders and require identical records, ranked lists and statistics."""
+    import paper_1805_08995_b200 as ch
+    params, cfg = ch.FamilyParams(), ch.MatchConfig()
+    fam = ch.build_hash_family(params)
+    decisions = differing = near_edge = moved_c = 0
+    try:
+        for seed in range(24):
+            rng = np.random.default_rng(1000 + seed)
+            n = 500
+            d = make_dataset(2, n, seed=100 + seed)
+            # pixel keypoints the way detectors report them: sub-pixel float32 positions in a ~1000 x 800 image
+            kp = [np.column_stack([rng.uniform(0, 1000, n), rng.uniform(0, 800, n), np.full(n, 2.0), np.zeros(n)])
+                  .astype(np.float32) for _ in range(2)]
+            if seed % 3 == 2:
+                F = np.array([[1.0, 0.0, -float(rng.integers(0, 900))], [0.0, 0.0, 0.0], [0.0, 50.0, -20000.0]])
+            else:
+                F = rng.normal(size=(3, 3))
+                F[:, 2] *= 300.0
+                if seed % 3 == 1:  # a properly scaled rank-2 matrix (normalize_scale_and_sign leaves |F| = 1)
+                    u, sv, vt = np.linalg.svd(F)
+                    F = (u * np.array([sv[0], sv[1], 0.0])) @ vt
+                    F /= np.linalg.norm(F)
+            band = float(rng.choice([0.5, 5.0, 40.0, 150.0, 300.0]))
+            d0, live = _band_distances(F, kp[0], kp[1], 0)
+            d1, _ = _band_distances(F, kp[0], kp[1], 1)
+            d0, d1 = d0[live], d1[live]
+            decisions += d0.size
+            differing += int(np.count_nonzero((d0 > band) != (d1 > band)))
+            edge = 4.0 * np.spacing(band)
+            near_edge += int(np.count_nonzero((np.abs(d0 - band) <= edge) | (np.abs(d1 - band) <= edge)))
+            moved_c += int(np.count_nonzero(d0 != d1))
+            cen = restatement.centering([d[0], d[1]])
+            codes = [restatement.compute_codes(params, fam.short_planes, fam.long_planes, cen, d[i]) for i in range(2)]
+            out = []
+            for order in (0, 1):
+                restatement.set_line_order(order)
+                out.append(restatement.guided_match_pair(params, cfg, d[0], kp[0], *codes[0], d[1], kp[1], *codes[1], F, band,
+                                                         want_ranked=True))
+            a, b = out
+            assert np.array_equal(a[0], b[0]) and a[1] == b[1] and np.array_equal(a[3], b[3]), seed
+            for q in np.flatnonzero(a[3]):
+                assert np.array_equal(a[2][q, :a[3][q]], b[2][q, :b[3][q]]), (seed, q)
+    finally:
+        restatement.set_line_order(0)
+    # the two orders do produce different distances (the test is not vacuous) ...
+    assert moved_c > 0 and decisions > 4_000_000
+    # ... and none of them is close enough to the band edge to change a decision
+    assert differing == 0 and near_edge == 0, (differing, near_edge, decisions)
+    print(f"f4 line-order bound: {decisions} decisions, {moved_c} distances differ between the orders, "
+          f"{near_edge} within 4 ulp of the band edge, {differing} decisions differ")
+
+
 # ---- the order-independent records checksum (bench.py's and the full-size GPU tests' comparison) ------------
 def _mix64(x):
     x = (x + np.uint64(0x9e3779b97f4a7c15))

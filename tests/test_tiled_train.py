@@ -34,6 +34,8 @@ CFGS = [ch.MatchConfig(), ch.MatchConfig(top_k=32, hamming_threshold=64, ratio=0
     (12288, 12288, "uniform"),
     (500, 24577, "sift"),        # 3 full tiles + one of a single point; skewed buckets inside the tiles
     (20000, 9000, "uniform"),    # large query image, train image below the capacity: the ordinary path
+    (1200, 65536, "uniform"),    # the envelope's edge: the largest image the device path holds (u16 point ids), 8 tiles
+    (65536, 3000, "uniform"),    # ... and as the query image
 ])
 def test_tiled_match_bit_exact(matcher, oracle, default_family, n_i, n_j, shape):
     fresh(matcher, default_family)
