@@ -297,19 +297,26 @@ def run_ours(args):
     from paper_1805_08995_b200.sharding import Comm
 
     gpu = ENGINE_FACTORY is None
+    # CHGPU_BENCH_SHARE_GPU=1: a FUNCTIONAL check of the N-rank path on a box with fewer GPUs — the ranks share the
+    # visible devices (rank r -> cuda:(r mod count)) and talk over gloo (NCCL refuses two ranks on one device).  The line
+    # says so ("functional_check_only"); it is never a scaling number.
+    share = gpu and world > 1 and os.environ.get("CHGPU_BENCH_SHARE_GPU") == "1"
+    backend = "gloo" if share else DIST_BACKEND
     if gpu:
         if not torch.cuda.is_available():
             raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+        if share:
+            local = local % torch.cuda.device_count()
         if local >= torch.cuda.device_count():
             raise SystemExit(f"bench.py: rank {rank} wants cuda:{local} but only {torch.cuda.device_count()} device(s) are visible")
         torch.cuda.set_device(local)
-    dev = torch.device("cuda", local) if gpu else torch.device("cpu")
+    dev = torch.device("cuda", local) if (gpu and not share) else torch.device("cpu")
     if world > 1:
         import torch.distributed as dist
-        if gpu:
-            dist.init_process_group(DIST_BACKEND, device_id=dev)
+        if gpu and not share:
+            dist.init_process_group(backend, device_id=dev)
         else:
-            dist.init_process_group(DIST_BACKEND)
+            dist.init_process_group(backend)
     comm = Comm(rank, world)  # host-side exchange (gloo group): centering sums, per-rank report
     strong = world > 1 and not args.weak
 
@@ -540,8 +547,11 @@ def run_ours(args):
                             "max_over_min": float(max(shard_weights)) / float(max(1, min(shard_weights)))}
                            if shard_weights is not None else None),
             "collectives": ("none on the data path; torch.distributed: barrier + max/sum of scalars "
-                            f"({DIST_BACKEND}), 1 KB centering exchange + per-rank report (gloo, host side)") if world > 1 else "none",
+                            f"({backend}), 1 KB centering exchange + per-rank report (gloo, host side)") if world > 1 else "none",
         }
+        if share:
+            line["functional_check_only"] = (f"{world} ranks share {torch.cuda.device_count()} GPU(s) (CHGPU_BENCH_SHARE_GPU=1): "
+                                             "the N-rank code path on hardware, not a scaling measurement")
         print(json.dumps(line), flush=True)
     m.close()
     if world > 1:
@@ -559,7 +569,7 @@ def free_port() -> int:
 def spawn_ranks(n: int, argv: list[str], script: str | None = None, check_devices: bool = True) -> int:
     """`bench.py --gpus N` without a launcher: become the launcher.  One process per GPU through torch.distributed.run
     (rank r -> cuda:r via LOCAL_RANK), rendezvous on 127.0.0.1.  Fails loudly when the box has fewer than N GPUs."""
-    if check_devices:
+    if check_devices and os.environ.get("CHGPU_BENCH_SHARE_GPU") != "1":
         import torch
         have = torch.cuda.device_count() if torch.cuda.is_available() else 0
         if have < n:
