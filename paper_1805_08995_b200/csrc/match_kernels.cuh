@@ -331,6 +331,33 @@ __device__ __forceinline__ bool verify_ranked(const uint8_t* __restrict__ desc_i
                                               uint32_t q, uint32_t n, uint32_t mykey, uint32_t lane, double ratio_sq,
                                               uint32_t& out_t, uint32_t& out_d) {
     constexpr uint32_t FULL = 0xffffffffu;
+#ifndef CHGPU_NO_VERIFY_SHORTCUT
+    // Shortcut (exact): usually the first ranked candidate is the match and the rest are far away.  Lanes 0-7 form its
+    // full distance F (16 bytes each); lane pairs 8+2j, 9+2j form the distance of candidate j + 1 over its FIRST 32
+    // dimensions only, P_c <= d^2_c (one 32-byte sector per candidate instead of four).  If F < ratio^2 * min P_c then
+    // F < P_c <= d^2_c for every other candidate (ratio^2 < 1): the first candidate is the strict best, `second` >=
+    // min P_c > 0, and by the monotonicity of the rounded product the reference's test best < ratio^2 * second holds:
+    // the record is (id_0, F), exactly the reference's.  Otherwise nothing is decided and the full evaluation below runs.
+    if (n <= 13u) {
+        const bool whole = lane < 8u;
+        const uint32_t cj = whole ? 0u : ((lane - 8u) >> 1) + 1u;  // rank of the candidate this lane works on
+        const uint32_t piece = whole ? lane : (lane & 1u);          // which 16 bytes of the rows
+        const uint32_t cid = __shfl_sync(FULL, mykey, min(cj, n - 1)) & 0xffffffu;
+        const uint4 qa = __ldg(reinterpret_cast<const uint4*>(desc_i + uint64_t(q) * kDim) + piece);
+        const uint4 ta = __ldg(reinterpret_cast<const uint4*>(desc_j + uint64_t(cid) * kDim) + piece);
+        uint32_t s = sqdiff4(qa.x, ta.x) + sqdiff4(qa.y, ta.y) + sqdiff4(qa.z, ta.z) + sqdiff4(qa.w, ta.w);
+        s += __shfl_xor_sync(FULL, s, 1);                        // pairs: P_c complete
+        uint32_t f = s + __shfl_xor_sync(FULL, s, 2);
+        f += __shfl_xor_sync(FULL, f, 4);                        // lanes 0-7: F complete
+        const uint32_t full0 = __shfl_sync(FULL, f, 0);
+        const uint32_t pmin = __reduce_min_sync(FULL, (!whole && cj < n) ? s : kNone);
+        if (double(full0) < __dmul_rn(ratio_sq, double(pmin))) {
+            out_t = __shfl_sync(FULL, mykey, 0) & 0xffffffu;
+            out_d = full0;
+            return true;
+        }
+    }
+#endif
     constexpr uint32_t VL = kVerifyLanes, ROWS = 32u / VL, PIECES = 8u / VL;
     const uint32_t part = lane % VL, cand = lane / VL;
     const uint4* __restrict__ qrow = reinterpret_cast<const uint4*>(desc_i + uint64_t(q) * kDim) + part * PIECES;
