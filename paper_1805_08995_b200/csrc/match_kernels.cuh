@@ -256,6 +256,27 @@ __device__ __forceinline__ uint32_t next_key(const uint32_t (&key)[SLOTS], uint3
     return g >= nb - 1u ? kNone : g - nb;
 }
 
+// This lane's own smallest key strictly greater than `prev` (no warp exchange), or kNone.
+template <int SLOTS>
+__device__ __forceinline__ uint32_t lane_next_key(const uint32_t (&key)[SLOTS], uint32_t prev) {
+    const uint32_t nb = ~prev;
+    uint32_t acc = nb - 1u, acc2 = key[0] + nb;  // kNone + nb; see next_key for the wrap argument
+#pragma unroll
+    for (int i = 1; i < SLOTS; ++i) {
+        if (i & 1) acc = min(acc, key[i] + nb);
+        else acc2 = min(acc2, key[i] + nb);
+    }
+    acc = min(acc, acc2);
+    return acc >= nb - 1u ? kNone : acc - nb;
+}
+
+// next_key that also hands back what every lane found on its own: *lane_min = this lane's smallest key > prev (or kNone).
+template <int SLOTS>
+__device__ __forceinline__ uint32_t next_key_keep(const uint32_t (&key)[SLOTS], uint32_t prev, uint32_t& lane_min) {
+    lane_min = lane_next_key(key, prev);
+    return __reduce_min_sync(0xffffffffu, lane_min);
+}
+
 // Hamming key of one candidate id: distance<<24 | id.
 template <bool SMEM_TRAIN>
 __device__ __forceinline__ uint32_t key_of(uint32_t id, const uint4& ql, uint32_t s_long, const uint4* __restrict__ g_long) {
@@ -491,6 +512,75 @@ __device__ __forceinline__ bool verify_ranked(const uint8_t* __restrict__ desc_i
 }
 #endif
 
+// Shortcut for the common shape of a matching query (exact): exactly one candidate k0 within tau, so the
+// reference re-ranks without the threshold (matcher.cpp:176-189) and verifies k0 plus the top_k - 1 next keys.  Instead of
+// pulling those keys one warp reduction at a time, every lane looks at its OWN slots: a1 < a2 < a3 = its three smallest
+// keys above k0.  With M3 = min over the lanes of a3: if at least top_k - 1 DISTINCT a1 values lie below M3, then the
+// (top_k - 1)-th smallest key above k0 lies below M3 as well, so every key of the reference's ranked list is some lane's a1
+// or a2 (a third key of any lane is >= M3).  The a1 / a2 candidates therefore form a SUPERSET of the list's runners-up, and
+// the smallest 16-dimension partial distance over that superset is a lower bound of the reference's `second`.  The test
+// F < ratio^2 * bound (F = full distance of k0's point) then proves, as in verify_ranked's shortcut, that k0's point is the
+// strict best and passes the reference's ratio test: the record is (id(k0), F) and the ranked list has exactly top_k
+// entries (the statistics need that number).  When the count is short or the test fails nothing is decided: the caller
+// goes on with the exact pulls and the full verification.
+// Loads of the shortcut, issued as early as their addresses are known so that they travel under the arithmetic that
+// follows: the pieces of the full distance (query row and k0's row, 8 lanes x 16 bytes) when k0 is known, ...
+struct FirstRow {
+    uint4 q, t;
+};
+__device__ __forceinline__ FirstRow load_first_row(const uint8_t* __restrict__ desc_i, const uint8_t* __restrict__ desc_j,
+                                                   uint32_t q, uint32_t k0, uint32_t lane) {
+    const uint32_t piece = lane & 7u;
+    FirstRow r;
+    r.q = __ldg(reinterpret_cast<const uint4*>(desc_i + uint64_t(q) * kDim) + piece);
+    r.t = __ldg(reinterpret_cast<const uint4*>(desc_j + uint64_t(k0 & 0xffffffu) * kDim) + piece);
+    return r;
+}
+
+template <int SLOTS>
+__device__ __forceinline__ bool rerank_shortcut(const uint32_t (&key)[SLOTS], uint32_t k0, uint32_t a1, uint32_t top_k,
+                                                const FirstRow& first, const uint8_t* __restrict__ desc_j, uint32_t lane,
+                                                double ratio_sq, uint32_t& out_t, uint32_t& out_d) {
+    constexpr uint32_t FULL = 0xffffffffu;
+    // ... and the first 16 dimensions of every lane's a1 point before a2, a3 and the count are worked out (a lane without a
+    // key re-reads k0's row: no new sector)
+    const uint4 t1 = __ldg(reinterpret_cast<const uint4*>(desc_j + uint64_t((a1 == kNone ? k0 : a1) & 0xffffffu) * kDim));
+    const uint32_t a2r = lane_next_key(key, a1), a2 = a1 == kNone ? kNone : a2r;
+    const uint32_t a3r = lane_next_key(key, a2), a3 = a2 == kNone ? kNone : a3r;
+    const uint32_t m3 = __reduce_min_sync(FULL, a3);
+    const uint32_t same = __match_any_sync(FULL, a1);
+    const bool leader = (same & ((1u << lane) - 1u)) == 0u;  // lowest lane holding this a1
+    const uint32_t distinct_below = __popc(__ballot_sync(FULL, leader && a1 < m3));
+    if (distinct_below + 1u < top_k) return false;
+#ifdef CHGPU_SHORTCUT_STATS
+    out_d = 1;  // experiment: the count check passed
+#endif
+    // the query's first 16 dimensions sit in the lanes with piece 0
+    uint4 q0;
+    q0.x = __shfl_sync(FULL, first.q.x, 0);
+    q0.y = __shfl_sync(FULL, first.q.y, 0);
+    q0.z = __shfl_sync(FULL, first.q.z, 0);
+    q0.w = __shfl_sync(FULL, first.q.w, 0);
+    uint32_t p2 = kNone;  // only keys below M3 can be on the list: few lanes have such an a2
+    if (a2 < m3) {
+        const uint4 t2 = __ldg(reinterpret_cast<const uint4*>(desc_j + uint64_t(a2 & 0xffffffu) * kDim));
+        p2 = sqdiff4(q0.x, t2.x) + sqdiff4(q0.y, t2.y) + sqdiff4(q0.z, t2.z) + sqdiff4(q0.w, t2.w);
+    }
+    const uint32_t p1 = a1 < m3 ? sqdiff4(q0.x, t1.x) + sqdiff4(q0.y, t1.y) + sqdiff4(q0.z, t1.z) + sqdiff4(q0.w, t1.w) : kNone;
+    const uint32_t bound = __reduce_min_sync(FULL, min(p1, p2));
+    uint32_t f = sqdiff4(first.q.x, first.t.x) + sqdiff4(first.q.y, first.t.y) + sqdiff4(first.q.z, first.t.z) +
+                 sqdiff4(first.q.w, first.t.w);
+    f += __shfl_xor_sync(FULL, f, 1);
+    f += __shfl_xor_sync(FULL, f, 2);
+    f += __shfl_xor_sync(FULL, f, 4);
+    if (double(f) < __dmul_rn(ratio_sq, double(bound))) {
+        out_t = k0 & 0xffffffu;
+        out_d = f;
+        return true;
+    }
+    return false;
+}
+
 // LT = number of table slots unrolled in registers (>= L); EXACT: L == LT, no per-table guards;
 // GUIDED: the epipolar band filter above is applied to every candidate.
 // DBG: the parity tests' ranked-list output (dbg_ranked / dbg_count); a separate instantiation so that production launches
@@ -654,6 +744,10 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 
                 uint32_t mykey = kNone;  // lane r holds the r-th ranked key
                 uint32_t n = 0;          // ranked count
+                bool decided = false;    // the re-rank shortcut has produced the record (out_t, out_d): no verification
+#ifdef CHGPU_SHORTCUT_STATS
+                bool attempted = false;
+#endif
                 // GUIDED: the band can only remove candidates, so a query whose UNFILTERED smallest key is beyond tau
                 // ranks nothing either way; the line and the filter are evaluated only for the others.
                 EpiLine line{};
@@ -729,23 +823,39 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     } else if ((k0 >> 24) <= P.tau) {
                         if (lane == 0) mykey = k0;
                         n = 1;
-                        uint32_t prev = k0, nk = kNone;
                         // keys within tau, in order (usually this loop ends at its first pull)
-                        while (n < P.top_k) {
-                            nk = next_key(key, kNone, prev);
-                            if ((nk >> 24) > P.tau) break;  // beyond the threshold, or kNone: no key left
-                            if (lane == n) mykey = nk;
-                            ++n;
-                            prev = nk;
+                        uint32_t a1;  // this lane's own smallest key above k0
+#ifndef CHGPU_NO_RERANK_SHORTCUT
+                        const FirstRow first = load_first_row(I.desc, J.desc, q, k0, lane);  // travels under the first pull
+#endif
+                        uint32_t nk = next_key_keep(key, k0, a1);
+#ifndef CHGPU_NO_RERANK_SHORTCUT
+                        // one candidate within tau, more beyond it: the re-rank case; most of these are decided without
+                        // pulling the other top_k - 1 keys (not in the ranked-list instantiation, which reports them)
+#ifdef CHGPU_SHORTCUT_STATS
+                        attempted = !DBG && nk != kNone && (nk >> 24) > P.tau;
+#endif
+                        if (!DBG && nk != kNone && (nk >> 24) > P.tau &&
+                            rerank_shortcut(key, k0, a1, P.top_k, first, J.desc, lane, P.ratio_sq, out_t, out_d)) {
+                            decided = true;
+                            n = P.top_k;
                         }
-                        // the threshold cut something and the ranking is too small: re-rank without it
-                        if (n < P.top_k && nk != kNone && n < P.min_ranked) {
-                            do {
+#endif
+                        if (!decided) {
+                            while ((nk >> 24) <= P.tau) {  // (beyond the threshold, or kNone: no key left)
                                 if (lane == n) mykey = nk;
-                                ++n;
-                                if (n == P.top_k) break;
+                                if (++n == P.top_k) break;
                                 nk = next_key(key, kNone, nk);
-                            } while (nk != kNone);
+                            }
+                            // the threshold cut something and the ranking is too small: re-rank without it
+                            if (n < P.top_k && nk != kNone && n < P.min_ranked) {
+                                do {
+                                    if (lane == n) mykey = nk;
+                                    ++n;
+                                    if (n == P.top_k) break;
+                                    nk = next_key(key, kNone, nk);
+                                } while (nk != kNone);
+                            }
                         }
                     }
                 } else {
@@ -830,10 +940,21 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                 }
 
                 // ---- 4. verification (euclidean_verify, matcher.cpp:115-137) ------------------
+#ifdef CHGPU_SHORTCUT_STATS
+                // experiment (scripts/exp7.sh): verified_queries = re-rank cases, distances = count checks passed, matches of
+                // the pair counts = accepted by the shortcut
+                if (MODE == kModeMatch && attempted) {
+                    st_vq += 1;
+                    st_dist += (decided || out_d == 1) ? 1 : 0;
+                    st_match += decided ? 1 : 0;
+                }
+                if (false) {
+#else
                 if (MODE == kModeMatch && n >= 2) {
+#endif
                     st_vq += 1;
                     st_dist += n;
-                    if (verify_ranked(I.desc, J.desc, q, n, mykey, lane, P.ratio_sq, out_t, out_d)) st_match += 1;
+                    if (decided || verify_ranked(I.desc, J.desc, q, n, mykey, lane, P.ratio_sq, out_t, out_d)) st_match += 1;
                 }
                 if (MODE == kModeMatch && lane == 0) __stcs(P.res + pd.res_off + q, make_uint2(out_t, out_d));
 
