@@ -19,20 +19,83 @@ sys.path.insert(0, str(ROOT))
 import paper_1805_08995_b200 as ch  # noqa: E402
 
 
+# ---- parity of a sample of the run against the CPU oracle (checker only; the run itself never touches oracle/) ----------
+def _mix64(x):
+    x = (x + np.uint64(0x9e3779b97f4a7c15))
+    x = (x ^ (x >> np.uint64(30))) * np.uint64(0xbf58476d1ce4e5b9)
+    x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94d049bb133111eb)
+    return x ^ (x >> np.uint64(31))
+
+
+def records_checksum(pair_index, records) -> int:
+    """The order-independent checksum compact_kernel and chor_time_match_pairs accumulate, over records tagged with the
+    position of their pair in the sample."""
+    with np.errstate(over="ignore"):
+        a = (pair_index.astype(np.uint64) << np.uint64(32)) | records["query_index"].astype(np.uint64)
+        b = (records["train_index"].astype(np.uint64) << np.uint64(32)) | records["distance_sq"].astype(np.uint64)
+        return int(np.sum(_mix64(_mix64(a) ^ b), dtype=np.uint64))
+
+
+class SampleCheck:
+    """Keeps the records the run delivers for the pairs among `window` consecutive images and compares them, record for
+    record through the checksum, with the reference's match_pair on the host."""
+
+    def __init__(self, K, n, neighbors, window=36, first=None):
+        self.n = n
+        self.first = (K // 2 if first is None else first)
+        self.window = min(window, K - self.first)
+        lo, hi = self.first, self.first + self.window
+        self.sample = [(i, i + d) for i in range(lo, hi) for d in range(1, neighbors + 1) if i + d < hi]
+        self.index = {p: k for k, p in enumerate(self.sample)}
+        self.kept = {}
+
+    def take(self, pairs, offs, recs):
+        """pairs: (k, 2) image ids of the delivered pairs; offs: (k + 1) record offsets; recs: their records."""
+        for k, (a, b) in enumerate(np.asarray(pairs).reshape(-1, 2)):
+            key = (int(a), int(b))
+            if key in self.index:
+                self.kept[key] = recs[int(offs[k]):int(offs[k + 1])].copy()
+
+    def verdict(self, centering) -> dict:
+        sys.path.insert(0, str(ROOT / "tests"))
+        import oracle_lib
+        orc = oracle_lib.best()
+        params, cfg = ch.FamilyParams(), ch.MatchConfig()
+        fam = ch.build_hash_family(params)
+        desc = ch.make_dataset(self.window, self.n, seed=7, first=self.first)
+        codes = [orc.compute_codes(params, fam.short_planes, fam.long_planes, centering, desc[i]) for i in range(self.window)]
+        local = np.array([[a - self.first, b - self.first] for a, b in self.sample], dtype=np.uint32)
+        import os
+        sec, cpu_matches, cpu_checksum = orc.time_match_pairs(params, cfg, [desc[i] for i in range(self.window)],
+                                                              [c[0] for c in codes], [c[1] for c in codes], local,
+                                                              os.cpu_count() or 1)
+        missing = [p for p in self.sample if p not in self.kept]
+        idx = np.concatenate([np.full(len(self.kept[p]), k, np.uint64) for k, p in enumerate(self.sample) if p in self.kept] or
+                             [np.zeros(0, np.uint64)])
+        rec = np.concatenate([self.kept[p] for p in self.sample if p in self.kept] or [np.zeros(0, ch.RECORD_DTYPE)])
+        got = records_checksum(idx, rec)
+        return {"sample_pairs": len(self.sample), "images": [self.first, self.first + self.window], "oracle": orc.name,
+                "pairs_missing_from_the_run": len(missing), "gpu_matches": int(len(rec)), "cpu_matches": int(cpu_matches),
+                "records_checksum_equal": bool(got == cpu_checksum and not missing), "records_checksum": f"{got:#018x}",
+                "cpu_seconds": sec}
+
+
 def streamed(args, paths, accepted, K, n, write_s):
     """The same workload with bounded residency: centering pass over the files, then the guided plan replayed under
     the residency schedule (Load / Evict of blocks, matching task by task)."""
     with ch.Matcher(0) as m:
         m.set_family(ch.build_hash_family(ch.FamilyParams()))
         t0 = time.perf_counter()
-        _, res = m.centering_pass_files(paths, args.block_images, io_threads=args.io_threads)
+        centering, res = m.centering_pass_files(paths, args.block_images, io_threads=args.io_threads)
         assert all(r == n for r in res)
         t1 = time.perf_counter()
         got = {"records": 0, "pairs": 0, "peak_used": 0}
+        check = SampleCheck(K, n, args.neighbors)
 
         def sink(task, pr, offs, recs):
             got["records"] += len(recs)
             got["pairs"] += len(pr)
+            check.take(pr, offs, recs)
 
         st, res = m.match_plan_streamed(paths, args.block_images, args.blocks_per_group, ch.MatchConfig(), accepted_pairs=accepted,
                                         group_slots=args.group_slots, block_slots=args.block_slots, io_threads=args.io_threads,
@@ -40,8 +103,11 @@ def streamed(args, paths, accepted, K, n, write_s):
         t2 = time.perf_counter()
         assert got["records"] == st["matches"] and got["pairs"] == st["pairs"]
         props = m.device_props()
+    parity = check.verdict(np.asarray(centering, dtype=np.float64))
+    assert parity["records_checksum_equal"], parity
     tasks = ch.plan_tasks(K, args.block_images, args.blocks_per_group, accepted)
     line = {
+        "parity_sample": parity,
         "workload": f"BASELINE configs[3] Rome16K-shaped, OUT OF CORE: {K} images x {n} descriptors from CHFT files, (i,i+d) "
                     f"d=1..{args.neighbors}; blocks of {args.block_images} images, {args.block_slots} block slots, " + ("reuse order" if args.reuse_order else "plan order"),
         "images": K, "pairs": int(st["pairs"]), "tasks": len(tasks), "file_bytes": int(K * (16 + 144 * n)),
@@ -112,21 +178,26 @@ def main():
         m.centering_reset()
         results, lst = m.load_chft_files(paths, ids, io_threads=args.io_threads, accumulate_centering=True)
         assert all(r == n for r in results)
-        m.centering_apply()
+        centering = m.centering_apply()
         t1 = time.perf_counter()
         m.hash(ids)
         m.sync()
         t2 = time.perf_counter()
         got = {"records": 0}
+        check = SampleCheck(K, n, args.neighbors)
 
         def sink(first, offs, recs):
             got["records"] += len(recs)
+            check.take(pairs[first:first + len(offs) - 1], offs, recs)
 
         st = m.match_pairs_stream(pairs, ch.MatchConfig(), sink)
         t3 = time.perf_counter()
         assert got["records"] == st["matches"]
         props = m.device_props()
+    parity = check.verdict(np.asarray(centering, dtype=np.float64))
+    assert parity["records_checksum_equal"], parity
     line = {
+        "parity_sample": parity,
         "workload": f"BASELINE configs[3] Rome16K-shaped: {K} images x {n} descriptors from CHFT files, (i,i+d) d=1..{args.neighbors}",
         "images": K, "pairs": len(pairs), "file_bytes": int(K * (16 + 144 * n)), "dataset_write_s": write_s,
         "load": {"seconds": t1 - t0, "GB_per_s": K * (16 + 144 * n) / (t1 - t0) / 1e9, "io_threads": args.io_threads,
