@@ -199,8 +199,11 @@ chgpu_status chgpu_hash_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32
  *                       reference's fp64 operation order (reduce_dot, hashing.hpp:24-43).  Falls back to EXACT by
  *                       itself for planes / centerings outside the bound's premises (non-finite or huge values).
  *   EXACT:              every dot in the reference's fp64 operation order.
- * The environment variable CHGPU_HASH_EXACT=1 selects EXACT for new contexts. */
-typedef enum chgpu_hash_mode { CHGPU_HASH_FILTERED = 0, CHGPU_HASH_EXACT = 1 } chgpu_hash_mode;
+ *   TENSOR:             the FILTERED contract with the filter on the tensor cores (tcgen05.mma kind::i8): the planes as
+ *                       three int8 limbs of a 23-bit fixed-point value, exact s32 accumulators in tensor memory, a bound
+ *                       ~45x tighter than the fp32 one; undecided dots go to the same exact path.
+ * The environment variables CHGPU_HASH_EXACT=1 / CHGPU_HASH_TENSOR=1 select EXACT / TENSOR for new contexts. */
+typedef enum chgpu_hash_mode { CHGPU_HASH_FILTERED = 0, CHGPU_HASH_EXACT = 1, CHGPU_HASH_TENSOR = 2 } chgpu_hash_mode;
 typedef struct chgpu_hash_stats {
     uint64_t undecided_dots;      /* dots the filter handed to the exact path (cumulative per context) */
     uint64_t flipped_bits;        /* of those, bits whose fp32 sign differed from the reference's */

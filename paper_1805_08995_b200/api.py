@@ -681,9 +681,11 @@ class Matcher:
         ids = np.ascontiguousarray(image_ids, dtype=np.uint32)
         self._ck(self.lib.chgpu_hash_images(self.h, ids.ctypes.data_as(N.u32p), len(ids), reduce_rounds))
 
-    def set_hash_mode(self, exact: bool):
-        """False: fp32 filter + exact fp64 fixup (default); True: every dot in the reference's fp64 order."""
-        self._ck(self.lib.chgpu_set_hash_mode(self.h, 1 if exact else 0))
+    def set_hash_mode(self, exact):
+        """False / 0: fp32 filter + exact fp64 fixup (default); True / 1: every dot in the reference's fp64 order;
+        2 or "tensor": the filter on the tensor cores (tcgen05 int8 limbs), same exact fixup."""
+        mode = 2 if exact in (2, "tensor") else (1 if exact else 0)
+        self._ck(self.lib.chgpu_set_hash_mode(self.h, mode))
 
     def hash_stats(self) -> dict:
         st = N.HashStatsC()

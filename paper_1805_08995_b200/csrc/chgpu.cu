@@ -34,6 +34,7 @@
 
 #include "dev_types.cuh"
 #include "hash_kernels.cuh"
+#include "hash_tc.cuh"
 #include "compact_kernels.cuh"
 #include "match_launch.cuh"
 
@@ -184,6 +185,11 @@ struct chgpu_ctx {
     double* d_hnorm = nullptr;      // [gpad]
     uint32_t gpad = 0;
     double filt_a_rel = 0.0, filt_a_abs = 0.0;
+    // K1t (tensor-core filter): int8 limbs of the planes and the per-plane constants of its bound
+    int8_t* d_tc_limbs = nullptr;   // [3][tc_npad][128]
+    double* d_tc_const = nullptr;   // [4][tc_npad]: 1/S_g | bias_g | alpha_g | beta_g
+    uint32_t tc_npad = 0;
+    bool tc_ready = false;
     bool filter_ready = false;      // constants valid for the current planes + centering
     int hash_mode = 0;              // chgpu_hash_mode
     uint2* d_hq = nullptr;          // queue of undecided dots
@@ -560,12 +566,40 @@ cudaError_t launch_hash_filtered(chgpu_ctx* ctx, const uint32_t* slots, uint32_t
     P.queue = ctx->d_hq;
     P.queue_cap = kHashQueueCap;
     P.queue_count = ctx->d_hq_count;
-    const size_t smem = hash_filter_smem_bytes();
-    e = cudaFuncSetAttribute(hash_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    const dim3 grid((max_n + kFiltPoints - 1) / kFiltPoints, count);
-    hash_filter_kernel<<<grid, kFiltThreads, smem, ctx->compute>>>(P);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (ctx->hash_mode == CHGPU_HASH_TENSOR && ctx->tc_ready) {
+        // K1t: the same filter contract on the tensor cores (hash_tc.cuh); queue, fixup and overflow path are shared
+        HashTcParams T{};
+        T.images = ctx->d_images;
+        T.slots = slots;
+        T.limbs = ctx->d_tc_limbs;
+        T.inv_scale = ctx->d_tc_const;
+        T.bias = ctx->d_tc_const + ctx->tc_npad;
+        T.alpha = ctx->d_tc_const + 2 * size_t(ctx->tc_npad);
+        T.beta = ctx->d_tc_const + 3 * size_t(ctx->tc_npad);
+        T.npad = ctx->tc_npad;
+        T.m = P.m;
+        T.L = P.L;
+        T.nlong = P.nlong;
+        T.count = count;
+        T.tiles_max = (max_n + kTcPoints - 1) / kTcPoints;
+        T.queue = P.queue;
+        T.queue_cap = P.queue_cap;
+        T.queue_count = P.queue_count;
+        const size_t tsmem = hash_tc_smem_bytes(ctx->tc_npad);
+        e = cudaFuncSetAttribute(hash_filter_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tsmem));
+        if (e != cudaSuccess) return e;
+        const uint64_t units = uint64_t(count) * T.tiles_max;
+        const uint32_t tgrid = uint32_t(std::min<uint64_t>(units, uint64_t(ctx->prop.multiProcessorCount)));
+        hash_filter_tc_kernel<<<tgrid, kTcThreads, tsmem, ctx->compute>>>(T);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    } else {
+        const size_t smem = hash_filter_smem_bytes();
+        e = cudaFuncSetAttribute(hash_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        const dim3 grid((max_n + kFiltPoints - 1) / kFiltPoints, count);
+        hash_filter_kernel<<<grid, kFiltThreads, smem, ctx->compute>>>(P);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     hash_fixup_kernel<<<ctx->prop.multiProcessorCount * 4, 128, 0, ctx->compute>>>(
         ctx->d_images, ctx->d_planes, ctx->d_centering, ctx->d_hq, kHashQueueCap, ctx->d_hq_count, P.m, P.L,
         reduce_rounds, ctx->d_hstats);
@@ -617,6 +651,57 @@ chgpu_status refresh_hash_filter(chgpu_ctx* ctx) {
     ctx->filt_a_rel = 136.0 * std::ldexp(1.0, -24) + std::ldexp(1.0, -44);
     ctx->filt_a_abs = std::ldexp(1.0, -44) * std::sqrt(mean_sq) * (1.0 + 1e-12);
     ctx->filter_ready = true;
+
+    // K1t: H_x = rint(h_x * 2^(22 - e_g)) as three balanced int8 limbs; constants of the bound (hash_tc.cuh)
+    ctx->tc_ready = false;
+    const uint32_t npad = (G + kTcPassPlanes - 1) / kTcPassPlanes * kTcPassPlanes;
+    if (npad <= uint32_t(kTcMaxPlanes)) {
+        std::vector<int8_t> limbs(size_t(3) * npad * kDim, 0);
+        std::vector<double> cst(size_t(4) * npad, 0.0);
+        const double cnorm = std::sqrt(mean_sq) * (1.0 + 1e-12);
+        const double up = 1.0 + std::ldexp(1.0, -40);
+        for (uint32_t g = 0; g < npad; ++g) {
+            double inv = 1.0, alpha = 0.0, beta = 1e-30, b = 0.0;
+            if (g < G) {
+                const double* h = ctx->h_planes.data() + size_t(g) * kDim;
+                double hmax = 0.0;
+                for (int x = 0; x < kDim; ++x) hmax = std::max(hmax, std::fabs(h[x]));
+                int e = hmax > 0.0 ? std::ilogb(hmax) + 1 : 0;  // 2^e > hmax
+                e = std::min(std::max(e, -900), 900);
+                const double S = std::ldexp(1.0, 22 - e);
+                for (int x = 0; x < kDim; ++x) {
+                    long long H = std::llrint(h[x] * S);  // |H| <= 2^22 (h below 2^-900: 0, inside the bound all the same)
+                    const long long l2 = ((H + 128) & 255) - 128;
+                    H = (H - l2) / 256;
+                    const long long l1 = ((H + 128) & 255) - 128;
+                    const long long l0 = (H - l1) / 256;  // in [-64, 64]
+                    limbs[(size_t(0) * npad + g) * kDim + x] = static_cast<int8_t>(l0);
+                    limbs[(size_t(1) * npad + g) * kDim + x] = static_cast<int8_t>(l1);
+                    limbs[(size_t(2) * npad + g) * kDim + x] = static_cast<int8_t>(l2);
+                }
+                inv = std::ldexp(1.0, e - 22);
+                b = bias[g];
+                alpha = (std::ldexp(1.0, e - 23) + std::ldexp(1.0, -45) * hnorm[g]) * up;
+                beta = (std::ldexp(1.0, -45) * cnorm * hnorm[g] + 1e-30) * up;
+            }
+            cst[g] = inv;
+            cst[npad + g] = b;
+            cst[2 * size_t(npad) + g] = std::nextafter(alpha, HUGE_VAL);
+            cst[3 * size_t(npad) + g] = std::nextafter(beta, HUGE_VAL);
+        }
+        if (npad != ctx->tc_npad || !ctx->d_tc_limbs) {
+            cudaFree(ctx->d_tc_limbs);
+            cudaFree(ctx->d_tc_const);
+            ctx->d_tc_limbs = nullptr;
+            ctx->d_tc_const = nullptr;
+            CK(cudaMalloc(&ctx->d_tc_limbs, limbs.size()));
+            CK(cudaMalloc(&ctx->d_tc_const, cst.size() * sizeof(double)));
+            ctx->tc_npad = npad;
+        }
+        CK(cudaMemcpy(ctx->d_tc_limbs, limbs.data(), limbs.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_tc_const, cst.data(), cst.size() * sizeof(double), cudaMemcpyHostToDevice));
+        ctx->tc_ready = true;
+    }
     return CHGPU_OK;
 }
 
@@ -1185,6 +1270,7 @@ chgpu_status chgpu_create(int device, chgpu_ctx** out) {
     ok &= cudaMalloc(&ctx->d_hstats, sizeof(HashFilterStats)) == cudaSuccess;
     ok &= cudaMemset(ctx->d_hstats, 0, sizeof(HashFilterStats)) == cudaSuccess;
     if (const char* e = getenv("CHGPU_HASH_EXACT")) ctx->hash_mode = (e[0] == '1') ? CHGPU_HASH_EXACT : CHGPU_HASH_FILTERED;
+    if (const char* e = getenv("CHGPU_HASH_TENSOR")) if (e[0] == '1') ctx->hash_mode = CHGPU_HASH_TENSOR;
     if (!ok) return bail(CHGPU_ECUDA);
     *out = ctx;
     return CHGPU_OK;
@@ -1221,6 +1307,7 @@ void chgpu_destroy(chgpu_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     for (auto& b : ctx->load_scratch) cudaFree(b.first);
     cudaFree(ctx->d_planes_t); cudaFree(ctx->d_bias); cudaFree(ctx->d_hnorm); cudaFree(ctx->d_hq);
+    cudaFree(ctx->d_tc_limbs); cudaFree(ctx->d_tc_const);
     cudaFree(ctx->d_hq_count); cudaFree(ctx->d_hstats);
     if (ctx->ev_upload) cudaEventDestroy(ctx->ev_upload);
     if (ctx->ev_compute) cudaEventDestroy(ctx->ev_compute);
@@ -1303,7 +1390,7 @@ chgpu_status chgpu_set_family(chgpu_ctx* ctx, const chgpu_family_params* p, cons
 }
 
 chgpu_status chgpu_set_hash_mode(chgpu_ctx* ctx, chgpu_hash_mode mode) {
-    if (!ctx || (mode != CHGPU_HASH_FILTERED && mode != CHGPU_HASH_EXACT)) return CHGPU_EINVAL;
+    if (!ctx || (mode != CHGPU_HASH_FILTERED && mode != CHGPU_HASH_EXACT && mode != CHGPU_HASH_TENSOR)) return CHGPU_EINVAL;
     ctx->hash_mode = mode;
     return CHGPU_OK;
 }
@@ -1317,7 +1404,7 @@ chgpu_status chgpu_get_hash_stats(chgpu_ctx* ctx, chgpu_hash_stats* out) {
     out->undecided_dots = hs.undecided;
     out->flipped_bits = hs.flipped;
     out->overflowed_batches = hs.overflows;
-    out->filter_active = (ctx->hash_mode == CHGPU_HASH_FILTERED && ctx->filter_ready) ? 1 : 0;
+    out->filter_active = (ctx->hash_mode != CHGPU_HASH_EXACT && ctx->filter_ready) ? 1 : 0;
     return CHGPU_OK;
 }
 
@@ -2150,7 +2237,7 @@ chgpu_status chgpu_hash_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32
     CK(cudaStreamSynchronize(ctx->compute));
     CK(cudaMemcpyAsync(ctx->d_slots, all.data(), all.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->compute));
     if (max_n) {
-        if (ctx->hash_mode == CHGPU_HASH_FILTERED && ctx->filter_ready) {
+        if (ctx->hash_mode != CHGPU_HASH_EXACT && ctx->filter_ready) {
             // fp32 filter + exact fixup, in launches of <= kHashBatchImages images (one queue per launch)
             for (uint32_t first = 0; first < count; first += kHashBatchImages) {
                 const uint32_t cnt = std::min(kHashBatchImages, count - first);

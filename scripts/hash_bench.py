@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Hash-build throughput (K1/K1f + K2) on resident images: fp32-filtered default versus the exact fp64 kernel.
+"""Hash-build throughput (K1 / K1f / K1t + K2) on resident images: fp32 filter, tensor-core filter and the exact fp64 kernel.
 Prints one JSON line.    python scripts/hash_bench.py --images 1000 --points 8192"""
 import argparse
 import json
@@ -32,7 +32,7 @@ def main():
             m.centering_add(i)
         m.centering_apply()
         codes = {}
-        for name, exact in (("filtered", False), ("exact", True)):
+        for name, exact in (("filtered", False), ("tensor", 2), ("exact", True)):
             m.set_hash_mode(exact)
             m.hash(ids)
             m.sync()
@@ -50,9 +50,10 @@ def main():
                          "descriptors_per_s": K * n / best,
                          "undecided_dots_per_image": (s1["undecided_dots"] - s0["undecided_dots"]) / args.reps / K,
                          "flipped_bits_per_image": (s1["flipped_bits"] - s0["flipped_bits"]) / args.reps / K}
-        out["codes_identical"] = bool(np.array_equal(codes["filtered"][0], codes["exact"][0]) and
-                                      np.array_equal(codes["filtered"][1], codes["exact"][1]))
+        out["codes_identical"] = bool(all(np.array_equal(codes[k][0], codes["exact"][0]) and
+                                          np.array_equal(codes[k][1], codes["exact"][1]) for k in ("filtered", "tensor")))
         out["speedup"] = out["exact"]["seconds"] / out["filtered"]["seconds"]
+        out["speedup_tensor"] = out["exact"]["seconds"] / out["tensor"]["seconds"]
         out["device"] = m.device_props()["name"]
     print(json.dumps(out))
 

@@ -1,4 +1,5 @@
-"""Hash build through the fp32 filter (K1f, hash_kernels.cuh) versus the exact fp64 kernel and the CPU oracle.
+"""Hash build through the filters (K1f fp32 SIMT, hash_kernels.cuh; K1t tensor cores / tcgen05 int8 limbs, hash_tc.cuh)
+versus the exact fp64 kernel and the CPU oracle.
 
 The filter proves most hyperplane signs from an fp32 contraction and an a-priori error bound; every dot it
 cannot decide is re-evaluated in the reference's fp64 operation order (reduce_dot, hashing.hpp:24-43).  Codes
@@ -21,7 +22,14 @@ def oracle():
     return oracle_lib.best()
 
 
-def install(matcher, fam):
+@pytest.fixture(params=[0, 2], ids=["fp32_filter", "tensor_filter"])
+def mode(request, matcher):
+    """Every test runs under both filters; the context goes back to the default afterwards."""
+    yield request.param
+    matcher.set_hash_mode(0)
+
+
+def install(matcher, fam, mode=0):
     for img in list(getattr(matcher, "_test_ids", set())):
         try:
             matcher.evict(img)
@@ -29,7 +37,7 @@ def install(matcher, fam):
             pass
     matcher._test_ids = set()
     matcher.set_family(fam)
-    matcher.set_hash_mode(False)
+    matcher.set_hash_mode(mode)
 
 
 def put(matcher, image_id, desc):
@@ -48,9 +56,9 @@ def check(matcher, oracle, fam, cen, descs, rrs=(3,)):
 
 
 @pytest.mark.parametrize("params", [ch.FamilyParams(), ch.FamilyParams(12, 128, 8, 3), ch.FamilyParams(5, 33, 7, 4)])
-def test_filtered_and_exact_modes_agree_with_the_oracle(matcher, oracle, params):
+def test_filtered_and_exact_modes_agree_with_the_oracle(matcher, oracle, params, mode):
     fam = ch.build_hash_family(params)
-    install(matcher, fam)
+    install(matcher, fam, mode)
     descs = list(make_dataset(3, 3000, seed=31)) + [make_dataset(1, 777, seed=32, shape="sift")[0]]
     cen = oracle.centering(descs)
     matcher.set_centering(cen)
@@ -74,13 +82,13 @@ def test_filtered_and_exact_modes_agree_with_the_oracle(matcher, oracle, params)
             assert np.array_equal(c.shorts, filtered[i].shorts) and np.array_equal(c.longs, filtered[i].longs)
         assert matcher.hash_stats()["undecided_dots"] == after["undecided_dots"]
     finally:
-        matcher.set_hash_mode(False)
+        matcher.set_hash_mode(mode)
 
 
-def test_dots_at_and_near_zero_go_to_the_exact_path(matcher, oracle):
+def test_dots_at_and_near_zero_go_to_the_exact_path(matcher, oracle, mode):
     """Descriptors at / next to an integer centering: every dot is 0 or tiny, far below the fp32 bound."""
     fam = ch.build_hash_family(ch.FamilyParams())
-    install(matcher, fam)
+    install(matcher, fam, mode)
     rng = np.random.default_rng(3)
     cen = rng.integers(40, 200, 128).astype(np.float64)
     d = np.tile(cen.astype(np.uint8), (2000, 1))
@@ -95,17 +103,19 @@ def test_dots_at_and_near_zero_go_to_the_exact_path(matcher, oracle):
     c = matcher.codes(BASE)
     assert not c.shorts[0].any() and not c.longs[0].any()
     after = matcher.hash_stats()
-    # |dot| is 0 or a few |h_x|: a good part of them sits below the bound (~0.1 here)
-    assert after["undecided_dots"] - before["undecided_dots"] > 4 * 2000 * 176 * 0.1
+    # |dot| is 0 or a few |h_x|: a good part of them sits below the fp32 bound (~0.1 here); the integer filter's bound is
+    # ~45x tighter and keeps little more than the exact zeros (row 0: 176 dots in each of the 4 runs)
+    undecided = after["undecided_dots"] - before["undecided_dots"]
+    assert undecided > (4 * 2000 * 176 * 0.1 if mode == 0 else 4 * 176 - 1)
     # a fractional centering that puts dots within 1e-9 of zero
     cen2 = cen + 1e-9
     matcher.set_centering(cen2)
     check(matcher, oracle, fam, cen2, [d])
 
 
-def test_queue_overflow_falls_back_to_the_exact_kernel(matcher, oracle):
+def test_queue_overflow_falls_back_to_the_exact_kernel(matcher, oracle, mode):
     fam = ch.build_hash_family(ch.FamilyParams())
-    install(matcher, fam)
+    install(matcher, fam, mode)
     cen = np.full(128, 100.0)
     n = 16384   # 16384 x 176 undecided dots > the 2^21-entry queue
     d = np.full((n, 128), 100, np.uint8)
@@ -118,9 +128,9 @@ def test_queue_overflow_falls_back_to_the_exact_kernel(matcher, oracle):
     assert after["overflowed_batches"] == before["overflowed_batches"] + 1
 
 
-def test_centering_outside_the_bound_premises_uses_the_exact_kernel(matcher, oracle):
+def test_centering_outside_the_bound_premises_uses_the_exact_kernel(matcher, oracle, mode):
     fam = ch.build_hash_family(ch.FamilyParams())
-    install(matcher, fam)
+    install(matcher, fam, mode)
     d = make_dataset(1, 1000, seed=11)[0]
     cen = oracle.centering([d])
     cen[5] = 3e7
@@ -132,10 +142,10 @@ def test_centering_outside_the_bound_premises_uses_the_exact_kernel(matcher, ora
     assert matcher.hash_stats()["filter_active"] == 1
 
 
-def test_more_images_than_one_hash_launch_holds(matcher, oracle):
+def test_more_images_than_one_hash_launch_holds(matcher, oracle, mode):
     """The filtered path hashes in launches of <= 2,048 images (one undecided-dot queue per launch)."""
     fam = ch.build_hash_family(ch.FamilyParams())
-    install(matcher, fam)
+    install(matcher, fam, mode)
     k = 2300
     d = make_dataset(k, 24, seed=77)
     cen = oracle.centering(list(d))
