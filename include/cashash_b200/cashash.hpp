@@ -676,7 +676,8 @@ public:
     }
     // How the hyperplane signs are evaluated (both exact): fp32 filter with an error bound + fp64 re-evaluation
     // of the undecided dots (default), or every dot in reduce_dot's fp64 order (hashing.hpp:24-43).
-    void set_exact_hashing(bool exact) { ck(chgpu_set_hash_mode(ctx_, exact ? CHGPU_HASH_EXACT : CHGPU_HASH_FILTERED)); }
+    void set_exact_hashing(bool exact) { ck(chgpu_set_hash_mode(ctx_, exact ? CHGPU_HASH_EXACT : CHGPU_HASH_TENSOR)); }
+    void set_hash_mode(chgpu_hash_mode mode) { ck(chgpu_set_hash_mode(ctx_, mode)); }  // TENSOR (default) / FILTERED / EXACT
     chgpu_hash_stats hash_stats() {
         chgpu_hash_stats st{};
         ck(chgpu_get_hash_stats(ctx_, &st));

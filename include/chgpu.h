@@ -192,17 +192,16 @@ chgpu_status chgpu_download_descriptors(chgpu_ctx* ctx, uint32_t image_id, uint8
 /* Replaces compute_codes (hashing.hpp:131, hashing.cpp:130-149) + build_bucket_index
  * (matcher.hpp:43, matcher.cpp:27-51) for the listed images.  reduce_rounds = N_r in 0..7. */
 chgpu_status chgpu_hash_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32_t count, int reduce_rounds);
-/* How chgpu_hash_images evaluates the L*m + n hyperplane signs of a descriptor.  Both modes give the reference's
+/* How chgpu_hash_images evaluates the L*m + n hyperplane signs of a descriptor.  All modes give the reference's
  * bits exactly (compute_codes, hashing.cpp:130-149).
- *   FILTERED (default): an fp32 contraction with an a-priori error bound decides every sign it can prove; the dots
- *                       it cannot (|value| below the bound, ~1e-4 of them, ties included) are re-evaluated in the
- *                       reference's fp64 operation order (reduce_dot, hashing.hpp:24-43).  Falls back to EXACT by
- *                       itself for planes / centerings outside the bound's premises (non-finite or huge values).
+ *   TENSOR (default):   a filter on the tensor cores (tcgen05.mma kind::i8): the planes as three int8 limbs of a 23-bit
+ *                       fixed-point value, exact s32 accumulators in tensor memory, an a-priori error bound in fp64; the
+ *                       dots it cannot prove (|value| below the bound, ~7e-6 of them, ties included) are re-evaluated in
+ *                       the reference's fp64 operation order (reduce_dot, hashing.hpp:24-43).
+ *   FILTERED:           the same contract with an fp32 SIMT contraction (bound ~45x wider, ~1.5e-4 undecided).
  *   EXACT:              every dot in the reference's fp64 operation order.
- *   TENSOR:             the FILTERED contract with the filter on the tensor cores (tcgen05.mma kind::i8): the planes as
- *                       three int8 limbs of a 23-bit fixed-point value, exact s32 accumulators in tensor memory, a bound
- *                       ~45x tighter than the fp32 one; undecided dots go to the same exact path.
- * The environment variables CHGPU_HASH_EXACT=1 / CHGPU_HASH_TENSOR=1 select EXACT / TENSOR for new contexts. */
+ * Both filters fall back to EXACT by themselves for planes / centerings outside the bound's premises (non-finite or
+ * huge values).  CHGPU_HASH_FP32=1 / CHGPU_HASH_EXACT=1 select FILTERED / EXACT for new contexts. */
 typedef enum chgpu_hash_mode { CHGPU_HASH_FILTERED = 0, CHGPU_HASH_EXACT = 1, CHGPU_HASH_TENSOR = 2 } chgpu_hash_mode;
 typedef struct chgpu_hash_stats {
     uint64_t undecided_dots;      /* dots the filter handed to the exact path (cumulative per context) */

@@ -682,8 +682,8 @@ class Matcher:
         self._ck(self.lib.chgpu_hash_images(self.h, ids.ctypes.data_as(N.u32p), len(ids), reduce_rounds))
 
     def set_hash_mode(self, exact):
-        """False / 0: fp32 filter + exact fp64 fixup (default); True / 1: every dot in the reference's fp64 order;
-        2 or "tensor": the filter on the tensor cores (tcgen05 int8 limbs), same exact fixup."""
+        """2 or "tensor": the filter on the tensor cores (tcgen05 int8 limbs) + exact fp64 fixup (the context's default);
+        False / 0: the fp32 SIMT filter, same fixup; True / 1: every dot in the reference's fp64 order."""
         mode = 2 if exact in (2, "tensor") else (1 if exact else 0)
         self._ck(self.lib.chgpu_set_hash_mode(self.h, mode))
 

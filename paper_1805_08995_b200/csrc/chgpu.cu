@@ -1269,8 +1269,10 @@ chgpu_status chgpu_create(int device, chgpu_ctx** out) {
     ok &= cudaMalloc(&ctx->d_hq_count, sizeof(unsigned int)) == cudaSuccess;
     ok &= cudaMalloc(&ctx->d_hstats, sizeof(HashFilterStats)) == cudaSuccess;
     ok &= cudaMemset(ctx->d_hstats, 0, sizeof(HashFilterStats)) == cudaSuccess;
-    if (const char* e = getenv("CHGPU_HASH_EXACT")) ctx->hash_mode = (e[0] == '1') ? CHGPU_HASH_EXACT : CHGPU_HASH_FILTERED;
-    if (const char* e = getenv("CHGPU_HASH_TENSOR")) if (e[0] == '1') ctx->hash_mode = CHGPU_HASH_TENSOR;
+    // default: the tensor-core filter (K1t); CHGPU_HASH_FP32=1 / CHGPU_HASH_EXACT=1 select the fp32 filter / the exact kernel
+    ctx->hash_mode = CHGPU_HASH_TENSOR;
+    if (const char* e = getenv("CHGPU_HASH_FP32")) if (e[0] == '1') ctx->hash_mode = CHGPU_HASH_FILTERED;
+    if (const char* e = getenv("CHGPU_HASH_EXACT")) if (e[0] == '1') ctx->hash_mode = CHGPU_HASH_EXACT;
     if (!ok) return bail(CHGPU_ECUDA);
     *out = ctx;
     return CHGPU_OK;

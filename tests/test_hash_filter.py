@@ -26,7 +26,7 @@ def oracle():
 def mode(request, matcher):
     """Every test runs under both filters; the context goes back to the default afterwards."""
     yield request.param
-    matcher.set_hash_mode(0)
+    matcher.set_hash_mode(2)  # the context's default
 
 
 def install(matcher, fam, mode=0):
