@@ -35,6 +35,7 @@
 #include "dev_types.cuh"
 #include "hash_kernels.cuh"
 #include "hash_tc.cuh"
+#include "join_kernels.cuh"
 #include "compact_kernels.cuh"
 #include "match_launch.cuh"
 
@@ -210,6 +211,9 @@ struct chgpu_ctx {
     uint16_t* d_act = nullptr;    // tiled train images: active queries per (query image, tile) pair
     uint32_t* d_nact = nullptr;
     size_t act_cap = 0, nact_cap = 0;
+    uint8_t* d_hit = nullptr;     // join pass: one flag per query of a sub-batch
+    size_t hit_cap = 0;
+    bool join_enabled = true;     // tensor-core Hamming pass in front of the match kernel (CHGPU_NO_JOIN=1 switches it off)
     MatchBuffers mb[2];
     DevStats* d_stats = nullptr;
     DevStats* h_stats = nullptr;  // pinned
@@ -290,7 +294,7 @@ size_t tile_block_bytes(uint32_t n, uint32_t m, uint32_t L, uint32_t ntiles, uin
     return o;
 }
 
-size_t image_block_bytes(uint32_t n, uint32_t m, uint32_t L, size_t off[7]) {
+size_t image_block_bytes(uint32_t n, uint32_t m, uint32_t L, size_t off[9], bool sorted_copies) {
     size_t o = 0;
     off[0] = o; o += align_up(size_t(n) * kDim);
     off[1] = o; o += align_up(size_t(n) * 16);
@@ -300,6 +304,11 @@ size_t image_block_bytes(uint32_t n, uint32_t m, uint32_t L, size_t off[7]) {
     off[5] = o; o += align_up(size_t(L) * n * 2);
     off[6] = o; o += align_up(size_t(L) * n * 2);
     o += kAlign;  // slack: the match kernel may read one id past an empty last bucket
+    off[7] = off[8] = 0;
+    if (sorted_copies) {  // bucket-sorted codes of the join pass (DevImage::scodes, spop)
+        off[7] = o; o += align_up(size_t(L) * n * 32);
+        off[8] = o; o += align_up(size_t(L) * n * 2);
+    }
     return std::max(o, kAlign);
 }
 
@@ -447,9 +456,10 @@ chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t
         give_back();
         return s;
     }
-    size_t off[7];
+    size_t off[9];
     std::vector<size_t> toff;
-    const size_t own = image_block_bytes(n, m, L, off);
+    const bool sorted_copies = ntiles == 0 && n != 0;
+    const size_t own = image_block_bytes(n, m, L, off, sorted_copies);
     const size_t bytes = own + tile_block_bytes(n, m, L, ntiles, tp, &toff);
     char* block = nullptr;
     const cudaError_t e = ctx->arena.alloc(bytes, &block);
@@ -470,6 +480,8 @@ chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t
     r.dev.offs = reinterpret_cast<uint32_t*>(block + off[4]);
     r.dev.points = reinterpret_cast<uint16_t*>(block + off[5]);
     r.dev.scan = reinterpret_cast<uint16_t*>(block + off[6]);
+    r.dev.scodes = sorted_copies ? reinterpret_cast<uint4*>(block + off[7]) : nullptr;
+    r.dev.spop = sorted_copies ? reinterpret_cast<int16_t*>(block + off[8]) : nullptr;
     r.dev.n = n;
     r.dev.flags = 0;
     r.tile_slots = tile_slots;
@@ -486,6 +498,8 @@ chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t
         t.dev.offs = reinterpret_cast<uint32_t*>(block + own + toff[3 * k]);
         t.dev.points = reinterpret_cast<uint16_t*>(block + own + toff[3 * k + 1]);
         t.dev.scan = reinterpret_cast<uint16_t*>(block + own + toff[3 * k + 2]);
+        t.dev.scodes = nullptr;
+        t.dev.spop = nullptr;
         t.dev.n = std::min(tp, n - k * tp);
         t.dev.flags = 0;
         if (const chgpu_status s = publish_slot(ctx, tile_slots[k])) return s;
@@ -890,7 +904,7 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
                 subs.push_back(cur);
                 cur = SubBatch{k, 0, 0, 0, 0, false, 0, 0};
             }
-            descs[k] = PairDesc{si, sj, cur.queries, 0u, 0u, cur.count, 0u};
+            descs[k] = PairDesc{si, sj, cur.queries, 0u, 0u, cur.count, uint32_t(cur.queries)};  // (act_off: join pass)
             cur.tiled = tiled;
             cur.max_tiles = std::max(cur.max_tiles, tiles);
             cur.tile_pairs += tiles;
@@ -1158,6 +1172,63 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
             CK(cudaEventRecord(b.ev_k1, ctx->compute));
             st.match_launches += 2;
             st.total_launches += 3;
+        } else if (ctx->join_enabled && smem_train && !run.fmats && !run.dbg_ranked && sb.queries <= UINT32_MAX) {
+            // Tensor-core Hamming pass (join_kernels.cuh): which queries have a candidate within tau at all; the match
+            // kernel then visits those only.  Every other query keeps the "no match" the scratch is initialised with.
+            if (ctx->hit_cap < sb.queries || ctx->act_cap < sb.queries || ctx->nact_cap < sb.count) {
+                CK(cudaStreamSynchronize(ctx->compute));
+                if (ctx->hit_cap < sb.queries) {
+                    cudaFree(ctx->d_hit);
+                    ctx->d_hit = nullptr;
+                    ctx->hit_cap = 0;
+                    CK(cudaMalloc(&ctx->d_hit, sb.queries));
+                    ctx->hit_cap = sb.queries;
+                }
+                if (ctx->act_cap < sb.queries) {
+                    cudaFree(ctx->d_act);
+                    ctx->d_act = nullptr;
+                    ctx->act_cap = 0;
+                    CK(cudaMalloc(&ctx->d_act, std::max<size_t>(sb.queries, 8) * sizeof(uint16_t)));
+                    ctx->act_cap = std::max<size_t>(sb.queries, 8);
+                }
+                if (ctx->nact_cap < sb.count) {
+                    cudaFree(ctx->d_nact);
+                    ctx->d_nact = nullptr;
+                    ctx->nact_cap = 0;
+                    CK(cudaMalloc(&ctx->d_nact, size_t(sb.count) * sizeof(uint32_t)));
+                    ctx->nact_cap = sb.count;
+                }
+            }
+            CK(cudaEventRecord(b.ev_k0, ctx->compute));
+            CK(cudaMemsetAsync(ctx->d_hit, 0, sb.queries, ctx->compute));
+            CK(cudaMemsetAsync(ctx->d_res, 0xff, sb.queries * sizeof(uint2), ctx->compute));
+            JoinParams JP{};
+            JP.images = ctx->d_images;
+            JP.pairs = b.d_pairs;
+            JP.npairs = sb.count;
+            JP.m = ctx->fam.short_bits;
+            JP.L = ctx->fam.table_count;
+            JP.tau = run.cfg.hamming_threshold;
+            JP.hit = ctx->d_hit;
+            JP.stats = ctx->d_stats;
+            JP.counter = ctx->d_counter;
+            const uint32_t jcells = JP.L << JP.m;
+            const uint64_t junits = uint64_t(sb.count) * ((jcells + 31) / 32);
+            const uint32_t jgrid = uint32_t(std::min<uint64_t>((junits + kJoinThreads / 32 - 1) / (kJoinThreads / 32),
+                                                               uint64_t(ctx->prop.multiProcessorCount) * 8));
+            join_hits_kernel<<<std::max(jgrid, 1u), kJoinThreads, 0, ctx->compute>>>(JP);
+            CK(cudaGetLastError());
+            join_compact_kernel<<<(sb.count + 7) / 8, 256, 0, ctx->compute>>>(ctx->d_images, b.d_pairs, sb.count, ctx->d_hit,
+                                                                                ctx->d_act, ctx->d_nact);
+            CK(cudaGetLastError());
+            CK(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), ctx->compute));
+            P.act = ctx->d_act;
+            P.nact = ctx->d_nact;
+            P.smem_long_bytes = std::max<uint32_t>(sb.max_nt * 16u, 16u);
+            const size_t smem = size_t(P.smem_long_bytes) + offs_smem_bytes(ctx) + stage_smem_bytes(ctx, false);
+            CK(launch_match_active(P, smem, ctx->prop.multiProcessorCount, ctx->compute, &grid));
+            CK(cudaEventRecord(b.ev_k1, ctx->compute));
+            st.total_launches += 2;  // join + list kernels (match_launches keeps counting sub-batches)
         } else {
             CK(cudaEventRecord(b.ev_k0, ctx->compute));
             CK(launch_match(ctx, P, smem_train, sb.max_nt, &grid));
@@ -1269,6 +1340,7 @@ chgpu_status chgpu_create(int device, chgpu_ctx** out) {
     ok &= cudaMalloc(&ctx->d_hq_count, sizeof(unsigned int)) == cudaSuccess;
     ok &= cudaMalloc(&ctx->d_hstats, sizeof(HashFilterStats)) == cudaSuccess;
     ok &= cudaMemset(ctx->d_hstats, 0, sizeof(HashFilterStats)) == cudaSuccess;
+    if (const char* e = getenv("CHGPU_NO_JOIN")) if (e[0] == '1') ctx->join_enabled = false;
     // default: the tensor-core filter (K1t); CHGPU_HASH_FP32=1 / CHGPU_HASH_EXACT=1 select the fp32 filter / the exact kernel
     ctx->hash_mode = CHGPU_HASH_TENSOR;
     if (const char* e = getenv("CHGPU_HASH_FP32")) if (e[0] == '1') ctx->hash_mode = CHGPU_HASH_FILTERED;
@@ -1299,7 +1371,7 @@ void chgpu_destroy(chgpu_ctx* ctx) {
     }
     cudaFree(ctx->d_planes); cudaFree(ctx->d_centering); cudaFree(ctx->d_sums); cudaFree(ctx->d_res);
     cudaFree(ctx->d_stats); cudaFreeHost(ctx->h_stats); cudaFree(ctx->d_counter); cudaFree(ctx->d_slots);
-    cudaFree(ctx->d_dbg); cudaFree(ctx->d_gmin); cudaFree(ctx->d_gdone); cudaFree(ctx->d_lists); cudaFree(ctx->d_act); cudaFree(ctx->d_nact);
+    cudaFree(ctx->d_dbg); cudaFree(ctx->d_gmin); cudaFree(ctx->d_gdone); cudaFree(ctx->d_lists); cudaFree(ctx->d_act); cudaFree(ctx->d_nact); cudaFree(ctx->d_hit);
     cudaFreeHost(ctx->load_pinned);
     cudaFree(ctx->load_region);
     cudaFreeHost(ctx->h_split_jobs);

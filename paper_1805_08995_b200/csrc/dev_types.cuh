@@ -23,6 +23,11 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 //   scan   L x n u16           the same buckets in the order the match kernel walks them: ids dealt
 //                              round-robin over (id mod 8), so that 8 consecutive entries gather their
 //                              16-byte codes from 8 different shared-memory bank groups
+//   scodes 2 x L x n uint4     (images the join pass handles: not tiled) the long codes in bucket order of every table,
+//                              entry p of table t = point points[t*n + p]; first the codes as they are, then (L*n entries
+//                              on) with the bits of every byte reversed — the train-side operand of the tensor-core
+//                              Hamming pass
+//   spop   L x n i16           64 x popcount of the same codes (the join pass's column penalty / row threshold)
 struct DevImage {
     const uint8_t* desc;
     const float4* kp;
@@ -31,6 +36,8 @@ struct DevImage {
     uint32_t* offs;
     uint16_t* points;
     uint16_t* scan;
+    uint4* scodes;   // nullptr: no bucket-sorted copies (tiled images, tiles)
+    int16_t* spop;
     uint32_t n;
     uint32_t flags;  // bit0: codes + buckets valid
 };

@@ -539,6 +539,22 @@ __global__ void bucket_build_kernel(const DevImage* __restrict__ images, const u
         __syncwarp();
     }
 
+    // Bucket-sorted copies of the long codes for the join pass (join_kernels.cuh): entry p of this table = the code of point
+    // pts[p], plain and with the bits of every byte reversed, and its popcount.
+    if (img.scodes != nullptr) {
+        __syncwarp();
+        uint4* sc = img.scodes + uint64_t(t) * n;             // plain copies: L x n
+        uint4* sr = img.scodes + uint64_t(L + t) * n;         // reversed copies behind them: L x n
+        int16_t* sp = img.spop + uint64_t(t) * n;
+        for (uint32_t p = lane; p < n; p += 32) {
+            const uint4 c = img.longs[pts[p]];
+            sc[p] = c;
+            sr[p] = make_uint4(__byte_perm(__brev(c.x), 0, 0x0123), __byte_perm(__brev(c.y), 0, 0x0123),
+                               __byte_perm(__brev(c.z), 0, 0x0123), __byte_perm(__brev(c.w), 0, 0x0123));
+            sp[p] = int16_t(64 * (__popc(c.x) + __popc(c.y) + __popc(c.z) + __popc(c.w)));
+        }
+    }
+
     // Pass 3: scan order.  The match kernel gathers the 16-byte codes of 8 consecutive bucket entries
     // with one quarter-warp LDS.128; the gather is conflict-free iff their ids differ mod 8.  Entries are
     // re-dealt by (rank inside the residue class, residue): the first min-count rounds hold all 8

@@ -1,0 +1,8 @@
+// match_active.cu — the match kernel over the queries the join pass (join_kernels.cuh) found a candidate within tau for.
+#include "match_launch.cuh"
+
+namespace chgpu {
+cudaError_t launch_match_active(const MatchParams& P, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid) {
+    return launch_match_any<true, false, kModeMatchActive>(P, smem, sm_count, stream, grid);
+}
+}  // namespace chgpu

@@ -123,6 +123,10 @@ struct MatchParams {
 // tile_merge_kernel then merges the lists of a query, applies the threshold / re-rank rule of
 // matcher.cpp:176-189 to the merged ranking and verifies it exactly like MODE 0 does.
 constexpr int kModeMatch = 0, kModeTileMin = 1, kModeTileTopK = 2;
+// kModeMatchActive: kModeMatch over the queries the join pass (join_kernels.cuh) found a candidate within tau for — the
+// pair's list P.act / P.nact, ascending query indices; every other query keeps the "no match" of the initialised scratch
+// and the raw-candidate statistic has been taken by the join pass.
+constexpr int kModeMatchActive = 3;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -592,6 +596,8 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
     __shared__ __align__(8) uint64_t s_bar;
 
     constexpr int KS = LT + kOverSlots;
+    constexpr bool kMatch = MODE == kModeMatch || MODE == kModeMatchActive;    // the reference's match semantics
+    constexpr bool kActive = MODE == kModeTileTopK || MODE == kModeMatchActive;  // walks the pair's active-query list
     constexpr uint32_t kWarps = kMatchThreads / 32;
     constexpr uint32_t FULL = 0xffffffffu;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -647,17 +653,17 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 
         // query range of this unit: chunks are multiples of 32 queries
         // (MODE 2 walks positions of the pair's active-query list instead of query indices)
-        const uint32_t nq_unit = MODE == kModeTileTopK ? __ldg(P.nact + pair) : I.n;
+        const uint32_t nq_unit = kActive ? __ldg(P.nact + pair) : I.n;
         const uint32_t qc = (((nq_unit + P.chunks_per_pair - 1) / P.chunks_per_pair) + 31u) & ~31u;
         const uint32_t q0 = min(nq_unit, chunk * qc), q1 = min(nq_unit, q0 + qc);
-        const uint16_t* __restrict__ act = MODE == kModeTileTopK ? P.act + pd.act_off : nullptr;
+        const uint16_t* __restrict__ act = kActive ? P.act + pd.act_off : nullptr;
         uint32_t qa_lane = 0;  // MODE 2: the query index behind batch position `lane`
         const uint16_t* __restrict__ ids = CH_IDS(J);
 
         uint32_t st_raw = 0, st_vq = 0, st_dist = 0, st_match = 0;
 
         if (J.n == 0) {
-            if (MODE == kModeMatch)
+            if (MODE == kModeMatch)  // (kModeMatchActive: the scratch was initialised with "no match")
                 for (uint32_t q = q0 + tid; q < q1; q += kMatchThreads) __stcs(P.res + pd.res_off + q, make_uint2(kNone, 0u));
         } else {
             // ---- 1. bucket lookup, kBatch queries at a time, one query per lane -------------------
@@ -668,7 +674,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                 const uint32_t qpos = qb + lane * kWarps;
                 const bool live = lane < kBatch && qpos < q1;
                 uint32_t q = qpos;
-                if (MODE == kModeTileTopK) {
+                if (kActive) {
                     q = live ? uint32_t(__ldg(act + qpos)) : 0u;
                     qa_lane = q;
                 }
@@ -709,7 +715,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                     }
                     const uint32_t base1 = __popc(m0), base2 = base1 + __popc(m1);
                     sts128(rec + 16u, make_uint4(min(pre, 255u) | (empty << 8) | (base1 << 16) | (base2 << 24), m0, m1, m2));
-                    if (MODE != kModeTileTopK) st_raw += total;  // per lane; reduced over the warp when the unit ends
+                    if (!kActive) st_raw += total;  // per lane; reduced over the warp when the unit ends
                 }
                 __syncwarp();
             };
@@ -754,7 +760,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 
                 constexpr bool skip = false;
                 bool emit = MODE == kModeTileTopK;  // this (query, tile) writes its list
-                const uint32_t qa = MODE == kModeTileTopK ? __shfl_sync(FULL, qa_lane, slot) : q;  // the query's index
+                const uint32_t qa = kActive ? __shfl_sync(FULL, qa_lane, slot) : q;  // the query's index
                 if (skip) {
                 } else if (tover <= 32u * kOverSlots) {
                     // ---- 2. Hamming scan: the first 32 entries of every bucket, one table per slot,
@@ -812,7 +818,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                         emit = (k0 >> 24) <= P.tau && P.fmats == nullptr;
                     }
                     if (MODE == kModeTileMin && !emit) {
-                    } else if (MODE != kModeMatch) {
+                    } else if (!kMatch) {
                         // the tile's top_k smallest distinct keys, whatever their distance
                         uint32_t prev = k0;
                         while (prev != kNone) {
@@ -826,7 +832,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                         // keys within tau, in order (usually this loop ends at its first pull)
                         uint32_t a1;  // this lane's own smallest key above k0
 #ifndef CHGPU_NO_RERANK_SHORTCUT
-                        const FirstRow first = load_first_row(I.desc, J.desc, q, k0, lane);  // travels under the first pull
+                        const FirstRow first = load_first_row(I.desc, J.desc, qa, k0, lane);  // travels under the first pull
 #endif
                         uint32_t nk = next_key_keep(key, k0, a1);
 #ifndef CHGPU_NO_RERANK_SHORTCUT
@@ -887,7 +893,7 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                         emit = (gmin >> 24) <= P.tau && P.fmats == nullptr;
                     }
                     if (MODE == kModeTileMin && !emit) {
-                    } else if (MODE != kModeMatch || (gmin >> 24) <= P.tau) {
+                    } else if (!kMatch || (gmin >> 24) <= P.tau) {
                         // pass 2: merge every round into the running top-k (ascending, unique)
                         if (GUIDED) {
                             line = epipolar_band(P.fmats + uint64_t(pd.pair_idx) * 9, __ldg(I.kp + qa));
@@ -923,40 +929,40 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
                         const bool anycut = (__reduce_max_sync(FULL, lmax) >> 24) > P.tau;
                         const uint32_t tot = __popc(__ballot_sync(FULL, mykey != kNone));
                         const uint32_t s = __popc(__ballot_sync(FULL, mykey != kNone && (mykey >> 24) <= P.tau));
-                        n = (MODE == kModeMatch && (s >= P.min_ranked || !anycut)) ? s : tot;
-                        if (GUIDED && MODE == kModeMatch && s == 0) n = 0;  // the band removed everything within tau: no ranking, no fallback
+                        n = (kMatch && (s >= P.min_ranked || !anycut)) ? s : tot;
+                        if (GUIDED && kMatch && s == 0) n = 0;  // the band removed everything within tau: no ranking, no fallback
                     }
                 }
 
-                if (MODE != kModeMatch && emit) {
+                if (!kMatch && emit) {
                     if (lane < P.top_k)
                         P.lists[(pd.res_off + qa) * P.list_stride + pd.tile_idx * P.top_k + lane] = lane < n ? mykey + pd.tile_base : kNone;
                     if (MODE == kModeTileMin && lane == 0) atomicOr(P.gdone + pd.res_off + q, 1ull << pd.tile_idx);
                 }
 
-                if (DBG && MODE == kModeMatch) {
-                    if (lane < n) P.dbg_ranked[uint64_t(q) * P.top_k + lane] = mykey & 0xffffffu;
-                    if (lane == 0) P.dbg_count[q] = n;
+                if (DBG && kMatch) {
+                    if (lane < n) P.dbg_ranked[uint64_t(qa) * P.top_k + lane] = mykey & 0xffffffu;
+                    if (lane == 0) P.dbg_count[qa] = n;
                 }
 
                 // ---- 4. verification (euclidean_verify, matcher.cpp:115-137) ------------------
 #ifdef CHGPU_SHORTCUT_STATS
                 // experiment (scripts/exp7.sh): verified_queries = re-rank cases, distances = count checks passed, matches of
                 // the pair counts = accepted by the shortcut
-                if (MODE == kModeMatch && attempted) {
+                if (kMatch && attempted) {
                     st_vq += 1;
                     st_dist += (decided || out_d == 1) ? 1 : 0;
                     st_match += decided ? 1 : 0;
                 }
                 if (false) {
 #else
-                if (MODE == kModeMatch && n >= 2) {
+                if (kMatch && n >= 2) {
 #endif
                     st_vq += 1;
                     st_dist += n;
-                    if (decided || verify_ranked(I.desc, J.desc, q, n, mykey, lane, P.ratio_sq, out_t, out_d)) st_match += 1;
+                    if (decided || verify_ranked(I.desc, J.desc, qa, n, mykey, lane, P.ratio_sq, out_t, out_d)) st_match += 1;
                 }
-                if (MODE == kModeMatch && lane == 0) __stcs(P.res + pd.res_off + q, make_uint2(out_t, out_d));
+                if (kMatch && lane == 0) __stcs(P.res + pd.res_off + qa, make_uint2(out_t, out_d));
 
                 // batch boundary: resolve the next kBatch queries (this one's ranges are in registers)
                 if (slot == kBatch - 1 && q + kWarps < q1) {

@@ -21,6 +21,8 @@ cudaError_t launch_match_dbg(const MatchParams& P, bool smem_train, size_t smem,
 cudaError_t launch_match_tiled(const MatchParams& P, int mode, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid);
 cudaError_t launch_tile_compact(const MatchParams& P, uint32_t ntile_pairs, cudaStream_t stream);  // P.pairs = tile pairs
 cudaError_t launch_tile_merge(const MatchParams& P, uint32_t npairs, uint32_t max_nq, cudaStream_t stream);
+// The match kernel over the hit queries the join pass listed (P.act / P.nact; match_active.cu): train codes in shared memory.
+cudaError_t launch_match_active(const MatchParams& P, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid);
 // Table slots (LT) the launchers pick for L tables; the staging area is sized with it.
 inline int match_table_slots(uint32_t L, bool guided) { return guided ? (L == 6 ? 6 : 8) : (L <= 4 ? 4 : (L <= 6 ? 6 : 8)); }
 
@@ -40,17 +42,17 @@ cudaError_t launch_match_variant(const MatchParams& P, size_t smem, int sm_count
     return cudaGetLastError();
 }
 
-template <bool SMEM, bool DBG = false>
+template <bool SMEM, bool DBG = false, int MODE = kModeMatch>
 cudaError_t launch_match_any(const MatchParams& P, size_t smem, int sm_count, cudaStream_t stream, uint32_t* grid) {
     switch (P.L) {
-        case 4: return launch_match_variant<SMEM, 4, true, false, kModeMatch, DBG>(P, smem, sm_count, stream, grid);
-        case 6: return launch_match_variant<SMEM, 6, true, false, kModeMatch, DBG>(P, smem, sm_count, stream, grid);
-        case 8: return launch_match_variant<SMEM, 8, true, false, kModeMatch, DBG>(P, smem, sm_count, stream, grid);
+        case 4: return launch_match_variant<SMEM, 4, true, false, MODE, DBG>(P, smem, sm_count, stream, grid);
+        case 6: return launch_match_variant<SMEM, 6, true, false, MODE, DBG>(P, smem, sm_count, stream, grid);
+        case 8: return launch_match_variant<SMEM, 8, true, false, MODE, DBG>(P, smem, sm_count, stream, grid);
         default: break;
     }
-    if (P.L < 4) return launch_match_variant<SMEM, 4, false, false, kModeMatch, DBG>(P, smem, sm_count, stream, grid);
-    if (P.L < 6) return launch_match_variant<SMEM, 6, false, false, kModeMatch, DBG>(P, smem, sm_count, stream, grid);
-    return launch_match_variant<SMEM, 8, false, false, kModeMatch, DBG>(P, smem, sm_count, stream, grid);
+    if (P.L < 4) return launch_match_variant<SMEM, 4, false, false, MODE, DBG>(P, smem, sm_count, stream, grid);
+    if (P.L < 6) return launch_match_variant<SMEM, 6, false, false, MODE, DBG>(P, smem, sm_count, stream, grid);
+    return launch_match_variant<SMEM, 8, false, false, MODE, DBG>(P, smem, sm_count, stream, grid);
 }
 
 }  // namespace chgpu

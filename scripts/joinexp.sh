@@ -1,0 +1,17 @@
+t() { ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file /tmp/jl.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --images 200 --pairs 7992 > /dev/null 2>&1
+python - <<PY
+import csv,collections
+rows=[r for r in csv.reader(open("/tmp/jl.csv")) if len(r)>10]
+hdr=rows[0]; ki=hdr.index("Kernel Name"); vi=hdr.index("Metric Value")
+agg=collections.defaultdict(list)
+for r in rows[1:]:
+    agg[r[ki][:30]].append(float(r[vi].replace(",","")))
+print("RESULT $1", {k.split("(")[0]: round(v[-1]/1e3,2) for k,v in agg.items() if "join" in k or "match_kernel" in k})
+PY
+}
+b() { CHGPU_NVCC_EXTRA="$1" python -m paper_1805_08995_b200.build --force > /dev/null 2>&1; }
+python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "match or golden or edge or pair_cases or config2" 2>&1 | tail -2
+t occ2_default
+b "-DCHGPU_JOIN_OCC=3"; t occ3
+b "-DCHGPU_JOIN_OCC=1"; t occ1
+b ""; 
