@@ -214,6 +214,7 @@ struct chgpu_ctx {
     uint8_t* d_hit = nullptr;     // join pass: one flag per query of a sub-batch
     size_t hit_cap = 0;
     bool join_enabled = true;     // tensor-core Hamming pass in front of the match kernel (CHGPU_NO_JOIN=1 switches it off)
+    uint32_t join_min_bucket = 20;  // ... for sub-batches whose images average at least this many points per bucket
     MatchBuffers mb[2];
     DevStats* d_stats = nullptr;
     DevStats* h_stats = nullptr;  // pinned
@@ -767,6 +768,10 @@ struct SubBatch {
     // train images larger than the shared-memory tile: matched tile by tile (match_kernels.cuh MODE 1 / 2 + merge)
     bool tiled;
     uint32_t max_tiles, tile_pairs;
+    // the join pass needs the bucket-sorted code copies of every image of the sub-batch (DevImage::scodes: not kept for
+    // images that are matched through tiles, whichever side of a pair they are on) and buckets large enough to fill its tiles
+    bool no_join = false;
+    uint64_t train_points = 0;
 };
 constexpr uint64_t kTileListBytes = uint64_t(1) << 30;  // cap of the per-query list scratch of a tiled sub-batch
 
@@ -906,6 +911,8 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
             }
             descs[k] = PairDesc{si, sj, cur.queries, 0u, 0u, cur.count, uint32_t(cur.queries)};  // (act_off: join pass)
             cur.tiled = tiled;
+            cur.no_join = cur.no_join || (I.n != 0 && I.scodes == nullptr) || (J.n != 0 && J.scodes == nullptr);
+            cur.train_points += J.n;
             cur.max_tiles = std::max(cur.max_tiles, tiles);
             cur.tile_pairs += tiles;
             cur.count += 1;
@@ -1172,7 +1179,11 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
             CK(cudaEventRecord(b.ev_k1, ctx->compute));
             st.match_launches += 2;
             st.total_launches += 3;
-        } else if (ctx->join_enabled && smem_train && !run.fmats && !run.dbg_ranked && sb.queries <= UINT32_MAX) {
+        } else if (ctx->join_enabled && !sb.no_join && smem_train && !run.fmats && !run.dbg_ranked && sb.queries <= UINT32_MAX &&
+                   // the pass works on 16 x 8 tiles of a bucket's queries x train points: it pays from ~20 points per bucket
+                   // on both sides (measured: +6 % at 24, +9 % at 32, -4 % at 16, -36 % at 4 per bucket; scripts/sweep.py)
+                   ((sb.queries / sb.count) >> ctx->fam.short_bits) >= ctx->join_min_bucket &&
+                   ((sb.train_points / sb.count) >> ctx->fam.short_bits) >= ctx->join_min_bucket) {
             // Tensor-core Hamming pass (join_kernels.cuh): which queries have a candidate within tau at all; the match
             // kernel then visits those only.  Every other query keeps the "no match" the scratch is initialised with.
             if (ctx->hit_cap < sb.queries || ctx->act_cap < sb.queries || ctx->nact_cap < sb.count) {
@@ -1341,6 +1352,7 @@ chgpu_status chgpu_create(int device, chgpu_ctx** out) {
     ok &= cudaMalloc(&ctx->d_hstats, sizeof(HashFilterStats)) == cudaSuccess;
     ok &= cudaMemset(ctx->d_hstats, 0, sizeof(HashFilterStats)) == cudaSuccess;
     if (const char* e = getenv("CHGPU_NO_JOIN")) if (e[0] == '1') ctx->join_enabled = false;
+    if (const char* e = getenv("CHGPU_JOIN_MIN_BUCKET")) ctx->join_min_bucket = uint32_t(std::max(0, atoi(e)));
     // default: the tensor-core filter (K1t); CHGPU_HASH_FP32=1 / CHGPU_HASH_EXACT=1 select the fp32 filter / the exact kernel
     ctx->hash_mode = CHGPU_HASH_TENSOR;
     if (const char* e = getenv("CHGPU_HASH_FP32")) if (e[0] == '1') ctx->hash_mode = CHGPU_HASH_FILTERED;

@@ -621,6 +621,11 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
     }
     uint32_t bar_parity = 0;
     uint32_t resident = kNone;
+    // The re-rank shortcut pays when its partial-distance bound usually holds (uniform descriptors: 72 % of the attempts
+    // decide the query) and costs when it rarely does (SIFT-shaped descriptors: the first 16 dimensions of a random pair
+    // are too close for the bound, 0.5 %).  Every warp keeps score and stops trying once, after 64 attempts, fewer than
+    // half have decided their query; a launch starts over.  Results never depend on it — only who computes them.
+    uint32_t sc_try = 0, sc_ok = 0;
 
     for (;;) {
         if (tid == 0) s_unit = atomicAdd(P.unit_counter, 1u);
@@ -841,10 +846,13 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 #ifdef CHGPU_SHORTCUT_STATS
                         attempted = !DBG && nk != kNone && (nk >> 24) > P.tau;
 #endif
-                        if (!DBG && nk != kNone && (nk >> 24) > P.tau &&
-                            rerank_shortcut(key, k0, a1, P.top_k, first, J.desc, lane, P.ratio_sq, out_t, out_d)) {
-                            decided = true;
-                            n = P.top_k;
+                        if (!DBG && nk != kNone && (nk >> 24) > P.tau && (sc_try < 64u || 2u * sc_ok >= sc_try)) {
+                            ++sc_try;
+                            if (rerank_shortcut(key, k0, a1, P.top_k, first, J.desc, lane, P.ratio_sq, out_t, out_d)) {
+                                ++sc_ok;
+                                decided = true;
+                                n = P.top_k;
+                            }
                         }
 #endif
                         if (!decided) {

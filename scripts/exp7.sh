@@ -1,9 +1,10 @@
 # how often the re-rank shortcut is attempted / passes its count check / decides the query (experiment build)
 CHGPU_NVCC_EXTRA="-DCHGPU_SHORTCUT_STATS" python -m paper_1805_08995_b200.build --force > /dev/null 2>&1
-python - <<'PY'
+CHGPU_NO_JOIN=1 python - <<'PY'
 import numpy as np, paper_1805_08995_b200 as ch
 m = ch.Matcher(0); fam = ch.build_hash_family(ch.FamilyParams()); m.set_family(fam)
-d = ch.make_dataset(64, 8192, seed=7)
+import os
+d = ch.make_dataset(64, 8192, seed=7, shape=os.environ.get("SHAPE", "uniform"))
 ids = np.arange(64, dtype=np.uint32)
 m.upload_many(ids, d); m.centering_reset(); m.centering_add_many(ids); m.centering_apply(); m.hash(ids)
 pairs = ch.plan_exhaustive(64, 50, 4)
