@@ -110,6 +110,12 @@ chgpu_status chgpu_sync(chgpu_ctx* ctx);
 /* Tuning knob: upper bound on the sum of query points per sub-batch (one match-kernel launch);
  * 0 restores the default (32 Mi).  Results never depend on it. */
 chgpu_status chgpu_set_sub_batch_queries(chgpu_ctx* ctx, uint64_t max_queries);
+/* The tensor-core Hamming pass in front of the match kernel (csrc/join_kernels.cuh; no reference counterpart: it computes
+ * which queries of a pair have a candidate within hamming_threshold, matcher.cpp:164-175, the match kernel then visits those
+ * only; results are the same records).  enabled = 0 switches it off; min_points_per_bucket = the average bucket occupancy
+ * (points >> short_bits, both images of a pair) from which a sub-batch takes it (default 20; 0 = always, what the parity
+ * tests use).  CHGPU_NO_JOIN=1 / CHGPU_JOIN_MIN_BUCKET=n set the same for new contexts. */
+chgpu_status chgpu_set_join(chgpu_ctx* ctx, int enabled, uint32_t min_points_per_bucket);
 /* Pinned host memory for zero-staging uploads / result sinks. */
 chgpu_status chgpu_host_alloc(chgpu_ctx* ctx, size_t bytes, void** out);
 chgpu_status chgpu_host_free(chgpu_ctx* ctx, void* p);

@@ -449,6 +449,10 @@ class Matcher:
     def sync(self):
         self._ck(self.lib.chgpu_sync(self.h))
 
+    def set_join(self, enabled: bool = True, min_points_per_bucket: int = 20):
+        """The tensor-core Hamming pass in front of the match kernel: off / on from this average bucket occupancy (0: always)."""
+        self._ck(self.lib.chgpu_set_join(self.h, 1 if enabled else 0, min_points_per_bucket))
+
     def set_sub_batch_queries(self, max_queries: int):
         self._ck(self.lib.chgpu_set_sub_batch_queries(self.h, max_queries))
 

@@ -1429,6 +1429,13 @@ chgpu_status chgpu_sync(chgpu_ctx* ctx) {
     return CHGPU_OK;
 }
 
+chgpu_status chgpu_set_join(chgpu_ctx* ctx, int enabled, uint32_t min_points_per_bucket) {
+    if (!ctx) return CHGPU_EINVAL;
+    ctx->join_enabled = enabled != 0;
+    ctx->join_min_bucket = min_points_per_bucket;
+    return CHGPU_OK;
+}
+
 chgpu_status chgpu_set_sub_batch_queries(chgpu_ctx* ctx, uint64_t max_queries) {
     if (!ctx) return CHGPU_EINVAL;
     ctx->sub_batch_queries = max_queries ? max_queries : kSubBatchQueries;

@@ -32,6 +32,16 @@ def fresh(matcher, family):
     matcher.set_sub_batch_queries(0)
 
 
+@pytest.fixture(autouse=True, params=["join_by_size", "join_always"])
+def join_mode(request, matcher):
+    """Every test of this module runs twice: with the tensor-core Hamming pass (join_kernels.cuh) taken by the library's
+    own rule (sub-batches of >= 20 points per bucket: none of the small cases here) and forced for every sub-batch it can
+    serve, so that the pass and the active-list form of the match kernel see every edge case the plain kernel sees."""
+    matcher.set_join(True, 0 if request.param == "join_always" else 20)
+    yield request.param
+    matcher.set_join(True, 20)
+
+
 def put(matcher, image_id, desc, kp=None):
     matcher.upload(image_id, desc, kp)
     matcher._test_ids.add(image_id)
