@@ -70,7 +70,18 @@ def main():
         top = [{"pct_of_stall_samples": round(100.0 * s / tot, 2), "sass": t} for n, s, t in sorted(data, key=lambda x: -x[1])[:20]]
         mix = sorted(ops.items(), key=lambda kv: -kv[1])[:16]
         kernels[0]["sass_opcode_mix_warp_instructions"] = {k: v for k, v in mix}
-    json.dump({"report": rep, "kernels": kernels, "top_stall_locations": top}, open(out, "w"), indent=1)
+    doc = {"report": rep, "kernels": kernels, "top_stall_locations": top}
+    if queries and len(kernels) > 1:
+        # one launch each of the kernels that make up a step of the hot path (join pass + match kernel): the step's totals
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        doc["step"] = {
+            "kernels": [k["kernel"].split("(")[0] for k in kernels],
+            "warp_instructions_per_query": sum(k["warp_instructions_per_query"] for k in kernels),
+            "duration_ms": sum(float(k["metrics"]["gpu__time_duration.sum"]["value"]) for k in kernels),
+            "dram_bytes": sum(float(k["metrics"][n]["value"]) * scale[k["metrics"][n]["unit"]] for k in kernels
+                              for n in ("dram__bytes_read.sum", "dram__bytes_write.sum")),
+        }
+    json.dump(doc, open(out, "w"), indent=1)
     print("wrote", out)
 
 
