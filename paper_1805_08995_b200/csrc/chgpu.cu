@@ -459,7 +459,7 @@ chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t
     }
     size_t off[9];
     std::vector<size_t> toff;
-    const bool sorted_copies = ntiles == 0 && n != 0;
+    const bool sorted_copies = n != 0;  // (tiled images too: the join pass replaces the tiles' min pass)
     const size_t own = image_block_bytes(n, m, L, off, sorted_copies);
     const size_t bytes = own + tile_block_bytes(n, m, L, ntiles, tp, &toff);
     char* block = nullptr;
@@ -1170,7 +1170,30 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
             P.nunits = ntp * chunks;
             P.act = ctx->d_act;
             P.nact = ctx->d_nact;
-            CK(launch_match_tiled(P, kModeTileMin, smem, ctx->prop.multiProcessorCount, ctx->compute, &grid));
+            if (ctx->join_enabled && !sb.no_join) {
+                // The tensor-core Hamming pass over the WHOLE images (their own bucket index and sorted copies) marks the
+                // queries with a candidate within tau in the min-key scratch (0 instead of "none"): it replaces the min
+                // pass over every (query, tile); the top-k pass then visits every tile of the marked queries.
+                JoinParams JP{};
+                JP.images = ctx->d_images;
+                JP.pairs = b.d_pairs;
+                JP.npairs = sb.count;
+                JP.m = ctx->fam.short_bits;
+                JP.L = ctx->fam.table_count;
+                JP.tau = run.cfg.hamming_threshold;
+                JP.hit = nullptr;
+                JP.hit_key = ctx->d_gmin;
+                JP.stats = ctx->d_stats;
+                JP.counter = ctx->d_counter;
+                const uint32_t jcells = JP.L << JP.m;
+                const uint64_t junits = uint64_t(sb.count) * ((jcells + 31) / 32);
+                const uint32_t jgrid = uint32_t(std::min<uint64_t>((junits + kJoinThreads / 32 - 1) / (kJoinThreads / 32),
+                                                                   uint64_t(ctx->prop.multiProcessorCount) * 8));
+                join_hits_kernel<<<std::max(jgrid, 1u), kJoinThreads, 0, ctx->compute>>>(JP);
+                CK(cudaGetLastError());
+            } else {
+                CK(launch_match_tiled(P, kModeTileMin, smem, ctx->prop.multiProcessorCount, ctx->compute, &grid));
+            }
             CK(launch_tile_compact(P, ntp, ctx->compute));
             CK(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), ctx->compute));
             CK(launch_match_tiled(P, kModeTileTopK, smem_topk, ctx->prop.multiProcessorCount, ctx->compute, &grid));

@@ -32,7 +32,8 @@ struct JoinParams {
     const PairDesc* pairs;
     uint32_t npairs;
     uint32_t m, L, tau;
-    uint8_t* hit;            // per query of the sub-batch (PairDesc::res_off + q)
+    uint8_t* hit;            // per query of the sub-batch (PairDesc::res_off + q): set to 1, or ...
+    uint32_t* hit_key;       // ... (tiled train images) the per-query minimum-key scratch of the tile passes, set to 0
     DevStats* stats;
     unsigned int* counter;   // work counter (units of 32 buckets)
 };
@@ -57,7 +58,7 @@ template <int MT>
 __device__ __forceinline__ void join_pass(const uint4* __restrict__ qc, const int16_t* __restrict__ qp,
                                           const uint16_t* __restrict__ qi, uint32_t r0, uint32_t nq,
                                           const uint4* __restrict__ tr, const int16_t* __restrict__ tp, uint32_t nt, int tau,
-                                          uint8_t* __restrict__ hit, uint32_t g, uint32_t tq) {
+                                          uint8_t* __restrict__ hit, uint32_t* __restrict__ hit_key, uint32_t g, uint32_t tq) {
     constexpr uint32_t FULL = 0xffffffffu;
     const uint32_t ma0 = 0x01010101u << (2u * tq), ma1 = ma0 << 1;   // A: bits 2tq, 2tq + 1 of every byte, value 2^j
     const uint32_t mb0 = 0x80808080u >> (2u * tq), mb1 = mb0 >> 1;   // B (bit-reversed bytes): the same bits, value 2^(7-j)
@@ -122,7 +123,11 @@ __device__ __forceinline__ void join_pass(const uint4* __restrict__ qc, const in
                 mythr = thr[j];
             }
         const uint32_t slot = uint32_t(base) + tq, row = r0 + g + 8u * slot;
-        if (slot < uint32_t(2 * MT) && row < nq && mine >= mythr) hit[__ldg(qi + row)] = 1;
+        if (slot < uint32_t(2 * MT) && row < nq && mine >= mythr) {
+            const uint32_t qid = __ldg(qi + row);
+            if (hit_key != nullptr) hit_key[qid] = 0u;
+            else hit[qid] = 1;
+        }
     }
 }
 
@@ -132,20 +137,20 @@ __device__ __forceinline__ void join_pass(const uint4* __restrict__ qc, const in
 __device__ __forceinline__ void join_bucket(const uint4* __restrict__ qc, const int16_t* __restrict__ qp,
                                             const uint16_t* __restrict__ qi, uint32_t nq, const uint4* __restrict__ tr,
                                             const int16_t* __restrict__ tp, uint32_t nt, int tau, uint8_t* __restrict__ hit,
-                                            uint32_t lane) {
+                                            uint32_t* __restrict__ hit_key, uint32_t lane) {
     // the bucket's train-side lines into L1 (nt x 16 bytes of codes, nt popcount bytes): one prefetch instruction
     if (lane * 8u < nt) asm volatile("prefetch.global.L1 [%0];" ::"l"(tr + lane * 8u));
     if (lane == 31) asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
     const uint32_t g = lane >> 2, tq = lane & 3;
     uint32_t r0 = 0;
     while (nq - r0 > 48) {
-        join_pass<2>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, g, tq);
+        join_pass<2>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, hit_key, g, tq);
         r0 += 32;
     }
     const uint32_t left = nq - r0;  // 1 .. 48 rows: one pass of 1, 2 or 3 tiles
-    if (left > 32) join_pass<3>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, g, tq);
-    else if (left > 16) join_pass<2>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, g, tq);
-    else join_pass<1>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, g, tq);
+    if (left > 32) join_pass<3>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, hit_key, g, tq);
+    else if (left > 16) join_pass<2>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, hit_key, g, tq);
+    else join_pass<1>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, hit_key, g, tq);
 }
 
 __global__ void __launch_bounds__(kJoinThreads, CHGPU_JOIN_OCC) join_hits_kernel(const JoinParams P) {
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(kJoinThreads, CHGPU_JOIN_OCC) join_hits_kernel
                            bnt = __shfl_sync(0xffffffffu, nt, src);
             const uint64_t qo = uint64_t(bt) * I.n + bqa, to = uint64_t(bt) * J.n + bta;
             join_bucket(I.scodes + qo, I.spop + qo, I.points + qo, bnq, J.scodes + rev + to, J.spop + to, bnt, int(64u * P.tau),
-                        P.hit + pd.res_off, lane);
+                        P.hit + pd.res_off, P.hit_key ? P.hit_key + pd.res_off : nullptr, lane);
         }
     }
     // sum over the queries of their bucket sizes (raw_candidates, matcher.cpp:168)

@@ -57,7 +57,7 @@ MARKS = [  # (first line containing the text, phase of the lines from there on)
     ('} else if (tover <= 32u * kOverSlots) {', 'scan'),
     ('// ---- 3. ranking', 'rank'),
     ('// ---- long buckets', 'longbuckets'),
-    ('if (MODE != kModeMatch && emit) {', 'emit_dbg'),
+    ('if (!kMatch && emit) {', 'emit_dbg'),
     ('// ---- 4. verification', 'verify'),
     ('// batch boundary', 'loop'),
     ('st_raw = __reduce_add_sync', 'unit'),
