@@ -1202,7 +1202,7 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
             CK(cudaEventRecord(b.ev_k1, ctx->compute));
             st.match_launches += 2;
             st.total_launches += 3;
-        } else if (ctx->join_enabled && !sb.no_join && smem_train && !run.fmats && !run.dbg_ranked && sb.queries <= UINT32_MAX &&
+        } else if (ctx->join_enabled && !sb.no_join && smem_train && !run.dbg_ranked && sb.queries <= UINT32_MAX &&
                    // the pass works on 16 x 8 tiles of a bucket's queries x train points: it pays from ~20 points per bucket
                    // on both sides (measured: +6 % at 24, +9 % at 32, -4 % at 16, -36 % at 4 per bucket; scripts/sweep.py)
                    ((sb.queries / sb.count) >> ctx->fam.short_bits) >= ctx->join_min_bucket &&
@@ -1259,7 +1259,7 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
             P.act = ctx->d_act;
             P.nact = ctx->d_nact;
             P.smem_long_bytes = std::max<uint32_t>(sb.max_nt * 16u, 16u);
-            const size_t smem = size_t(P.smem_long_bytes) + offs_smem_bytes(ctx) + stage_smem_bytes(ctx, false);
+            const size_t smem = size_t(P.smem_long_bytes) + offs_smem_bytes(ctx) + stage_smem_bytes(ctx, run.fmats != nullptr);
             CK(launch_match_active(P, smem, ctx->prop.multiProcessorCount, ctx->compute, &grid));
             CK(cudaEventRecord(b.ev_k1, ctx->compute));
             st.total_launches += 2;  // join + list kernels (match_launches keeps counting sub-batches)
