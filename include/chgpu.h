@@ -401,6 +401,9 @@ void chgpu_auto_partition_sizing(uint64_t mean_image_bytes, uint64_t memory_budg
 /* The same rule with the numbers of this device: block_slots blocks share device_bytes (HBM left for images),
  * group_slots groups share host_bytes (page cache the read-ahead may occupy); device_image_bytes is what one image
  * occupies in HBM (descriptors, keypoints, codes, bucket index), file_image_bytes its CHFT file. */
+/* What an image of n points occupies in this context's HBM arena under the installed family (descriptors, keypoints, codes,
+ * bucket index, the bucket-sorted copies of the Hamming pass, tiles of a large image): the device_image_bytes of the rule below. */
+chgpu_status chgpu_image_device_bytes(chgpu_ctx* ctx, uint32_t n, uint64_t* bytes);
 void chgpu_partition_sizing_for_device(uint64_t device_image_bytes, uint64_t file_image_bytes, uint64_t device_bytes,
                                        uint64_t host_bytes, uint32_t block_slots, uint32_t group_slots,
                                        uint32_t* block_images, uint32_t* blocks_per_group);

@@ -113,6 +113,7 @@ SIGNATURES = {
     "chgpu_sync": (C.c_int, [C.c_void_p]),
     "chgpu_set_sub_batch_queries": (C.c_int, [C.c_void_p, C.c_uint64]),
     "chgpu_set_join": (C.c_int, [C.c_void_p, C.c_int, C.c_uint32]),
+    "chgpu_image_device_bytes": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64)]),
     "chgpu_host_alloc": (C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     "chgpu_host_free": (C.c_int, [C.c_void_p, C.c_void_p]),
     "chgpu_family_generate": (C.c_int, [C.POINTER(FamilyParamsC), f64p, f64p]),

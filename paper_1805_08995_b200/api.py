@@ -449,6 +449,12 @@ class Matcher:
     def sync(self):
         self._ck(self.lib.chgpu_sync(self.h))
 
+    def image_device_bytes(self, n: int) -> int:
+        """HBM bytes an image of n points occupies under the installed family (chgpu_image_device_bytes)."""
+        out = C.c_uint64(0)
+        self._ck(self.lib.chgpu_image_device_bytes(self.h, n, C.byref(out)))
+        return int(out.value)
+
     def set_join(self, enabled: bool = True, min_points_per_bucket: int = 20):
         """The tensor-core Hamming pass in front of the match kernel: off / on from this average bucket occupancy (0: always)."""
         self._ck(self.lib.chgpu_set_join(self.h, 1 if enabled else 0, min_points_per_bucket))

@@ -1452,6 +1452,16 @@ chgpu_status chgpu_sync(chgpu_ctx* ctx) {
     return CHGPU_OK;
 }
 
+chgpu_status chgpu_image_device_bytes(chgpu_ctx* ctx, uint32_t n, uint64_t* bytes) {
+    if (!ctx || !bytes) return CHGPU_EINVAL;
+    if (!ctx->has_family) return fail(ctx, CHGPU_ELOGIC, "chgpu_set_family must precede chgpu_image_device_bytes (the layout depends on m, L)");
+    if (n > kMaxPoints) return fail(ctx, CHGPU_EUNSUPPORTED, "%u points; device path holds <= %u", n, kMaxPoints);
+    const uint32_t m = ctx->fam.short_bits, L = ctx->fam.table_count;
+    size_t off[9];
+    *bytes = image_block_bytes(n, m, L, off, n != 0) + tile_block_bytes(n, m, L, tile_count_of(ctx, n), tile_points_of(ctx), nullptr);
+    return CHGPU_OK;
+}
+
 chgpu_status chgpu_set_join(chgpu_ctx* ctx, int enabled, uint32_t min_points_per_bucket) {
     if (!ctx) return CHGPU_EINVAL;
     ctx->join_enabled = enabled != 0;

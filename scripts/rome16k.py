@@ -103,6 +103,7 @@ def streamed(args, paths, accepted, K, n, write_s):
         t2 = time.perf_counter()
         assert got["records"] == st["matches"] and got["pairs"] == st["pairs"]
         props = m.device_props()
+        image_bytes = m.image_device_bytes(n)
     parity = check.verdict(np.asarray(centering, dtype=np.float64))
     assert parity["records_checksum_equal"], parity
     tasks = ch.plan_tasks(K, args.block_images, args.blocks_per_group, accepted)
@@ -114,7 +115,7 @@ def streamed(args, paths, accepted, K, n, write_s):
         "dataset_write_s": write_s,
         "centering_pass": {"seconds": t1 - t0, "GB_per_s": K * (16 + 144 * n) / (t1 - t0) / 1e9},
         "streamed_run": {"seconds": t2 - t1, "pairs_per_s": st["pairs"] / (t2 - t1), **st},
-        "resident_bound_GB": args.block_slots * args.block_images * 1_565_464 / 1e9,
+        "resident_bound_GB": args.block_slots * args.block_images * image_bytes / 1e9,
         "end_to_end": {"seconds": t2 - t0, "pairs_per_s": st["pairs"] / (t2 - t0)},
         "device": props["name"], "hbm_in_use_after_GB": (props["total_mem"] - props["free_mem"]) / 1e9,
     }

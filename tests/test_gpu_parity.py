@@ -650,6 +650,17 @@ def test_guided_match_bit_exact(matcher, oracle, n_i, n_j, params):
         matcher.match_pairs_guided([(BASE, BASE + 1)], F[None], -1.0, cfg)
 
 
+def test_image_device_bytes_is_what_an_upload_takes(matcher, default_family):
+    """chgpu_image_device_bytes (the device_image_bytes of chgpu_partition_sizing_for_device) against the arena's own growth."""
+    fresh(matcher, default_family)
+    assert matcher.image_device_bytes(0) > 0
+    small, big = matcher.image_device_bytes(8192), matcher.image_device_bytes(20000)
+    assert 8192 * (128 + 16 + 16 + 24 + 12 + 6 * 34) <= small <= 8192 * (128 + 16 + 16 + 24 + 12 + 6 * 34) + 64 * 1024
+    assert big > 20000 * (128 + 16 + 16 + 24 + 12 + 6 * 34 + 12)  # + the tiles' own bucket arrays
+    with pytest.raises(ch.UnsupportedError):
+        matcher.image_device_bytes(65537)
+
+
 # ---- failure paths ----------------------------------------------------------------------------------
 def test_failed_pair_list_leaves_the_context_usable(matcher, default_family):
     """A sink that aborts, and a record capacity that runs out, in the MIDDLE of a multi-sub-batch pair list
