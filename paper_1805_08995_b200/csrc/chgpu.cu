@@ -1252,7 +1252,7 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
                                                                uint64_t(ctx->prop.multiProcessorCount) * 8));
             join_hits_kernel<<<std::max(jgrid, 1u), kJoinThreads, 0, ctx->compute>>>(JP);
             CK(cudaGetLastError());
-            join_compact_kernel<<<(sb.count + 7) / 8, 256, 0, ctx->compute>>>(ctx->d_images, b.d_pairs, sb.count, ctx->d_hit,
+            join_compact_kernel<<<sb.count, 256, 0, ctx->compute>>>(ctx->d_images, b.d_pairs, sb.count, ctx->d_hit,
                                                                                 ctx->d_act, ctx->d_nact);
             CK(cudaGetLastError());
             CK(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), ctx->compute));

@@ -199,26 +199,42 @@ __global__ void __launch_bounds__(kJoinThreads, CHGPU_JOIN_OCC) join_hits_kernel
     if (lane == 0 && raw) atomicAdd(&P.stats->raw_candidates, raw);
 }
 
-// The hit flags of every pair -> the ascending list of its hit queries (PairDesc::act_off, u16) and their number.  One warp
-// per pair, ballot compaction in query order.
-__global__ void join_compact_kernel(const DevImage* __restrict__ images, const PairDesc* __restrict__ pairs, uint32_t npairs,
-                                    const uint8_t* __restrict__ hit, uint16_t* __restrict__ act, uint32_t* __restrict__ nact) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t pair = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+// The hit flags of every pair -> the ascending list of its hit queries (PairDesc::act_off, u16) and their number.  One CTA
+// per pair (eight warps over contiguous runs of the queries), ballot compaction in query order.
+__global__ void __launch_bounds__(256) join_compact_kernel(const DevImage* __restrict__ images, const PairDesc* __restrict__ pairs,
+                                                           uint32_t npairs, const uint8_t* __restrict__ hit,
+                                                           uint16_t* __restrict__ act, uint32_t* __restrict__ nact) {
+    // one CTA per pair: every warp counts the hits of a contiguous run of the queries, the CTA turns the counts into
+    // offsets, and the warp writes its part of the list in query order
+    __shared__ uint32_t s_count[8];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t pair = blockIdx.x;
     if (pair >= npairs) return;
     const PairDesc pd = pairs[pair];
     const uint32_t nq = images[pd.slot_i].n;
     const uint8_t* __restrict__ h = hit + pd.res_off;
-    uint16_t* __restrict__ out = act + pd.act_off;
+    const uint32_t run = ((nq + 8u * 32u - 1u) / (8u * 32u)) * 32u;
+    const uint32_t q0 = min(nq, warp * run), q1 = min(nq, q0 + run);
     uint32_t count = 0;
-    for (uint32_t q0 = 0; q0 < nq; q0 += 32) {
-        const uint32_t q = q0 + lane;
-        const bool f = q < nq && h[q] != 0;
-        const uint32_t bal = __ballot_sync(0xffffffffu, f);
-        if (f) out[count + __popc(bal & ((1u << lane) - 1u))] = uint16_t(q);
-        count += __popc(bal);
+    for (uint32_t q = q0; q < q1; q += 32) count += __popc(__ballot_sync(0xffffffffu, q + lane < q1 && h[q + lane] != 0));
+    if (lane == 0) s_count[warp] = count;
+    __syncthreads();
+    uint32_t base = 0, total = 0;
+#pragma unroll
+    for (uint32_t w = 0; w < 8; ++w) {
+        const uint32_t c = s_count[w];
+        if (w < warp) base += c;
+        total += c;
     }
-    if (lane == 0) nact[pair] = count;
+    uint16_t* __restrict__ out = act + pd.act_off + base;
+    uint32_t at = 0;
+    for (uint32_t q = q0; q < q1; q += 32) {
+        const bool f = q + lane < q1 && h[q + lane] != 0;
+        const uint32_t bal = __ballot_sync(0xffffffffu, f);
+        if (f) out[at + __popc(bal & ((1u << lane) - 1u))] = uint16_t(q + lane);
+        at += __popc(bal);
+    }
+    if (threadIdx.x == 0) nact[pair] = total;
 }
 
 }  // namespace chgpu

@@ -1001,23 +1001,40 @@ __global__ void __launch_bounds__(kMatchThreads, 1) match_kernel(const MatchPara
 // The queries the top-k pass visits for every (query image, tile) pair: gmin within tau and the tile's list not
 // yet written by the min pass.  One warp per pair, ballot compaction in query order.
 template <int kInstance>
-__global__ void tile_compact_kernel(const MatchParams P, uint32_t ntile_pairs) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t tp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+__global__ void __launch_bounds__(256) tile_compact_kernel(const MatchParams P, uint32_t ntile_pairs) {
+    // one CTA per (query image, tile) pair: every warp takes a contiguous run of the queries (a multiple of 32), counts its
+    // active ones, the CTA turns the counts into offsets, and the warp writes its part of the list in query order
+    __shared__ uint32_t s_count[8];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t tp = blockIdx.x;
     if (tp >= ntile_pairs) return;
     const PairDesc pd = P.pairs[tp];
     const uint32_t nq = P.images[pd.slot_i].n;
-    uint16_t* __restrict__ out = P.act + pd.act_off;
+    const uint32_t run = ((nq + 8u * 32u - 1u) / (8u * 32u)) * 32u;
+    const uint32_t q0 = min(nq, warp * run), q1 = min(nq, q0 + run);
+    auto active = [&](uint32_t q) {
+        return q < q1 && (__ldg(P.gmin + pd.res_off + q) >> 24) <= P.tau && !((__ldg(P.gdone + pd.res_off + q) >> pd.tile_idx) & 1ull);
+    };
     uint32_t count = 0;
-    for (uint32_t q0 = 0; q0 < nq; q0 += 32) {
-        const uint32_t q = q0 + lane;
-        const bool f = q < nq && (__ldg(P.gmin + pd.res_off + q) >> 24) <= P.tau &&
-                       !((__ldg(P.gdone + pd.res_off + q) >> pd.tile_idx) & 1ull);
-        const uint32_t bal = __ballot_sync(0xffffffffu, f);
-        if (f) out[count + __popc(bal & ((1u << lane) - 1u))] = uint16_t(q);
-        count += __popc(bal);
+    for (uint32_t q = q0; q < q1; q += 32) count += __popc(__ballot_sync(0xffffffffu, active(q + lane)));
+    if (lane == 0) s_count[warp] = count;
+    __syncthreads();
+    uint32_t base = 0, total = 0;
+#pragma unroll
+    for (uint32_t w = 0; w < 8; ++w) {
+        const uint32_t c = s_count[w];
+        if (w < warp) base += c;
+        total += c;
     }
-    if (lane == 0) P.nact[tp] = count;
+    uint16_t* __restrict__ out = P.act + pd.act_off + base;
+    uint32_t at = 0;
+    for (uint32_t q = q0; q < q1; q += 32) {
+        const bool f = active(q + lane);
+        const uint32_t bal = __ballot_sync(0xffffffffu, f);
+        if (f) out[at + __popc(bal & ((1u << lane) - 1u))] = uint16_t(q + lane);
+        at += __popc(bal);
+    }
+    if (threadIdx.x == 0) P.nact[tp] = total;
 }
 
 // Ascending bitonic sort of one value per lane (kNone sinks to the top lanes), and the last stage alone for a

@@ -27,7 +27,7 @@ cudaError_t launch_match_tiled(const MatchParams& P, int mode, size_t smem, int 
 
 cudaError_t launch_tile_compact(const MatchParams& P, uint32_t ntile_pairs, cudaStream_t stream) {
     if (ntile_pairs == 0) return cudaSuccess;
-    tile_compact_kernel<0><<<(ntile_pairs + 7) / 8, 256, 0, stream>>>(P, ntile_pairs);
+    tile_compact_kernel<0><<<ntile_pairs, 256, 0, stream>>>(P, ntile_pairs);
     return cudaGetLastError();
 }
 

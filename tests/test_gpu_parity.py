@@ -655,8 +655,9 @@ def test_image_device_bytes_is_what_an_upload_takes(matcher, default_family):
     fresh(matcher, default_family)
     assert matcher.image_device_bytes(0) > 0
     small, big = matcher.image_device_bytes(8192), matcher.image_device_bytes(20000)
-    assert 8192 * (128 + 16 + 16 + 24 + 12 + 6 * 34) <= small <= 8192 * (128 + 16 + 16 + 24 + 12 + 6 * 34) + 64 * 1024
-    assert big > 20000 * (128 + 16 + 16 + 24 + 12 + 6 * 34 + 12)  # + the tiles' own bucket arrays
+    per_point = 128 + 16 + 16 + 6 * 4 + 6 * 2 + 6 * 2 + 6 * 34  # desc, kp, long code, short codes, points, scan, sorted copies
+    assert 8192 * per_point <= small <= 8192 * per_point + 64 * 1024
+    assert big > 20000 * (per_point + 6 * 4)  # + the tiles' own points / scan arrays
     with pytest.raises(ch.UnsupportedError):
         matcher.image_device_bytes(65537)
 
