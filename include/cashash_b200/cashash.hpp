@@ -29,10 +29,13 @@
 // std::runtime_error when no sm_100 device is present.
 //
 // Parameter envelope.  The reference accepts short_bits <= 32, any table_count >= 1, any top_k >= 2 and any
-// image size (hashing.cpp:30-36, matcher.cpp:9-17); the device path holds short_bits <= 12, table_count <= 8,
-// top_k <= 32 and <= 65,536 points per image (kDeviceMax* below; chgpu.h).  Arguments that are valid for the
-// reference but outside that envelope throw `UnsupportedOnDevice` (a std::runtime_error) — never a wrong result
-// and never one of the reference's own exception classes, so a caller can tell "not offered here" from "invalid".
+// image size (hashing.cpp:30-36, matcher.cpp:9-17); the device path holds short_bits <= 32, any top_k >= 2,
+// table_count <= 8 and <= 65,536 points per image (kDeviceMax* below; chgpu.h).  The tuned kernels cover
+// short_bits <= 12 and top_k <= 32 (kTunedMax*); beyond that, and for match_pair_filtered with a host callback,
+// the same calls run through the general kernels (csrc/general_kernels.cuh) — same results, not tuned.
+// Arguments that are valid for the reference but outside the envelope throw `UnsupportedOnDevice` (a
+// std::runtime_error) — never a wrong result and never one of the reference's own exception classes, so a
+// caller can tell "not offered here" from "invalid".
 #pragma once
 
 #include <algorithm>
@@ -63,10 +66,12 @@ inline constexpr int kDefaultReduceRounds = 3;
 inline constexpr std::size_t kFeatureFileHeaderBytes = 16;
 inline constexpr std::size_t kFeatureRecordBytes = 16 + kDescriptorDim;
 // the device path's parameter envelope (include/chgpu.h); beyond it: UnsupportedOnDevice
-inline constexpr std::uint32_t kDeviceMaxShortBits = 12;
+inline constexpr std::uint32_t kDeviceMaxShortBits = 32;  // = the reference's own limit (hashing.cpp:31)
 inline constexpr std::uint32_t kDeviceMaxTables = 8;
-inline constexpr std::uint32_t kDeviceMaxTopK = 32;
 inline constexpr std::uint32_t kDeviceMaxPoints = 65536;
+// what the tuned kernels cover; larger values take the general path
+inline constexpr std::uint32_t kTunedMaxShortBits = 12;
+inline constexpr std::uint32_t kTunedMaxTopK = 32;
 
 // Arguments the reference accepts and the device path does not hold (see the header comment).
 class UnsupportedOnDevice : public std::runtime_error {
@@ -852,6 +857,43 @@ public:
         return stats;
     }
 
+    // match_pair_filtered (matcher.hpp:102-105) for two resident images with a HOST callback: the candidate lists are
+    // formed on the device (matcher.cpp:164-171), `filter` is called on this thread for every query with a non-empty
+    // list, in query order (matcher.cpp:172; its return value is ignored there as well), and whatever it leaves in the
+    // vector — fewer entries, another order, repeats — is ranked and verified on the device (matcher.cpp:173-192).
+    std::vector<MatchRecord> match_pair_filtered(std::uint32_t image_i, std::uint32_t image_j, const MatchConfig& cfg,
+                                                 const std::function<bool(std::uint32_t, std::vector<std::uint32_t>&)>& filter,
+                                                 chgpu_match_stats* stats = nullptr) {
+        std::uint32_t nq = 0;
+        ck(chgpu_image_points(ctx_, image_i, &nq));
+        std::vector<std::uint64_t> offs(std::size_t(nq) + 1, 0);
+        std::uint64_t total = 0;
+        chgpu_status st = chgpu_pair_candidates(ctx_, image_i, image_j, offs.data(), nullptr, 0, &total);
+        if (st != CHGPU_ENOMEM) ck(st);
+        std::vector<std::uint32_t> cands(std::max<std::uint64_t>(total, 1));
+        if (total) ck(chgpu_pair_candidates(ctx_, image_i, image_j, offs.data(), cands.data(), total, &total));
+        std::vector<std::uint64_t> new_offs(std::size_t(nq) + 1, 0);
+        std::vector<std::uint32_t> ids;
+        ids.reserve(total);
+        std::vector<std::uint32_t> one;
+        for (std::uint32_t q = 0; q < nq; ++q) {
+            one.assign(cands.begin() + offs[q], cands.begin() + offs[q + 1]);
+            if (filter && !one.empty()) filter(q, one);
+            ids.insert(ids.end(), one.begin(), one.end());
+            new_offs[q + 1] = ids.size();
+        }
+        const chgpu_match_cfg c = detail::to_c(cfg);
+        std::vector<MatchRecord> out(std::max<std::uint32_t>(nq, 1));
+        static_assert(sizeof(MatchRecord) == sizeof(chgpu_match_record), "record layout");
+        std::uint64_t count = 0;
+        st = chgpu_match_pair_lists(ctx_, image_i, image_j, &c, new_offs.data(), ids.empty() ? nullptr : ids.data(),
+                                    reinterpret_cast<chgpu_match_record*>(out.data()), nq, &count, stats);
+        if (st == CHGPU_EINVAL) throw std::invalid_argument(chgpu_last_error(ctx_));
+        ck(st);
+        out.resize(count);
+        return out;
+    }
+
     // epipolar-guided pair list (guided_match_pair, geometry.cpp:234-250): one row-major 3x3 F per pair
     std::vector<PairMatches> match_pairs_guided(std::span<const std::pair<std::uint32_t, std::uint32_t>> pairs,
                                                 std::span<const std::array<double, 9>> fmats, double band_px,
@@ -1074,6 +1116,42 @@ inline std::vector<MatchRecord> match_pair(const FeatureSet& fs_i, const Feature
     const std::pair<std::uint32_t, std::uint32_t> pr{detail::kScratchA, detail::kScratchB};
     std::vector<PairMatches> out = m.match_pairs({&pr, 1}, cfg);
     return std::move(out.front().matches);
+}
+
+// match_pair_filtered (matcher.hpp:102-105): match_pair with a host callback between lookup and ranking
+// (CandidateFilter, matcher.hpp:92-93).  Lookup and ranking + verification run on the device, the callback on the
+// calling thread in between (Matcher::match_pair_filtered).
+using CandidateFilter = std::function<bool(std::uint32_t query_index, std::vector<std::uint32_t>& candidates)>;
+
+inline std::vector<MatchRecord> match_pair_filtered(const FeatureSet& fs_i, const FeatureSet& fs_j, const ImageCodes& codes_i,
+                                                    const ImageCodes& codes_j, const MatchConfig& cfg,
+                                                    const CandidateFilter& filter) {
+    if (!(codes_i.params == codes_j.params))
+        throw std::invalid_argument("match_pair: codes come from different hash families");  // matcher.cpp:144
+    if (codes_i.shorts.point_count != fs_i.size() || codes_j.shorts.point_count != fs_j.size())
+        throw std::invalid_argument("match_pair: code/point count mismatch");  // matcher.cpp:146-148
+    static std::mutex fam_mu;
+    static std::vector<std::unique_ptr<HashFamily>> families;
+    const HashFamily* fam = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(fam_mu);
+        for (const auto& f : families)
+            if (f->params == codes_i.params) fam = f.get();
+        if (!fam) {
+            families.push_back(std::make_unique<HashFamily>(build_hash_family(codes_i.params)));
+            fam = families.back().get();
+        }
+    }
+    detail::DefaultContext& dc = detail::default_context();
+    std::lock_guard<std::mutex> lock(dc.mu);
+    Matcher& m = dc.with(*fam);
+    m.upload(detail::kScratchA, fs_i);
+    detail::ScopedImage ga{m, detail::kScratchA};
+    m.upload(detail::kScratchB, fs_j);
+    detail::ScopedImage gb{m, detail::kScratchB};
+    m.upload_codes(detail::kScratchA, codes_i);
+    m.upload_codes(detail::kScratchB, codes_j);
+    return m.match_pair_filtered(detail::kScratchA, detail::kScratchB, cfg, filter);
 }
 
 // guided_match_pair (geometry.hpp:86-89): match_pair with the epipolar band between lookup and ranking.

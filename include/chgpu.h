@@ -14,8 +14,11 @@
  *   - there is NO CPU fallback: without a CUDA device chgpu_create fails with CHGPU_ECUDA.
  *
  * Supported parameter envelope on the device path (CHGPU_EUNSUPPORTED outside it):
- *   short_bits m <= 12, table_count L <= 8, long_bits n <= 128, top_k <= 32,
- *   points per image <= 65,536.
+ *   short_bits m <= 32 (the reference's own limit, hashing.cpp:30-36), table_count L <= 8,
+ *   long_bits n <= 128, any top_k >= 2, points per image <= 65,536.
+ * The tuned kernels cover m <= 12 and top_k <= 32; beyond that (m = 13..32: sparse bucket index,
+ * top_k > 32, candidate lists edited by a host callback) the same calls run through the general
+ * kernels of csrc/general_kernels.cuh — same results, not tuned.
  */
 #ifndef CHGPU_H
 #define CHGPU_H
@@ -224,6 +227,10 @@ chgpu_status chgpu_download_codes(chgpu_ctx* ctx, uint32_t image_id, uint32_t* s
 chgpu_status chgpu_upload_codes(chgpu_ctx* ctx, uint32_t image_id, const uint32_t* shorts, const uint64_t* longs);
 /* Dense CSR of the bucket index: offsets L*(2^m+1) u32, points L*n u32 (bucket-major, ascending id). */
 chgpu_status chgpu_download_bucket_index(chgpu_ctx* ctx, uint32_t image_id, uint32_t* offsets, uint32_t* points);
+/* The same index in the form build_bucket_index leaves it before grouping (matcher.cpp:34-37): per table the
+ * points sorted by (short code, point id).  codes, points: L*n u32 each, table-major.  Works for every
+ * short_bits (short_bits > 12 has no dense offset table: CHGPU_EUNSUPPORTED from the call above). */
+chgpu_status chgpu_download_sorted_index(chgpu_ctx* ctx, uint32_t image_id, uint32_t* codes, uint32_t* points);
 
 /* ---- code cache / centering files (interop with the CPU reference, resume) -------------- */
 /* centering_fingerprint (hashing.cpp:151-162): FNV-1a over the 128 doubles' bytes. */
@@ -291,6 +298,23 @@ chgpu_status chgpu_match_pairs_guided(chgpu_ctx* ctx, const uint32_t* pairs, uin
 chgpu_status chgpu_match_pairs_guided_stream(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
                                              const chgpu_match_cfg* cfg, const double* fmats, double band_px,
                                              chgpu_sink_fn sink, void* user, chgpu_match_stats* stats /* nullable */);
+
+/* match_pair_filtered with a HOST callback (matcher.hpp:92-105; hook matcher.cpp:172) in two device steps with the
+ * caller's filter in between:
+ *   1. chgpu_pair_candidates: the candidate list of every query of image_i in image_j — its L buckets concatenated,
+ *      sorted, made unique (matcher.cpp:164-171).  offsets: n_i + 1 entries; candidates: capacity entries.  If the
+ *      capacity is too small the call returns CHGPU_ENOMEM with *total = entries required and offsets filled
+ *      (capacity 0 / candidates NULL is the sizing call).
+ *   2. the caller edits the lists (the reference hands the filter a mutable vector: entries may be removed,
+ *      reordered, repeated), then chgpu_match_pair_lists ranks and verifies from the lists as they are: Hamming
+ *      ranking as a stable counting sort (ties keep the list order, fill_histogram matcher.cpp:68-84), threshold and
+ *      re-rank rule (matcher.cpp:176-189), Euclidean verification (matcher.cpp:115-137).  Queries with an empty
+ *      list produce nothing (matcher.cpp:173).  list_ids entries must be < n_j. */
+chgpu_status chgpu_pair_candidates(chgpu_ctx* ctx, uint32_t image_i, uint32_t image_j, uint64_t* offsets,
+                                   uint32_t* candidates /* nullable with capacity 0 */, uint64_t capacity, uint64_t* total);
+chgpu_status chgpu_match_pair_lists(chgpu_ctx* ctx, uint32_t image_i, uint32_t image_j, const chgpu_match_cfg* cfg,
+                                    const uint64_t* list_offsets, const uint32_t* list_ids, chgpu_match_record* records,
+                                    uint64_t capacity, uint64_t* total, chgpu_match_stats* stats /* nullable */);
 
 /* Parity hook: the ranked candidate list each query hands to verification (after the re-rank
  * fallback, matcher.cpp:176-189).  ranked: n_i*top_k u32, ranked_count: n_i u32. */

@@ -172,11 +172,20 @@ struct BandFilter {
     }
 };
 
+// A filter given as data: the candidate list of query q is REPLACED by ids[offs[q] .. offs[q + 1]) — what an arbitrary
+// CandidateFilter (matcher.hpp:92-93) may do to the vector it is handed (chor_match_pair_lists).
+struct ListFilter {
+    const uint64_t* offs;
+    const uint32_t* ids;
+    void apply(uint32_t q, std::vector<uint32_t>& cands) const { cands.assign(ids + offs[q], ids + offs[q + 1]); }
+};
+
 int match_pair_impl(const chor_family_params& p, const chor_match_cfg& cfg,
                     const uint8_t* desc_i, uint32_t n_i, const uint32_t* shorts_i, const uint64_t* longs_i,
                     const uint8_t* desc_j, uint32_t n_j, const uint32_t* shorts_j, const uint64_t* longs_j,
                     chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
-                    uint32_t* ranked_out, uint32_t* ranked_count, const BandFilter* filter = nullptr) {
+                    uint32_t* ranked_out, uint32_t* ranked_count, const BandFilter* filter = nullptr,
+                    const ListFilter* lists = nullptr) {
     // matcher.cpp:141-195.  Family equality / count checks are structural in this flat ABI.
     if (!family_ok(p) || !cfg_ok(cfg, p.long_bits)) return 1;
     chor_pair_stats st{};
@@ -200,6 +209,7 @@ int match_pair_impl(const chor_family_params& p, const chor_match_cfg& cfg,
             cands.erase(std::unique(cands.begin(), cands.end()), cands.end());
             st.unique_candidates += cands.size();
             if (filter && !cands.empty()) filter->apply(q, cands);  // matcher.cpp:172
+            if (lists && !cands.empty()) lists->apply(q, cands);
             if (cands.empty()) continue;
 
             const uint64_t* ql = longs_i + 2 * static_cast<size_t>(q);
@@ -385,6 +395,17 @@ int chor_guided_match_pair(const chor_family_params* p, const chor_match_cfg* cf
     const BandFilter filter{kp_i, kp_j, F, band_px};
     return match_pair_impl(*p, *cfg, desc_i, n_i, shorts_i, longs_i, desc_j, n_j, shorts_j, longs_j, records,
                            record_count, stats, ranked, ranked_count, &filter);
+}
+
+int chor_match_pair_lists(const chor_family_params* p, const chor_match_cfg* cfg,
+                          const uint8_t* desc_i, uint32_t n_i, const uint32_t* shorts_i, const uint64_t* longs_i,
+                          const uint8_t* desc_j, uint32_t n_j, const uint32_t* shorts_j, const uint64_t* longs_j,
+                          const uint64_t* list_offsets, const uint32_t* list_ids,
+                          chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
+                          uint32_t* ranked, uint32_t* ranked_count) {
+    const ListFilter lists{list_offsets, list_ids};
+    return match_pair_impl(*p, *cfg, desc_i, n_i, shorts_i, longs_i, desc_j, n_j, shorts_j, longs_j, records,
+                           record_count, stats, ranked, ranked_count, nullptr, &lists);
 }
 
 int chor_brute_force_match(const uint8_t* desc_i, uint32_t n_i, const uint8_t* desc_j, uint32_t n_j,

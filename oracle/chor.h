@@ -114,6 +114,17 @@ int chor_guided_match_pair(const chor_family_params* p, const chor_match_cfg* cf
                            chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
                            uint32_t* ranked, uint32_t* ranked_count);
 
+/* match_pair_filtered (matcher.hpp:102-105) with a filter given as data: whenever the reference calls the filter
+ * (non-empty candidate list, matcher.cpp:172) the list of query q is REPLACED by
+ * list_ids[list_offsets[q] .. list_offsets[q + 1]) — entries may be removed, reordered or repeated, as an arbitrary
+ * CandidateFilter may do.  In oracle/_ref this drives the reference's own match_pair_filtered. */
+int chor_match_pair_lists(const chor_family_params* p, const chor_match_cfg* cfg,
+                          const uint8_t* desc_i, uint32_t n_i, const uint32_t* shorts_i, const uint64_t* longs_i,
+                          const uint8_t* desc_j, uint32_t n_j, const uint32_t* shorts_j, const uint64_t* longs_j,
+                          const uint64_t* list_offsets, const uint32_t* list_ids,
+                          chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
+                          uint32_t* ranked, uint32_t* ranked_count);
+
 /* Association order of the line's third component used by chor_guided_match_pair of THIS library (the restatement):
  * 0 (default) F20 x + (F21 y + F22); 1 (F20 x + F21 y) + F22.  Test instrumentation for the bound on row f4. */
 void chor_set_line_order(int order);

@@ -309,6 +309,27 @@ int chor_guided_match_pair(const chor_family_params* p, const chor_match_cfg* cf
     });
 }
 
+int chor_match_pair_lists(const chor_family_params* p, const chor_match_cfg* cfg,
+                          const uint8_t* desc_i, uint32_t n_i, const uint32_t* shorts_i, const uint64_t* longs_i,
+                          const uint8_t* desc_j, uint32_t n_j, const uint32_t* shorts_j, const uint64_t* longs_j,
+                          const uint64_t* list_offsets, const uint32_t* list_ids,
+                          chor_match_record* records, uint32_t* record_count, chor_pair_stats* stats,
+                          uint32_t* ranked, uint32_t* ranked_count) {
+    return guarded([&] {
+        const FamilyParams fp = to_params(*p);
+        validate(fp);
+        const MatchConfig mc = to_cfg(*cfg);
+        const FeatureSet fi = to_features(desc_i, n_i), fj = to_features(desc_j, n_j);
+        const ImageCodes ci = to_codes(fp, shorts_i, longs_i, n_i), cj = to_codes(fp, shorts_j, longs_j, n_j);
+        // the reference's own match_pair_filtered, driven by a filter that replaces the vector it is handed
+        const CandidateFilter filter = [&](std::uint32_t q, std::vector<std::uint32_t>& candidates) {
+            candidates.assign(list_ids + list_offsets[q], list_ids + list_offsets[q + 1]);
+            return true;
+        };
+        match_pair_body(fp, mc, fi, fj, ci, cj, &filter, records, record_count, stats, ranked, ranked_count);
+    });
+}
+
 int chor_brute_force_match(const uint8_t* desc_i, uint32_t n_i, const uint8_t* desc_j, uint32_t n_j,
                            double ratio, chor_match_record* records, uint32_t* record_count) {
     return guarded([&] {

@@ -143,6 +143,10 @@ SIGNATURES = {
     "chgpu_download_codes": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
     "chgpu_upload_codes": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
     "chgpu_download_bucket_index": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "chgpu_download_sorted_index": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "chgpu_pair_candidates": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint64, u64p]),
+    "chgpu_match_pair_lists": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(MatchCfgC), C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_uint64, u64p, C.POINTER(MatchStatsC)]),
     "chgpu_centering_fingerprint": (C.c_uint64, [f64p]),
     "chgpu_save_code_cache": (C.c_int, [C.c_char_p, C.POINTER(FamilyParamsC), C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p]),
     "chgpu_read_code_cache_header": (C.c_int, [C.c_char_p, C.POINTER(FamilyParamsC), u64p, u32p]),

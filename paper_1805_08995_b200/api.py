@@ -735,7 +735,66 @@ class Matcher:
         self._ck(self.lib.chgpu_download_bucket_index(self.h, image_id, offs.ctypes.data, pts.ctypes.data))
         return BucketIndex(m, n, offs, pts)
 
+    def sorted_index(self, image_id: int) -> tuple[np.ndarray, np.ndarray]:
+        """Per table the points sorted by (short code, id) — build_bucket_index before grouping (matcher.cpp:34-37).
+        Returns (codes, points), each (L, n) u32; defined for every short_bits."""
+        n = self.points(image_id)
+        L = self.params.table_count
+        codes = np.zeros((L, n), dtype=np.uint32)
+        pts = np.zeros((L, n), dtype=np.uint32)
+        self._ck(self.lib.chgpu_download_sorted_index(self.h, image_id, codes.ctypes.data, pts.ctypes.data))
+        return codes, pts
+
     # -- match ----------------------------------------------------------------------------------
+    def pair_candidates(self, image_i: int, image_j: int) -> tuple[np.ndarray, np.ndarray]:
+        """Candidate list of every query of image_i in image_j (matcher.cpp:164-171): (offsets (n_i+1) u64, ids u32)."""
+        n = self.points(image_i)
+        offsets = np.zeros(n + 1, dtype=np.uint64)
+        total = C.c_uint64(0)
+        st = self.lib.chgpu_pair_candidates(self.h, image_i, image_j, offsets.ctypes.data, None, 0, C.byref(total))
+        if st != N.ENOMEM:
+            self._ck(st)
+        cands = np.zeros(max(int(total.value), 1), dtype=np.uint32)
+        if total.value:
+            self._ck(self.lib.chgpu_pair_candidates(self.h, image_i, image_j, offsets.ctypes.data, cands.ctypes.data,
+                                                    int(total.value), C.byref(total)))
+        return offsets, cands[: int(total.value)]
+
+    def match_pair_lists(self, image_i: int, image_j: int, offsets, ids, cfg: MatchConfig = MatchConfig()):
+        """Ranking + verification from explicit per-query candidate lists (the second half of match_pair_filtered)."""
+        n = self.points(image_i)
+        offs = np.ascontiguousarray(offsets, dtype=np.uint64)
+        lst = np.ascontiguousarray(ids, dtype=np.uint32)
+        if len(offs) != n + 1 or int(offs[-1]) != len(lst):
+            raise ValueError("match_pair_lists: offsets must have n_i + 1 entries and end at len(ids)")
+        records = np.zeros(max(n, 1), dtype=RECORD_DTYPE)
+        total = C.c_uint64(0)
+        stats = N.MatchStatsC()
+        c = cfg.c()
+        self._ck(self.lib.chgpu_match_pair_lists(self.h, image_i, image_j, C.byref(c), offs.ctypes.data,
+                                                 lst.ctypes.data if len(lst) else None, records.ctypes.data, n,
+                                                 C.byref(total), C.byref(stats)))
+        return records[: total.value], stats.as_dict()
+
+    def match_pair_filtered(self, image_i: int, image_j: int, candidate_filter, cfg: MatchConfig = MatchConfig()):
+        """match_pair_filtered (matcher.hpp:102-105) with a HOST callback `candidate_filter(query_index, candidates) ->
+        list | None`: called for every query with a non-empty list (matcher.cpp:172), in query order; it returns the edited
+        list (None: unchanged).  Lookup before it and ranking + verification after it run on the device."""
+        offsets, cands = self.pair_candidates(image_i, image_j)
+        n = len(offsets) - 1
+        out_lists = []
+        new_offs = np.zeros(n + 1, dtype=np.uint64)
+        for q in range(n):
+            lst = cands[int(offsets[q]): int(offsets[q + 1])]
+            if len(lst):
+                edited = candidate_filter(q, lst.tolist())
+                if edited is not None:
+                    lst = np.asarray(edited, dtype=np.uint32).reshape(-1)
+            out_lists.append(lst)
+            new_offs[q + 1] = new_offs[q] + len(lst)
+        ids = np.concatenate(out_lists) if out_lists else np.zeros(0, dtype=np.uint32)
+        return self.match_pair_lists(image_i, image_j, new_offs, ids.astype(np.uint32), cfg)
+
     def match_pairs(self, pairs, cfg: MatchConfig = MatchConfig(), capacity: int | None = None):
         """Returns (offsets (npairs+1) u64, records structured array, stats dict)."""
         pr = np.ascontiguousarray(pairs, dtype=np.uint32).reshape(-1, 2)

@@ -27,7 +27,7 @@ NVCC_FLAGS = [
 # translation units of libchgpu.so; the match kernel's variants are split so they compile in parallel
 CHGPU_UNITS = ["chgpu.cu", "match_smem.cu", "match_global.cu", "match_guided.cu", "match_tiled.cu", "match_dbg.cu", "match_active.cu", "host_util.cpp",
                "residency.cpp"]
-CHGPU_HEADERS = ["dev_types.cuh", "hash_kernels.cuh", "hash_tc.cuh", "join_kernels.cuh", "match_kernels.cuh", "match_launch.cuh", "compact_kernels.cuh", "plan_tasks.hpp"]
+CHGPU_HEADERS = ["dev_types.cuh", "hash_kernels.cuh", "hash_tc.cuh", "join_kernels.cuh", "general_kernels.cuh", "match_kernels.cuh", "match_launch.cuh", "compact_kernels.cuh", "plan_tasks.hpp"]
 
 
 def _nvcc() -> str:

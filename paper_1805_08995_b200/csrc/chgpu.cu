@@ -37,6 +37,7 @@
 #include "hash_tc.cuh"
 #include "join_kernels.cuh"
 #include "compact_kernels.cuh"
+#include "general_kernels.cuh"
 #include "match_launch.cuh"
 
 using namespace chgpu;
@@ -174,6 +175,9 @@ struct chgpu_ctx {
 
     // family
     bool has_family = false, has_centering = false;
+    bool sparse = false;  // short_bits > kMaxShortBits: images carry sorted (code, point) keys, matched by the general path
+    unsigned long long* d_list_offs = nullptr;  // explicit candidate lists of one pair (chgpu_match_pair_lists)
+    uint32_t* d_list_ids = nullptr;
     uint32_t centering_gen = 1;  // bumped when a DIFFERENT centering vector is installed: codes hashed before are stale
     chgpu_family_params fam{};
     double* d_planes = nullptr;
@@ -275,7 +279,7 @@ uint32_t tile_points_of(const chgpu_ctx* ctx) {
     return uint32_t(std::max<size_t>(1024, std::min(cap, want)));
 }
 uint32_t tile_count_of(const chgpu_ctx* ctx, uint32_t n) {
-    if (n <= smem_train_capacity(ctx)) return 0;
+    if (ctx->sparse || n <= smem_train_capacity(ctx)) return 0;  // (sparse indices: the general path reads global memory)
     const uint32_t tp = tile_points_of(ctx);
     return (n + tp - 1) / tp;
 }
@@ -301,6 +305,14 @@ size_t image_block_bytes(uint32_t n, uint32_t m, uint32_t L, size_t off[9], bool
     off[1] = o; o += align_up(size_t(n) * 16);
     off[2] = o; o += align_up(size_t(n) * 16);
     off[3] = o; o += align_up(size_t(n) * L * 4);
+    if (m > uint32_t(kMaxShortBits)) {
+        // sparse bucket index (general_kernels.cuh): L x n keys  code << 16 | point  in the place of the dense offsets;
+        // no point / scan lists, no bucket-sorted copies
+        off[4] = o; o += align_up(size_t(L) * n * 8);
+        off[5] = off[6] = o;
+        off[7] = off[8] = 0;
+        return std::max(o + kAlign, kAlign);
+    }
     off[4] = o; o += align_up(size_t(L) * ((size_t(1) << m) + 1) * 4);
     off[5] = o; o += align_up(size_t(L) * n * 2);
     off[6] = o; o += align_up(size_t(L) * n * 2);
@@ -459,7 +471,7 @@ chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t
     }
     size_t off[9];
     std::vector<size_t> toff;
-    const bool sorted_copies = n != 0;  // (tiled images too: the join pass replaces the tiles' min pass)
+    const bool sorted_copies = n != 0 && !ctx->sparse;  // (tiled images too: the join pass replaces the tiles' min pass)
     const size_t own = image_block_bytes(n, m, L, off, sorted_copies);
     const size_t bytes = own + tile_block_bytes(n, m, L, ntiles, tp, &toff);
     char* block = nullptr;
@@ -531,6 +543,11 @@ chgpu_status ensure_slots_scratch(chgpu_ctx* ctx, size_t count) {
 
 chgpu_status launch_bucket_build(chgpu_ctx* ctx, uint32_t count) {
     const uint32_t m = ctx->fam.short_bits, L = ctx->fam.table_count;
+    if (ctx->sparse) {
+        sparse_index_kernel<<<dim3(count, L), kSparseThreads, 0, ctx->compute>>>(ctx->d_images, ctx->d_slots, L);
+        CK(cudaGetLastError());
+        return CHGPU_OK;
+    }
     const size_t smem = size_t(L) << m << 2;
     CK(cudaFuncSetAttribute(bucket_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     bucket_build_kernel<<<count, L * 32, smem, ctx->compute>>>(ctx->d_images, ctx->d_slots, m, L);
@@ -839,6 +856,8 @@ struct MatchRun {
     // debug
     uint32_t* dbg_ranked = nullptr;
     uint32_t* dbg_count = nullptr;
+    // explicit candidate lists of the ONE pair of the run (chgpu_match_pair_lists): already on the device
+    bool lists = false;
 };
 
 chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* stats_out);
@@ -861,8 +880,8 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
     if (!ctx->has_family) return fail(ctx, CHGPU_ELOGIC, "no hash family installed");
     const char* why = nullptr;
     if (!cfg_valid(run.cfg, ctx->fam.long_bits, &why)) return fail(ctx, CHGPU_EINVAL, "%s", why);
-    if (run.cfg.top_k > uint32_t(kMaxTopK))
-        return fail(ctx, CHGPU_EUNSUPPORTED, "top_k %u > %d is outside the device envelope", run.cfg.top_k, kMaxTopK);
+    // what the tuned kernels are not laid out for goes through the general path (general_kernels.cuh)
+    const bool general = ctx->sparse || run.cfg.top_k > uint32_t(kMaxTopK) || run.lists;
     const uint32_t npairs = run.npairs;
     chgpu_match_stats st{};
     st.pairs = npairs;
@@ -902,7 +921,7 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
             if ((gi && gi != ctx->centering_gen) || (gj && gj != ctx->centering_gen))
                 return fail(ctx, CHGPU_ELOGIC, "pair (%u,%u): codes were computed under a centering that has been replaced "
                             "(call chgpu_hash_images again)", run.pairs[2 * k], run.pairs[2 * k + 1]);
-            const uint32_t tiles = uint32_t(ctx->images[sj].tile_slots.size());
+            const uint32_t tiles = general ? 0u : uint32_t(ctx->images[sj].tile_slots.size());
             const bool tiled = tiles != 0;
             if (cur.count && (cur.queries + I.n > ctx->sub_batch_queries || cur.count >= pairs_cap || tiled != cur.tiled ||
                               (tiled && (cur.queries + I.n) * std::max(cur.max_tiles, tiles) * run.cfg.top_k * 4 > kTileListBytes))) {
@@ -1093,7 +1112,23 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
             P.dbg_count = ctx->d_dbg + size_t(sb.max_nq) * run.cfg.top_k;
         }
         uint32_t grid = 0;
-        if (sb.tiled) {
+        if (general) {
+            GeneralParams G{};
+            G.base = P;
+            G.npairs = sb.count;
+            G.queries = sb.queries;
+            G.sparse = ctx->sparse ? 1u : 0u;
+            G.list_offs = run.lists ? ctx->d_list_offs : nullptr;
+            G.list_ids = run.lists ? ctx->d_list_ids : nullptr;
+            const size_t gsmem = size_t(kGenWarps) * kGenCacheKeys * sizeof(uint32_t);
+            CK(cudaFuncSetAttribute(general_match_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsmem)));
+            const uint64_t want = (sb.queries + kGenWarps - 1) / kGenWarps;
+            grid = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(ctx->prop.multiProcessorCount) * 24)));
+            CK(cudaEventRecord(b.ev_k0, ctx->compute));
+            general_match_kernel<<<grid, kGenThreads, gsmem, ctx->compute>>>(G);
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(b.ev_k1, ctx->compute));
+        } else if (sb.tiled) {
             // (query image, tile) pairs: min pass, top-k pass for the queries with a candidate within tau, merge
             const uint32_t tp = tile_points_of(ctx);
             if (b.tpairs_cap < sb.tile_pairs) {
@@ -1406,6 +1441,7 @@ void chgpu_destroy(chgpu_ctx* ctx) {
     }
     cudaFree(ctx->d_planes); cudaFree(ctx->d_centering); cudaFree(ctx->d_sums); cudaFree(ctx->d_res);
     cudaFree(ctx->d_stats); cudaFreeHost(ctx->h_stats); cudaFree(ctx->d_counter); cudaFree(ctx->d_slots);
+    cudaFree(ctx->d_list_offs); cudaFree(ctx->d_list_ids);
     cudaFree(ctx->d_dbg); cudaFree(ctx->d_gmin); cudaFree(ctx->d_gdone); cudaFree(ctx->d_lists); cudaFree(ctx->d_act); cudaFree(ctx->d_nact); cudaFree(ctx->d_hit);
     cudaFreeHost(ctx->load_pinned);
     cudaFree(ctx->load_region);
@@ -1496,9 +1532,8 @@ chgpu_status chgpu_set_family(chgpu_ctx* ctx, const chgpu_family_params* p, cons
     DeviceGuard guard(ctx->device);
     if (chgpu_host_check_family(p) != 0)
         return fail(ctx, CHGPU_EINVAL, "family parameters violate 1<=m<=32, m<n<=128, L>=1 (hashing.cpp:30-36)");
-    if (p->short_bits > uint32_t(kMaxShortBits) || p->table_count > uint32_t(kMaxTables))
-        return fail(ctx, CHGPU_EUNSUPPORTED, "device envelope is m <= %d, L <= %d (got m=%u, L=%u)", kMaxShortBits,
-                    kMaxTables, p->short_bits, p->table_count);
+    if (p->table_count > uint32_t(kMaxTables))
+        return fail(ctx, CHGPU_EUNSUPPORTED, "device envelope is L <= %d (got L=%u)", kMaxTables, p->table_count);
     if (!ctx->slot_of.empty())
         return fail(ctx, CHGPU_ELOGIC, "evict all images before installing a different family");
     CK(cudaStreamSynchronize(ctx->compute));
@@ -1510,6 +1545,7 @@ chgpu_status chgpu_set_family(chgpu_ctx* ctx, const chgpu_family_params* p, cons
     CK(cudaMemcpy(ctx->d_planes + ns * kDim, long_planes, nl * kDim * sizeof(double), cudaMemcpyHostToDevice));
     ctx->fam = *p;
     ctx->has_family = true;
+    ctx->sparse = p->short_bits > uint32_t(kMaxShortBits);
     ctx->h_planes.assign(short_planes, short_planes + ns * kDim);
     ctx->h_planes.insert(ctx->h_planes.end(), long_planes, long_planes + nl * kDim);
     return refresh_hash_filter(ctx);
@@ -2443,6 +2479,9 @@ chgpu_status chgpu_download_bucket_index(chgpu_ctx* ctx, uint32_t image_id, uint
     if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
     const DevImage& d = ctx->images[slot].dev;
     if (!(d.flags & 1u)) return fail(ctx, CHGPU_ELOGIC, "image %u: codes not computed", image_id);
+    if (ctx->sparse)
+        return fail(ctx, CHGPU_EUNSUPPORTED, "short_bits %u: the image has no dense offset table (chgpu_download_sorted_index)",
+                    ctx->fam.short_bits);
     if (const chgpu_status s = chgpu_sync(ctx)) return s;
     const uint32_t L = ctx->fam.table_count;
     const size_t noff = size_t(L) * ((size_t(1) << ctx->fam.short_bits) + 1);
@@ -2597,6 +2636,147 @@ chgpu_status chgpu_debug_ranked(chgpu_ctx* ctx, uint32_t image_i, uint32_t image
     run.dbg_ranked = ranked;
     run.dbg_count = ranked_count;
     return run_match(ctx, run, nullptr);
+}
+
+// ---- general path: sorted index, candidate lists, match from explicit lists (general_kernels.cuh) ---------------------
+chgpu_status chgpu_download_sorted_index(chgpu_ctx* ctx, uint32_t image_id, uint32_t* codes, uint32_t* points) {
+    if (!ctx || !codes || !points) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    uint32_t slot = 0;
+    if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
+    const DevImage& d = ctx->images[slot].dev;
+    if (!(d.flags & 1u)) return fail(ctx, CHGPU_ELOGIC, "image %u: codes not computed", image_id);
+    if (const chgpu_status s = chgpu_sync(ctx)) return s;
+    const uint32_t L = ctx->fam.table_count, nb1 = ctx->sparse ? 0u : (1u << ctx->fam.short_bits) + 1u;
+    const size_t entries = size_t(L) * d.n;
+    if (entries == 0) return CHGPU_OK;
+    if (ctx->sparse) {
+        std::vector<unsigned long long> keys(entries);
+        CK(cudaMemcpy(keys.data(), d.offs, entries * 8, cudaMemcpyDeviceToHost));
+        for (size_t e = 0; e < entries; ++e) {
+            codes[e] = uint32_t(keys[e] >> 16);
+            points[e] = uint32_t(keys[e] & 0xffffu);
+        }
+    } else {
+        std::vector<uint32_t> offs(size_t(L) * nb1);
+        std::vector<uint16_t> pts(entries);
+        CK(cudaMemcpy(offs.data(), d.offs, offs.size() * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(pts.data(), d.points, entries * 2, cudaMemcpyDeviceToHost));
+        for (uint32_t t = 0; t < L; ++t)
+            for (uint32_t c = 0; c + 1 < nb1; ++c)
+                for (uint32_t e = offs[size_t(t) * nb1 + c]; e < offs[size_t(t) * nb1 + c + 1]; ++e) {
+                    codes[size_t(t) * d.n + e] = c;
+                    points[size_t(t) * d.n + e] = pts[size_t(t) * d.n + e];
+                }
+    }
+    return CHGPU_OK;
+}
+
+chgpu_status chgpu_pair_candidates(chgpu_ctx* ctx, uint32_t image_i, uint32_t image_j, uint64_t* offsets, uint32_t* candidates,
+                                   uint64_t capacity, uint64_t* total) {
+    if (!ctx || !offsets || (capacity && !candidates)) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    if (!ctx->has_family) return fail(ctx, CHGPU_ELOGIC, "no hash family installed");
+    uint32_t si = 0, sj = 0;
+    if (const chgpu_status s = find_slot(ctx, image_i, &si)) return s;
+    if (const chgpu_status s = find_slot(ctx, image_j, &sj)) return s;
+    const DevImage& I = ctx->images[si].dev;
+    const DevImage& J = ctx->images[sj].dev;
+    if (!(I.flags & 1u) || !(J.flags & 1u))
+        return fail(ctx, CHGPU_ELOGIC, "pair (%u,%u): codes not computed (call chgpu_hash_images first)", image_i, image_j);
+    offsets[0] = 0;
+    if (total) *total = 0;
+    if (I.n == 0) return CHGPU_OK;
+    if (const chgpu_status s = order_compute_after_copy(ctx)) return s;
+    uint32_t* d_counts = nullptr;
+    unsigned long long* d_offs = nullptr;
+    uint32_t* d_out = nullptr;
+    auto cleanup = [&] {
+        cudaFree(d_counts);
+        cudaFree(d_offs);
+        cudaFree(d_out);
+    };
+    const size_t smem = size_t(kGenWarps) * kGenBitmapWords * sizeof(uint32_t);
+    const uint32_t grid = std::max(1u, std::min((I.n + kGenWarps - 1) / kGenWarps, uint32_t(ctx->prop.multiProcessorCount) * 3u));
+    chgpu_status rc = CHGPU_OK;
+    auto run = [&]() -> chgpu_status {
+        CK(cudaFuncSetAttribute(cand_union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        CK(cudaMalloc(&d_counts, size_t(I.n) * sizeof(uint32_t)));
+        cand_union_kernel<<<grid, kGenThreads, smem, ctx->compute>>>(ctx->d_images, si, sj, ctx->fam.short_bits, ctx->fam.table_count,
+                                                                    ctx->sparse ? 1u : 0u, d_counts, nullptr, nullptr);
+        CK(cudaGetLastError());
+        std::vector<uint32_t> counts(I.n);
+        CK(cudaMemcpyAsync(counts.data(), d_counts, size_t(I.n) * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->compute));
+        CK(cudaStreamSynchronize(ctx->compute));
+        for (uint32_t q = 0; q < I.n; ++q) offsets[q + 1] = offsets[q] + counts[q];
+        const uint64_t sum = offsets[I.n];
+        if (total) *total = sum;
+        if (sum > capacity) return fail(ctx, CHGPU_ENOMEM, "candidate capacity %llu < %llu required", (unsigned long long)capacity,
+                                        (unsigned long long)sum);
+        if (sum == 0) return CHGPU_OK;
+        static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "offset width");
+        CK(cudaMalloc(&d_offs, (size_t(I.n) + 1) * sizeof(unsigned long long)));
+        CK(cudaMalloc(&d_out, sum * sizeof(uint32_t)));
+        CK(cudaMemcpyAsync(d_offs, offsets, (size_t(I.n) + 1) * sizeof(unsigned long long), cudaMemcpyHostToDevice, ctx->compute));
+        cand_union_kernel<<<grid, kGenThreads, smem, ctx->compute>>>(ctx->d_images, si, sj, ctx->fam.short_bits, ctx->fam.table_count,
+                                                                    ctx->sparse ? 1u : 0u, nullptr, d_offs, d_out);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(candidates, d_out, sum * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->compute));
+        CK(cudaStreamSynchronize(ctx->compute));
+        return CHGPU_OK;
+    };
+    rc = run();
+    if (rc != CHGPU_OK && rc != CHGPU_ENOMEM) {
+        cudaStreamSynchronize(ctx->compute);
+        cudaGetLastError();
+    }
+    cleanup();
+    return rc;
+}
+
+chgpu_status chgpu_match_pair_lists(chgpu_ctx* ctx, uint32_t image_i, uint32_t image_j, const chgpu_match_cfg* cfg,
+                                    const uint64_t* list_offsets, const uint32_t* list_ids, chgpu_match_record* records,
+                                    uint64_t capacity, uint64_t* total, chgpu_match_stats* stats) {
+    if (!ctx || !cfg || !list_offsets || (capacity && !records)) return CHGPU_EINVAL;
+    DeviceGuard guard(ctx->device);
+    uint32_t si = 0, sj = 0;
+    if (const chgpu_status s = find_slot(ctx, image_i, &si)) return s;
+    if (const chgpu_status s = find_slot(ctx, image_j, &sj)) return s;
+    const uint32_t nq = ctx->images[si].dev.n, nt = ctx->images[sj].dev.n;
+    const uint64_t sum = list_offsets[nq];
+    if (list_offsets[0] != 0) return fail(ctx, CHGPU_EINVAL, "candidate lists: offsets must start at 0");
+    for (uint32_t q = 0; q < nq; ++q) {
+        if (list_offsets[q + 1] < list_offsets[q]) return fail(ctx, CHGPU_EINVAL, "candidate lists: offsets decrease at query %u", q);
+        if (list_offsets[q + 1] - list_offsets[q] >= (1ull << 24))
+            return fail(ctx, CHGPU_EUNSUPPORTED, "candidate list of query %u has %llu entries; the device ranks < 2^24 per query", q,
+                        (unsigned long long)(list_offsets[q + 1] - list_offsets[q]));
+    }
+    if (sum && !list_ids) return CHGPU_EINVAL;
+    for (uint64_t e = 0; e < sum; ++e)
+        if (list_ids[e] >= nt) return fail(ctx, CHGPU_EINVAL, "candidate lists: entry %llu names train point %u of %u", (unsigned long long)e, list_ids[e], nt);
+    CK(cudaStreamSynchronize(ctx->compute));
+    cudaFree(ctx->d_list_offs);
+    cudaFree(ctx->d_list_ids);
+    ctx->d_list_offs = nullptr;
+    ctx->d_list_ids = nullptr;
+    static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "offset width");
+    CK(cudaMalloc(&ctx->d_list_offs, (size_t(nq) + 1) * sizeof(unsigned long long)));
+    CK(cudaMalloc(&ctx->d_list_ids, std::max<uint64_t>(sum, 1) * sizeof(uint32_t)));
+    CK(cudaMemcpy(ctx->d_list_offs, list_offsets, (size_t(nq) + 1) * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    if (sum) CK(cudaMemcpy(ctx->d_list_ids, list_ids, sum * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    const uint32_t pr[2] = {image_i, image_j};
+    uint64_t offs[2] = {0, 0};
+    MatchRun run{pr, 1, *cfg, SinkMode::Host};
+    run.offsets = offs;
+    run.records = records;
+    run.capacity = capacity;
+    run.lists = true;
+    const chgpu_status s = run_match(ctx, run, stats);
+    if (total) *total = run.total;
+    if (s != CHGPU_OK) return s;
+    if (run.overflow)
+        return fail(ctx, CHGPU_ENOMEM, "record capacity %llu < %llu required", (unsigned long long)capacity, (unsigned long long)run.total);
+    return CHGPU_OK;
 }
 
 }  // extern "C"

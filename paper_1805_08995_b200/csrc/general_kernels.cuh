@@ -1,0 +1,323 @@
+// general_kernels.cuh — KG, the general match path: everything the reference accepts and the tuned kernels (K3, K3j, the
+// tiles) are not laid out for.
+//
+//   * short codes of 13..32 bits (hashing.cpp:30-36 allows 1..32): a dense 2^m + 1 offset table per image does not exist
+//     for them.  The bucket index of such an image is the reference's own form (build_bucket_index, matcher.cpp:27-51:
+//     the points of a table sorted by (code, point)), stored as one u64 key  code << 16 | point  per entry and searched
+//     by bisection (BucketIndex::bucket, matcher.cpp:19-25) — sparse_index_kernel builds it with a sorting network.
+//   * top_k > 32 (validate, matcher.cpp:9-17 asks for >= 2 only): the tuned kernels keep the ranked list one entry per
+//     lane.  Here the list is never stored: every ranked key is verified the moment it is pulled.
+//   * match_pair_filtered with a HOST callback (matcher.hpp:92-105, hook matcher.cpp:172): the candidate lists of a pair
+//     are formed on the device (cand_union_kernel: concatenate the L buckets, sort, unique — matcher.cpp:164-171), handed
+//     to the caller's filter on the host, and whatever comes back is ranked and verified on the device from the explicit
+//     lists.  The reference ranks such a list with a stable counting sort (fill_histogram, matcher.cpp:68-84): ties in
+//     the distance keep the ORDER OF THE LIST, duplicates stay — so the key is  distance << 24 | position.
+//
+// One warp per query.  A candidate's key is  distance << 24 | id  (buckets; the same point reached through several
+// tables has the same key, so pulling keys in strictly ascending order is the reference's sort + unique) or
+// distance << 24 | position (explicit lists).  The ranked list is the first keys in ascending order, cut by the threshold
+// and re-ranked without it by the rule of matcher.cpp:176-189; each is verified as it is pulled (euclidean_verify,
+// matcher.cpp:115-137: exact integer distances, best / second with strict '<', Lowe ratio in fp64).  Keys are kept in a
+// per-warp shared-memory cache when the query has at most kGenCacheKeys candidates and recomputed per pull otherwise.
+// Not tuned: this path exists so that no input the reference accepts fails on the device.
+#pragma once
+
+#include "match_kernels.cuh"
+
+namespace chgpu {
+
+constexpr int kGenThreads = 256;
+constexpr uint32_t kGenWarps = kGenThreads / 32;
+constexpr uint32_t kGenCacheKeys = 2048;  // per warp: 8 KB
+constexpr uint32_t kGenBitmapWords = kMaxPoints / 32;  // cand_union_kernel: one bit per train point, per warp
+
+struct GeneralParams {
+    MatchParams base;  // images, pairs, res, pair_counts, stats, m, L, top_k, tau, min_ranked, ratio_sq, fmats, band_px, dbg_*
+    uint32_t npairs;
+    unsigned long long queries;            // of the sub-batch (PairDesc::res_off indexes them)
+    uint32_t sparse;                       // the images carry sorted (code, point) keys instead of dense offsets
+    const unsigned long long* list_offs;   // explicit candidate lists of ONE pair: n_i + 1 offsets into list_ids, or nullptr
+    const uint32_t* list_ids;
+};
+
+// The L bucket ranges of one query in the train image's index: table t covers entries [first[t], first[t] + len[t]) of the
+// image's entry array (points / sorted keys, table-major).  Lane t resolves table t.
+struct BucketRanges {
+    uint32_t first[kMaxTables], len[kMaxTables];
+    uint32_t total;
+};
+__device__ __forceinline__ BucketRanges resolve_ranges(const DevImage& I, const DevImage& J, uint32_t q, uint32_t L, uint32_t m,
+                                                       bool sparse, uint32_t lane) {
+    constexpr uint32_t FULL = 0xffffffffu;
+    uint32_t a = 0, n = 0;
+    if (lane < L) {
+        const uint32_t code = __ldg(I.shorts + uint64_t(q) * L + lane);
+        if (!sparse) {
+            const uint32_t* o = J.offs + uint64_t(lane) * ((1u << m) + 1u) + code;
+            a = __ldg(o);
+            n = __ldg(o + 1) - a;
+        } else {
+            // BucketIndex::bucket (matcher.cpp:19-25) on the sorted keys: entries with this code form one run
+            const unsigned long long* keys = reinterpret_cast<const unsigned long long*>(J.offs) + uint64_t(lane) * J.n;
+            const unsigned long long lo_key = (unsigned long long)code << 16, hi_key = lo_key | 0xffffull;
+            uint32_t lo = 0, hi = J.n;
+            while (lo < hi) {  // first entry >= lo_key
+                const uint32_t mid = (lo + hi) >> 1;
+                if (__ldg(keys + mid) < lo_key) lo = mid + 1;
+                else hi = mid;
+            }
+            a = lo;
+            hi = J.n;
+            while (lo < hi) {  // first entry > hi_key
+                const uint32_t mid = (lo + hi) >> 1;
+                if (__ldg(keys + mid) <= hi_key) lo = mid + 1;
+                else hi = mid;
+            }
+            n = lo - a;
+        }
+        a += lane * J.n;
+    }
+    BucketRanges r;
+    r.total = 0;
+#pragma unroll
+    for (int t = 0; t < kMaxTables; ++t) {
+        r.first[t] = __shfl_sync(FULL, a, t);
+        r.len[t] = uint32_t(t) < L ? __shfl_sync(FULL, n, t) : 0u;
+        r.total += r.len[t];
+    }
+    return r;
+}
+// point id behind flat candidate index i (< r.total) of the concatenated buckets
+__device__ __forceinline__ uint32_t range_id(const BucketRanges& r, const DevImage& J, bool sparse, uint32_t i) {
+    uint32_t e = 0;
+    bool found = false;
+#pragma unroll
+    for (int t = 0; t < kMaxTables; ++t) {
+        if (!found && i < r.len[t]) {
+            e = r.first[t] + i;
+            found = true;
+        }
+        if (!found) i -= r.len[t];
+    }
+    if (sparse) return uint32_t(__ldg(reinterpret_cast<const unsigned long long*>(J.offs) + e) & 0xffffull);
+    return __ldg(J.points + e);
+}
+
+// pair whose queries contain entry g of the sub-batch's query space (PairDesc::res_off ascending; pairs without queries
+// share their successor's offset and are skipped by taking the LAST pair with res_off <= g)
+__device__ __forceinline__ uint32_t pair_of_query(const PairDesc* __restrict__ pairs, uint32_t npairs, unsigned long long g) {
+    uint32_t lo = 0, hi = npairs;  // last k with res_off <= g
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (pairs[mid].res_off <= g) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kGenThreads) general_match_kernel(const GeneralParams G) {
+    extern __shared__ __align__(16) uint32_t s_keys_all[];  // kGenWarps x kGenCacheKeys
+    constexpr uint32_t FULL = 0xffffffffu;
+    const MatchParams& P = G.base;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* s_keys = s_keys_all + warp * kGenCacheKeys;
+    const bool explicit_lists = G.list_offs != nullptr;
+    const bool sparse = G.sparse != 0;
+    const bool guided = P.fmats != nullptr;
+
+    for (unsigned long long g = (unsigned long long)blockIdx.x * kGenWarps + warp; g < G.queries;
+         g += (unsigned long long)gridDim.x * kGenWarps) {
+        const uint32_t pair = pair_of_query(P.pairs, G.npairs, g);
+        const PairDesc pd = P.pairs[pair];
+        const uint32_t q = uint32_t(g - pd.res_off);
+        const DevImage I = P.images[pd.slot_i];
+        const DevImage J = P.images[pd.slot_j];
+        uint32_t out_t = kNone, out_d = 0, n = 0;
+        if (J.n != 0) {
+            const uint4 ql = __ldg(I.longs + q);
+            BucketRanges r{};
+            unsigned long long list_lo = 0;
+            uint32_t C;
+            if (explicit_lists) {
+                list_lo = G.list_offs[q];
+                C = uint32_t(G.list_offs[q + 1] - list_lo);
+            } else {
+                r = resolve_ranges(I, J, q, P.L, P.m, sparse, lane);
+                C = r.total;
+                if (lane == 0 && C) atomicAdd(&P.stats->raw_candidates, (unsigned long long)C);  // matcher.cpp:168
+            }
+            EpiLine line{};
+            if (guided) line = epipolar_band(P.fmats + uint64_t(pd.pair_idx) * 9, __ldg(I.kp + q));
+            auto id_of = [&](uint32_t i) -> uint32_t {
+                return explicit_lists ? __ldg(G.list_ids + list_lo + i) : range_id(r, J, sparse, i);
+            };
+            auto key_at = [&](uint32_t i) -> uint32_t {
+                const uint32_t id = id_of(i);
+                const uint32_t d = hamming128(__ldg(J.longs + id), ql);
+                uint32_t key = (d << 24) | (explicit_lists ? i : id);
+                if (guided) key = band_filter(key, line, J.kp, P.band_px);
+                return key;
+            };
+            const bool cached = C <= kGenCacheKeys;
+            // smallest key above `prev` (first: smallest key at all), kNone when there is none
+            auto pull = [&](uint32_t prev, bool first) -> uint32_t {
+                uint32_t best = kNone;
+                for (uint32_t i = lane; i < C; i += 32) {
+                    const uint32_t k = cached ? s_keys[i] : key_at(i);
+                    if ((first || k > prev) && k < best) best = k;
+                }
+                return __reduce_min_sync(FULL, best);
+            };
+            __syncwarp();  // the previous query's cache is no longer read
+            if (cached)
+                for (uint32_t i = lane; i < C; i += 32) s_keys[i] = key_at(i);
+            __syncwarp();
+
+            // this lane's 4 bytes of the query row
+            const uint32_t qrow = __ldg(reinterpret_cast<const uint32_t*>(I.desc + uint64_t(q) * kDim) + lane);
+            uint32_t best = kNone, second = kNone, best_id = kNone;
+            uint32_t nk = pull(0u, true);
+            bool unthresholded = false;  // the re-rank of matcher.cpp:183-189 is under way
+            if (nk != kNone && (nk >> 24) <= P.tau) {
+                for (;;) {
+                    // rank n: verified at once (euclidean_verify's loop body, matcher.cpp:124-133)
+                    const uint32_t id = explicit_lists ? __ldg(G.list_ids + list_lo + (nk & 0xffffffu)) : (nk & 0xffffffu);
+                    const uint32_t trow = __ldg(reinterpret_cast<const uint32_t*>(J.desc + uint64_t(id) * kDim) + lane);
+                    const uint32_t d = __reduce_add_sync(FULL, sqdiff4(qrow, trow));
+                    if (d < best) {
+                        second = best;
+                        best = d;
+                        best_id = id;
+                    } else if (d < second) {
+                        second = d;
+                    }
+                    if (P.dbg_ranked != nullptr && lane == 0) P.dbg_ranked[uint64_t(q) * P.top_k + n] = id;
+                    ++n;
+                    if (n == P.top_k) break;
+                    nk = pull(nk, false);
+                    if (nk == kNone) break;
+                    if (!unthresholded && (nk >> 24) > P.tau) {
+                        // the threshold cut something; a ranking too small for the ratio test is redone without it
+                        if (n < P.min_ranked) unthresholded = true;
+                        else break;
+                    }
+                }
+            }
+            if (n >= 2) {
+                if (lane == 0) {
+                    atomicAdd(&P.stats->verified_queries, 1ull);
+                    atomicAdd(&P.stats->distances, (unsigned long long)n);
+                }
+                if (second != 0u && double(best) < __dmul_rn(P.ratio_sq, double(second))) {
+                    out_t = best_id;
+                    out_d = best;
+                    if (lane == 0) atomicAdd(&P.pair_counts[pair], 1u);
+                }
+            }
+        }
+        if (P.dbg_count != nullptr && lane == 0) P.dbg_count[q] = n;
+        if (lane == 0) __stcs(P.res + g, make_uint2(out_t, out_d));
+    }
+}
+
+// Candidate lists of one pair (matcher.cpp:164-171): per query the L buckets concatenated, sorted, made unique — through a
+// bitmap over the train image's point ids in shared memory (one bit per point, per warp).  out == nullptr: counts[q] = size
+// of the list; otherwise the list of query q goes to out[offsets[q] ...], ascending ids.
+__global__ void __launch_bounds__(kGenThreads) cand_union_kernel(const DevImage* __restrict__ images, uint32_t slot_i, uint32_t slot_j,
+                                                                 uint32_t m, uint32_t L, uint32_t sparse, uint32_t* __restrict__ counts,
+                                                                 const unsigned long long* __restrict__ offsets,
+                                                                 uint32_t* __restrict__ out) {
+    extern __shared__ __align__(16) uint32_t s_bits_all[];  // kGenWarps x kGenBitmapWords
+    constexpr uint32_t FULL = 0xffffffffu;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* bits = s_bits_all + warp * kGenBitmapWords;
+    const DevImage I = images[slot_i];
+    const DevImage J = images[slot_j];
+    const uint32_t words = (J.n + 31) / 32;
+    for (uint32_t w = lane; w < words; w += 32) bits[w] = 0;
+    __syncwarp();
+    for (uint32_t q = blockIdx.x * kGenWarps + warp; q < I.n; q += gridDim.x * kGenWarps) {
+        uint32_t total = 0;
+        if (J.n != 0) {
+            const BucketRanges r = resolve_ranges(I, J, q, L, m, sparse != 0, lane);
+            uint32_t wmin = kNone, wmax = 0;
+            for (uint32_t i = lane; i < r.total; i += 32) {
+                const uint32_t id = range_id(r, J, sparse != 0, i);
+                atomicOr(bits + (id >> 5), 1u << (id & 31));
+                wmin = min(wmin, id >> 5);
+                wmax = max(wmax, id >> 5);
+            }
+            wmin = __reduce_min_sync(FULL, wmin);
+            wmax = __reduce_max_sync(FULL, wmax);
+            __syncwarp();
+            if (r.total != 0) {
+                uint32_t* dst = out ? out + offsets[q] : nullptr;
+                for (uint32_t w0 = wmin; w0 <= wmax; w0 += 32) {
+                    const uint32_t w = w0 + lane;
+                    uint32_t word = w <= wmax ? bits[w] : 0u;
+                    if (w <= wmax) bits[w] = 0;
+                    const uint32_t c = __popc(word);
+                    uint32_t incl = c;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t u = __shfl_up_sync(FULL, incl, d);
+                        if (int(lane) >= d) incl += u;
+                    }
+                    if (dst) {
+                        uint32_t at = total + incl - c;
+                        while (word) {
+                            dst[at++] = w * 32u + uint32_t(__ffs(word) - 1);
+                            word &= word - 1;
+                        }
+                    }
+                    total += __shfl_sync(FULL, incl, 31);
+                }
+            }
+            __syncwarp();
+        }
+        if (!out && lane == 0) counts[q] = total;
+    }
+}
+
+// Sparse bucket index of one (image, table): keys  code << 16 | point  sorted ascending = the reference's sort of (code,
+// point) pairs (matcher.cpp:34-37).  A bitonic network whose every compare-exchange is ascending (the first step of each
+// merge mirrors its block), so the positions past n behave as +infinity without being stored: an exchange whose upper
+// partner lies past n is a no-op.
+constexpr int kSparseThreads = 1024;
+__global__ void __launch_bounds__(kSparseThreads) sparse_index_kernel(const DevImage* __restrict__ images, const uint32_t* __restrict__ slots,
+                                                                      uint32_t L) {
+    const DevImage img = images[slots[blockIdx.x]];
+    const uint32_t t = blockIdx.y, n = img.n;
+    if (n == 0) return;
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(img.offs) + uint64_t(t) * n;
+    for (uint32_t p = threadIdx.x; p < n; p += kSparseThreads)
+        keys[p] = ((unsigned long long)__ldg(img.shorts + uint64_t(p) * L + t) << 16) | p;
+    uint32_t npow = 1;
+    while (npow < n) npow <<= 1;
+    auto exchange = [&](uint32_t lo, uint32_t hi) {
+        if (hi < n) {
+            const unsigned long long a = keys[lo], b = keys[hi];
+            if (a > b) {
+                keys[lo] = b;
+                keys[hi] = a;
+            }
+        }
+    };
+    for (uint32_t k = 2; k <= npow; k <<= 1) {
+        __syncthreads();
+        const uint32_t half = k >> 1;
+        for (uint32_t x = threadIdx.x; x < npow / 2; x += kSparseThreads) {
+            const uint32_t base = (x / half) * k, o = x % half;
+            exchange(base + o, base + k - 1u - o);
+        }
+        for (uint32_t j = k >> 2; j > 0; j >>= 1) {
+            __syncthreads();
+            for (uint32_t x = threadIdx.x; x < npow / 2; x += kSparseThreads) {
+                const uint32_t lo = (x / j) * 2u * j + (x % j);
+                exchange(lo, lo + j);
+            }
+        }
+    }
+}
+
+}  // namespace chgpu

@@ -373,16 +373,57 @@ static void device_checks(const std::filesystem::path& tmp) {
         bad = {};
         bad.hamming_threshold = 129;
         CHECK(throws<std::invalid_argument>([&] { ch::match_pair(sets[0], sets[1], codes[0], codes[1], bad); }));
-        // valid for the reference, outside the device envelope: a distinct exception, at the first value beyond it
+        // beyond the tuned kernels (top_k > 32, short_bits > 12) the same calls take the general path: same records
         ch::MatchConfig wide;
-        wide.top_k = ch::kDeviceMaxTopK + 1;
-        CHECK(throws<ch::UnsupportedOnDevice>([&] { ch::match_pair(sets[0], sets[1], codes[0], codes[1], wide); }));
-        wide.top_k = ch::kDeviceMaxTopK;  // the last value inside it works
-        CHECK(!throws<ch::UnsupportedOnDevice>([&] { ch::match_pair(sets[0], sets[1], codes[0], codes[1], wide); }));
-        ch::FamilyParams fp13;
-        fp13.short_bits = ch::kDeviceMaxShortBits + 1;
-        const ch::HashFamily fam13 = ch::build_hash_family(fp13);  // host-side: the family itself is legal
-        CHECK(throws<ch::UnsupportedOnDevice>([&] { ch::Matcher m13; m13.set_family(fam13); }));
+        wide.top_k = ch::kTunedMaxTopK + 1;
+        CHECK(ch::match_pair(sets[0], sets[1], codes[0], codes[1], wide) == oracle_match(fam, wide, sets[0], ocodes[0], sets[1], ocodes[1]));
+        wide.top_k = 500;
+        CHECK(ch::match_pair(sets[0], sets[1], codes[0], codes[1], wide) == oracle_match(fam, wide, sets[0], ocodes[0], sets[1], ocodes[1]));
+        {
+            ch::FamilyParams fp13;
+            fp13.short_bits = ch::kTunedMaxShortBits + 1;
+            ch::HashFamily fam13 = ch::build_hash_family(fp13);
+            ch::set_centering(fam13, std::span<const ch::FeatureSet>(sets.data(), 2));
+            const ch::ImageCodes c0 = ch::compute_codes(fam13, sets[0]), c1 = ch::compute_codes(fam13, sets[1]);
+            const OracleCodes o0 = oracle_codes(fam13, sets[0], 3), o1 = oracle_codes(fam13, sets[1], 3);
+            CHECK(c0.shorts.values == o0.shorts && c1.shorts.values == o1.shorts);
+            const auto want13 = oracle_match(fam13, {}, sets[0], o0, sets[1], o1);
+            CHECK(!want13.empty() && ch::match_pair(sets[0], sets[1], c0, c1, {}) == want13);
+        }
+        // match_pair_filtered (matcher.hpp:102-105) with a host callback that thins, reverses and repeats candidates:
+        // the oracle side runs match_pair_filtered with the lists the same callback leaves
+        {
+            const ch::CandidateFilter filter = [](std::uint32_t q, std::vector<std::uint32_t>& c) {
+                if (q % 4 == 0) c.clear();
+                else if (q % 4 == 1) std::reverse(c.begin(), c.end());
+                else if (q % 4 == 2) c.push_back(c.front());
+                return true;
+            };
+            const auto got = ch::match_pair_filtered(sets[0], sets[1], codes[0], codes[1], {}, filter);
+            std::vector<std::uint64_t> lo{0};
+            std::vector<std::uint32_t> ids, one(sets[1].size());
+            for (std::uint32_t q = 0; q < sets[0].size(); ++q) {
+                std::uint32_t cnt = 0;
+                CHECK(chor_lookup_candidates(8, 6, ocodes[0].shorts.data() + std::size_t(q) * 6, ocodes[1].shorts.data(),
+                                             std::uint32_t(sets[1].size()), one.data(), &cnt) == 0);
+                std::vector<std::uint32_t> c(one.begin(), one.begin() + cnt);
+                if (!c.empty()) filter(q, c);
+                ids.insert(ids.end(), c.begin(), c.end());
+                lo.push_back(ids.size());
+            }
+            std::vector<ch::MatchRecord> want(sets[0].size() + 1);
+            std::uint32_t count = 0;
+            const chor_family_params p = to_chor(fam.params);
+            const chor_match_cfg c = to_chor(ch::MatchConfig{});
+            CHECK(chor_match_pair_lists(&p, &c, sets[0].descriptors.front().data(), std::uint32_t(sets[0].size()), ocodes[0].shorts.data(),
+                                        ocodes[0].longs.data(), sets[1].descriptors.front().data(), std::uint32_t(sets[1].size()),
+                                        ocodes[1].shorts.data(), ocodes[1].longs.data(), lo.data(), ids.data(),
+                                        reinterpret_cast<chor_match_record*>(want.data()), &count, nullptr, nullptr, nullptr) == 0);
+            want.resize(count);
+            CHECK(!want.empty() && got == want);
+            CHECK(ch::match_pair_filtered(sets[0], sets[1], codes[0], codes[1], {}, nullptr) ==
+                  oracle_match(fam, {}, sets[0], ocodes[0], sets[1], ocodes[1]));
+        }
         ch::FamilyParams fp9;
         fp9.table_count = ch::kDeviceMaxTables + 1;
         const ch::HashFamily fam9 = ch::build_hash_family(fp9);

@@ -60,6 +60,7 @@ class Oracle:
             "chor_build_bucket_index": [U32, U32, P, U32, P, P],
             "chor_lookup_candidates": [U32, U32, P, P, U32, P, P],
             "chor_match_pair": [P, P, P, U32, P, P, P, U32, P, P, P, P, P, P, P],
+            "chor_match_pair_lists": [P, P, P, U32, P, P, P, U32, P, P, P, P, P, P, P, P, P],
             "chor_brute_force_match": [P, U32, P, U32, D, P, P],
             "chor_guided_match_pair": [P, P, P, P, U32, P, P, P, P, U32, P, P, P, D, P, P, P, P, P],
             "chor_save_matches": [C.c_char_p, C.c_char_p, P, U32, C.c_char_p],
@@ -181,6 +182,36 @@ class Oracle:
             sj.ctypes.data, lj.ctypes.data, rec.ctypes.data, C.byref(cnt), C.byref(stats),
             C.c_void_p(ranked.ctypes.data if want_ranked else None),
             C.c_void_p(rcount.ctypes.data if want_ranked else None)), "match_pair")
+        out = rec[: cnt.value].copy()
+        if want_ranked:
+            return out, stats.as_dict(), ranked[:ni], rcount[:ni]
+        return out, stats.as_dict()
+
+    def match_pair_lists(self, params, cfg, desc_i, shorts_i, longs_i, desc_j, shorts_j, longs_j, list_offsets, list_ids,
+                         want_ranked=False):
+        """match_pair_filtered with a filter that replaces the candidates of query q by list_ids[offs[q]:offs[q+1]]."""
+        p, c = self._fp(params), self._cfg(cfg)
+        di = np.ascontiguousarray(desc_i, dtype=np.uint8).reshape(-1, 128)
+        dj = np.ascontiguousarray(desc_j, dtype=np.uint8).reshape(-1, 128)
+        si = np.ascontiguousarray(shorts_i, dtype=np.uint32)
+        sj = np.ascontiguousarray(shorts_j, dtype=np.uint32)
+        li = np.ascontiguousarray(longs_i, dtype=np.uint64)
+        lj = np.ascontiguousarray(longs_j, dtype=np.uint64)
+        lo = np.ascontiguousarray(list_offsets, dtype=np.uint64)
+        ids = np.ascontiguousarray(list_ids, dtype=np.uint32)
+        if len(ids) == 0:
+            ids = np.zeros(1, dtype=np.uint32)
+        ni, nj = len(di), len(dj)
+        rec = np.zeros(max(ni, 1), dtype=RECORD_DTYPE)
+        cnt = C.c_uint32(0)
+        stats = PairStatsC()
+        ranked = np.zeros((max(ni, 1), cfg.top_k), dtype=np.uint32) if want_ranked else None
+        rcount = np.zeros(max(ni, 1), dtype=np.uint32) if want_ranked else None
+        self._check(self.lib.chor_match_pair_lists(
+            C.byref(p), C.byref(c), di.ctypes.data, ni, si.ctypes.data, li.ctypes.data, dj.ctypes.data, nj,
+            sj.ctypes.data, lj.ctypes.data, lo.ctypes.data, ids.ctypes.data, rec.ctypes.data, C.byref(cnt), C.byref(stats),
+            C.c_void_p(ranked.ctypes.data if want_ranked else None),
+            C.c_void_p(rcount.ctypes.data if want_ranked else None)), "match_pair_lists")
         out = rec[: cnt.value].copy()
         if want_ranked:
             return out, stats.as_dict(), ranked[:ni], rcount[:ni]

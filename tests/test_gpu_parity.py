@@ -323,16 +323,14 @@ def test_errors_follow_the_reference(matcher, default_family):
                 ch.MatchConfig(ratio=0.0), ch.MatchConfig(reduce_rounds=8), ch.MatchConfig(reduce_rounds=-1)):
         with pytest.raises(ValueError):         # matcher.cpp:9-17
             matcher.match_pairs([(BASE, BASE + 1)], bad)
-    with pytest.raises(ch.UnsupportedError):
-        matcher.match_pairs([(BASE, BASE + 1)], ch.MatchConfig(top_k=33))
+    matcher.match_pairs([(BASE, BASE + 1)], ch.MatchConfig(top_k=33))  # general path (tests/test_general_path.py)
     with pytest.raises(KeyError):
         matcher.match_pairs([(BASE, 999999)], ch.MatchConfig())
     with pytest.raises(ch.UnsupportedError):
         matcher.upload(BASE + 2, np.zeros((65537, 128), np.uint8))
     m3 = ch.Matcher(0)
     try:
-        with pytest.raises(ch.UnsupportedError):
-            m3.set_family(ch.build_hash_family(ch.FamilyParams(short_bits=13)))
+        m3.set_family(ch.build_hash_family(ch.FamilyParams(short_bits=13)))  # sparse bucket index: general path
         with pytest.raises(ch.UnsupportedError):
             m3.set_family(ch.build_hash_family(ch.FamilyParams(table_count=9)))
     finally:
