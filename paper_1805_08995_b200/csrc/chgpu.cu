@@ -125,6 +125,7 @@ struct ImageRec {
     // id-range tiles of an image too large for the match kernel's shared-memory tile: hidden slots of the
     // image table whose DevImages are slices of this block with their own bucket index (local point ids)
     std::vector<uint32_t> tile_slots;
+    uint32_t tile_points = 0;  // points per tile (balanced_tile_points)
 };
 
 struct MatchBuffers {
@@ -282,6 +283,13 @@ uint32_t tile_count_of(const chgpu_ctx* ctx, uint32_t n) {
     if (ctx->sparse || n <= smem_train_capacity(ctx)) return 0;  // (sparse indices: the general path reads global memory)
     const uint32_t tp = tile_points_of(ctx);
     return (n + tp - 1) / tp;
+}
+// Points per tile of ONE image: its tiles are balanced (12,288 points = 2 x 6,144, not 8,192 + 4,096), so no tile carries the
+// overflow scan steps of a full one next to a half-empty neighbour; a multiple of 16 keeps every slice aligned.
+uint32_t balanced_tile_points(const chgpu_ctx* ctx, uint32_t n) {
+    const uint32_t tiles = tile_count_of(ctx, n);
+    if (tiles == 0) return tile_points_of(ctx);
+    return std::min(tile_points_of(ctx), ((n + tiles - 1) / tiles + 15u) & ~15u);
 }
 
 // Layout of the tiles' bucket arrays behind the image's own: per tile offs | points | scan.
@@ -455,7 +463,7 @@ chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t
         dense_set(ctx, image_id, kNone);
     }
     const uint32_t m = ctx->fam.short_bits, L = ctx->fam.table_count;
-    const uint32_t ntiles = tile_count_of(ctx, n), tp = tile_points_of(ctx);
+    const uint32_t ntiles = tile_count_of(ctx, n), tp = balanced_tile_points(ctx, n);
     const uint32_t slot = take_slot(ctx);
     std::vector<uint32_t> tile_slots(ntiles);
     for (uint32_t& ts : tile_slots) ts = take_slot(ctx);
@@ -498,6 +506,7 @@ chgpu_status alloc_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, uint32_t
     r.dev.n = n;
     r.dev.flags = 0;
     r.tile_slots = tile_slots;
+    r.tile_points = tp;
     for (uint32_t k = 0; k < ntiles; ++k) {
         ImageRec& t = ctx->images[tile_slots[k]];
         t = ImageRec{};
@@ -1172,7 +1181,7 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
                 const std::vector<uint32_t>& ts = ctx->images[pd.slot_j].tile_slots;
                 const size_t nq = (size_t(ctx->images[pd.slot_i].dev.n) + 7) & ~size_t(7);
                 for (uint32_t t = 0; t < ts.size(); ++t) {
-                    b.h_tpairs[ntp++] = PairDesc{pd.slot_i, ts[t], pd.res_off, t * tp, t, k, uint32_t(act_need)};
+                    b.h_tpairs[ntp++] = PairDesc{pd.slot_i, ts[t], pd.res_off, t * ctx->images[pd.slot_j].tile_points, t, k, uint32_t(act_need)};
                     act_need += nq;
                 }
             }
@@ -1494,7 +1503,7 @@ chgpu_status chgpu_image_device_bytes(chgpu_ctx* ctx, uint32_t n, uint64_t* byte
     if (n > kMaxPoints) return fail(ctx, CHGPU_EUNSUPPORTED, "%u points; device path holds <= %u", n, kMaxPoints);
     const uint32_t m = ctx->fam.short_bits, L = ctx->fam.table_count;
     size_t off[9];
-    *bytes = image_block_bytes(n, m, L, off, n != 0) + tile_block_bytes(n, m, L, tile_count_of(ctx, n), tile_points_of(ctx), nullptr);
+    *bytes = image_block_bytes(n, m, L, off, n != 0) + tile_block_bytes(n, m, L, tile_count_of(ctx, n), balanced_tile_points(ctx, n), nullptr);
     return CHGPU_OK;
 }
 
