@@ -28,7 +28,7 @@ namespace chgpu {
 
 constexpr int kGenThreads = 256;
 constexpr uint32_t kGenWarps = kGenThreads / 32;
-constexpr uint32_t kGenCacheKeys = 2048;  // per warp: 8 KB
+constexpr uint32_t kGenCacheKeys = 1024;  // per warp: 4 KB (32 KB per CTA: the occupancy of this latency-bound kernel matters more)
 constexpr uint32_t kGenBitmapWords = kMaxPoints / 32;  // cand_union_kernel: one bit per train point, per warp
 
 struct GeneralParams {
