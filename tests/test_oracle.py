@@ -318,6 +318,42 @@ def test_restatement_equals_reference_random(restatement, reference, params, n, 
         assert np.array_equal(oa[0], ob[0]) and np.array_equal(oa[1], ob[1])
 
 
+def test_list_filter_restatement_equals_reference(restatement, reference):
+    """chor_match_pair_lists: match_pair_filtered (matcher.hpp:102-105) with the candidates of every query replaced by a
+    given list — thinned, reordered, with repeats.  In oracle/_ref it is the reference's own function; the restatement must
+    agree on records, statistics and ranked lists, and unchanged lists must give match_pair."""
+    params = FamilyParams()
+    sp, lp = reference.build_family(params)
+    desc = make_dataset(2, 700, seed=321)
+    cen = reference.centering(list(desc))
+    codes = [reference.compute_codes(params, sp, lp, cen, desc[i]) for i in range(2)]
+    rng = np.random.default_rng(5)
+    same_lo, same_ids, lo, ids = [0], [], [0], []
+    for q in range(700):
+        c = reference.lookup_candidates(params.short_bits, params.table_count, codes[0][0][q], codes[1][0]).tolist()
+        same_ids += c
+        same_lo.append(len(same_ids))
+        kind = q % 4
+        if kind == 1:
+            c = c[::-1]
+        elif kind == 2:
+            c = [x for x in c if rng.random() < 0.7] + c[:1]
+        elif kind == 3:
+            c = []
+        ids += c
+        lo.append(len(ids))
+    for cfg in (MatchConfig(), MatchConfig(top_k=40, hamming_threshold=60), MatchConfig(top_k=3, min_candidates_for_ratio=6)):
+        args = (params, cfg, desc[0], *codes[0], desc[1], *codes[1])
+        a = reference.match_pair_lists(*args, lo, ids, want_ranked=True)
+        b = restatement.match_pair_lists(*args, lo, ids, want_ranked=True)
+        assert len(a[0]) > 0 and np.array_equal(a[0], b[0]) and a[1] == b[1] and np.array_equal(a[3], b[3])
+        for q in range(700):
+            assert np.array_equal(a[2][q, :a[3][q]], b[2][q, :b[3][q]])
+        plain = reference.match_pair(*args)
+        assert np.array_equal(reference.match_pair_lists(*args, same_lo, same_ids)[0], plain[0])
+        assert np.array_equal(restatement.match_pair_lists(*args, same_lo, same_ids)[0], plain[0])
+
+
 def test_restatement_matches_golden_guided_plans(restatement, golden):
     g = golden["plans_guided"]
     for key in [k for k in g.files if k.startswith("accepted_")]:
