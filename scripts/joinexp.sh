@@ -1,3 +1,4 @@
+# A/B of the join pass on the GPU box: parity subset, then per-kernel times (ncu launch list of a 2-launch bench) per build switch
 t() { ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file /tmp/jl.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --images 200 --pairs 7992 > /dev/null 2>&1
 python - <<PY
 import csv,collections
@@ -11,7 +12,6 @@ PY
 }
 b() { CHGPU_NVCC_EXTRA="$1" python -m paper_1805_08995_b200.build --force > /dev/null 2>&1; }
 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "match or golden or edge or pair_cases or config2" 2>&1 | tail -2
-t occ2_default
-b "-DCHGPU_JOIN_OCC=3"; t occ3
-b "-DCHGPU_JOIN_OCC=1"; t occ1
-b ""; 
+t default
+for v in "$@"; do b "$v"; t "$v"; done
+b ""
