@@ -21,8 +21,9 @@
 //
 // A caller of the reference switches by including this header and `namespace cashash =
 // cashash_b200;`.  The free functions run on a process-wide default
-// context for device 0 and serialise on it; they exist for drop-in use and for parity tests.
-// Throughput comes from the batch interface, `Matcher`: upload every image once, hash them in
+// context for device 0 and serialise on it; they exist for drop-in use and for parity tests
+// (match_pair and its variants keep the images they are handed resident by content, so a pair-list
+// walk uploads every image once).  Throughput comes from the batch interface, `Matcher`: upload every image once, hash them in
 // one launch, match a whole pair list per call.
 //
 // There is no CPU fallback: every function that computes goes through libchgpu.so and throws
@@ -953,10 +954,92 @@ struct DefaultContext {
     FamilyParams installed_params{};
     bool has_family = false;
 
+    // Images the free match functions have uploaded, kept resident by CONTENT: a caller that walks a pair list with
+    // match_pair (the reference's worker loop, engine.cpp:686-696) hands over every image K - 1 times; the second time
+    // its descriptors, keypoints and codes are already on the device with their bucket index built.  Keyed by a 64-bit
+    // hash of all the bytes handed over (plus point count and family parameters), least recently used out first.
+    struct CachedImage {
+        std::uint64_t key;
+        std::uint32_t id, points;
+        std::uint64_t stamp;
+    };
+    static constexpr std::size_t kCachedImages = 64;
+    std::vector<CachedImage> cache;
+    std::uint64_t cache_clock = 0, cache_hits = 0, cache_misses = 0;
+    std::uint32_t cache_next = 0;
+
+    static std::uint64_t hash_bytes(std::uint64_t h, const void* p, std::size_t bytes) {
+        const unsigned char* b = static_cast<const unsigned char*>(p);
+        std::uint64_t h2 = h ^ 0x9e3779b97f4a7c15ull;
+        std::size_t i = 0;
+        for (; i + 16 <= bytes; i += 16) {  // two independent lanes
+            std::uint64_t w0, w1;
+            std::memcpy(&w0, b + i, 8);
+            std::memcpy(&w1, b + i + 8, 8);
+            h = (h ^ w0) * 0xff51afd7ed558ccdull;
+            h ^= h >> 32;
+            h2 = (h2 ^ w1) * 0xc4ceb9fe1a85ec53ull;
+            h2 ^= h2 >> 29;
+        }
+        for (; i < bytes; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
+        h ^= h2 + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+        return (h ^ (h >> 31)) * 0xd6e8feb86659fd93ull;
+    }
+    void drop_cache() {
+        for (const CachedImage& c : cache) {
+            try {
+                matcher->evict(c.id);
+            } catch (...) {
+            }
+        }
+        cache.clear();
+    }
+    // Resident image id for (fs, codes): uploaded now or found from an earlier call.
+    std::uint32_t resident(Matcher& m, const FeatureSet& fs, const ImageCodes& codes) {
+        std::uint64_t key = 0x243f6a8885a308d3ull ^ fs.size();
+        const FamilyParams& p = codes.params;
+        const std::uint64_t pp[4] = {p.short_bits, p.long_bits, p.table_count, p.seed};
+        key = hash_bytes(key, pp, sizeof(pp));
+        if (!fs.empty()) {
+            key = hash_bytes(key, fs.descriptors.data(), fs.size() * kDescriptorDim);
+            key = hash_bytes(key, fs.keypoints.data(), fs.keypoints.size() * sizeof(Keypoint));
+            key = hash_bytes(key, codes.shorts.values.data(), codes.shorts.values.size() * sizeof(std::uint32_t));
+            for (const LongCode& c : codes.longs.codes) key = hash_bytes(key, c.words.data(), 16);  // (the struct has padding)
+        }
+        for (CachedImage& c : cache)
+            if (c.key == key && c.points == fs.size()) {
+                c.stamp = ++cache_clock;
+                ++cache_hits;
+                return c.id;
+            }
+        ++cache_misses;
+        if (cache.size() >= kCachedImages) {
+            std::size_t lru = 0;
+            for (std::size_t i = 1; i < cache.size(); ++i)
+                if (cache[i].stamp < cache[lru].stamp) lru = i;
+            m.evict(cache[lru].id);
+            cache.erase(cache.begin() + lru);
+        }
+        const std::uint32_t id = 0xE1000000u + (cache_next++ & 0x00FFFFFFu);
+        m.upload(id, fs);
+        try {
+            m.upload_codes(id, codes);
+        } catch (...) {
+            try {
+                m.evict(id);
+            } catch (...) {
+            }
+            throw;
+        }
+        cache.push_back(CachedImage{key, id, std::uint32_t(fs.size()), ++cache_clock});
+        return id;
+    }
+
     // Installs `family` (planes + centering) unless it is the one already resident.
     Matcher& with(const HashFamily& family) {
         if (!matcher) matcher = std::make_unique<Matcher>(0);
         if (!has_family || installed != &family || !(installed_params == family.params)) {
+            drop_cache();  // image blocks are laid out per family
             matcher->set_family(family);
             installed = &family;
             installed_params = family.params;
@@ -1107,13 +1190,7 @@ inline std::vector<MatchRecord> match_pair(const FeatureSet& fs_i, const Feature
     detail::DefaultContext& dc = detail::default_context();
     std::lock_guard<std::mutex> lock(dc.mu);
     Matcher& m = dc.with(*fam);
-    m.upload(detail::kScratchA, fs_i);
-    detail::ScopedImage ga{m, detail::kScratchA};
-    m.upload(detail::kScratchB, fs_j);
-    detail::ScopedImage gb{m, detail::kScratchB};
-    m.upload_codes(detail::kScratchA, codes_i);
-    m.upload_codes(detail::kScratchB, codes_j);
-    const std::pair<std::uint32_t, std::uint32_t> pr{detail::kScratchA, detail::kScratchB};
+    const std::pair<std::uint32_t, std::uint32_t> pr{dc.resident(m, fs_i, codes_i), dc.resident(m, fs_j, codes_j)};
     std::vector<PairMatches> out = m.match_pairs({&pr, 1}, cfg);
     return std::move(out.front().matches);
 }
@@ -1145,13 +1222,8 @@ inline std::vector<MatchRecord> match_pair_filtered(const FeatureSet& fs_i, cons
     detail::DefaultContext& dc = detail::default_context();
     std::lock_guard<std::mutex> lock(dc.mu);
     Matcher& m = dc.with(*fam);
-    m.upload(detail::kScratchA, fs_i);
-    detail::ScopedImage ga{m, detail::kScratchA};
-    m.upload(detail::kScratchB, fs_j);
-    detail::ScopedImage gb{m, detail::kScratchB};
-    m.upload_codes(detail::kScratchA, codes_i);
-    m.upload_codes(detail::kScratchB, codes_j);
-    return m.match_pair_filtered(detail::kScratchA, detail::kScratchB, cfg, filter);
+    const std::uint32_t a = dc.resident(m, fs_i, codes_i), b = dc.resident(m, fs_j, codes_j);
+    return m.match_pair_filtered(a, b, cfg, filter);
 }
 
 // guided_match_pair (geometry.hpp:86-89): match_pair with the epipolar band between lookup and ranking.
@@ -1181,13 +1253,7 @@ inline std::vector<MatchRecord> guided_match_pair(const FeatureSet& fs_i, const 
     detail::DefaultContext& dc = detail::default_context();
     std::lock_guard<std::mutex> lock(dc.mu);
     Matcher& m = dc.with(*fam);
-    m.upload(detail::kScratchA, fs_i);
-    detail::ScopedImage ga{m, detail::kScratchA};
-    m.upload(detail::kScratchB, fs_j);
-    detail::ScopedImage gb{m, detail::kScratchB};
-    m.upload_codes(detail::kScratchA, codes_i);
-    m.upload_codes(detail::kScratchB, codes_j);
-    const std::pair<std::uint32_t, std::uint32_t> pr{detail::kScratchA, detail::kScratchB};
+    const std::pair<std::uint32_t, std::uint32_t> pr{dc.resident(m, fs_i, codes_i), dc.resident(m, fs_j, codes_j)};
     std::vector<PairMatches> out = m.match_pairs_guided({&pr, 1}, {&f, 1}, band_px, cfg);
     return std::move(out.front().matches);
 }

@@ -358,6 +358,33 @@ static void device_checks(const std::filesystem::path& tmp) {
         CHECK(ch::match_pair(none, sets[1], cnone, codes[1], {}).empty());
         CHECK(ch::match_pair(sets[1], none, codes[1], cnone, {}).empty());
     }
+    // The free functions keep what they upload resident by content (DefaultContext::resident): walking a pair list with
+    // match_pair the way the reference's workers do (engine.cpp:686-696) uploads every image once; a changed descriptor
+    // under the same address is a different image.
+    {
+        auto& dc = ch::detail::default_context();
+        const std::uint64_t hits0 = dc.cache_hits, miss0 = dc.cache_misses;
+        for (int round = 0; round < 2; ++round)
+            for (int a = 0; a < 4; ++a)
+                for (int b = a + 1; b < 4; ++b)
+                    CHECK(ch::match_pair(sets[a], sets[b], codes[a], codes[b], {}) == oracle_match(fam, {}, sets[a], ocodes[a], sets[b], ocodes[b]));
+        CHECK(dc.cache_misses - miss0 <= 4);  // (the images of the calls above may be resident already)
+        CHECK(dc.cache_hits - hits0 >= 20);
+        ch::FeatureSet changed = sets[0];
+        changed.descriptors[5][7] ^= 0x55;
+        const std::uint64_t miss1 = dc.cache_misses;
+        const auto got = ch::match_pair(changed, sets[1], codes[0], codes[1], {});
+        CHECK(dc.cache_misses == miss1 + 1);
+        CHECK(got == oracle_match(fam, {}, changed, ocodes[0], sets[1], ocodes[1]));
+        // more images than the cache holds: the least recently used go, results stay right
+        std::vector<ch::FeatureSet> many;
+        for (int i = 0; i < 70; ++i) many.push_back(make_image(500 + i, 64, 20, "m" + std::to_string(i)));
+        for (int i = 0; i < 70; ++i) {
+            const ch::ImageCodes ci = ch::compute_codes(fam, many[i]);
+            CHECK(ch::match_pair(many[i], sets[1], ci, codes[1], {}) == oracle_match(fam, {}, many[i], oracle_codes(fam, many[i]), sets[1], ocodes[1]));
+        }
+        CHECK(dc.cache.size() <= ch::detail::DefaultContext::kCachedImages);
+    }
     // argument errors (matcher.cpp:144-148, :9-17)
     {
         ch::ImageCodes other = codes[1];
