@@ -10,7 +10,9 @@
  * Conventions
  *   - plain pointers and sizes only; all pointers are HOST pointers unless stated otherwise;
  *   - every call returns a chgpu_status; chgpu_last_error(ctx) gives the message;
- *   - one context per GPU; a context is thread-compatible (serialise calls on one context);
+ *   - one context per GPU; every call that takes a context holds the context's mutex for its duration, so calls
+ *     from several threads on one context are safe and serialised (a sink callback runs under it and may call
+ *     back into the same context from the same thread);
  *   - there is NO CPU fallback: without a CUDA device chgpu_create fails with CHGPU_ECUDA.
  *
  * Supported parameter envelope on the device path (CHGPU_EUNSUPPORTED outside it):

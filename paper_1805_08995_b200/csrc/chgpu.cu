@@ -175,6 +175,7 @@ struct chgpu_ctx {
     int stage_next = 0;
 
     // family
+    std::recursive_mutex mu;  // held by every entry point (CtxLock)
     bool has_family = false, has_centering = false;
     bool sparse = false;  // short_bits > kMaxShortBits: images carry sorted (code, point) keys, matched by the general path
     unsigned long long* d_list_offs = nullptr;  // explicit candidate lists of one pair (chgpu_match_pair_lists)
@@ -267,6 +268,20 @@ chgpu_status fail(chgpu_ctx* ctx, chgpu_status s, const char* fmt, ...) {
 
 struct DeviceGuard {
     explicit DeviceGuard(int dev) { cudaSetDevice(dev); }
+};
+
+// Every entry point that takes a context holds the context's mutex for its duration: calls from several threads on one
+// context are serialised (a sink callback runs under it too; it may call back into the same context from the same thread).
+struct CtxLock {
+    explicit CtxLock(chgpu_ctx* ctx) : mu(ctx ? &ctx->mu : nullptr) {
+        if (mu) mu->lock();
+    }
+    ~CtxLock() {
+        if (mu) mu->unlock();
+    }
+    CtxLock(const CtxLock&) = delete;
+    CtxLock& operator=(const CtxLock&) = delete;
+    std::recursive_mutex* mu;
 };
 
 size_t smem_train_capacity(const chgpu_ctx* ctx, bool guided = false);
@@ -1477,6 +1492,7 @@ void chgpu_destroy(chgpu_ctx* ctx) {
 const char* chgpu_last_error(const chgpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 chgpu_status chgpu_get_device_props(chgpu_ctx* ctx, chgpu_device_props* out) {
+    CtxLock lock_(ctx);
     if (!ctx || !out) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     memset(out, 0, sizeof(*out));
@@ -1490,6 +1506,7 @@ chgpu_status chgpu_get_device_props(chgpu_ctx* ctx, chgpu_device_props* out) {
 }
 
 chgpu_status chgpu_sync(chgpu_ctx* ctx) {
+    CtxLock lock_(ctx);
     if (!ctx) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     CK(cudaStreamSynchronize(ctx->copy));
@@ -1498,6 +1515,7 @@ chgpu_status chgpu_sync(chgpu_ctx* ctx) {
 }
 
 chgpu_status chgpu_image_device_bytes(chgpu_ctx* ctx, uint32_t n, uint64_t* bytes) {
+    CtxLock lock_(ctx);
     if (!ctx || !bytes) return CHGPU_EINVAL;
     if (!ctx->has_family) return fail(ctx, CHGPU_ELOGIC, "chgpu_set_family must precede chgpu_image_device_bytes (the layout depends on m, L)");
     if (n > kMaxPoints) return fail(ctx, CHGPU_EUNSUPPORTED, "%u points; device path holds <= %u", n, kMaxPoints);
@@ -1508,6 +1526,7 @@ chgpu_status chgpu_image_device_bytes(chgpu_ctx* ctx, uint32_t n, uint64_t* byte
 }
 
 chgpu_status chgpu_set_join(chgpu_ctx* ctx, int enabled, uint32_t min_points_per_bucket) {
+    CtxLock lock_(ctx);
     if (!ctx) return CHGPU_EINVAL;
     ctx->join_enabled = enabled != 0;
     ctx->join_min_bucket = min_points_per_bucket;
@@ -1515,12 +1534,14 @@ chgpu_status chgpu_set_join(chgpu_ctx* ctx, int enabled, uint32_t min_points_per
 }
 
 chgpu_status chgpu_set_sub_batch_queries(chgpu_ctx* ctx, uint64_t max_queries) {
+    CtxLock lock_(ctx);
     if (!ctx) return CHGPU_EINVAL;
     ctx->sub_batch_queries = max_queries ? max_queries : kSubBatchQueries;
     return CHGPU_OK;
 }
 
 chgpu_status chgpu_host_alloc(chgpu_ctx* ctx, size_t bytes, void** out) {
+    CtxLock lock_(ctx);
     if (!ctx || !out) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     CK(cudaMallocHost(out, std::max<size_t>(bytes, 1)));
@@ -1528,6 +1549,7 @@ chgpu_status chgpu_host_alloc(chgpu_ctx* ctx, size_t bytes, void** out) {
 }
 
 chgpu_status chgpu_host_free(chgpu_ctx* ctx, void* p) {
+    CtxLock lock_(ctx);
     if (!ctx) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     CK(cudaFreeHost(p));
@@ -1537,6 +1559,7 @@ chgpu_status chgpu_host_free(chgpu_ctx* ctx, void* p) {
 // ---- family -------------------------------------------------------------------------------------
 chgpu_status chgpu_set_family(chgpu_ctx* ctx, const chgpu_family_params* p, const double* short_planes,
                               const double* long_planes) {
+    CtxLock lock_(ctx);
     if (!ctx || !p || !short_planes || !long_planes) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     if (chgpu_host_check_family(p) != 0)
@@ -1561,12 +1584,14 @@ chgpu_status chgpu_set_family(chgpu_ctx* ctx, const chgpu_family_params* p, cons
 }
 
 chgpu_status chgpu_set_hash_mode(chgpu_ctx* ctx, chgpu_hash_mode mode) {
+    CtxLock lock_(ctx);
     if (!ctx || (mode != CHGPU_HASH_FILTERED && mode != CHGPU_HASH_EXACT && mode != CHGPU_HASH_TENSOR)) return CHGPU_EINVAL;
     ctx->hash_mode = mode;
     return CHGPU_OK;
 }
 
 chgpu_status chgpu_get_hash_stats(chgpu_ctx* ctx, chgpu_hash_stats* out) {
+    CtxLock lock_(ctx);
     if (!ctx || !out) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     HashFilterStats hs;
@@ -1580,6 +1605,7 @@ chgpu_status chgpu_get_hash_stats(chgpu_ctx* ctx, chgpu_hash_stats* out) {
 }
 
 chgpu_status chgpu_centering_reset(chgpu_ctx* ctx) {
+    CtxLock lock_(ctx);
     if (!ctx) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     CK(cudaMemsetAsync(ctx->d_sums, 0, 128 * sizeof(unsigned long long), ctx->compute));
@@ -1589,6 +1615,7 @@ chgpu_status chgpu_centering_reset(chgpu_ctx* ctx) {
 }
 
 chgpu_status chgpu_centering_add_image(chgpu_ctx* ctx, uint32_t image_id) {
+    CtxLock lock_(ctx);
     if (!ctx) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     uint32_t slot = 0;
@@ -1604,6 +1631,7 @@ chgpu_status chgpu_centering_add_image(chgpu_ctx* ctx, uint32_t image_id) {
 }
 
 chgpu_status chgpu_centering_add_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32_t count) {
+    CtxLock lock_(ctx);
     if (!ctx || (count && !image_ids)) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     if (count == 0) return CHGPU_OK;
@@ -1631,6 +1659,7 @@ chgpu_status chgpu_centering_add_images(chgpu_ctx* ctx, const uint32_t* image_id
 }
 
 chgpu_status chgpu_centering_get_sums(chgpu_ctx* ctx, uint64_t* sums128, uint64_t* count) {
+    CtxLock lock_(ctx);
     if (!ctx || !sums128 || !count) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     unsigned long long tmp[128];
@@ -1642,6 +1671,7 @@ chgpu_status chgpu_centering_get_sums(chgpu_ctx* ctx, uint64_t* sums128, uint64_
 }
 
 chgpu_status chgpu_centering_add_sums(chgpu_ctx* ctx, const uint64_t* sums128, uint64_t count) {
+    CtxLock lock_(ctx);
     if (!ctx || !sums128) return CHGPU_EINVAL;
     for (int i = 0; i < 128; ++i) ctx->extra_sums[i] += sums128[i];
     ctx->sum_count += count;
@@ -1649,6 +1679,7 @@ chgpu_status chgpu_centering_add_sums(chgpu_ctx* ctx, const uint64_t* sums128, u
 }
 
 chgpu_status chgpu_set_centering(chgpu_ctx* ctx, const double* centering128) {
+    CtxLock lock_(ctx);
     if (!ctx || !centering128) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     CK(cudaStreamSynchronize(ctx->compute));
@@ -1663,6 +1694,7 @@ chgpu_status chgpu_set_centering(chgpu_ctx* ctx, const double* centering128) {
 }
 
 chgpu_status chgpu_centering_apply(chgpu_ctx* ctx, double* centering128_out) {
+    CtxLock lock_(ctx);
     if (!ctx) return CHGPU_EINVAL;
     uint64_t sums[128], count = 0;
     if (const chgpu_status s = chgpu_centering_get_sums(ctx, sums, &count)) return s;
@@ -1676,6 +1708,7 @@ chgpu_status chgpu_centering_apply(chgpu_ctx* ctx, double* centering128_out) {
 // ---- descriptor load ----------------------------------------------------------------------------
 chgpu_status chgpu_upload_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, const uint8_t* desc,
                                 const float* keypoints) {
+    CtxLock lock_(ctx);
     if (!ctx || (n && !desc)) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     uint32_t slot = 0;
@@ -1693,6 +1726,7 @@ chgpu_status chgpu_upload_image(chgpu_ctx* ctx, uint32_t image_id, uint32_t n, c
 
 chgpu_status chgpu_upload_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32_t count, uint32_t n,
                                  const uint8_t* desc, const float* keypoints) {
+    CtxLock lock_(ctx);
     if (!ctx || (count && !image_ids) || (count && n && !desc)) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     if (count == 0) return CHGPU_OK;
@@ -1728,6 +1762,7 @@ chgpu_status chgpu_upload_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint
 
 chgpu_status chgpu_upload_chft(chgpu_ctx* ctx, uint32_t image_id, const void* blob, size_t nbytes,
                                uint32_t* count_out, chgpu_file_fault* fault, uint64_t* fault_offset) {
+    CtxLock lock_(ctx);
     if (!ctx || !blob) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     auto bad = [&](chgpu_file_fault f, uint64_t off, const char* what) {
@@ -2283,6 +2318,7 @@ chgpu_status load_finish(chgpu_load_job* job, chgpu_file_result* results, chgpu_
 chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, const uint32_t* image_ids, uint32_t count,
                                    uint32_t io_threads, int accumulate_centering, chgpu_file_result* results,
                                    chgpu_load_stats* stats) {
+    CtxLock lock_(ctx);
     if (!ctx || (count && (!paths || !image_ids || !results))) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     if (!ctx->has_family)
@@ -2299,6 +2335,7 @@ chgpu_status chgpu_load_chft_files(chgpu_ctx* ctx, const char* const* paths, con
 
 chgpu_status chgpu_load_chft_files_begin(chgpu_ctx* ctx, const char* const* paths, const uint32_t* image_ids, uint32_t count,
                                          uint32_t io_threads, int accumulate_centering) {
+    CtxLock lock_(ctx);
     if (!ctx || (count && (!paths || !image_ids))) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     if (!ctx->has_family)
@@ -2320,6 +2357,7 @@ chgpu_status chgpu_load_chft_files_begin(chgpu_ctx* ctx, const char* const* path
 }
 
 chgpu_status chgpu_load_chft_files_end(chgpu_ctx* ctx, chgpu_file_result* results, chgpu_load_stats* stats) {
+    CtxLock lock_(ctx);
     if (!ctx) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     if (!ctx->load_job) {
@@ -2332,6 +2370,7 @@ chgpu_status chgpu_load_chft_files_end(chgpu_ctx* ctx, chgpu_file_result* result
 }
 
 chgpu_status chgpu_evict_image(chgpu_ctx* ctx, uint32_t image_id) {
+    CtxLock lock_(ctx);
     if (!ctx) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     uint32_t slot = 0;
@@ -2345,6 +2384,7 @@ chgpu_status chgpu_evict_image(chgpu_ctx* ctx, uint32_t image_id) {
 }
 
 chgpu_status chgpu_evict_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32_t count) {
+    CtxLock lock_(ctx);
     if (!ctx || (count && !image_ids)) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     if (count == 0) return CHGPU_OK;
@@ -2366,6 +2406,7 @@ chgpu_status chgpu_evict_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint3
 }
 
 chgpu_status chgpu_image_points(chgpu_ctx* ctx, uint32_t image_id, uint32_t* n) {
+    CtxLock lock_(ctx);
     if (!ctx || !n) return CHGPU_EINVAL;
     uint32_t slot = 0;
     if (const chgpu_status s = find_slot(ctx, image_id, &slot)) return s;
@@ -2374,6 +2415,7 @@ chgpu_status chgpu_image_points(chgpu_ctx* ctx, uint32_t image_id, uint32_t* n) 
 }
 
 chgpu_status chgpu_download_descriptors(chgpu_ctx* ctx, uint32_t image_id, uint8_t* desc, float* keypoints) {
+    CtxLock lock_(ctx);
     if (!ctx) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     uint32_t slot = 0;
@@ -2387,6 +2429,7 @@ chgpu_status chgpu_download_descriptors(chgpu_ctx* ctx, uint32_t image_id, uint8
 
 // ---- hash build ---------------------------------------------------------------------------------
 chgpu_status chgpu_hash_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32_t count, int reduce_rounds) {
+    CtxLock lock_(ctx);
     if (!ctx || (count && !image_ids)) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     if (reduce_rounds < 0 || reduce_rounds > 7)
@@ -2441,6 +2484,7 @@ chgpu_status chgpu_hash_images(chgpu_ctx* ctx, const uint32_t* image_ids, uint32
 }
 
 chgpu_status chgpu_download_codes(chgpu_ctx* ctx, uint32_t image_id, uint32_t* shorts, uint64_t* longs) {
+    CtxLock lock_(ctx);
     if (!ctx) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     uint32_t slot = 0;
@@ -2455,6 +2499,7 @@ chgpu_status chgpu_download_codes(chgpu_ctx* ctx, uint32_t image_id, uint32_t* s
 }
 
 chgpu_status chgpu_upload_codes(chgpu_ctx* ctx, uint32_t image_id, const uint32_t* shorts, const uint64_t* longs) {
+    CtxLock lock_(ctx);
     if (!ctx || !shorts || !longs) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     uint32_t slot = 0;
@@ -2482,6 +2527,7 @@ chgpu_status chgpu_upload_codes(chgpu_ctx* ctx, uint32_t image_id, const uint32_
 }
 
 chgpu_status chgpu_download_bucket_index(chgpu_ctx* ctx, uint32_t image_id, uint32_t* offsets, uint32_t* points) {
+    CtxLock lock_(ctx);
     if (!ctx) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     uint32_t slot = 0;
@@ -2505,6 +2551,7 @@ chgpu_status chgpu_download_bucket_index(chgpu_ctx* ctx, uint32_t image_id, uint
 
 // ---- code caches ----------------------------------------------------------------------------------
 chgpu_status chgpu_image_save_code_cache(chgpu_ctx* ctx, uint32_t image_id, const char* path) {
+    CtxLock lock_(ctx);
     if (!ctx || !path) return CHGPU_EINVAL;
     if (!ctx->has_centering) return fail(ctx, CHGPU_ELOGIC, "code cache: centering has not been set");
     uint32_t slot = 0;
@@ -2521,6 +2568,7 @@ chgpu_status chgpu_image_save_code_cache(chgpu_ctx* ctx, uint32_t image_id, cons
 
 chgpu_status chgpu_image_load_code_cache(chgpu_ctx* ctx, uint32_t image_id, const char* path, chgpu_file_fault* fault,
                                          uint64_t* fault_offset) {
+    CtxLock lock_(ctx);
     if (!ctx || !path) return CHGPU_EINVAL;
     if (!ctx->has_centering) return fail(ctx, CHGPU_ELOGIC, "code cache: centering has not been set");
     uint32_t slot = 0;
@@ -2544,6 +2592,7 @@ chgpu_status chgpu_image_load_code_cache(chgpu_ctx* ctx, uint32_t image_id, cons
 chgpu_status chgpu_match_pairs(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs, const chgpu_match_cfg* cfg,
                                uint64_t* offsets, chgpu_match_record* records, uint64_t capacity, uint64_t* total,
                                chgpu_match_stats* stats) {
+    CtxLock lock_(ctx);
     if (!ctx || !cfg || !offsets || (npairs && !pairs) || (capacity && !records)) return CHGPU_EINVAL;
     MatchRun run{pairs, npairs, *cfg, SinkMode::Host};
     run.offsets = offsets;
@@ -2561,6 +2610,7 @@ chgpu_status chgpu_match_pairs(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t n
 chgpu_status chgpu_match_pairs_stream(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
                                       const chgpu_match_cfg* cfg, chgpu_sink_fn sink, void* user,
                                       chgpu_match_stats* stats) {
+    CtxLock lock_(ctx);
     if (!ctx || !cfg || (npairs && !pairs)) return CHGPU_EINVAL;
     MatchRun run{pairs, npairs, *cfg, SinkMode::Stream};
     run.sink = sink;
@@ -2571,6 +2621,7 @@ chgpu_status chgpu_match_pairs_stream(chgpu_ctx* ctx, const uint32_t* pairs, uin
 chgpu_status chgpu_match_pairs_guided(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs, const chgpu_match_cfg* cfg,
                                       const double* fmats, double band_px, uint64_t* offsets, chgpu_match_record* records,
                                       uint64_t capacity, uint64_t* total, chgpu_match_stats* stats) {
+    CtxLock lock_(ctx);
     if (!ctx || !cfg || !offsets || (npairs && (!pairs || !fmats)) || (capacity && !records)) return CHGPU_EINVAL;
     if (!(band_px >= 0.0)) return fail(ctx, CHGPU_EINVAL, "band_px must be >= 0");
     MatchRun run{pairs, npairs, *cfg, SinkMode::Host};
@@ -2591,6 +2642,7 @@ chgpu_status chgpu_match_pairs_guided(chgpu_ctx* ctx, const uint32_t* pairs, uin
 chgpu_status chgpu_match_pairs_guided_stream(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
                                              const chgpu_match_cfg* cfg, const double* fmats, double band_px,
                                              chgpu_sink_fn sink, void* user, chgpu_match_stats* stats) {
+    CtxLock lock_(ctx);
     if (!ctx || !cfg || (npairs && (!pairs || !fmats))) return CHGPU_EINVAL;
     if (!(band_px >= 0.0)) return fail(ctx, CHGPU_EINVAL, "band_px must be >= 0");
     MatchRun run{pairs, npairs, *cfg, SinkMode::Stream};
@@ -2603,6 +2655,7 @@ chgpu_status chgpu_match_pairs_guided_stream(chgpu_ctx* ctx, const uint32_t* pai
 
 chgpu_status chgpu_match_pairs_to_files(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs, const chgpu_match_cfg* cfg,
                                         chgpu_sink* sink, chgpu_match_stats* stats) {
+    CtxLock lock_(ctx);
     if (!ctx || !cfg || !sink || (npairs && !pairs)) return CHGPU_EINVAL;
     struct Feed {
         chgpu_sink* sink;
@@ -2620,6 +2673,7 @@ chgpu_status chgpu_match_pairs_to_files(chgpu_ctx* ctx, const uint32_t* pairs, u
 
 chgpu_status chgpu_match_pairs_device(chgpu_ctx* ctx, const uint32_t* pairs, uint32_t npairs,
                                       const chgpu_match_cfg* cfg, chgpu_match_stats* stats) {
+    CtxLock lock_(ctx);
     if (!ctx || !cfg || (npairs && !pairs)) return CHGPU_EINVAL;
     MatchRun run{pairs, npairs, *cfg, SinkMode::Device};
     return run_match(ctx, run, stats);
@@ -2627,6 +2681,7 @@ chgpu_status chgpu_match_pairs_device(chgpu_ctx* ctx, const uint32_t* pairs, uin
 
 chgpu_status chgpu_debug_ranked_guided(chgpu_ctx* ctx, uint32_t image_i, uint32_t image_j, const chgpu_match_cfg* cfg,
                                        const double* fmat, double band_px, uint32_t* ranked, uint32_t* ranked_count) {
+    CtxLock lock_(ctx);
     if (!ctx || !cfg || !ranked || !ranked_count || !fmat) return CHGPU_EINVAL;
     const uint32_t pr[2] = {image_i, image_j};
     MatchRun run{pr, 1, *cfg, SinkMode::Device};
@@ -2639,6 +2694,7 @@ chgpu_status chgpu_debug_ranked_guided(chgpu_ctx* ctx, uint32_t image_i, uint32_
 
 chgpu_status chgpu_debug_ranked(chgpu_ctx* ctx, uint32_t image_i, uint32_t image_j, const chgpu_match_cfg* cfg,
                                 uint32_t* ranked, uint32_t* ranked_count) {
+    CtxLock lock_(ctx);
     if (!ctx || !cfg || !ranked || !ranked_count) return CHGPU_EINVAL;
     const uint32_t pr[2] = {image_i, image_j};
     MatchRun run{pr, 1, *cfg, SinkMode::Device};
@@ -2649,6 +2705,7 @@ chgpu_status chgpu_debug_ranked(chgpu_ctx* ctx, uint32_t image_i, uint32_t image
 
 // ---- general path: sorted index, candidate lists, match from explicit lists (general_kernels.cuh) ---------------------
 chgpu_status chgpu_download_sorted_index(chgpu_ctx* ctx, uint32_t image_id, uint32_t* codes, uint32_t* points) {
+    CtxLock lock_(ctx);
     if (!ctx || !codes || !points) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     uint32_t slot = 0;
@@ -2683,6 +2740,7 @@ chgpu_status chgpu_download_sorted_index(chgpu_ctx* ctx, uint32_t image_id, uint
 
 chgpu_status chgpu_pair_candidates(chgpu_ctx* ctx, uint32_t image_i, uint32_t image_j, uint64_t* offsets, uint32_t* candidates,
                                    uint64_t capacity, uint64_t* total) {
+    CtxLock lock_(ctx);
     if (!ctx || !offsets || (capacity && !candidates)) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     if (!ctx->has_family) return fail(ctx, CHGPU_ELOGIC, "no hash family installed");
@@ -2746,6 +2804,7 @@ chgpu_status chgpu_pair_candidates(chgpu_ctx* ctx, uint32_t image_i, uint32_t im
 chgpu_status chgpu_match_pair_lists(chgpu_ctx* ctx, uint32_t image_i, uint32_t image_j, const chgpu_match_cfg* cfg,
                                     const uint64_t* list_offsets, const uint32_t* list_ids, chgpu_match_record* records,
                                     uint64_t capacity, uint64_t* total, chgpu_match_stats* stats) {
+    CtxLock lock_(ctx);
     if (!ctx || !cfg || !list_offsets || (capacity && !records)) return CHGPU_EINVAL;
     DeviceGuard guard(ctx->device);
     uint32_t si = 0, sj = 0;

@@ -750,3 +750,44 @@ def test_replaced_centering_invalidates_hashed_codes(matcher, oracle, default_fa
     matcher.hash(ids)
     offs_c, rec_c, _ = matcher.match_pairs([(BASE, BASE + 1)], cfg)
     assert np.array_equal(offs_c, offs_a) and np.array_equal(rec_c, rec_a)
+
+
+# ---- threads ------------------------------------------------------------------------------------------
+def test_calls_from_several_threads_on_one_context(matcher, default_family):
+    """Every entry point holds the context's mutex (chgpu.cu CtxLock): W host threads that share one context — the
+    reference's worker model, engine.cpp:686-696 — get serialised calls and the records of a single-threaded run."""
+    import threading
+
+    fresh(matcher, default_family)
+    ds = make_dataset(6, 900, seed=55)
+    for i, d in enumerate(ds):
+        put(matcher, BASE + i, d)
+    matcher.centering_reset()
+    for i in range(6):
+        matcher.centering_add(BASE + i)
+    matcher.centering_apply()
+    matcher.hash([BASE + i for i in range(6)])
+    pairs = [(BASE + a, BASE + b) for a in range(6) for b in range(a + 1, 6)]
+    cfg = ch.MatchConfig()
+    want = [matcher.match_pairs([p], cfg)[1] for p in pairs]
+    got = [None] * len(pairs)
+    errors = []
+
+    def worker(w):
+        try:
+            for rep in range(3):
+                for k in range(w, len(pairs), 4):
+                    got[k] = matcher.match_pairs([pairs[k]], cfg)[1]
+                    matcher.codes(pairs[k][0])           # other entry points in between
+                    matcher.ranked(pairs[k][0], pairs[k][1], cfg)
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(w,)) for w in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for k in range(len(pairs)):
+        assert np.array_equal(got[k], want[k]), k
