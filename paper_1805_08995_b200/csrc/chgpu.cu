@@ -1148,6 +1148,7 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
             CK(cudaFuncSetAttribute(general_match_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsmem)));
             const uint64_t want = (sb.queries + kGenWarps - 1) / kGenWarps;
             grid = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(ctx->prop.multiProcessorCount) * 24)));
+            G.slice = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(8, sb.queries / (uint64_t(grid) * kGenWarps * 4))));  // (longer runs unbalance the warps: matching queries cluster)
             CK(cudaEventRecord(b.ev_k0, ctx->compute));
             general_match_kernel<<<grid, kGenThreads, gsmem, ctx->compute>>>(G);
             CK(cudaGetLastError());

@@ -36,6 +36,7 @@ struct GeneralParams {
     uint32_t npairs;
     unsigned long long queries;            // of the sub-batch (PairDesc::res_off indexes them)
     uint32_t sparse;                       // the images carry sorted (code, point) keys instead of dense offsets
+    uint32_t slice;                        // consecutive queries a warp takes per visit
     const unsigned long long* list_offs;   // explicit candidate lists of ONE pair: n_i + 1 offsets into list_ids, or nullptr
     const uint32_t* list_ids;
 };
@@ -67,8 +68,13 @@ __device__ __forceinline__ BucketRanges resolve_ranges(const DevImage& I, const 
                 else hi = mid;
             }
             a = lo;
-            hi = J.n;
-            while (lo < hi) {  // first entry > hi_key
+            // first entry > hi_key: runs are short (n / 2^m points on average), so gallop from the start of the run
+            // and bisect the last stride instead of bisecting the whole table again
+            uint32_t step = 1;
+            while (a + step <= J.n && __ldg(keys + a + step - 1) <= hi_key) step <<= 1;   // entry a + step - 1 is past the run
+            lo = a + (step >> 1);                       // entries below lo belong to the run (or lo == a: maybe empty)
+            hi = min(a + step - 1, J.n);                // entry hi is past the run (or the end of the table)
+            while (lo < hi) {
                 const uint32_t mid = (lo + hi) >> 1;
                 if (__ldg(keys + mid) <= hi_key) lo = mid + 1;
                 else hi = mid;
@@ -115,7 +121,7 @@ __device__ __forceinline__ uint32_t pair_of_query(const PairDesc* __restrict__ p
     return lo;
 }
 
-__global__ void __launch_bounds__(kGenThreads) general_match_kernel(const GeneralParams G) {
+__global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const GeneralParams G) {
     extern __shared__ __align__(16) uint32_t s_keys_all[];  // kGenWarps x kGenCacheKeys
     constexpr uint32_t FULL = 0xffffffffu;
     const MatchParams& P = G.base;
@@ -125,13 +131,25 @@ __global__ void __launch_bounds__(kGenThreads) general_match_kernel(const Genera
     const bool sparse = G.sparse != 0;
     const bool guided = P.fmats != nullptr;
 
-    for (unsigned long long g = (unsigned long long)blockIdx.x * kGenWarps + warp; g < G.queries;
-         g += (unsigned long long)gridDim.x * kGenWarps) {
-        const uint32_t pair = pair_of_query(P.pairs, G.npairs, g);
-        const PairDesc pd = P.pairs[pair];
+    // every warp takes a contiguous run of the sub-batch's queries in short slices: the pair (and its two image records)
+    // changes rarely along a run, so it is looked up once and then only advanced
+    const unsigned long long total_warps = (unsigned long long)gridDim.x * kGenWarps;
+    const unsigned long long my_warp = (unsigned long long)blockIdx.x * kGenWarps + warp;
+    const unsigned long long kSlice = G.slice;  // queries per visit (host: 1..8, shorter when the sub-batch is small)
+    uint32_t pair = kNone;
+    PairDesc pd{};
+    DevImage I{}, J{};
+    unsigned long long pair_end = 0;  // first query past the current pair
+    for (unsigned long long g0 = my_warp * kSlice; g0 < G.queries; g0 += total_warps * kSlice)
+    for (unsigned long long g = g0; g < min(g0 + kSlice, G.queries); ++g) {
+        if (pair == kNone || g >= pair_end || g < pd.res_off) {
+            pair = pair_of_query(P.pairs, G.npairs, g);
+            pd = P.pairs[pair];
+            I = P.images[pd.slot_i];
+            J = P.images[pd.slot_j];
+            pair_end = pd.res_off + I.n;
+        }
         const uint32_t q = uint32_t(g - pd.res_off);
-        const DevImage I = P.images[pd.slot_i];
-        const DevImage J = P.images[pd.slot_j];
         uint32_t out_t = kNone, out_d = 0, n = 0;
         if (J.n != 0) {
             const uint4 ql = __ldg(I.longs + q);
@@ -169,20 +187,38 @@ __global__ void __launch_bounds__(kGenThreads) general_match_kernel(const Genera
                 return __reduce_min_sync(FULL, best);
             };
             __syncwarp();  // the previous query's cache is no longer read
-            if (cached)
-                for (uint32_t i = lane; i < C; i += 32) s_keys[i] = key_at(i);
+            // keys of all candidates, four independent gather chains (id -> code) per lane in flight; the smallest on the way
+            uint32_t kmin = kNone;
+            for (uint32_t i0 = 0; i0 < C; i0 += 128u) {
+                uint32_t k4[4];
+#pragma unroll
+                for (uint32_t u = 0; u < 4; ++u) {
+                    const uint32_t i = i0 + 32u * u + lane;
+                    k4[u] = i < C ? key_at(i) : kNone;
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < 4; ++u) {
+                    const uint32_t i = i0 + 32u * u + lane;
+                    if (cached && i < C) s_keys[i] = k4[u];
+                    kmin = min(kmin, k4[u]);
+                }
+            }
             __syncwarp();
+            uint32_t nk = __reduce_min_sync(FULL, kmin);
 
-            // this lane's 4 bytes of the query row
-            const uint32_t qrow = __ldg(reinterpret_cast<const uint32_t*>(I.desc + uint64_t(q) * kDim) + lane);
             uint32_t best = kNone, second = kNone, best_id = kNone;
-            uint32_t nk = pull(0u, true);
             bool unthresholded = false;  // the re-rank of matcher.cpp:183-189 is under way
             if (nk != kNone && (nk >> 24) <= P.tau) {
+                // this lane's 4 bytes of the query row
+                const uint32_t qrow = __ldg(reinterpret_cast<const uint32_t*>(I.desc + uint64_t(q) * kDim) + lane);
                 for (;;) {
-                    // rank n: verified at once (euclidean_verify's loop body, matcher.cpp:124-133)
+                    // rank n: verified at once (euclidean_verify's loop body, matcher.cpp:124-133); the row travels while the
+                    // next key is pulled
                     const uint32_t id = explicit_lists ? __ldg(G.list_ids + list_lo + (nk & 0xffffffu)) : (nk & 0xffffffu);
                     const uint32_t trow = __ldg(reinterpret_cast<const uint32_t*>(J.desc + uint64_t(id) * kDim) + lane);
+                    if (P.dbg_ranked != nullptr && lane == 0) P.dbg_ranked[uint64_t(q) * P.top_k + n] = id;
+                    ++n;
+                    const uint32_t nxt = n == P.top_k ? kNone : pull(nk, false);
                     const uint32_t d = __reduce_add_sync(FULL, sqdiff4(qrow, trow));
                     if (d < best) {
                         second = best;
@@ -191,11 +227,8 @@ __global__ void __launch_bounds__(kGenThreads) general_match_kernel(const Genera
                     } else if (d < second) {
                         second = d;
                     }
-                    if (P.dbg_ranked != nullptr && lane == 0) P.dbg_ranked[uint64_t(q) * P.top_k + n] = id;
-                    ++n;
-                    if (n == P.top_k) break;
-                    nk = pull(nk, false);
-                    if (nk == kNone) break;
+                    if (nxt == kNone) break;  // the list is full, or no key is left
+                    nk = nxt;
                     if (!unthresholded && (nk >> 24) > P.tau) {
                         // the threshold cut something; a ranking too small for the ratio test is redone without it
                         if (n < P.min_ranked) unthresholded = true;
