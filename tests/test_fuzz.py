@@ -102,3 +102,69 @@ def test_random_case_matches_the_oracle(matcher, oracle, seed):
         assert np.array_equal(rc, gc[: len(rc)]), (seed, "guided counts")
         for q in np.nonzero(rc)[0]:
             assert np.array_equal(ranked[q, :rc[q]], gr[q, :rc[q]]), (seed, "guided ranked", q)
+
+
+def random_general_case(seed):
+    """Cases outside the tuned kernels' range (csrc/general_kernels.cuh): short codes of up to 32 bits and / or top_k > 32."""
+    rng = np.random.default_rng(70000 + seed)
+    wide_m = rng.random() < 0.7
+    m = int(rng.integers(13, 33)) if wide_m else int(rng.integers(1, 13))
+    n = int(rng.integers(m + 1, 129))
+    L = int(rng.integers(1, 9))
+    params = ch.FamilyParams(m, n, L, int(rng.integers(1, 1 << 30)))
+    top_k = int(rng.integers(33, 200)) if (not wide_m or rng.random() < 0.4) else int(rng.integers(2, 33))
+    cfg = ch.MatchConfig(top_k=top_k, hamming_threshold=int(rng.integers(0, n + 1)), ratio=float(rng.uniform(0.3, 0.99)),
+                         min_candidates_for_ratio=int(rng.integers(0, 12)), reduce_rounds=int(rng.integers(0, 8)))
+    sizes = [0, 1, 2, 33, 200, 777, 1500, 3000, 9000, 12000]
+    n_i, n_j = (int(x) for x in rng.choice(sizes, 2))
+    # low noise for long short codes: twins have to share a bucket for anything to be ranked at all
+    sigma = 8.0 if m <= 14 else (3.0 if m <= 22 else 1.0)
+    return params, cfg, n_i, n_j, sigma, rng
+
+
+@pytest.mark.parametrize("seed", list(range(int(os.environ.get("CHFUZZ_GENERAL_COUNT", "24")))))
+def test_random_general_case_matches_the_oracle(matcher, oracle, seed):
+    params, cfg, n_i, n_j, sigma, rng = random_general_case(seed)
+    fam = ch.build_hash_family(params)
+    fresh(matcher, fam)
+    d = make_dataset(2, max(n_i, n_j, 1), seed=5000 + seed, sigma=sigma)
+    desc = [d[0][:n_i].copy(), d[1][:n_j].copy()]
+    if n_i and n_j:  # exact and near duplicates across the pair and inside the train image: rankings of several candidates
+        k = min(n_i, n_j // 2, 40)
+        desc[1][:k] = desc[0][:k]
+        desc[1][-k:] = np.clip(desc[0][:k].astype(np.int16) + rng.integers(-1, 2, size=(k, 128)), 0, 255).astype(np.uint8) if k else desc[1][-k:]
+    kp = [np.column_stack([np.floor(rng.uniform(0, 900, n)), rng.uniform(0, 700, n), np.full(n, 2.0), np.zeros(n)]).astype(np.float32)
+          for n in (n_i, n_j)]
+    cen = oracle.centering([x for x in desc if len(x)]) if n_i + n_j else np.zeros(128)
+    matcher.set_centering(cen)
+    for i in range(2):
+        put(matcher, BASE + i, desc[i], kp[i])
+    rr = cfg.reduce_rounds
+    matcher.hash([BASE, BASE + 1], rr)
+    codes = [oracle.compute_codes(params, fam.short_planes, fam.long_planes, cen, desc[i], rr) for i in range(2)]
+    for i in range(2):
+        c = matcher.codes(BASE + i)
+        assert np.array_equal(c.shorts, codes[i][0]) and np.array_equal(c.longs, codes[i][1]), (seed, "codes", i)
+    want, ws, wr, wc = oracle.match_pair(params, cfg, desc[0], *codes[0], desc[1], *codes[1], want_ranked=True)
+    offs, rec, st = matcher.match_pairs([(BASE, BASE + 1)], cfg)
+    assert np.array_equal(rec, want), (seed, params, cfg, n_i, n_j)
+    assert (st["raw_candidates"], st["verified_queries"], st["distances"]) == \
+        (ws["raw_candidates"], ws["verified_queries"], ws["distances"]), seed
+    if n_i:
+        ranked, rc = matcher.ranked(BASE, BASE + 1, cfg)
+        assert np.array_equal(rc, wc[: len(rc)]), seed
+        for q in np.nonzero(rc)[0]:
+            assert np.array_equal(ranked[q, :rc[q]], wr[q, :rc[q]]), (seed, q)
+    F = rng.normal(size=(3, 3))
+    F[:, 2] *= 300.0
+    band = float(rng.choice([5.0, 40.0, 300.0, 1e9]))
+    gw, gs = oracle.guided_match_pair(params, cfg, desc[0], kp[0], *codes[0], desc[1], kp[1], *codes[1], F, band)
+    _, grec, gst = matcher.match_pairs_guided([(BASE, BASE + 1)], F[None], band, cfg)
+    assert np.array_equal(grec, gw), (seed, "guided", params, cfg, n_i, n_j, band)
+    assert (gst["verified_queries"], gst["distances"]) == (gs["verified_queries"], gs["distances"]), (seed, "guided stats")
+    # the candidate lists behind match_pair_filtered (matcher.cpp:164-171), on a sample of the queries
+    if n_i and n_j:
+        lo, cands = matcher.pair_candidates(BASE, BASE + 1)
+        for q in rng.choice(n_i, size=min(n_i, 25), replace=False):
+            w = oracle.lookup_candidates(params.short_bits, params.table_count, codes[0][0][q], codes[1][0])
+            assert np.array_equal(cands[int(lo[q]): int(lo[q + 1])], w), (seed, "candidates", int(q))
