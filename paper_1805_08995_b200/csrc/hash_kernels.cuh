@@ -560,6 +560,11 @@ __global__ void bucket_build_kernel(const DevImage* __restrict__ images, const u
     // re-dealt by (rank inside the residue class, residue): the first min-count rounds hold all 8
     // residues.  Only the order inside a bucket changes, which no result depends on.  One bucket per lane.
     uint16_t* scan = img.scan + uint64_t(t) * n;
+    // The match kernel reads entry `first` of a query's bucket even when the bucket is empty (its key is discarded
+    // afterwards); for an empty bucket at the very end of the last table that is entry L n, one past the lists.  The arena
+    // hands out recycled blocks, so that slot must hold a valid point id and not whatever the block held before (an id
+    // beyond the shared-memory window would fault in the code gather).
+    if (t == L - 1 && lane == 0) img.scan[uint64_t(L) * n] = 0;
     for (uint32_t b = lane; b < nb; b += 32) {
         const uint32_t lo = offs[b], hi = offs[b + 1], s = hi - lo;
         if (s <= 8 || s >= 256) {  // one octet, or counts that do not fit the packed bytes: keep the order

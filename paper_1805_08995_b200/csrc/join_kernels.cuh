@@ -143,6 +143,7 @@ __device__ __forceinline__ void join_bucket(const uint4* __restrict__ qc, const 
     if (lane == 31) asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
     const uint32_t g = lane >> 2, tq = lane & 3;
     uint32_t r0 = 0;
+#ifndef CHGPU_JOIN_MAXMT2
     while (nq - r0 > 48) {
         join_pass<2>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, hit_key, g, tq);
         r0 += 32;
@@ -151,6 +152,16 @@ __device__ __forceinline__ void join_bucket(const uint4* __restrict__ qc, const 
     if (left > 32) join_pass<3>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, hit_key, g, tq);
     else if (left > 16) join_pass<2>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, hit_key, g, tq);
     else join_pass<1>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, hit_key, g, tq);
+#else
+    // A/B switch: at most two row tiles per pass (32 A-fragment registers instead of 48); buckets of 33-48 rows stream the
+    // train columns twice.  Measured slower at 3 and at 4 CTAs per SM.
+    while (nq - r0 > 32) {
+        join_pass<2>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, hit_key, g, tq);
+        r0 += 32;
+    }
+    if (nq - r0 > 16) join_pass<2>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, hit_key, g, tq);
+    else join_pass<1>(qc, qp, qi, r0, nq, tr, tp, nt, tau, hit, hit_key, g, tq);
+#endif
 }
 
 __global__ void __launch_bounds__(kJoinThreads, CHGPU_JOIN_OCC) join_hits_kernel(const JoinParams P) {

@@ -38,7 +38,11 @@ def random_case(seed):
 
 
 # CHFUZZ_FIRST / CHFUZZ_COUNT widen the run (e.g. CHFUZZ_COUNT=1000 for a soak)
-SEEDS = range(int(os.environ.get("CHFUZZ_FIRST", "0")), int(os.environ.get("CHFUZZ_FIRST", "0")) + int(os.environ.get("CHFUZZ_COUNT", "40")))
+SEEDS = list(range(int(os.environ.get("CHFUZZ_FIRST", "0")), int(os.environ.get("CHFUZZ_FIRST", "0")) + int(os.environ.get("CHFUZZ_COUNT", "40"))))
+if "CHFUZZ_FIRST" not in os.environ:
+    # regression (round 2, found by a 400-seed soak): 14,000 / 11,500-point images, then a 2 x 1-point pair in recycled arena
+    # blocks — the id the match kernel reads one past an empty last bucket was whatever the block held before
+    SEEDS += [1115, 1116, 1117]
 
 
 @pytest.fixture(autouse=True)
