@@ -33,6 +33,9 @@ def random_case(seed):
     sizes = [0, 1, 2, 31, 33, 200, 777, 1500, 3000, 4096, 9000, 11500, 14000]
     weights = np.array([1, 1, 1, 1, 1, 4, 4, 4, 4, 3, 2, 2, 2], dtype=float)
     n_i, n_j = (int(x) for x in rng.choice(sizes, 2, p=weights / weights.sum()))
+    if os.environ.get("CHFUZZ_SIZES"):  # e.g. CHFUZZ_SIZES=17000,33000,65536: a soak over images of three and more tiles
+        big = [int(x) for x in os.environ["CHFUZZ_SIZES"].split(",")]
+        n_i, n_j = (int(x) for x in rng.choice(big, 2))
     shape = "sift" if rng.random() < 0.4 else "uniform"
     return params, cfg, n_i, n_j, shape, rng
 
@@ -172,3 +175,41 @@ def test_random_general_case_matches_the_oracle(matcher, oracle, seed):
         for q in rng.choice(n_i, size=min(n_i, 25), replace=False):
             w = oracle.lookup_candidates(params.short_bits, params.table_count, codes[0][0][q], codes[1][0])
             assert np.array_equal(cands[int(lo[q]): int(lo[q + 1])], w), (seed, "candidates", int(q))
+
+
+@pytest.mark.parametrize("seed", list(range(int(os.environ.get("CHFUZZ_LISTS_COUNT", "6")))))
+def test_random_pair_list_matches_the_oracle(matcher, oracle, seed):
+    """Pair LISTS over images of mixed sizes (empty, tiny, one shared-memory tile, several tiles), repeated and self pairs,
+    cut into many sub-batches by a small query budget: tiled and untiled sub-batches alternate, the join pass comes and goes
+    with the images' sizes, results arrive in pair order — every pair's records equal the oracle's."""
+    rng = np.random.default_rng(90000 + seed)
+    params = ch.FamilyParams(int(rng.integers(4, 11)), int(rng.integers(64, 129)), int(rng.integers(2, 9)), int(rng.integers(1, 1 << 30)))
+    cfg = ch.MatchConfig(top_k=int(rng.integers(2, 33)), hamming_threshold=int(rng.integers(20, params.long_bits + 1)),
+                         ratio=float(rng.uniform(0.5, 0.95)), min_candidates_for_ratio=int(rng.integers(0, 6)))
+    fam = ch.build_hash_family(params)
+    fresh(matcher, fam)
+    sizes = [int(x) for x in rng.choice([0, 1, 40, 600, 2500, 5000, 9000, 12000, 15000], size=7)]
+    d = make_dataset(7, max(max(sizes), 1), seed=3000 + seed, shape="sift" if rng.random() < 0.4 else "uniform")
+    desc = [d[i][: sizes[i]] for i in range(7)]
+    cen = oracle.centering([x for x in desc if len(x)]) if sum(sizes) else np.zeros(128)
+    matcher.set_centering(cen)
+    for i in range(7):
+        put(matcher, BASE + i, desc[i])
+    matcher.hash([BASE + i for i in range(7)])
+    codes = [oracle.compute_codes(params, fam.short_planes, fam.long_planes, cen, desc[i]) for i in range(7)]
+    pairs = [(int(a), int(b)) for a, b in rng.integers(0, 7, size=(int(rng.integers(20, 45)), 2))]
+    matcher.set_sub_batch_queries(int(rng.choice([1, 3000, 20000, 100000])))
+    matcher.set_join(True, int(rng.choice([0, 20])))
+    try:
+        offs, rec, st = matcher.match_pairs([(BASE + a, BASE + b) for a, b in pairs], cfg)
+    finally:
+        matcher.set_sub_batch_queries(0)
+    cache = {}
+    matches = 0
+    for k, (a, b) in enumerate(pairs):
+        if (a, b) not in cache:
+            cache[(a, b)] = oracle.match_pair(params, cfg, desc[a], *codes[a], desc[b], *codes[b])[0]
+        want = cache[(a, b)]
+        matches += len(want)
+        assert np.array_equal(rec[int(offs[k]): int(offs[k + 1])], want), (seed, k, a, b, sizes[a], sizes[b])
+    assert st["matches"] == matches and int(offs[-1]) == matches
