@@ -6,6 +6,7 @@ restatement, against the reference itself where oracle/_ref exists, and SPEC.md 
 (every unordered pair exactly once; never more than 3 / 2 resident; no stall under unit cost).
 GPU part: chgpu_match_plan_streamed with a handful of slots returns exactly the records of the fully resident run.
 """
+import os
 import struct
 
 import numpy as np
@@ -501,3 +502,51 @@ def test_streamed_sharded_job_single_rank(matcher, restatement, tmp_path):
     stats, results = job.match(paths, 3, 2, ch.MatchConfig(), io_threads=2, sink=lambda t, p, o, r: seen.append(p))
     assert results == sizes and stats["pairs"] == 12 * 11 // 2
     assert sorted(map(tuple, np.concatenate(seen).tolist())) == sorted(map(tuple, api.plan_exhaustive(12, 3, 2).tolist()))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", list(range(int(os.environ.get("CHSTREAM_SOAK", "4")))))
+def test_streamed_run_random_partitions(matcher, tmp_path, seed):
+    """Random datasets (empty, tiny, tiled images), partitions, slot limits, task orders and hash families — short codes of
+    more than 12 bits and top_k > 32 (the general kernels) included: the out-of-core run delivers the records of the resident
+    run, pair for pair, and leaves nothing on the device."""
+    rng = np.random.default_rng(4200 + seed)
+    k = int(rng.integers(5, 19))
+    sizes = [int(x) for x in rng.choice([0, 1, 50, 400, 900, 1500, 2600, 12000], size=k, p=[.05, .05, .1, .2, .25, .2, .1, .05])]
+    desc, paths = write_dataset(tmp_path, sizes, seed=600 + seed)
+    np_, m_ = int(rng.integers(1, 5)), int(rng.integers(1, 4))
+    short_bits = int(rng.choice([4, 8, 10, 14, 20]))
+    fam = ch.build_hash_family(ch.FamilyParams(short_bits=short_bits, table_count=int(rng.integers(2, 9))))
+    fresh(matcher, fam)
+    cfg = ch.MatchConfig(top_k=int(rng.choice([2, 10, 32, 40])), hamming_threshold=int(rng.integers(30, 129)))
+    centering, results = matcher.centering_pass_files(paths, block_images=int(rng.integers(1, 6)), io_threads=int(rng.integers(1, 5)))
+    assert results == sizes
+    acc = None
+    if rng.random() < 0.4:
+        acc = rng.integers(0, k, (int(rng.integers(1, 60)), 2)).astype(np.uint32)
+        acc = acc[acc[:, 0] != acc[:, 1]]
+        if len(acc) == 0:
+            acc = None
+    flat = api.plan_exhaustive(k, np_, m_) if acc is None else api.plan_guided(k, np_, m_, acc)
+    slots = int(rng.choice([0, 3, 4, 6]))
+    order = int(rng.choice([api.ORDER_REFERENCE, api.ORDER_REUSE]))
+    got = {}
+
+    def sink(task, pairs, offs, rec):
+        o = offs.astype(np.int64)
+        for i, (a, b) in enumerate(pairs):
+            assert (int(a), int(b)) not in got
+            got[(int(a), int(b))] = rec[o[i]: o[i + 1]].copy()
+
+    stats, results = matcher.match_plan_streamed(paths, np_, m_, cfg, accepted_pairs=acc, group_slots=slots, block_slots=slots,
+                                                 io_threads=int(rng.integers(1, 5)), sink=sink, task_order=order)
+    assert stats["pairs"] == len(flat) == len(got)
+    touched = {int(x) for x in np.asarray(flat).reshape(-1)}
+    for i in range(k):  # (a guided plan never loads the blocks none of its pairs needs: those files report nothing)
+        assert results[i] == sizes[i] or (i not in touched and results[i] == 0), (seed, i, results[i], sizes[i])
+        with pytest.raises(KeyError):
+            matcher.points(i)
+    offs, rec = resident_reference(matcher, desc, flat, cfg, centering)
+    o = offs.astype(np.int64)
+    for i, (a, b) in enumerate(flat):
+        assert np.array_equal(got[(int(a), int(b))], rec[o[i]: o[i + 1]]), (seed, int(a), int(b))
