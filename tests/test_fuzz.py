@@ -53,7 +53,8 @@ def join_always(matcher):
     """The fuzz cases are small: the tensor-core Hamming pass is forced for every sub-batch it can serve (the library's own
     rule would skip them), so random families / thresholds / sizes go through it; ranked lists and guided runs still take the
     plain kernel."""
-    matcher.set_join(True, 0)
+    mode = os.environ.get("CHFUZZ_JOIN", "always")  # soaks: "size" = the library's own rule, "off" = never
+    matcher.set_join(mode != "off", 0 if mode == "always" else 20)
     yield
     matcher.set_join(True, 20)
 
