@@ -108,6 +108,8 @@ typedef struct chgpu_device_props {
 /* ---- context --------------------------------------------------------------------------- */
 chgpu_status chgpu_create(int device, chgpu_ctx** out);
 void chgpu_destroy(chgpu_ctx* ctx);
+/* Message of the calling thread's last failed call on this context (the pointer stays valid until that thread's next
+ * failing call or next chgpu_last_error). */
 const char* chgpu_last_error(const chgpu_ctx* ctx);
 const char* chgpu_status_name(chgpu_status s);
 chgpu_status chgpu_get_device_props(chgpu_ctx* ctx, chgpu_device_props* out);

@@ -246,6 +246,9 @@ struct chgpu_ctx {
 
 namespace {
 
+thread_local std::string tl_err;
+thread_local const chgpu_ctx* tl_err_ctx = nullptr;
+
 chgpu_status fail(chgpu_ctx* ctx, chgpu_status s, const char* fmt, ...) {
     if (ctx) {
         char buf[512];
@@ -254,6 +257,8 @@ chgpu_status fail(chgpu_ctx* ctx, chgpu_status s, const char* fmt, ...) {
         vsnprintf(buf, sizeof(buf), fmt, ap);
         va_end(ap);
         ctx->err = buf;
+        tl_err = buf;  // the calling thread's own copy: chgpu_last_error stays valid while other threads use the context
+        tl_err_ctx = ctx;
     }
     return s;
 }
@@ -1446,6 +1451,7 @@ chgpu_status chgpu_create(int device, chgpu_ctx** out) {
 }
 
 void chgpu_destroy(chgpu_ctx* ctx) {
+    if (tl_err_ctx == ctx) tl_err_ctx = nullptr;
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     chgpu_load_chft_files_end(ctx, nullptr, nullptr);  // a background load left open
@@ -1490,7 +1496,16 @@ void chgpu_destroy(chgpu_ctx* ctx) {
     delete ctx;
 }
 
-const char* chgpu_last_error(const chgpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+const char* chgpu_last_error(const chgpu_ctx* ctx) {
+    if (!ctx) return "null context";
+    // the message of this thread's own last failure on the context; a thread that has had none sees the context's latest
+    if (tl_err_ctx != ctx) {
+        CtxLock lock_(const_cast<chgpu_ctx*>(ctx));
+        tl_err = ctx->err;
+        tl_err_ctx = ctx;
+    }
+    return tl_err.c_str();
+}
 
 chgpu_status chgpu_get_device_props(chgpu_ctx* ctx, chgpu_device_props* out) {
     CtxLock lock_(ctx);
