@@ -126,7 +126,10 @@ __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const Gen
     constexpr uint32_t FULL = 0xffffffffu;
     const MatchParams& P = G.base;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t* s_keys = s_keys_all + warp * kGenCacheKeys;
+    // the warp's key cache by 32-bit shared-window address, pinned in a register (the compiler otherwise re-derives the
+    // window base in front of every access: 7 instructions per key read)
+    uint32_t s_keys = smem_addr(s_keys_all + warp * kGenCacheKeys);
+    asm volatile("" : "+r"(s_keys));
     const bool explicit_lists = G.list_offs != nullptr;
     const bool sparse = G.sparse != 0;
     const bool guided = P.fmats != nullptr;
@@ -136,6 +139,7 @@ __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const Gen
     const unsigned long long total_warps = (unsigned long long)gridDim.x * kGenWarps;
     const unsigned long long my_warp = (unsigned long long)blockIdx.x * kGenWarps + warp;
     const unsigned long long kSlice = G.slice;  // queries per visit (host: 1..8, shorter when the sub-batch is small)
+    unsigned long long st_raw = 0, st_vq = 0, st_dist = 0;  // statistics of this warp's queries (uniform over its lanes)
     uint32_t pair = kNone;
     PairDesc pd{};
     DevImage I{}, J{};
@@ -162,7 +166,7 @@ __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const Gen
             } else {
                 r = resolve_ranges(I, J, q, P.L, P.m, sparse, lane);
                 C = r.total;
-                if (lane == 0 && C) atomicAdd(&P.stats->raw_candidates, (unsigned long long)C);  // matcher.cpp:168
+                st_raw += C;  // matcher.cpp:168 (lane 0 adds the warp's total once, when its queries are done)
             }
             EpiLine line{};
             if (guided) line = epipolar_band(P.fmats + uint64_t(pd.pair_idx) * 9, __ldg(I.kp + q));
@@ -180,8 +184,18 @@ __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const Gen
             // smallest key above `prev` (first: smallest key at all), kNone when there is none
             auto pull = [&](uint32_t prev, bool first) -> uint32_t {
                 uint32_t best = kNone;
+                if (cached) {
+                    // keys <= prev wrap to the top of the u32 range (see next_key in match_kernels.cuh): one add-and-min per key
+                    const uint32_t nb = first ? 0u : ~prev;
+                    uint32_t acc = kNone;
+#pragma unroll 4
+                    for (uint32_t i = lane; i < C; i += 32) acc = min(acc, lds32(s_keys + i * 4u) + nb);
+                    const uint32_t g = __reduce_min_sync(FULL, acc);
+                    if (first) return g;
+                    return g >= nb - 1u ? kNone : g - nb;
+                }
                 for (uint32_t i = lane; i < C; i += 32) {
-                    const uint32_t k = cached ? s_keys[i] : key_at(i);
+                    const uint32_t k = key_at(i);
                     if ((first || k > prev) && k < best) best = k;
                 }
                 return __reduce_min_sync(FULL, best);
@@ -199,7 +213,7 @@ __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const Gen
 #pragma unroll
                 for (uint32_t u = 0; u < 4; ++u) {
                     const uint32_t i = i0 + 32u * u + lane;
-                    if (cached && i < C) s_keys[i] = k4[u];
+                    if (cached && i < C) sts32(s_keys + i * 4u, k4[u]);
                     kmin = min(kmin, k4[u]);
                 }
             }
@@ -237,10 +251,8 @@ __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const Gen
                 }
             }
             if (n >= 2) {
-                if (lane == 0) {
-                    atomicAdd(&P.stats->verified_queries, 1ull);
-                    atomicAdd(&P.stats->distances, (unsigned long long)n);
-                }
+                st_vq += 1;
+                st_dist += n;
                 if (second != 0u && double(best) < __dmul_rn(P.ratio_sq, double(second))) {
                     out_t = best_id;
                     out_d = best;
@@ -250,6 +262,12 @@ __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const Gen
         }
         if (P.dbg_count != nullptr && lane == 0) P.dbg_count[q] = n;
         if (lane == 0) __stcs(P.res + g, make_uint2(out_t, out_d));
+    }
+    // one atomic per warp and counter (an atomic per query on one address serialises the whole grid)
+    if (lane == 0) {
+        if (st_raw) atomicAdd(&P.stats->raw_candidates, st_raw);
+        if (st_vq) atomicAdd(&P.stats->verified_queries, st_vq);
+        if (st_dist) atomicAdd(&P.stats->distances, st_dist);
     }
 }
 
