@@ -139,12 +139,13 @@ __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const Gen
     const unsigned long long total_warps = (unsigned long long)gridDim.x * kGenWarps;
     const unsigned long long my_warp = (unsigned long long)blockIdx.x * kGenWarps + warp;
     const unsigned long long kSlice = G.slice;  // queries per visit (host: 1..8, shorter when the sub-batch is small)
-    unsigned long long st_raw = 0, st_vq = 0, st_dist = 0;  // statistics of this warp's queries (uniform over its lanes)
+    // statistics of the queries of one visit (<= 8 queries of at most L n = 2^19 candidates each; uniform over the lanes)
+    uint32_t st_raw = 0, st_vq = 0, st_dist = 0;
     uint32_t pair = kNone;
     PairDesc pd{};
     DevImage I{}, J{};
     unsigned long long pair_end = 0;  // first query past the current pair
-    for (unsigned long long g0 = my_warp * kSlice; g0 < G.queries; g0 += total_warps * kSlice)
+    for (unsigned long long g0 = my_warp * kSlice; g0 < G.queries; g0 += total_warps * kSlice) {
     for (unsigned long long g = g0; g < min(g0 + kSlice, G.queries); ++g) {
         if (pair == kNone || g >= pair_end || g < pd.res_off) {
             pair = pair_of_query(P.pairs, G.npairs, g);
@@ -263,11 +264,13 @@ __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const Gen
         if (P.dbg_count != nullptr && lane == 0) P.dbg_count[q] = n;
         if (lane == 0) __stcs(P.res + g, make_uint2(out_t, out_d));
     }
-    // one atomic per warp and counter (an atomic per query on one address serialises the whole grid)
+    // one atomic per visit and counter
     if (lane == 0) {
-        if (st_raw) atomicAdd(&P.stats->raw_candidates, st_raw);
-        if (st_vq) atomicAdd(&P.stats->verified_queries, st_vq);
-        if (st_dist) atomicAdd(&P.stats->distances, st_dist);
+        if (st_raw) atomicAdd(&P.stats->raw_candidates, (unsigned long long)st_raw);
+        if (st_vq) atomicAdd(&P.stats->verified_queries, (unsigned long long)st_vq);
+        if (st_dist) atomicAdd(&P.stats->distances, (unsigned long long)st_dist);
+    }
+    st_raw = st_vq = st_dist = 0;
     }
 }
 
