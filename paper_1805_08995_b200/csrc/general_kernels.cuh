@@ -19,7 +19,7 @@
 // and re-ranked without it by the rule of matcher.cpp:176-189; each is verified as it is pulled (euclidean_verify,
 // matcher.cpp:115-137: exact integer distances, best / second with strict '<', Lowe ratio in fp64).  Keys are kept in a
 // per-warp shared-memory cache when the query has at most kGenCacheKeys candidates and recomputed per pull otherwise.
-// Not tuned: this path exists so that no input the reference accepts fails on the device.
+// Lightly tuned (KG): this path exists so that no input the reference accepts fails on the device.
 #pragma once
 
 #include "match_kernels.cuh"
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const Gen
             } else {
                 r = resolve_ranges(I, J, q, P.L, P.m, sparse, lane);
                 C = r.total;
-                st_raw += C;  // matcher.cpp:168 (lane 0 adds the warp's total once, when its queries are done)
+                st_raw += C;  // matcher.cpp:168 (lane 0 adds the visit's total once)
             }
             EpiLine line{};
             if (guided) line = epipolar_band(P.fmats + uint64_t(pd.pair_idx) * 9, __ldg(I.kp + q));
