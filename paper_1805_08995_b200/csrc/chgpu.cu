@@ -1150,12 +1150,18 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
             G.list_offs = run.lists ? ctx->d_list_offs : nullptr;
             G.list_ids = run.lists ? ctx->d_list_ids : nullptr;
             const size_t gsmem = size_t(kGenWarps) * kGenCacheKeys * sizeof(uint32_t);
-            CK(cudaFuncSetAttribute(general_match_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsmem)));
+            // CHGPU_GEN_HEADS=0: the A/B reference without the per-lane sorted lists (KG)
+            static const bool gen_heads = [] {
+                const char* e = getenv("CHGPU_GEN_HEADS");
+                return !(e && atoi(e) == 0);
+            }();
+            void (*gen_kernel)(const GeneralParams) = gen_heads ? general_match_kernel<true> : general_match_kernel<false>;
+            CK(cudaFuncSetAttribute(gen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsmem)));
             const uint64_t want = (sb.queries + kGenWarps - 1) / kGenWarps;
             grid = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(ctx->prop.multiProcessorCount) * 24)));
             G.slice = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(8, sb.queries / (uint64_t(grid) * kGenWarps * 4))));  // (longer runs unbalance the warps: matching queries cluster)
             CK(cudaEventRecord(b.ev_k0, ctx->compute));
-            general_match_kernel<<<grid, kGenThreads, gsmem, ctx->compute>>>(G);
+            gen_kernel<<<grid, kGenThreads, gsmem, ctx->compute>>>(G);
             CK(cudaGetLastError());
             CK(cudaEventRecord(b.ev_k1, ctx->compute));
         } else if (sb.tiled) {

@@ -121,6 +121,8 @@ __device__ __forceinline__ uint32_t pair_of_query(const PairDesc* __restrict__ p
     return lo;
 }
 
+// HEADS: the pulls of a query with 33..256 keys come from per-lane sorted lists (below); false = the A/B reference
+template <bool HEADS>
 __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const GeneralParams G) {
     extern __shared__ __align__(16) uint32_t s_keys_all[];  // kGenWarps x kGenCacheKeys
     constexpr uint32_t FULL = 0xffffffffu;
@@ -182,9 +184,27 @@ __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const Gen
                 return key;
             };
             const bool cached = C <= kGenCacheKeys;
+            // HEADS: a query with 33..256 cached keys that gets past the threshold has every lane sort ITS (at most 8) keys,
+            // cache entries lane + 32 j, with a network in registers and write them back; from then on a lane keeps only the
+            // head of its list (hv) and where it came from (hp), and a pull is the minimum over the 32 heads plus one reload
+            // in the lanes that held it — 8 instructions instead of a pass over all cached keys
+            bool heads = false;
+            uint32_t hv = kNone, hp = 0;
             // smallest key above `prev` (first: smallest key at all), kNone when there is none
             auto pull = [&](uint32_t prev, bool first) -> uint32_t {
                 uint32_t best = kNone;
+                if (HEADS && heads) {
+                    uint32_t g;
+                    do {  // a point reached through several tables has its key in several lists: equal heads leave together, a
+                          // repeat inside one list is pulled again and skipped (g == prev)
+                        g = __reduce_min_sync(FULL, hv);
+                        if (hv == g && g != kNone) {
+                            hp += 128u;
+                            hv = hp < s_keys + C * 4u ? lds32(hp) : kNone;
+                        }
+                    } while (g == prev);
+                    return g;
+                }
                 if (cached) {
                     // keys <= prev wrap to the top of the u32 range (see next_key in match_kernels.cuh): one add-and-min per key
                     const uint32_t nb = first ? 0u : ~prev;
@@ -226,6 +246,26 @@ __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const Gen
             if (nk != kNone && (nk >> 24) <= P.tau) {
                 // this lane's 4 bytes of the query row
                 const uint32_t qrow = __ldg(reinterpret_cast<const uint32_t*>(I.desc + uint64_t(q) * kDim) + lane);
+                if (HEADS && cached && C > 32u && C <= 256u) {
+                    heads = true;
+                    uint32_t hk[8];
+#pragma unroll
+                    for (uint32_t j = 0; j < 8; ++j) hk[j] = lane + 32u * j < C ? lds32(s_keys + (lane + 32u * j) * 4u) : kNone;
+                    auto cx = [&](int a, int b) {
+                        const uint32_t lo = min(hk[a], hk[b]), hi = max(hk[a], hk[b]);
+                        hk[a] = lo;
+                        hk[b] = hi;
+                    };
+                    // 19-exchange sorting network for 8 keys
+                    cx(0, 1); cx(2, 3); cx(4, 5); cx(6, 7); cx(0, 2); cx(1, 3); cx(4, 6); cx(5, 7); cx(1, 2); cx(5, 6);
+                    cx(0, 4); cx(3, 7); cx(1, 5); cx(2, 6); cx(1, 4); cx(3, 6); cx(2, 4); cx(3, 5); cx(3, 4);
+                    // back to the lane's own entries (no other lane reads them while the lists are in use)
+#pragma unroll
+                    for (uint32_t j = 0; j < 8; ++j)
+                        if (lane + 32u * j < C) sts32(s_keys + (lane + 32u * j) * 4u, hk[j]);
+                    hp = s_keys + lane * 4u;
+                    hv = hk[0];
+                }
                 for (;;) {
                     // rank n: verified at once (euclidean_verify's loop body, matcher.cpp:124-133); the row travels while the
                     // next key is pulled

@@ -45,5 +45,8 @@ def run(m, images, n, short_bits, top_k):
 
 if __name__ == "__main__":
     with ch.Matcher(0) as m:
-        for sb, k in ((8, 10), (8, 33), (8, 64), (12, 10), (13, 10), (16, 10), (24, 10)):
+        cases = ((8, 10), (8, 33), (8, 64), (12, 10), (13, 10), (16, 10), (24, 10))
+        if "--general-only" in sys.argv:  # A/B runs of the general kernel's variants (CHGPU_GEN_VARIANT)
+            cases = ((8, 33), (8, 64), (8, 200), (13, 10), (24, 10))
+        for sb, k in cases:
             print(json.dumps(run(m, 64, 8192, sb, k)), flush=True)
