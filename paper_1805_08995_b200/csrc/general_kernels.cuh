@@ -29,6 +29,10 @@ namespace chgpu {
 constexpr int kGenThreads = 256;
 constexpr uint32_t kGenWarps = kGenThreads / 32;
 constexpr uint32_t kGenCacheKeys = 1024;  // per warp: 4 KB (32 KB per CTA: the occupancy of this latency-bound kernel matters more)
+#ifndef CHGPU_GEN_CHAINS
+#define CHGPU_GEN_CHAINS 4
+#endif
+constexpr uint32_t kGenChains = CHGPU_GEN_CHAINS;  // independent id -> code gather chains per lane while the keys are formed
 constexpr uint32_t kGenBitmapWords = kMaxPoints / 32;  // cand_union_kernel: one bit per train point, per warp
 
 struct GeneralParams {
@@ -41,10 +45,11 @@ struct GeneralParams {
     const uint32_t* list_ids;
 };
 
-// The L bucket ranges of one query in the train image's index: table t covers entries [first[t], first[t] + len[t]) of the
-// image's entry array (points / sorted keys, table-major).  Lane t resolves table t.
+// The L bucket ranges of one query in the train image's index: table t covers entries [first_t, first_t + len_t) of the
+// image's entry array (points / sorted keys, table-major).  Lane t resolves table t.  Kept in the form the flat candidate
+// index needs: start[t] = len_0 + ... + len_(t-1) (the flat index of the table's first candidate), shift[t] = first_t - start[t].
 struct BucketRanges {
-    uint32_t first[kMaxTables], len[kMaxTables];
+    uint32_t start[kMaxTables], shift[kMaxTables];
     uint32_t total;
 };
 __device__ __forceinline__ BucketRanges resolve_ranges(const DevImage& I, const DevImage& J, uint32_t q, uint32_t L, uint32_t m,
@@ -87,24 +92,19 @@ __device__ __forceinline__ BucketRanges resolve_ranges(const DevImage& I, const 
     r.total = 0;
 #pragma unroll
     for (int t = 0; t < kMaxTables; ++t) {
-        r.first[t] = __shfl_sync(FULL, a, t);
-        r.len[t] = uint32_t(t) < L ? __shfl_sync(FULL, n, t) : 0u;
-        r.total += r.len[t];
+        r.start[t] = r.total;  // tables past L: start == total, never reached by an index below total
+        r.shift[t] = __shfl_sync(FULL, a, t) - r.total;
+        r.total += uint32_t(t) < L ? __shfl_sync(FULL, n, t) : 0u;
     }
     return r;
 }
 // point id behind flat candidate index i (< r.total) of the concatenated buckets
 __device__ __forceinline__ uint32_t range_id(const BucketRanges& r, const DevImage& J, bool sparse, uint32_t i) {
-    uint32_t e = 0;
-    bool found = false;
+    uint32_t shift = r.shift[0];  // the last table whose first candidate is not past i
 #pragma unroll
-    for (int t = 0; t < kMaxTables; ++t) {
-        if (!found && i < r.len[t]) {
-            e = r.first[t] + i;
-            found = true;
-        }
-        if (!found) i -= r.len[t];
-    }
+    for (int t = 1; t < kMaxTables; ++t)
+        if (i >= r.start[t]) shift = r.shift[t];
+    const uint32_t e = i + shift;
     if (sparse) return uint32_t(__ldg(reinterpret_cast<const unsigned long long*>(J.offs) + e) & 0xffffull);
     return __ldg(J.points + e);
 }
@@ -222,20 +222,20 @@ __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const Gen
                 return __reduce_min_sync(FULL, best);
             };
             __syncwarp();  // the previous query's cache is no longer read
-            // keys of all candidates, four independent gather chains (id -> code) per lane in flight; the smallest on the way
+            // keys of all candidates, kGenChains independent gather chains (id -> code) per lane in flight; the smallest on the way
             uint32_t kmin = kNone;
-            for (uint32_t i0 = 0; i0 < C; i0 += 128u) {
-                uint32_t k4[4];
+            for (uint32_t i0 = 0; i0 < C; i0 += 32u * kGenChains) {
+                uint32_t kc[kGenChains];
 #pragma unroll
-                for (uint32_t u = 0; u < 4; ++u) {
+                for (uint32_t u = 0; u < kGenChains; ++u) {
                     const uint32_t i = i0 + 32u * u + lane;
-                    k4[u] = i < C ? key_at(i) : kNone;
+                    kc[u] = i < C ? key_at(i) : kNone;
                 }
 #pragma unroll
-                for (uint32_t u = 0; u < 4; ++u) {
+                for (uint32_t u = 0; u < kGenChains; ++u) {
                     const uint32_t i = i0 + 32u * u + lane;
-                    if (cached && i < C) sts32(s_keys + i * 4u, k4[u]);
-                    kmin = min(kmin, k4[u]);
+                    if (cached && i < C) sts32(s_keys + i * 4u, kc[u]);
+                    kmin = min(kmin, kc[u]);
                 }
             }
             __syncwarp();
