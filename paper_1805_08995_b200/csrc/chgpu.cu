@@ -1155,7 +1155,7 @@ chgpu_status run_match_impl(chgpu_ctx* ctx, MatchRun& run, chgpu_match_stats* st
                 const char* e = getenv("CHGPU_GEN_HEADS");
                 return !(e && atoi(e) == 0);
             }();
-            void (*gen_kernel)(const GeneralParams) = gen_heads ? general_match_kernel<true> : general_match_kernel<false>;
+            const GeneralKernel gen_kernel = general_kernel_for(gen_heads, G.list_offs != nullptr, G.sparse != 0, P.fmats != nullptr);
             CK(cudaFuncSetAttribute(gen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsmem)));
             const uint64_t want = (sb.queries + kGenWarps - 1) / kGenWarps;
             grid = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(ctx->prop.multiProcessorCount) * 24)));

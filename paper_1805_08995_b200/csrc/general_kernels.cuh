@@ -121,8 +121,10 @@ __device__ __forceinline__ uint32_t pair_of_query(const PairDesc* __restrict__ p
     return lo;
 }
 
-// HEADS: the pulls of a query with 33..256 keys come from per-lane sorted lists (below); false = the A/B reference
-template <bool HEADS>
+// HEADS: the pulls of a query with 33..256 keys come from per-lane sorted lists (below); false = the A/B reference.
+// LISTS / SPARSE / GUIDED: explicit candidate lists, the sorted-key index, the epipolar band — build-time, because the
+// per-key code otherwise re-tests them (ncu: ~100 of 1,530 instructions per query were branches on these three flags)
+template <bool HEADS, bool LISTS, bool SPARSE, bool GUIDED>
 __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const GeneralParams G) {
     extern __shared__ __align__(16) uint32_t s_keys_all[];  // kGenWarps x kGenCacheKeys
     constexpr uint32_t FULL = 0xffffffffu;
@@ -132,9 +134,7 @@ __global__ void __launch_bounds__(kGenThreads, 4) general_match_kernel(const Gen
     // window base in front of every access: 7 instructions per key read)
     uint32_t s_keys = smem_addr(s_keys_all + warp * kGenCacheKeys);
     asm volatile("" : "+r"(s_keys));
-    const bool explicit_lists = G.list_offs != nullptr;
-    const bool sparse = G.sparse != 0;
-    const bool guided = P.fmats != nullptr;
+    constexpr bool explicit_lists = LISTS, sparse = SPARSE, guided = GUIDED;
 
     // every warp takes a contiguous run of the sub-batch's queries in short slices: the pair (and its two image records)
     // changes rarely along a run, so it is looked up once and then only advanced
@@ -412,6 +412,17 @@ __global__ void __launch_bounds__(kSparseThreads) sparse_index_kernel(const DevI
             }
         }
     }
+}
+
+// the instantiation for a run's flags (HEADS = false only as the A/B reference of the plain bucket run)
+using GeneralKernel = void (*)(const GeneralParams);
+inline GeneralKernel general_kernel_for(bool heads, bool lists, bool sparse, bool guided) {
+    if (lists) {  // explicit lists: the bucket index is not read (SPARSE is irrelevant)
+        return guided ? general_match_kernel<true, true, false, true> : general_match_kernel<true, true, false, false>;
+    }
+    if (sparse) return guided ? general_match_kernel<true, false, true, true> : general_match_kernel<true, false, true, false>;
+    if (guided) return general_match_kernel<true, false, false, true>;
+    return heads ? general_match_kernel<true, false, false, false> : general_match_kernel<false, false, false, false>;
 }
 
 }  // namespace chgpu
